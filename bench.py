@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark: inference through the VGG-16 FC stack stored Deep-Compression
+style (BASELINE.json config C5: fc6 25088->4096 @4%, fc7 4096->4096 @4%,
+fc8 4096->1000 @23%, 5-bit codebooks, 4-bit gaps, Huffman-coded), batch 512.
+
+One step = cdn_model_infer on one batch of synthetic ReLU(N(0,1)) images with
+inputs resident in HBM: layout transpose -> fc6 -> fc7 -> fc8 (each: parallel
+Huffman decode -> gap prefix sum -> dequantize -> sparse multiply -> bias ->
+ReLU) -> scores.  Multi-GPU (torchrun): every layer row-block sharded, NCCL
+all-gather between layers (strong scaling: the batch is fixed).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the
+reference arm for this tier)."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+CFG = "C5"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--batch", type=int, default=512)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--b1-replicas", type=int, default=8, help="cold-L2 B=1 replicas (0: skip)")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_model(cdn, rank, world, nccl_id, cdni_bytes):
+    m = cdn.Model(int(os.environ.get("LOCAL_RANK", 0)), rank=rank, world=world, nccl_id=nccl_id)
+    for spec, buf in zip(synth.CONFIGS[CFG].fc, cdni_bytes):
+        m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+    return m
+
+
+def compressed_layers(cdn):
+    out = []
+    for spec in synth.CONFIGS[CFG].fc:
+        W, v = synth.fc_weights(spec, synth.CONFIGS[CFG].seed)
+        out.append(cdn.compress_dense(W, spec.density, spec.r, spec.k, v))
+        del W
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1711_00244_b200 as cdn
+    from paper_1711_00244_b200 import build as _build
+    _build.build()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.tensor(list(cdn.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nccl_id = bytes(t.cpu().tolist())
+
+    B = args.batch
+    specs = synth.CONFIGS[CFG].fc
+    layers = compressed_layers(cdn)
+    m = build_model(cdn, rank, world, nccl_id, layers)
+    m.set_plan([B] * len(specs))
+    stats = [m.stats(i) for i in range(len(specs))]
+    K_in, N_out = specs[0].cols, specs[-1].rows
+
+    a = synth.fc_inputs(K_in, B, synth.CONFIGS[CFG].seed)
+    x_dev = torch.from_numpy(a).to(dev)
+    s_dev = torch.zeros((B, N_out), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def step():
+        m.infer(x_dev, B, s_dev, on_device=True, stream=sp)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                      # L2 flush between timed iterations
+            barrier()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        barrier()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+
+    # ---- end to end: pinned host input, host scores, copies inside the timed region
+    a_pin = torch.from_numpy(a).pin_memory()
+    s_pin = torch.zeros((B, N_out), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        m.infer(a_pin, B, s_pin, on_device=False, stream=sp)
+    barrier()
+    e_ms = 0.0
+    for i in range(args.steps):
+        flush.zero_()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m.infer(a_pin, B, s_pin, on_device=False, stream=sp)
+        e1.record(stream)
+        barrier()
+        e_ms += e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+
+    # ---- per-layer kernel durations inside the same workload (roofline of the dominant kernel)
+    xs = []
+    feats = [specs[0].cols] + [s.rows for s in specs]
+    bufs = [torch.from_numpy(np.ascontiguousarray(a.T)).to(dev)]
+    for i, s in enumerate(specs):
+        bufs.append(torch.zeros((stats[i]["row_end"] - stats[i]["row_begin"], B), dtype=torch.float32, device=dev))
+    lay_ms = np.zeros(len(specs))
+    reps = max(3, args.steps)
+    for r in range(reps + 2):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        for i in range(len(specs)):
+            xin = bufs[i] if i == 0 else torch.zeros((feats[i], B), dtype=torch.float32, device=dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            m.layer_forward(i, xin, B, B, bufs[i + 1], B, stream=sp)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if r >= 2:
+                lay_ms[i] += e0.elapsed_time(e1) / reps
+    dom = int(np.argmax(lay_ms))
+    st = stats[dom]
+    nloc = st["row_end"] - st["row_begin"]
+    flops = 2.0 * st["nnz"] * B + nloc * B
+    bytes_algo = st["algo_bytes_fixed"] + 4.0 * st["cols"] * B + 4.0 * nloc * B
+    pk = peaks()
+    sm_mhz_max = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * 2 * sm_mhz_max * 1e6 / 1e12      # fp32 FMA TFLOP/s
+    t_s = lay_ms[dom] / 1e3
+    ai = flops / bytes_algo
+    if ai * pk["hbm_gbs"] * 1e9 > alu_peak * 1e12:            # compute-bound
+        roof = {"bound": "alu", "achieved": flops / t_s / 1e12, "peak": alu_peak, "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": bytes_algo / t_s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = f"k_fc_forward ({specs[dom].name}, B={B})"
+    roof["ms"] = lay_ms[dom]
+    roof["peak_source"] = "MEASURED_PEAKS.json hbm_gbs / alu from 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"
+
+    # ---- B = 1 cold-L2 decode-bound measurement (HBM roofline on compressed bytes)
+    b1 = None
+    if args.b1_replicas > 0 and world == 1:
+        b1 = bench_b1(cdn, torch, dev, layers, specs, args.b1_replicas, flush, pk)
+
+    comp_bytes = sum(s["stream_bytes"] for s in stats)
+    images = B * args.steps
+    value = images / (tot_ms / 1e3)
+    res = {
+        "metric": "images/s (VGG-16 FC stack, compressed weights)",
+        "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C5 VGG-16 FC stack fc6/fc7/fc8 (4%/4%/23%, r=5, k=4, Huffman)",
+                   "global_batch": B, "parallelism": f"row-shard{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MB write) between timed steps", "plan": [B] * len(specs)},
+        "compressed_gbs": comp_bytes / (tot_ms / args.steps / 1e3) / 1e9,
+        "compressed_bytes": comp_bytes,
+        "e2e": {"value": images / (e_ms / 1e3), "unit": "images/s",
+                "h2d_bytes_per_step": int(a.nbytes), "d2h_bytes_per_step": int(B * N_out * 4)},
+        "gpu_launches": 5 * args.steps,
+        "roofline": roof,
+        "layer_ms": {s.name: float(t) for s, t in zip(specs, lay_ms)},
+        "clocks": clk.summary(),
+    }
+    if b1:
+        res["b1_cold"] = b1
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(layers, B, budget_s=15.0)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    m.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_b1(cdn, torch, dev, layers, specs, R, flush, pk):
+    """B=1, R independent resident replicas of the stack (the 'many models
+    resident' service case) so that streams are read from HBM, not L2."""
+    models = [build_model(cdn, 0, 1, None, layers) for _ in range(R)]
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    x = [torch.zeros((s.cols, 1), dtype=torch.float32, device=dev) for s in specs]
+    y = [torch.zeros((s.rows, 1), dtype=torch.float32, device=dev) for s in specs]
+    st = [models[0].stats(i) for i in range(len(specs))]
+    per_layer = {}
+    for i, s in enumerate(specs):
+        for mm in models:                      # warm-up
+            mm.layer_forward(i, x[i], 1, 1, y[i], 1, stream=sp)
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        ts = []
+        for mm in models:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            mm.layer_forward(i, x[i], 1, 1, y[i], 1, stream=sp)
+            e1.record(stream)
+            ts.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        ms = float(np.median([a.elapsed_time(b) for a, b in ts]))
+        algo = st[i]["algo_bytes_fixed"] + 4 * s.cols + 4 * s.rows
+        per_layer[s.name] = {"us": ms * 1e3, "algo_bytes": algo, "gbs": algo / (ms / 1e3) / 1e9,
+                             "frac": algo / (ms / 1e3) / 1e9 / pk["hbm_gbs"],
+                             "index_bytes": st[i]["index_bytes"], "lanes_per_row": st[i]["lanes_per_row"]}
+    for mm in models:
+        mm.close()
+    return {"replicas": R, "note": "median per-launch CUDA-event time, each replica's streams cold in L2",
+            "layers": per_layer}
+
+
+def cpu_baseline(layers, B, budget_s=15.0):
+    """Oracle (plain Python decode + fp64 product) on a bounded sample: a few
+    rows of each layer for all B images, scaled to the whole stack."""
+    from oracle import cdni as ocdni, decode as odecode, infer as oinfer
+    import scipy.sparse as sp
+    specs = synth.CONFIGS[CFG].fc
+    t_total = 0.0
+    rows_done = []
+    for spec, buf in zip(specs, layers):
+        L = ocdni.deserialize(buf)[0]
+        a = synth.fc_inputs(spec.cols, B, 0)
+        t0 = time.perf_counter()
+        n = 0
+        rows = []
+        while time.perf_counter() - t0 < budget_s / len(specs) and n < L.rows:
+            rows.append(n)
+            n += max(1, L.rows // 64)
+        R, Cc, S, V = odecode.decode_layer(L, rows)
+        real = S != 0
+        Wq = sp.csr_matrix((V[real].astype(np.float64), (R[real], Cc[real])), shape=(L.rows, L.cols))
+        oinfer.fc_forward(Wq[rows], a)
+        dt = time.perf_counter() - t0
+        t_total += dt * L.rows / len(rows)
+        rows_done.append(len(rows))
+    return {"value": B / t_total, "unit": "images/s", "cores": 1, "kind": "oracle",
+            "sample": f"plain-Python Huffman decode + fp64 product of {rows_done} rows of fc6/fc7/fc8 "
+                      f"at B={B}, time scaled by rows/sampled rows"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1711_00244_b200 as cdn
+    from paper_1711_00244_b200 import build as _build
+    _build.build()
+    layers = compressed_layers(cdn)
+    B = args.batch
+    per = max(1.0, 120.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_baseline(layers, B, budget_s=min(per, 3.0))
+    vals = []
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(layers, B, budget_s=min(per, 6.0)))
+    v = float(np.mean([x["value"] for x in vals]))
+    res = {"impl": "reference", "metric": "images/s (VGG-16 FC stack, compressed weights)", "value": v,
+           "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": B / v * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "C5 VGG-16 FC stack fc6/fc7/fc8 (4%/4%/23%, r=5, k=4, Huffman)",
+                      "global_batch": B, "parallelism": "cpu-oracle"},
+           "cpu_baseline": {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle",
+                            "sample": vals[-1]["sample"]},
+           "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

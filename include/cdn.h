@@ -1,0 +1,201 @@
+/*
+ * cdn.h -- C ABI of the B200-native compressed-DNN inference library
+ * (arxiv 1711.00244, "inference from Deep-Compression models under memory
+ * constraints").  Citations: P:Lnnn = /root/reference/PAPER.md line,
+ * S:Lnnn = SPEC.md line, C-nn = reading listed in DESIGN.md.
+ *
+ * The calls follow the paper's statement of the problem (P:L754, L651,
+ * L724-726): a user loads compressed layers once (the model stays resident,
+ * P:L40, L173), sets a memory budget TOT and optionally a latency threshold,
+ * and asks for inference of K inputs with maximum throughput.
+ *
+ * Conventions
+ *  - Every function returns cdn_status: 0 = CDN_OK, negative = error.  No C++
+ *    exception or abort crosses this boundary.  cdn_last_error() returns a
+ *    thread-local message describing the last failure on the calling thread.
+ *  - Pointers are plain host or device pointers as stated per argument.  The
+ *    library never takes ownership of caller buffers; it copies what it keeps.
+ *  - One call at a time per cdn_model handle; distinct handles are
+ *    independent.  Loaded layers are immutable.
+ *  - Floating point is fp32 (FC: fp32 FMA, fp32 accumulate; CONV: bf16 inputs,
+ *    fp32 accumulate, config C4).
+ *  - Device work runs on the stream given (NULL = the library's own stream, in
+ *    which case the call returns with results complete).
+ */
+#ifndef CDN_H_
+#define CDN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CDN_ABI_VERSION 1
+
+typedef int32_t cdn_status;
+enum {
+  CDN_OK = 0,
+  CDN_E_ARG = -1,          /* bad argument (NULL, out of range)                        */
+  CDN_E_MAGIC = -2,        /* CDNI magic is not "CDNI"                                 */
+  CDN_E_VERSION = -3,      /* unknown CDNI version                                     */
+  CDN_E_TRUNCATED = -4,    /* buffer shorter than the CDNI structure requires          */
+  CDN_E_MALFORMED = -5,    /* Kraft violation, offsets non-monotone, val/gap token     */
+                           /* counts differ, column >= cols, pad invariant broken      */
+  CDN_E_UNSUPPORTED = -6,  /* code length > 32, r > 8, k > 8, blocked layout (bh != 1) */
+  CDN_E_SHAPE = -7,        /* layer shapes do not chain / input shape mismatch         */
+  CDN_E_OOM = -8,          /* device or host allocation failed                         */
+  CDN_E_INFEASIBLE = -9,   /* no batch plan satisfies TOT / latency     */
+  CDN_E_CUDA = -10,        /* CUDA runtime error (message has the CUDA error string)   */
+  CDN_E_NCCL = -11,        /* NCCL error                                               */
+  CDN_E_STATE = -12        /* call not valid in this state (no layers, concurrent use) */
+};
+
+typedef struct cdn_model cdn_model;
+
+enum { CDN_LAYER_FC = 0, CDN_LAYER_CONV = 1 };
+
+/* How a loaded weight matrix is used.  FC: b = W a + v (Eq. 1-2).
+ * CONV: W has one row per filter and K = kh*kw*in_c/groups columns flattened
+ * as (r, s, c), channel fastest (C-18); activations are NHWC. */
+typedef struct {
+  int32_t kind;                  /* CDN_LAYER_FC or CDN_LAYER_CONV                    */
+  int32_t relu;                  /* 1: ReLU after the bias                             */
+  int32_t in_c, in_h, in_w;      /* CONV input geometry (ignored for FC)               */
+  int32_t kh, kw, stride, pad, groups;
+  int32_t lrn;                   /* CONV: cross-channel LRN after ReLU (C-20)          */
+  int32_t pool_k, pool_s;        /* CONV: max-pool after (0 = none)                    */
+} cdn_layer_desc;
+
+typedef struct {
+  uint32_t rows, cols;           /* full layer geometry                               */
+  uint32_t row_begin, row_end;   /* rows held by this rank (row-block shard)          */
+  uint32_t k, r;                 /* relative-index bits, quantization bits            */
+  uint32_t lanes_per_row;        /* G: decode lanes per row (column bands)             */
+  uint32_t max_len_val, max_len_gap;
+  uint64_t tokens;               /* tokens of this rank's rows, pads included         */
+  uint64_t nnz;                  /* real (non-pad) tokens of this rank's rows         */
+  uint64_t stream_bytes;         /* ceil(val bits/8) + ceil(gap bits/8) of the shard  */
+  uint64_t algo_bytes_fixed;     /* stream + row_ptr + codebook + tables + bias bytes */
+  uint64_t index_bytes;          /* decode-lane index bytes (overhead)                */
+  uint64_t ws_bytes;             /* WS(i): device scratch the layer uses     */
+  uint64_t in_features, out_features; /* per image                                     */
+} cdn_layer_stats;
+
+/* ---- library / errors ------------------------------------------------- */
+int cdn_abi_version(void);
+const char* cdn_last_error(void);
+
+/* ---- multi-GPU bootstrap: rank 0 creates the 128-byte NCCL unique id;
+ * the caller broadcasts it (e.g. with torch.distributed).  Errors: CDN_E_NCCL. */
+cdn_status cdn_nccl_unique_id(uint8_t out[128]);
+
+/* ---- model lifecycle --------------------------------------------------
+ * device: CUDA ordinal; rank/world: this process's place in the row-block
+ * sharding (world == 1: single GPU, nccl_id may be NULL).  world > 1 with
+ * nccl_id == NULL creates a shard-only handle: it loads rank's row block and
+ * serves cdn_layer_forward / cdn_layer_decode, but infer/plan return
+ * CDN_E_STATE (used to test sharding on one GPU).  The library owns
+ * its device memory, streams and NCCL communicator.  Errors: CDN_E_ARG,
+ * CDN_E_CUDA, CDN_E_NCCL, CDN_E_OOM. */
+cdn_status cdn_model_create(int device, int rank, int world, const uint8_t* nccl_id,
+                            cdn_model** out);
+void cdn_model_destroy(cdn_model* m); /* NULL-safe */
+
+/* ---- load compressed layer (the stored model of Fig. 1e) ----
+ * cdni/n: host buffer holding a CDNI container (format in DESIGN.md);
+ * the bytes are copied, the caller may free them on return.  layer_in_file
+ * selects one layer of a multi-layer file.  Layers are appended in network
+ * order; shapes are validated against the previous layer.  Each rank keeps
+ * only its block of output rows; the streams are sliced at row_ptr bit
+ * offsets, never re-encoded.  Load builds the decode-lane index (DESIGN.md
+ * "container") on the host and copies everything to the device once.
+ * Errors: CDN_E_MAGIC, CDN_E_VERSION, CDN_E_TRUNCATED, CDN_E_MALFORMED,
+ * CDN_E_UNSUPPORTED, CDN_E_SHAPE, CDN_E_OOM, CDN_E_CUDA. */
+cdn_status cdn_model_load_layer(cdn_model* m, const void* cdni, size_t n, int layer_in_file,
+                                const cdn_layer_desc* desc, int* layer_idx);
+
+/* ---- memory budget (P:L651 TOT; P:L724-726 latency threshold) ----------
+ * tot_bytes counts activations + workspace per GPU, EXCLUDING the resident
+ * compressed model.  latency_ms <= 0: no threshold.  Invalidates the
+ * cached plan.  Errors: CDN_E_ARG. */
+cdn_status cdn_model_set_memory_budget(cdn_model* m, uint64_t tot_bytes, double latency_ms);
+
+/* ---- plan: profiles Time(i,B) on the device for B = 1..K
+ * (cached), runs the variable-batch DP and returns the per-layer batch sizes
+ * of the first round (batch_per_layer has n_layers entries) and the predicted
+ * total time for all K inputs including remainder re-plans.
+ * Errors: CDN_E_INFEASIBLE, CDN_E_CUDA, CDN_E_STATE. */
+cdn_status cdn_model_plan(cdn_model* m, int K, int* batch_per_layer, double* predicted_ms);
+
+/* Use a fixed plan instead of the DP (batch sizes must form a divisor chain
+ * B_1 | B_2 | ... | B_f).  n == 0 clears it. */
+cdn_status cdn_model_set_plan(cdn_model* m, const int* batch_per_layer, int n);
+
+/* ---- infer(batch) -> class scores --------------------------------------
+ * input : fp32, image-major: [K][features] for FC-only nets, [K][H][W][C] NHWC
+ *         for conv nets.  Host or device memory per on_device.
+ * scores: fp32 [K][classes] raw (no softmax), host or device per on_device.
+ * Runs the planned per-layer batches with B/b phases.  Under
+ * world > 1 every rank calls it with the same input; only rank 0's scores are
+ * written.  stream: cudaStream_t or NULL.  Errors: CDN_E_SHAPE,
+ * CDN_E_INFEASIBLE, CDN_E_CUDA, CDN_E_NCCL, CDN_E_STATE. */
+cdn_status cdn_model_infer(cdn_model* m, const float* input, int K, float* scores, int on_device,
+                           void* stream);
+
+/* ---- one layer on device-resident, feature-major activations ------------
+ * x: device [in_features][ldx] fp32 (column b = image b), y: device
+ * [rows of this rank][ldy] fp32.  B images.  The hot path of one layer
+ * (parallel Huffman decode -> gap prefix sum -> codebook dequantize -> sparse
+ * multiply -> bias -> ReLU) in the fused kernels; used by infer, the profiler,
+ * parity tests and bench.  Errors: CDN_E_ARG, CDN_E_CUDA. */
+cdn_status cdn_layer_forward(cdn_model* m, int layer, const float* x, int ldx, int B, float* y,
+                             int ldy, void* stream);
+
+/* ---- decode only (parity hook, kernel K2) -------------------------------
+ * Writes every token of this rank's rows in row-major token order, pads
+ * included: row, abs column (Alg. 1 l.7), val symbol, codebook value (l.8).
+ * Device pointers; call first with all four NULL to get *n_tokens.
+ * Errors: CDN_E_ARG, CDN_E_CUDA. */
+cdn_status cdn_layer_decode(cdn_model* m, int layer, int32_t* row, int32_t* col, uint8_t* sym,
+                            float* val, uint64_t* n_tokens, void* stream);
+
+cdn_status cdn_model_num_layers(const cdn_model* m, int* n);
+cdn_status cdn_layer_stats_get(const cdn_model* m, int layer, cdn_layer_stats* out);
+
+/* ---- profiler: Time(i,B) for B = 1..Bmax, ms (median of reps), written to
+ * time_ms[i*Bmax + (B-1)].  Errors: CDN_E_CUDA, CDN_E_STATE. */
+cdn_status cdn_model_profile(cdn_model* m, int Bmax, int reps, double* time_ms);
+
+/* ---- host-only utilities (no device needed) ----------------------------- */
+
+/* Compress a dense fp32 row-major rows x cols matrix: magnitude
+ * prune to floor(density*rows*cols + 0.5) entries (C-10), r-bit linear
+ * codebook (C-04/05/07), k-bit relative index with pads (C-01..03), Huffman
+ * per stream (C-14..17).  bias may be NULL.  *out receives a malloc'd
+ * single-layer CDNI buffer the caller frees with cdn_free.
+ * Errors: CDN_E_ARG, CDN_E_UNSUPPORTED, CDN_E_OOM. */
+cdn_status cdn_compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols,
+                              double density, int r, int k, void** out, size_t* out_len);
+void cdn_free(void* p);
+
+/* Variable-batch DP of P:L694-720 on a given table (host).  time_ms[i*Bmax + B-1]
+ * = Time(i,B); in/out bytes per image; ws bytes per layer; tot; latency (<=0:
+ * none); step: memory-axis granularity in bytes (A + IN rounded UP, C-25).
+ * Outputs the batch per layer and OPT(f,B*,0).  Errors: CDN_E_INFEASIBLE. */
+cdn_status cdn_plan_dp(const double* time_ms, const uint64_t* in_bytes, const uint64_t* out_bytes,
+                       const uint64_t* ws_bytes, int f, int Bmax, uint64_t tot, double latency_ms,
+                       uint64_t step, int* batches, double* opt_ms);
+
+/* Parse + validate a CDNI layer and run the load-time host walk that builds
+ * the decode-lane index; returns the tokens it walked (test hook for the
+ * container builder; not used by inference).  Call with NULL outputs to get
+ * *n_tokens.  row/col int32, sym uint8 (host). */
+cdn_status cdn_debug_host_walk(const void* cdni, size_t n, int layer_in_file, int32_t* row,
+                               int32_t* col, uint8_t* sym, uint64_t* n_tokens);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CDN_H_ */

@@ -1,0 +1,13 @@
+"""B200-native inference from Deep-Compression-style models (arxiv 1711.00244).
+
+Thin ctypes binding over libcdn.so (include/cdn.h).  Argument marshalling only:
+every step of the hot path (Huffman decode, gap prefix sum, dequantize, sparse
+multiply, bias, ReLU) runs in the library's CUDA kernels.  PyTorch is used only
+for device memory, streams and process groups.  There is no CPU fallback: if
+the library is missing or fails to load, importing the binding raises.
+"""
+from .binding import (CDNError, LayerDesc, LayerStats, Model, abi_version, compress_dense,
+                      debug_host_walk, lib_path, load_library, nccl_unique_id, plan_dp)
+
+__all__ = ["CDNError", "LayerDesc", "LayerStats", "Model", "abi_version", "compress_dense",
+           "debug_host_walk", "lib_path", "load_library", "nccl_unique_id", "plan_dp"]

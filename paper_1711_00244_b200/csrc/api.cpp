@@ -1,0 +1,640 @@
+// C ABI (include/cdn.h): model state, container upload, layer forward,
+// variable-batch executor, profiler + DP planner,
+// NCCL row-block sharding.  Every entry point catches everything.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/cdn.h"
+#include "host.hpp"
+#include "kernels.cuh"
+
+using namespace cdn;
+
+namespace {
+thread_local std::string g_err;
+
+cdn_status fail(cdn_status c, const std::string& m) {
+  g_err = m;
+  return c;
+}
+
+#define CUDA_OK(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw Error(e_ == cudaErrorMemoryAllocation ? CDN_E_OOM : CDN_E_CUDA,                  \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+
+#define NCCL_OK(expr)                                                                        \
+  do {                                                                                       \
+    ncclResult_t r_ = (expr);                                                                \
+    if (r_ != ncclSuccess) throw Error(CDN_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// Owning device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t bytes) {
+    if (bytes <= n && p) return;
+    release();
+    CUDA_OK(cudaMalloc(&p, bytes ? bytes : 16));
+    n = bytes;
+  }
+  template <class T> void upload(const std::vector<T>& v) {
+    alloc(v.size() * sizeof(T));
+    if (!v.empty()) CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct Layer {
+  cdn_layer_desc desc{};
+  uint32_t rows = 0, cols = 0, row0 = 0, row1 = 0, k = 0, r = 0;
+  FcDev dev;
+  DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias;
+  cdn_layer_stats stats{};
+};
+
+struct Model {
+  int device = 0, rank = 0, world = 1, num_sms = 148;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<std::unique_ptr<Layer>> layers;
+  uint64_t tot = 0;
+  double latency = 0.0;
+  std::vector<int> fixed_plan;
+  // profile cache
+  int prof_bmax = 0;
+  std::vector<double> prof;
+  // executor scratch
+  std::vector<DBuf> lvl;        // per-level input buffers [K_i][B_i]
+  DBuf out, stage_in, loc, gath, host_stage;
+  bool busy = false;
+};
+
+uint32_t rows_per_rank(uint32_t rows, int world) { return (rows + world - 1) / world; }
+
+// Upload one stream slice [b0, b1) bits as big-endian words starting at word b0/32.
+void upload_words(DBuf& d, const std::vector<uint8_t>& bytes, uint64_t b0, uint64_t b1, uint64_t* base_bit) {
+  const uint64_t w0 = b0 >> 5;
+  const uint64_t nw = ((b1 + 31) >> 5) - w0 + 4;
+  std::vector<uint32_t> words(nw, 0);
+  const uint64_t nbytes = bytes.size();
+  for (uint64_t w = 0; w < nw; ++w) {
+    uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) {
+      uint64_t bi = (w0 + w) * 4 + i;
+      v = (v << 8) | (bi < nbytes ? bytes[bi] : 0u);
+    }
+    words[w] = v;
+  }
+  d.upload(words);
+  *base_bit = w0 * 32;
+}
+
+std::vector<uint32_t> build_lut(const HuffCode& h, int Lb) {
+  std::vector<uint32_t> lut((size_t)1 << Lb, 0);
+  for (int i = 0; i < h.n; ++i) {
+    const int L = h.lens[i];
+    if (L > Lb) continue;
+    const uint32_t code = h.code_of[h.syms[i]];
+    const uint32_t lo = code << (Lb - L), cnt = 1u << (Lb - L);
+    for (uint32_t q = 0; q < cnt; ++q) lut[lo + q] = ((uint32_t)L << 16) | h.syms[i];
+  }
+  return lut;
+}
+
+std::vector<uint32_t> build_tab(const HuffCode& h) {
+  std::vector<uint32_t> t(99, 0);
+  for (int L = 0; L <= 32; ++L) {
+    t[L] = h.first_code[L];
+    t[33 + L] = h.count[L];
+    t[66 + L] = h.first_index[L];
+  }
+  return t;
+}
+
+void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer_desc& d, int* out_idx) {
+  HostLayer H = parse_cdni_layer(buf, n, idx);
+  if (d.kind != CDN_LAYER_FC && d.kind != CDN_LAYER_CONV) throw Error(CDN_E_ARG, "unknown layer kind");
+  if (d.kind == CDN_LAYER_CONV) throw Error(CDN_E_UNSUPPORTED, "CONV layers: use the conv entry points");
+  if (!m.layers.empty()) {
+    const Layer& prev = *m.layers.back();
+    if (prev.rows != H.cols)
+      throw Error(CDN_E_SHAPE, "layer input features " + std::to_string(H.cols) + " != previous rows " +
+                                   std::to_string(prev.rows));
+  }
+  auto Lp = std::make_unique<Layer>();
+  Layer& L = *Lp;
+  L.desc = d;
+  L.rows = H.rows;
+  L.cols = H.cols;
+  L.k = H.k;
+  L.r = H.r;
+  const uint32_t rb = rows_per_rank(H.rows, m.world);
+  L.row0 = std::min<uint32_t>(H.rows, rb * (uint32_t)m.rank);
+  L.row1 = std::min<uint32_t>(H.rows, L.row0 + rb);
+  const uint32_t nr = L.row1 - L.row0;
+  int target = 64;
+  if (const char* e = std::getenv("CDN_LANE_TOKENS")) target = std::max(1, std::atoi(e));
+  int G = choose_lanes_per_row(H, 0, H.rows, target);  // whole layer: shard-invariant lanes
+  if (const char* e = std::getenv("CDN_LANES_PER_ROW")) G = std::max(1, std::min(32, std::atoi(e)));
+  LaneIndex ix;
+  build_lane_index(H, L.row0, L.row1, G, ix);
+  const uint64_t v0 = H.rp[2ull * L.row0], v1 = H.rp[2ull * L.row1];
+  const uint64_t g0 = H.rp[2ull * L.row0 + 1], g1 = H.rp[2ull * L.row1 + 1];
+  uint64_t vbase = 0, gbase = 0;
+  upload_words(L.vw, H.vbytes, v0, v1, &vbase);
+  upload_words(L.gw, H.gbytes, g0, g1, &gbase);
+  if (v1 - vbase >= (1ull << 32) || g1 - gbase >= (1ull << 32))
+    throw Error(CDN_E_UNSUPPORTED, "stream slice larger than 2^32 bits");
+  std::vector<uint32_t> rp(2ull * (nr + 1));
+  for (uint32_t i = 0; i <= nr; ++i) {
+    rp[2ull * i] = (uint32_t)(H.rp[2ull * (L.row0 + i)] - vbase);
+    rp[2ull * i + 1] = (uint32_t)(H.rp[2ull * (L.row0 + i) + 1] - gbase);
+  }
+  L.rp.upload(rp);
+  if (ix.rec64) L.rec.upload(ix.rec64v); else L.rec.upload(ix.rec32);
+  L.tok.upload(ix.tok_start);
+  const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
+  const int Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
+  L.vlut.upload(build_lut(H.val, Lv));
+  L.glut.upload(build_lut(H.gap, Lg));
+  L.vtab.upload(build_tab(H.val));
+  L.gtab.upload(build_tab(H.gap));
+  std::vector<uint16_t> vs = H.val.sorted, gs = H.gap.sorted;
+  vs.push_back(0);
+  gs.push_back(0);
+  L.vsorted.upload(vs);
+  L.gsorted.upload(gs);
+  L.cb.upload(H.codebook);
+  std::vector<float> bias(nr, 0.f);
+  if (H.has_bias)
+    for (uint32_t i = 0; i < nr; ++i) bias[i] = H.bias[L.row0 + i];
+  L.bias.upload(bias);
+
+  FcDev& f = L.dev;
+  f.vw = L.vw.as<uint32_t>();
+  f.gw = L.gw.as<uint32_t>();
+  f.rp = L.rp.as<uint32_t>();
+  f.rec = L.rec.p;
+  f.tok_start = L.tok.as<uint64_t>();
+  f.vlut = L.vlut.as<uint32_t>();
+  f.glut = L.glut.as<uint32_t>();
+  f.vtab = L.vtab.as<uint32_t>();
+  f.gtab = L.gtab.as<uint32_t>();
+  f.vsorted = L.vsorted.as<uint16_t>();
+  f.gsorted = L.gsorted.as<uint16_t>();
+  f.codebook = L.cb.as<float>();
+  f.bias = L.bias.as<float>();
+  f.nrows = (int)nr;
+  f.cols = (int)H.cols;
+  f.G = ix.G;
+  f.log2G = ix.log2G;
+  f.W = (int)ix.W;
+  f.k = (int)H.k;
+  f.Lv = Lv;
+  f.Lg = Lg;
+  f.vmax = H.val.max_len;
+  f.gmax = H.gap.max_len;
+  f.ncb = (int)H.codebook.size();
+  f.nvs = H.val.n;
+  f.ngs = H.gap.n;
+  f.rec64 = ix.rec64 ? 1 : 0;
+
+  cdn_layer_stats& s = L.stats;
+  s.rows = H.rows;
+  s.cols = H.cols;
+  s.row_begin = L.row0;
+  s.row_end = L.row1;
+  s.k = H.k;
+  s.r = H.r;
+  s.lanes_per_row = (uint32_t)ix.G;
+  s.max_len_val = (uint32_t)H.val.max_len;
+  s.max_len_gap = (uint32_t)H.gap.max_len;
+  s.tokens = ix.tokens;
+  s.nnz = ix.nnz;
+  s.stream_bytes = (v1 - v0 + 7) / 8 + (g1 - g0 + 7) / 8;
+  s.algo_bytes_fixed = s.stream_bytes + 8ull * (nr + 1) + 4ull * H.codebook.size() +
+                       3ull * (H.val.n + H.gap.n) + 4ull * nr;
+  s.index_bytes = ix.rec64 ? 8ull * ix.rec64v.size() : 4ull * ix.rec32.size();
+  s.ws_bytes = 0;
+  s.in_features = H.cols;
+  s.out_features = H.rows;
+  m.layers.push_back(std::move(Lp));
+  m.prof_bmax = 0;
+  if (out_idx) *out_idx = (int)m.layers.size() - 1;
+}
+
+cudaStream_t pick(Model& m, void* s) { return s ? (cudaStream_t)s : m.stream; }
+
+// One layer step: local rows -> (all-gather if world > 1) -> dst [rows][ld_dst].
+void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, int ld_dst, cudaStream_t s) {
+  Layer& L = *m.layers[li];
+  const int relu = L.desc.relu;
+  if (m.world == 1) {
+    CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, dst, ld_dst, relu, s, m.num_sms));
+    return;
+  }
+  const uint32_t rb = rows_per_rank(L.rows, m.world);
+  const size_t slab = (size_t)rb * B;
+  m.loc.alloc(slab * sizeof(float));
+  m.gath.alloc(slab * m.world * sizeof(float));
+  CUDA_OK(cudaMemsetAsync(m.loc.p, 0, slab * sizeof(float), s));
+  CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, m.loc.as<float>(), B, relu, s, m.num_sms));
+  NCCL_OK(ncclAllGather(m.loc.p, m.gath.p, slab, ncclFloat, m.comm, s));
+  CUDA_OK(cudaMemcpy2DAsync(dst, (size_t)ld_dst * sizeof(float), m.gath.p, (size_t)B * sizeof(float),
+                            (size_t)B * sizeof(float), L.rows, cudaMemcpyDeviceToDevice, s));
+}
+
+struct Exec {
+  Model& m;
+  const std::vector<int>& bs;   // batch per layer
+  const float* input;           // image-major [K][features] (host or device)
+  bool on_device;
+  cudaStream_t s;
+  float* scores;                // [K][classes] (host or device)
+  // compute layer i for images [o, o + bs[i]) into dst (feature-major, ld)
+  void run(int i, int o, float* dst, int ld) {
+    const int Bi = bs[i];
+    Layer& L = *m.layers[i];
+    float* xin = m.lvl[i].as<float>();
+    if (i == 0) {
+      const float* src = input + (size_t)o * L.cols;
+      if (!on_device) {
+        m.stage_in.alloc((size_t)Bi * L.cols * sizeof(float));
+        CUDA_OK(cudaMemcpyAsync(m.stage_in.p, src, (size_t)Bi * L.cols * sizeof(float), cudaMemcpyHostToDevice, s));
+        src = m.stage_in.as<float>();
+      }
+      CUDA_OK(launch_transpose(src, Bi, (int)L.cols, (int)L.cols, xin, Bi, s));
+    } else {
+      const int b = bs[i - 1];
+      for (int p = 0; p < Bi / b; ++p) run(i - 1, o + p * b, xin + p * b, Bi);
+    }
+    layer_step(m, i, xin, Bi, Bi, dst, ld, s);
+  }
+  void round(int o) {
+    const int f = (int)m.layers.size();
+    const int Bf = bs[f - 1];
+    const uint32_t classes = m.layers[f - 1]->rows;
+    m.out.alloc((size_t)classes * Bf * sizeof(float));
+    run(f - 1, o, m.out.as<float>(), Bf);
+    if (m.rank != 0) return;
+    // [classes][Bf] -> scores[o..o+Bf)[classes]
+    float* dst = scores + (size_t)o * classes;
+    if (on_device) {
+      CUDA_OK(launch_transpose(m.out.as<float>(), (int)classes, Bf, Bf, dst, (int)classes, s));
+    } else {
+      m.host_stage.alloc((size_t)classes * Bf * sizeof(float));
+      CUDA_OK(launch_transpose(m.out.as<float>(), (int)classes, Bf, Bf, m.host_stage.as<float>(), (int)classes, s));
+      CUDA_OK(cudaMemcpyAsync(dst, m.host_stage.p, (size_t)classes * Bf * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+  }
+};
+
+void alloc_levels(Model& m, const std::vector<int>& bs) {
+  m.lvl.resize(m.layers.size());
+  for (size_t i = 0; i < m.layers.size(); ++i)
+    m.lvl[i].alloc((size_t)m.layers[i]->cols * bs[i] * sizeof(float));
+}
+
+void check_chain(const Model& m, const std::vector<int>& bs) {
+  if (bs.size() != m.layers.size()) throw Error(CDN_E_ARG, "plan length != number of layers");
+  for (size_t i = 0; i < bs.size(); ++i) {
+    if (bs[i] < 1) throw Error(CDN_E_ARG, "batch < 1");
+    if (i && (bs[i] < bs[i - 1] || bs[i] % bs[i - 1]))
+      throw Error(CDN_E_ARG, "plan is not a divisor chain (P:L675-679)");
+  }
+}
+
+void profile(Model& m, int Bmax, int reps) {
+  if (m.prof_bmax == Bmax && !m.prof.empty()) return;
+  const int f = (int)m.layers.size();
+  m.prof.assign((size_t)f * Bmax, 0.0);
+  cudaStream_t s = m.stream;
+  size_t maxin = 0, maxout = 0;
+  for (auto& L : m.layers) { maxin = std::max<size_t>(maxin, L->cols); maxout = std::max<size_t>(maxout, L->rows); }
+  DBuf xb, yb;
+  xb.alloc(maxin * Bmax * sizeof(float));
+  yb.alloc(maxout * Bmax * sizeof(float));
+  CUDA_OK(cudaMemsetAsync(xb.p, 0, maxin * Bmax * sizeof(float), s));
+  cudaEvent_t e0, e1;
+  CUDA_OK(cudaEventCreate(&e0));
+  CUDA_OK(cudaEventCreate(&e1));
+  std::vector<float> t(reps);
+  for (int i = 0; i < f; ++i)
+    for (int B = 1; B <= Bmax; ++B) {
+      layer_step(m, i, xb.as<float>(), B, B, yb.as<float>(), B, s);  // warm-up
+      for (int r = 0; r < reps; ++r) {
+        CUDA_OK(cudaEventRecord(e0, s));
+        layer_step(m, i, xb.as<float>(), B, B, yb.as<float>(), B, s);
+        CUDA_OK(cudaEventRecord(e1, s));
+        CUDA_OK(cudaEventSynchronize(e1));
+        CUDA_OK(cudaEventElapsedTime(&t[r], e0, e1));
+      }
+      std::sort(t.begin(), t.end());
+      m.prof[(size_t)i * Bmax + (B - 1)] = t[reps / 2];
+    }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  m.prof_bmax = Bmax;
+}
+
+std::vector<uint64_t> in_bytes(const Model& m) {
+  std::vector<uint64_t> v;
+  for (auto& L : m.layers) v.push_back(4ull * L->cols);
+  return v;
+}
+std::vector<uint64_t> out_bytes(const Model& m) {
+  std::vector<uint64_t> v;
+  for (auto& L : m.layers) v.push_back(4ull * L->rows);
+  return v;
+}
+std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
+  std::vector<uint64_t> v;
+  for (auto& L : m.layers) {
+    uint64_t ws = L->stats.ws_bytes;
+    if (m.world > 1) ws += 4ull * rows_per_rank(L->rows, m.world) * (m.world + 1) * Bmax;  // C-24: max over grid
+    v.push_back(ws);
+  }
+  return v;
+}
+
+PlanResult plan_for(Model& m, int K) {
+  profile(m, K, 5);
+  const int f = (int)m.layers.size();
+  auto inb = in_bytes(m), outb = out_bytes(m), ws = ws_bytes(m, K);
+  return plan_dp(m.prof.data(), inb.data(), outb.data(), ws.data(), f, K, m.tot, m.latency, 64 * 1024);
+}
+
+}  // namespace
+
+struct cdn_model {
+  Model m;
+};
+
+#define API_BEGIN try {
+#define API_END                                                      \
+  }                                                                  \
+  catch (const Error& e) { return fail(e.code, e.what()); }          \
+  catch (const std::bad_alloc&) { return fail(CDN_E_OOM, "host out of memory"); } \
+  catch (const std::exception& e) { return fail(CDN_E_ARG, e.what()); }           \
+  catch (...) { return fail(CDN_E_ARG, "unknown error"); }           \
+  return CDN_OK;
+
+extern "C" {
+
+int cdn_abi_version(void) { return CDN_ABI_VERSION; }
+const char* cdn_last_error(void) { return g_err.c_str(); }
+
+cdn_status cdn_nccl_unique_id(uint8_t out[128]) {
+  API_BEGIN
+  if (!out) return fail(CDN_E_ARG, "out is NULL");
+  ncclUniqueId id;
+  NCCL_OK(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+  API_END
+}
+
+cdn_status cdn_model_create(int device, int rank, int world, const uint8_t* nccl_id, cdn_model** out) {
+  API_BEGIN
+  if (!out || world < 1 || rank < 0 || rank >= world) return fail(CDN_E_ARG, "bad rank/world/out");
+  *out = nullptr;
+  auto h = std::make_unique<cdn_model>();
+  Model& m = h->m;
+  m.device = device;
+  m.rank = rank;
+  m.world = world;
+  CUDA_OK(cudaSetDevice(device));
+  CUDA_OK(cudaDeviceGetAttribute(&m.num_sms, cudaDevAttrMultiProcessorCount, device));
+  CUDA_OK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
+  if (world > 1 && nccl_id) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, 128);
+    NCCL_OK(ncclCommInitRank(&m.comm, world, id, rank));
+  }
+  *out = h.release();
+  API_END
+}
+
+void cdn_model_destroy(cdn_model* h) {
+  if (!h) return;
+  try {
+    cudaSetDevice(h->m.device);
+    cudaStreamSynchronize(h->m.stream);
+    h->m.layers.clear();
+    h->m.lvl.clear();
+    if (h->m.comm) ncclCommDestroy(h->m.comm);
+    if (h->m.stream) cudaStreamDestroy(h->m.stream);
+  } catch (...) {
+  }
+  delete h;
+}
+
+cdn_status cdn_model_load_layer(cdn_model* h, const void* cdni, size_t n, int layer_in_file,
+                                const cdn_layer_desc* desc, int* layer_idx) {
+  API_BEGIN
+  if (!h || !cdni || !desc) return fail(CDN_E_ARG, "NULL argument");
+  CUDA_OK(cudaSetDevice(h->m.device));
+  load_layer(h->m, (const uint8_t*)cdni, n, layer_in_file, *desc, layer_idx);
+  API_END
+}
+
+cdn_status cdn_model_set_memory_budget(cdn_model* h, uint64_t tot, double latency_ms) {
+  API_BEGIN
+  if (!h) return fail(CDN_E_ARG, "NULL model");
+  h->m.tot = tot;
+  h->m.latency = latency_ms > 0 ? latency_ms : 0.0;
+  API_END
+}
+
+cdn_status cdn_model_set_plan(cdn_model* h, const int* b, int n) {
+  API_BEGIN
+  if (!h || (n && !b)) return fail(CDN_E_ARG, "NULL argument");
+  std::vector<int> bs(b, b + n);
+  if (n) check_chain(h->m, bs);
+  h->m.fixed_plan = bs;
+  API_END
+}
+
+cdn_status cdn_model_plan(cdn_model* h, int K, int* batches, double* predicted_ms) {
+  API_BEGIN
+  if (!h || K < 1) return fail(CDN_E_ARG, "bad arguments");
+  Model& m = h->m;
+  if (m.layers.empty()) return fail(CDN_E_STATE, "no layers loaded");
+  if (m.tot == 0) return fail(CDN_E_STATE, "set a memory budget first");
+  if (m.world > 1 && !m.comm) return fail(CDN_E_STATE, "shard-only handle (no NCCL id)");
+  CUDA_OK(cudaSetDevice(m.device));
+  double total = 0.0;
+  int rem = K;
+  bool first = true;
+  while (rem > 0) {
+    PlanResult pr = plan_for(m, rem);
+    if (!pr.feasible) return fail(CDN_E_INFEASIBLE, "no batch plan fits TOT/latency (P:L671, L724)");
+    const int Bf = pr.batches.back();
+    const int rounds = rem / Bf;
+    total += rounds * pr.opt;
+    rem -= rounds * Bf;
+    if (first && batches) std::copy(pr.batches.begin(), pr.batches.end(), batches);
+    first = false;
+  }
+  if (predicted_ms) *predicted_ms = total;
+  API_END
+}
+
+cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* scores, int on_device, void* stream) {
+  API_BEGIN
+  if (!h || !input || K < 1 || (!scores && h->m.rank == 0)) return fail(CDN_E_ARG, "bad arguments");
+  Model& m = h->m;
+  if (m.layers.empty()) return fail(CDN_E_STATE, "no layers loaded");
+  if (m.busy) return fail(CDN_E_STATE, "concurrent call on one handle");
+  if (m.world > 1 && !m.comm) return fail(CDN_E_STATE, "shard-only handle (no NCCL id): use cdn_layer_forward");
+  m.busy = true;
+  struct Clear { bool& b; ~Clear() { b = false; } } clr{m.busy};
+  CUDA_OK(cudaSetDevice(m.device));
+  cudaStream_t s = pick(m, stream);
+  const int f = (int)m.layers.size();
+  int o = 0;
+  while (o < K) {
+    const int rem = K - o;
+    std::vector<int> bs;
+    if (!m.fixed_plan.empty() && m.fixed_plan.back() <= rem) {
+      bs = m.fixed_plan;
+    } else if (m.tot > 0) {
+      PlanResult pr = plan_for(m, rem);
+      if (!pr.feasible) return fail(CDN_E_INFEASIBLE, "no batch plan fits TOT/latency");
+      bs = pr.batches;
+    } else {
+      bs.assign(f, rem);  // no budget: the whole request as one batch
+    }
+    check_chain(m, bs);
+    alloc_levels(m, bs);
+    Exec ex{m, bs, input, on_device != 0, s, scores};
+    const int Bf = bs.back();
+    const int rounds = rem / Bf;
+    for (int r = 0; r < rounds; ++r) ex.round(o + r * Bf);
+    o += rounds * Bf;
+  }
+  if (!stream) CUDA_OK(cudaStreamSynchronize(s));
+  CUDA_OK(cudaGetLastError());
+  API_END
+}
+
+cdn_status cdn_layer_forward(cdn_model* h, int layer, const float* x, int ldx, int B, float* y, int ldy,
+                             void* stream) {
+  API_BEGIN
+  if (!h || layer < 0 || layer >= (int)h->m.layers.size() || !x || !y || B < 0)
+    return fail(CDN_E_ARG, "bad arguments");
+  Model& m = h->m;
+  Layer& L = *m.layers[layer];
+  if (ldx < B || ldy < B) return fail(CDN_E_ARG, "leading dimension < B");
+  cudaStream_t s = pick(m, stream);
+  CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, y, ldy, L.desc.relu, s, m.num_sms));
+  if (!stream) CUDA_OK(cudaStreamSynchronize(s));
+  API_END
+}
+
+cdn_status cdn_layer_decode(cdn_model* h, int layer, int32_t* row, int32_t* col, uint8_t* sym, float* val,
+                            uint64_t* n_tokens, void* stream) {
+  API_BEGIN
+  if (!h || layer < 0 || layer >= (int)h->m.layers.size() || !n_tokens) return fail(CDN_E_ARG, "bad arguments");
+  Layer& L = *h->m.layers[layer];
+  *n_tokens = L.stats.tokens;
+  if (!row && !col && !sym && !val) return CDN_OK;
+  if (!row || !col || !sym || !val) return fail(CDN_E_ARG, "all four outputs required");
+  cudaStream_t s = pick(h->m, stream);
+  CUDA_OK(launch_decode(L.dev, (int)L.row0, row, col, sym, val, s, h->m.num_sms));
+  if (!stream) CUDA_OK(cudaStreamSynchronize(s));
+  API_END
+}
+
+cdn_status cdn_model_num_layers(const cdn_model* h, int* n) {
+  if (!h || !n) return fail(CDN_E_ARG, "NULL");
+  *n = (int)h->m.layers.size();
+  return CDN_OK;
+}
+
+cdn_status cdn_layer_stats_get(const cdn_model* h, int layer, cdn_layer_stats* out) {
+  if (!h || !out || layer < 0 || layer >= (int)h->m.layers.size()) return fail(CDN_E_ARG, "bad arguments");
+  *out = h->m.layers[layer]->stats;
+  return CDN_OK;
+}
+
+cdn_status cdn_model_profile(cdn_model* h, int Bmax, int reps, double* time_ms) {
+  API_BEGIN
+  if (!h || Bmax < 1 || reps < 1 || !time_ms) return fail(CDN_E_ARG, "bad arguments");
+  if (h->m.layers.empty()) return fail(CDN_E_STATE, "no layers loaded");
+  CUDA_OK(cudaSetDevice(h->m.device));
+  h->m.prof_bmax = 0;
+  profile(h->m, Bmax, reps);
+  std::copy(h->m.prof.begin(), h->m.prof.end(), time_ms);
+  API_END
+}
+
+cdn_status cdn_compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols, double density,
+                              int r, int k, void** out, size_t* out_len) {
+  API_BEGIN
+  if (!W || !out || !out_len) return fail(CDN_E_ARG, "NULL argument");
+  std::vector<uint8_t> v = compress_dense(W, bias, rows, cols, density, r, k);
+  void* p = std::malloc(v.size());
+  if (!p) return fail(CDN_E_OOM, "malloc");
+  std::memcpy(p, v.data(), v.size());
+  *out = p;
+  *out_len = v.size();
+  API_END
+}
+
+void cdn_free(void* p) { std::free(p); }
+
+cdn_status cdn_plan_dp(const double* time_ms, const uint64_t* in_b, const uint64_t* out_b, const uint64_t* ws,
+                       int f, int Bmax, uint64_t tot, double latency_ms, uint64_t step, int* batches,
+                       double* opt_ms) {
+  API_BEGIN
+  if (!time_ms || !in_b || !out_b || !ws || !batches || f < 1 || Bmax < 1) return fail(CDN_E_ARG, "bad arguments");
+  PlanResult pr = plan_dp(time_ms, in_b, out_b, ws, f, Bmax, tot, latency_ms, step);
+  if (!pr.feasible) return fail(CDN_E_INFEASIBLE, "no feasible plan");
+  std::copy(pr.batches.begin(), pr.batches.end(), batches);
+  if (opt_ms) *opt_ms = pr.opt;
+  API_END
+}
+
+cdn_status cdn_debug_host_walk(const void* cdni, size_t n, int layer_in_file, int32_t* row, int32_t* col,
+                               uint8_t* sym, uint64_t* n_tokens) {
+  API_BEGIN
+  if (!cdni || !n_tokens) return fail(CDN_E_ARG, "NULL argument");
+  HostLayer H = parse_cdni_layer((const uint8_t*)cdni, n, layer_in_file);
+  LaneIndex ix;
+  std::vector<Token> toks;
+  build_lane_index(H, 0, H.rows, choose_lanes_per_row(H, 0, H.rows, 64), ix, row ? &toks : nullptr);
+  *n_tokens = ix.tokens;
+  if (row && col && sym)
+    for (size_t i = 0; i < toks.size(); ++i) { row[i] = toks[i].row; col[i] = toks[i].col; sym[i] = toks[i].sym; }
+  API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// Host side of the library: CDNI container, canonical Huffman tables, the
+// load-time decode-lane index (container row a1 of SURVEY §8(a)), the
+// product-side compressor and the variable-batch DP.  No CUDA here.
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cdn.h"
+
+namespace cdn {
+
+struct Error : std::runtime_error {
+  cdn_status code;
+  Error(cdn_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// Canonical Huffman code rebuilt from (symbol, length) pairs (C-17).
+struct HuffCode {
+  int n = 0;
+  int max_len = 0;
+  std::vector<uint16_t> syms;     // ascending symbol order (as stored)
+  std::vector<uint8_t> lens;
+  std::vector<uint16_t> sorted;   // canonical order: (length, symbol)
+  uint32_t count[33] = {0};
+  uint32_t first_code[33] = {0};
+  uint32_t first_index[33] = {0};
+  std::vector<uint32_t> code_of;  // per symbol (alphabet-sized), encode side
+  std::vector<uint8_t> len_of;
+
+  // Validates lengths (1..32 else UNSUPPORTED/MALFORMED), symbol range, Kraft
+  // equality (complete code for n >= 2; a single symbol has length 1).
+  void build(int alphabet, const char* what);
+  // Decode one symbol from a 32-bit left-aligned window.  false: no code.
+  bool decode(uint32_t window, uint32_t& sym, uint32_t& len) const;
+};
+
+struct HostLayer {
+  uint32_t rows = 0, cols = 0, bh = 1, bw = 0, k = 0, r = 0;
+  std::vector<float> codebook;
+  HuffCode val, gap;
+  std::vector<uint64_t> rp;       // 2*(rows+1): (val bit, gap bit) per row start
+  std::vector<uint8_t> vbytes, gbytes;  // streams, + 8 zero bytes of padding
+  uint64_t vbits = 0, gbits = 0;
+  bool has_bias = false;
+  std::vector<float> bias;
+};
+
+// Parse layer `idx` of a CDNI buffer (format in DESIGN.md).
+HostLayer parse_cdni_layer(const uint8_t* p, size_t n, int idx, int* n_layers_out = nullptr);
+
+// Decode-lane index for rows [r0, r1) of a layer.
+// G lanes per row; lane j owns the tokens whose absolute column falls in
+// [j*W, (j+1)*W), W = ceil(cols/G).  Record per (row, lane): the lane's bit
+// lengths in both streams and delta = j*W - (column of the previous token),
+// 1 <= delta <= 2^k (pads bound every gap by 2^k).
+struct LaneIndex {
+  int G = 1, log2G = 0;
+  uint32_t W = 1;
+  bool rec64 = false;
+  std::vector<uint32_t> rec32;
+  std::vector<uint64_t> rec64v;
+  std::vector<uint64_t> tok_start;  // (rows*G + 1) token index of each lane's first token
+  uint64_t tokens = 0, nnz = 0;
+};
+
+struct Token { int32_t row, col; uint8_t sym; };
+
+// Host walk of rows [r0, r1): validates the streams (both end exactly at the
+// next row_ptr, equal token counts, columns < cols, pad invariant C-06) and
+// fills the lane index.  tokens_out, if non-null, receives every token.
+void build_lane_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, LaneIndex& out,
+                      std::vector<Token>* tokens_out = nullptr);
+
+int choose_lanes_per_row(const HostLayer& L, uint32_t r0, uint32_t r1, int target_tokens);
+
+// Product-side compressor (independent of oracle/, same readings).
+std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols,
+                                    double density, int r, int k);
+
+// Variable-batch DP with memory axis granularity `step` bytes.
+struct PlanResult {
+  bool feasible = false;
+  std::vector<int> batches;
+  double opt = 0.0;
+};
+PlanResult plan_dp(const double* time_ms, const uint64_t* in_b, const uint64_t* out_b,
+                   const uint64_t* ws, int f, int Bmax, uint64_t tot, double latency, uint64_t step);
+
+}  // namespace cdn

@@ -1,0 +1,371 @@
+// CUDA kernels for sm_100a: parallel Huffman decode of the val / col_ind
+// streams, gap -> absolute column prefix sum, codebook dequantize, and the
+// fused sparse FC multiply (Alg. 1 lines 5-9).
+//
+// Parallel decomposition:
+//   * G decode lanes per weight row; lane j owns the tokens whose absolute
+//     column lies in the band [j*W, (j+1)*W).  Its start bit offsets in both
+//     streams are the row's row_ptr tuple plus an exclusive
+//     warp scan of the lanes' recorded bit lengths; its previous column is
+//     j*W - delta (pads bound every gap by 2^k, so delta needs k bits).
+//   * each lane walks its tokens: LUT decode (smem) of one val and one gap
+//     code, c += g + 1 (Alg. 1 l.7, reading C-01), w = C[sym] (l.8), and for
+//     real tokens (sym != 0) acc[b] += w * x[c][b] (l.9, Eq. 2);
+//   * the G partial sums of a row are reduced with a fixed shuffle tree
+//     (deterministic), then bias + ReLU and one store per (row, image).
+#include "kernels.cuh"
+
+namespace cdn {
+
+namespace {
+
+__device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// MSB-first bit reader over big-endian packed words.  Invariant: nb > 32 after
+// every skip, so peek() always returns 32 valid bits; the next word is loaded
+// one refill ahead to keep the global load off the decode critical path.
+struct BitReader {
+  const uint32_t* p;
+  uint64_t buf;
+  uint32_t nb;
+  uint32_t nxt;
+  __device__ __forceinline__ void init(const uint32_t* words, uint32_t bit) {
+    p = words + (bit >> 5);
+    const uint32_t s = bit & 31;
+    const uint64_t w0 = ldg_u32(p), w1 = ldg_u32(p + 1);
+    nxt = ldg_u32(p + 2);
+    p += 3;
+    buf = ((w0 << 32) | w1) << s;
+    nb = 64 - s;
+  }
+  __device__ __forceinline__ uint32_t peek() const { return (uint32_t)(buf >> 32); }
+  __device__ __forceinline__ void skip(uint32_t n) {
+    buf <<= n;
+    nb -= n;
+    if (nb <= 32) {
+      buf |= (uint64_t)nxt << (32 - nb);
+      nb += 32;
+      nxt = ldg_u32(p);
+      ++p;
+    }
+  }
+};
+
+struct SmemTables {
+  uint32_t* vlut;
+  uint32_t* glut;
+  float* cb;
+  uint32_t* vtab;
+  uint32_t* gtab;
+  uint16_t* vsorted;
+  uint16_t* gsorted;
+};
+
+__device__ __forceinline__ SmemTables carve(const FcDev& L, unsigned char* base) {
+  SmemTables t;
+  size_t off = 0;
+  t.vlut = (uint32_t*)(base + off); off += sizeof(uint32_t) << L.Lv;
+  t.glut = (uint32_t*)(base + off); off += sizeof(uint32_t) << L.Lg;
+  t.cb = (float*)(base + off); off += sizeof(float) * L.ncb;
+  t.vtab = (uint32_t*)(base + off); off += sizeof(uint32_t) * 99;
+  t.gtab = (uint32_t*)(base + off); off += sizeof(uint32_t) * 99;
+  t.vsorted = (uint16_t*)(base + off); off += sizeof(uint16_t) * (L.nvs + 1);
+  t.gsorted = (uint16_t*)(base + off);
+  return t;
+}
+
+__device__ void stage_tables(const FcDev& L, const SmemTables& t) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < (1 << L.Lv); i += nt) t.vlut[i] = L.vlut[i];
+  for (int i = tid; i < (1 << L.Lg); i += nt) t.glut[i] = L.glut[i];
+  for (int i = tid; i < L.ncb; i += nt) t.cb[i] = L.codebook[i];
+  for (int i = tid; i < 99; i += nt) { t.vtab[i] = L.vtab[i]; t.gtab[i] = L.gtab[i]; }
+  for (int i = tid; i < L.nvs; i += nt) t.vsorted[i] = L.vsorted[i];
+  for (int i = tid; i < L.ngs; i += nt) t.gsorted[i] = L.gsorted[i];
+}
+
+// Canonical decode of the code starting at the top of w: primary LUT on the
+// first Lb bits, canonical first_code/count walk for longer codes.
+__device__ __forceinline__ uint32_t decode_sym(uint32_t w, const uint32_t* lut, int Lb,
+                                               const uint32_t* tab, const uint16_t* sorted,
+                                               int maxlen, uint32_t& len) {
+  const uint32_t e = lut[w >> (32 - Lb)];
+  if (e != 0) {
+    len = e >> 16;
+    return e & 0xFFFFu;
+  }
+  for (int l = Lb + 1; l <= maxlen; ++l) {
+    const uint32_t c = (l == 32) ? w : (w >> (32 - l));
+    const uint32_t off = c - tab[l];
+    if (off < tab[33 + l]) {
+      len = (uint32_t)l;
+      return sorted[tab[66 + l] + off];
+    }
+  }
+  len = 32;  // unreachable for a validated container
+  return 0;
+}
+
+struct LaneStart {
+  uint32_t vbit, gbit, vlen;
+  int col;  // column of the previous token (-1 at row start)
+};
+
+// Lane start state from the row_ptr tuple + warp scan of the lane lengths.
+template <bool REC64>
+__device__ __forceinline__ LaneStart lane_start(const FcDev& L, int row, bool active, int lj) {
+  uint32_t vlen = 0, glen = 0, dm1 = 0;
+  if (active) {
+    const size_t q = (size_t)row * L.G + lj;
+    if (REC64) {
+      const uint64_t r = ((const uint64_t*)L.rec)[q];
+      vlen = (uint32_t)(r & 0xFFFFFFu);
+      glen = (uint32_t)((r >> 24) & 0xFFFFFFu);
+      dm1 = (uint32_t)(r >> 48);
+    } else {
+      const uint32_t r = ((const uint32_t*)L.rec)[q];
+      vlen = r & 0xFFFu;
+      glen = (r >> 12) & 0xFFFu;
+      dm1 = r >> 24;
+    }
+  }
+  uint32_t vs = vlen, gs = glen;
+  for (int o = 1; o < L.G; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, vs, o, L.G);
+    const uint32_t b = __shfl_up_sync(0xffffffffu, gs, o, L.G);
+    if (lj >= o) { vs += a; gs += b; }
+  }
+  LaneStart st;
+  const uint32_t v0 = active ? L.rp[2 * row] : 0u;
+  const uint32_t g0 = active ? L.rp[2 * row + 1] : 0u;
+  st.vbit = v0 + vs - vlen;
+  st.gbit = g0 + gs - glen;
+  st.vlen = vlen;
+  st.col = lj * L.W - (int)(dm1 + 1);
+  return st;
+}
+
+template <int BS, bool REC64, bool VEC>
+__global__ void __launch_bounds__(256, 4) k_fc_forward(FcDev L, const float* __restrict__ x, int ldx,
+                                                    int B, float* __restrict__ y, int ldy, int relu) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemTables t = carve(L, smem);
+  stage_tables(L, t);
+  __syncthreads();
+
+  const int b0 = blockIdx.y * BS;
+  const int nb = min(BS, B - b0);
+  x += b0;
+  y += b0;
+  const int lj = threadIdx.x & (L.G - 1);
+  const int rows_per_cta = blockDim.x >> L.log2G;
+  const uint32_t padg = (1u << L.k) - 1u;
+  (void)padg;
+
+  for (int rbase = blockIdx.x * rows_per_cta; rbase < L.nrows; rbase += gridDim.x * rows_per_cta) {
+    const int row = rbase + (threadIdx.x >> L.log2G);
+    const bool active = row < L.nrows;
+    const LaneStart st = lane_start<REC64>(L, row, active, lj);
+    float acc[BS];
+#pragma unroll
+    for (int b = 0; b < BS; ++b) acc[b] = 0.f;
+    if (st.vlen) {
+      BitReader vr, gr;
+      vr.init(L.vw, st.vbit);
+      gr.init(L.gw, st.gbit);
+      int rem = (int)st.vlen;
+      int col = st.col;
+      while (rem > 0) {
+        uint32_t lv, lg;
+        const uint32_t vs = decode_sym(vr.peek(), t.vlut, L.Lv, t.vtab, t.vsorted, L.vmax, lv);
+        vr.skip(lv);
+        rem -= (int)lv;
+        const uint32_t gs = decode_sym(gr.peek(), t.glut, L.Lg, t.gtab, t.gsorted, L.gmax, lg);
+        gr.skip(lg);
+        col += (int)gs + 1;
+        if (vs != 0) {
+          const float w = t.cb[vs];
+          const float* xp = x + (size_t)col * ldx;
+          if (VEC && BS % 4 == 0) {
+#pragma unroll
+            for (int b = 0; b < BS; b += 4) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(xp + b));
+              acc[b] = fmaf(w, v.x, acc[b]);
+              acc[b + 1] = fmaf(w, v.y, acc[b + 1]);
+              acc[b + 2] = fmaf(w, v.z, acc[b + 2]);
+              acc[b + 3] = fmaf(w, v.w, acc[b + 3]);
+            }
+          } else {
+#pragma unroll
+            for (int b = 0; b < BS; ++b)
+              if (b < nb) acc[b] = fmaf(w, __ldg(xp + b), acc[b]);
+          }
+        }
+      }
+    }
+    // fixed-order reduction of the G lane partials of each row
+#pragma unroll
+    for (int b = 0; b < BS; ++b)
+      for (int o = L.G >> 1; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o, L.G);
+    if (active && lj == 0) {
+      const float v = L.bias[row];
+#pragma unroll
+      for (int b = 0; b < BS; ++b) {
+        if (b < nb) {
+          float o = acc[b] + v;
+          if (relu) o = fmaxf(o, 0.f);
+          y[(size_t)row * ldy + b] = o;
+        }
+      }
+    }
+  }
+}
+
+template <bool REC64>
+__global__ void __launch_bounds__(256, 4) k_decode(FcDev L, int row_offset, int32_t* __restrict__ orow,
+                                                int32_t* __restrict__ ocol, uint8_t* __restrict__ osym,
+                                                float* __restrict__ oval) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemTables t = carve(L, smem);
+  stage_tables(L, t);
+  __syncthreads();
+  const int lj = threadIdx.x & (L.G - 1);
+  const int rows_per_cta = blockDim.x >> L.log2G;
+  for (int rbase = blockIdx.x * rows_per_cta; rbase < L.nrows; rbase += gridDim.x * rows_per_cta) {
+    const int row = rbase + (threadIdx.x >> L.log2G);
+    const bool active = row < L.nrows;
+    const LaneStart st = lane_start<REC64>(L, row, active, lj);
+    if (!st.vlen) continue;
+    uint64_t pos = L.tok_start[(size_t)row * L.G + lj];
+    BitReader vr, gr;
+    vr.init(L.vw, st.vbit);
+    gr.init(L.gw, st.gbit);
+    int rem = (int)st.vlen;
+    int col = st.col;
+    while (rem > 0) {
+      uint32_t lv, lg;
+      const uint32_t vs = decode_sym(vr.peek(), t.vlut, L.Lv, t.vtab, t.vsorted, L.vmax, lv);
+      vr.skip(lv);
+      rem -= (int)lv;
+      const uint32_t gs = decode_sym(gr.peek(), t.glut, L.Lg, t.gtab, t.gsorted, L.gmax, lg);
+      gr.skip(lg);
+      col += (int)gs + 1;
+      orow[pos] = row + row_offset;
+      ocol[pos] = col;
+      osym[pos] = (uint8_t)vs;
+      oval[pos] = t.cb[vs];
+      ++pos;
+    }
+  }
+}
+
+__global__ void k_transpose(const float* __restrict__ in, int rows, int cols, int ldi,
+                            float* __restrict__ out, int ldo) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[(size_t)r * ldi + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[(size_t)c * ldo + r] = tile[threadIdx.x][i];
+  }
+}
+
+// Resident CTAs per SM for (kernel, smem); cached so the launch path does no
+// occupancy query after the first call (it is host latency inside a step).
+template <class K>
+int occupancy_grid(K kernel, int threads, size_t smem, int num_sms, int work_ctas) {
+  struct Entry { const void* k; size_t smem; int per_sm; };
+  static thread_local Entry cache[64];
+  static thread_local int ncache = 0;
+  int per_sm = 0;
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].k == (const void*)kernel && cache[i].smem == smem) { per_sm = cache[i].per_sm; break; }
+  if (per_sm == 0) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (ncache < 64) cache[ncache++] = Entry{(const void*)kernel, smem, per_sm};
+  }
+  int g = per_sm * num_sms;
+  return work_ctas < g ? (work_ctas > 0 ? work_ctas : 1) : g;
+}
+
+template <int BS, bool REC64, bool VEC>
+cudaError_t launch_fc_t(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu,
+                        cudaStream_t s, int num_sms) {
+  const int threads = 256;
+  const size_t smem = fc_smem_bytes(L);
+  auto kern = k_fc_forward<BS, REC64, VEC>;
+  const int rows_per_cta = threads / L.G;
+  const int work = (L.nrows + rows_per_cta - 1) / rows_per_cta;
+  dim3 grid(occupancy_grid(kern, threads, smem, num_sms, work), (B + BS - 1) / BS);
+  kern<<<grid, threads, smem, s>>>(L, x, ldx, B, y, ldy, relu);
+  return cudaGetLastError();
+}
+
+template <int BS, bool REC64>
+cudaError_t launch_fc_bs(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu,
+                         cudaStream_t s, int num_sms) {
+  const bool vec = (BS % 4 == 0) && (ldx % 4 == 0) && (((uintptr_t)x & 15) == 0) && (B % BS == 0);
+  if (vec) return launch_fc_t<BS, REC64, true>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+  return launch_fc_t<BS, REC64, false>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+}
+
+template <bool REC64>
+cudaError_t launch_fc_rec(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu,
+                          cudaStream_t s, int num_sms) {
+  if (B <= 1) return launch_fc_bs<1, REC64>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+  if (B <= 2) return launch_fc_bs<2, REC64>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+  if (B <= 4) return launch_fc_bs<4, REC64>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+  return launch_fc_bs<8, REC64>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+}
+
+}  // namespace
+
+size_t fc_smem_bytes(const FcDev& L) {
+  size_t b = (sizeof(uint32_t) << L.Lv) + (sizeof(uint32_t) << L.Lg) + sizeof(float) * L.ncb +
+             2 * 99 * sizeof(uint32_t) + sizeof(uint16_t) * (L.nvs + 1) + sizeof(uint16_t) * (L.ngs + 1);
+  return (b + 15) & ~(size_t)15;
+}
+
+cudaError_t launch_fc_forward(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy,
+                              int relu, cudaStream_t s, int num_sms) {
+  if (B <= 0 || L.nrows <= 0) return cudaSuccess;
+  if (L.rec64) return launch_fc_rec<true>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+  return launch_fc_rec<false>(L, x, ldx, B, y, ldy, relu, s, num_sms);
+}
+
+cudaError_t launch_decode(const FcDev& L, int row_offset, int32_t* row, int32_t* col, uint8_t* sym,
+                          float* val, cudaStream_t s, int num_sms) {
+  if (L.nrows <= 0) return cudaSuccess;
+  const int threads = 256;
+  const size_t smem = fc_smem_bytes(L);
+  const int rows_per_cta = threads / L.G;
+  const int work = (L.nrows + rows_per_cta - 1) / rows_per_cta;
+  if (L.rec64) {
+    auto k = k_decode<true>;
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, row_offset, row, col, sym, val);
+  } else {
+    auto k = k_decode<false>;
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, row_offset, row, col, sym, val);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float* out, int ldo,
+                             cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+  k_transpose<<<grid, block, 0, s>>>(in, rows, cols, ldi, out, ldo);
+  return cudaGetLastError();
+}
+
+}  // namespace cdn

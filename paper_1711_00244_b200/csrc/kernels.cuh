@@ -1,0 +1,48 @@
+// Device-side data of one loaded FC/CONV weight matrix (a rank's row block)
+// and the kernel launchers.  Layout rationale: DESIGN.md "Data layout in HBM".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cdn {
+
+constexpr int kLutMaxBits = 10;   // primary LUT width cap; longer codes take the canonical slow path
+
+struct FcDev {
+  const uint32_t* vw = nullptr;      // val stream as big-endian u32 words (bit i = bit 31-(i%32) of word i/32)
+  const uint32_t* gw = nullptr;      // gap (col_ind) stream, same packing
+  const uint32_t* rp = nullptr;      // 2*(nrows+1): (val bit, gap bit) at each local row start (row_ptr)
+  const void* rec = nullptr;         // nrows*G lane records (u32 or u64, see host.hpp LaneIndex)
+  const uint64_t* tok_start = nullptr;  // nrows*G+1 token index per lane (decode kernel only)
+  const uint32_t* vlut = nullptr;    // 2^Lv entries: (len << 16) | sym, 0 = longer code
+  const uint32_t* glut = nullptr;    // 2^Lg entries
+  const uint32_t* vtab = nullptr;    // [0..32] first_code, [33..65] count, [66..98] first_index
+  const uint32_t* gtab = nullptr;
+  const uint16_t* vsorted = nullptr; // symbols in canonical order
+  const uint16_t* gsorted = nullptr;
+  const float* codebook = nullptr;   // 2^r fp32 centres, [0] = 0.0 (pads)
+  const float* bias = nullptr;       // nrows fp32 (zeros if absent)
+  int nrows = 0, cols = 0;
+  int G = 1, log2G = 0, W = 1;       // lanes per row, lane column width
+  int k = 4, Lv = 1, Lg = 1, vmax = 0, gmax = 0;
+  int ncb = 32, nvs = 0, ngs = 0;
+  int rec64 = 0;
+};
+
+// y[r][b] = act( sum_j W_q[r][j] x[j][b] + v[r] ) for the rank's rows, B images,
+// feature-major activations (x: [cols][ldx], y: [nrows][ldy]).
+cudaError_t launch_fc_forward(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy,
+                              int relu, cudaStream_t s, int num_sms);
+
+// Every token of the rank's rows (pads included) -> row (global index), column,
+// val symbol, codebook value.  row_offset converts local to global rows.
+cudaError_t launch_decode(const FcDev& L, int row_offset, int32_t* row, int32_t* col, uint8_t* sym,
+                          float* val, cudaStream_t s, int num_sms);
+
+// [B][K] image-major -> [K][ldo] feature-major (and the reverse).
+cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float* out, int ldo,
+                             cudaStream_t s);
+
+size_t fc_smem_bytes(const FcDev& L);
+
+}  // namespace cdn

@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Decode: bit-exact (row, column, symbol, codebook value),
+pads included.  Layer outputs: ||y_gpu - y_ref||_inf / ||y_ref||_inf <= 1e-4
+against the fp64 oracle on the same fp32 input (north_star tolerance); the
+elementwise error relative to sum_j |w_ij a_j| + |v_i| is also checked against
+a bound derived from fp32 accumulation."""
+import os
+import zlib
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import cdni, compress, decode, infer
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    return torch, torch.device("cuda:0")
+
+
+_CACHE = {}
+
+
+def oracle_layer(key, W, d, r, k, bias):
+    if key not in _CACHE:
+        c = compress.compress_layer(W, d, r, k, bias)
+        _CACHE[key] = (c, cdni.serialize([c.layer]))
+    return _CACHE[key]
+
+
+def config_layer(cfg, i):
+    spec = synth.CONFIGS[cfg].fc[i]
+    W, v = synth.fc_weights(spec, synth.CONFIGS[cfg].seed)
+    c, buf = oracle_layer((cfg, i), W, spec.density, spec.r, spec.k, v)
+    return spec, c, buf
+
+
+def make_model(torch, buf, relu=False, rank=0, world=1):
+    import paper_1711_00244_b200 as cdn
+    m = cdn.Model(0, rank=rank, world=world)
+    m.load_layer(buf, cdn.LayerDesc.fc(relu))
+    return m
+
+
+def gpu_decode(torch, dev, m, layer=0):
+    n = m.decode_count(layer)
+    row = torch.empty(n, dtype=torch.int32, device=dev)
+    col = torch.empty(n, dtype=torch.int32, device=dev)
+    sym = torch.empty(n, dtype=torch.uint8, device=dev)
+    val = torch.empty(n, dtype=torch.float32, device=dev)
+    m.decode(layer, row, col, sym, val)
+    torch.cuda.synchronize()
+    return row.cpu().numpy(), col.cpu().numpy(), sym.cpu().numpy(), val.cpu().numpy()
+
+
+def expected_tokens(c):
+    """(row, col, sym, val) of every token from the oracle's own pre-encoding
+    streams: columns by the C-01 prefix sum, values from the codebook."""
+    rows = np.repeat(np.arange(c.row_tokens.size), c.row_tokens)
+    g = c.gap_tokens + 1
+    cs = np.cumsum(g)
+    starts = np.zeros(c.row_tokens.size + 1, dtype=np.int64)
+    np.cumsum(c.row_tokens, out=starts[1:])
+    base = np.zeros_like(cs)
+    nonempty = c.row_tokens > 0
+    first = starts[:-1][nonempty]
+    offs = np.where(first > 0, cs[first - 1], 0)
+    base_idx = np.repeat(offs, c.row_tokens[nonempty])
+    col = cs - base_idx - 1
+    sym = c.val_tokens
+    val = c.layer.codebook[sym]
+    return rows, col, sym, val
+
+
+def check_decode(torch, dev, c, buf):
+    m = make_model(torch, buf)
+    R, Cc, S, V = gpu_decode(torch, dev, m)
+    er, ec, es, ev = expected_tokens(c)
+    assert np.array_equal(R, er)
+    assert np.array_equal(Cc, ec)
+    assert np.array_equal(S, es.astype(np.uint8))
+    assert np.array_equal(V.view(np.uint32), ev.astype(np.float32).view(np.uint32))
+    # real tokens are exactly the kept entries with their centres
+    real = S != 0
+    assert np.array_equal(c.mask[R[real], Cc[real]], np.ones(real.sum(), bool))
+    assert real.sum() == c.mask.sum()
+    return m, (R, Cc, S, V)
+
+
+def rel_err(y, ref):
+    return np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-30)
+
+
+def gpu_forward(torch, dev, m, a, N, layer=0):
+    """a: image-major [B][K] fp32 -> y image-major [B][N] via feature-major device buffers."""
+    B = a.shape[0]
+    x = torch.from_numpy(np.ascontiguousarray(a.T)).to(dev)
+    y = torch.full((N, B), float("nan"), dtype=torch.float32, device=dev)
+    m.layer_forward(layer, x, B, B, y, B)
+    torch.cuda.synchronize()
+    return y.cpu().numpy().T
+
+
+def check_forward(torch, dev, m, c, bias, a, relu):
+    y = gpu_forward(torch, dev, m, a, c.layer.rows)
+    ref = infer.fc_forward(c.dense_q(), a, bias, apply_relu=relu)
+    assert np.isfinite(y).all()
+    e = rel_err(y, ref)
+    assert e <= TOL, e
+    scale = infer.fc_abs_scale(c.dense_q(), a, bias)
+    kmax = max(1, int(c.row_tokens.max()))
+    elem = (np.abs(y - ref) / np.maximum(scale, 1e-30)).max()
+    assert elem <= 2 * kmax * 2.0 ** -24 + 1e-12, elem    # fp32 summation bound gamma_n
+    return e
+
+
+# --------------------------------------------------------------------- decode
+
+def test_decode_c1_bit_exact_vs_plain_decode(torch_dev):
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C1", 0)
+    m, (R, Cc, S, V) = check_decode(torch, dev, c, buf)
+    # and against the plain bit-by-bit Alg. 1 decode of the container
+    L = cdni.deserialize(buf)[0]
+    r2, c2, s2, v2 = decode.decode_layer(L)
+    assert np.array_equal(R, r2) and np.array_equal(Cc, c2) and np.array_equal(S, s2)
+
+
+@pytest.mark.parametrize("cfg,i", [("C2", 0), ("C3", 1), ("C3", 2), ("C5", 0), ("C5", 1), ("C5", 2)])
+def test_decode_config_layers_bit_exact(torch_dev, cfg, i):
+    torch, dev = torch_dev
+    spec, c, buf = config_layer(cfg, i)
+    m, (R, Cc, S, V) = check_decode(torch, dev, c, buf)
+    # sampled rows against the plain decode (long codes of up to 20 bits included)
+    L = cdni.deserialize(buf)[0]
+    rows = [0, 1, L.rows // 2, L.rows - 1]
+    r2, c2, s2, _ = decode.decode_layer(L, rows)
+    sel = np.isin(R, rows)
+    assert np.array_equal(R[sel], r2) and np.array_equal(Cc[sel], c2) and np.array_equal(S[sel], s2)
+
+
+@pytest.mark.parametrize("G", ["1", "2", "8", "32"])
+def test_decode_every_lane_split(torch_dev, G, monkeypatch):
+    torch, dev = torch_dev
+    monkeypatch.setenv("CDN_LANES_PER_ROW", G)
+    spec, c, buf = config_layer("C2", 0)
+    m, _ = check_decode(torch, dev, c, buf)
+    st = m.stats(0)
+    assert st["lanes_per_row"] == int(G)
+
+
+EDGE = [
+    # name, rows, cols, density, r, k, scale
+    ("all_pruned", 16, 50, 0.0, 5, 4, 1.0),
+    ("single_nnz", 16, 50, 1.0 / 800, 5, 4, 1.0),
+    ("k2_long_pads", 33, 700, 0.01, 5, 2, 1.0),
+    ("k1_pads", 9, 300, 0.05, 3, 1, 1.0),
+    ("r1_single_symbol", 20, 64, 0.3, 1, 4, 1.0),
+    ("dense_k8_r8", 40, 363, 0.84, 8, 8, 1.0),
+    ("ragged_tiny", 1, 5, 0.6, 2, 2, 1.0),
+    ("wide_rows", 3, 25088, 0.04, 5, 4, 1.0),
+    ("tall", 2000, 17, 0.3, 5, 4, 1.0),
+]
+
+
+@pytest.mark.parametrize("name,rows,cols,d,r,k,scale", EDGE)
+def test_edge_fixtures_decode_and_forward(torch_dev, name, rows, cols, d, r, k, scale):
+    torch, dev = torch_dev
+    W = synth.random_matrix(rows, cols, seed=zlib.crc32(name.encode()) % 1000, scale=scale)
+    v = synth.random_matrix(1, rows, seed=7).ravel()
+    c, buf = oracle_layer(name, W, d, r, k, v)
+    m, _ = check_decode(torch, dev, c, buf)
+    for B in (1, 3, 8, 13):
+        a = synth.random_activations(cols, B, seed=B)
+        check_forward(torch, dev, m, c, v, a, relu=False)
+
+
+def test_long_codes_take_the_slow_path(torch_dev):
+    """Skewed symbol counts give val codes longer than the 10-bit primary LUT."""
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C5", 0)
+    assert max(c.layer.val_lengths.values()) > 10
+    # tokens with long codes exist and decoded exactly (covered by the full check)
+    long_syms = [s for s, L in c.layer.val_lengths.items() if L > 10]
+    assert np.isin(c.val_tokens, long_syms).any()
+
+
+# --------------------------------------------------------------------- forward
+
+@pytest.mark.parametrize("B", [1, 2, 3, 8, 31, 32, 33, 128])
+def test_forward_c2(torch_dev, B):
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C2", 0)
+    m = make_model(torch, buf, relu=False)
+    W, v = synth.fc_weights(spec, 0)
+    a = synth.fc_inputs(spec.cols, B, 0)
+    check_forward(torch, dev, m, c, v, a, relu=False)
+
+
+def test_forward_c1_b1(torch_dev):
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C1", 0)
+    m = make_model(torch, buf)
+    _, v = synth.fc_weights(spec, 0)
+    check_forward(torch, dev, m, c, v, synth.fc_inputs(spec.cols, 1, 0), relu=False)
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+@pytest.mark.parametrize("B", [1, 8, 64])
+def test_forward_c5_layers(torch_dev, i, B):
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C5", i)
+    m = make_model(torch, buf, relu=spec.relu)
+    _, v = synth.fc_weights(spec, 0)
+    a = synth.fc_inputs(spec.cols, B, 0)
+    check_forward(torch, dev, m, c, v, a, relu=spec.relu)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_shards_concatenate_to_full(torch_dev, world):
+    """Row-block sharding: each rank's slice of the same streams
+    gives exactly the rows of the 1-GPU result."""
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C3", 2)   # fc8 1000 rows: ragged last shard at 3 and 8
+    _, v = synth.fc_weights(spec, 0)
+    a = synth.fc_inputs(spec.cols, 4, 0)
+    full = gpu_forward(torch, dev, make_model(torch, buf), a, spec.rows)
+    parts = []
+    for r in range(world):
+        m = make_model(torch, buf, rank=r, world=world)
+        st = m.stats(0)
+        y = gpu_forward(torch, dev, m, a, st["row_end"] - st["row_begin"])
+        parts.append(y)
+        R, Cc, S, V = gpu_decode(torch, dev, m)
+        assert (R >= st["row_begin"]).all() and (R < st["row_end"]).all()
+    got = np.concatenate(parts, axis=1)
+    assert np.array_equal(got, full)
+
+
+# ----------------------------------------------------------------- end to end
+
+def test_infer_c3_stack_matches_oracle_chain(torch_dev):
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    cfg = synth.CONFIGS["C3"]
+    m = cdn.Model(0)
+    comps = []
+    for i, spec in enumerate(cfg.fc):
+        _, c, buf = config_layer("C3", i)
+        m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+        comps.append((c, synth.fc_weights(spec, 0)[1], spec.relu))
+    K = 24
+    a = synth.fc_inputs(cfg.fc[0].cols, K, 0)
+    scores = np.zeros((K, cfg.fc[-1].rows), np.float32)
+    m.set_plan([2, 6, 12])              # variable batch: 12/6 phases of 6, 6/2 phases of 2
+    m.infer(a, K, scores, on_device=False)
+    x = a
+    for c, v, relu in comps:
+        x = infer.fc_forward(c.dense_q(), x, v, apply_relu=relu).astype(np.float32)
+    assert rel_err(scores, x) <= TOL
+    # device-resident input/output, plan = whole batch
+    m.set_plan([K, K, K])
+    xi = torch.from_numpy(a).to(dev)
+    so = torch.zeros((K, cfg.fc[-1].rows), dtype=torch.float32, device=dev)
+    m.infer(xi, K, so, on_device=True)
+    torch.cuda.synchronize()
+    assert rel_err(so.cpu().numpy(), x) <= TOL
