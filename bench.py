@@ -285,24 +285,26 @@ def bench_b1(cdn, torch, dev, layers, specs, R, flush, pk):
     for i, s in enumerate(specs):
         for mm in models:                      # warm-up
             mm.layer_forward(i, x[i], 1, 1, y[i], 1, stream=sp)
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        ts = []
-        for mm in models:
+        samples = []
+        for _ in range(5):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            torch.cuda._sleep(3_000_000)       # GPU busy while the host enqueues the launches
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            mm.layer_forward(i, x[i], 1, 1, y[i], 1, stream=sp)
+            for mm in models:
+                mm.layer_forward(i, x[i], 1, 1, y[i], 1, stream=sp)
             e1.record(stream)
-            ts.append((e0, e1))
-        torch.cuda.synchronize(dev)
-        ms = float(np.median([a.elapsed_time(b) for a, b in ts]))
+            torch.cuda.synchronize(dev)
+            samples.append(e0.elapsed_time(e1) / len(models))
+        ms = float(np.median(samples))
         algo = st[i]["algo_bytes_fixed"] + 4 * s.cols + 4 * s.rows
         per_layer[s.name] = {"us": ms * 1e3, "algo_bytes": algo, "gbs": algo / (ms / 1e3) / 1e9,
                              "frac": algo / (ms / 1e3) / 1e9 / pk["hbm_gbs"],
                              "index_bytes": st[i]["index_bytes"], "lanes_per_row": st[i]["lanes_per_row"]}
     for mm in models:
         mm.close()
-    return {"replicas": R, "note": "median per-launch CUDA-event time, each replica's streams cold in L2",
+    return {"replicas": R, "note": "back-to-back launches over R replicas after an L2 flush (GPU kept busy while the host enqueues); time per launch",
             "layers": per_layer}
 
 

@@ -75,7 +75,7 @@ struct Layer {
   cdn_layer_desc desc{};
   uint32_t rows = 0, cols = 0, row0 = 0, row1 = 0, k = 0, r = 0;
   FcDev dev;
-  DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias;
+  DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias, flut, ctr;
   cdn_layer_stats stats{};
 };
 
@@ -124,6 +124,37 @@ std::vector<uint32_t> build_lut(const HuffCode& h, int Lb) {
     const uint32_t code = h.code_of[h.syms[i]];
     const uint32_t lo = code << (Lb - L), cnt = 1u << (Lb - L);
     for (uint32_t q = 0; q < cnt; ++q) lut[lo + q] = ((uint32_t)L << 16) | h.syms[i];
+  }
+  return lut;
+}
+
+// Pad-folding val LUT (kernels.cuh FcDev::flut): for every Lb-bit window, the
+// number of leading padding codes (symbol 0, C-04) and the real code that
+// follows when it lies entirely inside the window.
+std::vector<uint32_t> build_fold_lut(const HuffCode& h, int Lb, int pad_gap_len) {
+  std::vector<uint32_t> lut((size_t)1 << Lb, kFoldSlow);
+  const bool has_pad = h.n > 0 && h.len_of.size() > 0 && h.len_of[0] > 0;
+  for (uint32_t w = 0; w < (1u << Lb); ++w) {
+    const uint32_t win = w << (32 - Lb);
+    int pos = 0, pads = 0;
+    bool has = false;
+    uint32_t sym = 0;
+    while (pos < Lb) {
+      uint32_t s, l;
+      if (!h.decode(win << pos, s, l) || (int)l > Lb - pos) break;
+      if (has_pad && s == 0) {
+        ++pads;
+        pos += (int)l;
+        continue;
+      }
+      has = true;
+      sym = s;
+      pos += (int)l;
+      break;
+    }
+    if (pads == 0 && !has) continue;  // slow path: a code longer than the window
+    // real symbols are never 0 (C-04), so sym == 0 marks a pads-only window
+    lut[w] = sym | ((uint32_t)(pads * pad_gap_len) << 8) | ((uint32_t)pads << 24) | ((uint32_t)pos << 28);
   }
   return lut;
 }
@@ -184,6 +215,12 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   const int Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
   L.vlut.upload(build_lut(H.val, Lv));
   L.glut.upload(build_lut(H.gap, Lg));
+  const int Lf = kFoldLutBits;
+  const uint32_t padg = (1u << H.k) - 1;
+  const int pad_glen = padg < H.gap.len_of.size() ? H.gap.len_of[padg] : 0;
+  L.flut.upload(build_fold_lut(H.val, Lf, pad_glen));
+  L.ctr.alloc(sizeof(int) * kMaxBatchTiles);
+  CUDA_OK(cudaMemset(L.ctr.p, 0, sizeof(int) * kMaxBatchTiles));
   L.vtab.upload(build_tab(H.val));
   L.gtab.upload(build_tab(H.gap));
   std::vector<uint16_t> vs = H.val.sorted, gs = H.gap.sorted;
@@ -225,6 +262,10 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.nvs = H.val.n;
   f.ngs = H.gap.n;
   f.rec64 = ix.rec64 ? 1 : 0;
+  f.flut = L.flut.as<uint32_t>();
+  f.ctr = L.ctr.as<int>();
+  f.Lf = Lf;
+  f.Lpg = pad_glen;
 
   cdn_layer_stats& s = L.stats;
   s.rows = H.rows;

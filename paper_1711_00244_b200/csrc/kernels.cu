@@ -149,61 +149,175 @@ __device__ __forceinline__ LaneStart lane_start(const FcDev& L, int row, bool ac
   return st;
 }
 
+// Canonical slow path for a code longer than the LUT width (rare: < 0.5% of
+// val tokens on the configs).  Returns (len << 16) | sym by value so the fast
+// path keeps everything in registers.
+__device__ __noinline__ uint32_t slow_sym(uint32_t w, int from, const uint32_t* tab, const uint16_t* sorted,
+                                          int maxlen) {
+  for (int l = from; l <= maxlen; ++l) {
+    const uint32_t c = (l == 32) ? w : (w >> (32 - l));
+    const uint32_t off = c - tab[l];
+    if (off < tab[33 + l]) return ((uint32_t)l << 16) | sorted[tab[66 + l] + off];
+  }
+  return 32u << 16;
+}
+
+// Word-granular MSB-first reader: the 64 bits (w0:w1) = words[cur], words[cur+1];
+// peek() = the 32 bits starting `off` bits into w0.  skip(n) for any n: advance
+// the word index by (off + n) / 32 and reload the pair when it moved.
+struct WordReader {
+  const uint32_t* base;
+  uint32_t cur, off, w0, w1;
+  __device__ __forceinline__ void init(const uint32_t* words, uint32_t bit) {
+    base = words;
+    cur = bit >> 5;
+    off = bit & 31;
+    w0 = ldg_u32(base + cur);
+    w1 = ldg_u32(base + cur + 1);
+  }
+  __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
+  __device__ __forceinline__ void skip(uint32_t n) {
+    off += n;
+    const uint32_t adv = off >> 5;
+    off &= 31;
+    if (adv) {
+      cur += adv;
+      w0 = ldg_u32(base + cur);
+      w1 = ldg_u32(base + cur + 1);
+    }
+  }
+};
+
+// Fold-LUT entry layout (built in api.cpp build_fold_lut):
+//   [0:8) real symbol (0: the window held only padding codes)
+//   [8:24) gap-stream bits taken by the folded pads = pads * len(code(2^k-1))
+//   [24:28) number of folded pads    [28:32) val bits consumed (<= 15)
+// kFoldSlow: a code longer than the window starts here (canonical slow path).
+
+// Next real nonzero of this lane: returns its symbol (0 at lane end) and
+// updates col.  Pads advance the column by 2^k each and never multiply.
+__device__ __forceinline__ uint32_t next_nonzero(WordReader& vr, WordReader& gr, uint32_t& vrem, int& col,
+                                                 const uint32_t* s_flut, const uint32_t* s_glut,
+                                                 const uint32_t* s_vtab, const uint16_t* s_vsorted,
+                                                 const uint32_t* s_gtab, const uint16_t* s_gsorted,
+                                                 const FcDev& L, int fsh, int gsh) {
+  while (vrem) {
+    const uint32_t w = vr.peek();
+    const uint32_t e = s_flut[w >> fsh];
+    uint32_t len, sym;
+    if (e != kFoldSlow) {
+      len = e >> 28;
+      sym = e & 0xFFu;
+    } else {
+      const uint32_t r = slow_sym(w, L.Lf + 1, s_vtab, s_vsorted, L.vmax);
+      len = r >> 16;
+      sym = r & 0xFFu;
+    }
+    if (len > vrem) { vrem = 0; break; }   // only padding left in this lane
+    vrem -= len;
+    vr.skip(len);
+    if (e != kFoldSlow) {
+      col += (int)(((e >> 24) & 15u) << L.k);
+      gr.skip((e >> 8) & 0xFFFFu);
+    }
+    if (!sym) continue;
+    const uint32_t gwin = gr.peek();
+    uint32_t ge = s_glut[gwin >> gsh];
+    if (ge == 0) ge = slow_sym(gwin, L.Lg + 1, s_gtab, s_gsorted, L.gmax);
+    gr.skip(ge >> 16);
+    col += (int)(ge & 0xFFFFu) + 1;
+    return sym;
+  }
+  return 0;
+}
+
+// Fused FC forward, small batch (BS images per blockIdx.y tile).
+// Warps take work units (32 lanes = 32/G rows) from an atomic counter, so the
+// row blocks are balanced across SMs dynamically.  The val LUT folds a run of
+// padding codes together with the real code that follows (pads: val 0, gap
+// 2^k-1, advance 2^k columns, no multiply, C-02/C-06): one lookup
+// per real nonzero on the val stream.  Nonzeros are decoded four at a time and
+// their activation gathers issued together, so the load latency is exposed
+// once per four multiplies.
 template <int BS, bool REC64, bool VEC>
-__global__ void __launch_bounds__(256, 4) k_fc_forward(FcDev L, const float* __restrict__ x, int ldx,
+__global__ void __launch_bounds__(512, 2) k_fc_fold(FcDev L, const float* __restrict__ x, int ldx,
                                                     int B, float* __restrict__ y, int ldy, int relu) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const SmemTables t = carve(L, smem);
-  stage_tables(L, t);
+  uint32_t* s_flut = (uint32_t*)smem;
+  uint32_t* s_glut = s_flut + (1 << L.Lf);
+  float* s_cb = (float*)(s_glut + (1 << L.Lg));
+  uint32_t* s_vtab = (uint32_t*)(s_cb + L.ncb);
+  uint32_t* s_gtab = s_vtab + 99;
+  uint16_t* s_vsorted = (uint16_t*)(s_gtab + 99);
+  uint16_t* s_gsorted = s_vsorted + (L.nvs + 1);
+  {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < (1 << L.Lf); i += nt) s_flut[i] = L.flut[i];
+    for (int i = tid; i < (1 << L.Lg); i += nt) s_glut[i] = L.glut[i];
+    for (int i = tid; i < L.ncb; i += nt) s_cb[i] = L.codebook[i];
+    for (int i = tid; i < 99; i += nt) { s_vtab[i] = L.vtab[i]; s_gtab[i] = L.gtab[i]; }
+    for (int i = tid; i < L.nvs; i += nt) s_vsorted[i] = L.vsorted[i];
+    for (int i = tid; i < L.ngs; i += nt) s_gsorted[i] = L.gsorted[i];
+  }
   __syncthreads();
 
   const int b0 = blockIdx.y * BS;
   const int nb = min(BS, B - b0);
   x += b0;
   y += b0;
-  const int lj = threadIdx.x & (L.G - 1);
-  const int rows_per_cta = blockDim.x >> L.log2G;
-  const uint32_t padg = (1u << L.k) - 1u;
-  (void)padg;
+  const int lane = threadIdx.x & 31;
+  const int lj = lane & (L.G - 1);
+  const int rows_per_warp = 32 >> L.log2G;
+  const int nunits = (L.nrows + rows_per_warp - 1) >> (5 - L.log2G);
+  const int fsh = 32 - L.Lf, gsh = 32 - L.Lg;
+  int* ctr = L.ctr + blockIdx.y;
 
-  for (int rbase = blockIdx.x * rows_per_cta; rbase < L.nrows; rbase += gridDim.x * rows_per_cta) {
-    const int row = rbase + (threadIdx.x >> L.log2G);
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(ctr, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nunits) break;
+    const int row = u * rows_per_warp + (lane >> L.log2G);
     const bool active = row < L.nrows;
     const LaneStart st = lane_start<REC64>(L, row, active, lj);
     float acc[BS];
 #pragma unroll
     for (int b = 0; b < BS; ++b) acc[b] = 0.f;
     if (st.vlen) {
-      BitReader vr, gr;
+      WordReader vr, gr;
       vr.init(L.vw, st.vbit);
       gr.init(L.gw, st.gbit);
-      int rem = (int)st.vlen;
+      uint32_t vrem = st.vlen;
       int col = st.col;
-      while (rem > 0) {
-        uint32_t lv, lg;
-        const uint32_t vs = decode_sym(vr.peek(), t.vlut, L.Lv, t.vtab, t.vsorted, L.vmax, lv);
-        vr.skip(lv);
-        rem -= (int)lv;
-        const uint32_t gs = decode_sym(gr.peek(), t.glut, L.Lg, t.gtab, t.gsorted, L.gmax, lg);
-        gr.skip(lg);
-        col += (int)gs + 1;
-        if (vs != 0) {
-          const float w = t.cb[vs];
-          const float* xp = x + (size_t)col * ldx;
+      while (vrem) {
+        int c[4];
+        uint32_t sy[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          sy[q] = next_nonzero(vr, gr, vrem, col, s_flut, s_glut, s_vtab, s_vsorted, s_gtab, s_gsorted, L, fsh, gsh);
+          c[q] = col;
+        }
+        float xv[4][BS];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* xp = x + (sy[q] ? c[q] : 0) * ldx;
           if (VEC && BS % 4 == 0) {
 #pragma unroll
             for (int b = 0; b < BS; b += 4) {
               const float4 v = __ldg(reinterpret_cast<const float4*>(xp + b));
-              acc[b] = fmaf(w, v.x, acc[b]);
-              acc[b + 1] = fmaf(w, v.y, acc[b + 1]);
-              acc[b + 2] = fmaf(w, v.z, acc[b + 2]);
-              acc[b + 3] = fmaf(w, v.w, acc[b + 3]);
+              xv[q][b] = v.x; xv[q][b + 1] = v.y; xv[q][b + 2] = v.z; xv[q][b + 3] = v.w;
             }
           } else {
 #pragma unroll
-            for (int b = 0; b < BS; ++b)
-              if (b < nb) acc[b] = fmaf(w, __ldg(xp + b), acc[b]);
+            for (int b = 0; b < BS; ++b) xv[q][b] = (b < nb) ? __ldg(xp + b) : 0.f;
           }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float wv = s_cb[sy[q]];
+#pragma unroll
+          for (int b = 0; b < BS; ++b)
+            if (sy[q]) acc[b] = fmaf(wv, xv[q][b], acc[b]);
         }
       }
     }
@@ -298,15 +412,26 @@ int occupancy_grid(K kernel, int threads, size_t smem, int num_sms, int work_cta
   return work_ctas < g ? (work_ctas > 0 ? work_ctas : 1) : g;
 }
 
+size_t fold_smem_bytes(const FcDev& L) {
+  size_t b = (sizeof(uint32_t) << L.Lf) + (sizeof(uint32_t) << L.Lg) + sizeof(float) * L.ncb +
+             2 * 99 * sizeof(uint32_t) + sizeof(uint16_t) * (L.nvs + 1) + sizeof(uint16_t) * (L.ngs + 1);
+  return (b + 15) & ~(size_t)15;
+}
+
 template <int BS, bool REC64, bool VEC>
 cudaError_t launch_fc_t(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu,
                         cudaStream_t s, int num_sms) {
-  const int threads = 256;
-  const size_t smem = fc_smem_bytes(L);
-  auto kern = k_fc_forward<BS, REC64, VEC>;
-  const int rows_per_cta = threads / L.G;
-  const int work = (L.nrows + rows_per_cta - 1) / rows_per_cta;
-  dim3 grid(occupancy_grid(kern, threads, smem, num_sms, work), (B + BS - 1) / BS);
+  const int threads = 512;
+  const size_t smem = fold_smem_bytes(L);
+  auto kern = k_fc_fold<BS, REC64, VEC>;
+  const int tiles = (B + BS - 1) / BS;
+  if (tiles > kMaxBatchTiles) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(L.ctr, 0, sizeof(int) * tiles, s);
+  if (e != cudaSuccess) return e;
+  const int rows_per_warp = 32 / L.G;
+  const int units = (L.nrows + rows_per_warp - 1) / rows_per_warp;
+  const int work = (units + threads / 32 - 1) / (threads / 32);
+  dim3 grid(occupancy_grid(kern, threads, smem, num_sms, work), tiles);
   kern<<<grid, threads, smem, s>>>(L, x, ldx, B, y, ldy, relu);
   return cudaGetLastError();
 }

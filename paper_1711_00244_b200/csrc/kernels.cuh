@@ -6,7 +6,10 @@
 
 namespace cdn {
 
-constexpr int kLutMaxBits = 10;   // primary LUT width cap; longer codes take the canonical slow path
+constexpr int kLutMaxBits = 10;   // plain LUT width cap (decode kernel); longer codes take the canonical slow path
+constexpr int kFoldLutBits = 11;  // pad-folding val LUT width (fused forward)
+constexpr uint32_t kFoldSlow = 0xFFFFFFFFu;
+constexpr int kMaxBatchTiles = 1024;
 
 struct FcDev {
   const uint32_t* vw = nullptr;      // val stream as big-endian u32 words (bit i = bit 31-(i%32) of word i/32)
@@ -20,6 +23,8 @@ struct FcDev {
   const uint32_t* gtab = nullptr;
   const uint16_t* vsorted = nullptr; // symbols in canonical order
   const uint16_t* gsorted = nullptr;
+  const uint32_t* flut = nullptr;    // 2^Lf pad-folding entries: sym | len<<8 | pads<<13 | has<<18, or kFoldSlow
+  int* ctr = nullptr;                // kMaxBatchTiles work counters (dynamic row scheduling)
   const float* codebook = nullptr;   // 2^r fp32 centres, [0] = 0.0 (pads)
   const float* bias = nullptr;       // nrows fp32 (zeros if absent)
   int nrows = 0, cols = 0;
@@ -27,6 +32,7 @@ struct FcDev {
   int k = 4, Lv = 1, Lg = 1, vmax = 0, gmax = 0;
   int ncb = 32, nvs = 0, ngs = 0;
   int rec64 = 0;
+  int Lf = 1, Lpg = 0;               // folding LUT width; code length of the pad gap symbol 2^k-1
 };
 
 // y[r][b] = act( sum_j W_q[r][j] x[j][b] + v[r] ) for the rank's rows, B images,

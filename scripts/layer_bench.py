@@ -23,7 +23,8 @@ def main():
     ap.add_argument("--batches", default="1,8,64,512")
     ap.add_argument("--replicas", type=int, default=8)
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--single", action="store_true", help="one launch, no timing (ncu target)")
     args = ap.parse_args()
     import torch
     import paper_1711_00244_b200 as cdn
@@ -55,25 +56,25 @@ def main():
                     m.layer_forward(0, x, B, B, y, B, stream=s.cuda_stream)
             torch.cuda.synchronize()
             times = []
-            if not args.no_graph:
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=s):
-                    for m in models:
-                        m.layer_forward(0, x, B, B, y, B, stream=s.cuda_stream)
-                for _ in range(args.reps):
+            if args.single:
+                models[0].layer_forward(0, x, B, B, y, B, stream=s.cuda_stream)
+                torch.cuda.synchronize()
+                continue
+            for _ in range(args.reps):
+                if not args.no_flush:
                     flush.zero_()
-                    torch.cuda.synchronize()
+                torch.cuda.synchronize()
+                with torch.cuda.stream(s):
+                    # keep the GPU busy while the host enqueues, so host launch
+                    # latency never sits between the events
+                    torch.cuda._sleep(3_000_000)
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(s)
-                    g.replay()
-                    e1.record(s)
-                    torch.cuda.synchronize()
-                    times.append(e0.elapsed_time(e1) / len(models))
-            else:
-                for _ in range(args.reps):
                     for m in models:
                         m.layer_forward(0, x, B, B, y, B, stream=s.cuda_stream)
+                    e1.record(s)
                 torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1) / len(models))
             if not times:
                 continue
             ms = float(np.median(times))
