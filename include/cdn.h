@@ -153,6 +153,14 @@ cdn_status cdn_model_infer(cdn_model* m, const float* input, int K, float* score
 cdn_status cdn_layer_forward(cdn_model* m, int layer, const float* x, int ldx, int B, float* y,
                              int ldy, void* stream);
 
+/* ---- FC kernel policy (tuning / parity hook) ---------------------------
+ * band_min_batch: batches B >= this run the warp-specialised large-batch band
+ * kernel (when x meets its alignment rule: ldx % 4 == 0, ldx >= B rounded up
+ * to 4, x 16-byte aligned), smaller ones the lane-parallel small-batch kernel.
+ * <= 0 restores the default (env CDN_BAND_MIN_B, else 16).  Both kernels
+ * compute the same layer; only the summation order differs.  Errors: CDN_E_ARG. */
+cdn_status cdn_model_set_kernel_policy(cdn_model* m, int band_min_batch);
+
 /* ---- decode only (parity hook, kernel K2) -------------------------------
  * Writes every token of this rank's rows in row-major token order, pads
  * included: row, abs column (Alg. 1 l.7), val symbol, codebook value (l.8).

@@ -69,6 +69,7 @@ _SIGS = {
                                       C.c_void_p]),
     "cdn_layer_decode": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.POINTER(C.c_uint64), C.c_void_p]),
+    "cdn_model_set_kernel_policy": (C.c_int32, [C.c_void_p, C.c_int]),
     "cdn_model_num_layers": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int)]),
     "cdn_layer_stats_get": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(LayerStats)]),
     "cdn_model_profile": (C.c_int32, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
@@ -214,6 +215,10 @@ class Model:
 
     def layer_forward(self, layer: int, x, ldx: int, B: int, y, ldy: int, stream: int = 0):
         _check(self._lib.cdn_layer_forward(self._h, layer, _ptr(x), ldx, B, _ptr(y), ldy, stream or None))
+
+    def set_kernel_policy(self, band_min_batch: int = 0):
+        """B >= band_min_batch -> large-batch band kernel (0: library default)."""
+        _check(self._lib.cdn_model_set_kernel_policy(self._h, int(band_min_batch)))
 
     def decode_count(self, layer: int) -> int:
         n = C.c_uint64()

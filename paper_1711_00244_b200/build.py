@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcdn.so")
-SOURCES = ["host.cpp", "kernels.cu", "api.cpp"]
+SOURCES = ["host.cpp", "kernels.cu", "band.cu", "api.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-I", os.path.join(ROOT, "include"), "-I", inc,
            "-o", LIB + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES],
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib, "-lcuda"]
+           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib,]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -76,6 +76,8 @@ struct Layer {
   uint32_t rows = 0, cols = 0, row0 = 0, row1 = 0, k = 0, r = 0;
   FcDev dev;
   DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias, flut, ctr;
+  DBuf ivg, ivm;        // band-kernel interval restart index
+  DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
   cdn_layer_stats stats{};
 };
 
@@ -94,6 +96,7 @@ struct Model {
   std::vector<DBuf> lvl;        // per-level input buffers [K_i][B_i]
   DBuf out, stage_in, loc, gath, host_stage;
   bool busy = false;
+  int band_min = 0;             // cdn_model_set_kernel_policy (0: default)
 };
 
 uint32_t rows_per_rank(uint32_t rows, int world) { return (rows + world - 1) / world; }
@@ -101,7 +104,7 @@ uint32_t rows_per_rank(uint32_t rows, int world) { return (rows + world - 1) / w
 // Upload one stream slice [b0, b1) bits as big-endian words starting at word b0/32.
 void upload_words(DBuf& d, const std::vector<uint8_t>& bytes, uint64_t b0, uint64_t b1, uint64_t* base_bit) {
   const uint64_t w0 = b0 >> 5;
-  const uint64_t nw = ((b1 + 31) >> 5) - w0 + 4;
+  const uint64_t nw = ((((b1 + 31) >> 5) - w0 + 24) + 3) & ~3ull;  // >= 20 words of read-ahead padding
   std::vector<uint32_t> words(nw, 0);
   const uint64_t nbytes = bytes.size();
   for (uint64_t w = 0; w < nw; ++w) {
@@ -211,6 +214,40 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   L.rp.upload(rp);
   if (ix.rec64) L.rec.upload(ix.rec64v); else L.rec.upload(ix.rec32);
   L.tok.upload(ix.tok_start);
+  {
+    // Interval restart index of the large-batch band kernel (host.hpp
+    // IntervalIndex): interval width from the density (about 3 nonzeros per
+    // interval), chunk = the most intervals whose per-row nonzeros always fit
+    // the kernel's list capacity.
+    const double dens = nr ? (double)ix.nnz / ((double)nr * H.cols) : 1.0;
+    uint32_t Wi = 16;
+    while (Wi < 64 && (double)(2 * Wi) * dens <= 3.0) Wi <<= 1;
+    IntervalIndex iv;
+    build_interval_index(H, L.row0, L.row1, Wi, iv);
+    std::vector<uint32_t> ivg(2 * iv.v.size());
+    std::vector<uint16_t> ivm(iv.v.size());
+    for (size_t q = 0; q < iv.v.size(); ++q) {
+      ivg[2 * q] = (uint32_t)(iv.v[q] - vbase);
+      ivg[2 * q + 1] = (uint32_t)(iv.g[q] - gbase);
+      ivm[q] = (uint16_t)(iv.dm1[q] | ((uint16_t)iv.nnz[q] << 8));
+    }
+    int cint = band_max_chunk();
+    for (; cint > 1; cint >>= 1) {
+      uint32_t mx = 0;
+      for (uint32_t r = 0; r < nr && mx <= (uint32_t)band_list_capacity(); ++r)
+        for (uint32_t c0 = 0; c0 < iv.NI; c0 += cint) {
+          uint32_t sum = 0;
+          for (uint32_t i = c0; i < std::min<uint32_t>(iv.NI, c0 + cint); ++i) sum += iv.nnz[(size_t)r * iv.NI + i];
+          mx = std::max(mx, sum);
+        }
+      if (mx <= (uint32_t)band_list_capacity()) break;
+    }
+    L.ivg.upload(ivg);
+    L.ivm.upload(ivm);
+    L.dev.Wi = (int)Wi;
+    L.dev.NI = (int)iv.NI;
+    L.dev.Cint = cint;
+  }
   const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
   const int Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
   L.vlut.upload(build_lut(H.val, Lv));
@@ -266,6 +303,8 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.ctr = L.ctr.as<int>();
   f.Lf = Lf;
   f.Lpg = pad_glen;
+  f.ivg = L.ivg.as<uint2>();
+  f.ivm = L.ivm.as<uint16_t>();
 
   cdn_layer_stats& s = L.stats;
   s.rows = H.rows;
@@ -293,12 +332,39 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
 
 cudaStream_t pick(Model& m, void* s) { return s ? (cudaStream_t)s : m.stream; }
 
+int band_min_batch() {
+  static int v = [] {
+    const char* e = std::getenv("CDN_BAND_MIN_B");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
+  return v;
+}
+
+// One fused FC layer launch: the warp-specialised band kernel for large
+// batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
+void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s) {
+  const int relu = L.desc.relu;
+  if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
+    BandPlan p = plan_fc_band(L.dev, x, ldx, B, m.num_sms);
+    if (p.ok) {
+      if (p.ws_floats) L.bws.alloc(p.ws_floats * sizeof(float));
+      const size_t need = sizeof(int) * (size_t)p.tiles;
+      if (L.bctr.n < need || !L.bctr.p) {
+        L.bctr.alloc(need);
+        CUDA_OK(cudaMemsetAsync(L.bctr.p, 0, need, s));
+      }
+      CUDA_OK(launch_fc_band(L.dev, p, x, ldx, B, y, ldy, relu, L.bws.as<float>(), L.bctr.as<int>(), s));
+      return;
+    }
+  }
+  CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, y, ldy, relu, s, m.num_sms));
+}
+
 // One layer step: local rows -> (all-gather if world > 1) -> dst [rows][ld_dst].
 void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, int ld_dst, cudaStream_t s) {
   Layer& L = *m.layers[li];
-  const int relu = L.desc.relu;
   if (m.world == 1) {
-    CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, dst, ld_dst, relu, s, m.num_sms));
+    fc_forward(m, L, x, ldx, B, dst, ld_dst, s);
     return;
   }
   const uint32_t rb = rows_per_rank(L.rows, m.world);
@@ -306,7 +372,7 @@ void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, in
   m.loc.alloc(slab * sizeof(float));
   m.gath.alloc(slab * m.world * sizeof(float));
   CUDA_OK(cudaMemsetAsync(m.loc.p, 0, slab * sizeof(float), s));
-  CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, m.loc.as<float>(), B, relu, s, m.num_sms));
+  fc_forward(m, L, x, ldx, B, m.loc.as<float>(), B, s);
   NCCL_OK(ncclAllGather(m.loc.p, m.gath.p, slab, ncclFloat, m.comm, s));
   CUDA_OK(cudaMemcpy2DAsync(dst, (size_t)ld_dst * sizeof(float), m.gath.p, (size_t)B * sizeof(float),
                             (size_t)B * sizeof(float), L.rows, cudaMemcpyDeviceToDevice, s));
@@ -595,9 +661,16 @@ cdn_status cdn_layer_forward(cdn_model* h, int layer, const float* x, int ldx, i
   Layer& L = *m.layers[layer];
   if (ldx < B || ldy < B) return fail(CDN_E_ARG, "leading dimension < B");
   cudaStream_t s = pick(m, stream);
-  CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, y, ldy, L.desc.relu, s, m.num_sms));
+  fc_forward(m, L, x, ldx, B, y, ldy, s);
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
   API_END
+}
+
+cdn_status cdn_model_set_kernel_policy(cdn_model* h, int band_min_batch) {
+  if (!h) return fail(CDN_E_ARG, "NULL model");
+  h->m.band_min = band_min_batch > 0 ? band_min_batch : 0;
+  h->m.prof_bmax = 0;  // Time(i,B) depends on the policy
+  return CDN_OK;
 }
 
 cdn_status cdn_layer_decode(cdn_model* h, int layer, int32_t* row, int32_t* col, uint8_t* sym, float* val,

@@ -204,6 +204,9 @@ void build_lane_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, LaneI
   const uint32_t padsym = (1u << L.k) - 1;
   std::vector<uint32_t> vlen((size_t)nr * G), glen((size_t)nr * G), dl((size_t)nr * G);
   out.tok_start.assign((size_t)nr * G + 1, 0);
+  out.start_v.assign((size_t)nr * G, 0);
+  out.start_g.assign((size_t)nr * G, 0);
+  out.start_prev.assign((size_t)nr * G, -1);
   bool need64 = false;
   uint64_t t = 0, nnz = 0;
   std::vector<uint64_t> vs(G + 1), gs(G + 1);
@@ -250,6 +253,9 @@ void build_lane_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, LaneI
     vs[G] = vend; gs[G] = gend;
     for (int j = 0; j < G; ++j) {
       size_t q = (size_t)(i - r0) * G + j;
+      out.start_v[q] = vs[j];
+      out.start_g[q] = gs[j];
+      out.start_prev[q] = (int32_t)pc[j];
       vlen[q] = (uint32_t)(vs[j + 1] - vs[j]);
       glen[q] = (uint32_t)(gs[j + 1] - gs[j]);
       int64_t d = (int64_t)j * W - pc[j];
@@ -274,6 +280,45 @@ void build_lane_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, LaneI
         throw Error(CDN_E_UNSUPPORTED, "lane longer than 2^24 bits");
       out.rec64v[q] = (uint64_t)vlen[q] | ((uint64_t)glen[q] << 24) | ((uint64_t)dl[q] << 48);
     }
+  }
+}
+
+void build_interval_index(const HostLayer& L, uint32_t r0, uint32_t r1, uint32_t W, IntervalIndex& out) {
+  out.W = W;
+  const uint32_t NI = (L.cols + W - 1) / W;
+  out.NI = NI;
+  const size_t n = (size_t)(r1 - r0) * NI;
+  out.v.assign(n, 0);
+  out.g.assign(n, 0);
+  out.dm1.assign(n, 0);
+  out.nnz.assign(n, 0);
+  for (uint32_t i = r0; i < r1; ++i) {
+    const size_t base = (size_t)(i - r0) * NI;
+    uint64_t vpos = L.rp[2ull * i], gpos = L.rp[2ull * i + 1];
+    const uint64_t vend = L.rp[2ull * i + 2];
+    int64_t prev = -1;
+    uint32_t next = 0;  // next interval whose start is not yet recorded
+    auto record = [&](uint32_t upto) {  // intervals [next, upto] start here
+      for (; next <= upto && next < NI; ++next) {
+        out.v[base + next] = vpos;
+        out.g[base + next] = gpos;
+        const int64_t d = (int64_t)next * W - prev;
+        out.dm1[base + next] = (uint8_t)std::min<int64_t>(std::max<int64_t>(d - 1, 0), 255);
+      }
+    };
+    while (vpos < vend) {
+      uint32_t vsym, vl, gsym, gl;
+      if (!L.val.decode(window32(L.vbytes, vpos), vsym, vl) || !L.gap.decode(window32(L.gbytes, gpos), gsym, gl))
+        throw Error(CDN_E_MALFORMED, "row " + std::to_string(i) + ": bad code (interval index)");
+      const int64_t c = prev + (int64_t)gsym + 1;
+      const uint32_t iv = (uint32_t)std::min<int64_t>(c / W, NI - 1);
+      record(iv);
+      if (vsym != 0) out.nnz[base + iv]++;
+      vpos += vl;
+      gpos += gl;
+      prev = c;
+    }
+    record(NI - 1);  // trailing empty intervals start at the row end
   }
 }
 

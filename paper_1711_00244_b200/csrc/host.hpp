@@ -62,6 +62,10 @@ struct LaneIndex {
   std::vector<uint32_t> rec32;
   std::vector<uint64_t> rec64v;
   std::vector<uint64_t> tok_start;  // (rows*G + 1) token index of each lane's first token
+  // Absolute decoder state at every lane start (val bit, gap bit, previous
+  // column): the restart points of the large-batch band kernel's K-splits.
+  std::vector<uint64_t> start_v, start_g;
+  std::vector<int32_t> start_prev;
   uint64_t tokens = 0, nnz = 0;
 };
 
@@ -72,6 +76,19 @@ struct Token { int32_t row, col; uint8_t sym; };
 // fills the lane index.  tokens_out, if non-null, receives every token.
 void build_lane_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, LaneIndex& out,
                       std::vector<Token>* tokens_out = nullptr);
+
+// Restart index of the large-batch band kernel: every row split into NI
+// intervals of W columns; per (row, interval) the decoder state before the
+// first token whose column is >= i*W (bit offsets in both streams, previous
+// column = i*W - (dm1+1)), and the number of real (non-pad) tokens whose
+// column lies in the interval.  Built by the load-time host walk (SURVEY §8(a)
+// a1: chunk start-bit offsets and row boundaries).
+struct IntervalIndex {
+  uint32_t W = 16, NI = 0;
+  std::vector<uint64_t> v, g;     // absolute start bits, rows*NI
+  std::vector<uint8_t> dm1, nnz;  // rows*NI
+};
+void build_interval_index(const HostLayer& L, uint32_t r0, uint32_t r1, uint32_t W, IntervalIndex& out);
 
 int choose_lanes_per_row(const HostLayer& L, uint32_t r0, uint32_t r1, int target_tokens);
 

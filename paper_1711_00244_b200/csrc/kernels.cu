@@ -13,17 +13,15 @@
 //     real tokens (sym != 0) acc[b] += w * x[c][b] (l.9, Eq. 2);
 //   * the G partial sums of a row are reduced with a fixed shuffle tree
 //     (deterministic), then bias + ReLU and one store per (row, image).
+#include "dev_common.cuh"
 #include "kernels.cuh"
 
 namespace cdn {
 
 namespace {
 
-__device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
+using dev::ldg_u32;
+using dev::slow_sym;
 
 // MSB-first bit reader over big-endian packed words.  Invariant: nb > 32 after
 // every skip, so peek() always returns 32 valid bits; the next word is loaded
@@ -149,19 +147,6 @@ __device__ __forceinline__ LaneStart lane_start(const FcDev& L, int row, bool ac
   return st;
 }
 
-// Canonical slow path for a code longer than the LUT width (rare: < 0.5% of
-// val tokens on the configs).  Returns (len << 16) | sym by value so the fast
-// path keeps everything in registers.
-__device__ __noinline__ uint32_t slow_sym(uint32_t w, int from, const uint32_t* tab, const uint16_t* sorted,
-                                          int maxlen) {
-  for (int l = from; l <= maxlen; ++l) {
-    const uint32_t c = (l == 32) ? w : (w >> (32 - l));
-    const uint32_t off = c - tab[l];
-    if (off < tab[33 + l]) return ((uint32_t)l << 16) | sorted[tab[66 + l] + off];
-  }
-  return 32u << 16;
-}
-
 // Word-granular MSB-first reader: the 64 bits (w0:w1) = words[cur], words[cur+1];
 // peek() = the 32 bits starting `off` bits into w0.  skip(n) for any n: advance
 // the word index by (off + n) / 32 and reload the pair when it moved.
@@ -219,6 +204,9 @@ __device__ __forceinline__ uint32_t next_nonzero(WordReader& vr, WordReader& gr,
     if (e != kFoldSlow) {
       col += (int)(((e >> 24) & 15u) << L.k);
       gr.skip((e >> 8) & 0xFFFFu);
+    } else if (!sym) {                     // a pad code longer than the window (C-04, C-06)
+      col += 1 << L.k;
+      gr.skip((uint32_t)L.Lpg);
     }
     if (!sym) continue;
     const uint32_t gwin = gr.peek();

@@ -33,7 +33,28 @@ struct FcDev {
   int ncb = 32, nvs = 0, ngs = 0;
   int rec64 = 0;
   int Lf = 1, Lpg = 0;               // folding LUT width; code length of the pad gap symbol 2^k-1
+  // large-batch band kernel: interval restart index (host.hpp IntervalIndex),
+  // nrows x NI entries: (val bit, gap bit) relative to the slice words, and
+  // (dm1 | nnz << 8): previous column = i*Wi - (dm1+1), real tokens in interval
+  const uint2* ivg = nullptr;
+  const uint16_t* ivm = nullptr;
+  int Wi = 64, NI = 0;               // interval width (= band width), intervals per row
+  int Cint = 16;                     // intervals per decode chunk
 };
+
+// Launch plan of the band kernel for one (layer, B, x) — ok == false means the
+// inputs do not meet its alignment rules (the small-batch kernel then runs).
+struct BandPlan {
+  bool ok = false;
+  int vec = 4, nbt = 1, S = 1, nchunks = 0, units = 0, tiles = 0, grid = 0;
+  size_t ws_floats = 0, smem = 0;
+};
+BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms);
+cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, int ldx, int B, float* y, int ldy,
+                           int relu, float* ws, int* tctr, cudaStream_t s);
+int band_rows_per_unit();
+int band_list_capacity();
+int band_max_chunk();
 
 // y[r][b] = act( sum_j W_q[r][j] x[j][b] + v[r] ) for the rank's rows, B images,
 // feature-major activations (x: [cols][ldx], y: [nrows][ldy]).

@@ -231,7 +231,7 @@ def test_row_shards_concatenate_to_full(torch_dev, world):
     torch, dev = torch_dev
     spec, c, buf = config_layer("C3", 2)   # fc8 1000 rows: ragged last shard at 3 and 8
     _, v = synth.fc_weights(spec, 0)
-    a = synth.fc_inputs(spec.cols, 4, 0)
+    a = synth.fc_inputs(spec.cols, 4, 0)     # B = 4: small-batch kernel, shard-invariant order
     full = gpu_forward(torch, dev, make_model(torch, buf), a, spec.rows)
     parts = []
     for r in range(world):
@@ -273,3 +273,105 @@ def test_infer_c3_stack_matches_oracle_chain(torch_dev):
     m.infer(xi, K, so, on_device=True)
     torch.cuda.synchronize()
     assert rel_err(so.cpu().numpy(), x) <= TOL
+
+
+# ------------------------------------------------- large-batch band kernel (K3b)
+
+def sparse_q(c):
+    """prune∘quantize(W) as a scipy CSR matrix (same values as dense_q)."""
+    import scipy.sparse as sp
+    r, col = np.nonzero(c.mask)
+    vals = c.layer.codebook[c.q[r, col]].astype(np.float32)
+    return sp.csr_matrix((vals, (r, col)), shape=c.mask.shape)
+
+
+def check_forward_sparse(torch, dev, m, c, bias, a, relu):
+    y = gpu_forward(torch, dev, m, a, c.layer.rows)
+    Wq = sparse_q(c)
+    ref = infer.fc_forward(Wq, a, bias, apply_relu=relu)
+    assert np.isfinite(y).all()
+    e = rel_err(y, ref)
+    assert e <= TOL, e
+    scale = infer.fc_abs_scale(Wq, a, bias)
+    kmax = max(1, int(c.row_tokens.max()))
+    elem = (np.abs(y - ref) / np.maximum(scale, 1e-30)).max()
+    assert elem <= 2 * kmax * 2.0 ** -24 + 1e-12, elem
+    return e
+
+
+BAND_CASES = [("C1", 0, B) for B in (16, 32, 48, 100, 200)] + \
+             [("C2", 0, B) for B in (16, 40, 64, 96, 128, 256)] + \
+             [("C5", 0, 128), ("C5", 0, 512), ("C5", 1, 64), ("C5", 1, 512), ("C5", 2, 64), ("C5", 2, 512),
+              ("C3", 2, 160)]
+
+
+@pytest.mark.parametrize("cfg,i,B", BAND_CASES)
+def test_band_forward_configs(torch_dev, cfg, i, B):
+    """Warp-specialised band kernel (every VEC width, K-split reduction S > 1,
+    ragged row blocks: fc8 has 1000 rows, ragged batch tiles) vs the oracle."""
+    torch, dev = torch_dev
+    spec, c, buf = config_layer(cfg, i)
+    m = make_model(torch, buf, relu=spec.relu)
+    m.set_kernel_policy(1)
+    _, v = synth.fc_weights(spec, synth.CONFIGS[cfg].seed)
+    a = synth.fc_inputs(spec.cols, B, synth.CONFIGS[cfg].seed)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=spec.relu)
+
+
+@pytest.mark.parametrize("name,rows,cols,d,r,k,scale", EDGE)
+@pytest.mark.parametrize("B", [1, 5, 36])
+def test_band_edge_fixtures(torch_dev, name, rows, cols, d, r, k, scale, B):
+    """Edge fixtures (all pruned, single nonzero, long pad runs, k=1, one
+    symbol, dense r=8/k=8, 1x5, very wide, very tall) through the band kernel,
+    including batches smaller than one tile."""
+    torch, dev = torch_dev
+    W = synth.random_matrix(rows, cols, seed=zlib.crc32(name.encode()) % 1000, scale=scale)
+    v = synth.random_matrix(1, rows, seed=7).ravel()
+    c, buf = oracle_layer(name, W, d, r, k, v)
+    m = make_model(torch, buf)
+    m.set_kernel_policy(1)
+    a = synth.random_activations(cols, B, seed=B + 100)
+    check_forward(torch, dev, m, c, v, a, relu=False)
+
+
+def test_band_list_overflow_repeats_band(torch_dev):
+    """A few rows carry all the large weights (dense rows in a 5%-dense layer):
+    their per-band lists overflow the 32-entry stage capacity, so the decode
+    warps repeat the band; the result must not change."""
+    torch, dev = torch_dev
+    rows, cols = 300, 4000
+    W = synth.random_matrix(rows, cols, seed=5, scale=0.01)
+    W[::37] *= 1000.0                  # 9 rows hold the largest magnitudes
+    v = synth.random_matrix(1, rows, seed=6).ravel()
+    c, buf = oracle_layer("skewed_rows", W, 0.05, 5, 4, v)
+    assert c.mask[::37].mean() > 0.9    # those rows survive pruning almost whole
+    m = make_model(torch, buf, relu=True)
+    m.set_kernel_policy(1)
+    for B in (8, 64, 128):
+        a = synth.random_activations(cols, B, seed=B)
+        check_forward(torch, dev, m, c, v, a, relu=True)
+
+
+def test_band_and_small_kernels_agree(torch_dev):
+    """The two FC kernels compute the same layer (different summation order)."""
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C2", 0)
+    a = synth.fc_inputs(spec.cols, 24, 0)
+    m1 = make_model(torch, buf)
+    m1.set_kernel_policy(1000)          # small-batch kernel
+    m2 = make_model(torch, buf)
+    m2.set_kernel_policy(1)             # band kernel
+    y1 = gpu_forward(torch, dev, m1, a, spec.rows)
+    y2 = gpu_forward(torch, dev, m2, a, spec.rows)
+    assert rel_err(y2, y1) <= 2e-6
+
+
+def test_band_repeated_launches_are_deterministic(torch_dev):
+    """Split partials are reduced in a fixed order and the arrival counters
+    reset themselves: repeated launches are bit-identical."""
+    torch, dev = torch_dev
+    spec, c, buf = config_layer("C5", 2)
+    m = make_model(torch, buf, relu=False)
+    a = synth.fc_inputs(spec.cols, 512, 0)
+    ys = [gpu_forward(torch, dev, m, a, spec.rows) for _ in range(3)]
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[1], ys[2])
