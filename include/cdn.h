@@ -153,6 +153,26 @@ cdn_status cdn_model_infer(cdn_model* m, const float* input, int K, float* score
 cdn_status cdn_layer_forward(cdn_model* m, int layer, const float* x, int ldx, int B, float* y,
                              int ldy, void* stream);
 
+/* ---- one CONV layer on a device-resident NHWC batch ----
+ * x: device fp32 [B][in_h][in_w][in_c] (NHWC), y: device fp32
+ * [B][out_h][out_w][rows] with out_* from cdn_layer_out_shape.  The layer's
+ * compressed filters are Huffman-decoded to a dense bf16 matrix (RNE of the
+ * codebook value, reading C-21), the input is unfolded to bf16 patches with K
+ * order (r, s, c) per group (C-18), the contraction runs on tcgen05 tensor
+ * cores with fp32 accumulation, then bias, ReLU, LRN (C-20) and max-pool as
+ * the descriptor asks.  Every rank holds all filters
+ * (CONV layers are replicated).  Errors: CDN_E_ARG (not a CONV layer),
+ * CDN_E_CUDA, CDN_E_OOM. */
+cdn_status cdn_conv_forward(cdn_model* m, int layer, const float* x, int B, float* y, void* stream);
+/* Output geometry of a layer per image: CONV -> (out_h, out_w, filters) after
+ * the optional pool; FC -> (1, 1, rows).  Errors: CDN_E_ARG. */
+cdn_status cdn_layer_out_shape(const cdn_model* m, int layer, int* out_h, int* out_w, int* out_c);
+/* Test hook of the tcgen05 GEMM: out[i*ldo + n] = act(sum_k A[i][k] Wt[n][k] + bias[n])
+ * with A [M][Kpad], Wt [N][Kpad] bf16 (device, K contiguous, Kpad % 64 == 0),
+ * bias [N] fp32, out fp32 (device).  Errors: CDN_E_ARG, CDN_E_CUDA. */
+cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int Kpad, const float* bias, int relu,
+                               float* out, int ldo, void* stream);
+
 /* ---- FC kernel policy (tuning / parity hook) ---------------------------
  * band_min_batch: batches B >= this run the warp-specialised large-batch band
  * kernel (when x meets its alignment rule: ldx % 4 == 0, ldx >= B rounded up

@@ -31,6 +31,17 @@ class LayerDesc(C.Structure):
                 ("pool_s", C.c_int32)]
 
     @classmethod
+    def conv(cls, in_c: int, in_h: int, in_w: int, kh: int, kw: int, stride: int, pad: int, groups: int = 1,
+             relu: bool = True, lrn: bool = False, pool_k: int = 0, pool_s: int = 0) -> "LayerDesc":
+        d = cls()
+        d.kind = CDN_LAYER_CONV
+        d.relu = int(bool(relu))
+        d.in_c, d.in_h, d.in_w = in_c, in_h, in_w
+        d.kh, d.kw, d.stride, d.pad, d.groups = kh, kw, stride, pad, groups
+        d.lrn, d.pool_k, d.pool_s = int(bool(lrn)), pool_k, pool_s
+        return d
+
+    @classmethod
     def fc(cls, relu: bool) -> "LayerDesc":
         d = cls()
         d.kind = CDN_LAYER_FC
@@ -70,6 +81,11 @@ _SIGS = {
     "cdn_layer_decode": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.POINTER(C.c_uint64), C.c_void_p]),
     "cdn_model_set_kernel_policy": (C.c_int32, [C.c_void_p, C.c_int]),
+    "cdn_conv_forward": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "cdn_layer_out_shape": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int)]),
+    "cdn_debug_gemm_bf16": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                        C.c_void_p, C.c_int, C.c_void_p]),
     "cdn_model_num_layers": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int)]),
     "cdn_layer_stats_get": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(LayerStats)]),
     "cdn_model_profile": (C.c_int32, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
@@ -154,6 +170,12 @@ def plan_dp(time_ms: np.ndarray, in_bytes: Sequence[int], out_bytes: Sequence[in
     return bs.tolist(), opt.value
 
 
+def debug_gemm_bf16(A, M: int, Wt, N: int, Kpad: int, bias, relu: bool, out, ldo: int, stream: int = 0):
+    """tcgen05 GEMM test hook (device tensors; A/Wt bf16 bit patterns)."""
+    _check(load_library().cdn_debug_gemm_bf16(_ptr(A), int(M), _ptr(Wt), int(N), int(Kpad), _ptr(bias),
+                                              int(bool(relu)), _ptr(out), int(ldo), stream or None))
+
+
 def debug_host_walk(cdni: bytes, layer_in_file: int = 0):
     lib = load_library()
     n = C.c_uint64()
@@ -215,6 +237,15 @@ class Model:
 
     def layer_forward(self, layer: int, x, ldx: int, B: int, y, ldy: int, stream: int = 0):
         _check(self._lib.cdn_layer_forward(self._h, layer, _ptr(x), ldx, B, _ptr(y), ldy, stream or None))
+
+    def conv_forward(self, layer: int, x, B: int, y, stream: int = 0):
+        """NHWC device batch through one CONV layer (decode -> im2col -> tcgen05 GEMM -> ReLU/LRN/pool)."""
+        _check(self._lib.cdn_conv_forward(self._h, layer, _ptr(x), int(B), _ptr(y), stream or None))
+
+    def out_shape(self, layer: int) -> Tuple[int, int, int]:
+        h, w, c = C.c_int(), C.c_int(), C.c_int()
+        _check(self._lib.cdn_layer_out_shape(self._h, layer, C.byref(h), C.byref(w), C.byref(c)))
+        return h.value, w.value, c.value
 
     def set_kernel_policy(self, band_min_batch: int = 0):
         """B >= band_min_batch -> large-batch band kernel (0: library default)."""

@@ -78,7 +78,13 @@ struct Layer {
   DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias, flut, ctr;
   DBuf ivg, ivm;        // band-kernel interval restart index
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
+  DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
+  int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
   cdn_layer_stats stats{};
+  bool is_conv() const { return desc.kind == CDN_LAYER_CONV; }
+  // features per image this layer produces (NHWC flatten for CONV, C-22)
+  uint64_t out_elems() const { return is_conv() ? (uint64_t)out_h * out_w * rows : rows; }
+  uint64_t in_elems() const { return is_conv() ? (uint64_t)desc.in_h * desc.in_w * desc.in_c : cols; }
 };
 
 struct Model {
@@ -95,6 +101,7 @@ struct Model {
   // executor scratch
   std::vector<DBuf> lvl;        // per-level input buffers [K_i][B_i]
   DBuf out, stage_in, loc, gath, host_stage;
+  DBuf conv_a, conv_o, conv_t;  // CONV scratch: bf16 patches, conv output, LRN output
   bool busy = false;
   int band_min = 0;             // cdn_model_set_kernel_policy (0: default)
 };
@@ -175,22 +182,47 @@ std::vector<uint32_t> build_tab(const HuffCode& h) {
 void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer_desc& d, int* out_idx) {
   HostLayer H = parse_cdni_layer(buf, n, idx);
   if (d.kind != CDN_LAYER_FC && d.kind != CDN_LAYER_CONV) throw Error(CDN_E_ARG, "unknown layer kind");
-  if (d.kind == CDN_LAYER_CONV) throw Error(CDN_E_UNSUPPORTED, "CONV layers: use the conv entry points");
+  const bool conv = d.kind == CDN_LAYER_CONV;
+  int conv_h = 0, conv_w = 0, out_h = 0, out_w = 0;
+  if (conv) {
+    if (d.in_c <= 0 || d.in_h <= 0 || d.in_w <= 0 || d.kh <= 0 || d.kw <= 0 || d.stride <= 0 || d.pad < 0 ||
+        d.groups <= 0 || d.in_c % d.groups || H.rows % (uint32_t)d.groups)
+      throw Error(CDN_E_ARG, "bad CONV geometry");
+    if ((uint64_t)d.kh * d.kw * (d.in_c / d.groups) != H.cols)
+      throw Error(CDN_E_SHAPE, "CONV: kh*kw*in_c/groups != matrix columns (C-18)");
+    conv_h = (d.in_h + 2 * d.pad - d.kh) / d.stride + 1;
+    conv_w = (d.in_w + 2 * d.pad - d.kw) / d.stride + 1;
+    if (conv_h <= 0 || conv_w <= 0) throw Error(CDN_E_SHAPE, "CONV output is empty");
+    out_h = conv_h;
+    out_w = conv_w;
+    if (d.pool_k > 0) {
+      if (d.pool_s <= 0 || d.pool_k > conv_h || d.pool_k > conv_w) throw Error(CDN_E_ARG, "bad pool geometry");
+      out_h = (conv_h - d.pool_k) / d.pool_s + 1;
+      out_w = (conv_w - d.pool_k) / d.pool_s + 1;
+    }
+  }
   if (!m.layers.empty()) {
     const Layer& prev = *m.layers.back();
-    if (prev.rows != H.cols)
-      throw Error(CDN_E_SHAPE, "layer input features " + std::to_string(H.cols) + " != previous rows " +
-                                   std::to_string(prev.rows));
+    const uint64_t need = conv ? (uint64_t)d.in_h * d.in_w * d.in_c : H.cols;
+    if (prev.out_elems() != need || (conv && prev.is_conv() && (int)prev.rows != d.in_c))
+      throw Error(CDN_E_SHAPE, "layer input features " + std::to_string(need) + " != previous output " +
+                                   std::to_string(prev.out_elems()));
   }
   auto Lp = std::make_unique<Layer>();
   Layer& L = *Lp;
   L.desc = d;
+  L.conv_h = conv_h;
+  L.conv_w = conv_w;
+  L.out_h = out_h;
+  L.out_w = out_w;
   L.rows = H.rows;
   L.cols = H.cols;
   L.k = H.k;
   L.r = H.r;
-  const uint32_t rb = rows_per_rank(H.rows, m.world);
-  L.row0 = std::min<uint32_t>(H.rows, rb * (uint32_t)m.rank);
+  // FC: row-block shard per rank; CONV: replicas (every rank
+  // holds all filters; the batch is what multi-GPU splits for conv layers).
+  const uint32_t rb = conv ? H.rows : rows_per_rank(H.rows, m.world);
+  L.row0 = conv ? 0 : std::min<uint32_t>(H.rows, rb * (uint32_t)m.rank);
   L.row1 = std::min<uint32_t>(H.rows, L.row0 + rb);
   const uint32_t nr = L.row1 - L.row0;
   int target = 64;
@@ -323,8 +355,13 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
                        3ull * (H.val.n + H.gap.n) + 4ull * nr;
   s.index_bytes = ix.rec64 ? 8ull * ix.rec64v.size() : 4ull * ix.rec32.size();
   s.ws_bytes = 0;
-  s.in_features = H.cols;
-  s.out_features = H.rows;
+  s.in_features = L.in_elems();
+  s.out_features = L.out_elems();
+  if (conv) {
+    L.kpad = (int)((H.cols + 63) / 64 * 64);
+    L.wd.alloc((size_t)H.rows * L.kpad * 2);
+    s.ws_bytes = (uint64_t)H.rows * L.kpad * 2;  // decoded bf16 filters (per-call scratch, C-24)
+  }
   m.layers.push_back(std::move(Lp));
   m.prof_bmax = 0;
   if (out_idx) *out_idx = (int)m.layers.size() - 1;
@@ -358,6 +395,40 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
     }
   }
   CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, y, ldy, relu, s, m.num_sms));
+}
+
+// CONV layer on an NHWC fp32 batch: decode the filters into
+// dense bf16, im2col per group, tcgen05 GEMM (+bias, ReLU), then LRN and
+// max-pool as the descriptor asks.  y: [B][out_h][out_w][rows] NHWC fp32.
+void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStream_t s) {
+  if (B <= 0) return;
+  const cdn_layer_desc& d = L.desc;
+  const int M = (int)L.rows, G = d.groups, cg = d.in_c / G, mg = M / G;
+  const int Ho = L.conv_h, Wo = L.conv_w;
+  const long npos = (long)B * Ho * Wo;
+  __nv_bfloat16* wd = static_cast<__nv_bfloat16*>(L.wd.p);
+  CUDA_OK(cudaMemsetAsync(L.wd.p, 0, L.wd.n, s));
+  CUDA_OK(launch_decode_dense(L.dev, wd, L.kpad, s, m.num_sms));
+  m.conv_a.alloc((size_t)npos * L.kpad * 2);
+  const bool post = d.lrn || d.pool_k > 0;
+  float* cout = y;
+  if (post) {
+    m.conv_o.alloc((size_t)npos * M * sizeof(float));
+    cout = m.conv_o.as<float>();
+  }
+  for (int g = 0; g < G; ++g) {
+    CUDA_OK(launch_im2col(x, B, d.in_h, d.in_w, d.in_c, d.kh, d.kw, d.stride, d.pad, g * cg, cg, Ho, Wo,
+                          (int)L.cols, L.kpad, static_cast<__nv_bfloat16*>(m.conv_a.p), s, m.num_sms));
+    CUDA_OK(launch_gemm_bf16(static_cast<__nv_bfloat16*>(m.conv_a.p), (int)npos, wd + (size_t)g * mg * L.kpad, mg,
+                             L.kpad, L.bias.as<float>() + g * mg, d.relu, cout, M, g * mg, s));
+  }
+  const float* cur = cout;
+  if (d.lrn) {
+    float* dst = d.pool_k > 0 ? (m.conv_t.alloc((size_t)npos * M * sizeof(float)), m.conv_t.as<float>()) : y;
+    CUDA_OK(launch_lrn(cur, npos, M, dst, s, m.num_sms));
+    cur = dst;
+  }
+  if (d.pool_k > 0) CUDA_OK(launch_maxpool(cur, B, Ho, Wo, M, d.pool_k, d.pool_s, y, s, m.num_sms));
 }
 
 // One layer step: local rows -> (all-gather if world > 1) -> dst [rows][ld_dst].
@@ -659,9 +730,45 @@ cdn_status cdn_layer_forward(cdn_model* h, int layer, const float* x, int ldx, i
     return fail(CDN_E_ARG, "bad arguments");
   Model& m = h->m;
   Layer& L = *m.layers[layer];
+  if (L.is_conv()) return fail(CDN_E_ARG, "CONV layer: use cdn_conv_forward");
   if (ldx < B || ldy < B) return fail(CDN_E_ARG, "leading dimension < B");
   cudaStream_t s = pick(m, stream);
   fc_forward(m, L, x, ldx, B, y, ldy, s);
+  if (!stream) CUDA_OK(cudaStreamSynchronize(s));
+  API_END
+}
+
+cdn_status cdn_conv_forward(cdn_model* h, int layer, const float* x, int B, float* y, void* stream) {
+  API_BEGIN
+  if (!h || layer < 0 || layer >= (int)h->m.layers.size() || !x || !y || B < 0) return fail(CDN_E_ARG, "bad arguments");
+  Model& m = h->m;
+  Layer& L = *m.layers[layer];
+  if (!L.is_conv()) return fail(CDN_E_ARG, "layer is not a CONV layer");
+  CUDA_OK(cudaSetDevice(m.device));
+  cudaStream_t s = pick(m, stream);
+  conv_forward(m, L, x, B, y, s);
+  if (!stream) CUDA_OK(cudaStreamSynchronize(s));
+  API_END
+}
+
+cdn_status cdn_layer_out_shape(const cdn_model* h, int layer, int* out_h, int* out_w, int* out_c) {
+  if (!h || layer < 0 || layer >= (int)h->m.layers.size() || !out_h || !out_w || !out_c)
+    return fail(CDN_E_ARG, "bad arguments");
+  const Layer& L = *h->m.layers[layer];
+  *out_h = L.is_conv() ? L.out_h : 1;
+  *out_w = L.is_conv() ? L.out_w : 1;
+  *out_c = (int)L.rows;
+  return CDN_OK;
+}
+
+cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int Kpad, const float* bias, int relu,
+                               float* out, int ldo, void* stream) {
+  API_BEGIN
+  if (!A || !Wt || !bias || !out || M < 0 || N < 0 || Kpad <= 0 || Kpad % 64 || ldo < N)
+    return fail(CDN_E_ARG, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_OK(launch_gemm_bf16(static_cast<const __nv_bfloat16*>(A), M, static_cast<const __nv_bfloat16*>(Wt), N, Kpad,
+                           bias, relu, out, ldo, 0, s));
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
   API_END
 }

@@ -28,6 +28,7 @@
 
 #include "dev_common.cuh"
 #include "kernels.cuh"
+#include "tmap.hpp"
 
 namespace cdn {
 
@@ -42,8 +43,8 @@ constexpr int kThreads = kWorkers + 32;          // + 1 producer warp
 constexpr int kRowsPerWarp = kR / kWorkWarps;    // 8
 constexpr int kLC = 64;                          // list entries per row per chunk
 constexpr int kMaxCint = 32;
-constexpr int kStages = 3;
-constexpr int kXStageBytes = 32 * 1024;
+constexpr int kStages = 2;
+constexpr int kXStageBytes = 64 * 1024;
 constexpr int kWorkBar = 1;                      // named barrier of the 16 worker warps
 
 struct BandArgs {
@@ -54,11 +55,17 @@ struct BandArgs {
   float* ws;   // [tiles][S][kR][BT] split partials (S > 1)
   int* tctr;   // [tiles] arrival counters, zero between launches
   int S, nbt, units, nch;
+  int ipb;     // intervals per band (one band = one X stage)
 };
 
 template <int VEC>
 __device__ __forceinline__ void load_x(const unsigned char* p, float (&v)[VEC]) {
-  if constexpr (VEC == 4) {
+  if constexpr (VEC == 8) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    const float4 u = *reinterpret_cast<const float4*>(p + 512);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    v[4] = u.x; v[5] = u.y; v[6] = u.z; v[7] = u.w;
+  } else if constexpr (VEC == 4) {
     const float4 t = *reinterpret_cast<const float4*>(p);
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   } else if constexpr (VEC == 2) {
@@ -121,6 +128,22 @@ struct TReader {
   }
 };
 
+// Batch column of accumulator v of a lane: lanes cover 16-byte quads so every
+// LDS.128 of x is one contiguous 512-byte warp access (VEC 8 = two of them).
+template <int VEC>
+__device__ __forceinline__ int bcol(int lane, int v) {
+  if constexpr (VEC == 8) return (v >> 2) * 128 + lane * 4 + (v & 3);
+  else return lane * VEC + v;
+}
+
+struct Task {
+  int rl, j;
+  size_t q;
+  uint32_t m, off;
+  uint2 st;
+  TReader vr, gr;
+};
+
 template <int VEC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_fc_band(FcDev L, BandArgs a, const __grid_constant__ CUtensorMap tmx) {
@@ -158,7 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t xstage_bytes = (uint32_t)L.Wi * BT * 4;
+  const int ipb = a.ipb;
+  const uint32_t xstage_bytes = (uint32_t)(L.Wi * ipb) * BT * 4;
 
   if (warp == kWorkWarps) {
     // ---------------------------------------------------------------- producer
@@ -166,11 +190,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t g = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         const UnitCoord c = unit_coord(L, a, u);
-        for (int i = c.i0; i < c.i1; ++i, ++g) {
-          const int s = g % kStages;
-          mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], xstage_bytes);
-          tma_load_2d(xs + s * kXStageBytes, &tmx, c.bt * BT, i * L.Wi, &full[s]);
+        for (int ib = c.i0; ib < c.i1; ib += L.Cint) {
+          const int ni = min(L.Cint, c.i1 - ib);
+          for (int b0 = 0; b0 < ni; b0 += ipb, ++g) {
+            const int s = g % kStages;
+            mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[s], xstage_bytes);
+            tma_load_2d(xs + s * kXStageBytes, &tmx, c.bt * BT, (ib + b0) * L.Wi, &full[s]);
+          }
         }
       }
     }
@@ -188,37 +215,54 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int rr = 0; rr < kRowsPerWarp; ++rr)
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[rr][v] = 0.f;
-  const unsigned char* xl = xs + lane * VEC * 4;
+  const unsigned char* xl = xs + lane * (VEC == 8 ? 16 : VEC * 4);
   uint32_t g = 0;
 
   for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
     const UnitCoord uc = unit_coord(L, a, u);
     for (int ib = uc.i0; ib < uc.i1; ib += Cint) {
       const int ni = min(Cint, uc.i1 - ib);
-      // ---- decode phase: one lane per (row, interval) of the chunk
-      for (int pass = 0; pass < npass; ++pass) {
-        const int t = pass * kWorkers + tid;
-        const int rl = t / Cint, j = t % Cint;
-        const int row = uc.rb * kR + rl;
-        const bool valid = rl < kR && row < L.nrows && j < ni;
-        const size_t q = (size_t)row * L.NI + ib + j;
-        const uint32_t m = valid ? (uint32_t)L.ivm[q] : 0u;
-        const uint32_t nnz = m >> 8;
-        uint32_t off = nnz;  // inclusive scan over the Cint lanes of this row
-        for (int o = 1; o < Cint; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, off, o, Cint);
-          if (j >= o) off += y;
+      // ---- decode phase: one lane per (row, interval) of the chunk; two
+      // passes' index and stream loads are issued together (one round trip)
+      for (int pass = 0; pass < npass; pass += 2) {
+        Task tk[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int t = (pass + h) * kWorkers + tid;
+          tk[h].rl = t / Cint;
+          tk[h].j = t % Cint;
+          const int row = uc.rb * kR + tk[h].rl;
+          const bool valid = pass + h < npass && tk[h].rl < kR && row < L.nrows && tk[h].j < ni;
+          tk[h].q = (size_t)row * L.NI + ib + tk[h].j;
+          tk[h].m = valid ? (uint32_t)L.ivm[tk[h].q] : 0u;
+          tk[h].st = valid ? L.ivg[tk[h].q] : make_uint2(0, 0);
         }
-        off -= nnz;
-        if (rl < kR) bse[rl * kMaxCint + j] = off | ((off + nnz) << 16);
-        if (nnz) {
-          const uint2 st = L.ivg[q];
-          TReader vr, gr;
-          vr.init(L.vw, st.x);
-          gr.init(L.gw, st.y);
-          const int ibase = (ib + j) * L.Wi;
-          int col = ibase - (int)(m & 0xFFu) - 1;
-          float2* dst = lists + rl * kLC + off;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t nnz = tk[h].m >> 8;
+          uint32_t off = nnz;  // inclusive scan over the Cint lanes of this row
+          for (int o = 1; o < Cint; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, off, o, Cint);
+            if (tk[h].j >= o) off += y;
+          }
+          off -= nnz;
+          tk[h].off = off;
+          if (pass + h < npass && tk[h].rl < kR) bse[tk[h].rl * kMaxCint + tk[h].j] = off | ((off + nnz) << 16);
+          if (nnz) {
+            tk[h].vr.init(L.vw, tk[h].st.x);
+            tk[h].gr.init(L.gw, tk[h].st.y);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t nnz = tk[h].m >> 8;
+          if (!nnz) continue;
+          const int iv = ib + tk[h].j;
+          const int bstart = (ib + (tk[h].j / ipb) * ipb) * L.Wi;  // first column of the band's X stage
+          int col = iv * L.Wi - (int)(tk[h].m & 0xFFu) - 1;
+          float2* dst = lists + tk[h].rl * kLC + tk[h].off;
+          TReader& vr = tk[h].vr;
+          TReader& gr = tk[h].gr;
           uint32_t done = 0;
           while (done < nnz) {
             const uint32_t w = vr.peek();
@@ -249,26 +293,28 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (ge == 0) ge = slow_sym(gwin, L.Lg + 1, s_gtab, s_gsorted, L.gmax);
               gr.skip(ge >> 16);
               col += (int)(ge & 0xFFFFu) + 1;
-              dst[done++] = make_float2(s_cb[sym], __uint_as_float((uint32_t)(col - ibase) * (BT * 4)));
+              dst[done++] = make_float2(s_cb[sym], __uint_as_float((uint32_t)(col - bstart) * (BT * 4)));
             }
           }
         }
       }
       named_bar_sync(kWorkBar, kWorkers);
 
-      // ---- FMA phase: one band (interval) per pipeline stage
-      for (int j = 0; j < ni; ++j, ++g) {
+      // ---- FMA phase: one band (ipb intervals) per pipeline stage
+      for (int j0 = 0; j0 < ni; j0 += ipb, ++g) {
         const int s = g % kStages;
+        const int j1 = min(ni, j0 + ipb) - 1;
         mbar_wait(&full[s], (g / kStages) & 1);
         const unsigned char* xb = xl + s * kXStageBytes;
 #pragma unroll
         for (int rr = 0; rr < kRowsPerWarp; ++rr) {
           const int rl = warp + kWorkWarps * rr;
-          const uint32_t se = bse[rl * kMaxCint + j];
+          const int e0 = (int)(bse[rl * kMaxCint + j0] & 0xFFFFu);
+          const int e1 = (int)(bse[rl * kMaxCint + j1] >> 16);
           const float2* lr = lists + rl * kLC;
           // one broadcast LDS.64 (w, x offset) + one VEC-wide LDS of x per entry
 #pragma unroll 2
-          for (int e = (int)(se & 0xFFFFu); e < (int)(se >> 16); ++e) {
+          for (int e = e0; e < e1; ++e) {
             const float2 p = lr[e];
             float xv[VEC];
             load_x<VEC>(xb + __float_as_uint(p.y), xv);
@@ -293,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float* yp = a.y + (size_t)row * a.ldy + uc.bt * BT;
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
-            const int b = lane * VEC + v;
+            const int b = bcol<VEC>(lane, v);
             float o = acc[rr][v] + bias;
             if (a.relu) o = fmaxf(o, 0.f);
             if (b < nb) yp[b] = o;
@@ -304,9 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* slab = a.ws + ((size_t)uc.tile * a.S + uc.sp) * kR * BT;
 #pragma unroll
       for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-        float* p = slab + (size_t)(warp + kWorkWarps * rr) * BT + lane * VEC;
+        float* p = slab + (size_t)(warp + kWorkWarps * rr) * BT;
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) __stcg(p + v, acc[rr][v]);
+        for (int v = 0; v < VEC; ++v) __stcg(p + bcol<VEC>(lane, v), acc[rr][v]);
       }
       __threadfence();
       named_bar_sync(kWorkBar, kWorkers);
@@ -329,15 +375,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int v = 0; v < VEC; ++v) sum[v] = 0.f;
           for (int jj = 0; jj < a.S; ++jj) {
-            const float* p = base + ((size_t)jj * kR + rl) * BT + lane * VEC;
+            const float* p = base + ((size_t)jj * kR + rl) * BT;
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) sum[v] += __ldcg(p + v);
+            for (int v = 0; v < VEC; ++v) sum[v] += __ldcg(p + bcol<VEC>(lane, v));
           }
           const float bias = L.bias[row];
           float* yp = a.y + (size_t)row * a.ldy + uc.bt * BT;
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
-            const int b = lane * VEC + v;
+            const int b = bcol<VEC>(lane, v);
             float o = sum[v] + bias;
             if (a.relu) o = fmaxf(o, 0.f);
             if (b < nb) yp[b] = o;
@@ -383,11 +429,15 @@ int band_max_chunk() { return kMaxCint; }
 BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms) {
   BandPlan p;
   if (B <= 0 || L.nrows <= 0 || !L.ivg || L.Cint <= 0) return p;
-  const int vec = B > 64 ? 4 : (B > 32 ? 2 : 1);
+  const int vec = B > 128 ? 8 : (B > 64 ? 4 : (B > 32 ? 2 : 1));
   const int BT = 32 * vec;
   if ((ldx & 3) || ldx < B || ((uintptr_t)x & 15)) return p;  // TMA: 16-byte row pitch and base
   if ((size_t)L.Wi * BT * 4 > (size_t)kXStageBytes) return p;
   p.vec = vec;
+  p.ipb = 1;
+  while (p.ipb * 2 <= L.Cint && (size_t)L.Wi * (p.ipb * 2) * BT * 4 <= (size_t)kXStageBytes &&
+         L.Wi * p.ipb * 2 <= 256)
+    p.ipb *= 2;
   p.nbt = (B + BT - 1) / BT;
   p.nchunks = (L.NI + L.Cint - 1) / L.Cint;
   const int tiles = ((L.nrows + kR - 1) / kR) * p.nbt;
@@ -414,49 +464,34 @@ BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sm
 
 cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, int ldx, int B, float* y, int ldy,
                            int relu, float* ws, int* tctr, cudaStream_t s) {
-  BandArgs a{x, ldx, B, y, ldy, relu, ws, tctr, p.S, p.nbt, p.units, p.nchunks};
+  BandArgs a{x, ldx, B, y, ldy, relu, ws, tctr, p.S, p.nbt, p.units, p.nchunks, p.ipb};
   // Tensor map of x viewed as [cols][B] fp32 with row pitch ldx; box [Wi][BT].
   // Encoding is host work: cache the last few (same buffers every step).
   struct Entry { const float* x; int ldx, B, cols, bt, wi; CUtensorMap m; };
+  const int box_rows = L.Wi * p.ipb;
   static thread_local Entry cache[8];
   static thread_local int ncache = 0, next = 0;
   const int BT = 32 * p.vec;
   const CUtensorMap* map = nullptr;
   for (int i = 0; i < ncache; ++i) {
     const Entry& e = cache[i];
-    if (e.x == x && e.ldx == ldx && e.B == B && e.cols == L.cols && e.bt == BT && e.wi == L.Wi) { map = &e.m; break; }
+    if (e.x == x && e.ldx == ldx && e.B == B && e.cols == L.cols && e.bt == BT && e.wi == box_rows) { map = &e.m; break; }
   }
   if (!map) {
     Entry& e = cache[next];
     next = (next + 1) % 8;
     if (ncache < 8) ++ncache;
-    e = Entry{x, ldx, B, L.cols, BT, L.Wi, {}};
-    const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)L.cols};
-    const cuuint64_t strides[1] = {(cuuint64_t)ldx * sizeof(float)};
-    const cuuint32_t box[2] = {(cuuint32_t)BT, (cuuint32_t)L.Wi};
-    const cuuint32_t estr[2] = {1, 1};
-    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static EncodeFn encode = nullptr;
-    if (!encode) {
-      void* fn = nullptr;
-      cudaDriverEntryPointQueryResult q{};
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-          q != cudaDriverEntryPointSuccess || !fn)
-        return cudaErrorNotSupported;
-      encode = reinterpret_cast<EncodeFn>(fn);
-    }
-    CUresult r = encode(&e.m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides,
-                                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
+    e = Entry{x, ldx, B, L.cols, BT, box_rows, {}};
+    if (encode_tmap_2d(&e.m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, (uint64_t)B, (uint64_t)L.cols,
+                       (uint64_t)ldx * sizeof(float), (uint32_t)BT, (uint32_t)box_rows,
+                       CU_TENSOR_MAP_SWIZZLE_NONE) != cudaSuccess) {
       e.x = nullptr;
       return cudaErrorInvalidValue;
     }
     map = &e.m;
   }
   switch (p.vec) {
+    case 8: return launch_band_t<8>(L, p, a, *map, s);
     case 4: return launch_band_t<4>(L, p, a, *map, s);
     case 2: return launch_band_t<2>(L, p, a, *map, s);
     default: return launch_band_t<1>(L, p, a, *map, s);

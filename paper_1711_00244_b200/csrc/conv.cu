@@ -1,0 +1,295 @@
+// CONV path (Eq. 1 for a convolution layer in its
+// im2col form): per call the layer's compressed filter matrix is
+// Huffman-decoded straight into a dense bf16 matrix (kernels.cu
+// k_decode_dense, L2-resident: <= 2.4 MB per AlexNet layer), the NHWC input is
+// unfolded to bf16 patches (K order (r, s, c), channel fastest, reading C-18),
+// and the contraction runs on the 5th-generation tensor cores:
+//
+//   k_gemm_bf16: D[pos][filter] = sum_k A[pos][k] * W[filter][k]
+//     * 128 positions x BN filters per CTA, K in 64-element (128-byte) tiles;
+//     * warp 0 / lane 0: TMA producer (cp.async.bulk.tensor, 128B swizzle)
+//       into a 4-stage smem ring on full/empty mbarriers;
+//     * warp 1 / lane 0: issues tcgen05.mma.cta_group::1.kind::f16 (bf16 x
+//       bf16 -> fp32 accumulator in TMEM), commits to the stage's empty
+//       barrier and, after the last tile, to the accumulator-ready barrier;
+//     * 4 warps: epilogue tcgen05.ld (32x32b) -> + bias -> ReLU -> fp32 NHWC.
+//   k_lrn, k_maxpool: the AlexNet norm / pool layers (C-19, C-20), NHWC fp32.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "dev_common.cuh"
+#include "kernels.cuh"
+#include "tmap.hpp"
+
+namespace cdn {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kGStages = 4;
+constexpr int kGThreads = 128;
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  // K-major, 128-byte swizzle canonical layout: 8-row x 128-byte atoms,
+  // stride between 8-row groups (SBO) 1024 B, LBO unused (1), version 1.
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// out[pos * ldo + col0 + n] = act( sum_k A[pos][k] W[n][k] + bias[n] ),
+// pos in [0, Mrows), n in [0, Nrows).  A: tensor map over [Mrows][Kpad] bf16,
+// W: over [Nrows][Kpad] bf16; nk = Kpad / 64.
+__global__ void __launch_bounds__(kGThreads, 1)
+    k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int Mrows, int Nrows,
+                int nk, int BN, int tmem_cols, const float* __restrict__ bias, float* __restrict__ out, int ldo,
+                int col0, int relu) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int a_bytes = kBM * kBK * 2, b_bytes = BN * kBK * 2;
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + kGStages * a_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kGStages * b_bytes);
+  uint64_t* empty = full + kGStages;
+  uint64_t* done = empty + kGStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % kGStages;
+      mbar_wait(&empty[s], ((kt / kGStages) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], (uint32_t)(a_bytes + b_bytes));
+      tma2d(sA + s * a_bytes, &ta, kt * kBK, m0, &full[s]);
+      tma2d(sB + s * b_bytes, &tb, kt * kBK, n0, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer: 4 x (128 x BN x 16) per 64-wide K tile
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(kBM >> 4) << 24);
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % kGStages;
+      mbar_wait(&full[s], (kt / kGStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t ad = sw128_desc(smem_addr(sA + s * a_bytes));
+      const uint64_t bd = sw128_desc(smem_addr(sB + s * b_bytes));
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k)
+        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kt | k) != 0);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM lane = position row, column = filter
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + warp * 32 + lane;
+  for (int c = 0; c < BN; c += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+    if (row < Mrows) {
+      float* op = out + (size_t)row * ldo + col0 + n0 + c;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = n0 + c + i;
+        if (n < Nrows) {
+          float o = v[i] + bias[n];
+          if (relu) o = fmaxf(o, 0.f);
+          op[i] = o;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+}
+
+// NHWC fp32 -> bf16 (RNE) patches [pos][Kpad] of channels [c0, c0+cg):
+// k = (r*kw + s)*cg + c, zero for padding taps and k >= kh*kw*cg.
+__global__ void k_im2col(const float* __restrict__ x, int B, int H, int W, int C, int kh, int kw, int stride, int pad,
+                         int c0, int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* __restrict__ out) {
+  const int kq = Kpad / 8;
+  const long total = (long)B * Ho * Wo * kq;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const long pos = idx / kq;
+    const int k0 = (int)(idx % kq) * 8;
+    const int b = (int)(pos / (Ho * Wo));
+    const int rem = (int)(pos % (Ho * Wo));
+    const int oh = rem / Wo, ow = rem % Wo;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = k0 + j;
+      float f = 0.f;
+      if (k < Kreal) {
+        const int c = k % cg, rs = k / cg;
+        const int s = rs % kw, r = rs / kw;
+        const int ih = oh * stride - pad + r, iw = ow * stride - pad + s;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) f = x[(((size_t)b * H + ih) * W + iw) * C + c0 + c];
+      }
+      v[j] = __float2bfloat16_rn(f);
+    }
+    *reinterpret_cast<uint4*>(out + pos * Kpad + k0) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+// Cross-channel LRN (reading C-20: n = 5, alpha = 1e-4, beta = 0.75, k = 2,
+// alpha/n scaling, window clipped at the channel ends), NHWC fp32.
+__global__ void k_lrn(const float* __restrict__ x, long npos, int C, float* __restrict__ y) {
+  const long total = npos * C;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const float* px = x + (i - c);
+    float s = 0.f;
+    const int lo = max(0, c - 2), hi = min(C - 1, c + 2);
+    for (int q = lo; q <= hi; ++q) s = fmaf(px[q], px[q], s);
+    y[i] = px[c] * powf(2.0f + (1e-4f / 5.0f) * s, -0.75f);
+  }
+}
+
+// k x k / stride s max-pool, no padding, NHWC fp32.
+__global__ void k_maxpool(const float* __restrict__ x, int B, int H, int W, int C, int k, int s, int Ho, int Wo,
+                          float* __restrict__ y) {
+  const long total = (long)B * Ho * Wo * C;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    long p = i / C;
+    const int ow = (int)(p % Wo);
+    p /= Wo;
+    const int oh = (int)(p % Ho);
+    const int b = (int)(p / Ho);
+    float m = -INFINITY;
+    for (int r = 0; r < k; ++r)
+      for (int q = 0; q < k; ++q)
+        m = fmaxf(m, x[(((size_t)b * H + oh * s + r) * W + ow * s + q) * C + c]);
+    y[i] = m;
+  }
+}
+
+int grid_for(long work, int threads, int num_sms) {
+  const long g = (work + threads - 1) / threads;
+  const long cap = (long)num_sms * 16;
+  return (int)(g < cap ? (g > 0 ? g : 1) : cap);
+}
+
+}  // namespace
+
+int gemm_tile_n(int Nrows) {
+  int tiles = (Nrows + 255) / 256;
+  int bn = (Nrows + tiles - 1) / tiles;
+  return (bn + 15) & ~15;
+}
+
+size_t gemm_smem_bytes(int BN) {
+  return 1024 + (size_t)kGStages * (kBM * kBK * 2 + BN * kBK * 2) + (2 * kGStages + 1) * 8 + 16;
+}
+
+cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
+                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s) {
+  if (Mrows <= 0 || Nrows <= 0) return cudaSuccess;
+  if (Kpad % kBK) return cudaErrorInvalidValue;
+  const int BN = gemm_tile_n(Nrows);
+  int tcols = 32;
+  while (tcols < BN) tcols <<= 1;
+  CUtensorMap ta, tb;
+  cudaError_t e = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, A, (uint64_t)Kpad, (uint64_t)Mrows,
+                                 (uint64_t)Kpad * 2, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  e = encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Wt, (uint64_t)Kpad, (uint64_t)Nrows, (uint64_t)Kpad * 2,
+                     kBK, (uint32_t)BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  const size_t smem = gemm_smem_bytes(BN);
+  static thread_local size_t set_smem = 0;
+  if (smem > set_smem) {
+    e = cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set_smem = smem;
+  }
+  dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN);
+  k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, bias, out, ldo, col0, relu);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, int kw, int stride, int pad, int c0,
+                          int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
+                          int num_sms) {
+  const long work = (long)B * Ho * Wo * (Kpad / 8);
+  k_im2col<<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo, Kreal,
+                                                        Kpad, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms) {
+  k_lrn<<<grid_for(npos * C, 256, num_sms), 256, 0, s>>>(x, npos, C, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
+                           int num_sms) {
+  const int Ho = (H - k) / st + 1, Wo = (W - k) / st + 1;
+  k_maxpool<<<grid_for((long)B * Ho * Wo * C, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y);
+  return cudaGetLastError();
+}
+
+}  // namespace cdn

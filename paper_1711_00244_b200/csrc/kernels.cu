@@ -13,6 +13,8 @@
 //     real tokens (sym != 0) acc[b] += w * x[c][b] (l.9, Eq. 2);
 //   * the G partial sums of a row are reduced with a fixed shuffle tree
 //     (deterministic), then bias + ReLU and one store per (row, image).
+#include <cuda_bf16.h>
+
 #include "dev_common.cuh"
 #include "kernels.cuh"
 
@@ -365,6 +367,40 @@ __global__ void __launch_bounds__(256, 4) k_decode(FcDev L, int row_offset, int3
   }
 }
 
+// Decode straight into a dense bf16 matrix W[row][col] (RNE of the codebook
+// value, reading C-21) for the CONV tensor-core path; pads and pruned entries
+// stay 0 (the caller zero-fills W).
+template <bool REC64>
+__global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16* __restrict__ W, int ldw) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemTables t = carve(L, smem);
+  stage_tables(L, t);
+  __syncthreads();
+  const int lj = threadIdx.x & (L.G - 1);
+  const int rows_per_cta = blockDim.x >> L.log2G;
+  for (int rbase = blockIdx.x * rows_per_cta; rbase < L.nrows; rbase += gridDim.x * rows_per_cta) {
+    const int row = rbase + (threadIdx.x >> L.log2G);
+    const bool active = row < L.nrows;
+    const LaneStart st = lane_start<REC64>(L, row, active, lj);
+    if (!st.vlen) continue;
+    BitReader vr, gr;
+    vr.init(L.vw, st.vbit);
+    gr.init(L.gw, st.gbit);
+    int rem = (int)st.vlen;
+    int col = st.col;
+    while (rem > 0) {
+      uint32_t lv, lg;
+      const uint32_t vs = decode_sym(vr.peek(), t.vlut, L.Lv, t.vtab, t.vsorted, L.vmax, lv);
+      vr.skip(lv);
+      rem -= (int)lv;
+      const uint32_t gs = decode_sym(gr.peek(), t.glut, L.Lg, t.gtab, t.gsorted, L.gmax, lg);
+      gr.skip(lg);
+      col += (int)gs + 1;
+      if (vs) W[(size_t)row * ldw + col] = __float2bfloat16_rn(t.cb[vs]);
+    }
+  }
+}
+
 __global__ void k_transpose(const float* __restrict__ in, int rows, int cols, int ldi,
                             float* __restrict__ out, int ldo) {
   __shared__ float tile[32][33];
@@ -469,6 +505,22 @@ cudaError_t launch_decode(const FcDev& L, int row_offset, int32_t* row, int32_t*
   } else {
     auto k = k_decode<false>;
     k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, row_offset, row, col, sym, val);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms) {
+  if (L.nrows <= 0) return cudaSuccess;
+  const int threads = 256;
+  const size_t smem = fc_smem_bytes(L);
+  const int rows_per_cta = threads / L.G;
+  const int work = (L.nrows + rows_per_cta - 1) / rows_per_cta;
+  if (L.rec64) {
+    auto k = k_decode_dense<true>;
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw);
+  } else {
+    auto k = k_decode_dense<false>;
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw);
   }
   return cudaGetLastError();
 }

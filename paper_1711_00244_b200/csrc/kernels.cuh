@@ -2,6 +2,7 @@
 // and the kernel launchers.  Layout rationale: DESIGN.md "Data layout in HBM".
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace cdn {
@@ -46,7 +47,7 @@ struct FcDev {
 // inputs do not meet its alignment rules (the small-batch kernel then runs).
 struct BandPlan {
   bool ok = false;
-  int vec = 4, nbt = 1, S = 1, nchunks = 0, units = 0, tiles = 0, grid = 0;
+  int vec = 4, nbt = 1, S = 1, nchunks = 0, units = 0, tiles = 0, grid = 0, ipb = 1;
   size_t ws_floats = 0, smem = 0;
 };
 BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms);
@@ -71,5 +72,19 @@ cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float
                              cudaStream_t s);
 
 size_t fc_smem_bytes(const FcDev& L);
+
+// ---- CONV path (conv.cu)
+// Decode the rank's rows into dense bf16 W[row][col] (zero-filled by caller).
+cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms);
+// NHWC fp32 -> bf16 patches [B*Ho*Wo][Kpad] of channels [c0, c0+cg), k = (r*kw+s)*cg + c.
+cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, int kw, int stride, int pad, int c0,
+                          int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
+                          int num_sms);
+// tcgen05 GEMM: out[pos*ldo + col0 + n] = act(sum_k A[pos][k] Wt[n][k] + bias[n]); Kpad % 64 == 0.
+cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
+                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s);
+cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms);
+cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
+                           int num_sms);
 
 }  // namespace cdn

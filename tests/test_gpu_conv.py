@@ -1,0 +1,130 @@
+"""GPU parity of the CONV path: Huffman decode of the filter
+matrix -> dense bf16 -> im2col -> tcgen05 GEMM (fp32 accumulate) -> bias ->
+ReLU -> LRN -> max-pool, against the oracle's bf16-emulating fp64 convolution
+(O9, readings C-18..C-21) on the SAME fp32 input (per-layer isolation, C-21).
+Gate: ||y_gpu - y_ref||_inf / ||y_ref||_inf <= 1e-4 (north_star)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import cdni, compress, infer
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    return torch, torch.device("cuda:0")
+
+
+def bf16_bits(x):
+    """fp32 -> bf16 bit patterns (RNE), via the oracle's rounding."""
+    return (infer.bf16_round(x).view(np.uint32) >> 16).astype(np.uint16)
+
+
+def rel_err(y, ref):
+    return np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-30)
+
+
+@pytest.mark.parametrize("M,N,K,relu", [(128, 96, 64, False), (300, 128, 384, True), (257, 192, 1216, False),
+                                        (640, 384, 2304, True), (77, 40, 128, False), (1, 16, 64, False)])
+def test_tcgen05_gemm_hook(torch_dev, M, N, K, relu):
+    """The tensor-core GEMM alone: bf16 operands, fp32 accumulate, vs fp64."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    rng = np.random.default_rng(M * 7 + N)
+    a = rng.standard_normal((M, K), dtype=np.float32)
+    w = rng.standard_normal((N, K), dtype=np.float32)
+    bias = rng.standard_normal(N, dtype=np.float32)
+    ta = torch.from_numpy(bf16_bits(a).view(np.int16)).to(dev)
+    tw = torch.from_numpy(bf16_bits(w).view(np.int16)).to(dev)
+    tb = torch.from_numpy(bias).to(dev)
+    out = torch.full((M, N), float("nan"), dtype=torch.float32, device=dev)
+    cdn.debug_gemm_bf16(ta, M, tw, N, K, tb, relu, out, N)
+    torch.cuda.synchronize()
+    ref = infer.bf16_round(a).astype(np.float64) @ infer.bf16_round(w).astype(np.float64).T + bias
+    if relu:
+        ref = np.maximum(ref, 0)
+    y = out.cpu().numpy()
+    assert np.isfinite(y).all()
+    assert rel_err(y, ref) <= 1e-5
+    scale = np.abs(infer.bf16_round(a)).astype(np.float64) @ np.abs(infer.bf16_round(w)).astype(np.float64).T
+    assert (np.abs(y - ref) <= 2 * K * 2.0 ** -24 * scale + 1e-6).all()
+
+
+_CACHE = {}
+
+
+def conv_case(i):
+    spec = synth.ALEXNET_CONV[i]
+    if i not in _CACHE:
+        W, v = synth.fc_weights(spec, 0)
+        c = compress.compress_layer(W, spec.density, spec.r, spec.k, v)
+        _CACHE[i] = (spec, c, cdni.serialize([c.layer]), v)
+    return _CACHE[i]
+
+
+IN_HW = [227, 27, 13, 13, 13]
+
+
+def conv_input(i, B):
+    spec = synth.ALEXNET_CONV[i]
+    if i == 0:
+        return synth.conv_inputs(B, 227, 3, seed=0)
+    rng = np.random.default_rng(100 + i)
+    x = rng.standard_normal((B, IN_HW[i], IN_HW[i], spec.in_ch), dtype=np.float32)
+    return np.maximum(x, np.float32(0))
+
+
+def oracle_conv(spec, c, v, x):
+    y = infer.conv_forward(x, c.dense_q(), v, spec.kh, spec.kw, spec.stride, spec.pad, spec.groups,
+                           apply_relu=True, bf16=True)
+    if spec.lrn:
+        y = infer.lrn(y)
+    if spec.pool:
+        y = infer.maxpool(y, 3, 2)
+    return y
+
+
+@pytest.mark.parametrize("i,B", [(0, 2), (1, 2), (2, 3), (3, 2), (4, 2)])
+def test_alexnet_conv_layer_vs_oracle(torch_dev, i, B):
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    spec, c, buf, v = conv_case(i)
+    x = conv_input(i, B)
+    m = cdn.Model(0)
+    m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, IN_HW[i], IN_HW[i], spec.kh, spec.kw, spec.stride, spec.pad,
+                                         spec.groups, relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
+                                         pool_s=2 if spec.pool else 0))
+    oh, ow, oc = m.out_shape(0)
+    xd = torch.from_numpy(x).to(dev)
+    yd = torch.full((B, oh, ow, oc), float("nan"), dtype=torch.float32, device=dev)
+    m.conv_forward(0, xd, B, yd)
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy()
+    ref = oracle_conv(spec, c, v, x)
+    assert y.shape == ref.shape
+    assert np.isfinite(y).all()
+    e = rel_err(y, ref)
+    assert e <= TOL, e
+    m.close()
+
+
+def test_conv_rejects_fc_entry_and_bad_geometry(torch_dev):
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    spec, c, buf, v = conv_case(2)
+    m = cdn.Model(0)
+    with pytest.raises(cdn.CDNError) as e:
+        m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, 13, 13, 5, 5, 1, 1))   # kh*kw*C != cols
+    assert e.value.name == "CDN_E_SHAPE"
+    m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, 13, 13, 3, 3, 1, 1))
+    x = torch.zeros((spec.in_ch, 1), device=dev)
+    with pytest.raises(cdn.CDNError):
+        m.layer_forward(0, x, 1, 1, x, 1)
+    m.close()
