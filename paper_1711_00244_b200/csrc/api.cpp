@@ -102,6 +102,7 @@ struct Model {
   std::vector<DBuf> lvl;        // per-level input buffers [K_i][B_i]
   DBuf out, stage_in, loc, gath, host_stage;
   DBuf conv_a, conv_o, conv_t;  // CONV scratch: bf16 patches, conv output, LRN output
+  DBuf ctmp;                    // conv -> FC boundary: image-major conv output of one phase
   bool busy = false;
   int band_min = 0;             // cdn_model_set_kernel_policy (0: default)
 };
@@ -449,46 +450,72 @@ void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, in
                             (size_t)B * sizeof(float), L.rows, cudaMemcpyDeviceToDevice, s));
 }
 
+int ld4(int b) { return (b + 3) & ~3; }  // feature-major leading dimension (16-byte rows for TMA)
+
 struct Exec {
   Model& m;
   const std::vector<int>& bs;   // batch per layer
-  const float* input;           // image-major [K][features] (host or device)
+  const float* input;           // image-major [K][features] (FC net) or [K][H][W][C] NHWC (conv net)
   bool on_device;
   cudaStream_t s;
   float* scores;                // [K][classes] (host or device)
-  // compute layer i for images [o, o + bs[i]) into dst (feature-major, ld)
+  // Compute layer i for images [o, o + bs[i]) into dst (layer i
+  // runs bs[i]/bs[i-1] phases of layer i-1 into its input buffer first).
+  // FC layer: dst is feature-major [rows][ld]; CONV layer: dst is NHWC
+  // [bs[i]][out_h][out_w][rows] (ld unused).
   void run(int i, int o, float* dst, int ld) {
     const int Bi = bs[i];
     Layer& L = *m.layers[i];
+    const int li = ld4(Bi);
     float* xin = m.lvl[i].as<float>();
     if (i == 0) {
-      const float* src = input + (size_t)o * L.cols;
+      const size_t per = L.in_elems();
+      const float* src = input + (size_t)o * per;
       if (!on_device) {
-        m.stage_in.alloc((size_t)Bi * L.cols * sizeof(float));
-        CUDA_OK(cudaMemcpyAsync(m.stage_in.p, src, (size_t)Bi * L.cols * sizeof(float), cudaMemcpyHostToDevice, s));
+        m.stage_in.alloc((size_t)Bi * per * sizeof(float));
+        CUDA_OK(cudaMemcpyAsync(m.stage_in.p, src, (size_t)Bi * per * sizeof(float), cudaMemcpyHostToDevice, s));
         src = m.stage_in.as<float>();
       }
-      CUDA_OK(launch_transpose(src, Bi, (int)L.cols, (int)L.cols, xin, Bi, s));
+      if (L.is_conv())
+        xin = const_cast<float*>(src);  // NHWC image-major is the conv layout
+      else
+        CUDA_OK(launch_transpose(src, Bi, (int)per, (int)per, xin, li, s));
     } else {
+      const Layer& P = *m.layers[i - 1];
       const int b = bs[i - 1];
-      for (int p = 0; p < Bi / b; ++p) run(i - 1, o + p * b, xin + p * b, Bi);
+      for (int p = 0; p < Bi / b; ++p) {
+        if (L.is_conv()) {
+          run(i - 1, o + p * b, xin + (size_t)p * b * L.in_elems(), 0);
+        } else if (P.is_conv()) {  // flatten (h, w, c) (C-22) and go feature-major
+          float* t = m.ctmp.as<float>();
+          run(i - 1, o + p * b, t, 0);
+          CUDA_OK(launch_transpose(t, b, (int)L.cols, (int)L.cols, xin + p * b, li, s));
+        } else {
+          run(i - 1, o + p * b, xin + p * b, li);
+        }
+      }
     }
-    layer_step(m, i, xin, Bi, Bi, dst, ld, s);
+    if (L.is_conv())
+      conv_forward(m, L, xin, Bi, dst, s);
+    else
+      layer_step(m, i, xin, li, Bi, dst, ld, s);
   }
   void round(int o) {
     const int f = (int)m.layers.size();
     const int Bf = bs[f - 1];
+    if (m.layers[f - 1]->is_conv()) throw Error(CDN_E_UNSUPPORTED, "the last layer must be FC (class scores)");
     const uint32_t classes = m.layers[f - 1]->rows;
-    m.out.alloc((size_t)classes * Bf * sizeof(float));
-    run(f - 1, o, m.out.as<float>(), Bf);
+    const int lf = ld4(Bf);
+    m.out.alloc((size_t)classes * lf * sizeof(float));
+    run(f - 1, o, m.out.as<float>(), lf);
     if (m.rank != 0) return;
-    // [classes][Bf] -> scores[o..o+Bf)[classes]
+    // [classes][lf] -> scores[o..o+Bf)[classes]
     float* dst = scores + (size_t)o * classes;
     if (on_device) {
-      CUDA_OK(launch_transpose(m.out.as<float>(), (int)classes, Bf, Bf, dst, (int)classes, s));
+      CUDA_OK(launch_transpose(m.out.as<float>(), (int)classes, Bf, lf, dst, (int)classes, s));
     } else {
       m.host_stage.alloc((size_t)classes * Bf * sizeof(float));
-      CUDA_OK(launch_transpose(m.out.as<float>(), (int)classes, Bf, Bf, m.host_stage.as<float>(), (int)classes, s));
+      CUDA_OK(launch_transpose(m.out.as<float>(), (int)classes, Bf, lf, m.host_stage.as<float>(), (int)classes, s));
       CUDA_OK(cudaMemcpyAsync(dst, m.host_stage.p, (size_t)classes * Bf * sizeof(float), cudaMemcpyDeviceToHost, s));
     }
   }
@@ -496,8 +523,15 @@ struct Exec {
 
 void alloc_levels(Model& m, const std::vector<int>& bs) {
   m.lvl.resize(m.layers.size());
-  for (size_t i = 0; i < m.layers.size(); ++i)
-    m.lvl[i].alloc((size_t)m.layers[i]->cols * bs[i] * sizeof(float));
+  for (size_t i = 0; i < m.layers.size(); ++i) {
+    const Layer& L = *m.layers[i];
+    if (L.is_conv()) {
+      if (i > 0) m.lvl[i].alloc((size_t)L.in_elems() * bs[i] * sizeof(float));
+    } else {
+      m.lvl[i].alloc((size_t)L.cols * ld4(bs[i]) * sizeof(float));
+      if (i > 0 && m.layers[i - 1]->is_conv()) m.ctmp.alloc((size_t)L.cols * bs[i - 1] * sizeof(float));
+    }
+  }
 }
 
 void check_chain(const Model& m, const std::vector<int>& bs) {
@@ -515,21 +549,32 @@ void profile(Model& m, int Bmax, int reps) {
   m.prof.assign((size_t)f * Bmax, 0.0);
   cudaStream_t s = m.stream;
   size_t maxin = 0, maxout = 0;
-  for (auto& L : m.layers) { maxin = std::max<size_t>(maxin, L->cols); maxout = std::max<size_t>(maxout, L->rows); }
+  for (auto& L : m.layers) {
+    maxin = std::max<size_t>(maxin, L->in_elems());
+    maxout = std::max<size_t>(maxout, L->is_conv() ? L->out_elems() : (size_t)L->rows);
+  }
   DBuf xb, yb;
-  xb.alloc(maxin * Bmax * sizeof(float));
-  yb.alloc(maxout * Bmax * sizeof(float));
-  CUDA_OK(cudaMemsetAsync(xb.p, 0, maxin * Bmax * sizeof(float), s));
+  const size_t bpad = (size_t)ld4(Bmax);
+  xb.alloc(maxin * bpad * sizeof(float));
+  yb.alloc(maxout * bpad * sizeof(float));
+  CUDA_OK(cudaMemsetAsync(xb.p, 0, maxin * bpad * sizeof(float), s));
   cudaEvent_t e0, e1;
   CUDA_OK(cudaEventCreate(&e0));
   CUDA_OK(cudaEventCreate(&e1));
   std::vector<float> t(reps);
-  for (int i = 0; i < f; ++i)
+  for (int i = 0; i < f; ++i) {
+    Layer& L = *m.layers[i];
+    auto step = [&](int B) {
+      if (L.is_conv())
+        conv_forward(m, L, xb.as<float>(), B, yb.as<float>(), s);
+      else
+        layer_step(m, i, xb.as<float>(), ld4(B), B, yb.as<float>(), ld4(B), s);
+    };
     for (int B = 1; B <= Bmax; ++B) {
-      layer_step(m, i, xb.as<float>(), B, B, yb.as<float>(), B, s);  // warm-up
+      step(B);  // warm-up
       for (int r = 0; r < reps; ++r) {
         CUDA_OK(cudaEventRecord(e0, s));
-        layer_step(m, i, xb.as<float>(), B, B, yb.as<float>(), B, s);
+        step(B);
         CUDA_OK(cudaEventRecord(e1, s));
         CUDA_OK(cudaEventSynchronize(e1));
         CUDA_OK(cudaEventElapsedTime(&t[r], e0, e1));
@@ -537,6 +582,7 @@ void profile(Model& m, int Bmax, int reps) {
       std::sort(t.begin(), t.end());
       m.prof[(size_t)i * Bmax + (B - 1)] = t[reps / 2];
     }
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   m.prof_bmax = Bmax;
@@ -544,19 +590,26 @@ void profile(Model& m, int Bmax, int reps) {
 
 std::vector<uint64_t> in_bytes(const Model& m) {
   std::vector<uint64_t> v;
-  for (auto& L : m.layers) v.push_back(4ull * L->cols);
+  for (auto& L : m.layers) v.push_back(4ull * L->in_elems());
   return v;
 }
 std::vector<uint64_t> out_bytes(const Model& m) {
   std::vector<uint64_t> v;
-  for (auto& L : m.layers) v.push_back(4ull * L->rows);
+  for (auto& L : m.layers) v.push_back(4ull * L->out_elems());
   return v;
 }
 std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
   std::vector<uint64_t> v;
   for (auto& L : m.layers) {
     uint64_t ws = L->stats.ws_bytes;
-    if (m.world > 1) ws += 4ull * rows_per_rank(L->rows, m.world) * (m.world + 1) * Bmax;  // C-24: max over grid
+    if (L->is_conv()) {
+      // C-24: the batch-dependent CONV scratch at the largest batch of the grid:
+      // bf16 patches + conv output + LRN output (NHWC fp32)
+      const uint64_t pos = (uint64_t)L->conv_h * L->conv_w;
+      ws += (uint64_t)Bmax * pos * (2ull * L->kpad + (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows);
+    } else if (m.world > 1) {
+      ws += 4ull * rows_per_rank(L->rows, m.world) * (m.world + 1) * Bmax;  // C-24: max over grid
+    }
     v.push_back(ws);
   }
   return v;

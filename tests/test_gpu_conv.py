@@ -128,3 +128,76 @@ def test_conv_rejects_fc_entry_and_bad_geometry(torch_dev):
     with pytest.raises(cdn.CDNError):
         m.layer_forward(0, x, 1, 1, x, 1)
     m.close()
+
+
+def test_c4_alexnet_end_to_end(torch_dev):
+    """Config C4: conv1-conv5 (84/38/35/37/37 %, r = k = 8) + fc6/fc7/fc8, batch
+    64 of 227x227x3 U(0,1) images through cdn_model_infer.  Every layer is
+    gated at 1e-4 against the oracle on the GPU's own input for that layer
+    (per-layer isolation, C-21); infer's scores equal the layer-by-layer GPU
+    chain; the chained bf16 error against the all-oracle chain is reported and
+    loosely bounded (SURVEY [EST-5])."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    B = 64
+    cfg = synth.CONFIGS["C4"]
+    m = cdn.Model(0)
+    comps = []
+    hw = 227
+    for i, spec in enumerate(cfg.conv):
+        _, c, buf, v = conv_case(i)
+        m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, hw, hw, spec.kh, spec.kw, spec.stride, spec.pad,
+                                             spec.groups, relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
+                                             pool_s=2 if spec.pool else 0))
+        hw = m.out_shape(i)[0]
+        comps.append(("conv", spec, c, v))
+    for spec in cfg.fc:
+        W, v = synth.fc_weights(spec, cfg.seed)
+        c = compress.compress_layer(W, spec.density, spec.r, spec.k, v)
+        m.load_layer(cdni.serialize([c.layer]), cdn.LayerDesc.fc(spec.relu))
+        comps.append(("fc", spec, c, v))
+    x = synth.conv_inputs(B, 227, 3, seed=cfg.seed)
+    m.set_plan([B] * len(comps))
+    scores = np.zeros((B, cfg.fc[-1].rows), np.float32)
+    m.infer(x, B, scores, on_device=False)
+
+    # layer by layer on the GPU, each gated against the oracle on the same input
+    cur = torch.from_numpy(x).to(dev)
+    chain = x
+    for li, (kind, spec, c, v) in enumerate(comps):
+        if kind == "conv":
+            oh, ow, oc = m.out_shape(li)
+            y = torch.empty((B, oh, ow, oc), dtype=torch.float32, device=dev)
+            m.conv_forward(li, cur, B, y)
+            torch.cuda.synchronize()
+            ref = oracle_conv(spec, c, v, cur.cpu().numpy())
+            chain = oracle_conv(spec, c, v, chain).astype(np.float32)
+            yn = y.cpu().numpy()
+        else:
+            a = cur.reshape(B, -1)
+            xf = a.T.contiguous()
+            ld = (B + 3) // 4 * 4
+            xp = torch.zeros((xf.shape[0], ld), dtype=torch.float32, device=dev)
+            xp[:, :B] = xf
+            yf = torch.zeros((spec.rows, ld), dtype=torch.float32, device=dev)
+            m.layer_forward(li, xp, ld, B, yf, ld)
+            torch.cuda.synchronize()
+            y = yf[:, :B].T.contiguous()
+            ref = infer.fc_forward(sparse_q(c), a.cpu().numpy(), v, apply_relu=spec.relu)
+            chain = infer.fc_forward(sparse_q(c), chain.reshape(B, -1), v, apply_relu=spec.relu).astype(np.float32)
+            yn = y.cpu().numpy()
+        e = rel_err(yn, ref)
+        assert e <= TOL, (li, e)
+        cur = y
+    assert np.array_equal(scores, cur.cpu().numpy())
+    e2e = rel_err(scores, chain)
+    print(f"C4 end-to-end chained error vs oracle chain: {e2e:.2e}")
+    assert e2e <= 2e-2
+    m.close()
+
+
+def sparse_q(c):
+    import scipy.sparse as sp
+    r, col = np.nonzero(c.mask)
+    vals = c.layer.codebook[c.q[r, col]].astype(np.float32)
+    return sp.csr_matrix((vals, (r, col)), shape=c.mask.shape)
