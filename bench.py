@@ -40,6 +40,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--b1-replicas", type=int, default=8, help="cold-L2 B=1 replicas (0: skip)")
+    p.add_argument("--no-c4", action="store_true", help="skip the AlexNet conv+fc (config C4) line")
     return p.parse_args()
 
 
@@ -143,8 +144,13 @@ def run_ours(args):
     a = synth.fc_inputs(K_in, B, synth.CONFIGS[CFG].seed)
     x_dev = torch.from_numpy(a).to(dev)
     s_dev = torch.zeros((B, N_out), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # A dedicated stream: torch's default (legacy) stream has handle 0, which the
+    # C ABI reads as "library stream, synchronous" -- the events would then not
+    # bracket the kernels.  Every launch and event below goes to this stream.
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
+    assert sp
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     def barrier():
@@ -240,6 +246,10 @@ def run_ours(args):
     if args.b1_replicas > 0 and world == 1:
         b1 = bench_b1(cdn, torch, dev, layers, specs, args.b1_replicas, flush, pk)
 
+    c4 = None
+    if world == 1 and not args.no_c4:
+        c4 = bench_c4(cdn, torch, dev, flush, max(3, min(args.steps, 10)))
+
     comp_bytes = sum(s["stream_bytes"] for s in stats)
     images = B * args.steps
     value = images / (tot_ms / 1e3)
@@ -263,6 +273,8 @@ def run_ours(args):
     }
     if b1:
         res["b1_cold"] = b1
+    if c4:
+        res["c4_alexnet"] = c4
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(layers, B, budget_s=15.0)
     if rank == 0:
@@ -278,6 +290,7 @@ def bench_b1(cdn, torch, dev, layers, specs, R, flush, pk):
     models = [build_model(cdn, 0, 1, None, layers) for _ in range(R)]
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
+    assert sp, "needs a non-default stream (see run_ours)"
     x = [torch.zeros((s.cols, 1), dtype=torch.float32, device=dev) for s in specs]
     y = [torch.zeros((s.rows, 1), dtype=torch.float32, device=dev) for s in specs]
     st = [models[0].stats(i) for i in range(len(specs))]
@@ -306,6 +319,54 @@ def bench_b1(cdn, torch, dev, layers, specs, R, flush, pk):
         mm.close()
     return {"replicas": R, "note": "back-to-back launches over R replicas after an L2 flush (GPU kept busy while the host enqueues); time per launch",
             "layers": per_layer}
+
+
+def bench_c4(cdn, torch, dev, flush, steps):
+    """Config C4: AlexNet conv1-conv5 + fc6-fc8, batch 64 of 227x227x3 images
+    (device-resident NHWC input), one cdn_model_infer per step."""
+    cfg = synth.CONFIGS["C4"]
+    m = cdn.Model(0)
+    hw = cfg.image_hw
+    for i, spec in enumerate(cfg.conv):
+        W, v = synth.fc_weights(spec, cfg.seed)
+        m.load_layer(cdn.compress_dense(W, spec.density, spec.r, spec.k, v),
+                     cdn.LayerDesc.conv(spec.in_ch, hw, hw, spec.kh, spec.kw, spec.stride, spec.pad, spec.groups,
+                                        relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
+                                        pool_s=2 if spec.pool else 0))
+        hw = m.out_shape(i)[0]
+    for spec in cfg.fc:
+        W, v = synth.fc_weights(spec, cfg.seed)
+        m.load_layer(cdn.compress_dense(W, spec.density, spec.r, spec.k, v), cdn.LayerDesc.fc(spec.relu))
+    B = cfg.batches[0]
+    nl = len(cfg.conv) + len(cfg.fc)
+    m.set_plan([B] * nl)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    x = torch.from_numpy(synth.conv_inputs(B, cfg.image_hw, cfg.image_c, cfg.seed)).to(dev)
+    out = torch.zeros((B, cfg.fc[-1].rows), dtype=torch.float32, device=dev)
+    for _ in range(3):
+        m.infer(x, B, out, on_device=True, stream=sp)
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m.infer(x, B, out, on_device=True, stream=sp)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms.append(e0.elapsed_time(e1))
+    t = float(np.median(ms))
+    conv_dense_flop = 0.0
+    h = cfg.image_hw
+    for spec in cfg.conv:
+        ho = (h + 2 * spec.pad - spec.kh) // spec.stride + 1
+        conv_dense_flop += 2.0 * B * ho * ho * spec.out_ch * spec.cols
+        h = (ho - 3) // 2 + 1 if spec.pool else ho
+    m.close()
+    return {"workload": "C4 AlexNet conv1-5 (bf16 tcgen05) + fc6-8, batch 64, device-resident input",
+            "images_per_s": B / (t / 1e3), "ms_per_step": t, "steps": steps,
+            "conv_dense_tflops": conv_dense_flop / (t / 1e3) / 1e12}
 
 
 def cpu_baseline(layers, B, budget_s=15.0):

@@ -441,15 +441,16 @@ BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sm
   p.nbt = (B + BT - 1) / BT;
   p.nchunks = (L.NI + L.Cint - 1) / L.Cint;
   const int tiles = ((L.nrows + kR - 1) / kR) * p.nbt;
-  // K-splits over chunks: cost ~ waves / S (unit time ~ 1/S) + a small
-  // per-split reduction charge; the smallest S within 2% of the best wins.
+  // K-splits over chunks: cost ~ waves / S (unit time ~ 1/S) plus a 3% charge
+  // per extra split (each writes and re-reads an R x BT partial slab); the
+  // smallest S within 2% of the best wins.
   double best = 1e30;
   int bestS = 1;
   const int smax = p.nchunks < 64 ? p.nchunks : 64;
   for (int S = 1; S <= smax; ++S) {
     const long units = (long)tiles * S;
     const long waves = (units + num_sms - 1) / num_sms;
-    const double cost = (double)waves / S * (1.0 + 0.004 * S);
+    const double cost = (double)waves / S * (1.0 + 0.03 * (S - 1));  // split partials cost HBM traffic
     if (cost < best * 0.98) { best = cost; bestS = S; }
   }
   p.S = bestS;
