@@ -79,6 +79,7 @@ struct Layer {
   DBuf ivg, ivm;        // band-kernel interval restart index
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
+  DBuf msv, msg;        // small-batch multi-symbol LUTs
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
   cdn_layer_stats stats{};
   bool is_conv() const { return desc.kind == CDN_LAYER_CONV; }
@@ -166,6 +167,27 @@ std::vector<uint32_t> build_fold_lut(const HuffCode& h, int Lb, int pad_gap_len)
     if (pads == 0 && !has) continue;  // slow path: a code longer than the window
     // real symbols are never 0 (C-04), so sym == 0 marks a pads-only window
     lut[w] = sym | ((uint32_t)(pads * pad_gap_len) << 8) | ((uint32_t)pads << 24) | ((uint32_t)pos << 28);
+  }
+  return lut;
+}
+
+// Multi-symbol LUTs of the small-batch kernel (small.cu): for every Lb-bit
+// window, the complete codes it starts with (up to maxn), their total length
+// and the symbols packed at `bits` bits each from bit 8; n == 0 when the first
+// code is longer than the window (canonical slow path).
+std::vector<uint32_t> build_multi_lut(const HuffCode& h, int Lb, int maxn, int bits) {
+  std::vector<uint32_t> lut((size_t)1 << Lb, 0);
+  for (uint32_t w = 0; w < (1u << Lb); ++w) {
+    const uint32_t win = w << (32 - Lb);
+    uint32_t pos = 0, n = 0, packed = 0;
+    while ((int)n < maxn) {
+      uint32_t sym, len;
+      if (!h.decode(win << pos, sym, len) || (int)(pos + len) > Lb) break;
+      packed |= sym << (bits * n);
+      pos += len;
+      ++n;
+    }
+    lut[w] = n | (pos << 3) | (packed << 8);
   }
   return lut;
 }
@@ -289,6 +311,16 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   const uint32_t padg = (1u << H.k) - 1;
   const int pad_glen = padg < H.gap.len_of.size() ? H.gap.len_of[padg] : 0;
   L.flut.upload(build_fold_lut(H.val, Lf, pad_glen));
+  if (H.r <= 5 && H.k <= 4) {
+    // Windows wider than the longest code still pay: they hold several codes.
+    // 11-bit val window (longer codes are ~0.05% of tokens on C1-C5, up to 4
+    // codes per lookup), 12-bit gap window (up to 6 codes): 24 KB of LUTs per CTA.
+    const int mLv = 11, mLg = 12;
+    L.msv.upload(build_multi_lut(H.val, mLv, 4, 5));
+    L.msg.upload(build_multi_lut(H.gap, mLg, 6, 4));
+    L.dev.msLv = mLv;
+    L.dev.msLg = mLg;
+  }
   L.ctr.alloc(sizeof(int) * kMaxBatchTiles);
   CUDA_OK(cudaMemset(L.ctr.p, 0, sizeof(int) * kMaxBatchTiles));
   L.vtab.upload(build_tab(H.val));
@@ -336,6 +368,8 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.ctr = L.ctr.as<int>();
   f.Lf = Lf;
   f.Lpg = pad_glen;
+  f.msv = L.msv.p ? L.msv.as<uint32_t>() : nullptr;
+  f.msg = L.msg.p ? L.msg.as<uint32_t>() : nullptr;
   f.ivg = L.ivg.as<uint2>();
   f.ivm = L.ivm.as<uint16_t>();
 
@@ -394,6 +428,14 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       CUDA_OK(launch_fc_band(L.dev, p, x, ldx, B, y, ldy, relu, L.bws.as<float>(), L.bctr.as<int>(), s));
       return;
     }
+  }
+  static const bool force_fold = [] {
+    const char* e = std::getenv("CDN_SMALL_KERNEL");
+    return e && std::strcmp(e, "fold") == 0;
+  }();
+  if (B <= 8 && !force_fold && ms_supported(L.dev)) {
+    CUDA_OK(launch_fc_ms(L.dev, x, ldx, B, y, ldy, relu, s, m.num_sms));
+    return;
   }
   CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, y, ldy, relu, s, m.num_sms));
 }

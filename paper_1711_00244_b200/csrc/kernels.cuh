@@ -41,6 +41,10 @@ struct FcDev {
   const uint16_t* ivm = nullptr;
   int Wi = 64, NI = 0;               // interval width (= band width), intervals per row
   int Cint = 16;                     // intervals per decode chunk
+  // small-batch multi-symbol LUTs (small.cu): 2^msLv / 2^msLg entries
+  const uint32_t* msv = nullptr;
+  const uint32_t* msg = nullptr;
+  int msLv = 12, msLg = 12;
 };
 
 // Launch plan of the band kernel for one (layer, B, x) — ok == false means the
@@ -53,6 +57,10 @@ struct BandPlan {
 BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms);
 cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, int ldx, int B, float* y, int ldy,
                            int relu, float* ws, int* tctr, cudaStream_t s);
+// Small-batch multi-symbol kernel (B <= 8; r <= 5, k <= 4, 32-bit lane records).
+bool ms_supported(const FcDev& L);
+cudaError_t launch_fc_ms(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu, cudaStream_t s,
+                         int num_sms);
 int band_rows_per_unit();
 int band_list_capacity();
 int band_max_chunk();
