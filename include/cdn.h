@@ -223,6 +223,14 @@ cdn_status cdn_plan_dp(const double* time_ms, const uint64_t* in_bytes, const ui
 cdn_status cdn_debug_host_walk(const void* cdni, size_t n, int layer_in_file, int32_t* row,
                                int32_t* col, uint8_t* sym, uint64_t* n_tokens);
 
+/* The same host walk on the row-block shard of `rank` out of `world`
+ * (ceil(rows/world) rows per rank): the shard's stream bytes are
+ * cut at word-aligned bit positions and its row_ptr rebased exactly as
+ * cdn_model_load_layer does, then walked; rows are reported as global row
+ * indices.  Host-only (multi-rank sharding logic is tested on CPU with it). */
+cdn_status cdn_debug_host_walk_shard(const void* cdni, size_t n, int layer_in_file, int rank, int world,
+                                     int32_t* row, int32_t* col, uint8_t* sym, uint64_t* n_tokens);
+
 #ifdef __cplusplus
 }
 #endif

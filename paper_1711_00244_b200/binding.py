@@ -94,6 +94,8 @@ _SIGS = {
     "cdn_free": (None, [C.c_void_p]),
     "cdn_plan_dp": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_uint64,
                                 C.c_double, C.c_uint64, C.c_void_p, C.POINTER(C.c_double)]),
+    "cdn_debug_host_walk_shard": (C.c_int32, [C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                              C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
     "cdn_debug_host_walk": (C.c_int32, [C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.POINTER(C.c_uint64)]),
 }
@@ -174,6 +176,19 @@ def debug_gemm_bf16(A, M: int, Wt, N: int, Kpad: int, bias, relu: bool, out, ldo
     """tcgen05 GEMM test hook (device tensors; A/Wt bf16 bit patterns)."""
     _check(load_library().cdn_debug_gemm_bf16(_ptr(A), int(M), _ptr(Wt), int(N), int(Kpad), _ptr(bias),
                                               int(bool(relu)), _ptr(out), int(ldo), stream or None))
+
+
+def debug_host_walk_shard(cdni: bytes, rank: int, world: int, layer_in_file: int = 0):
+    """Host walk of one rank's row-block shard (tokens with global row indices)."""
+    lib = load_library()
+    n = C.c_uint64()
+    _check(lib.cdn_debug_host_walk_shard(cdni, len(cdni), layer_in_file, rank, world, None, None, None, C.byref(n)))
+    row = np.zeros(n.value, np.int32)
+    col = np.zeros(n.value, np.int32)
+    sym = np.zeros(n.value, np.uint8)
+    _check(lib.cdn_debug_host_walk_shard(cdni, len(cdni), layer_in_file, rank, world, row.ctypes.data,
+                                         col.ctypes.data, sym.ctypes.data, C.byref(n)))
+    return row, col, sym
 
 
 def debug_host_walk(cdni: bytes, layer_in_file: int = 0):

@@ -244,9 +244,9 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   L.r = H.r;
   // FC: row-block shard per rank; CONV: replicas (every rank
   // holds all filters; the batch is what multi-GPU splits for conv layers).
-  const uint32_t rb = conv ? H.rows : rows_per_rank(H.rows, m.world);
-  L.row0 = conv ? 0 : std::min<uint32_t>(H.rows, rb * (uint32_t)m.rank);
-  L.row1 = std::min<uint32_t>(H.rows, L.row0 + rb);
+  const ShardSlice sl = shard_slice(H, m.rank, m.world, conv);
+  L.row0 = sl.row0;
+  L.row1 = sl.row1;
   const uint32_t nr = L.row1 - L.row0;
   int target = 64;
   if (const char* e = std::getenv("CDN_LANE_TOKENS")) target = std::max(1, std::atoi(e));
@@ -259,6 +259,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   uint64_t vbase = 0, gbase = 0;
   upload_words(L.vw, H.vbytes, v0, v1, &vbase);
   upload_words(L.gw, H.gbytes, g0, g1, &gbase);
+  if (vbase != sl.vbase || gbase != sl.gbase) throw Error(CDN_E_ARG, "internal: shard slice bases disagree");
   if (v1 - vbase >= (1ull << 32) || g1 - gbase >= (1ull << 32))
     throw Error(CDN_E_UNSUPPORTED, "stream slice larger than 2^32 bits");
   std::vector<uint32_t> rp(2ull * (nr + 1));
@@ -936,6 +937,26 @@ cdn_status cdn_plan_dp(const double* time_ms, const uint64_t* in_b, const uint64
   if (!pr.feasible) return fail(CDN_E_INFEASIBLE, "no feasible plan");
   std::copy(pr.batches.begin(), pr.batches.end(), batches);
   if (opt_ms) *opt_ms = pr.opt;
+  API_END
+}
+
+cdn_status cdn_debug_host_walk_shard(const void* cdni, size_t n, int layer_in_file, int rank, int world,
+                                     int32_t* row, int32_t* col, uint8_t* sym, uint64_t* n_tokens) {
+  API_BEGIN
+  if (!cdni || !n_tokens || world < 1 || rank < 0 || rank >= world) return fail(CDN_E_ARG, "bad arguments");
+  HostLayer H = parse_cdni_layer((const uint8_t*)cdni, n, layer_in_file);
+  const ShardSlice sl = shard_slice(H, rank, world, false);
+  HostLayer S = slice_rows(H, sl);
+  LaneIndex ix;
+  std::vector<Token> toks;
+  build_lane_index(S, 0, S.rows, choose_lanes_per_row(H, 0, H.rows, 64), ix, row ? &toks : nullptr);
+  *n_tokens = ix.tokens;
+  if (row && col && sym)
+    for (size_t i = 0; i < toks.size(); ++i) {
+      row[i] = toks[i].row + (int32_t)sl.row0;
+      col[i] = toks[i].col;
+      sym[i] = toks[i].sym;
+    }
   API_END
 }
 

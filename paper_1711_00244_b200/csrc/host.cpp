@@ -322,6 +322,48 @@ void build_interval_index(const HostLayer& L, uint32_t r0, uint32_t r1, uint32_t
   }
 }
 
+ShardSlice shard_slice(const HostLayer& H, int rank, int world, bool replicate) {
+  ShardSlice sl;
+  const uint32_t rb = replicate ? H.rows : (H.rows + (uint32_t)world - 1) / (uint32_t)world;
+  sl.row0 = replicate ? 0 : std::min<uint64_t>(H.rows, (uint64_t)rb * (uint32_t)rank);
+  sl.row1 = std::min<uint32_t>(H.rows, sl.row0 + rb);
+  sl.vbase = (H.rp[2ull * sl.row0] >> 5) << 5;
+  sl.gbase = (H.rp[2ull * sl.row0 + 1] >> 5) << 5;
+  return sl;
+}
+
+HostLayer slice_rows(const HostLayer& H, const ShardSlice& sl) {
+  HostLayer S;
+  S.rows = sl.row1 - sl.row0;
+  S.cols = H.cols;
+  S.bh = H.bh;
+  S.bw = H.bw;
+  S.k = H.k;
+  S.r = H.r;
+  S.codebook = H.codebook;
+  S.val = H.val;
+  S.gap = H.gap;
+  const uint64_t v1 = H.rp[2ull * sl.row1], g1 = H.rp[2ull * sl.row1 + 1];
+  auto cut = [](const std::vector<uint8_t>& b, uint64_t base_bit, uint64_t end_bit) {
+    const uint64_t b0 = base_bit >> 3, b1 = (end_bit + 7) >> 3;
+    std::vector<uint8_t> out(b.begin() + (ptrdiff_t)b0, b.begin() + (ptrdiff_t)std::min<uint64_t>(b.size(), b1));
+    out.resize(out.size() + 8, 0);  // read-ahead padding (window32 reads 8 bytes)
+    return out;
+  };
+  S.vbytes = cut(H.vbytes, sl.vbase, v1);
+  S.gbytes = cut(H.gbytes, sl.gbase, g1);
+  S.vbits = v1 - sl.vbase;
+  S.gbits = g1 - sl.gbase;
+  S.rp.resize(2ull * (S.rows + 1));
+  for (uint32_t i = 0; i <= S.rows; ++i) {
+    S.rp[2ull * i] = H.rp[2ull * (sl.row0 + i)] - sl.vbase;
+    S.rp[2ull * i + 1] = H.rp[2ull * (sl.row0 + i) + 1] - sl.gbase;
+  }
+  S.has_bias = H.has_bias;
+  if (H.has_bias) S.bias.assign(H.bias.begin() + sl.row0, H.bias.begin() + sl.row1);
+  return S;
+}
+
 // -------------------------------------------------------------- compressor
 
 namespace {

@@ -90,6 +90,20 @@ struct IntervalIndex {
 };
 void build_interval_index(const HostLayer& L, uint32_t r0, uint32_t r1, uint32_t W, IntervalIndex& out);
 
+// Row-block shard of a rank: rows [row0, row1) with
+// ceil(rows/world) rows per rank, and the word-aligned bit positions where the
+// rank's slices of the val / gap streams start (streams are cut, never
+// re-encoded).  replicate: every rank keeps all rows (CONV layers).
+struct ShardSlice {
+  uint32_t row0 = 0, row1 = 0;
+  uint64_t vbase = 0, gbase = 0;
+};
+ShardSlice shard_slice(const HostLayer& H, int rank, int world, bool replicate);
+// A standalone layer holding only the shard's rows: stream bytes cut at the
+// slice bases, row_ptr rebased, bias sliced.  Decoding it must give exactly the
+// shard's rows of the full layer (the invariant row-block sharding relies on).
+HostLayer slice_rows(const HostLayer& H, const ShardSlice& s);
+
 int choose_lanes_per_row(const HostLayer& L, uint32_t r0, uint32_t r1, int target_tokens);
 
 // Product-side compressor (independent of oracle/, same readings).
