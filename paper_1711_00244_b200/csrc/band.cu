@@ -37,15 +37,18 @@ namespace {
 using namespace dev;
 
 constexpr int kR = 128;                          // rows per unit
-constexpr int kWorkWarps = 16;
+constexpr int kWorkWarps = 16;                   // FMA warps
 constexpr int kWorkers = kWorkWarps * 32;
-constexpr int kThreads = kWorkers + 32;          // + 1 producer warp
+constexpr int kDecWarps = 8;                     // decode warps
+constexpr int kDecoders = kDecWarps * 32;
+constexpr int kThreads = kWorkers + kDecoders + 32;  // + 1 producer warp
 constexpr int kRowsPerWarp = kR / kWorkWarps;    // 8
-constexpr int kLC = 64;                          // list entries per row per chunk
-constexpr int kMaxCint = 32;
-constexpr int kStages = 2;
-constexpr int kXStageBytes = 64 * 1024;
-constexpr int kWorkBar = 1;                      // named barrier of the 16 worker warps
+constexpr int kLC = 32;                          // list entries per row per chunk
+constexpr int kMaxCint = 16;
+constexpr int kStages = 2;                       // activation-band ring
+constexpr int kLBufs = 2;                        // decoded-list ring
+constexpr int kXStageBytes = 32 * 1024;
+constexpr int kWorkBar = 1;                      // named barrier of the 16 FMA warps
 
 struct BandArgs {
   const float* x;
@@ -149,12 +152,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_fc_band(FcDev L, BandArgs a, const __grid_constant__ CUtensorMap tmx) {
   constexpr int BT = 32 * VEC;
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* xs = smem;                                                  // [kStages][Wi][BT] fp32
-  float2* lists = reinterpret_cast<float2*>(smem + kStages * kXStageBytes);  // [kR][kLC] (w, x byte offset)
-  uint32_t* bse = reinterpret_cast<uint32_t*>(lists + kR * kLC);            // [kR][kMaxCint] start | end << 16
-  uint64_t* full = reinterpret_cast<uint64_t*>(bse + kR * kMaxCint);
+  unsigned char* xs = smem;                                                  // [kStages][ipb*Wi][BT] fp32
+  float2* lists = reinterpret_cast<float2*>(smem + kStages * kXStageBytes);  // [kLBufs][kR][kLC] (w, x offset)
+  uint32_t* bse = reinterpret_cast<uint32_t*>(lists + kLBufs * kR * kLC);   // [kLBufs][kR][kMaxCint]
+  uint64_t* full = reinterpret_cast<uint64_t*>(bse + kLBufs * kR * kMaxCint);
   uint64_t* empty = full + kStages;
-  int* s_last = reinterpret_cast<int*>(empty + kStages);                    // [4]
+  uint64_t* lfull = empty + kStages;
+  uint64_t* lempty = lfull + kLBufs;
+  int* meta = reinterpret_cast<int*>(lempty + kLBufs);                      // [kLBufs][4]: ni | flags, tile, sp
+  int* s_last = meta + kLBufs * 4;                                          // [4]
   uint32_t* s_flut = reinterpret_cast<uint32_t*>(s_last + 4);
   uint32_t* s_glut = s_flut + (1 << L.Lf);
   float* s_cb = reinterpret_cast<float*>(s_glut + (1 << L.Lg));
@@ -175,6 +181,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], kWorkWarps);
       }
+      for (int b = 0; b < kLBufs; ++b) {
+        mbar_init(&lfull[b], kDecWarps);
+        mbar_init(&lempty[b], kWorkWarps);
+      }
       mbar_fence_init();
     }
   }
@@ -183,15 +193,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ipb = a.ipb;
   const uint32_t xstage_bytes = (uint32_t)(L.Wi * ipb) * BT * 4;
+  const int Cint = L.Cint;
 
-  if (warp == kWorkWarps) {
+  if (warp == kWorkWarps + kDecWarps) {
     // ---------------------------------------------------------------- producer
     if (lane == 0) {
       uint32_t g = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         const UnitCoord c = unit_coord(L, a, u);
-        for (int ib = c.i0; ib < c.i1; ib += L.Cint) {
-          const int ni = min(L.Cint, c.i1 - ib);
+        for (int ib = c.i0; ib < c.i1; ib += Cint) {
+          const int ni = min(Cint, c.i1 - ib);
           for (int b0 = 0; b0 < ni; b0 += ipb, ++g) {
             const int s = g % kStages;
             mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
@@ -204,12 +215,127 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
 
-  // ------------------------------------------------------------------ workers
+  if (warp >= kWorkWarps) {
+    // ------------------------------------------------------------ decode warps
+    // one lane per (row, interval) task of a chunk; known output offsets (the
+    // interval index carries each interval's real-token count)
+    const int dtid = threadIdx.x - kWorkers;
+    const int dwarp = warp - kWorkWarps;
+    const int fsh = 32 - L.Lf, gsh = 32 - L.Lg, k = L.k;
+    const int npass = (kR * Cint + kDecoders - 1) / kDecoders;
+    uint32_t c = 0;  // chunk counter (list ring position)
+    for (int u = blockIdx.x;; u += gridDim.x) {
+      const bool done = u >= a.units;
+      UnitCoord uc{};
+      if (!done) uc = unit_coord(L, a, u);
+      // every unit emits >= 1 chunk (an empty K-split still flushes its partial)
+      for (int ib = uc.i0;; ib += Cint, ++c) {
+        const int lb = c % kLBufs;
+        mbar_wait(&lempty[lb], ((c / kLBufs) & 1) ^ 1);
+        if (done) {
+          if (dwarp == 0 && lane == 0) meta[lb * 4] = 1 << 30;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lfull[lb]);
+          ++c;
+          break;
+        }
+        const int ni = max(0, min(Cint, uc.i1 - ib));
+        const bool last_chunk = ib + Cint >= uc.i1;
+        float2* lst = lists + (size_t)lb * kR * kLC;
+        uint32_t* bs = bse + (size_t)lb * kR * kMaxCint;
+        for (int pass = 0; pass < npass; pass += 2) {
+          Task tk[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int t = (pass + h) * kDecoders + dtid;
+            tk[h].rl = t / Cint;
+            tk[h].j = t % Cint;
+            const int row = uc.rb * kR + tk[h].rl;
+            const bool valid = pass + h < npass && tk[h].rl < kR && row < L.nrows && tk[h].j < ni;
+            tk[h].q = (size_t)row * L.NI + ib + tk[h].j;
+            tk[h].m = valid ? (uint32_t)L.ivm[tk[h].q] : 0u;
+            tk[h].st = valid ? L.ivg[tk[h].q] : make_uint2(0, 0);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t nnz = tk[h].m >> 8;
+            uint32_t off = nnz;  // inclusive scan over the Cint lanes of this row
+            for (int o = 1; o < Cint; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, off, o, Cint);
+              if (tk[h].j >= o) off += y;
+            }
+            off -= nnz;
+            tk[h].off = off;
+            if (pass + h < npass && tk[h].rl < kR) bs[tk[h].rl * kMaxCint + tk[h].j] = off | ((off + nnz) << 16);
+            if (nnz) {
+              tk[h].vr.init(L.vw, tk[h].st.x);
+              tk[h].gr.init(L.gw, tk[h].st.y);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t nnz = tk[h].m >> 8;
+            if (!nnz) continue;
+            const int iv = ib + tk[h].j;
+            const int bstart = (ib + (tk[h].j / ipb) * ipb) * L.Wi;  // first column of the band's X stage
+            int col = iv * L.Wi - (int)(tk[h].m & 0xFFu) - 1;
+            float2* dst = lst + tk[h].rl * kLC + tk[h].off;
+            TReader& vr = tk[h].vr;
+            TReader& gr = tk[h].gr;
+            uint32_t ndone = 0;
+            while (ndone < nnz) {
+              const uint32_t w = vr.peek();
+              const uint32_t e = s_flut[w >> fsh];
+              uint32_t len, sym, pads, pbits;
+              if (e != kFoldSlow) {
+                len = e >> 28;
+                sym = e & 0xFFu;
+                pads = (e >> 24) & 15u;
+                pbits = (e >> 8) & 0xFFFFu;
+              } else {
+                const uint32_t r = slow_sym(w, L.Lf + 1, s_vtab, s_vsorted, L.vmax);
+                len = r >> 16;
+                sym = r & 0xFFu;
+                pads = sym == 0;  // a long pad code (C-04: symbol 0 <=> pad)
+                pbits = pads ? (uint32_t)L.Lpg : 0u;
+              }
+              vr.skip(len);
+              col += (int)(pads << k);
+              if (pbits <= 32) {
+                gr.skip(pbits);
+              } else {
+                for (uint32_t z = 0; z < pads; ++z) gr.skip((uint32_t)L.Lpg);  // long pad codes (rare)
+              }
+              if (sym) {
+                const uint32_t gwin = gr.peek();
+                uint32_t ge = s_glut[gwin >> gsh];
+                if (ge == 0) ge = slow_sym(gwin, L.Lg + 1, s_gtab, s_gsorted, L.gmax);
+                gr.skip(ge >> 16);
+                col += (int)(ge & 0xFFFFu) + 1;
+                dst[ndone++] = make_float2(s_cb[sym], __uint_as_float((uint32_t)(col - bstart) * (BT * 4)));
+              }
+            }
+          }
+        }
+        if (dwarp == 0 && lane == 0) {
+          meta[lb * 4 + 0] = ni | (last_chunk ? (1 << 29) : 0);  // bit 29: last chunk of the unit
+          meta[lb * 4 + 1] = uc.tile;
+          meta[lb * 4 + 2] = uc.sp;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&lfull[lb]);
+        if (last_chunk) {
+          ++c;
+          break;
+        }
+      }
+      if (done) break;
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- FMA warps
   const int tid = threadIdx.x;
-  const int fsh = 32 - L.Lf, gsh = 32 - L.Lg, k = L.k;
-  const int Cint = L.Cint;
-  const int rows_per_pass = kWorkers / Cint;
-  const int npass = (kR + rows_per_pass - 1) / rows_per_pass;
   float acc[kRowsPerWarp][VEC];
 #pragma unroll
   for (int rr = 0; rr < kRowsPerWarp; ++rr)
@@ -217,126 +343,60 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int v = 0; v < VEC; ++v) acc[rr][v] = 0.f;
   const unsigned char* xl = xs + lane * (VEC == 8 ? 16 : VEC * 4);
   uint32_t g = 0;
-
-  for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-    const UnitCoord uc = unit_coord(L, a, u);
-    for (int ib = uc.i0; ib < uc.i1; ib += Cint) {
-      const int ni = min(Cint, uc.i1 - ib);
-      // ---- decode phase: one lane per (row, interval) of the chunk; two
-      // passes' index and stream loads are issued together (one round trip)
-      for (int pass = 0; pass < npass; pass += 2) {
-        Task tk[2];
+  for (uint32_t c = 0;; ++c) {
+    const int lb = c % kLBufs;
+    mbar_wait(&lfull[lb], (c / kLBufs) & 1);
+    const int m0 = meta[lb * 4 + 0];
+    if (m0 & (1 << 30)) break;
+    const int ni = m0 & 0xFFFF;
+    const bool last = (m0 >> 29) & 1;
+    const int tile = meta[lb * 4 + 1], sp = meta[lb * 4 + 2];
+    const float2* lst = lists + (size_t)lb * kR * kLC;
+    const uint32_t* bs = bse + (size_t)lb * kR * kMaxCint;
+    for (int j0 = 0; j0 < ni; j0 += ipb, ++g) {
+      const int s = g % kStages;
+      const int j1 = min(ni, j0 + ipb) - 1;
+      mbar_wait(&full[s], (g / kStages) & 1);
+      const unsigned char* xb = xl + s * kXStageBytes;
+      int eb[kRowsPerWarp], ee[kRowsPerWarp];  // all 8 rows' entry ranges up front
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int t = (pass + h) * kWorkers + tid;
-          tk[h].rl = t / Cint;
-          tk[h].j = t % Cint;
-          const int row = uc.rb * kR + tk[h].rl;
-          const bool valid = pass + h < npass && tk[h].rl < kR && row < L.nrows && tk[h].j < ni;
-          tk[h].q = (size_t)row * L.NI + ib + tk[h].j;
-          tk[h].m = valid ? (uint32_t)L.ivm[tk[h].q] : 0u;
-          tk[h].st = valid ? L.ivg[tk[h].q] : make_uint2(0, 0);
-        }
+      for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+        const int rl = warp + kWorkWarps * rr;
+        eb[rr] = (int)(bs[rl * kMaxCint + j0] & 0xFFFFu);
+        ee[rr] = (int)(bs[rl * kMaxCint + j1] >> 16);
+      }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t nnz = tk[h].m >> 8;
-          uint32_t off = nnz;  // inclusive scan over the Cint lanes of this row
-          for (int o = 1; o < Cint; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, off, o, Cint);
-            if (tk[h].j >= o) off += y;
-          }
-          off -= nnz;
-          tk[h].off = off;
-          if (pass + h < npass && tk[h].rl < kR) bse[tk[h].rl * kMaxCint + tk[h].j] = off | ((off + nnz) << 16);
-          if (nnz) {
-            tk[h].vr.init(L.vw, tk[h].st.x);
-            tk[h].gr.init(L.gw, tk[h].st.y);
-          }
-        }
+      for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+        const int rl = warp + kWorkWarps * rr;
+        const int e0 = eb[rr], e1 = ee[rr];
+        const float2* lr = lst + rl * kLC;
+        // one broadcast LDS.64 (w, x offset) + one VEC-wide LDS of x per entry
+#pragma unroll 4
+        for (int e = e0; e < e1; ++e) {
+          const float2 p = lr[e];
+          float xv[VEC];
+          load_x<VEC>(xb + __float_as_uint(p.y), xv);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t nnz = tk[h].m >> 8;
-          if (!nnz) continue;
-          const int iv = ib + tk[h].j;
-          const int bstart = (ib + (tk[h].j / ipb) * ipb) * L.Wi;  // first column of the band's X stage
-          int col = iv * L.Wi - (int)(tk[h].m & 0xFFu) - 1;
-          float2* dst = lists + tk[h].rl * kLC + tk[h].off;
-          TReader& vr = tk[h].vr;
-          TReader& gr = tk[h].gr;
-          uint32_t done = 0;
-          while (done < nnz) {
-            const uint32_t w = vr.peek();
-            const uint32_t e = s_flut[w >> fsh];
-            uint32_t len, sym, pads, pbits;
-            if (e != kFoldSlow) {
-              len = e >> 28;
-              sym = e & 0xFFu;
-              pads = (e >> 24) & 15u;
-              pbits = (e >> 8) & 0xFFFFu;
-            } else {
-              const uint32_t r = slow_sym(w, L.Lf + 1, s_vtab, s_vsorted, L.vmax);
-              len = r >> 16;
-              sym = r & 0xFFu;
-              pads = sym == 0;  // a long pad code (C-04: symbol 0 <=> pad)
-              pbits = pads ? (uint32_t)L.Lpg : 0u;
-            }
-            vr.skip(len);
-            col += (int)(pads << k);
-            if (pbits <= 32) {
-              gr.skip(pbits);
-            } else {
-              for (uint32_t z = 0; z < pads; ++z) gr.skip((uint32_t)L.Lpg);  // long pad codes (rare)
-            }
-            if (sym) {
-              const uint32_t gwin = gr.peek();
-              uint32_t ge = s_glut[gwin >> gsh];
-              if (ge == 0) ge = slow_sym(gwin, L.Lg + 1, s_gtab, s_gsorted, L.gmax);
-              gr.skip(ge >> 16);
-              col += (int)(ge & 0xFFFFu) + 1;
-              dst[done++] = make_float2(s_cb[sym], __uint_as_float((uint32_t)(col - bstart) * (BT * 4)));
-            }
-          }
+          for (int v = 0; v < VEC; ++v) acc[rr][v] = fmaf(p.x, xv[v], acc[rr][v]);
         }
       }
-      named_bar_sync(kWorkBar, kWorkers);
-
-      // ---- FMA phase: one band (ipb intervals) per pipeline stage
-      for (int j0 = 0; j0 < ni; j0 += ipb, ++g) {
-        const int s = g % kStages;
-        const int j1 = min(ni, j0 + ipb) - 1;
-        mbar_wait(&full[s], (g / kStages) & 1);
-        const unsigned char* xb = xl + s * kXStageBytes;
-#pragma unroll
-        for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-          const int rl = warp + kWorkWarps * rr;
-          const int e0 = (int)(bse[rl * kMaxCint + j0] & 0xFFFFu);
-          const int e1 = (int)(bse[rl * kMaxCint + j1] >> 16);
-          const float2* lr = lists + rl * kLC;
-          // one broadcast LDS.64 (w, x offset) + one VEC-wide LDS of x per entry
-#pragma unroll 2
-          for (int e = e0; e < e1; ++e) {
-            const float2 p = lr[e];
-            float xv[VEC];
-            load_x<VEC>(xb + __float_as_uint(p.y), xv);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[rr][v] = fmaf(p.x, xv[v], acc[rr][v]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
-      named_bar_sync(kWorkBar, kWorkers);  // lists / bse are rewritten by the next chunk
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&lempty[lb]);
+    if (!last) continue;
 
     // ---- unit complete: bias + ReLU (S == 1) or split partial + ordered reduction
-    const int nb = min(BT, a.B - uc.bt * BT);
+    const int rb0 = tile / a.nbt, bt = tile % a.nbt;
+    const int nb = min(BT, a.B - bt * BT);
     if (a.S == 1) {
 #pragma unroll
       for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-        const int row = uc.rb * kR + warp + kWorkWarps * rr;
+        const int row = rb0 * kR + warp + kWorkWarps * rr;
         if (row < L.nrows) {
           const float bias = L.bias[row];
-          float* yp = a.y + (size_t)row * a.ldy + uc.bt * BT;
+          float* yp = a.y + (size_t)row * a.ldy + bt * BT;
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             const int b = bcol<VEC>(lane, v);
@@ -347,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      float* slab = a.ws + ((size_t)uc.tile * a.S + uc.sp) * kR * BT;
+      float* slab = a.ws + ((size_t)tile * a.S + sp) * kR * BT;
 #pragma unroll
       for (int rr = 0; rr < kRowsPerWarp; ++rr) {
         float* p = slab + (size_t)(warp + kWorkWarps * rr) * BT;
@@ -357,19 +417,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       __threadfence();
       named_bar_sync(kWorkBar, kWorkers);
       if (tid == 0) {
-        const int old = atomicAdd(&a.tctr[uc.tile], 1);
+        const int old = atomicAdd(&a.tctr[tile], 1);
         const int is_last = old == a.S - 1;
-        if (is_last) a.tctr[uc.tile] = 0;
+        if (is_last) a.tctr[tile] = 0;
         s_last[0] = is_last;
       }
       named_bar_sync(kWorkBar, kWorkers);
       if (s_last[0]) {
         __threadfence();
-        const float* base = a.ws + (size_t)uc.tile * a.S * kR * BT;
+        const float* base = a.ws + (size_t)tile * a.S * kR * BT;
 #pragma unroll
         for (int rr = 0; rr < kRowsPerWarp; ++rr) {
           const int rl = warp + kWorkWarps * rr;
-          const int row = uc.rb * kR + rl;
+          const int row = rb0 * kR + rl;
           if (row >= L.nrows) continue;
           float sum[VEC];
 #pragma unroll
@@ -380,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int v = 0; v < VEC; ++v) sum[v] += __ldcg(p + bcol<VEC>(lane, v));
           }
           const float bias = L.bias[row];
-          float* yp = a.y + (size_t)row * a.ldy + uc.bt * BT;
+          float* yp = a.y + (size_t)row * a.ldy + bt * BT;
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             const int b = bcol<VEC>(lane, v);
@@ -390,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      named_bar_sync(kWorkBar, kWorkers);  // s_last is rewritten by the next flush
     }
 #pragma unroll
     for (int rr = 0; rr < kRowsPerWarp; ++rr)
@@ -399,8 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 size_t band_smem_bytes(const FcDev& L) {
-  size_t b = (size_t)kStages * kXStageBytes + sizeof(float2) * kR * kLC + sizeof(uint32_t) * kR * kMaxCint +
-             sizeof(uint64_t) * 2 * kStages + sizeof(int) * 4;
+  size_t b = (size_t)kStages * kXStageBytes + sizeof(float2) * kLBufs * kR * kLC +
+             sizeof(uint32_t) * kLBufs * kR * kMaxCint + sizeof(uint64_t) * 2 * (kStages + kLBufs) +
+             sizeof(int) * (kLBufs * 4 + 4);
   b += (sizeof(uint32_t) << L.Lf) + (sizeof(uint32_t) << L.Lg) + sizeof(float) * L.ncb + 2 * 99 * sizeof(uint32_t) +
        sizeof(uint16_t) * (L.nvs + 1) + sizeof(uint16_t) * (L.ngs + 1);
   return (b + 127) & ~(size_t)127;
@@ -429,7 +491,7 @@ int band_max_chunk() { return kMaxCint; }
 BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms) {
   BandPlan p;
   if (B <= 0 || L.nrows <= 0 || !L.ivg || L.Cint <= 0) return p;
-  const int vec = B > 128 ? 8 : (B > 64 ? 4 : (B > 32 ? 2 : 1));
+  const int vec = B > 64 ? 4 : (B > 32 ? 2 : 1);
   const int BT = 32 * vec;
   if ((ldx & 3) || ldx < B || ((uintptr_t)x & 15)) return p;  // TMA: 16-byte row pitch and base
   if ((size_t)L.Wi * BT * 4 > (size_t)kXStageBytes) return p;
@@ -492,7 +554,6 @@ cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, in
     map = &e.m;
   }
   switch (p.vec) {
-    case 8: return launch_band_t<8>(L, p, a, *map, s);
     case 4: return launch_band_t<4>(L, p, a, *map, s);
     case 2: return launch_band_t<2>(L, p, a, *map, s);
     default: return launch_band_t<1>(L, p, a, *map, s);
