@@ -47,7 +47,7 @@ constexpr int kLC = 32;                          // list entries per row per chu
 constexpr int kMaxCint = 16;
 constexpr int kStages = 2;                       // activation-band ring
 constexpr int kLBufs = 2;                        // decoded-list ring
-constexpr int kXStageBytes = 32 * 1024;
+constexpr int kXStageBytes = 64 * 1024;
 constexpr int kWorkBar = 1;                      // named barrier of the 16 FMA warps
 
 struct BandArgs {
