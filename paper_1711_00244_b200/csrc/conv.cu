@@ -29,7 +29,7 @@ using namespace dev;
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kGStages = 4;
+constexpr int kGMaxStages = 4;
 constexpr int kGThreads = 128;
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -78,8 +78,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // W: over [Nrows][Kpad] bf16; nk = Kpad / 64.
 __global__ void __launch_bounds__(kGThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int Mrows, int Nrows,
-                int nk, int BN, int tmem_cols, const float* __restrict__ bias, float* __restrict__ out, int ldo,
-                int col0, int relu) {
+                int nk, int BN, int tmem_cols, int kGStages, const float* __restrict__ bias,
+                float* __restrict__ out, int ldo, int col0, int relu) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int a_bytes = kBM * kBK * 2, b_bytes = BN * kBK * 2;
@@ -148,13 +148,26 @@ __global__ void __launch_bounds__(kGThreads, 1)
     tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
     if (row < Mrows) {
       float* op = out + (size_t)row * ldo + col0 + n0 + c;
+      if (n0 + c + 16 <= Nrows && ((((uintptr_t)op) & 15) == 0)) {
+        const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int n = n0 + c + i;
-        if (n < Nrows) {
-          float o = v[i] + bias[n];
-          if (relu) o = fmaxf(o, 0.f);
-          op[i] = o;
+        for (int q = 0; q < 4; ++q) {
+          const float4 bq = __ldg(bp + q);
+          float4 o = make_float4(v[4 * q] + bq.x, v[4 * q + 1] + bq.y, v[4 * q + 2] + bq.z, v[4 * q + 3] + bq.w);
+          if (relu) {
+            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+          }
+          reinterpret_cast<float4*>(op)[q] = o;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int n = n0 + c + i;
+          if (n < Nrows) {
+            float o = v[i] + bias[n];
+            if (relu) o = fmaxf(o, 0.f);
+            op[i] = o;
+          }
         }
       }
     }
@@ -167,6 +180,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
 // NHWC fp32 -> bf16 (RNE) patches [pos][Kpad] of channels [c0, c0+cg):
 // k = (r*kw + s)*cg + c, zero for padding taps and k >= kh*kw*cg.
+template <bool VEC8>
 __global__ void k_im2col(const float* __restrict__ x, int B, int H, int W, int C, int kh, int kw, int stride, int pad,
                          int c0, int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* __restrict__ out) {
   const int kq = Kpad / 8;
@@ -178,17 +192,35 @@ __global__ void k_im2col(const float* __restrict__ x, int B, int H, int W, int C
     const int rem = (int)(pos % (Ho * Wo));
     const int oh = rem / Wo, ow = rem % Wo;
     __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = k0 + j;
-      float f = 0.f;
-      if (k < Kreal) {
-        const int c = k % cg, rs = k / cg;
+    if (VEC8) {
+      // cg % 8 == 0: the 8 k's are 8 consecutive channels of one (r, s) tap
+      float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (k0 < Kreal) {
+        const int c = k0 % cg, rs = k0 / cg;
         const int s = rs % kw, r = rs / kw;
         const int ih = oh * stride - pad + r, iw = ow * stride - pad + s;
-        if (ih >= 0 && ih < H && iw >= 0 && iw < W) f = x[(((size_t)b * H + ih) * W + iw) * C + c0 + c];
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) {
+          const float4* px = reinterpret_cast<const float4*>(x + (((size_t)b * H + ih) * W + iw) * C + c0 + c);
+          const float4 a0 = __ldg(px), a1 = __ldg(px + 1);
+          f[0] = a0.x; f[1] = a0.y; f[2] = a0.z; f[3] = a0.w;
+          f[4] = a1.x; f[5] = a1.y; f[6] = a1.z; f[7] = a1.w;
+        }
       }
-      v[j] = __float2bfloat16_rn(f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(f[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + j;
+        float f = 0.f;
+        if (k < Kreal) {
+          const int c = k % cg, rs = k / cg;
+          const int s = rs % kw, r = rs / kw;
+          const int ih = oh * stride - pad + r, iw = ow * stride - pad + s;
+          if (ih >= 0 && ih < H && iw >= 0 && iw < W) f = x[(((size_t)b * H + ih) * W + iw) * C + c0 + c];
+        }
+        v[j] = __float2bfloat16_rn(f);
+      }
     }
     *reinterpret_cast<uint4*>(out + pos * Kpad + k0) = *reinterpret_cast<const uint4*>(v);
   }
@@ -241,8 +273,17 @@ int gemm_tile_n(int Nrows) {
   return (bn + 15) & ~15;
 }
 
+// Pipeline depth: as many stages as fit ~100 KB, so two CTAs share an SM and
+// one CTA's epilogue overlaps the other's tensor-core main loop.
+int gemm_stages(int BN) {
+  const int per = kBM * kBK * 2 + BN * kBK * 2;
+  int st = (100 * 1024) / per;
+  return st < 2 ? 2 : (st > kGMaxStages ? kGMaxStages : st);
+}
+
 size_t gemm_smem_bytes(int BN) {
-  return 1024 + (size_t)kGStages * (kBM * kBK * 2 + BN * kBK * 2) + (2 * kGStages + 1) * 8 + 16;
+  const int st = gemm_stages(BN);
+  return 1024 + (size_t)st * (kBM * kBK * 2 + BN * kBK * 2) + (2 * st + 1) * 8 + 16;
 }
 
 cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
@@ -267,7 +308,8 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
     set_smem = smem;
   }
   dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN);
-  k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, bias, out, ldo, col0, relu);
+  k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
+                                            ldo, col0, relu);
   return cudaGetLastError();
 }
 
@@ -275,8 +317,13 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
                           int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
                           int num_sms) {
   const long work = (long)B * Ho * Wo * (Kpad / 8);
-  k_im2col<<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo, Kreal,
-                                                        Kpad, out);
+  const bool vec8 = (cg % 8 == 0) && (C % 4 == 0) && (c0 % 4 == 0) && (((uintptr_t)x & 15) == 0);
+  if (vec8)
+    k_im2col<true><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
+                                                                Kreal, Kpad, out);
+  else
+    k_im2col<false><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
+                                                                 Kreal, Kpad, out);
   return cudaGetLastError();
 }
 
