@@ -375,3 +375,50 @@ def test_band_repeated_launches_are_deterministic(torch_dev):
     a = synth.fc_inputs(spec.cols, 512, 0)
     ys = [gpu_forward(torch, dev, m, a, spec.rows) for _ in range(3)]
     assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[1], ys[2])
+
+
+# ----------------------------------------------------------------- planner (C3)
+
+def test_c3_planner_under_64mib_budget(torch_dev):
+    """Config C3: AlexNet FC stack, TOT = 64 MiB, batch chosen by the planner
+    from 1..K.  On the device-profiled Time table, the library's
+    plan is a divisor chain, feasible under the EXACT memory model, never
+    better than the exact oracle DP (C-25), equal to the host C++ DP on the same
+    table; infer with it (remainder re-plan) matches the oracle chain."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    from oracle import planner as oplanner
+    cfg = synth.CONFIGS["C3"]
+    m = cdn.Model(0)
+    comps = []
+    for i, spec in enumerate(cfg.fc):
+        _, c, buf = config_layer("C3", i)
+        m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+        comps.append((c, synth.fc_weights(spec, 0)[1], spec.relu))
+    K = 100
+    m.set_memory_budget(cfg.tot_bytes)
+    T = m.profile(K, 5)
+    batches, predicted = m.plan(K)
+    st = [m.stats(i) for i in range(3)]
+    inb = [4 * s["in_features"] for s in st]
+    outb = [4 * s["out_features"] for s in st]
+    ws = [s["ws_bytes"] for s in st]
+    p = oplanner.Problem([{B: float(T[i][B - 1]) for B in range(1, K + 1)} for i in range(3)], inb, outb, ws,
+                         cfg.tot_bytes)
+    assert all(batches[i + 1] % batches[i] == 0 for i in range(2))
+    cost = oplanner.chain_cost(p, batches)
+    assert np.isfinite(cost)
+    exact = oplanner.dp_plan(p, K)
+    assert cost / batches[-1] >= exact.per_image * (1 - 1e-9)
+    bs2, opt2 = cdn.plan_dp(T, inb, outb, ws, cfg.tot_bytes, 0.0, step=64 * 1024)
+    assert bs2 == batches
+    assert predicted > 0
+    # the whole request through the planned executor
+    a = synth.fc_inputs(cfg.fc[0].cols, K, 0)
+    scores = np.zeros((K, cfg.fc[-1].rows), np.float32)
+    m.infer(a, K, scores, on_device=False)
+    x = a
+    for c, v, relu in comps:
+        x = infer.fc_forward(sparse_q(c), x, v, apply_relu=relu).astype(np.float32)
+    assert rel_err(scores, x) <= TOL
+    m.close()
