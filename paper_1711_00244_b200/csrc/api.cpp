@@ -638,7 +638,16 @@ std::vector<uint64_t> in_bytes(const Model& m) {
 }
 std::vector<uint64_t> out_bytes(const Model& m) {
   std::vector<uint64_t> v;
-  for (auto& L : m.layers) v.push_back(4ull * L->out_elems());
+  for (auto& L : m.layers) {
+    uint64_t b = 4ull * L->out_elems();
+    // CONV scratch grows with the batch (bf16 patches + conv / LRN outputs), so
+    // it is charged per image with OUT(i,B) rather than as a constant WS(i)
+    // (reading C-24 for CONV layers); WS(i) keeps the decoded filters.
+    if (L->is_conv())
+      b += (uint64_t)L->conv_h * L->conv_w *
+           (2ull * L->kpad + (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows);
+    v.push_back(b);
+  }
   return v;
 }
 std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
@@ -646,10 +655,7 @@ std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
   for (auto& L : m.layers) {
     uint64_t ws = L->stats.ws_bytes;
     if (L->is_conv()) {
-      // C-24: the batch-dependent CONV scratch at the largest batch of the grid:
-      // bf16 patches + conv output + LRN output (NHWC fp32)
-      const uint64_t pos = (uint64_t)L->conv_h * L->conv_w;
-      ws += (uint64_t)Bmax * pos * (2ull * L->kpad + (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows);
+      // decoded bf16 filters only (the per-image scratch is in out_bytes)
     } else if (m.world > 1) {
       ws += 4ull * rows_per_rank(L->rows, m.world) * (m.world + 1) * Bmax;  // C-24: max over grid
     }

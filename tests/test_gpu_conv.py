@@ -201,3 +201,40 @@ def sparse_q(c):
     r, col = np.nonzero(c.mask)
     vals = c.layer.codebook[c.q[r, col]].astype(np.float32)
     return sp.csr_matrix((vals, (r, col)), shape=c.mask.shape)
+
+
+def test_c4_variable_batch_plan_under_budget(torch_dev):
+    """SURVEY NEXT #1 on the device: AlexNet conv1-5 + fc6-8 under TOT = 128 MiB
+    for K = 32 images.  conv1's per-image footprint (input, patches, conv/LRN
+    outputs) caps the conv batch well below what the FC layers afford, so the
+    DP picks a variable-batch divisor chain; infer with it
+    reproduces the fixed-batch GPU scores (same kernels, different grouping)."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    cfg = synth.CONFIGS["C4"]
+    m = cdn.Model(0)
+    hw = 227
+    for i, spec in enumerate(cfg.conv):
+        _, c, buf, v = conv_case(i)
+        m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, hw, hw, spec.kh, spec.kw, spec.stride, spec.pad,
+                                             spec.groups, relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
+                                             pool_s=2 if spec.pool else 0))
+        hw = m.out_shape(i)[0]
+    for spec in cfg.fc:
+        W, v = synth.fc_weights(spec, cfg.seed)
+        c = compress.compress_layer(W, spec.density, spec.r, spec.k, v)
+        m.load_layer(cdni.serialize([c.layer]), cdn.LayerDesc.fc(spec.relu))
+    K = 32
+    m.set_memory_budget(128 << 20)
+    batches, predicted = m.plan(K)
+    print("C4 plan under 128 MiB:", batches, f"{predicted:.3f} ms for {K} images")
+    assert all(batches[i + 1] % batches[i] == 0 for i in range(len(batches) - 1))
+    assert batches[0] < batches[-1]            # conv batch capped below the FC batch
+    x = synth.conv_inputs(K, 227, 3, seed=1)
+    s_plan = np.zeros((K, 1000), np.float32)
+    m.infer(x, K, s_plan, on_device=False)
+    m.set_plan([K] * len(batches))
+    s_fix = np.zeros((K, 1000), np.float32)
+    m.infer(x, K, s_fix, on_device=False)
+    assert rel_err(s_plan, s_fix) <= 1e-4
+    m.close()
