@@ -209,17 +209,26 @@ __global__ void k_im2col(const float* __restrict__ x, int B, int H, int W, int C
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(f[j]);
     } else {
+      // one (c, s, r) decomposition per thread, then incremental steps
+      int c = k0 % cg, rs = k0 / cg;
+      int sx = rs % kw, r = rs / kw;
+      const float* xb = x + (size_t)b * H * W * C + c0;
+      const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int k = k0 + j;
         float f = 0.f;
-        if (k < Kreal) {
-          const int c = k % cg, rs = k / cg;
-          const int s = rs % kw, r = rs / kw;
-          const int ih = oh * stride - pad + r, iw = ow * stride - pad + s;
-          if (ih >= 0 && ih < H && iw >= 0 && iw < W) f = x[(((size_t)b * H + ih) * W + iw) * C + c0 + c];
+        if (k0 + j < Kreal) {
+          const int ih = ih0 + r, iw = iw0 + sx;
+          if (ih >= 0 && ih < H && iw >= 0 && iw < W) f = __ldg(xb + ((size_t)ih * W + iw) * C + c);
         }
         v[j] = __float2bfloat16_rn(f);
+        if (++c == cg) {
+          c = 0;
+          if (++sx == kw) {
+            sx = 0;
+            ++r;
+          }
+        }
       }
     }
     *reinterpret_cast<uint4*>(out + pos * Kpad + k0) = *reinterpret_cast<const uint4*>(v);
@@ -236,7 +245,8 @@ __global__ void k_lrn(const float* __restrict__ x, long npos, int C, float* __re
     float s = 0.f;
     const int lo = max(0, c - 2), hi = min(C - 1, c + 2);
     for (int q = lo; q <= hi; ++q) s = fmaf(px[q], px[q], s);
-    y[i] = px[c] * powf(2.0f + (1e-4f / 5.0f) * s, -0.75f);
+    // base in [2, 2 + 2e-5 * sum a^2]: exp2/log2 intrinsics are ~1e-7 relative here
+    y[i] = px[c] * exp2f(-0.75f * __log2f(2.0f + (1e-4f / 5.0f) * s));
   }
 }
 
