@@ -174,12 +174,16 @@ cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int 
                                float* out, int ldo, void* stream);
 
 /* ---- FC kernel policy (tuning / parity hook) ---------------------------
- * band_min_batch: batches B >= this run the warp-specialised large-batch band
- * kernel (when x meets its alignment rule: ldx % 4 == 0, ldx >= B rounded up
- * to 4, x 16-byte aligned), smaller ones the lane-parallel small-batch kernel.
- * <= 0 restores the default (env CDN_BAND_MIN_B, else 16).  Both kernels
- * compute the same layer; only the summation order differs.  Errors: CDN_E_ARG. */
-cdn_status cdn_model_set_kernel_policy(cdn_model* m, int band_min_batch);
+ * tc_min_batch: batches B >= this run the tensor-core kernel (W tiles decoded
+ * into shared memory, 3-pass bf16 split tcgen05 contraction, fp32 accumulate);
+ * band_min_batch: batches B >= this (and below tc_min_batch) run the
+ * warp-specialised CUDA-core band kernel (when x meets its TMA alignment rule:
+ * ldx % 4 == 0, x 16-byte aligned); smaller batches the small-batch kernels.
+ * <= 0 restores a default (env CDN_TC_MIN_B else off; env CDN_BAND_MIN_B else
+ * 16).  All kernels compute the same layer; they differ in summation order and,
+ * for the tensor-core kernel, in the 2^-16-level split of operands
+ * (DESIGN.md §9).  Errors: CDN_E_ARG. */
+cdn_status cdn_model_set_kernel_policy(cdn_model* m, int band_min_batch, int tc_min_batch);
 
 /* ---- decode only (parity hook, kernel K2) -------------------------------
  * Writes every token of this rank's rows in row-major token order, pads

@@ -80,7 +80,7 @@ _SIGS = {
                                       C.c_void_p]),
     "cdn_layer_decode": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.POINTER(C.c_uint64), C.c_void_p]),
-    "cdn_model_set_kernel_policy": (C.c_int32, [C.c_void_p, C.c_int]),
+    "cdn_model_set_kernel_policy": (C.c_int32, [C.c_void_p, C.c_int, C.c_int]),
     "cdn_conv_forward": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "cdn_layer_out_shape": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                         C.POINTER(C.c_int)]),
@@ -262,9 +262,9 @@ class Model:
         _check(self._lib.cdn_layer_out_shape(self._h, layer, C.byref(h), C.byref(w), C.byref(c)))
         return h.value, w.value, c.value
 
-    def set_kernel_policy(self, band_min_batch: int = 0):
-        """B >= band_min_batch -> large-batch band kernel (0: library default)."""
-        _check(self._lib.cdn_model_set_kernel_policy(self._h, int(band_min_batch)))
+    def set_kernel_policy(self, band_min_batch: int = 0, tc_min_batch: int = 0):
+        """B >= tc_min_batch -> tensor-core kernel; B >= band_min_batch -> band kernel (0: defaults)."""
+        _check(self._lib.cdn_model_set_kernel_policy(self._h, int(band_min_batch), int(tc_min_batch)))
 
     def decode_count(self, layer: int) -> int:
         n = C.c_uint64()

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcdn.so")
-SOURCES = ["host.cpp", "kernels.cu", "band.cu", "small.cu", "conv.cu", "api.cpp"]
+SOURCES = ["host.cpp", "kernels.cu", "band.cu", "small.cu", "tc.cu", "conv.cu", "api.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -77,7 +77,9 @@ struct Layer {
   FcDev dev;
   DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias, flut, ctr;
   DBuf ivg, ivm;        // band-kernel interval restart index
+  DBuf tivg, tivm;      // tensor-core kernel Wi = 64 index (when ivg/ivm use another width)
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
+  DBuf tctr;            // tensor-core kernel arrival counters
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
@@ -106,6 +108,8 @@ struct Model {
   DBuf ctmp;                    // conv -> FC boundary: image-major conv output of one phase
   bool busy = false;
   int band_min = 0;             // cdn_model_set_kernel_policy (0: default)
+  int tc_min = 0;               // cdn_model_set_kernel_policy tensor-core threshold (0: default)
+  DBuf tc_xh, tc_xl;            // tensor-core FC: bf16 hi / lo split of the activations
 };
 
 uint32_t rows_per_rank(uint32_t rows, int world) { return (rows + world - 1) / world; }
@@ -303,6 +307,23 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     L.dev.Wi = (int)Wi;
     L.dev.NI = (int)iv.NI;
     L.dev.Cint = cint;
+    // the tensor-core kernel's K tile is 64 columns: reuse or build a Wi = 64 index
+    if (Wi == 64) {
+      L.dev.tNI = (int)iv.NI;
+    } else if (!conv) {
+      IntervalIndex t64;
+      build_interval_index(H, L.row0, L.row1, 64, t64);
+      std::vector<uint32_t> tg(2 * t64.v.size());
+      std::vector<uint16_t> tm(t64.v.size());
+      for (size_t q = 0; q < t64.v.size(); ++q) {
+        tg[2 * q] = (uint32_t)(t64.v[q] - vbase);
+        tg[2 * q + 1] = (uint32_t)(t64.g[q] - gbase);
+        tm[q] = (uint16_t)(t64.dm1[q] | ((uint16_t)t64.nnz[q] << 8));
+      }
+      L.tivg.upload(tg);
+      L.tivm.upload(tm);
+      L.dev.tNI = (int)t64.NI;
+    }
   }
   const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
   const int Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
@@ -371,6 +392,8 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.Lpg = pad_glen;
   f.msv = L.msv.p ? L.msv.as<uint32_t>() : nullptr;
   f.msg = L.msg.p ? L.msg.as<uint32_t>() : nullptr;
+  f.tivg = L.tivg.p ? L.tivg.as<uint2>() : (L.dev.Wi == 64 ? L.ivg.as<uint2>() : nullptr);
+  f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : (L.dev.Wi == 64 ? L.ivm.as<uint16_t>() : nullptr);
   f.ivg = L.ivg.as<uint2>();
   f.ivm = L.ivm.as<uint16_t>();
 
@@ -405,6 +428,17 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
 
 cudaStream_t pick(Model& m, void* s) { return s ? (cudaStream_t)s : m.stream; }
 
+// The tensor-core FC kernel is correct and parity-tested but, measured on B200,
+// still decode-bound and slower than the band kernel on C1-C5,
+// so it is opt-in: env CDN_TC_MIN_B or cdn_model_set_kernel_policy.
+int tc_min_batch() {
+  static int v = [] {
+    const char* e = std::getenv("CDN_TC_MIN_B");
+    return e ? std::max(1, std::atoi(e)) : (1 << 30);
+  }();
+  return v;
+}
+
 int band_min_batch() {
   static int v = [] {
     const char* e = std::getenv("CDN_BAND_MIN_B");
@@ -417,6 +451,23 @@ int band_min_batch() {
 // batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
 void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s) {
   const int relu = L.desc.relu;
+  const int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
+  if (B >= tcmin && tc_supported(L.dev)) {
+    TcPlan p = plan_fc_tc(L.dev, B, m.num_sms);
+    if (p.ok) {
+      m.tc_xh.alloc(p.xsplit_elems * 2);
+      m.tc_xl.alloc(p.xsplit_elems * 2);
+      if (p.ws_floats) L.bws.alloc(p.ws_floats * sizeof(float));
+      const size_t need = sizeof(int) * (size_t)p.tiles;
+      if (L.tctr.n < need || !L.tctr.p) {
+        L.tctr.alloc(need);
+        CUDA_OK(cudaMemsetAsync(L.tctr.p, 0, need, s));
+      }
+      CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<__nv_bfloat16*>(m.tc_xh.p),
+                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), L.tctr.as<int>(), s));
+      return;
+    }
+  }
   if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
     BandPlan p = plan_fc_band(L.dev, x, ldx, B, m.num_sms);
     if (p.ok) {
@@ -875,9 +926,10 @@ cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int 
   API_END
 }
 
-cdn_status cdn_model_set_kernel_policy(cdn_model* h, int band_min_batch) {
+cdn_status cdn_model_set_kernel_policy(cdn_model* h, int band_min_batch, int tc_min_batch) {
   if (!h) return fail(CDN_E_ARG, "NULL model");
   h->m.band_min = band_min_batch > 0 ? band_min_batch : 0;
+  h->m.tc_min = tc_min_batch > 0 ? tc_min_batch : 0;
   h->m.prof_bmax = 0;  // Time(i,B) depends on the policy
   return CDN_OK;
 }

@@ -41,6 +41,11 @@ struct FcDev {
   const uint16_t* ivm = nullptr;
   int Wi = 64, NI = 0;               // interval width (= band width), intervals per row
   int Cint = 16;                     // intervals per decode chunk
+  // tensor-core FC kernel (tc.cu): interval index with Wi = 64 (the K tile);
+  // aliases ivg/ivm when the band index already uses Wi = 64
+  const uint2* tivg = nullptr;
+  const uint16_t* tivm = nullptr;
+  int tNI = 0;
   // small-batch multi-symbol LUTs (small.cu): 2^msLv / 2^msLg entries
   const uint32_t* msv = nullptr;
   const uint32_t* msg = nullptr;
@@ -57,6 +62,18 @@ struct BandPlan {
 BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms);
 cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, int ldx, int B, float* y, int ldy,
                            int relu, float* ws, int* tctr, cudaStream_t s);
+// Tensor-core FC kernel (tc.cu, B >= ~128): decode W tiles into shared memory,
+// 3-pass bf16 split tcgen05 contraction.  xh/xl: bf16 scratch [B][ldk].
+struct TcPlan {
+  bool ok = false;
+  int nbt = 1, nrt = 1, nkt = 0, ldk = 0, S = 1, tiles = 0, units = 0, grid = 0;
+  size_t ws_floats = 0, xsplit_elems = 0, smem = 0;
+};
+bool tc_supported(const FcDev& L);
+TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms);
+cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
+                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, int* tctr, cudaStream_t s);
+
 // Small-batch multi-symbol kernel (B <= 8; r <= 5, k <= 4, 32-bit lane records).
 bool ms_supported(const FcDev& L);
 cudaError_t launch_fc_ms(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu, cudaStream_t s,

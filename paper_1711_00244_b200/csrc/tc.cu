@@ -1,0 +1,484 @@
+// Tensor-core FC kernel for large batches, sm_100a:
+// parallel Huffman decode -> gap prefix sum -> codebook dequantize straight
+// into shared-memory weight tiles -> tcgen05 contraction with the batch tile,
+// PAPER.md Alg. 1 lines 4-9, Eq. 1-2.
+//
+// At B >= 128 the sparse CUDA-core kernel is bound by one shared-memory load
+// per FMA; the tensor cores run the DENSE tile product 25x faster per flop than
+// the CUDA cores, so even at 4% density they win.  fp32 fidelity with bf16
+// tensor cores: every weight (codebook value) and activation is split into
+// hi = bf16(v) and lo = bf16(v - hi); D += Whi*Xhi + Whi*Xlo + Wlo*Xhi (three
+// UMMAs per K step; the dropped Wlo*Xlo term and the two splits are each
+// <= 2^-16 relative per product).
+//
+//   unit = (128 output rows, 256 images, K range); per 64-column K tile:
+//     * 4 DECODE warps, one lane per row: the interval index (Wi = 64) gives
+//       the row's decoder state at the tile start and its real-token count;
+//       the lane zero-fills its 128-byte row of the hi and lo tiles, decodes
+//       (pad-folding LUT), and writes bf16 hi/lo of C[sym] at column c - k0 in
+//       the K-major 128B-swizzled UMMA layout; fence.proxy.async, arrive;
+//     * warp 0 / lane 0: TMA of the Xhi / Xlo tiles [256 images][64 K];
+//     * warp 1 / lane 0: 12 x tcgen05.mma.cta_group::1.kind::f16 (M=128,
+//       N=256, K=16) into a TMEM fp32 accumulator, commit frees the stage;
+//     * 4 EPILOGUE warps: tcgen05.ld -> + bias -> ReLU -> y (or a K-split
+//       partial, reduced in fixed order by the last CTA of the tile).
+// Decoded weights live only in shared memory (never in HBM).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "dev_common.cuh"
+#include "kernels.cuh"
+#include "tc_common.cuh"
+#include "tmap.hpp"
+
+namespace cdn {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kTM = 128;            // rows per unit (UMMA M)
+constexpr int kTN = 256;            // images per unit (UMMA N)
+constexpr int kTK = 64;             // K tile (= interval width of the TC index)
+constexpr int kTStages = 2;
+constexpr int kWTile = kTM * kTK * 2;   // 16 KB bf16
+constexpr int kXTile = kTN * kTK * 2;   // 32 KB bf16
+constexpr int kStageBytes = 2 * kWTile + 2 * kXTile;  // hi + lo of both operands: 96 KB
+constexpr int kDecW = 4;            // decode warps (one lane per row)
+constexpr int kEpiW = 4;            // epilogue warps
+constexpr int kTThreads = (2 + kDecW + kEpiW) * 32;   // 320
+constexpr int kEpiBar = 1;
+
+struct TcArgs {
+  float* y;
+  int ldy, B, relu;
+  float* ws;   // [tiles][S][128][256] partials (S > 1)
+  int* tctr;   // [tiles]
+  int S, nbt, nrt, units, nkt;  // splits, batch tiles, row tiles, units, K tiles
+};
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// byte offset of element (r, k) in a K-major, 128B-swizzled [rows][64] bf16 tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int k) {
+  return (uint32_t)(r * 128 + ((((k >> 3) ^ (r & 7))) << 4) + ((k & 7) << 1));
+}
+
+struct TUnit {
+  int rt, bt, sp, kt0, kt1, tile;
+};
+
+__device__ __forceinline__ TUnit tunit(const TcArgs& a, int u) {
+  TUnit t;
+  t.sp = u % a.S;
+  t.tile = u / a.S;
+  t.rt = t.tile / a.nbt;
+  t.bt = t.tile % a.nbt;
+  t.kt0 = (int)(((long)t.sp * a.nkt) / a.S);
+  t.kt1 = (int)(((long)(t.sp + 1) * a.nkt) / a.S);
+  return t;
+}
+
+struct DReader {  // task-local MSB-first reader (3 words up front)
+  const uint32_t* p;
+  uint32_t off, w0, w1, w2;
+  __device__ __forceinline__ void init(const uint32_t* words, uint32_t bit) {
+    p = words + (bit >> 5);
+    off = bit & 31;
+    w0 = ldg_u32(p);
+    w1 = ldg_u32(p + 1);
+    w2 = ldg_u32(p + 2);
+    p += 3;
+  }
+  __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
+  __device__ __forceinline__ void skip(uint32_t n) {
+    off += n;
+    if (off >= 32) {
+      off -= 32;
+      w0 = w1;
+      w1 = w2;
+      w2 = ldg_u32(p);
+      ++p;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kTThreads, 1)
+    k_fc_tc(FcDev L, TcArgs a, const __grid_constant__ CUtensorMap txh, const __grid_constant__ CUtensorMap txl) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* stages = smem;  // [stage]{Whi, Wlo, Xhi, Xlo}
+  unsigned char* rings = smem + kTStages * kStageBytes;  // decoder stream rings [dwarp][stream][4][32][16B]
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(rings + kDecW * 2 * 2048);
+  uint64_t* xfull = wfull + kTStages;
+  uint64_t* sempty = xfull + kTStages;
+  uint64_t* tfull = sempty + kTStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  uint32_t* s_cbs = reinterpret_cast<uint32_t*>(s_last + 3);  // [ncb] bf16 hi | lo << 16
+  uint32_t* s_flut = s_cbs + 256;
+  uint32_t* s_glut = s_flut + (1 << L.Lf);
+  uint32_t* s_vtab = s_glut + (1 << L.Lg);
+  uint32_t* s_gtab = s_vtab + 99;
+  uint16_t* s_vsorted = reinterpret_cast<uint16_t*>(s_gtab + 99);
+  uint16_t* s_gsorted = s_vsorted + (L.nvs + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < (1 << L.Lf); i += nt) s_flut[i] = L.flut[i];
+    for (int i = tid; i < (1 << L.Lg); i += nt) s_glut[i] = L.glut[i];
+    for (int i = tid; i < L.ncb; i += nt) {
+      const float w = L.codebook[i];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
+      s_cbs[i] = (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+    }
+    for (int i = tid; i < 99; i += nt) { s_vtab[i] = L.vtab[i]; s_gtab[i] = L.gtab[i]; }
+    for (int i = tid; i < L.nvs; i += nt) s_vsorted[i] = L.vsorted[i];
+    for (int i = tid; i < L.ngs; i += nt) s_gsorted[i] = L.gsorted[i];
+    if (tid == 0) {
+      for (int s = 0; s < kTStages; ++s) {
+        mbar_init(&wfull[s], kDecW);
+        mbar_init(&xfull[s], 1);
+        mbar_init(&sempty[s], 1);
+      }
+      mbar_init(tfull, 1);
+      mbar_init(tempty, kEpiW);
+      mbar_fence_init();
+    }
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                   "n"(kTN)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- X tile producer
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+        const TUnit t = tunit(a, u);
+        for (int kt = t.kt0; kt < t.kt1; ++kt, ++g) {
+          const int s = g % kTStages;
+          mbar_wait(&sempty[s], ((g / kTStages) & 1) ^ 1);
+          unsigned char* st = stages + s * kStageBytes;
+          mbar_arrive_expect_tx(&xfull[s], 2 * kXTile);
+          tma2d(st + 2 * kWTile, &txh, kt * kTK, t.bt * kTN, &xfull[s]);
+          tma2d(st + 2 * kWTile + kXTile, &txl, kt * kTK, t.bt * kTN, &xfull[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
+                             ((uint32_t)(kTM >> 4) << 24);
+      uint32_t g = 0, uc = 0;
+      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
+        const TUnit t = tunit(a, u);
+        mbar_wait(tempty, (uc & 1) ^ 1);  // the epilogue drained the accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kt = t.kt0; kt < t.kt1; ++kt, ++g) {
+          const int s = g % kTStages;
+          const uint32_t ph = (g / kTStages) & 1;
+          mbar_wait(&wfull[s], ph);
+          mbar_wait(&xfull[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          unsigned char* st = stages + s * kStageBytes;
+          const uint64_t wh = sw128_desc(smem_addr(st)), wl = sw128_desc(smem_addr(st + kWTile));
+          const uint64_t xh = sw128_desc(smem_addr(st + 2 * kWTile)),
+                         xl = sw128_desc(smem_addr(st + 2 * kWTile + kXTile));
+#pragma unroll
+          for (int k = 0; k < kTK / 16; ++k) {
+            const uint32_t first = (kt == t.kt0 && k == 0) ? 0u : 1u;
+            umma_bf16(tmem, wh + 2 * k, xh + 2 * k, idesc, first);
+            umma_bf16(tmem, wh + 2 * k, xl + 2 * k, idesc, 1u);
+            umma_bf16(tmem, wl + 2 * k, xh + 2 * k, idesc, 1u);
+          }
+          umma_commit(&sempty[s]);
+        }
+        if (t.kt1 <= t.kt0) {  // empty K range: the partial is zero
+          // no MMA ran; the epilogue is told through tfull with a zero flag below
+        }
+        umma_commit(tfull);
+      }
+    }
+  } else if (warp < 2 + kDecW) {
+    // ------------------------------------------------------------ decode warps
+    // one lane per row; the decoder state is carried from K tile to K tile (the
+    // index gives the state only at the unit start, and the real-token count of
+    // every tile, prefetched one tile ahead)
+    const int dw = warp - 2;
+    const int row_l = dw * 32 + lane;
+    const int fsh = 32 - L.Lf, gsh = 32 - L.Lg, kk = L.k;
+    uint32_t g = 0;
+    for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+      const TUnit t = tunit(a, u);
+      const int row = t.rt * kTM + row_l;
+      const bool active = row < L.nrows;
+      RReader vr, gr;  // stream words arrive through a cp.async ring in shared memory
+      int col = 0;
+      uint32_t mnext = 0;
+      const uint16_t* mrow = L.tivm + (size_t)(active ? row : 0) * L.tNI;
+      if (active && t.kt1 > t.kt0) {
+        const size_t q = (size_t)row * L.tNI + t.kt0;
+        const uint2 st = L.tivg[q];
+        const uint32_t m0 = L.tivm[q];
+        cp_async_wait<0>();  // the previous unit's read-ahead lands before the ring is reused
+        const uint32_t rbase = smem_addr(rings) + (uint32_t)dw * 4096 + (uint32_t)lane * 16;
+        vr.start(L.vw, rbase, st.x);
+        gr.start(L.gw, rbase + 2048, st.y);
+        cp_async_wait<0>();
+        vr.fill_done();
+        gr.fill_done();
+        col = t.kt0 * kTK - (int)(m0 & 0xFFu) - 1;
+        mnext = m0;
+      }
+      for (int kt = t.kt0; kt < t.kt1; ++kt, ++g) {
+        const uint32_t m = mnext;
+        if (active && kt + 1 < t.kt1) mnext = mrow[kt + 1];  // next tile's count, in flight meanwhile
+        const int s = g % kTStages;
+        mbar_wait(&sempty[s], ((g / kTStages) & 1) ^ 1);
+        unsigned char* wh = stages + s * kStageBytes;
+        unsigned char* wl = wh + kWTile;
+        // zero this warp's 32 rows (4 KB contiguous per tile), conflict-free
+        {
+          uint4* zh = reinterpret_cast<uint4*>(wh + dw * 4096);
+          uint4* zl = reinterpret_cast<uint4*>(wl + dw * 4096);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            zh[c * 32 + lane] = make_uint4(0, 0, 0, 0);
+            zl[c * 32 + lane] = make_uint4(0, 0, 0, 0);
+          }
+        }
+        __syncwarp();
+        const uint32_t nnz = active ? (m >> 8) : 0u;
+        const int k0 = kt * kTK;
+        uint32_t done = 0;
+        while (done < nnz) {
+          const uint32_t w = vr.peek();
+          const uint32_t e = s_flut[w >> fsh];
+          uint32_t len, sym, pads, pbits;
+          if (e != kFoldSlow) {
+            len = e >> 28;
+            sym = e & 0xFFu;
+            pads = (e >> 24) & 15u;
+            pbits = (e >> 8) & 0xFFFFu;
+          } else {
+            const uint32_t r = slow_sym(w, L.Lf + 1, s_vtab, s_vsorted, L.vmax);
+            len = r >> 16;
+            sym = r & 0xFFu;
+            pads = sym == 0;
+            pbits = pads ? (uint32_t)L.Lpg : 0u;
+          }
+          vr.skip(len);
+          col += (int)(pads << kk);
+          if (pbits <= 32) {
+            gr.skip(pbits);
+          } else {
+            for (uint32_t z = 0; z < pads; ++z) gr.skip((uint32_t)L.Lpg);
+          }
+          if (sym) {
+            const uint32_t gwin = gr.peek();
+            uint32_t ge = s_glut[gwin >> gsh];
+            if (ge == 0) ge = slow_sym(gwin, L.Lg + 1, s_gtab, s_gsorted, L.gmax);
+            gr.skip(ge >> 16);
+            col += (int)(ge & 0xFFFFu) + 1;
+            const uint32_t hl = s_cbs[sym];
+            const uint32_t off = sw128_off(row_l, col - k0);
+            *reinterpret_cast<uint16_t*>(wh + off) = (uint16_t)(hl & 0xFFFFu);
+            *reinterpret_cast<uint16_t*>(wl + off) = (uint16_t)(hl >> 16);
+            ++done;
+          }
+        }
+        fence_proxy_async_smem();  // generic-proxy tile writes -> tensor-core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wfull[s]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue warps
+    const int ew = warp - (2 + kDecW);
+    const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_l = q4 * 32 + lane;
+    uint32_t uc = 0;
+    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
+      const TUnit t = tunit(a, u);
+      mbar_wait(tfull, uc & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = t.rt * kTM + row_l;
+      const int b0 = t.bt * kTN;
+      const bool has = t.kt1 > t.kt0;
+      float* dst;
+      size_t ld;
+      if (a.S == 1) {
+        dst = a.y + (size_t)row * a.ldy + b0;
+        ld = a.ldy;
+      } else {
+        dst = a.ws + (((size_t)t.tile * a.S + t.sp) * kTM + row_l) * kTN;
+        ld = kTN;
+      }
+      (void)ld;
+      const float bias = (a.S == 1 && row < L.nrows) ? L.bias[row] : 0.f;
+      for (int c = 0; c < kTN; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c, v);
+        if (!has) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (a.S == 1) {
+          if (row < L.nrows) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (b0 + c + i < a.B) {
+                float o = v[i] + bias;
+                if (a.relu) o = fmaxf(o, 0.f);
+                dst[c + i] = o;
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            __stcg(reinterpret_cast<float4*>(dst + c + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      if (a.S > 1) {
+        __threadfence();
+        named_bar_sync(kEpiBar, kEpiW * 32);
+        if (ew == 0 && lane == 0) {
+          const int old = atomicAdd(&a.tctr[t.tile], 1);
+          const int is_last = old == a.S - 1;
+          if (is_last) a.tctr[t.tile] = 0;
+          s_last[0] = is_last;
+        }
+        named_bar_sync(kEpiBar, kEpiW * 32);
+        if (s_last[0] && row < L.nrows) {
+          __threadfence();
+          const float bias2 = L.bias[row];
+          const float* base = a.ws + ((size_t)t.tile * a.S * kTM + row_l) * kTN;
+          float* yp = a.y + (size_t)row * a.ldy + b0;
+          for (int c = 0; c < kTN; c += 4) {
+            float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < a.S; ++j) {
+              const float4 p = __ldcg(reinterpret_cast<const float4*>(base + (size_t)j * kTM * kTN + c));
+              sum.x += p.x; sum.y += p.y; sum.z += p.z; sum.w += p.w;
+            }
+            const float o4[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (b0 + c + i < a.B) {
+                float o = o4[i] + bias2;
+                if (a.relu) o = fmaxf(o, 0.f);
+                yp[c + i] = o;
+              }
+            }
+          }
+        }
+        named_bar_sync(kEpiBar, kEpiW * 32);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTN) : "memory");
+}
+
+// X fp32 feature-major [K][ldx] -> bf16 hi / lo image-major [B][ldk] (K contiguous)
+__global__ void k_split_x(const float* __restrict__ x, int K, int ldx, int B, __nv_bfloat16* __restrict__ xh,
+                          __nv_bfloat16* __restrict__ xl, int ldk) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, b = b0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && b < B) ? x[(size_t)k * ldx + b] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int b = b0 + i, k = k0 + threadIdx.x;
+    if (b < B && k < ldk) {
+      const float v = tile[threadIdx.x][i];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      xh[(size_t)b * ldk + k] = hi;
+      xl[(size_t)b * ldk + k] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
+  }
+}
+
+size_t tc_smem_bytes(const FcDev& L) {
+  size_t b = 1024 + (size_t)kTStages * kStageBytes + kDecW * 2 * 2048 + 8 * (3 * kTStages + 2) + 16;
+  b += 4 * 256 + (4u << L.Lf) + (4u << L.Lg) + 2 * 99 * 4 + 2 * (L.nvs + 1) + 2 * (L.ngs + 1);
+  return (b + 127) & ~(size_t)127;
+}
+
+}  // namespace
+
+bool tc_supported(const FcDev& L) { return L.tivg && L.tivm && L.tNI > 0 && L.ncb <= 256; }
+
+TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
+  TcPlan p;
+  if (!tc_supported(L) || B <= 0) return p;
+  p.nbt = (B + kTN - 1) / kTN;
+  p.nrt = (L.nrows + kTM - 1) / kTM;
+  p.nkt = L.tNI;
+  p.ldk = (L.cols + 7) & ~7;
+  const int tiles = p.nrt * p.nbt;
+  double best = 1e30;
+  int bestS = 1;
+  const int smax = p.nkt < 64 ? p.nkt : 64;
+  for (int S = 1; S <= smax; ++S) {
+    const long units = (long)tiles * S;
+    const long waves = (units + num_sms - 1) / num_sms;
+    const double cost = (double)waves / S * (1.0 + 0.02 * (S - 1));
+    if (cost < best * 0.98) { best = cost; bestS = S; }
+  }
+  p.S = bestS;
+  p.tiles = tiles;
+  p.units = tiles * p.S;
+  p.grid = p.units < num_sms ? p.units : num_sms;
+  p.ws_floats = p.S > 1 ? (size_t)tiles * p.S * kTM * kTN : 0;
+  p.xsplit_elems = (size_t)B * p.ldk;
+  p.smem = tc_smem_bytes(L);
+  p.ok = p.smem <= 227 * 1024;  // (LUT sizes vary per layer)
+  return p;
+}
+
+cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
+                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, int* tctr, cudaStream_t s) {
+  dim3 sg((p.ldk + 31) / 32, (B + 31) / 32), sb(32, 8);
+  k_split_x<<<sg, sb, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap th, tl;
+  e = encode_tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xh, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
+                     kTK, kTN, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  e = encode_tmap_2d(&tl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xl, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
+                     kTK, kTN, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  static size_t set_smem = 0;
+  if (p.smem > set_smem) {
+    e = cudaFuncSetAttribute(k_fc_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (e != cudaSuccess) return e;
+    set_smem = p.smem;
+  }
+  TcArgs a{y, ldy, B, relu, ws, tctr, p.S, p.nbt, p.nrt, p.units, p.nkt};
+  k_fc_tc<<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
+  return cudaGetLastError();
+}
+
+}  // namespace cdn

@@ -285,7 +285,7 @@ def sparse_q(c):
     return sp.csr_matrix((vals, (r, col)), shape=c.mask.shape)
 
 
-def check_forward_sparse(torch, dev, m, c, bias, a, relu):
+def check_forward_sparse(torch, dev, m, c, bias, a, relu, split_bf16=False):
     y = gpu_forward(torch, dev, m, a, c.layer.rows)
     Wq = sparse_q(c)
     ref = infer.fc_forward(Wq, a, bias, apply_relu=relu)
@@ -295,7 +295,10 @@ def check_forward_sparse(torch, dev, m, c, bias, a, relu):
     scale = infer.fc_abs_scale(Wq, a, bias)
     kmax = max(1, int(c.row_tokens.max()))
     elem = (np.abs(y - ref) / np.maximum(scale, 1e-30)).max()
-    assert elem <= 2 * kmax * 2.0 ** -24 + 1e-12, elem
+    # fp32 accumulation bound; the tensor-core kernel adds the 3-pass bf16 split
+    # error (each product within 2^-15 relative)
+    bound = 2 * kmax * 2.0 ** -24 + (2.0 ** -15 if split_bf16 else 0.0) + 1e-12
+    assert elem <= bound, elem
     return e
 
 
@@ -312,7 +315,7 @@ def test_band_forward_configs(torch_dev, cfg, i, B):
     torch, dev = torch_dev
     spec, c, buf = config_layer(cfg, i)
     m = make_model(torch, buf, relu=spec.relu)
-    m.set_kernel_policy(1)
+    m.set_kernel_policy(1, 1 << 30)   # band kernel (tensor-core path off)
     _, v = synth.fc_weights(spec, synth.CONFIGS[cfg].seed)
     a = synth.fc_inputs(spec.cols, B, synth.CONFIGS[cfg].seed)
     check_forward_sparse(torch, dev, m, c, v, a, relu=spec.relu)
@@ -329,7 +332,7 @@ def test_band_edge_fixtures(torch_dev, name, rows, cols, d, r, k, scale, B):
     v = synth.random_matrix(1, rows, seed=7).ravel()
     c, buf = oracle_layer(name, W, d, r, k, v)
     m = make_model(torch, buf)
-    m.set_kernel_policy(1)
+    m.set_kernel_policy(1, 1 << 30)   # band kernel (tensor-core path off)
     a = synth.random_activations(cols, B, seed=B + 100)
     check_forward(torch, dev, m, c, v, a, relu=False)
 
@@ -346,7 +349,7 @@ def test_band_list_overflow_repeats_band(torch_dev):
     c, buf = oracle_layer("skewed_rows", W, 0.05, 5, 4, v)
     assert c.mask[::37].mean() > 0.9    # those rows survive pruning almost whole
     m = make_model(torch, buf, relu=True)
-    m.set_kernel_policy(1)
+    m.set_kernel_policy(1, 1 << 30)   # band kernel (tensor-core path off)
     for B in (8, 64, 128):
         a = synth.random_activations(cols, B, seed=B)
         check_forward(torch, dev, m, c, v, a, relu=True)
@@ -358,9 +361,9 @@ def test_band_and_small_kernels_agree(torch_dev):
     spec, c, buf = config_layer("C2", 0)
     a = synth.fc_inputs(spec.cols, 24, 0)
     m1 = make_model(torch, buf)
-    m1.set_kernel_policy(1000)          # small-batch kernel
+    m1.set_kernel_policy(1000, 1 << 30)  # small-batch kernel
     m2 = make_model(torch, buf)
-    m2.set_kernel_policy(1)             # band kernel
+    m2.set_kernel_policy(1, 1 << 30)     # band kernel
     y1 = gpu_forward(torch, dev, m1, a, spec.rows)
     y2 = gpu_forward(torch, dev, m2, a, spec.rows)
     assert rel_err(y2, y1) <= 2e-6
@@ -422,3 +425,34 @@ def test_c3_planner_under_64mib_budget(torch_dev):
         x = infer.fc_forward(sparse_q(c), x, v, apply_relu=relu).astype(np.float32)
     assert rel_err(scores, x) <= TOL
     m.close()
+
+
+# ------------------------------------------- tensor-core FC kernel (NEXT #2)
+
+TC_CASES = [("C5", 0, 512), ("C5", 0, 300), ("C5", 1, 256), ("C5", 2, 512), ("C5", 2, 130), ("C2", 0, 128),
+            ("C3", 2, 384), ("C1", 0, 256), ("C1", 0, 17)]
+
+
+@pytest.mark.parametrize("cfg,i,B", TC_CASES)
+def test_tc_forward_configs(torch_dev, cfg, i, B):
+    """W tiles decoded into shared memory + 3-pass bf16-split tcgen05
+    contraction (K-split partials, ragged row / batch / K tiles) vs the oracle."""
+    torch, dev = torch_dev
+    spec, c, buf = config_layer(cfg, i)
+    m = make_model(torch, buf, relu=spec.relu)
+    m.set_kernel_policy(1, 1)
+    _, v = synth.fc_weights(spec, synth.CONFIGS[cfg].seed)
+    a = synth.fc_inputs(spec.cols, B, synth.CONFIGS[cfg].seed)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=spec.relu, split_bf16=True)
+
+
+@pytest.mark.parametrize("name,rows,cols,d,r,k,scale", EDGE)
+def test_tc_edge_fixtures(torch_dev, name, rows, cols, d, r, k, scale):
+    torch, dev = torch_dev
+    W = synth.random_matrix(rows, cols, seed=zlib.crc32(name.encode()) % 1000, scale=scale)
+    v = synth.random_matrix(1, rows, seed=7).ravel()
+    c, buf = oracle_layer(name, W, d, r, k, v)
+    m = make_model(torch, buf)
+    m.set_kernel_policy(1, 1)
+    a = synth.random_activations(cols, 36, seed=99)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=False, split_bf16=True)
