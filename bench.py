@@ -236,8 +236,8 @@ def run_ours(args):
     else:
         roof = {"bound": "hbm", "achieved": bytes_algo / t_s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
-    roof["kernel"] = f"k_fc_forward ({specs[dom].name}, B={B})"
+    roof["kernel"] = f"k_fc_band<4> ({specs[dom].name}, B={B})"
+    roof["traffic"] = _traffic(roof["kernel"])
     roof["ms"] = lay_ms[dom]
     roof["peak_source"] = "MEASURED_PEAKS.json hbm_gbs / alu from 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"
 
@@ -282,6 +282,18 @@ def run_ours(args):
     m.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed `ncu --set full` capture (profiles/traffic.json,
+    written from the .ncu-rep named there); None if absent or for another kernel."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        e = t.get(kernel)
+        return None if e is None else e["dram_bytes"]
+    except Exception:
+        return None
 
 
 def bench_b1(cdn, torch, dev, layers, specs, R, flush, pk):
