@@ -109,6 +109,12 @@ __global__ void __launch_bounds__(kMsThreads, 4) k_fc_ms(FcDev L, const float* _
       ntok = (int)(L.tok_start[q + 1] - L.tok_start[q]);
       vr.init(L.vw, L.rp[2 * row] + vs - vlen);
       gr.init(L.gw, L.rp[2 * row + 1] + gs - glen);
+    } else {
+      // idle lane: the refill code still runs (uncommitted); keep the readers
+      // in a state whose skip(0) never loads
+      vr.p = L.vw;
+      vr.off = vr.w0 = vr.w1 = vr.n1 = vr.n2 = 0;
+      gr = vr;
     }
     float acc[BS];
 #pragma unroll
@@ -118,37 +124,35 @@ __global__ void __launch_bounds__(kMsThreads, 4) k_fc_ms(FcDev L, const float* _
     float pw[4] = {0.f, 0.f, 0.f, 0.f}, px[4] = {0.f, 0.f, 0.f, 0.f};  // pipelined products (BS == 1)
     const float* xcur = x + (ptrdiff_t)col * ldx;  // x row of the current column (BS == 1)
     while (__any_sync(0xffffffffu, ntok > 0)) {
-      if (ntok > 0) {
-        if (cv <= 8) {  // refill the symbol queue (up to 4 codes per lookup)
-          const uint32_t w = vr.peek();
-          uint32_t e = s_vl[w >> vsh];
-          uint32_t n = e & 7u, len = (e >> 3) & 31u;
-          uint64_t syms = e >> 8;
-          if (n == 0) {
-            const uint32_t r = slow_sym(w, L.msLv + 1, s_vtab, s_vsorted, L.vmax);
-            n = 1;
-            len = r >> 16;
-            syms = r & 31u;
-          }
-          qv |= syms << (5 * cv);
-          cv += (int)n;
-          vr.skip(len);
+      {  // refill the symbol queue (up to 4 codes per lookup); always look up, commit if room
+        const uint32_t w = vr.peek();
+        const uint32_t e = s_vl[w >> vsh];
+        uint32_t n = e & 7u, len = (e >> 3) & 31u, syms = e >> 8;
+        if (n == 0) {
+          const uint32_t r = slow_sym(w, L.msLv + 1, s_vtab, s_vsorted, L.vmax);
+          n = 1;
+          len = r >> 16;
+          syms = r & 31u;
         }
-        if (cg <= 10) {  // refill the gap queue (up to 6 codes per lookup)
-          const uint32_t w = gr.peek();
-          uint32_t e = s_gl[w >> gsh];
-          uint32_t n = e & 7u, len = (e >> 3) & 31u;
-          uint64_t gaps = e >> 8;
-          if (n == 0) {
-            const uint32_t r = slow_sym(w, L.msLg + 1, s_gtab, s_gsorted, L.gmax);
-            n = 1;
-            len = r >> 16;
-            gaps = r & 15u;
-          }
-          qg |= gaps << (4 * cg);
-          cg += (int)n;
-          gr.skip(len);
+        const bool room = cv <= 8 && ntok > 0;
+        qv |= (uint64_t)(room ? syms : 0u) << (5 * cv);
+        cv += room ? (int)n : 0;
+        vr.skip(room ? len : 0u);
+      }
+      {  // refill the gap queue (up to 6 codes per lookup)
+        const uint32_t w = gr.peek();
+        const uint32_t e = s_gl[w >> gsh];
+        uint32_t n = e & 7u, len = (e >> 3) & 31u, gaps = e >> 8;
+        if (n == 0) {
+          const uint32_t r = slow_sym(w, L.msLg + 1, s_gtab, s_gsorted, L.gmax);
+          n = 1;
+          len = r >> 16;
+          gaps = r & 15u;
         }
+        const bool room = cg <= 10 && ntok > 0;
+        qg |= (uint64_t)(room ? gaps : 0u) << (4 * cg);
+        cg += room ? (int)n : 0;
+        gr.skip(room ? len : 0u);
       }
       const int p = ntok > 0 ? min(min(cv, cg), min(ntok, 4)) : 0;
       if constexpr (BS == 1) {
@@ -156,11 +160,12 @@ __global__ void __launch_bounds__(kMsThreads, 4) k_fc_ms(FcDev L, const float* _
         // (whose x loads have had a whole decode step to arrive) first
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[0] = fmaf(pw[j], px[j], acc[0]);
+        const uint32_t qv32 = (uint32_t)qv, qg32 = (uint32_t)qg;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t sym = (uint32_t)(qv >> (5 * j)) & 31u;
+          const uint32_t sym = (qv32 >> (5 * j)) & 31u;
           const bool take = j < p;
-          xcur += take ? (int)(((qg >> (4 * j)) & 15u) + 1) * ldx : 0;
+          xcur += take ? (int)(((qg32 >> (4 * j)) & 15u) + 1) * ldx : 0;
           const bool use = take && sym != 0;
           float wv = 0.f, xv = 0.f;
           if (use) {  // predicated: xcur may sit one column before the row's first
