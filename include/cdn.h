@@ -200,6 +200,12 @@ cdn_status cdn_layer_stats_get(const cdn_model* m, int layer, cdn_layer_stats* o
  * time_ms[i*Bmax + (B-1)].  Errors: CDN_E_CUDA, CDN_E_STATE. */
 cdn_status cdn_model_profile(cdn_model* m, int Bmax, int reps, double* time_ms);
 
+/* ---- the planner's memory model for batches up to Bmax: per
+ * layer IN and OUT bytes per image and WS(i) bytes (readings C-23, C-24), the
+ * same numbers cdn_model_plan uses.  Arrays of n_layers.  Errors: CDN_E_ARG. */
+cdn_status cdn_model_memory_model(cdn_model* m, int Bmax, uint64_t* in_bytes, uint64_t* out_bytes,
+                                  uint64_t* ws_bytes);
+
 /* ---- host-only utilities (no device needed) ----------------------------- */
 
 /* Compress a dense fp32 row-major rows x cols matrix: magnitude

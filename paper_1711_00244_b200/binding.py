@@ -86,6 +86,7 @@ _SIGS = {
                                         C.POINTER(C.c_int)]),
     "cdn_debug_gemm_bf16": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p]),
+    "cdn_model_memory_model": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cdn_model_num_layers": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int)]),
     "cdn_layer_stats_get": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(LayerStats)]),
     "cdn_model_profile": (C.c_int32, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
@@ -261,6 +262,13 @@ class Model:
         h, w, c = C.c_int(), C.c_int(), C.c_int()
         _check(self._lib.cdn_layer_out_shape(self._h, layer, C.byref(h), C.byref(w), C.byref(c)))
         return h.value, w.value, c.value
+
+    def memory_model(self, Bmax: int):
+        """(IN per image, OUT per image, WS) bytes per layer, as the planner sees them."""
+        n = self.num_layers()
+        a, b, c = (np.zeros(n, np.uint64) for _ in range(3))
+        _check(self._lib.cdn_model_memory_model(self._h, int(Bmax), a.ctypes.data, b.ctypes.data, c.ctypes.data))
+        return a.tolist(), b.tolist(), c.tolist()
 
     def set_kernel_policy(self, band_min_batch: int = 0, tc_min_batch: int = 0):
         """B >= tc_min_batch -> tensor-core kernel; B >= band_min_batch -> band kernel (0: defaults)."""

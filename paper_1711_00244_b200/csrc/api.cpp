@@ -101,6 +101,7 @@ struct Model {
   // profile cache
   int prof_bmax = 0;
   std::vector<double> prof;
+  std::vector<std::pair<int, std::vector<int>>> plan_cache;  // (K, batches) under the current budget
   // executor scratch
   std::vector<DBuf> lvl;        // per-level input buffers [K_i][B_i]
   DBuf out, stage_in, loc, gath, host_stage;
@@ -423,6 +424,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   }
   m.layers.push_back(std::move(Lp));
   m.prof_bmax = 0;
+  m.plan_cache.clear();
   if (out_idx) *out_idx = (int)m.layers.size() - 1;
 }
 
@@ -638,7 +640,7 @@ void check_chain(const Model& m, const std::vector<int>& bs) {
 }
 
 void profile(Model& m, int Bmax, int reps) {
-  if (m.prof_bmax == Bmax && !m.prof.empty()) return;
+  if (m.prof_bmax >= Bmax && !m.prof.empty()) return;  // a wider table serves smaller requests
   const int f = (int)m.layers.size();
   m.prof.assign((size_t)f * Bmax, 0.0);
   cudaStream_t s = m.stream;
@@ -716,10 +718,15 @@ std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
 }
 
 PlanResult plan_for(Model& m, int K) {
+  if (m.prof_bmax < K) m.plan_cache.clear();  // the table is about to change
   profile(m, K, 5);
+  // Time(i, B) for B = 1..K out of the (possibly wider) cached table
+  std::vector<double> t((size_t)m.layers.size() * K);
+  for (size_t i = 0; i < m.layers.size(); ++i)
+    for (int B = 1; B <= K; ++B) t[i * K + (B - 1)] = m.prof[i * (size_t)m.prof_bmax + (B - 1)];
   const int f = (int)m.layers.size();
   auto inb = in_bytes(m), outb = out_bytes(m), ws = ws_bytes(m, K);
-  return plan_dp(m.prof.data(), inb.data(), outb.data(), ws.data(), f, K, m.tot, m.latency, 64 * 1024);
+  return plan_dp(t.data(), inb.data(), outb.data(), ws.data(), f, K, m.tot, m.latency, 64 * 1024);
 }
 
 }  // namespace
@@ -801,6 +808,7 @@ cdn_status cdn_model_set_memory_budget(cdn_model* h, uint64_t tot, double latenc
   if (!h) return fail(CDN_E_ARG, "NULL model");
   h->m.tot = tot;
   h->m.latency = latency_ms > 0 ? latency_ms : 0.0;
+  h->m.plan_cache.clear();
   API_END
 }
 
@@ -857,9 +865,18 @@ cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* score
     if (!m.fixed_plan.empty() && m.fixed_plan.back() <= rem) {
       bs = m.fixed_plan;
     } else if (m.tot > 0) {
-      PlanResult pr = plan_for(m, rem);
-      if (!pr.feasible) return fail(CDN_E_INFEASIBLE, "no batch plan fits TOT/latency");
-      bs = pr.batches;
+      // plans are cached per request size until the budget, layers or table change
+      const std::vector<int>* hit = nullptr;
+      for (auto& e : m.plan_cache)
+        if (e.first == rem && m.prof_bmax >= rem) hit = &e.second;
+      if (hit) {
+        bs = *hit;
+      } else {
+        PlanResult pr = plan_for(m, rem);
+        if (!pr.feasible) return fail(CDN_E_INFEASIBLE, "no batch plan fits TOT/latency");
+        bs = pr.batches;
+        m.plan_cache.emplace_back(rem, bs);
+      }
     } else {
       bs.assign(f, rem);  // no budget: the whole request as one batch
     }
@@ -931,6 +948,7 @@ cdn_status cdn_model_set_kernel_policy(cdn_model* h, int band_min_batch, int tc_
   h->m.band_min = band_min_batch > 0 ? band_min_batch : 0;
   h->m.tc_min = tc_min_batch > 0 ? tc_min_batch : 0;
   h->m.prof_bmax = 0;  // Time(i,B) depends on the policy
+  h->m.plan_cache.clear();
   return CDN_OK;
 }
 
@@ -966,8 +984,20 @@ cdn_status cdn_model_profile(cdn_model* h, int Bmax, int reps, double* time_ms) 
   if (h->m.layers.empty()) return fail(CDN_E_STATE, "no layers loaded");
   CUDA_OK(cudaSetDevice(h->m.device));
   h->m.prof_bmax = 0;
+  h->m.plan_cache.clear();
   profile(h->m, Bmax, reps);
   std::copy(h->m.prof.begin(), h->m.prof.end(), time_ms);
+  API_END
+}
+
+cdn_status cdn_model_memory_model(cdn_model* h, int Bmax, uint64_t* in_b, uint64_t* out_b, uint64_t* ws) {
+  API_BEGIN
+  if (!h || Bmax < 1 || !in_b || !out_b || !ws) return fail(CDN_E_ARG, "bad arguments");
+  Model& m = h->m;
+  auto a = in_bytes(m), b = out_bytes(m), c = ws_bytes(m, Bmax);
+  std::copy(a.begin(), a.end(), in_b);
+  std::copy(b.begin(), b.end(), out_b);
+  std::copy(c.begin(), c.end(), ws);
   API_END
 }
 
