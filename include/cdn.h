@@ -206,6 +206,12 @@ cdn_status cdn_model_profile(cdn_model* m, int Bmax, int reps, double* time_ms);
 cdn_status cdn_model_memory_model(cdn_model* m, int Bmax, uint64_t* in_bytes, uint64_t* out_bytes,
                                   uint64_t* ws_bytes);
 
+/* Name of the kernel a layer launches for batch B under the current policy
+ * (after the first-use autotune at that B, if any): "k_fc_ms", "k_fc_fold",
+ * "k_fc_band<V>", "k_fc_tc" or "k_gemm_bf16 (conv)"; "" for bad arguments.
+ * The string is static. */
+const char* cdn_layer_kernel_name(const cdn_model* m, int layer, int B);
+
 /* ---- host-only utilities (no device needed) ----------------------------- */
 
 /* Compress a dense fp32 row-major rows x cols matrix: magnitude

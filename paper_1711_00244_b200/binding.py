@@ -87,6 +87,7 @@ _SIGS = {
     "cdn_debug_gemm_bf16": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p]),
     "cdn_model_memory_model": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cdn_layer_kernel_name": (C.c_char_p, [C.c_void_p, C.c_int, C.c_int]),
     "cdn_model_num_layers": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int)]),
     "cdn_layer_stats_get": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(LayerStats)]),
     "cdn_model_profile": (C.c_int32, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
@@ -262,6 +263,9 @@ class Model:
         h, w, c = C.c_int(), C.c_int(), C.c_int()
         _check(self._lib.cdn_layer_out_shape(self._h, layer, C.byref(h), C.byref(w), C.byref(c)))
         return h.value, w.value, c.value
+
+    def kernel_name(self, layer: int, B: int) -> str:
+        return self._lib.cdn_layer_kernel_name(self._h, layer, int(B)).decode()
 
     def memory_model(self, Bmax: int):
         """(IN per image, OUT per image, WS) bytes per layer, as the planner sees them."""

@@ -80,6 +80,7 @@ struct Layer {
   DBuf tivg, tivm;      // tensor-core kernel Wi = 64 index (when ivg/ivm use another width)
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
   DBuf tctr;            // tensor-core kernel arrival counters
+  std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band) measured at first use
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
@@ -453,7 +454,39 @@ int band_min_batch() {
 // batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
 void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s) {
   const int relu = L.desc.relu;
-  const int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
+  // Default policy for B >= 128: both large-batch kernels are timed once at the
+  // first call with this B and the faster is kept for the layer (autotune).
+  int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
+  if (m.tc_min == 0 && m.band_min == 0 && B >= 128 && tc_supported(L.dev) && ldx % 4 == 0) {
+    int choice = -1;
+    for (auto& e : L.kchoice)
+      if (e.first == B) choice = e.second;
+    if (choice < 0) {
+      cudaEvent_t e0, e1, e2;
+      CUDA_OK(cudaEventCreate(&e0));
+      CUDA_OK(cudaEventCreate(&e1));
+      CUDA_OK(cudaEventCreate(&e2));
+      m.tc_min = B;  // force the tensor-core kernel for one timed launch
+      fc_forward(m, L, x, ldx, B, y, ldy, s);
+      CUDA_OK(cudaEventRecord(e0, s));
+      fc_forward(m, L, x, ldx, B, y, ldy, s);
+      CUDA_OK(cudaEventRecord(e1, s));
+      m.tc_min = 1 << 30;  // then the band kernel
+      fc_forward(m, L, x, ldx, B, y, ldy, s);
+      CUDA_OK(cudaEventRecord(e2, s));
+      m.tc_min = 0;
+      CUDA_OK(cudaEventSynchronize(e2));
+      float ttc = 0.f, tband = 0.f;
+      CUDA_OK(cudaEventElapsedTime(&ttc, e0, e1));
+      CUDA_OK(cudaEventElapsedTime(&tband, e1, e2));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaEventDestroy(e2);
+      choice = ttc < tband ? 1 : 0;
+      L.kchoice.emplace_back(B, choice);
+    }
+    tcmin = choice ? B : (1 << 30);
+  }
   if (B >= tcmin && tc_supported(L.dev)) {
     TcPlan p = plan_fc_tc(L.dev, B, m.num_sms);
     if (p.ok) {
@@ -988,6 +1021,25 @@ cdn_status cdn_model_profile(cdn_model* h, int Bmax, int reps, double* time_ms) 
   profile(h->m, Bmax, reps);
   std::copy(h->m.prof.begin(), h->m.prof.end(), time_ms);
   API_END
+}
+
+const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
+  if (!h || layer < 0 || layer >= (int)h->m.layers.size() || B < 1) return "";
+  const Model& m = h->m;
+  const Layer& L = *m.layers[layer];
+  if (L.is_conv()) return "k_gemm_bf16 (conv)";
+  int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
+  if (m.tc_min == 0 && m.band_min == 0 && B >= 128 && tc_supported(L.dev)) {
+    for (auto& e : L.kchoice)
+      if (e.first == B) tcmin = e.second ? B : (1 << 30);
+  }
+  if (B >= tcmin && tc_supported(L.dev)) return "k_fc_tc";
+  if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
+    const int vec = B > 64 ? 4 : (B > 32 ? 2 : 1);
+    return vec == 4 ? "k_fc_band<4>" : (vec == 2 ? "k_fc_band<2>" : "k_fc_band<1>");
+  }
+  if (B <= 8 && ms_supported(L.dev)) return "k_fc_ms";
+  return "k_fc_fold";
 }
 
 cdn_status cdn_model_memory_model(cdn_model* h, int Bmax, uint64_t* in_b, uint64_t* out_b, uint64_t* ws) {

@@ -44,9 +44,10 @@ constexpr int kTStages = 2;
 constexpr int kWTile = kTM * kTK * 2;   // 16 KB bf16
 constexpr int kXTile = kTN * kTK * 2;   // 32 KB bf16
 constexpr int kStageBytes = 2 * kWTile + 2 * kXTile;  // hi + lo of both operands: 96 KB
-constexpr int kDecW = 4;            // decode warps (one lane per row)
+constexpr int kDecW = 4;            // decode warps per K stream (one lane per row)
+constexpr int kStreams = 2;         // K halves of a unit decoded concurrently
 constexpr int kEpiW = 4;            // epilogue warps
-constexpr int kTThreads = (2 + kDecW + kEpiW) * 32;   // 320
+constexpr int kTThreads = (2 + kStreams * kDecW + kEpiW) * 32;   // 448
 constexpr int kEpiBar = 1;
 
 struct TcArgs {
@@ -110,8 +111,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* stages = smem;  // [stage]{Whi, Wlo, Xhi, Xlo}
-  unsigned char* rings = smem + kTStages * kStageBytes;  // decoder stream rings [dwarp][stream][4][32][16B]
-  uint64_t* wfull = reinterpret_cast<uint64_t*>(rings + kDecW * 2 * 2048);
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + kTStages * kStageBytes);
   uint64_t* xfull = wfull + kTStages;
   uint64_t* sempty = xfull + kTStages;
   uint64_t* tfull = sempty + kTStages;
@@ -161,20 +161,30 @@ __global__ void __launch_bounds__(kTThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // Each unit's K range is split in two halves (streams); stream q's tiles
+  // always use stage q, and the MMA alternates q = 0, 1, 0, 1, ... into one
+  // TMEM accumulator, so two decode warp groups (each carrying its decoder
+  // state through its half) work concurrently.
   if (warp == 0) {
     // ---------------------------------------------------------- X tile producer
     if (lane == 0) {
-      uint32_t g = 0;
+      uint32_t gq[kStreams] = {0, 0};
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         const TUnit t = tunit(a, u);
-        for (int kt = t.kt0; kt < t.kt1; ++kt, ++g) {
-          const int s = g % kTStages;
-          mbar_wait(&sempty[s], ((g / kTStages) & 1) ^ 1);
-          unsigned char* st = stages + s * kStageBytes;
-          mbar_arrive_expect_tx(&xfull[s], 2 * kXTile);
-          tma2d(st + 2 * kWTile, &txh, kt * kTK, t.bt * kTN, &xfull[s]);
-          tma2d(st + 2 * kWTile + kXTile, &txl, kt * kTK, t.bt * kTN, &xfull[s]);
-        }
+        const int mid = t.kt0 + (t.kt1 - t.kt0 + 1) / 2;
+        const int n0 = mid - t.kt0, n1 = t.kt1 - mid;
+        for (int j = 0; j < n0; ++j)
+#pragma unroll
+          for (int q = 0; q < kStreams; ++q) {
+            if (q == 1 && j >= n1) continue;
+            const int kt = (q == 0 ? t.kt0 : mid) + j;
+            mbar_wait(&sempty[q], (gq[q] & 1) ^ 1);
+            unsigned char* st = stages + q * kStageBytes;
+            mbar_arrive_expect_tx(&xfull[q], 2 * kXTile);
+            tma2d(st + 2 * kWTile, &txh, kt * kTK, t.bt * kTN, &xfull[q]);
+            tma2d(st + 2 * kWTile + kXTile, &txl, kt * kTK, t.bt * kTN, &xfull[q]);
+            ++gq[q];
+          }
       }
     }
   } else if (warp == 1) {
@@ -182,50 +192,59 @@ __global__ void __launch_bounds__(kTThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
                              ((uint32_t)(kTM >> 4) << 24);
-      uint32_t g = 0, uc = 0;
+      uint32_t gq[kStreams] = {0, 0}, uc = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
         const TUnit t = tunit(a, u);
         mbar_wait(tempty, (uc & 1) ^ 1);  // the epilogue drained the accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kt = t.kt0; kt < t.kt1; ++kt, ++g) {
-          const int s = g % kTStages;
-          const uint32_t ph = (g / kTStages) & 1;
-          mbar_wait(&wfull[s], ph);
-          mbar_wait(&xfull[s], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          unsigned char* st = stages + s * kStageBytes;
-          const uint64_t wh = sw128_desc(smem_addr(st)), wl = sw128_desc(smem_addr(st + kWTile));
-          const uint64_t xh = sw128_desc(smem_addr(st + 2 * kWTile)),
-                         xl = sw128_desc(smem_addr(st + 2 * kWTile + kXTile));
+        const int mid = t.kt0 + (t.kt1 - t.kt0 + 1) / 2;
+        const int n0 = mid - t.kt0, n1 = t.kt1 - mid;
+        int step = 0;
+        for (int j = 0; j < n0; ++j)
 #pragma unroll
-          for (int k = 0; k < kTK / 16; ++k) {
-            const uint32_t first = (kt == t.kt0 && k == 0) ? 0u : 1u;
-            umma_bf16(tmem, wh + 2 * k, xh + 2 * k, idesc, first);
-            umma_bf16(tmem, wh + 2 * k, xl + 2 * k, idesc, 1u);
-            umma_bf16(tmem, wl + 2 * k, xh + 2 * k, idesc, 1u);
+          for (int q = 0; q < kStreams; ++q) {
+            if (q == 1 && j >= n1) continue;
+            const uint32_t ph = gq[q] & 1;
+            mbar_wait(&wfull[q], ph);
+            mbar_wait(&xfull[q], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            unsigned char* st = stages + q * kStageBytes;
+            const uint64_t wh = sw128_desc(smem_addr(st)), wl = sw128_desc(smem_addr(st + kWTile));
+            const uint64_t xh = sw128_desc(smem_addr(st + 2 * kWTile)),
+                           xl = sw128_desc(smem_addr(st + 2 * kWTile + kXTile));
+#pragma unroll
+            for (int k = 0; k < kTK / 16; ++k) {
+              const uint32_t acc = (step == 0 && k == 0) ? 0u : 1u;
+              umma_bf16(tmem, wh + 2 * k, xh + 2 * k, idesc, acc);
+              umma_bf16(tmem, wh + 2 * k, xl + 2 * k, idesc, 1u);
+              umma_bf16(tmem, wl + 2 * k, xh + 2 * k, idesc, 1u);
+            }
+            umma_commit(&sempty[q]);
+            ++gq[q];
+            ++step;
           }
-          umma_commit(&sempty[s]);
-        }
-        if (t.kt1 <= t.kt0) {  // empty K range: the partial is zero
-          // no MMA ran; the epilogue is told through tfull with a zero flag below
-        }
-        umma_commit(tfull);
+        umma_commit(tfull);  // an empty K range leaves the accumulator untouched (epilogue writes zeros)
       }
     }
-  } else if (warp < 2 + kDecW) {
+  } else if (warp < 2 + kStreams * kDecW) {
     // ------------------------------------------------------------ decode warps
     // one lane per row; the decoder state is carried from K tile to K tile (the
     // index gives the state only at the unit start, and the real-token count of
     // every tile, prefetched one tile ahead)
-    const int dw = warp - 2;
+    const int dg = warp - 2;
+    const int q = dg / kDecW;          // K stream of this warp group
+    const int dw = dg % kDecW;
     const int row_l = dw * 32 + lane;
     const int fsh = 32 - L.Lf, gsh = 32 - L.Lg, kk = L.k;
-    uint32_t g = 0;
+    uint32_t g = 0;  // tiles of this stream so far (stage q phase)
     for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-      const TUnit t = tunit(a, u);
+      const TUnit tu = tunit(a, u);
+      const int mid = tu.kt0 + (tu.kt1 - tu.kt0 + 1) / 2;
+      TUnit t = tu;
+      if (q == 0) t.kt1 = mid; else t.kt0 = mid;
       const int row = t.rt * kTM + row_l;
       const bool active = row < L.nrows;
-      RReader vr, gr;  // stream words arrive through a cp.async ring in shared memory
+      DReader vr, gr;
       int col = 0;
       uint32_t mnext = 0;
       const uint16_t* mrow = L.tivm + (size_t)(active ? row : 0) * L.tNI;
@@ -233,21 +252,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
         const size_t q = (size_t)row * L.tNI + t.kt0;
         const uint2 st = L.tivg[q];
         const uint32_t m0 = L.tivm[q];
-        cp_async_wait<0>();  // the previous unit's read-ahead lands before the ring is reused
-        const uint32_t rbase = smem_addr(rings) + (uint32_t)dw * 4096 + (uint32_t)lane * 16;
-        vr.start(L.vw, rbase, st.x);
-        gr.start(L.gw, rbase + 2048, st.y);
-        cp_async_wait<0>();
-        vr.fill_done();
-        gr.fill_done();
+        vr.init(L.vw, st.x);
+        gr.init(L.gw, st.y);
         col = t.kt0 * kTK - (int)(m0 & 0xFFu) - 1;
         mnext = m0;
       }
       for (int kt = t.kt0; kt < t.kt1; ++kt, ++g) {
         const uint32_t m = mnext;
         if (active && kt + 1 < t.kt1) mnext = mrow[kt + 1];  // next tile's count, in flight meanwhile
-        const int s = g % kTStages;
-        mbar_wait(&sempty[s], ((g / kTStages) & 1) ^ 1);
+        const int s = q;
+        mbar_wait(&sempty[s], (g & 1) ^ 1);
         unsigned char* wh = stages + s * kStageBytes;
         unsigned char* wl = wh + kWTile;
         // zero this warp's 32 rows (4 KB contiguous per tile), conflict-free
@@ -307,7 +321,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
     }
   } else {
     // ---------------------------------------------------------- epilogue warps
-    const int ew = warp - (2 + kDecW);
+    const int ew = warp - (2 + kStreams * kDecW);
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
     const int row_l = q4 * 32 + lane;
     uint32_t uc = 0;
@@ -420,7 +434,7 @@ __global__ void k_split_x(const float* __restrict__ x, int K, int ldx, int B, __
 }
 
 size_t tc_smem_bytes(const FcDev& L) {
-  size_t b = 1024 + (size_t)kTStages * kStageBytes + kDecW * 2 * 2048 + 8 * (3 * kTStages + 2) + 16;
+  size_t b = 1024 + (size_t)kTStages * kStageBytes + 8 * (3 * kTStages + 2) + 16;
   b += 4 * 256 + (4u << L.Lf) + (4u << L.Lg) + 2 * 99 * 4 + 2 * (L.nvs + 1) + 2 * (L.ngs + 1);
   return (b + 127) & ~(size_t)127;
 }
@@ -440,10 +454,12 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   double best = 1e30;
   int bestS = 1;
   const int smax = p.nkt < 64 ? p.nkt : 64;
+  // unit time ~ its K tiles + a fixed ~16-tile cost (decoder start, epilogue
+  // drain, split partial; measured on C5); the smallest S within 2% of the best wins
   for (int S = 1; S <= smax; ++S) {
     const long units = (long)tiles * S;
     const long waves = (units + num_sms - 1) / num_sms;
-    const double cost = (double)waves / S * (1.0 + 0.02 * (S - 1));
+    const double cost = (double)waves * ((double)p.nkt / S + 16.0);
     if (cost < best * 0.98) { best = cost; bestS = S; }
   }
   p.S = bestS;
