@@ -41,7 +41,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 int nk, int BN, int tmem_cols, int kGStages, const float* __restrict__ bias,
                 float* __restrict__ out, int ldo, int col0, int relu) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space,
+  // so LUT/zero-fill accesses compile to LDS/STS instead of generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const int a_bytes = kBM * kBK * 2, b_bytes = BN * kBK * 2;
   unsigned char* sA = smem;
   unsigned char* sB = smem + kGStages * a_bytes;

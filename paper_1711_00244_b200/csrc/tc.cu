@@ -96,20 +96,26 @@ struct DReader {  // task-local MSB-first reader (3 words up front)
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
   __device__ __forceinline__ void skip(uint32_t n) {
     off += n;
-    if (off >= 32) {
+    const uint32_t adv = off >= 32;
+    if (adv) {
       off -= 32;
       w0 = w1;
       w1 = w2;
-      w2 = ldg_u32(p);
-      ++p;
     }
+    // predicated load straight into the live register: a plain `w2 = ldg(p)` lets the compiler
+    // load into a temporary and MOV it into w2 at once, which waits for the load right here
+    asm("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.u32 %0, [%1]; }"
+        : "+r"(w2) : "l"(p), "r"(adv));
+    p += adv;
   }
 };
 
 __global__ void __launch_bounds__(kTThreads, 1)
     k_fc_tc(FcDev L, TcArgs a, const __grid_constant__ CUtensorMap txh, const __grid_constant__ CUtensorMap txl) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space,
+  // so LUT/zero-fill accesses compile to LDS/STS instead of generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   unsigned char* stages = smem;  // [stage]{Whi, Wlo, Xhi, Xlo}
   uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + kTStages * kStageBytes);
   uint64_t* xfull = wfull + kTStages;
