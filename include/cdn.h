@@ -172,6 +172,10 @@ cdn_status cdn_layer_out_shape(const cdn_model* m, int layer, int* out_h, int* o
  * bias [N] fp32, out fp32 (device).  Errors: CDN_E_ARG, CDN_E_CUDA. */
 cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int Kpad, const float* bias, int relu,
                                float* out, int ldo, void* stream);
+/* Number of CUDA kernels this library has launched since it was loaded (all
+ * models, all threads; a host-side counter, no device work).  *out receives
+ * the count.  Errors: CDN_E_ARG (null out). */
+cdn_status cdn_debug_kernel_launches(uint64_t* out);
 
 /* ---- FC kernel policy (tuning / parity hook) ---------------------------
  * tc_min_batch: batches B >= this run the tensor-core kernel (W tiles decoded

@@ -86,6 +86,7 @@ _SIGS = {
                                         C.POINTER(C.c_int)]),
     "cdn_debug_gemm_bf16": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p]),
+    "cdn_debug_kernel_launches": (C.c_int32, [C.POINTER(C.c_uint64)]),
     "cdn_model_memory_model": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cdn_layer_kernel_name": (C.c_char_p, [C.c_void_p, C.c_int, C.c_int]),
     "cdn_model_num_layers": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int)]),
@@ -172,6 +173,13 @@ def plan_dp(time_ms: np.ndarray, in_bytes: Sequence[int], out_bytes: Sequence[in
     _check(load_library().cdn_plan_dp(t.ctypes.data, ib.ctypes.data, ob.ctypes.data, wb.ctypes.data, f, Bmax,
                                       int(tot), float(latency_ms), int(step), bs.ctypes.data, C.byref(opt)))
     return bs.tolist(), opt.value
+
+
+def kernel_launches() -> int:
+    """Kernels the library has launched since it was loaded (cdn_debug_kernel_launches)."""
+    out = C.c_uint64(0)
+    _check(load_library().cdn_debug_kernel_launches(C.byref(out)))
+    return int(out.value)
 
 
 def debug_gemm_bf16(A, M: int, Wt, N: int, Kpad: int, bias, relu: bool, out, ldo: int, stream: int = 0):

@@ -78,6 +78,7 @@ struct Layer {
   DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias, flut, ctr;
   DBuf ivg, ivm;        // band-kernel interval restart index
   DBuf tivg, tivm;      // tensor-core kernel Wi = 64 index (when ivg/ivm use another width)
+  DBuf tbase, troff, tlist;  // tensor-core kernel: list block bases / row offsets, decoded-entry list (per-call scratch)
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
   DBuf tctr;            // tensor-core kernel arrival counters
   std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band) measured at first use
@@ -310,11 +311,14 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     L.dev.NI = (int)iv.NI;
     L.dev.Cint = cint;
     // the tensor-core kernel's K tile is 64 columns: reuse or build a Wi = 64 index
+    IntervalIndex t64;
+    const IntervalIndex* i64 = nullptr;
     if (Wi == 64) {
       L.dev.tNI = (int)iv.NI;
+      i64 = &iv;
     } else if (!conv) {
-      IntervalIndex t64;
       build_interval_index(H, L.row0, L.row1, 64, t64);
+      i64 = &t64;
       std::vector<uint32_t> tg(2 * t64.v.size());
       std::vector<uint16_t> tm(t64.v.size());
       for (size_t q = 0; q < t64.v.size(); ++q) {
@@ -325,6 +329,33 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       L.tivg.upload(tg);
       L.tivm.upload(tm);
       L.dev.tNI = (int)t64.NI;
+    }
+    if (i64 && !conv) {
+      // decoded-list layout of the tensor-core path (tc.cu): one u16 per real
+      // token, grouped in (128-row tile, 64-column K tile) blocks, block (rt, kt)
+      // at tbase[rt * NI + kt], rows in order inside; troff[(rt * NI + kt) * 129 + r]
+      // = offset of row r's entries in the block ([128] = the block's count)
+      const uint32_t NI = i64->NI, nrt = (nr + 127) / 128;
+      std::vector<uint32_t> tb((size_t)nrt * NI);
+      std::vector<uint16_t> to((size_t)nrt * NI * 129);
+      uint64_t off = 0;
+      for (uint32_t rt = 0; rt < nrt; ++rt)
+        for (uint32_t kt = 0; kt < NI; ++kt) {
+          const size_t blk = (size_t)rt * NI + kt;
+          tb[blk] = (uint32_t)off;
+          uint32_t o = 0;
+          for (uint32_t r = 0; r < 128; ++r) {
+            to[blk * 129 + r] = (uint16_t)o;
+            const uint32_t row = rt * 128 + r;
+            if (row < nr) o += i64->nnz[(size_t)row * NI + kt];
+          }
+          to[blk * 129 + 128] = (uint16_t)o;  // <= 128 * 64
+          off += o;
+        }
+      if (off >= (1ull << 32)) throw Error(CDN_E_UNSUPPORTED, "shard with >= 2^32 nonzeros");
+      L.tbase.upload(tb);
+      L.troff.upload(to);
+      L.tlist.alloc((off + 64) * sizeof(uint16_t));
     }
   }
   const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
@@ -396,6 +427,9 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.msg = L.msg.p ? L.msg.as<uint32_t>() : nullptr;
   f.tivg = L.tivg.p ? L.tivg.as<uint2>() : (L.dev.Wi == 64 ? L.ivg.as<uint2>() : nullptr);
   f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : (L.dev.Wi == 64 ? L.ivm.as<uint16_t>() : nullptr);
+  f.tbase = L.tbase.as<uint32_t>();
+  f.troff = L.troff.as<uint16_t>();
+  f.tlist = L.tlist.as<uint16_t>();
   f.ivg = L.ivg.as<uint2>();
   f.ivm = L.ivm.as<uint16_t>();
 
@@ -973,6 +1007,13 @@ cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int 
   CUDA_OK(launch_gemm_bf16(static_cast<const __nv_bfloat16*>(A), M, static_cast<const __nv_bfloat16*>(Wt), N, Kpad,
                            bias, relu, out, ldo, 0, s));
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
+  API_END
+}
+
+cdn_status cdn_debug_kernel_launches(uint64_t* out) {
+  API_BEGIN
+  if (!out) return fail(CDN_E_ARG, "null out");
+  *out = g_launches.load(std::memory_order_relaxed);
   API_END
 }
 

@@ -479,7 +479,7 @@ cudaError_t launch_band_t(const FcDev& L, const BandPlan& p, const BandArgs& a, 
     set_smem = p.smem;
   }
   kern<<<p.grid, kThreads, p.smem, s>>>(L, a, tmx);
-  return cudaGetLastError();
+  return launched();
 }
 
 }  // namespace

@@ -282,7 +282,7 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
   dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN);
   k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
                                             ldo, col0, relu);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, int kw, int stride, int pad, int c0,
@@ -296,19 +296,19 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
   else
     k_im2col<false><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
                                                                  Kreal, Kpad, out);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms) {
   k_lrn<<<grid_for(npos * C, 256, num_sms), 256, 0, s>>>(x, npos, C, y);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
                            int num_sms) {
   const int Ho = (H - k) / st + 1, Wo = (W - k) / st + 1;
   k_maxpool<<<grid_for((long)B * Ho * Wo * C, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y);
-  return cudaGetLastError();
+  return launched();
 }
 
 }  // namespace cdn

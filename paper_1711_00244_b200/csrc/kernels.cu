@@ -20,6 +20,8 @@
 
 namespace cdn {
 
+std::atomic<unsigned long long> g_launches{0};
+
 namespace {
 
 using dev::ldg_u32;
@@ -457,7 +459,7 @@ cudaError_t launch_fc_t(const FcDev& L, const float* x, int ldx, int B, float* y
   const int work = (units + threads / 32 - 1) / (threads / 32);
   dim3 grid(occupancy_grid(kern, threads, smem, num_sms, work), tiles);
   kern<<<grid, threads, smem, s>>>(L, x, ldx, B, y, ldy, relu);
-  return cudaGetLastError();
+  return launched();
 }
 
 template <int BS, bool REC64>
@@ -506,7 +508,7 @@ cudaError_t launch_decode(const FcDev& L, int row_offset, int32_t* row, int32_t*
     auto k = k_decode<false>;
     k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, row_offset, row, col, sym, val);
   }
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms) {
@@ -522,7 +524,7 @@ cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaS
     auto k = k_decode_dense<false>;
     k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw);
   }
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float* out, int ldo,
@@ -530,7 +532,7 @@ cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
   k_transpose<<<grid, block, 0, s>>>(in, rows, cols, ldi, out, ldo);
-  return cudaGetLastError();
+  return launched();
 }
 
 }  // namespace cdn

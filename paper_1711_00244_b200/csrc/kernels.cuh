@@ -1,13 +1,23 @@
 // Device-side data of one loaded FC/CONV weight matrix (a rank's row block)
 // and the kernel launchers.  Layout rationale: DESIGN.md "Data layout in HBM".
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace cdn {
 
+// kernels this library has launched (cdn_debug_kernel_launches): every launcher
+// returns through launched(n) right after its n launches
+extern std::atomic<unsigned long long> g_launches;
+inline cudaError_t launched(int n = 1) {
+  g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 constexpr int kLutMaxBits = 10;   // plain LUT width cap (decode kernel); longer codes take the canonical slow path
+constexpr int kTcChunk = 8;       // K tiles per decode task of the tensor-core path's list decoder
 constexpr int kFoldLutBits = 11;  // pad-folding val LUT width (fused forward)
 constexpr uint32_t kFoldSlow = 0xFFFFFFFFu;
 constexpr int kMaxBatchTiles = 1024;
@@ -46,6 +56,13 @@ struct FcDev {
   const uint2* tivg = nullptr;
   const uint16_t* tivm = nullptr;
   int tNI = 0;
+  // decoded-entry list between the tensor-core path's two kernels: entry =
+  // (column - 64 kt) | codebook index << 6, one per real token, in blocks of
+  // (128-row tile rt, K tile kt) at tbase[rt * tNI + kt], rows in order inside,
+  // row r at troff[(rt * tNI + kt) * 129 + r] ([128]: the block's count)
+  const uint32_t* tbase = nullptr;
+  const uint16_t* troff = nullptr;
+  uint16_t* tlist = nullptr;
   // small-batch multi-symbol LUTs (small.cu): 2^msLv / 2^msLg entries
   const uint32_t* msv = nullptr;
   const uint32_t* msg = nullptr;

@@ -255,7 +255,7 @@ cudaError_t launch_ms_t(const FcDev& L, const float* x, int ldx, int B, float* y
   const int cap = per_sm * num_sms;
   dim3 grid(need < cap ? need : cap, (B + BS - 1) / BS);
   kern<<<grid, kMsThreads, smem, s>>>(L, x, ldx, B, y, ldy, relu);
-  return cudaGetLastError();
+  return launched();
 }
 
 template <int BS>

@@ -1,29 +1,44 @@
-// Tensor-core FC kernel for large batches, sm_100a:
-// parallel Huffman decode -> gap prefix sum -> codebook dequantize straight
-// into shared-memory weight tiles -> tcgen05 contraction with the batch tile,
-// PAPER.md Alg. 1 lines 4-9, Eq. 1-2.
+// Tensor-core FC path for large batches, sm_100a:
+// PAPER.md Alg. 1 lines 4-9, Eq. 1-2, as two kernels.
+//
+//  1. k_tc_list -- the bit-serial part (Huffman decode of both streams, gap
+//     prefix sum), in parallel over (row, 8-tile chunk) tasks from the Wi = 64
+//     restart index: one u16 entry (column - 64 kt) | codebook index << 6 per
+//     real token, rows in order.  Done ONCE per call, whatever the batch
+//     (the 2 B / nonzero list is per-call scratch; it is re-derived from the
+//     compressed streams on every forward).
+//  2. k_fc_tc -- dequantize + contraction: the W tile (128 rows x 64 K) is
+//     rebuilt from the list in REGISTERS and stored straight into tensor
+//     memory (tcgen05.st), where the UMMA reads it as its A operand; only the
+//     activation tile goes through shared memory (TMA).  Shared-memory
+//     bandwidth is the bound of an M = 128 UMMA pipeline, so keeping W out of
+//     it (no zero fill, no scatter, no A-operand reads) is the point.
 //
 // At B >= 128 the sparse CUDA-core kernel is bound by one shared-memory load
-// per FMA; the tensor cores run the DENSE tile product 25x faster per flop than
-// the CUDA cores, so even at 4% density they win.  fp32 fidelity with bf16
-// tensor cores: every weight (codebook value) and activation is split into
-// hi = bf16(v) and lo = bf16(v - hi); D += Whi*Xhi + Whi*Xlo + Wlo*Xhi (three
-// UMMAs per K step; the dropped Wlo*Xlo term and the two splits are each
-// <= 2^-16 relative per product).
+// per FMA; the tensor cores run the DENSE tile product 25x faster per flop, so
+// even at 4% density they win.  fp32 fidelity with bf16 tensor cores: every
+// weight (codebook value) and activation is split into hi = bf16(v) and
+// lo = bf16(v - hi); D += Whi*Xhi + Whi*Xlo + Wlo*Xhi (three UMMAs per K step;
+// the dropped Wlo*Xlo term and the two splits are each <= 2^-16 relative per
+// product).
 //
-//   unit = (128 output rows, 256 images, K range); per 64-column K tile:
-//     * 4 DECODE warps, one lane per row: the interval index (Wi = 64) gives
-//       the row's decoder state at the tile start and its real-token count;
-//       the lane zero-fills its 128-byte row of the hi and lo tiles, decodes
-//       (pad-folding LUT), and writes bf16 hi/lo of C[sym] at column c - k0 in
-//       the K-major 128B-swizzled UMMA layout; fence.proxy.async, arrive;
-//     * warp 0 / lane 0: TMA of the Xhi / Xlo tiles [256 images][64 K];
+//   unit = (128 output rows, 256 images, K range), split in two K halves
+//   ("streams") expanded concurrently; per 64-column K tile:
+//     * 4 EXPAND warps per stream, one lane per row (= TMEM lane): the lane
+//       walks its row's entries, builds each 8-column chunk of bf16 hi / lo in
+//       4 + 4 registers and tcgen05.st's them into the stream's free W buffer
+//       (2 per stream, 64 TMEM columns each: hi 32 | lo 32);
+//     * warp 0 / lane 0: TMA of the Xhi / Xlo tiles [256 images][64 K] into a
+//       3-stage shared-memory ring (consumption order);
 //     * warp 1 / lane 0: 12 x tcgen05.mma.cta_group::1.kind::f16 (M=128,
-//       N=256, K=16) into a TMEM fp32 accumulator, commit frees the stage;
+//       N=256, K=16, A from TMEM) into the fp32 accumulator (TMEM columns
+//       0-255); commits free the X stage and the W buffer;
 //     * 4 EPILOGUE warps: tcgen05.ld -> + bias -> ReLU -> y (or a K-split
 //       partial, reduced in fixed order by the last CTA of the tile).
-// Decoded weights live only in shared memory (never in HBM).
 #include <cuda.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cuda_bf16.h>
 
 #include "dev_common.cuh"
@@ -40,15 +55,20 @@ using namespace dev;
 constexpr int kTM = 128;            // rows per unit (UMMA M)
 constexpr int kTN = 256;            // images per unit (UMMA N)
 constexpr int kTK = 64;             // K tile (= interval width of the TC index)
-constexpr int kTStages = 2;
-constexpr int kWTile = kTM * kTK * 2;   // 16 KB bf16
+constexpr int kXStages = 3;         // X ring depth
+constexpr int kEnt = 16;            // list entries per row tile carried in registers (the rest: loads)
+constexpr int kRowBytes = 128;      // expand lane's private row: 64 bf16 (chunk-swizzled)
 constexpr int kXTile = kTN * kTK * 2;   // 32 KB bf16
-constexpr int kStageBytes = 2 * kWTile + 2 * kXTile;  // hi + lo of both operands: 96 KB
-constexpr int kDecW = 4;            // decode warps per K stream (one lane per row)
-constexpr int kStreams = 2;         // K halves of a unit decoded concurrently
+constexpr int kXStageBytes = 2 * kXTile;  // hi + lo
+constexpr int kDecW = 4;            // expand warps per K stream: 4 lane quarters (x {bf16 hi, lo} if 8)
+constexpr int kHalvesPerWarp = 8 / kDecW;  // bf16 halves (hi, lo) each expand warp builds
+constexpr int kStreams = 2;         // K halves of a unit expanded concurrently
+constexpr int kWBufs = 2;           // TMEM W buffers per stream
+constexpr int kWCols = 64;          // TMEM columns per W buffer: hi 32 | lo 32
 constexpr int kEpiW = 4;            // epilogue warps
 constexpr int kTThreads = (2 + kStreams * kDecW + kEpiW) * 32;   // 448
 constexpr int kEpiBar = 1;
+constexpr int kTmemCols = 512;      // accumulator 256 + W buffers 4 x 64
 
 struct TcArgs {
   float* y;
@@ -56,15 +76,11 @@ struct TcArgs {
   float* ws;   // [tiles][S][128][256] partials (S > 1)
   int* tctr;   // [tiles]
   int S, nbt, nrt, units, nkt;  // splits, batch tiles, row tiles, units, K tiles
+  unsigned long long* trace;    // debug (env CDN_TC_TRACE): CTA 0 event clocks [event][256], else null
 };
 
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-// byte offset of element (r, k) in a K-major, 128B-swizzled [rows][64] bf16 tile
-__device__ __forceinline__ uint32_t sw128_off(int r, int k) {
-  return (uint32_t)(r * 128 + ((((k >> 3) ^ (r & 7))) << 4) + ((k & 7) << 1));
+__device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
+  if (a.trace != nullptr && blockIdx.x == 0 && i < 256) a.trace[ev * 256 + i] = clock64();
 }
 
 struct TUnit {
@@ -82,74 +98,68 @@ __device__ __forceinline__ TUnit tunit(const TcArgs& a, int u) {
   return t;
 }
 
-struct DReader {  // task-local MSB-first reader (3 words up front)
-  const uint32_t* p;
-  uint32_t off, w0, w1, w2;
-  __device__ __forceinline__ void init(const uint32_t* words, uint32_t bit) {
-    p = words + (bit >> 5);
-    off = bit & 31;
-    w0 = ldg_u32(p);
-    w1 = ldg_u32(p + 1);
-    w2 = ldg_u32(p + 2);
-    p += 3;
-  }
-  __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
-  __device__ __forceinline__ void skip(uint32_t n) {
-    off += n;
-    const uint32_t adv = off >= 32;
-    if (adv) {
-      off -= 32;
-      w0 = w1;
-      w1 = w2;
-    }
-    // predicated load straight into the live register: a plain `w2 = ldg(p)` lets the compiler
-    // load into a temporary and MOV it into w2 at once, which waits for the load right here
-    asm("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.u32 %0, [%1]; }"
-        : "+r"(w2) : "l"(p), "r"(adv));
-    p += adv;
-  }
-};
+// byte offset of column c in a private row: 16-byte chunk c / 8 swizzled by the
+// row, so the 32 lanes of a warp reading chunk j hit 8 distinct chunk slots
+__device__ __forceinline__ uint32_t rsw_off(int r, uint32_t c) {
+  return (((c >> 3) ^ (uint32_t)(r & 7)) << 4) + ((c & 7u) << 1);
+}
+
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+
+__device__ __forceinline__ void sts_u16_if(uint32_t a, uint32_t v, bool p) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "h"((unsigned short)v),
+               "r"((uint32_t)p)
+               : "memory");
+}
+
+__device__ __forceinline__ uint4 lds_u128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+
+// stream q's K tiles of unit t: q = 0 the first half, q = 1 the second
+__device__ __forceinline__ void stream_range(const TUnit& t, int q, int& k0, int& k1) {
+  const int mid = t.kt0 + (t.kt1 - t.kt0 + 1) / 2;
+  k0 = q == 0 ? t.kt0 : mid;
+  k1 = q == 0 ? mid : t.kt1;
+}
 
 __global__ void __launch_bounds__(kTThreads, 1)
     k_fc_tc(FcDev L, TcArgs a, const __grid_constant__ CUtensorMap txh, const __grid_constant__ CUtensorMap txl) {
   extern __shared__ unsigned char smem_raw[];
-  // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space,
-  // so LUT/zero-fill accesses compile to LDS/STS instead of generic LD/ST)
+  // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space)
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-  unsigned char* stages = smem;  // [stage]{Whi, Wlo, Xhi, Xlo}
-  uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + kTStages * kStageBytes);
-  uint64_t* xfull = wfull + kTStages;
-  uint64_t* sempty = xfull + kTStages;
-  uint64_t* tfull = sempty + kTStages;
+  unsigned char* xst = smem;  // [kXStages]{Xhi, Xlo}
+  unsigned char* rows = smem + kXStages * kXStageBytes;  // [stream][128 rows] private zero rows
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(rows + kStreams * (kDecW / 4) * kTM * kRowBytes);
+  uint64_t* xempty = xfull + kXStages;
+  uint64_t* wfull = xempty + kXStages;      // [stream][buf]
+  uint64_t* wempty = wfull + kStreams * kWBufs;
+  uint64_t* tfull = wempty + kStreams * kWBufs;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
   uint32_t* s_cbs = reinterpret_cast<uint32_t*>(s_last + 3);  // [ncb] bf16 hi | lo << 16
-  uint32_t* s_flut = s_cbs + 256;
-  uint32_t* s_glut = s_flut + (1 << L.Lf);
-  uint32_t* s_vtab = s_glut + (1 << L.Lg);
-  uint32_t* s_gtab = s_vtab + 99;
-  uint16_t* s_vsorted = reinterpret_cast<uint16_t*>(s_gtab + 99);
-  uint16_t* s_gsorted = s_vsorted + (L.nvs + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int i = tid; i < (1 << L.Lf); i += nt) s_flut[i] = L.flut[i];
-    for (int i = tid; i < (1 << L.Lg); i += nt) s_glut[i] = L.glut[i];
     for (int i = tid; i < L.ncb; i += nt) {
       const float w = L.codebook[i];
       const __nv_bfloat16 hi = __float2bfloat16_rn(w);
       const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
       s_cbs[i] = (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
     }
-    for (int i = tid; i < 99; i += nt) { s_vtab[i] = L.vtab[i]; s_gtab[i] = L.gtab[i]; }
-    for (int i = tid; i < L.nvs; i += nt) s_vsorted[i] = L.vsorted[i];
-    for (int i = tid; i < L.ngs; i += nt) s_gsorted[i] = L.gsorted[i];
     if (tid == 0) {
-      for (int s = 0; s < kTStages; ++s) {
-        mbar_init(&wfull[s], kDecW);
+      for (int s = 0; s < kXStages; ++s) {
         mbar_init(&xfull[s], 1);
-        mbar_init(&sempty[s], 1);
+        mbar_init(&xempty[s], 1);
+      }
+      for (int s = 0; s < kStreams * kWBufs; ++s) {
+        mbar_init(&wfull[s], kDecW);
+        mbar_init(&wempty[s], 1);
       }
       mbar_init(tfull, 1);
       mbar_init(tempty, kEpiW);
@@ -157,7 +167,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
     }
     if (warp == 0) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
-                   "n"(kTN)
+                   "n"(kTmemCols)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -166,30 +176,35 @@ __global__ void __launch_bounds__(kTThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // zero the private rows once; each tile's entries are cleared after use
+  for (int i = threadIdx.x; i < kStreams * (kDecW / 4) * kTM * kRowBytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(rows)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const uint32_t tmem_w = tmem + kTN;  // W buffers: column kTN + (q * kWBufs + b) * kWCols
 
-  // Each unit's K range is split in two halves (streams); stream q's tiles
-  // always use stage q, and the MMA alternates q = 0, 1, 0, 1, ... into one
-  // TMEM accumulator, so two decode warp groups (each carrying its decoder
-  // state through its half) work concurrently.
+  // The MMA consumes the two streams' tiles alternately q = 0, 1, 0, 1, ...
+  // (the longer first half finishes alone); the X producer loads in that order.
   if (warp == 0) {
     // ---------------------------------------------------------- X tile producer
     if (lane == 0) {
-      uint32_t gq[kStreams] = {0, 0};
+      uint32_t xc = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         const TUnit t = tunit(a, u);
-        const int mid = t.kt0 + (t.kt1 - t.kt0 + 1) / 2;
-        const int n0 = mid - t.kt0, n1 = t.kt1 - mid;
-        for (int j = 0; j < n0; ++j)
+        int a0, a1, b0, b1;
+        stream_range(t, 0, a0, a1);
+        stream_range(t, 1, b0, b1);
+        for (int j = 0; j < a1 - a0; ++j)
 #pragma unroll
           for (int q = 0; q < kStreams; ++q) {
-            if (q == 1 && j >= n1) continue;
-            const int kt = (q == 0 ? t.kt0 : mid) + j;
-            mbar_wait(&sempty[q], (gq[q] & 1) ^ 1);
-            unsigned char* st = stages + q * kStageBytes;
-            mbar_arrive_expect_tx(&xfull[q], 2 * kXTile);
-            tma2d(st + 2 * kWTile, &txh, kt * kTK, t.bt * kTN, &xfull[q]);
-            tma2d(st + 2 * kWTile + kXTile, &txl, kt * kTK, t.bt * kTN, &xfull[q]);
-            ++gq[q];
+            if (q == 1 && j >= b1 - b0) continue;
+            const int kt = (q == 0 ? a0 : b0) + j;
+            const int s = (int)(xc % kXStages);
+            mbar_wait(&xempty[s], ((xc / kXStages) & 1) ^ 1);
+            unsigned char* st = xst + s * kXStageBytes;
+            mbar_arrive_expect_tx(&xfull[s], 2 * kXTile);
+            tma2d(st, &txh, kt * kTK, t.bt * kTN, &xfull[s]);
+            tma2d(st + kXTile, &txl, kt * kTK, t.bt * kTN, &xfull[s]);
+            ++xc;
           }
       }
     }
@@ -198,34 +213,41 @@ __global__ void __launch_bounds__(kTThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
                              ((uint32_t)(kTM >> 4) << 24);
-      uint32_t gq[kStreams] = {0, 0}, uc = 0;
+      uint32_t xc = 0, gq[kStreams] = {0, 0}, uc = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
         const TUnit t = tunit(a, u);
         mbar_wait(tempty, (uc & 1) ^ 1);  // the epilogue drained the accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int mid = t.kt0 + (t.kt1 - t.kt0 + 1) / 2;
-        const int n0 = mid - t.kt0, n1 = t.kt1 - mid;
+        int a0, a1, b0, b1;
+        stream_range(t, 0, a0, a1);
+        stream_range(t, 1, b0, b1);
         int step = 0;
-        for (int j = 0; j < n0; ++j)
+        for (int j = 0; j < a1 - a0; ++j)
 #pragma unroll
           for (int q = 0; q < kStreams; ++q) {
-            if (q == 1 && j >= n1) continue;
-            const uint32_t ph = gq[q] & 1;
-            mbar_wait(&wfull[q], ph);
-            mbar_wait(&xfull[q], ph);
+            if (q == 1 && j >= b1 - b0) continue;
+            const int wb = q * kWBufs + (int)(gq[q] % kWBufs);
+            const int s = (int)(xc % kXStages);
+            tc_trace(a, 8, step);
+            mbar_wait(&wfull[wb], (gq[q] / kWBufs) & 1);
+            tc_trace(a, 9, step);
+            mbar_wait(&xfull[s], (xc / kXStages) & 1);
+            tc_trace(a, 10, step);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            unsigned char* st = stages + q * kStageBytes;
-            const uint64_t wh = sw128_desc(smem_addr(st)), wl = sw128_desc(smem_addr(st + kWTile));
-            const uint64_t xh = sw128_desc(smem_addr(st + 2 * kWTile)),
-                           xl = sw128_desc(smem_addr(st + 2 * kWTile + kXTile));
+            unsigned char* st = xst + s * kXStageBytes;
+            const uint64_t xh = sw128_desc(smem_addr(st)), xl = sw128_desc(smem_addr(st + kXTile));
+            const uint32_t ah = tmem_w + (uint32_t)(wb * kWCols), al = ah + kWCols / 2;
 #pragma unroll
             for (int k = 0; k < kTK / 16; ++k) {
               const uint32_t acc = (step == 0 && k == 0) ? 0u : 1u;
-              umma_bf16(tmem, wh + 2 * k, xh + 2 * k, idesc, acc);
-              umma_bf16(tmem, wh + 2 * k, xl + 2 * k, idesc, 1u);
-              umma_bf16(tmem, wl + 2 * k, xh + 2 * k, idesc, 1u);
+              umma_bf16_ts(tmem, ah + 8 * k, xh + 2 * k, idesc, acc);
+              umma_bf16_ts(tmem, ah + 8 * k, xl + 2 * k, idesc, 1u);
+              umma_bf16_ts(tmem, al + 8 * k, xh + 2 * k, idesc, 1u);
             }
-            umma_commit(&sempty[q]);
+            umma_commit(&xempty[s]);
+            umma_commit(&wempty[wb]);
+            tc_trace(a, 11, step);
+            ++xc;
             ++gq[q];
             ++step;
           }
@@ -233,99 +255,124 @@ __global__ void __launch_bounds__(kTThreads, 1)
       }
     }
   } else if (warp < 2 + kStreams * kDecW) {
-    // ------------------------------------------------------------ decode warps
-    // one lane per row; the decoder state is carried from K tile to K tile (the
-    // index gives the state only at the unit start, and the real-token count of
-    // every tile, prefetched one tile ahead)
-    const int dg = warp - 2;
-    const int q = dg / kDecW;          // K stream of this warp group
-    const int dw = dg % kDecW;
-    const int row_l = dw * 32 + lane;
-    const int fsh = 32 - L.Lf, gsh = 32 - L.Lg, kk = L.k;
-    uint32_t g = 0;  // tiles of this stream so far (stage q phase)
+    // ------------------------------------------------------------ expand warps
+    // one lane per row = TMEM lane (a warp reaches lanes 32 (warp % 4) ...);
+    // the row's entries of K tile kt are the next nnz(kt) u16 of the list
+    // (k_tc_list), in column order, read through L1 with the next one in flight
+    const int q = (warp - 2) / kDecW;  // K stream of this warp group
+    const int hsel = kHalvesPerWarp == 2 ? 0 : ((warp - 2) % kDecW) >> 2;  // warp's half (kDecW == 8)
+    const int quarter = warp & 3;
+    const int row_l = quarter * 32 + lane;
+    const uint32_t tlane = (uint32_t)(quarter * 32) << 16;
+    const uint32_t prow = smem_addr(rows) + (uint32_t)(((q * (kDecW / 4) + hsel) * kTM + row_l) * kRowBytes);  // private row
+    uint32_t g = 0;  // tiles of this stream so far
     for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-      const TUnit tu = tunit(a, u);
-      const int mid = tu.kt0 + (tu.kt1 - tu.kt0 + 1) / 2;
-      TUnit t = tu;
-      if (q == 0) t.kt1 = mid; else t.kt0 = mid;
-      const int row = t.rt * kTM + row_l;
-      const bool active = row < L.nrows;
-      DReader vr, gr;
-      int col = 0;
-      uint32_t mnext = 0;
-      const uint16_t* mrow = L.tivm + (size_t)(active ? row : 0) * L.tNI;
-      if (active && t.kt1 > t.kt0) {
-        const size_t q = (size_t)row * L.tNI + t.kt0;
-        const uint2 st = L.tivg[q];
-        const uint32_t m0 = L.tivm[q];
-        vr.init(L.vw, st.x);
-        gr.init(L.gw, st.y);
-        col = t.kt0 * kTK - (int)(m0 & 0xFFu) - 1;
-        mnext = m0;
-      }
-      for (int kt = t.kt0; kt < t.kt1; ++kt, ++g) {
-        const uint32_t m = mnext;
-        if (active && kt + 1 < t.kt1) mnext = mrow[kt + 1];  // next tile's count, in flight meanwhile
-        const int s = q;
-        mbar_wait(&sempty[s], (g & 1) ^ 1);
-        unsigned char* wh = stages + s * kStageBytes;
-        unsigned char* wl = wh + kWTile;
-        // zero this warp's 32 rows (4 KB contiguous per tile), conflict-free
-        {
-          uint4* zh = reinterpret_cast<uint4*>(wh + dw * 4096);
-          uint4* zl = reinterpret_cast<uint4*>(wl + dw * 4096);
+      const TUnit t = tunit(a, u);
+      int k0, k1;
+      stream_range(t, q, k0, k1);
+      // tile kt's entries: block (rt, kt) of the list, this row's slice of it
+      const size_t blk0 = (size_t)t.rt * L.tNI;
+      // raw loads only: the base / count arithmetic happens a tile later, at use
+      struct Off { uint32_t b, o0, o1; };
+      auto offs = [&](int kt) -> Off {
+        const size_t blk = blk0 + kt;
+        return Off{L.tbase[blk], L.troff[blk * 129 + row_l], L.troff[blk * 129 + row_l + 1]};
+      };
+      if (k1 <= k0) continue;
+      Off fc = offs(k0);                          // tile kt
+      Off fn = offs(k0 + 1 < k1 ? k0 + 1 : k1 - 1);  // tile kt + 1 (loaded one tile ahead of use)
+      uint32_t oc = fc.b + fc.o0, nc = fc.o1 - fc.o0;
+      // the next tile's first kEnt entries ride in registers one tile ahead;
+      // every per-entry loop below stops at the warp's largest count (uniform branch)
+      uint32_t nx[kEnt];
+      {
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, nc);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            zh[c * 32 + lane] = make_uint4(0, 0, 0, 0);
-            zl[c * 32 + lane] = make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < kEnt; ++i) {
+          if ((uint32_t)i >= wm) break;
+          nx[i] = (uint32_t)i < nc ? __ldg(L.tlist + oc + i) : 0u;
+        }
+      }
+      for (int kt = k0; kt < k1; ++kt, ++g) {
+        const bool tr = quarter == 2 && hsel == 0 && lane == 0;
+        if (tr) tc_trace(a, 0 + 4 * q, kt - k0);
+        const uint32_t nnz = nc;
+        const uint32_t wmax = __reduce_max_sync(0xffffffffu, nnz);
+        const uint16_t* cur = L.tlist + oc;
+        uint32_t v[kEnt];
+#pragma unroll
+        for (int i = 0; i < kEnt; ++i) {
+          if ((uint32_t)i >= wmax) break;
+          v[i] = nx[i];
+        }
+        oc = fn.b + fn.o0;
+        nc = fn.o1 - fn.o0;
+        {
+          const uint32_t wm = __reduce_max_sync(0xffffffffu, nc);
+#pragma unroll
+          for (int i = 0; i < kEnt; ++i) {
+            if ((uint32_t)i >= wm) break;
+            nx[i] = (uint32_t)i < nc ? __ldg(L.tlist + oc + i) : 0u;
           }
         }
-        __syncwarp();
-        const uint32_t nnz = active ? (m >> 8) : 0u;
-        const int k0 = kt * kTK;
-        uint32_t done = 0;
-        while (done < nnz) {
-          const uint32_t w = vr.peek();
-          const uint32_t e = s_flut[w >> fsh];
-          uint32_t len, sym, pads, pbits;
-          if (e != kFoldSlow) {
-            len = e >> 28;
-            sym = e & 0xFFu;
-            pads = (e >> 24) & 15u;
-            pbits = (e >> 8) & 0xFFFFu;
-          } else {
-            const uint32_t r = slow_sym(w, L.Lf + 1, s_vtab, s_vsorted, L.vmax);
-            len = r >> 16;
-            sym = r & 0xFFu;
-            pads = sym == 0;
-            pbits = pads ? (uint32_t)L.Lpg : 0u;
-          }
-          vr.skip(len);
-          col += (int)(pads << kk);
-          if (pbits <= 32) {
-            gr.skip(pbits);
-          } else {
-            for (uint32_t z = 0; z < pads; ++z) gr.skip((uint32_t)L.Lpg);
-          }
-          if (sym) {
-            const uint32_t gwin = gr.peek();
-            uint32_t ge = s_glut[gwin >> gsh];
-            if (ge == 0) ge = slow_sym(gwin, L.Lg + 1, s_gtab, s_gsorted, L.gmax);
-            gr.skip(ge >> 16);
-            col += (int)(ge & 0xFFFFu) + 1;
-            const uint32_t hl = s_cbs[sym];
-            const uint32_t off = sw128_off(row_l, col - k0);
-            *reinterpret_cast<uint16_t*>(wh + off) = (uint16_t)(hl & 0xFFFFu);
-            *reinterpret_cast<uint16_t*>(wl + off) = (uint16_t)(hl >> 16);
-            ++done;
-          }
+        fn = offs(kt + 2 < k1 ? kt + 2 : k1 - 1);
+        const int wb = q * kWBufs + (int)(g % kWBufs);
+        mbar_wait(&wempty[wb], ((g / kWBufs) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tr) tc_trace(a, 2 + 4 * q, kt - k0);
+        const uint32_t tw = tmem_w + (uint32_t)(wb * kWCols) + tlane;
+        // per entry (predicated on i < nnz): this warp's bf16 half of C[sym] and
+        // its slot in the lane's private zero row
+        uint32_t hl[kEnt], ad[kEnt];
+#pragma unroll
+        for (int i = 0; i < kEnt; ++i) {
+          if ((uint32_t)i >= wmax) break;
+          hl[i] = s_cbs[(v[i] >> 6) & 255u];
+          ad[i] = prow + rsw_off(row_l, v[i] & 63u);
         }
-        fence_proxy_async_smem();  // generic-proxy tile writes -> tensor-core reads
+#pragma unroll
+        for (int hh = 0; hh < kHalvesPerWarp; ++hh) {
+          const int h = kHalvesPerWarp == 2 ? hh : hsel;  // 0: bf16 hi tile, 1: lo tile
+          const uint32_t hsh = 16u * (uint32_t)h;
+#pragma unroll
+          for (int i = 0; i < kEnt; ++i) {
+            if ((uint32_t)i >= wmax) break;
+            sts_u16_if(ad[i], (hl[i] >> hsh) & 0xFFFFu, (uint32_t)i < nnz);
+          }
+          for (uint32_t i = kEnt; i < nnz; ++i) {  // a denser row tile
+            const uint32_t e = __ldg(cur + i);
+            sts_u16_if(prow + rsw_off(row_l, e & 63u), (s_cbs[e >> 6] >> hsh) & 0xFFFFu, true);
+          }
+          if (tr && q == 0) tc_trace(a, 1, kt - k0);
+          {  // 8 conflict-free LDS.128 -> one tcgen05.st of 32 columns
+            uint32_t r[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint4 w4 = lds_u128(prow + ((uint32_t)(j ^ (row_l & 7)) << 4));
+              r[4 * j] = w4.x; r[4 * j + 1] = w4.y; r[4 * j + 2] = w4.z; r[4 * j + 3] = w4.w;
+            }
+            if (tr && q == 0) tc_trace(a, 14, kt - k0);
+            tmem_st32(tw + (uint32_t)(h * (kWCols / 2)), r);
+            if (tr && q == 0) tc_trace(a, 6, kt - k0);
+          }
+          // back to a zero row
+#pragma unroll
+          for (int i = 0; i < kEnt; ++i) {
+            if ((uint32_t)i >= wmax) break;
+            sts_u16_if(ad[i], 0u, (uint32_t)i < nnz);
+          }
+          for (uint32_t i = kEnt; i < nnz; ++i) sts_u16_if(prow + rsw_off(row_l, __ldg(cur + i) & 63u), 0u, true);
+        }
+        if (tr && q == 0) tc_trace(a, 7, kt - k0);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&wfull[s]);
+        if (tr) tc_trace(a, 3 + 4 * q, kt - k0);
+        if (lane == 0) mbar_arrive(&wfull[wb]);
       }
     }
   } else {
+
     // ---------------------------------------------------------- epilogue warps
     const int ew = warp - (2 + kStreams * kDecW);
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
@@ -333,7 +380,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
     uint32_t uc = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
       const TUnit t = tunit(a, u);
+      if (ew == 0 && lane == 0) tc_trace(a, 12, 0);
       mbar_wait(tfull, uc & 1);
+      if (ew == 0 && lane == 0) tc_trace(a, 13, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = t.rt * kTM + row_l;
       const int b0 = t.bt * kTN;
@@ -415,7 +464,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
 // X fp32 feature-major [K][ldx] -> bf16 hi / lo image-major [B][ldk] (K contiguous)
@@ -439,15 +488,112 @@ __global__ void k_split_x(const float* __restrict__ x, int K, int ldx, int B, __
   }
 }
 
-size_t tc_smem_bytes(const FcDev& L) {
-  size_t b = 1024 + (size_t)kTStages * kStageBytes + 8 * (3 * kTStages + 2) + 16;
-  b += 4 * 256 + (4u << L.Lf) + (4u << L.Lg) + 2 * 99 * 4 + 2 * (L.nvs + 1) + 2 * (L.ngs + 1);
+size_t tc_smem_bytes(const FcDev&) {
+  size_t b = 1024 + (size_t)kXStages * kXStageBytes + (size_t)kStreams * (kDecW / 4) * kTM * kRowBytes + 8 * (2 * kXStages + 2 * kStreams * kWBufs + 2) + 16 + 4 * 256;
   return (b + 127) & ~(size_t)127;
+}
+
+// ---------------------------------------------------------------------------
+// List decoder (first kernel of the tensor-core path): PAPER.md Alg. 1 lines
+// 4-7 -- Huffman decode of both streams, gap prefix sum -- for
+// every (row, 8-tile chunk) in parallel from the Wi = 64 restart index; each
+// real token becomes one u16 entry (column - 64 kt) | codebook index << 6 in
+// its (row tile, K tile) block of the list (tbase / troff, built at load).
+// Pads (symbol 0, C-04) produce nothing.  One thread per task; the 128 rows of
+// a row tile are consecutive threads, so their entry writes are adjacent.
+constexpr int kListThreads = 256;
+
+__global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
+  __shared__ uint32_t s_flut[1 << kFoldLutBits];
+  __shared__ uint32_t s_glut[1 << kLutMaxBits];
+  __shared__ uint32_t s_vtab[99], s_gtab[99];
+  __shared__ uint16_t s_vsorted[257], s_gsorted[257];
+  for (int i = threadIdx.x; i < (1 << L.Lf); i += blockDim.x) s_flut[i] = L.flut[i];
+  for (int i = threadIdx.x; i < (1 << L.Lg); i += blockDim.x) s_glut[i] = L.glut[i];
+  for (int i = threadIdx.x; i < 99; i += blockDim.x) { s_vtab[i] = L.vtab[i]; s_gtab[i] = L.gtab[i]; }
+  for (int i = threadIdx.x; i < L.nvs; i += blockDim.x) s_vsorted[i] = L.vsorted[i];
+  for (int i = threadIdx.x; i < L.ngs; i += blockDim.x) s_gsorted[i] = L.gsorted[i];
+  __syncthreads();
+  // task = (row tile, chunk of kTcChunk K tiles, row in tile): consecutive
+  // threads write adjacent slices of the same blocks
+  const int nch = (L.tNI + kTcChunk - 1) / kTcChunk;
+  const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
+  const int r = (int)(task & 127);
+  const size_t rc = task >> 7;
+  const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * kTcChunk;
+  const int row = rt * 128 + r;
+  if (row >= L.nrows) return;
+  const int nk = L.tNI - kt0 < kTcChunk ? L.tNI - kt0 : kTcChunk;
+  // output slot of this row's first entry in each of the chunk's tiles
+  uint32_t p[kTcChunk], n = 0;
+#pragma unroll
+  for (int k = 0; k < kTcChunk; ++k) {
+    p[k] = 0;
+    if (k < nk) {
+      const size_t blk = (size_t)rt * L.tNI + kt0 + k;
+      const uint32_t o0 = L.troff[blk * 129 + r], o1 = L.troff[blk * 129 + r + 1];
+      p[k] = L.tbase[blk] + o0;
+      n += o1 - o0;
+    }
+  }
+  if (n == 0) return;
+  const size_t q = (size_t)row * L.tNI + kt0;
+  const uint2 st = L.tivg[q];
+  int col = kt0 * 64 - (int)(L.tivm[q] & 0xFFu) - 1;
+  SReader vr, gr;
+  vr.init(L.vw, st.x);
+  gr.init(L.gw, st.y);
+  int ck = -1;       // tile of the last entry written
+  uint32_t pos = 0;  // its next slot
+  const int fsh = 32 - L.Lf, gsh = 32 - L.Lg, kk = L.k;
+  for (uint32_t i = 0; i < n;) {
+    const uint32_t w = vr.peek();
+    const uint32_t e = s_flut[w >> fsh];
+    uint32_t len, sym, pads, pbits;
+    if (e != kFoldSlow) {  // pads folded in front of the code (C-04), one lookup
+      len = e >> 28;
+      sym = e & 0xFFu;
+      pads = (e >> 24) & 15u;
+      pbits = (e >> 8) & 0xFFFFu;
+    } else {
+      const uint32_t r = slow_sym(w, L.Lf + 1, s_vtab, s_vsorted, L.vmax);
+      len = r >> 16;
+      sym = r & 0xFFu;
+      pads = sym == 0;
+      pbits = pads ? (uint32_t)L.Lpg : 0u;
+    }
+    vr.skip(len);
+    col += (int)(pads << kk);  // a pad advances the column by 2^k (gap 2^k - 1, C-01)
+    if (pbits <= 32) {
+      gr.skip(pbits);
+    } else {
+      for (uint32_t z = 0; z < pads; ++z) gr.skip((uint32_t)L.Lpg);
+    }
+    if (sym) {
+      const uint32_t gwin = gr.peek();
+      uint32_t ge = s_glut[gwin >> gsh];
+      if (ge == 0) ge = slow_sym(gwin, L.Lg + 1, s_gtab, s_gsorted, L.gmax);
+      gr.skip(ge >> 16);
+      col += (int)(ge & 0xFFFFu) + 1;  // c = prev + g + 1 (Alg. 1 l.7, C-01)
+      const int k = (col >> 6) - kt0;
+      if (k != ck) {  // entered the next tile of the chunk: its slot (register select)
+        ck = k;
+        pos = p[0];
+#pragma unroll
+        for (int j = 1; j < kTcChunk; ++j) pos = k == j ? p[j] : pos;
+      }
+      L.tlist[pos++] = (uint16_t)((col & 63) | (sym << 6));
+      ++i;
+    }
+  }
 }
 
 }  // namespace
 
-bool tc_supported(const FcDev& L) { return L.tivg && L.tivm && L.tNI > 0 && L.ncb <= 256; }
+bool tc_supported(const FcDev& L) {
+  return L.tivg && L.tivm && L.tNI > 0 && L.tbase && L.troff && L.tlist && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
+         L.Lf == kFoldLutBits && L.Lg <= kLutMaxBits;
+}
 
 TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   TcPlan p;
@@ -483,7 +629,11 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
                          __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, int* tctr, cudaStream_t s) {
   dim3 sg((p.ldk + 31) / 32, (B + 31) / 32), sb(32, 8);
   k_split_x<<<sg, sb, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launched();
+  if (e != cudaSuccess) return e;
+  const size_t tasks = (size_t)((L.nrows + 127) / 128) * ((L.tNI + kTcChunk - 1) / kTcChunk) * 128;
+  k_tc_list<<<(unsigned)((tasks + kListThreads - 1) / kListThreads), kListThreads, 0, s>>>(L);
+  e = launched();
   if (e != cudaSuccess) return e;
   CUtensorMap th, tl;
   e = encode_tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xh, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
@@ -498,9 +648,26 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     if (e != cudaSuccess) return e;
     set_smem = p.smem;
   }
-  TcArgs a{y, ldy, B, relu, ws, tctr, p.S, p.nbt, p.nrt, p.units, p.nkt};
+  static unsigned long long* trace = nullptr;
+  const char* trace_path = getenv("CDN_TC_TRACE");
+  if (trace_path && !trace) {
+    e = cudaMalloc(&trace, 16 * 256 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+  }
+  if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
+  TcArgs a{y, ldy, B, relu, ws, tctr, p.S, p.nbt, p.nrt, p.units, p.nkt, trace_path ? trace : nullptr};
   k_fc_tc<<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
-  return cudaGetLastError();
+  e = launched();
+  if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
+    std::vector<unsigned long long> h(16 * 256);
+    e = cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (FILE* fp = fopen(trace_path, "wb")) {
+      fwrite(h.data(), sizeof(h[0]), h.size(), fp);
+      fclose(fp);
+    }
+  }
+  return e;
 }
 
 }  // namespace cdn

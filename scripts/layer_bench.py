@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--single", action="store_true", help="one launch, no timing (ncu target)")
+    ap.add_argument("--policy", default="auto", choices=["auto", "tc", "band"],
+                    help="large-batch kernel: autotuned (default), tensor-core or band")
     args = ap.parse_args()
     import torch
     import paper_1711_00244_b200 as cdn
@@ -45,6 +47,10 @@ def main():
         for _ in range(args.replicas):
             m = cdn.Model(0)
             m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+            if args.policy == "tc":
+                m.set_kernel_policy(1, 1)
+            elif args.policy == "band":
+                m.set_kernel_policy(1, 1 << 30)
             models.append(m)
         st = models[0].stats(0)
         for B in [int(b) for b in args.batches.split(",")]:
@@ -81,6 +87,7 @@ def main():
             algo = st["algo_bytes_fixed"] + 4 * spec.cols * B + 4 * spec.rows * B
             flops = 2.0 * st["nnz"] * B + spec.rows * B
             print(json.dumps({"cfg": args.cfg, "layer": spec.name, "B": B, "us": ms * 1e3,
+                              "kernel": models[0].kernel_name(0, B),
                               "gbs": algo / ms / 1e6, "hbm_frac": algo / ms / 1e6 / peaks["hbm_gbs"],
                               "tflops": flops / ms / 1e9, "tokens": st["tokens"], "nnz": st["nnz"],
                               "G": st["lanes_per_row"], "index_bytes": st["index_bytes"],
