@@ -79,6 +79,15 @@ struct Layer {
   DBuf ivg, ivm;        // band-kernel interval restart index
   DBuf tivg, tivm;      // tensor-core kernel Wi = 64 index (when ivg/ivm use another width)
   DBuf tbase, troff, tlist;  // tensor-core kernel: list block bases / row offsets, decoded-entry list (per-call scratch)
+  // tlist state within one API call: 0 = not decoded yet, 1 = being decoded on
+  // the model's side stream (list_ev marks the end), 2 = decoded and ordered
+  // before everything enqueued after it on the call's stream (reused by later
+  // phases of the same call)
+  int list_state = 0;
+  cudaEvent_t list_ev = nullptr;
+  ~Layer() {
+    if (list_ev) cudaEventDestroy(list_ev);
+  }
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
   DBuf tctr;            // tensor-core kernel arrival counters
   std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band) measured at first use
@@ -96,6 +105,8 @@ struct Model {
   int device = 0, rank = 0, world = 1, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;    // list decoding ahead of the layers (tensor-core path)
+  cudaEvent_t ev_call = nullptr;  // start of the current call on its stream
   std::vector<std::unique_ptr<Layer>> layers;
   uint64_t tot = 0;
   double latency = 0.0;
@@ -356,6 +367,11 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       L.tbase.upload(tb);
       L.troff.upload(to);
       L.tlist.alloc((off + 64) * sizeof(uint16_t));
+      // list-decoder tasks: chunks of up to kTcChunk K tiles, fewer when that
+      // would leave the GPU short of threads (~128k wanted)
+      int tch = kTcChunk;
+      while (tch > 1 && (uint64_t)nrt * 128 * ((NI + tch - 1) / tch) < 131072) tch >>= 1;
+      L.dev.tch = tch;
     }
   }
   const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
@@ -503,6 +519,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       m.tc_min = B;  // force the tensor-core kernel for one timed launch
       fc_forward(m, L, x, ldx, B, y, ldy, s);
       CUDA_OK(cudaEventRecord(e0, s));
+      L.list_state = 0;  // the timed run decodes its list like a fresh call
       fc_forward(m, L, x, ldx, B, y, ldy, s);
       CUDA_OK(cudaEventRecord(e1, s));
       m.tc_min = 1 << 30;  // then the band kernel
@@ -532,6 +549,12 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
         L.tctr.alloc(need);
         CUDA_OK(cudaMemsetAsync(L.tctr.p, 0, need, s));
       }
+      if (L.list_state == 1) {
+        CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
+      } else if (L.list_state == 0) {
+        CUDA_OK(launch_tc_list(L.dev, s));
+      }
+      L.list_state = 2;
       CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<__nv_bfloat16*>(m.tc_xh.p),
                            static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), L.tctr.as<int>(), s));
       return;
@@ -559,6 +582,55 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
     return;
   }
   CUDA_OK(launch_fc_forward(L.dev, x, ldx, B, y, ldy, relu, s, m.num_sms));
+}
+
+// Whether fc_forward takes the tensor-core path for this layer and batch
+// (a batch whose first-use autotune has not run yet counts as no).
+bool uses_tc(const Model& m, const Layer& L, int B) {
+  if (L.is_conv() || !tc_supported(L.dev)) return false;
+  if (m.tc_min == 0 && m.band_min == 0 && B >= 128) {
+    for (auto& e : L.kchoice)
+      if (e.first == B) return e.second == 1;
+    return false;
+  }
+  const int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
+  return B >= tcmin;
+}
+
+// End of an API call: the decoded lists are per-call scratch.  A list still
+// being decoded on the side stream is ordered before later work on s.
+void reset_lists(Model& m, cudaStream_t s) {
+  for (auto& L : m.layers) {
+    if (L->list_state == 1) cudaStreamWaitEvent(s, L->list_ev, 0);
+    L->list_state = 0;
+  }
+}
+
+// Start of an infer call: the lists of every tensor-core layer are decoded on
+// the side stream right away, in layer order -- they depend on the compressed
+// weights only, so they overlap the earlier layers' work (and the activation
+// split) instead of sitting in front of each layer's contraction.
+void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
+  bool any = false;
+  for (size_t i = 0; i < m.layers.size(); ++i)
+    any |= m.layers[i]->list_state == 0 && uses_tc(m, *m.layers[i], bs[i]);
+  if (!any) return;
+  if (!m.side) {
+    int least = 0, greatest = 0;
+    CUDA_OK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CUDA_OK(cudaStreamCreateWithPriority(&m.side, cudaStreamNonBlocking, least));
+    CUDA_OK(cudaEventCreateWithFlags(&m.ev_call, cudaEventDisableTiming));
+  }
+  CUDA_OK(cudaEventRecord(m.ev_call, s));
+  CUDA_OK(cudaStreamWaitEvent(m.side, m.ev_call, 0));
+  for (size_t i = 0; i < m.layers.size(); ++i) {
+    Layer& L = *m.layers[i];
+    if (L.list_state != 0 || !uses_tc(m, L, bs[i])) continue;
+    if (!L.list_ev) CUDA_OK(cudaEventCreateWithFlags(&L.list_ev, cudaEventDisableTiming));
+    CUDA_OK(launch_tc_list(L.dev, m.side));
+    CUDA_OK(cudaEventRecord(L.list_ev, m.side));
+    L.list_state = 1;
+  }
 }
 
 // CONV layer on an NHWC fp32 batch: decode the filters into
@@ -728,6 +800,7 @@ void profile(Model& m, int Bmax, int reps) {
   for (int i = 0; i < f; ++i) {
     Layer& L = *m.layers[i];
     auto step = [&](int B) {
+      L.list_state = 0;  // every timed call decodes its list
       if (L.is_conv())
         conv_forward(m, L, xb.as<float>(), B, yb.as<float>(), s);
       else
@@ -748,6 +821,8 @@ void profile(Model& m, int Bmax, int reps) {
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  CUDA_OK(cudaStreamSynchronize(s));
+  for (auto& L : m.layers) L->list_state = 0;  // profiling's lists are not the caller's
   m.prof_bmax = Bmax;
 }
 
@@ -855,6 +930,10 @@ void cdn_model_destroy(cdn_model* h) {
     h->m.layers.clear();
     h->m.lvl.clear();
     if (h->m.comm) ncclCommDestroy(h->m.comm);
+    if (h->m.side) cudaStreamSynchronize(h->m.side);
+    h->m.layers.clear();
+    if (h->m.side) cudaStreamDestroy(h->m.side);
+    if (h->m.ev_call) cudaEventDestroy(h->m.ev_call);
     if (h->m.stream) cudaStreamDestroy(h->m.stream);
   } catch (...) {
   }
@@ -924,6 +1003,7 @@ cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* score
   struct Clear { bool& b; ~Clear() { b = false; } } clr{m.busy};
   CUDA_OK(cudaSetDevice(m.device));
   cudaStream_t s = pick(m, stream);
+  struct Lists { Model& m; cudaStream_t s; ~Lists() { reset_lists(m, s); } } lists{m, s};
   const int f = (int)m.layers.size();
   int o = 0;
   while (o < K) {
@@ -949,6 +1029,7 @@ cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* score
     }
     check_chain(m, bs);
     alloc_levels(m, bs);
+    prelaunch_lists(m, bs, s);
     Exec ex{m, bs, input, on_device != 0, s, scores};
     const int Bf = bs.back();
     const int rounds = rem / Bf;
@@ -970,6 +1051,8 @@ cdn_status cdn_layer_forward(cdn_model* h, int layer, const float* x, int ldx, i
   if (L.is_conv()) return fail(CDN_E_ARG, "CONV layer: use cdn_conv_forward");
   if (ldx < B || ldy < B) return fail(CDN_E_ARG, "leading dimension < B");
   cudaStream_t s = pick(m, stream);
+  struct Lists { Model& m; cudaStream_t s; ~Lists() { reset_lists(m, s); } } lists{m, s};
+  reset_lists(m, s);  // a single-layer call decodes its own list
   fc_forward(m, L, x, ldx, B, y, ldy, s);
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
   API_END

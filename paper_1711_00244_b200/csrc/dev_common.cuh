@@ -15,6 +15,11 @@ static __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
   return v;
 }
 
+// if (pred) v = *p, with the load targeting v's own register
+static __device__ __forceinline__ void ldg_u32_if(uint32_t& v, const uint32_t* p, uint32_t pred) {
+  asm("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.global.nc.u32 %0, [%1]; }" : "+r"(v) : "l"(p), "r"(pred));
+}
+
 // Canonical decode of a code longer than the LUT width (rare).  tab[0..32] =
 // first_code per length, tab[33..65] = count, tab[66..98] = first index into
 // the canonically sorted symbols.  Returns (len << 16) | sym.
@@ -61,13 +66,14 @@ struct PReader {
   }
 };
 
-// Lean MSB-first reader for the band kernel's decode lanes: a two-word window
-// (w0:w1) plus two prefetched words, so a one-word advance uses data loaded two
-// words (~10 tokens) earlier.  skip(n) for n <= 32.
-// Requires >= 4 words of tail padding.
+// Lean MSB-first reader for decode lanes: a two-word window (w0:w1) plus
+// four words in flight, so the word moved into the window on an advance was
+// requested four advances (~128 bits, tens of tokens) earlier -- a shallower
+// queue lets the predicated register rotation wait on L2 latency every few
+// steps.  skip(n) for n <= 32.  Requires >= 6 words of tail padding.
 struct SReader {
   const uint32_t* p;  // next word to prefetch
-  uint32_t off, w0, w1, n1, n2;
+  uint32_t off, w0, w1, n1, n2, n3, n4;
   __device__ __forceinline__ void init(const uint32_t* words, uint32_t bit) {
     p = words + (bit >> 5);
     off = bit & 31;
@@ -75,19 +81,27 @@ struct SReader {
     w1 = ldg_u32(p + 1);
     n1 = ldg_u32(p + 2);
     n2 = ldg_u32(p + 3);
-    p += 4;
+    n3 = ldg_u32(p + 4);
+    n4 = ldg_u32(p + 5);
+    p += 6;
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
   __device__ __forceinline__ void skip(uint32_t n) {
     off += n;
-    if (off >= 32) {
+    const uint32_t adv = off >= 32;
+    if (adv) {
       off -= 32;
       w0 = w1;
       w1 = n1;
       n1 = n2;
-      n2 = ldg_u32(p);
-      ++p;
+      n2 = n3;
+      n3 = n4;
     }
+    // predicated load straight into n4: a plain `n4 = ldg(p)` lets the compiler
+    // load into a temporary and MOV it into n4 a few instructions later, which
+    // waits for the load there and defeats the prefetch
+    ldg_u32_if(n4, p, adv);
+    p += adv;
   }
 };
 

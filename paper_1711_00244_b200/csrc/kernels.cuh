@@ -17,7 +17,7 @@ inline cudaError_t launched(int n = 1) {
 }
 
 constexpr int kLutMaxBits = 10;   // plain LUT width cap (decode kernel); longer codes take the canonical slow path
-constexpr int kTcChunk = 8;       // K tiles per decode task of the tensor-core path's list decoder
+constexpr int kTcChunk = 8;       // max K tiles per decode task of the tensor-core path's list decoder
 constexpr int kFoldLutBits = 11;  // pad-folding val LUT width (fused forward)
 constexpr uint32_t kFoldSlow = 0xFFFFFFFFu;
 constexpr int kMaxBatchTiles = 1024;
@@ -63,6 +63,7 @@ struct FcDev {
   const uint32_t* tbase = nullptr;
   const uint16_t* troff = nullptr;
   uint16_t* tlist = nullptr;
+  int tch = kTcChunk;                // K tiles per list-decoder task (fewer for small / dense layers)
   // small-batch multi-symbol LUTs (small.cu): 2^msLv / 2^msLg entries
   const uint32_t* msv = nullptr;
   const uint32_t* msg = nullptr;
@@ -88,11 +89,15 @@ struct TcPlan {
 };
 bool tc_supported(const FcDev& L);
 TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms);
+// list decoder of the tensor-core path (k_tc_list[_ms]): fills L.tlist from the
+// compressed streams; launch_fc_tc reads it (the caller orders the two)
+cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s);
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, int* tctr, cudaStream_t s);
 
 // Small-batch multi-symbol kernel (B <= 8; r <= 5, k <= 4, 32-bit lane records).
 bool ms_supported(const FcDev& L);
+size_t ms_smem_bytes(const FcDev& L);  // dynamic smem of the multi-symbol LUT kernels
 cudaError_t launch_fc_ms(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu, cudaStream_t s,
                          int num_sms);
 int band_rows_per_unit();

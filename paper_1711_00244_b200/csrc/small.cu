@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kMsThreads, 4) k_fc_ms(FcDev L, const float* _
       // idle lane: the refill code still runs (uncommitted); keep the readers
       // in a state whose skip(0) never loads
       vr.p = L.vw;
-      vr.off = vr.w0 = vr.w1 = vr.n1 = vr.n2 = 0;
+      vr.off = vr.w0 = vr.w1 = vr.n1 = vr.n2 = vr.n3 = vr.n4 = 0;
       gr = vr;
     }
     float acc[BS];
@@ -229,11 +229,6 @@ __global__ void __launch_bounds__(kMsThreads, 4) k_fc_ms(FcDev L, const float* _
   }
 }
 
-size_t ms_smem_bytes(const FcDev& L) {
-  size_t b = (sizeof(uint32_t) << L.msLv) + (sizeof(uint32_t) << L.msLg) + 2 * 99 * sizeof(uint32_t) +
-             sizeof(uint16_t) * (L.nvs + 1) + sizeof(uint16_t) * (L.ngs + 1);
-  return (b + 15) & ~(size_t)15;
-}
 
 template <int BS, bool VEC>
 cudaError_t launch_ms_t(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy, int relu, cudaStream_t s,
@@ -267,6 +262,12 @@ cudaError_t launch_ms_bs(const FcDev& L, const float* x, int ldx, int B, float* 
 }
 
 }  // namespace
+
+size_t ms_smem_bytes(const FcDev& L) {
+  size_t b = (sizeof(uint32_t) << L.msLv) + (sizeof(uint32_t) << L.msLg) + 2 * 99 * sizeof(uint32_t) +
+             sizeof(uint16_t) * (L.nvs + 1) + sizeof(uint16_t) * (L.ngs + 1);
+  return (b + 15) & ~(size_t)15;
+}
 
 bool ms_supported(const FcDev& L) {
   return L.msv && L.msg && L.ncb <= 32 && L.k <= 4 && !L.rec64;

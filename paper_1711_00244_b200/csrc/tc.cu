@@ -398,6 +398,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
       }
       (void)ld;
       const float bias = (a.S == 1 && row < L.nrows) ? L.bias[row] : 0.f;
+      // y rows are contiguous over the batch: whole float4s where the tile is inside B
+      const bool vec_ok = (a.ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
       for (int c = 0; c < kTN; c += 16) {
         float v[16];
         tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c, v);
@@ -409,11 +411,17 @@ __global__ void __launch_bounds__(kTThreads, 1)
           if (row < L.nrows) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              if (b0 + c + i < a.B) {
-                float o = v[i] + bias;
-                if (a.relu) o = fmaxf(o, 0.f);
-                dst[c + i] = o;
-              }
+              v[i] += bias;
+              if (a.relu) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (vec_ok && b0 + c + 16 <= a.B) {
+#pragma unroll
+              for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (b0 + c + i < a.B) dst[c + i] = v[i];
             }
           }
         } else {
@@ -435,25 +443,38 @@ __global__ void __launch_bounds__(kTThreads, 1)
           s_last[0] = is_last;
         }
         named_bar_sync(kEpiBar, kEpiW * 32);
-        if (s_last[0] && row < L.nrows) {
+        if (s_last[0]) {
+          // the last CTA of the tile sums the S partials in split order (deterministic):
+          // a warp per row, the lanes along the batch (8 columns each), coalesced
           __threadfence();
-          const float bias2 = L.bias[row];
-          const float* base = a.ws + ((size_t)t.tile * a.S * kTM + row_l) * kTN;
-          float* yp = a.y + (size_t)row * a.ldy + b0;
-          for (int c = 0; c < kTN; c += 4) {
-            float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+          const float* base = a.ws + (size_t)t.tile * a.S * kTM * kTN + 8 * lane;
+          const int cb = b0 + 8 * lane;  // first batch column of this lane
+          for (int rr = ew; rr < kTM; rr += kEpiW) {
+            const int rw = t.rt * kTM + rr;
+            if (rw >= L.nrows) break;
+            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
             for (int j = 0; j < a.S; ++j) {
-              const float4 p = __ldcg(reinterpret_cast<const float4*>(base + (size_t)j * kTM * kTN + c));
-              sum.x += p.x; sum.y += p.y; sum.z += p.z; sum.w += p.w;
+              const float* p = base + ((size_t)j * kTM + rr) * kTN;
+              const float4 p0 = __ldcg(reinterpret_cast<const float4*>(p));
+              const float4 p1 = __ldcg(reinterpret_cast<const float4*>(p + 4));
+              s0.x += p0.x; s0.y += p0.y; s0.z += p0.z; s0.w += p0.w;
+              s1.x += p1.x; s1.y += p1.y; s1.z += p1.z; s1.w += p1.w;
             }
-            const float o4[4] = {sum.x, sum.y, sum.z, sum.w};
+            const float bs = L.bias[rw];
+            float o[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (b0 + c + i < a.B) {
-                float o = o4[i] + bias2;
-                if (a.relu) o = fmaxf(o, 0.f);
-                yp[c + i] = o;
-              }
+            for (int i = 0; i < 8; ++i) {
+              o[i] += bs;
+              if (a.relu) o[i] = fmaxf(o[i], 0.f);
+            }
+            float* yp = a.y + (size_t)rw * a.ldy + cb;
+            if (vec_ok && cb + 8 <= a.B) {
+              *reinterpret_cast<float4*>(yp) = make_float4(o[0], o[1], o[2], o[3]);
+              *reinterpret_cast<float4*>(yp + 4) = make_float4(o[4], o[5], o[6], o[7]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (cb + i < a.B) yp[i] = o[i];
             }
           }
         }
@@ -467,23 +488,45 @@ __global__ void __launch_bounds__(kTThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
-// X fp32 feature-major [K][ldx] -> bf16 hi / lo image-major [B][ldk] (K contiguous)
-__global__ void k_split_x(const float* __restrict__ x, int K, int ldx, int B, __nv_bfloat16* __restrict__ xh,
-                          __nv_bfloat16* __restrict__ xl, int ldk) {
-  __shared__ float tile[32][33];
-  const int k0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int k = k0 + i, b = b0 + threadIdx.x;
-    tile[i][threadIdx.x] = (k < K && b < B) ? x[(size_t)k * ldx + b] : 0.f;
+// X fp32 feature-major [K][ldx] -> bf16 hi / lo image-major [B][ldk] (K contiguous).
+// Tile = 64 k x 32 images: coalesced 128-byte row loads, then each thread
+// converts 8 consecutive k of one image and writes them as one 16-byte store
+// per half (8 lanes cover a 128-byte run of an image row).
+constexpr int kSplitK = 64, kSplitB = 32;
+__global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, int K, int ldx, int B,
+                                                 __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl,
+                                                 int ldk) {
+  __shared__ float tile[kSplitK][kSplitB + 1];
+  const int k0 = blockIdx.x * kSplitK, b0 = blockIdx.y * kSplitB;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+#pragma unroll
+  for (int i = ty; i < kSplitK; i += 8) {
+    const int k = k0 + i, b = b0 + tx;
+    tile[i][tx] = (k < K && b < B) ? __ldg(x + (size_t)k * ldx + b) : 0.f;
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int b = b0 + i, k = k0 + threadIdx.x;
-    if (b < B && k < ldk) {
-      const float v = tile[threadIdx.x][i];
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      xh[(size_t)b * ldk + k] = hi;
-      xl[(size_t)b * ldk + k] = __float2bfloat16_rn(v - __bfloat162float(hi));
+  const int c = threadIdx.x & 7, bl = threadIdx.x >> 3;  // k chunk (8 values), image
+  const int b = b0 + bl, k = k0 + 8 * c;
+  if (b >= B || k >= ldk) return;
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float v0 = tile[8 * c + 2 * i][bl], v1 = tile[8 * c + 2 * i + 1][bl];
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(v0), h1 = __float2bfloat16_rn(v1);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(v0 - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(v1 - __bfloat162float(h1));
+    h[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+    l[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+  }
+  __nv_bfloat16* ph = xh + (size_t)b * ldk + k;
+  __nv_bfloat16* pl = xl + (size_t)b * ldk + k;
+  if (k + 8 <= ldk) {  // ldk % 8 == 0 and k % 8 == 0: 16-byte aligned
+    *reinterpret_cast<uint4*>(ph) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(pl) = make_uint4(l[0], l[1], l[2], l[3]);
+  } else {
+    for (int i = 0; i < 8 && k + i < ldk; ++i) {
+      ph[i] = __ushort_as_bfloat16((unsigned short)(h[i >> 1] >> (16 * (i & 1))));
+      pl[i] = __ushort_as_bfloat16((unsigned short)(l[i >> 1] >> (16 * (i & 1))));
     }
   }
 }
@@ -514,16 +557,17 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
   for (int i = threadIdx.x; i < L.nvs; i += blockDim.x) s_vsorted[i] = L.vsorted[i];
   for (int i = threadIdx.x; i < L.ngs; i += blockDim.x) s_gsorted[i] = L.gsorted[i];
   __syncthreads();
-  // task = (row tile, chunk of kTcChunk K tiles, row in tile): consecutive
+  // task = (row tile, chunk of L.tch <= kTcChunk K tiles, row in tile): consecutive
   // threads write adjacent slices of the same blocks
-  const int nch = (L.tNI + kTcChunk - 1) / kTcChunk;
+  const int tch = L.tch;
+  const int nch = (L.tNI + tch - 1) / tch;
   const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
   const int r = (int)(task & 127);
   const size_t rc = task >> 7;
-  const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * kTcChunk;
+  const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
   const int row = rt * 128 + r;
   if (row >= L.nrows) return;
-  const int nk = L.tNI - kt0 < kTcChunk ? L.tNI - kt0 : kTcChunk;
+  const int nk = L.tNI - kt0 < tch ? L.tNI - kt0 : tch;
   // output slot of this row's first entry in each of the chunk's tiles
   uint32_t p[kTcChunk], n = 0;
 #pragma unroll
@@ -588,6 +632,139 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
   }
 }
 
+
+// Multi-symbol variant of the list decoder (r <= 5, k <= 4: the layers the
+// small-batch kernel's LUTs serve, small.cu): one lookup on the val stream
+// yields up to 4 codes, one on the gap stream up to 6; the two queues are
+// consumed up to 4 tokens per step, a pad being a token whose gap advances the
+// column by 2^k and whose symbol 0 emits nothing (C-01, C-04).
+__global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* s_vl = sm;
+  uint32_t* s_gl = s_vl + (1 << L.msLv);
+  uint32_t* s_vtab = s_gl + (1 << L.msLg);
+  uint32_t* s_gtab = s_vtab + 99;
+  uint16_t* s_vsorted = reinterpret_cast<uint16_t*>(s_gtab + 99);
+  uint16_t* s_gsorted = s_vsorted + (L.nvs + 1);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+    const uint32_t vb = 4u << L.msLv, gb = 4u << L.msLg;
+    mbar_arrive_expect_tx(&s_bar, vb + gb);
+    bulk_g2s(s_vl, L.msv, vb, &s_bar);
+    bulk_g2s(s_gl, L.msg, gb, &s_bar);
+  }
+  for (int i = threadIdx.x; i < 99; i += blockDim.x) { s_vtab[i] = L.vtab[i]; s_gtab[i] = L.gtab[i]; }
+  for (int i = threadIdx.x; i < L.nvs; i += blockDim.x) s_vsorted[i] = L.vsorted[i];
+  for (int i = threadIdx.x; i < L.ngs; i += blockDim.x) s_gsorted[i] = L.gsorted[i];
+  __syncthreads();
+  mbar_wait(&s_bar, 0);
+  const int tch = L.tch;
+  const int nch = (L.tNI + tch - 1) / tch;
+  const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
+  const int r = (int)(task & 127);
+  const size_t rc = task >> 7;
+  const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
+  const int row = rt * 128 + r;
+  if (row >= L.nrows) return;
+  const int nk = L.tNI - kt0 < tch ? L.tNI - kt0 : tch;
+  uint32_t p[kTcChunk], left = 0;
+#pragma unroll
+  for (int k = 0; k < kTcChunk; ++k) {
+    p[k] = 0;
+    if (k < nk) {
+      const size_t blk = (size_t)rt * L.tNI + kt0 + k;
+      const uint32_t o0 = L.troff[blk * 129 + r], o1 = L.troff[blk * 129 + r + 1];
+      p[k] = L.tbase[blk] + o0;
+      left += o1 - o0;
+    }
+  }
+  if (left == 0) return;
+  const size_t q = (size_t)row * L.tNI + kt0;
+  const uint2 st = L.tivg[q];
+  // the task's bits end where the next chunk (or the row) starts: pull all of
+  // its stream lines into L2 at once, so the reader's refills never wait on HBM
+  const uint2 en = kt0 + nk < L.tNI ? L.tivg[q + nk] : make_uint2(L.rp[2 * row + 2], L.rp[2 * row + 3]);
+  for (uint32_t l = st.x >> 10; l <= (en.x + 64) >> 10; ++l)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(L.vw + (size_t)l * 32));
+  for (uint32_t l = st.y >> 10; l <= (en.y + 64) >> 10; ++l)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(L.gw + (size_t)l * 32));
+  int col = kt0 * 64 - (int)(L.tivm[q] & 0xFFu) - 1;
+  SReader vr, gr;
+  vr.init(L.vw, st.x);
+  gr.init(L.gw, st.y);
+  const int vsh = 32 - L.msLv, gsh = 32 - L.msLg;
+  uint64_t qv = 0, qg = 0;
+  int cv = 0, cg = 0;
+  int ck = -1;
+  uint32_t pos = 0;
+  while (left > 0) {
+    {  // refill the symbol queue (up to 4 codes per lookup)
+      const uint32_t w = vr.peek();
+      const uint32_t e = s_vl[w >> vsh];
+      uint32_t n = e & 7u, len = (e >> 3) & 31u, syms = e >> 8;
+      if (n == 0) {
+        const uint32_t x = slow_sym(w, L.msLv + 1, s_vtab, s_vsorted, L.vmax);
+        n = 1;
+        len = x >> 16;
+        syms = x & 31u;
+      }
+      const bool room = cv <= 8;
+      qv |= (uint64_t)(room ? syms : 0u) << (5 * cv);
+      cv += room ? (int)n : 0;
+      vr.skip(room ? len : 0u);
+    }
+    {  // refill the gap queue (up to 6 codes per lookup)
+      const uint32_t w = gr.peek();
+      const uint32_t e = s_gl[w >> gsh];
+      uint32_t n = e & 7u, len = (e >> 3) & 31u, gaps = e >> 8;
+      if (n == 0) {
+        const uint32_t x = slow_sym(w, L.msLg + 1, s_gtab, s_gsorted, L.gmax);
+        n = 1;
+        len = x >> 16;
+        gaps = x & 15u;
+      }
+      const bool room = cg <= 10;
+      qg |= (uint64_t)(room ? gaps : 0u) << (4 * cg);
+      cg += room ? (int)n : 0;
+      gr.skip(room ? len : 0u);
+    }
+    const int pn = min(min(cv, cg), 4);
+    const uint32_t qv32 = (uint32_t)qv, qg32 = (uint32_t)qg;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < pn) {
+        col += (int)((qg32 >> (4 * j)) & 15u) + 1;  // c = prev + g + 1 (Alg. 1 l.7, C-01)
+        const uint32_t sym = (qv32 >> (5 * j)) & 31u;
+        if (sym != 0 && left > 0) {
+          const int k = (col >> 6) - kt0;
+          if (k != ck) {
+            ck = k;
+            pos = p[0];
+#pragma unroll
+            for (int jj = 1; jj < kTcChunk; ++jj) pos = k == jj ? p[jj] : pos;
+          }
+          L.tlist[pos++] = (uint16_t)((col & 63) | (sym << 6));
+          --left;
+        }
+      }
+    }
+    qv >>= 5 * pn;
+    qg >>= 4 * pn;
+    cv -= pn;
+    cg -= pn;
+  }
+}
+
+bool list_fold_forced() {
+  static const bool v = [] {
+    const char* e = std::getenv("CDN_TC_LIST");
+    return e && e[0] == 'f';
+  }();
+  return v;
+}
+
 }  // namespace
 
 bool tc_supported(const FcDev& L) {
@@ -625,15 +802,30 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   return p;
 }
 
+cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  const size_t tasks = (size_t)((L.nrows + 127) / 128) * ((L.tNI + L.tch - 1) / L.tch) * 128;
+  const unsigned lgrid = (unsigned)((tasks + kListThreads - 1) / kListThreads);
+  if (ms_supported(L) && !list_fold_forced()) {
+    const size_t lsm = ms_smem_bytes(L);
+    static size_t set_lsm = 0;
+    if (lsm > set_lsm) {
+      e = cudaFuncSetAttribute(k_tc_list_ms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
+      if (e != cudaSuccess) return e;
+      set_lsm = lsm;
+    }
+    k_tc_list_ms<<<lgrid, kListThreads, lsm, s>>>(L);
+  } else {
+    k_tc_list<<<lgrid, kListThreads, 0, s>>>(L);
+  }
+  return launched();
+}
+
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, int* tctr, cudaStream_t s) {
-  dim3 sg((p.ldk + 31) / 32, (B + 31) / 32), sb(32, 8);
-  k_split_x<<<sg, sb, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
+  dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
+  k_split_x<<<sg, 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
   cudaError_t e = launched();
-  if (e != cudaSuccess) return e;
-  const size_t tasks = (size_t)((L.nrows + 127) / 128) * ((L.tNI + kTcChunk - 1) / kTcChunk) * 128;
-  k_tc_list<<<(unsigned)((tasks + kListThreads - 1) / kListThreads), kListThreads, 0, s>>>(L);
-  e = launched();
   if (e != cudaSuccess) return e;
   CUtensorMap th, tl;
   e = encode_tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xh, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,

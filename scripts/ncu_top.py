@@ -1,13 +1,19 @@
 """Summarise an ncu report: stall reasons and the hottest SASS lines.
-Usage: python scripts/ncu_top.py report.ncu-rep [n]"""
+Usage: python scripts/ncu_top.py report.ncu-rep [n] [--kernel REGEX]"""
 import csv
 import io
 import subprocess
 import sys
 
-rep = sys.argv[1]
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+args = [a for a in sys.argv[1:]]
+kfilt = []
+if "--kernel" in args:
+    i = args.index("--kernel")
+    kfilt = ["-k", "regex:" + args[i + 1]]
+    del args[i:i + 2]
+rep = args[0]
+n = int(args[1]) if len(args) > 1 else 40
+raw = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
 d = dict(zip(r[0], r[2]))
 st = sorted(((k, float(v.replace(",", "") or 0)) for k, v in d.items()
@@ -20,12 +26,21 @@ for k in ["gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__throughput.a
           "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "sm__warps_active.avg.pct_of_peak_sustained_active"]:
     if k in d:
         print(f"  {k} = {d[k]}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+src = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 h = rows[1]
-data = rows[2:]
+def _num(x):
+    try:
+        float(x[i_s] or 0)
+        return True
+    except (ValueError, IndexError):
+        return False
+
+
+data = None
 i_s = h.index("Warp Stall Sampling (All Samples)")
+data = [x for x in rows[2:] if _num(x)]
 i_src = h.index("Source")
 i_ex = h.index("Instructions Executed")
 tot = sum(float(x[i_s] or 0) for x in data) or 1
