@@ -165,6 +165,9 @@ def run_ours(args):
         step()
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # live per-kernel durations inside the timed steps (library CUDA events on the launch stream)
+    cdn.kernel_timer(True)
+    launches0 = cdn.kernel_launches()
     with Clocks(local) as clk:
         for i in range(args.steps):
             flush.zero_()                      # L2 flush between timed iterations
@@ -173,6 +176,10 @@ def run_ours(args):
             step()
             ev[i][1].record(stream)
         barrier()
+    launches = cdn.kernel_launches() - launches0
+    ktimes = {k: cdn.kernel_time(k) for k in ("k_fc_tc", "k_tc_list", "k_split_x", "k_fc_band", "k_fc_ms",
+                                              "k_fc_fold")}
+    cdn.kernel_timer(False)
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     tot_ms = float(sum(step_ms))
     if world > 1:
@@ -221,33 +228,46 @@ def run_ours(args):
             torch.cuda.synchronize(dev)
             if r >= 2:
                 lay_ms[i] += e0.elapsed_time(e1) / reps
-    dom = int(np.argmax(lay_ms))
-    st = stats[dom]
-    nloc = st["row_end"] - st["row_begin"]
-    flops = 2.0 * st["nnz"] * B + nloc * B
-    bytes_algo = st["algo_bytes_fixed"] + 4.0 * st["cols"] * B + 4.0 * nloc * B
+    # ---- roofline of the dominant kernel: its algorithmic work per launch (summed
+    # over the layers it ran in the timed steps) / its live CUDA-event durations
     pk = peaks()
     sm_mhz_max = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * 2 * sm_mhz_max * 1e6 / 1e12      # fp32 FMA TFLOP/s
-    t_s = lay_ms[dom] / 1e3
-    ai = flops / bytes_algo
-    if ai * pk["hbm_gbs"] * 1e9 > alu_peak * 1e12:            # compute-bound
-        roof = {"bound": "alu", "achieved": flops / t_s / 1e12, "peak": alu_peak, "unit": "TFLOP/s"}
+    kern_of = [m.kernel_name(i, B) for i in range(len(specs))]
+    dom_k = max((k for k in ktimes if ktimes[k][1] > 0), key=lambda k: ktimes[k][0])
+    k_ms, k_n = ktimes[dom_k]
+    lay = [i for i in range(len(specs)) if kern_of[i] == dom_k]
+    def nloc_of(i):
+        return stats[i]["row_end"] - stats[i]["row_begin"]
+    useful = sum(2.0 * stats[i]["nnz"] * B + nloc_of(i) * B for i in lay) * args.steps
+    t_s = k_ms / 1e3
+    if dom_k == "k_fc_tc":
+        # a dense contraction after decode: the tensor cores execute 3 bf16 passes
+        # (hi*hi + hi*lo + lo*hi) over the 128-row x 64-col tiles and 256-image tiles
+        def dense(i):
+            kpad = (specs[i].cols + 63) // 64 * 64
+            return 3 * 2.0 * (-(-nloc_of(i) // 128) * 128) * kpad * (-(-B // 256) * 256)
+        work = sum(dense(i) for i in lay) * args.steps
+        peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1392.1)))
+        roof = {"bound": "tensor", "achieved": work / t_s / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "useful_tflops": useful / t_s / 1e12,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, back to back); "
+                               "achieved = executed 3-pass bf16 tile flops (DESIGN.md)"}
+    elif dom_k == "k_fc_band":
+        roof = {"bound": "alu", "achieved": useful / t_s / 1e12, "peak": alu_peak, "unit": "TFLOP/s",
+                "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz; achieved = 2*nnz*B + N*B"}
     else:
-        roof = {"bound": "hbm", "achieved": bytes_algo / t_s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+        byt = sum(stats[i]["algo_bytes_fixed"] + 4.0 * stats[i]["cols"] * B + 4.0 * nloc_of(i) * B
+                  for i in lay) * args.steps
+        roof = {"bound": "hbm", "achieved": byt / t_s / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    kname = m.kernel_name(dom, B)
-    roof["kernel"] = f"{kname} ({specs[dom].name}, B={B})"
-    roof["traffic"] = _traffic(roof["kernel"])
-    if kname == "k_fc_tc":
-        # context: the dense 3-pass bf16 tile work the tensor cores actually execute
-        kpad = (specs[dom].cols + 63) // 64 * 64
-        dense = 3 * 2.0 * (-(-nloc // 128) * 128) * kpad * (-(-B // 256) * 256)
-        roof["executed_tensor_tflops"] = dense / t_s / 1e12
-        roof["executed_tensor_frac_of_bf16_peak"] = dense / t_s / 1e12 / pk.get("bf16_tflops", 1667.2)
-    roof["ms"] = lay_ms[dom]
-    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs / alu: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz; "
-                           "achieved = algorithmic flops 2*nnz*B + N*B (both FC kernels)")
+    roof["kernel"] = f"{dom_k} ({'/'.join(specs[i].name for i in lay)}, B={B})"
+    roof["launches"] = k_n
+    roof["avg_launch_us"] = k_ms / max(k_n, 1) * 1e3
+    roof["share_of_step"] = k_ms / tot_ms
+    roof["traffic"] = _traffic(dom_k, [specs[i].name for i in lay], B)
+    roof["kernels_ms_per_step"] = {k: v[0] / args.steps for k, v in ktimes.items() if v[1]}
 
     # ---- B = 1 cold-L2 decode-bound measurement (HBM roofline on compressed bytes)
     b1 = None
@@ -274,7 +294,7 @@ def run_ours(args):
         "compressed_bytes": comp_bytes,
         "e2e": {"value": images / (e_ms / 1e3), "unit": "images/s",
                 "h2d_bytes_per_step": int(a.nbytes), "d2h_bytes_per_step": int(B * N_out * 4)},
-        "gpu_launches": 5 * args.steps,
+        "gpu_launches": launches,
         "roofline": roof,
         "layer_ms": {s.name: float(t) for s, t in zip(specs, lay_ms)},
         "clocks": clk.summary(),
@@ -292,14 +312,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernel from the committed `ncu --set full` capture (profiles/traffic.json,
-    written from the .ncu-rep named there); None if absent or for another kernel."""
+def _traffic(kernel, layers, B):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`,
+    averaged over the layers it ran, from the committed `ncu --set full`
+    captures (profiles/traffic.json, keys "kernel (layer, B=..)", each naming
+    its .ncu-rep); None if a capture is missing."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        e = t.get(kernel)
-        return None if e is None else e["dram_bytes"]
+        v = [t[f"{kernel} ({l}, B={B})"]["dram_bytes"] for l in layers]
+        return sum(v) / len(v)
     except Exception:
         return None
 

@@ -176,6 +176,14 @@ cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int 
  * models, all threads; a host-side counter, no device work).  *out receives
  * the count.  Errors: CDN_E_ARG (null out). */
 cdn_status cdn_debug_kernel_launches(uint64_t* out);
+/* Kernel timer (measurement hook): enable != 0 starts recording, 0 stops;
+ * either way the previous records are dropped.  While on, the library brackets
+ * each launch of its main kernels (k_fc_tc, k_tc_list, k_split_x, k_fc_band,
+ * k_fc_ms, k_fc_fold) with CUDA events on the launch stream.  Errors: none. */
+cdn_status cdn_debug_kernel_timer(int enable);
+/* Sum of the recorded durations of `kernel` (ms) and the number of launches
+ * recorded; waits for the recorded events.  Errors: CDN_E_ARG, CDN_E_CUDA. */
+cdn_status cdn_debug_kernel_timer_read(const char* kernel, double* total_ms, int* launches);
 
 /* ---- FC kernel policy (tuning / parity hook) ---------------------------
  * tc_min_batch: batches B >= this run the tensor-core kernel (W tiles decoded

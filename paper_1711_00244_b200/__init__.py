@@ -7,9 +7,9 @@ for device memory, streams and process groups.  There is no CPU fallback: if
 the library is missing or fails to load, importing the binding raises.
 """
 from .binding import (CDNError, LayerDesc, LayerStats, Model, abi_version, compress_dense, debug_gemm_bf16,
-                      kernel_launches,
+                      kernel_launches, kernel_time, kernel_timer,
                       debug_host_walk, debug_host_walk_shard, lib_path, load_library, nccl_unique_id, plan_dp)
 
 __all__ = ["CDNError", "LayerDesc", "LayerStats", "Model", "abi_version", "compress_dense",
-           "debug_host_walk", "debug_host_walk_shard", "kernel_launches", "lib_path", "load_library",
+           "debug_host_walk", "debug_host_walk_shard", "kernel_launches", "kernel_time", "kernel_timer", "lib_path", "load_library",
            "nccl_unique_id", "plan_dp"]

@@ -87,6 +87,8 @@ _SIGS = {
     "cdn_debug_gemm_bf16": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                         C.c_void_p, C.c_int, C.c_void_p]),
     "cdn_debug_kernel_launches": (C.c_int32, [C.POINTER(C.c_uint64)]),
+    "cdn_debug_kernel_timer": (C.c_int32, [C.c_int]),
+    "cdn_debug_kernel_timer_read": (C.c_int32, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     "cdn_model_memory_model": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cdn_layer_kernel_name": (C.c_char_p, [C.c_void_p, C.c_int, C.c_int]),
     "cdn_model_num_layers": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int)]),
@@ -180,6 +182,18 @@ def kernel_launches() -> int:
     out = C.c_uint64(0)
     _check(load_library().cdn_debug_kernel_launches(C.byref(out)))
     return int(out.value)
+
+
+def kernel_timer(enable: bool):
+    """Start (True) or stop (False) recording per-kernel CUDA-event durations; drops old records."""
+    _check(load_library().cdn_debug_kernel_timer(1 if enable else 0))
+
+
+def kernel_time(kernel: str):
+    """(total ms, launches) recorded for `kernel` since kernel_timer(True)."""
+    ms, n = C.c_double(0.0), C.c_int(0)
+    _check(load_library().cdn_debug_kernel_timer_read(kernel.encode(), C.byref(ms), C.byref(n)))
+    return float(ms.value), int(n.value)
 
 
 def debug_gemm_bf16(A, M: int, Wt, N: int, Kpad: int, bias, relu: bool, out, ldo: int, stream: int = 0):

@@ -1093,6 +1093,19 @@ cdn_status cdn_debug_gemm_bf16(const void* A, int M, const void* Wt, int N, int 
   API_END
 }
 
+cdn_status cdn_debug_kernel_timer(int enable) {
+  API_BEGIN
+  ktimer_enable(enable != 0);
+  API_END
+}
+
+cdn_status cdn_debug_kernel_timer_read(const char* kernel, double* total_ms, int* launches) {
+  API_BEGIN
+  if (!kernel || !total_ms || !launches) return fail(CDN_E_ARG, "null argument");
+  CUDA_OK(ktimer_read(kernel, total_ms, launches));
+  API_END
+}
+
 cdn_status cdn_debug_kernel_launches(uint64_t* out) {
   API_BEGIN
   if (!out) return fail(CDN_E_ARG, "null out");

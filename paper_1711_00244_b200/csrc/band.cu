@@ -478,8 +478,11 @@ cudaError_t launch_band_t(const FcDev& L, const BandPlan& p, const BandArgs& a, 
     if (e != cudaSuccess) return e;
     set_smem = p.smem;
   }
+  ktimer_begin("k_fc_band", s);
   kern<<<p.grid, kThreads, p.smem, s>>>(L, a, tmx);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_fc_band", s);
+  return e_;
 }
 
 }  // namespace

@@ -13,6 +13,10 @@
 //     real tokens (sym != 0) acc[b] += w * x[c][b] (l.9, Eq. 2);
 //   * the G partial sums of a row are reduced with a fixed shuffle tree
 //     (deterministic), then bias + ReLU and one store per (row, image).
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 #include <cuda_bf16.h>
 
 #include "dev_common.cuh"
@@ -21,6 +25,77 @@
 namespace cdn {
 
 std::atomic<unsigned long long> g_launches{0};
+
+namespace {
+struct KTimer {
+  std::mutex mu;
+  bool on = false;
+  std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  std::map<std::string, cudaEvent_t> open;
+};
+KTimer& kt() {
+  static KTimer* t = new KTimer();  // never destroyed: events may outlive static destruction order
+  return *t;
+}
+}  // namespace
+
+void ktimer_begin(const char* kernel, cudaStream_t s) {
+  KTimer& t = kt();
+  std::lock_guard<std::mutex> g(t.mu);
+  if (!t.on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, s);
+  t.open[kernel] = e;
+}
+
+void ktimer_end(const char* kernel, cudaStream_t s) {
+  KTimer& t = kt();
+  std::lock_guard<std::mutex> g(t.mu);
+  auto it = t.open.find(kernel);
+  if (!t.on || it == t.open.end()) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, s);
+  t.ev[kernel].emplace_back(it->second, e);
+  t.open.erase(it);
+}
+
+void ktimer_enable(bool on) {
+  KTimer& t = kt();
+  std::lock_guard<std::mutex> g(t.mu);
+  for (auto& kv : t.ev)
+    for (auto& p : kv.second) {
+      cudaEventSynchronize(p.second);
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+  t.ev.clear();
+  for (auto& kv : t.open) cudaEventDestroy(kv.second);
+  t.open.clear();
+  t.on = on;
+}
+
+cudaError_t ktimer_read(const char* kernel, double* total_ms, int* launches) {
+  KTimer& t = kt();
+  std::lock_guard<std::mutex> g(t.mu);
+  double tot = 0.0;
+  int n = 0;
+  auto it = t.ev.find(kernel);
+  if (it != t.ev.end())
+    for (auto& p : it->second) {
+      cudaError_t e = cudaEventSynchronize(p.second);
+      if (e != cudaSuccess) return e;
+      float ms = 0.f;
+      e = cudaEventElapsedTime(&ms, p.first, p.second);
+      if (e != cudaSuccess) return e;
+      tot += ms;
+      ++n;
+    }
+  *total_ms = tot;
+  *launches = n;
+  return cudaSuccess;
+}
 
 namespace {
 
@@ -458,8 +533,11 @@ cudaError_t launch_fc_t(const FcDev& L, const float* x, int ldx, int B, float* y
   const int units = (L.nrows + rows_per_warp - 1) / rows_per_warp;
   const int work = (units + threads / 32 - 1) / (threads / 32);
   dim3 grid(occupancy_grid(kern, threads, smem, num_sms, work), tiles);
+  ktimer_begin("k_fc_fold", s);
   kern<<<grid, threads, smem, s>>>(L, x, ldx, B, y, ldy, relu);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_fc_fold", s);
+  return e_;
 }
 
 template <int BS, bool REC64>

@@ -16,6 +16,14 @@ inline cudaError_t launched(int n = 1) {
   return cudaGetLastError();
 }
 
+// Debug kernel timer (cdn_debug_kernel_timer): when enabled, the launchers
+// bracket their main kernel with CUDA events on the launch stream, so a caller
+// can read each kernel's live duration inside its own workload.
+void ktimer_begin(const char* kernel, cudaStream_t s);
+void ktimer_end(const char* kernel, cudaStream_t s);
+void ktimer_enable(bool on);  // (re)starts with no records
+cudaError_t ktimer_read(const char* kernel, double* total_ms, int* launches);
+
 constexpr int kLutMaxBits = 10;   // plain LUT width cap (decode kernel); longer codes take the canonical slow path
 constexpr int kTcChunk = 8;       // max K tiles per decode task of the tensor-core path's list decoder
 constexpr int kFoldLutBits = 11;  // pad-folding val LUT width (fused forward)

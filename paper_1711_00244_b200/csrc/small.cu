@@ -249,8 +249,11 @@ cudaError_t launch_ms_t(const FcDev& L, const float* x, int ldx, int B, float* y
   const int need = (units + kMsThreads / 32 - 1) / (kMsThreads / 32);
   const int cap = per_sm * num_sms;
   dim3 grid(need < cap ? need : cap, (B + BS - 1) / BS);
+  ktimer_begin("k_fc_ms", s);
   kern<<<grid, kMsThreads, smem, s>>>(L, x, ldx, B, y, ldy, relu);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_fc_ms", s);
+  return e_;
 }
 
 template <int BS>

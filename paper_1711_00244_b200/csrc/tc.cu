@@ -814,18 +814,24 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       set_lsm = lsm;
     }
+    ktimer_begin("k_tc_list", s);
     k_tc_list_ms<<<lgrid, kListThreads, lsm, s>>>(L);
   } else {
+    ktimer_begin("k_tc_list", s);
     k_tc_list<<<lgrid, kListThreads, 0, s>>>(L);
   }
-  return launched();
+  e = launched();
+  ktimer_end("k_tc_list", s);
+  return e;
 }
 
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, int* tctr, cudaStream_t s) {
   dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
+  ktimer_begin("k_split_x", s);
   k_split_x<<<sg, 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
   cudaError_t e = launched();
+  ktimer_end("k_split_x", s);
   if (e != cudaSuccess) return e;
   CUtensorMap th, tl;
   e = encode_tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xh, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
@@ -848,8 +854,10 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   }
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
   TcArgs a{y, ldy, B, relu, ws, tctr, p.S, p.nbt, p.nrt, p.units, p.nkt, trace_path ? trace : nullptr};
+  ktimer_begin("k_fc_tc", s);
   k_fc_tc<<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
   e = launched();
+  ktimer_end("k_fc_tc", s);
   if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
     std::vector<unsigned long long> h(16 * 256);
     e = cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s);

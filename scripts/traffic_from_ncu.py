@@ -1,6 +1,6 @@
 """Record the DRAM traffic of one kernel launch from an `ncu --set full`
 report into profiles/traffic.json (read by bench.py for roofline.traffic).
-Usage: python scripts/traffic_from_ncu.py REPORT.ncu-rep "KERNEL LABEL" """
+Usage: python scripts/traffic_from_ncu.py REPORT.ncu-rep "KERNEL LABEL" [KERNEL_REGEX]"""
 import csv
 import io
 import json
@@ -9,7 +9,8 @@ import subprocess
 import sys
 
 rep, label = sys.argv[1], sys.argv[2]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", rep, *kf, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
 h, units, vals = r[0], r[1], r[2]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
