@@ -89,7 +89,6 @@ struct Layer {
     if (list_ev) cudaEventDestroy(list_ev);
   }
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
-  DBuf tctr;            // tensor-core kernel arrival counters
   std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band) measured at first use
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
@@ -544,11 +543,6 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       m.tc_xh.alloc(p.xsplit_elems * 2);
       m.tc_xl.alloc(p.xsplit_elems * 2);
       if (p.ws_floats) L.bws.alloc(p.ws_floats * sizeof(float));
-      const size_t need = sizeof(int) * (size_t)p.tiles;
-      if (L.tctr.n < need || !L.tctr.p) {
-        L.tctr.alloc(need);
-        CUDA_OK(cudaMemsetAsync(L.tctr.p, 0, need, s));
-      }
       if (L.list_state == 1) {
         CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
       } else if (L.list_state == 0) {
@@ -556,7 +550,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       }
       L.list_state = 2;
       CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<__nv_bfloat16*>(m.tc_xh.p),
-                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), L.tctr.as<int>(), s));
+                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), s));
       return;
     }
   }

@@ -67,20 +67,22 @@ constexpr int kWBufs = 2;           // TMEM W buffers per stream
 constexpr int kWCols = 64;          // TMEM columns per W buffer: hi 32 | lo 32
 constexpr int kEpiW = 4;            // epilogue warps
 constexpr int kTThreads = (2 + kStreams * kDecW + kEpiW) * 32;   // 448
-constexpr int kEpiBar = 1;
 constexpr int kTmemCols = 512;      // accumulator 256 + W buffers 4 x 64
 
 struct TcArgs {
   float* y;
   int ldy, B, relu;
-  float* ws;   // [tiles][S][128][256] partials (S > 1)
-  int* tctr;   // [tiles]
+  float* ws;   // [tiles][S][128][256] partials (S > 1), summed by k_tc_reduce
   int S, nbt, nrt, units, nkt;  // splits, batch tiles, row tiles, units, K tiles
   unsigned long long* trace;    // debug (env CDN_TC_TRACE): CTA 0 event clocks [event][256], else null
 };
 
 __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
-  if (a.trace != nullptr && blockIdx.x == 0 && i < 256) a.trace[ev * 256 + i] = clock64();
+  if (a.trace != nullptr && blockIdx.x == 0 && i < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[ev * 256 + i] = t;  // ns
+  }
 }
 
 struct TUnit {
@@ -141,9 +143,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
   uint64_t* tfull = wempty + kStreams * kWBufs;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
-  uint32_t* s_cbs = reinterpret_cast<uint32_t*>(s_last + 3);  // [ncb] bf16 hi | lo << 16
+  uint32_t* s_cbs = tmem_slot + 4;  // [ncb] bf16 hi | lo << 16
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) tc_trace(a, 5, 0);
   {
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int i = tid; i < L.ncb; i += nt) {
@@ -343,7 +345,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
             const uint32_t e = __ldg(cur + i);
             sts_u16_if(prow + rsw_off(row_l, e & 63u), (s_cbs[e >> 6] >> hsh) & 0xFFFFu, true);
           }
-          if (tr && q == 0) tc_trace(a, 1, kt - k0);
           {  // 8 conflict-free LDS.128 -> one tcgen05.st of 32 columns
             uint32_t r[32];
 #pragma unroll
@@ -351,9 +352,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
               const uint4 w4 = lds_u128(prow + ((uint32_t)(j ^ (row_l & 7)) << 4));
               r[4 * j] = w4.x; r[4 * j + 1] = w4.y; r[4 * j + 2] = w4.z; r[4 * j + 3] = w4.w;
             }
-            if (tr && q == 0) tc_trace(a, 14, kt - k0);
             tmem_st32(tw + (uint32_t)(h * (kWCols / 2)), r);
-            if (tr && q == 0) tc_trace(a, 6, kt - k0);
           }
           // back to a zero row
 #pragma unroll
@@ -363,7 +362,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
           }
           for (uint32_t i = kEnt; i < nnz; ++i) sts_u16_if(prow + rsw_off(row_l, __ldg(cur + i) & 63u), 0u, true);
         }
-        if (tr && q == 0) tc_trace(a, 7, kt - k0);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -433,53 +431,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);
-      if (a.S > 1) {
-        __threadfence();
-        named_bar_sync(kEpiBar, kEpiW * 32);
-        if (ew == 0 && lane == 0) {
-          const int old = atomicAdd(&a.tctr[t.tile], 1);
-          const int is_last = old == a.S - 1;
-          if (is_last) a.tctr[t.tile] = 0;
-          s_last[0] = is_last;
-        }
-        named_bar_sync(kEpiBar, kEpiW * 32);
-        if (s_last[0]) {
-          // the last CTA of the tile sums the S partials in split order (deterministic):
-          // a warp per row, the lanes along the batch (8 columns each), coalesced
-          __threadfence();
-          const float* base = a.ws + (size_t)t.tile * a.S * kTM * kTN + 8 * lane;
-          const int cb = b0 + 8 * lane;  // first batch column of this lane
-          for (int rr = ew; rr < kTM; rr += kEpiW) {
-            const int rw = t.rt * kTM + rr;
-            if (rw >= L.nrows) break;
-            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
-            for (int j = 0; j < a.S; ++j) {
-              const float* p = base + ((size_t)j * kTM + rr) * kTN;
-              const float4 p0 = __ldcg(reinterpret_cast<const float4*>(p));
-              const float4 p1 = __ldcg(reinterpret_cast<const float4*>(p + 4));
-              s0.x += p0.x; s0.y += p0.y; s0.z += p0.z; s0.w += p0.w;
-              s1.x += p1.x; s1.y += p1.y; s1.z += p1.z; s1.w += p1.w;
-            }
-            const float bs = L.bias[rw];
-            float o[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              o[i] += bs;
-              if (a.relu) o[i] = fmaxf(o[i], 0.f);
-            }
-            float* yp = a.y + (size_t)rw * a.ldy + cb;
-            if (vec_ok && cb + 8 <= a.B) {
-              *reinterpret_cast<float4*>(yp) = make_float4(o[0], o[1], o[2], o[3]);
-              *reinterpret_cast<float4*>(yp + 4) = make_float4(o[4], o[5], o[6], o[7]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (cb + i < a.B) yp[i] = o[i];
-            }
-          }
-        }
-        named_bar_sync(kEpiBar, kEpiW * 32);
-      }
+      if (ew == 0 && lane == 0) tc_trace(a, 14, 0);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -528,6 +480,39 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
       ph[i] = __ushort_as_bfloat16((unsigned short)(h[i >> 1] >> (16 * (i & 1))));
       pl[i] = __ushort_as_bfloat16((unsigned short)(l[i >> 1] >> (16 * (i & 1))));
     }
+  }
+}
+
+// K-split reduction (S > 1): y[row][b] = act(sum_j partial_j[row][b] + bias),
+// partials summed in split order (deterministic); one thread per 4 images of a
+// row, coalesced, over every tile at once.
+__global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, int S, int nbt, int nrows, int B,
+                                                   const float* __restrict__ bias, int relu, float* __restrict__ y,
+                                                   int ldy, int vec_ok, long total) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int c4 = (int)(i % (kTN / 4));
+  const long tr = i / (kTN / 4);  // tile * 128 + row in tile
+  const int r = (int)(tr % kTM);
+  const long tile = tr / kTM;
+  const int rt = (int)(tile / nbt), bt = (int)(tile % nbt);
+  const int row = rt * kTM + r, b = bt * kTN + 4 * c4;
+  if (row >= nrows || b >= B) return;
+  const float* p = ws + ((size_t)tile * S * kTM + r) * kTN + 4 * c4;
+  float4 acc = __ldcg(reinterpret_cast<const float4*>(p));
+  for (int j = 1; j < S; ++j) {
+    const float4 q = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * kTN));
+    acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+  }
+  const float bs = bias[row];
+  float o[4] = {acc.x + bs, acc.y + bs, acc.z + bs, acc.w + bs};
+  if (relu)
+    for (int k = 0; k < 4; ++k) o[k] = fmaxf(o[k], 0.f);
+  float* yp = y + (size_t)row * ldy + b;
+  if (vec_ok && b + 4 <= B) {
+    *reinterpret_cast<float4*>(yp) = make_float4(o[0], o[1], o[2], o[3]);
+  } else {
+    for (int k = 0; k < 4 && b + k < B; ++k) yp[k] = o[k];
   }
 }
 
@@ -826,7 +811,7 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
 }
 
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, int* tctr, cudaStream_t s) {
+                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s) {
   dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
   ktimer_begin("k_split_x", s);
   k_split_x<<<sg, 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
@@ -853,11 +838,18 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     if (e != cudaSuccess) return e;
   }
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
-  TcArgs a{y, ldy, B, relu, ws, tctr, p.S, p.nbt, p.nrt, p.units, p.nkt, trace_path ? trace : nullptr};
+  TcArgs a{y, ldy, B, relu, ws, p.S, p.nbt, p.nrt, p.units, p.nkt, trace_path ? trace : nullptr};
   ktimer_begin("k_fc_tc", s);
   k_fc_tc<<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
   e = launched();
   ktimer_end("k_fc_tc", s);
+  if (e == cudaSuccess && p.S > 1) {
+    const long total = (long)p.tiles * kTM * (kTN / 4);
+    const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+    k_tc_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(ws, p.S, p.nbt, L.nrows, B, L.bias, relu, y, ldy,
+                                                                   vec_ok, total);
+    e = launched();
+  }
   if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
     std::vector<unsigned long long> h(16 * 256);
     e = cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, s);
