@@ -501,7 +501,8 @@ int band_min_batch() {
 
 // One fused FC layer launch: the warp-specialised band kernel for large
 // batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
-void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s) {
+void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s,
+                bool x_im = false) {
   const int relu = L.desc.relu;
   // Default policy for B >= 128: both large-batch kernels are timed once at the
   // first call with this B and the faster is kept for the layer (autotune).
@@ -550,10 +551,11 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       }
       L.list_state = 2;
       CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<__nv_bfloat16*>(m.tc_xh.p),
-                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), s));
+                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), s, x_im));
       return;
     }
   }
+  if (x_im) throw Error(CDN_E_ARG, "internal: an image-major input needs the tensor-core path");
   if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
     BandPlan p = plan_fc_band(L.dev, x, ldx, B, m.num_sms);
     if (p.ok) {
@@ -662,10 +664,12 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
 }
 
 // One layer step: local rows -> (all-gather if world > 1) -> dst [rows][ld_dst].
-void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, int ld_dst, cudaStream_t s) {
+// x: feature-major [K][ldx], or image-major [B][ldx] when x_im (tensor-core layers only)
+void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, int ld_dst, cudaStream_t s,
+                bool x_im = false) {
   Layer& L = *m.layers[li];
   if (m.world == 1) {
-    fc_forward(m, L, x, ldx, B, dst, ld_dst, s);
+    fc_forward(m, L, x, ldx, B, dst, ld_dst, s, x_im);
     return;
   }
   const uint32_t rb = rows_per_rank(L.rows, m.world);
@@ -673,7 +677,7 @@ void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, in
   m.loc.alloc(slab * sizeof(float));
   m.gath.alloc(slab * m.world * sizeof(float));
   CUDA_OK(cudaMemsetAsync(m.loc.p, 0, slab * sizeof(float), s));
-  fc_forward(m, L, x, ldx, B, m.loc.as<float>(), B, s);
+  fc_forward(m, L, x, ldx, B, m.loc.as<float>(), B, s, x_im);
   NCCL_OK(ncclAllGather(m.loc.p, m.gath.p, slab, ncclFloat, m.comm, s));
   CUDA_OK(cudaMemcpy2DAsync(dst, (size_t)ld_dst * sizeof(float), m.gath.p, (size_t)B * sizeof(float),
                             (size_t)B * sizeof(float), L.rows, cudaMemcpyDeviceToDevice, s));
@@ -705,10 +709,16 @@ struct Exec {
         CUDA_OK(cudaMemcpyAsync(m.stage_in.p, src, (size_t)Bi * per * sizeof(float), cudaMemcpyHostToDevice, s));
         src = m.stage_in.as<float>();
       }
-      if (L.is_conv())
+      if (L.is_conv()) {
         xin = const_cast<float*>(src);  // NHWC image-major is the conv layout
-      else
+      } else if (uses_tc(m, L, Bi)) {
+        // the tensor-core layer splits the image-major input into bf16 hi / lo
+        // directly (no feature-major copy)
+        layer_step(m, i, src, (int)per, Bi, dst, ld, s, true);
+        return;
+      } else {
         CUDA_OK(launch_transpose(src, Bi, (int)per, (int)per, xin, li, s));
+      }
     } else {
       const Layer& P = *m.layers[i - 1];
       const int b = bs[i - 1];

@@ -516,6 +516,38 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
   }
 }
 
+// X fp32 image-major [B][ldx] (the public infer input) -> bf16 hi / lo [B][ldk]:
+// a plain streaming conversion, 8 consecutive k per thread (two 16-byte loads
+// when aligned, one 16-byte store per half).
+__global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x, int K, int ldx, int B,
+                                                    __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl,
+                                                    int ldk, int vec) {
+  const int nk8 = ldk / 8;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)B * nk8) return;
+  const int b = (int)(i / nk8), k = (int)(i % nk8) * 8;
+  const float* p = x + (size_t)b * ldx + k;
+  float v[8];
+  if (vec && k + 8 <= K) {
+    const float4 a0 = __ldcs(reinterpret_cast<const float4*>(p)), a1 = __ldcs(reinterpret_cast<const float4*>(p + 4));
+    v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = k + j < K ? p[j] : 0.f;
+  }
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(v[2 * j]), h1 = __float2bfloat16_rn(v[2 * j + 1]);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(v[2 * j] - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(v[2 * j + 1] - __bfloat162float(h1));
+    h[j] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+    l[j] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+  }
+  *reinterpret_cast<uint4*>(xh + (size_t)b * ldk + k) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(xl + (size_t)b * ldk + k) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 size_t tc_smem_bytes(const FcDev&) {
   size_t b = 1024 + (size_t)kXStages * kXStageBytes + (size_t)kStreams * (kDecW / 4) * kTM * kRowBytes + 8 * (2 * kXStages + 2 * kStreams * kWBufs + 2) + 16 + 4 * 256;
   return (b + 127) & ~(size_t)127;
@@ -811,10 +843,16 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
 }
 
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s) {
-  dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
+                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s, bool x_image_major) {
   ktimer_begin("k_split_x", s);
-  k_split_x<<<sg, 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
+  if (x_image_major) {
+    const long n = (long)B * (p.ldk / 8);
+    const int vec = (ldx % 4) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk, vec);
+  } else {
+    dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
+    k_split_x<<<sg, 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
+  }
   cudaError_t e = launched();
   ktimer_end("k_split_x", s);
   if (e != cudaSuccess) return e;

@@ -248,6 +248,52 @@ def test_row_shards_concatenate_to_full(torch_dev, world):
     assert np.array_equal(got, full)
 
 
+def test_tc_infer_stack_image_major_and_phases(torch_dev):
+    """The tensor-core path inside infer: lists decoded ahead on the side stream
+    and reused by later phases of the call, the first layer splitting the
+    image-major input directly (no transpose), host and device buffers."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    cfg = synth.CONFIGS["C3"]
+    m = cdn.Model(0)
+    comps = []
+    for i, spec in enumerate(cfg.fc):
+        _, c, buf = config_layer("C3", i)
+        m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+        comps.append((c, synth.fc_weights(spec, 0)[1], spec.relu))
+    m.set_kernel_policy(1, 1)            # tensor-core kernel at every batch
+    K = 300
+    a = synth.fc_inputs(cfg.fc[0].cols, K, 0)
+    x = a
+    for c, v, relu in comps:
+        x = infer.fc_forward(sparse_q(c), x, v, apply_relu=relu).astype(np.float32)
+    for plan in ([100, 300, 300], [150, 150, 300], [K, K, K]):
+        m.set_plan(plan)
+        scores = np.zeros((K, cfg.fc[-1].rows), np.float32)
+        m.infer(a, K, scores, on_device=False)
+        assert rel_err(scores, x) <= TOL, plan
+    xi = torch.from_numpy(a).to(dev)
+    so = torch.zeros((K, cfg.fc[-1].rows), dtype=torch.float32, device=dev)
+    m.infer(xi, K, so, on_device=True)
+    torch.cuda.synchronize()
+    assert rel_err(so.cpu().numpy(), x) <= TOL
+    m.close()
+
+
+def test_tc_fold_list_decoder_subprocess():
+    """The pad-folding list decoder (layers outside the multi-symbol LUT
+    limits; forced here with CDN_TC_LIST=fold) through the same parity check."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_parity as t, torch; "
+            "t.test_tc_forward_configs((torch, torch.device('cuda:0')), 'C5', 2, 300); "
+            "t.test_tc_forward_configs((torch, torch.device('cuda:0')), 'C3', 0, 200); print('ok')")
+    env = dict(os.environ, CDN_TC_LIST="fold")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 # ----------------------------------------------------------------- end to end
 
 def test_infer_c3_stack_matches_oracle_chain(torch_dev):
