@@ -370,6 +370,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       // would leave the GPU short of threads (~128k wanted)
       int tch = kTcChunk;
       while (tch > 1 && (uint64_t)nrt * 128 * ((NI + tch - 1) / tch) < 131072) tch >>= 1;
+      if (const char* e = std::getenv("CDN_TC_CHUNK")) tch = std::max(1, std::min(kTcChunk, std::atoi(e)));
       L.dev.tch = tch;
     }
   }

@@ -92,7 +92,8 @@ cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, in
 // 3-pass bf16 split tcgen05 contraction.  xh/xl: bf16 scratch [B][ldk].
 struct TcPlan {
   bool ok = false;
-  int nbt = 1, nrt = 1, nkt = 0, ldk = 0, S = 1, tiles = 0, units = 0, grid = 0;
+  int nbt = 1, nrt = 1, nkt = 0, ldk = 0, tiles = 0, grid = 0, mpt = 1;  // mpt: max CTAs per tile
+  long W = 0;  // tile steps (stream-K split over `grid` CTAs)
   size_t ws_floats = 0, xsplit_elems = 0, smem = 0;
 };
 bool tc_supported(const FcDev& L);

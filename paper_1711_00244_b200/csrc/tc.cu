@@ -72,8 +72,9 @@ constexpr int kTmemCols = 512;      // accumulator 256 + W buffers 4 x 64
 struct TcArgs {
   float* y;
   int ldy, B, relu;
-  float* ws;   // [tiles][S][128][256] partials (S > 1), summed by k_tc_reduce
-  int S, nbt, nrt, units, nkt;  // splits, batch tiles, row tiles, units, K tiles
+  float* ws;   // [tiles][mpt][128][256] partials of split tiles, summed by k_tc_reduce
+  int nbt, nrt, nkt, G, mpt;  // batch tiles, row tiles, K tiles, CTAs, max pieces per tile
+  long W;                     // total tile steps = tiles * nkt (stream-K)
   unsigned long long* trace;    // debug (env CDN_TC_TRACE): CTA 0 event clocks [event][256], else null
 };
 
@@ -85,19 +86,33 @@ __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
   }
 }
 
+// Stream-K work split: the tiles x nkt tile steps are cut into G equal
+// contiguous ranges, one per CTA; a CTA's range falls into one or more pieces
+// (tile, K range).  A tile covered by several CTAs is summed by k_tc_reduce
+// from ws[tile][i], i = CTA - first CTA of the tile (fixed order).
 struct TUnit {
-  int rt, bt, sp, kt0, kt1, tile;
+  int rt, bt, kt0, kt1, tile, slot, count;  // slot: index among the tile's pieces; count: pieces of the tile
 };
 
-__device__ __forceinline__ TUnit tunit(const TcArgs& a, int u) {
-  TUnit t;
-  t.sp = u % a.S;
-  t.tile = u / a.S;
+__host__ __device__ __forceinline__ long sk_start(long c, long W, int G) { return c * W / G; }
+// CTA whose range holds step x
+__host__ __device__ __forceinline__ int sk_cta(long x, long W, int G) { return (int)(((x + 1) * G - 1) / W); }
+
+__device__ __forceinline__ bool cta_piece(const TcArgs& a, int c, int p, TUnit& t) {
+  const long s0 = sk_start(c, a.W, a.G), s1 = sk_start(c + 1, a.W, a.G);
+  if (s1 <= s0) return false;
+  const long tile = s0 / a.nkt + p;
+  const long t0 = tile * a.nkt;
+  if (t0 >= s1) return false;
+  t.tile = (int)tile;
   t.rt = t.tile / a.nbt;
   t.bt = t.tile % a.nbt;
-  t.kt0 = (int)(((long)t.sp * a.nkt) / a.S);
-  t.kt1 = (int)(((long)(t.sp + 1) * a.nkt) / a.S);
-  return t;
+  t.kt0 = (int)((s0 > t0 ? s0 : t0) - t0);
+  t.kt1 = (int)((s1 < t0 + a.nkt ? s1 : t0 + a.nkt) - t0);
+  const int clo = sk_cta(t0, a.W, a.G);
+  t.slot = c - clo;
+  t.count = sk_cta(t0 + a.nkt - 1, a.W, a.G) - clo + 1;
+  return true;
 }
 
 // byte offset of column c in a private row: 16-byte chunk c / 8 swizzled by the
@@ -190,8 +205,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
     // ---------------------------------------------------------- X tile producer
     if (lane == 0) {
       uint32_t xc = 0;
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-        const TUnit t = tunit(a, u);
+      TUnit t;
+      for (int pc = 0; cta_piece(a, blockIdx.x, pc, t); ++pc) {
         int a0, a1, b0, b1;
         stream_range(t, 0, a0, a1);
         stream_range(t, 1, b0, b1);
@@ -216,8 +231,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
                              ((uint32_t)(kTM >> 4) << 24);
       uint32_t xc = 0, gq[kStreams] = {0, 0}, uc = 0;
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
-        const TUnit t = tunit(a, u);
+      TUnit t;
+      for (int pc = 0; cta_piece(a, blockIdx.x, pc, t); ++pc, ++uc) {
         mbar_wait(tempty, (uc & 1) ^ 1);  // the epilogue drained the accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         int a0, a1, b0, b1;
@@ -268,8 +283,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
     const uint32_t tlane = (uint32_t)(quarter * 32) << 16;
     const uint32_t prow = smem_addr(rows) + (uint32_t)(((q * (kDecW / 4) + hsel) * kTM + row_l) * kRowBytes);  // private row
     uint32_t g = 0;  // tiles of this stream so far
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-      const TUnit t = tunit(a, u);
+    TUnit t;
+    for (int pc = 0; cta_piece(a, blockIdx.x, pc, t); ++pc) {
       int k0, k1;
       stream_range(t, q, k0, k1);
       // tile kt's entries: block (rt, kt) of the list, this row's slice of it
@@ -376,8 +391,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
     const int row_l = q4 * 32 + lane;
     uint32_t uc = 0;
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++uc) {
-      const TUnit t = tunit(a, u);
+    TUnit t;
+    for (int pc = 0; cta_piece(a, blockIdx.x, pc, t); ++pc, ++uc) {
       if (ew == 0 && lane == 0) tc_trace(a, 12, 0);
       mbar_wait(tfull, uc & 1);
       if (ew == 0 && lane == 0) tc_trace(a, 13, 0);
@@ -387,15 +402,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const bool has = t.kt1 > t.kt0;
       float* dst;
       size_t ld;
-      if (a.S == 1) {
+      const bool whole = t.count == 1;  // this CTA owns the tile's whole K range
+      if (whole) {
         dst = a.y + (size_t)row * a.ldy + b0;
         ld = a.ldy;
       } else {
-        dst = a.ws + (((size_t)t.tile * a.S + t.sp) * kTM + row_l) * kTN;
+        dst = a.ws + (((size_t)t.tile * a.mpt + t.slot) * kTM + row_l) * kTN;
         ld = kTN;
       }
       (void)ld;
-      const float bias = (a.S == 1 && row < L.nrows) ? L.bias[row] : 0.f;
+      const float bias = (whole && row < L.nrows) ? L.bias[row] : 0.f;
       // y rows are contiguous over the batch: whole float4s where the tile is inside B
       const bool vec_ok = (a.ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
       for (int c = 0; c < kTN; c += 16) {
@@ -405,7 +421,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
-        if (a.S == 1) {
+        if (whole) {
           if (row < L.nrows) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -483,24 +499,27 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
   }
 }
 
-// K-split reduction (S > 1): y[row][b] = act(sum_j partial_j[row][b] + bias),
-// partials summed in split order (deterministic); one thread per 4 images of a
-// row, coalesced, over every tile at once.
-__global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, int S, int nbt, int nrows, int B,
-                                                   const float* __restrict__ bias, int relu, float* __restrict__ y,
-                                                   int ldy, int vec_ok, long total) {
+// Split tiles (covered by several CTAs' ranges): y[row][b] = act(sum_i
+// ws[tile][i][row][b] + bias), i in CTA order (deterministic); one thread per 4
+// images of a row, coalesced, over every tile at once (whole tiles skip).
+__global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, long W, int G, int nkt, int mpt,
+                                                   int nbt, int nrows, int B, const float* __restrict__ bias, int relu,
+                                                   float* __restrict__ y, int ldy, int vec_ok, long total) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const int c4 = (int)(i % (kTN / 4));
   const long tr = i / (kTN / 4);  // tile * 128 + row in tile
   const int r = (int)(tr % kTM);
   const long tile = tr / kTM;
+  const long t0 = tile * nkt;
+  const int count = sk_cta(t0 + nkt - 1, W, G) - sk_cta(t0, W, G) + 1;
+  if (count == 1) return;
   const int rt = (int)(tile / nbt), bt = (int)(tile % nbt);
   const int row = rt * kTM + r, b = bt * kTN + 4 * c4;
   if (row >= nrows || b >= B) return;
-  const float* p = ws + ((size_t)tile * S * kTM + r) * kTN + 4 * c4;
+  const float* p = ws + ((size_t)tile * mpt * kTM + r) * kTN + 4 * c4;
   float4 acc = __ldcg(reinterpret_cast<const float4*>(p));
-  for (int j = 1; j < S; ++j) {
+  for (int j = 1; j < count; ++j) {
     const float4 q = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * kTN));
     acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
   }
@@ -796,26 +815,36 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   p.nrt = (L.nrows + kTM - 1) / kTM;
   p.nkt = L.tNI;
   p.ldk = (L.cols + 7) & ~7;
-  const int tiles = p.nrt * p.nbt;
-  double best = 1e30;
-  int bestS = 1;
-  const int smax = p.nkt < 64 ? p.nkt : 64;
-  // unit time ~ its K tiles + a fixed ~16-tile cost (decoder start, epilogue
-  // drain, split partial; measured on C5); the smallest S within 2% of the best wins
-  for (int S = 1; S <= smax; ++S) {
-    const long units = (long)tiles * S;
-    const long waves = (units + num_sms - 1) / num_sms;
-    const double cost = (double)waves * ((double)p.nkt / S + 16.0);
-    if (cost < best * 0.98) { best = cost; bestS = S; }
+  p.tiles = p.nrt * p.nbt;
+  p.W = (long)p.tiles * p.nkt;
+  long G;
+  if (p.W >= 64L * num_sms) {
+    // long shares: stream-K, every SM an equal contiguous share of the tile
+    // steps (no wave quantisation; a share spans at most a few pieces)
+    G = num_sms;
+  } else {
+    // short shares: each CTA one (tile, K/S range) piece (G = tiles * S, which
+    // the stream-K formulas reduce to); the piece start-up (~16 steps' worth,
+    // measured on C5) dominates, so S minimises waves * (nkt / S + 16)
+    double best = 1e30;
+    int bestS = 1;
+    const int smax = p.nkt < 64 ? p.nkt : 64;
+    for (int S = 1; S <= smax; ++S) {
+      const long units = (long)p.tiles * S;
+      const long waves = (units + num_sms - 1) / num_sms;
+      const double cost = (double)waves * ((double)p.nkt / S + 16.0);
+      if (cost < best * 0.98) { best = cost; bestS = S; }
+    }
+    G = (long)p.tiles * bestS;
   }
-  p.S = bestS;
-  p.tiles = tiles;
-  p.units = tiles * p.S;
-  p.grid = p.units < num_sms ? p.units : num_sms;
-  p.ws_floats = p.S > 1 ? (size_t)tiles * p.S * kTM * kTN : 0;
+  p.grid = (int)G;
+  const long per = p.W / G;  // >= 1
+  p.mpt = (int)((p.nkt + per - 1) / per) + 1;
+  if (p.mpt > (int)G) p.mpt = (int)G;
+  p.ws_floats = (size_t)p.tiles * p.mpt * kTM * kTN;
   p.xsplit_elems = (size_t)B * p.ldk;
   p.smem = tc_smem_bytes(L);
-  p.ok = p.smem <= 227 * 1024;  // (LUT sizes vary per layer)
+  p.ok = p.smem <= 227 * 1024;
   return p;
 }
 
@@ -876,16 +905,16 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     if (e != cudaSuccess) return e;
   }
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
-  TcArgs a{y, ldy, B, relu, ws, p.S, p.nbt, p.nrt, p.units, p.nkt, trace_path ? trace : nullptr};
+  TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr};
   ktimer_begin("k_fc_tc", s);
   k_fc_tc<<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
   e = launched();
   ktimer_end("k_fc_tc", s);
-  if (e == cudaSuccess && p.S > 1) {
+  if (e == cudaSuccess && p.grid != p.tiles) {  // some tile is split over CTAs
     const long total = (long)p.tiles * kTM * (kTN / 4);
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
-    k_tc_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(ws, p.S, p.nbt, L.nrows, B, L.bias, relu, y, ldy,
-                                                                   vec_ok, total);
+    k_tc_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(ws, p.W, p.grid, p.nkt, p.mpt, p.nbt, L.nrows, B,
+                                                                   L.bias, relu, y, ldy, vec_ok, total);
     e = launched();
   }
   if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
