@@ -597,6 +597,8 @@ bool uses_tc(const Model& m, const Layer& L, int B) {
 // End of an API call: the decoded lists are per-call scratch.  A list still
 // being decoded on the side stream is ordered before later work on s.
 void reset_lists(Model& m, cudaStream_t s) {
+  static const bool keep = std::getenv("CDN_DEBUG_KEEP_LISTS") != nullptr;  // timing experiment only
+  if (keep) return;
   for (auto& L : m.layers) {
     if (L->list_state == 1) cudaStreamWaitEvent(s, L->list_ev, 0);
     L->list_state = 0;
@@ -620,9 +622,15 @@ void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
   }
   CUDA_OK(cudaEventRecord(m.ev_call, s));
   CUDA_OK(cudaStreamWaitEvent(m.side, m.ev_call, 0));
+  static const int max_ahead = [] {
+    const char* e = std::getenv("CDN_LISTS_AHEAD");
+    return e ? std::atoi(e) : 1 << 20;
+  }();
+  int ahead = 0;
   for (size_t i = 0; i < m.layers.size(); ++i) {
     Layer& L = *m.layers[i];
     if (L.list_state != 0 || !uses_tc(m, L, bs[i])) continue;
+    if (ahead++ >= max_ahead) break;
     if (!L.list_ev) CUDA_OK(cudaEventCreateWithFlags(&L.list_ev, cudaEventDisableTiming));
     CUDA_OK(launch_tc_list(L.dev, m.side));
     CUDA_OK(cudaEventRecord(L.list_ev, m.side));

@@ -125,6 +125,12 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
 
+__device__ __forceinline__ void st_u16_if(uint16_t* p, uint32_t v, bool pred) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.u16 [%0], %1; }" ::"l"(p), "h"((unsigned short)v),
+               "r"((uint32_t)pred)
+               : "memory");
+}
+
 __device__ __forceinline__ void sts_u16_if(uint32_t a, uint32_t v, bool p) {
   asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "h"((unsigned short)v),
                "r"((uint32_t)p)
@@ -683,6 +689,7 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   uint16_t* s_vsorted = reinterpret_cast<uint16_t*>(s_gtab + 99);
   uint16_t* s_gsorted = s_vsorted + (L.nvs + 1);
   __shared__ __align__(8) uint64_t s_bar;
+  __shared__ uint32_t s_pos[kTcChunk * kListThreads];
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     mbar_fence_init();
@@ -705,16 +712,19 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   const int row = rt * 128 + r;
   if (row >= L.nrows) return;
   const int nk = L.tNI - kt0 < tch ? L.tNI - kt0 : tch;
-  uint32_t p[kTcChunk], left = 0;
+  // this thread's first list slot in each tile of the chunk, in shared memory
+  // ([k][thread]: conflict-free) so the emission below picks it without branches
+  uint32_t left = 0;
 #pragma unroll
   for (int k = 0; k < kTcChunk; ++k) {
-    p[k] = 0;
+    uint32_t pk = 0;
     if (k < nk) {
       const size_t blk = (size_t)rt * L.tNI + kt0 + k;
       const uint32_t o0 = L.troff[blk * 129 + r], o1 = L.troff[blk * 129 + r + 1];
-      p[k] = L.tbase[blk] + o0;
+      pk = L.tbase[blk] + o0;
       left += o1 - o0;
     }
+    s_pos[k * kListThreads + threadIdx.x] = pk;
   }
   if (left == 0) return;
   const size_t q = (size_t)row * L.tNI + kt0;
@@ -769,22 +779,19 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
     const int pn = min(min(cv, cg), 4);
     const uint32_t qv32 = (uint32_t)qv, qg32 = (uint32_t)qg;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (j < pn) {
-        col += (int)((qg32 >> (4 * j)) & 15u) + 1;  // c = prev + g + 1 (Alg. 1 l.7, C-01)
-        const uint32_t sym = (qv32 >> (5 * j)) & 31u;
-        if (sym != 0 && left > 0) {
-          const int k = (col >> 6) - kt0;
-          if (k != ck) {
-            ck = k;
-            pos = p[0];
-#pragma unroll
-            for (int jj = 1; jj < kTcChunk; ++jj) pos = k == jj ? p[jj] : pos;
-          }
-          L.tlist[pos++] = (uint16_t)((col & 63) | (sym << 6));
-          --left;
-        }
-      }
+    for (int j = 0; j < 4; ++j) {  // branch-free: every slot computes, only real tokens store
+      const bool take = j < pn;
+      col += take ? (int)((qg32 >> (4 * j)) & 15u) + 1 : 0;  // c = prev + g + 1 (Alg. 1 l.7, C-01)
+      const uint32_t sym = (qv32 >> (5 * j)) & 31u;
+      int k = (col >> 6) - kt0;
+      k = k < kTcChunk - 1 ? k : kTcChunk - 1;  // tokens past the chunk never store
+      const uint32_t pk = s_pos[k * kListThreads + threadIdx.x];
+      pos = k != ck ? pk : pos;  // columns only grow: a tile is entered once
+      ck = k;
+      const bool em = take && sym != 0 && left > 0;
+      st_u16_if(L.tlist + pos, (col & 63) | (sym << 6), em);
+      pos += em;
+      left -= em;
     }
     qv >>= 5 * pn;
     qg >>= 4 * pn;
