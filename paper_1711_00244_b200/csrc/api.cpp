@@ -367,9 +367,9 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       L.troff.upload(to);
       L.tlist.alloc((off + 64) * sizeof(uint16_t));
       // list-decoder tasks: chunks of up to kTcChunk K tiles, fewer when that
-      // would leave the GPU short of threads (~128k wanted)
+      // would leave the GPU short of threads (~64k wanted; measured on C5 fc7/fc8)
       int tch = kTcChunk;
-      while (tch > 1 && (uint64_t)nrt * 128 * ((NI + tch - 1) / tch) < 131072) tch >>= 1;
+      while (tch > 1 && (uint64_t)nrt * 128 * ((NI + tch - 1) / tch) < 65536) tch >>= 1;
       if (const char* e = std::getenv("CDN_TC_CHUNK")) tch = std::max(1, std::min(kTcChunk, std::atoi(e)));
       L.dev.tch = tch;
     }

@@ -712,6 +712,10 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   const int row = rt * 128 + r;
   if (row >= L.nrows) return;
   const int nk = L.tNI - kt0 < tch ? L.tNI - kt0 : tch;
+  // the decoder state first (its loads gate everything), the output slots meanwhile
+  const size_t q = (size_t)row * L.tNI + kt0;
+  const uint2 st = L.tivg[q];
+  const uint32_t m0 = L.tivm[q];
   // this thread's first list slot in each tile of the chunk, in shared memory
   // ([k][thread]: conflict-free) so the emission below picks it without branches
   uint32_t left = 0;
@@ -726,20 +730,11 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
     }
     s_pos[k * kListThreads + threadIdx.x] = pk;
   }
-  if (left == 0) return;
-  const size_t q = (size_t)row * L.tNI + kt0;
-  const uint2 st = L.tivg[q];
-  // the task's bits end where the next chunk (or the row) starts: pull all of
-  // its stream lines into L2 at once, so the reader's refills never wait on HBM
-  const uint2 en = kt0 + nk < L.tNI ? L.tivg[q + nk] : make_uint2(L.rp[2 * row + 2], L.rp[2 * row + 3]);
-  for (uint32_t l = st.x >> 10; l <= (en.x + 64) >> 10; ++l)
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(L.vw + (size_t)l * 32));
-  for (uint32_t l = st.y >> 10; l <= (en.y + 64) >> 10; ++l)
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(L.gw + (size_t)l * 32));
-  int col = kt0 * 64 - (int)(L.tivm[q] & 0xFFu) - 1;
   SReader vr, gr;
   vr.init(L.vw, st.x);
   gr.init(L.gw, st.y);
+  if (left == 0) return;
+  int col = kt0 * 64 - (int)(m0 & 0xFFu) - 1;
   const int vsh = 32 - L.msLv, gsh = 32 - L.msLg;
   uint64_t qv = 0, qg = 0;
   int cv = 0, cg = 0;
