@@ -32,6 +32,16 @@ struct KTimer {
   bool on = false;
   std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> ev;
   std::map<std::string, cudaEvent_t> open;
+  std::vector<cudaEvent_t> pool;  // reused between measurements (creating events costs host time)
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    return cudaEventCreate(&e) == cudaSuccess ? e : nullptr;
+  }
 };
 KTimer& kt() {
   static KTimer* t = new KTimer();  // never destroyed: events may outlive static destruction order
@@ -43,8 +53,8 @@ void ktimer_begin(const char* kernel, cudaStream_t s) {
   KTimer& t = kt();
   std::lock_guard<std::mutex> g(t.mu);
   if (!t.on) return;
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEvent_t e = t.get();
+  if (!e) return;
   cudaEventRecord(e, s);
   t.open[kernel] = e;
 }
@@ -54,8 +64,8 @@ void ktimer_end(const char* kernel, cudaStream_t s) {
   std::lock_guard<std::mutex> g(t.mu);
   auto it = t.open.find(kernel);
   if (!t.on || it == t.open.end()) return;
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEvent_t e = t.get();
+  if (!e) return;
   cudaEventRecord(e, s);
   t.ev[kernel].emplace_back(it->second, e);
   t.open.erase(it);
@@ -67,11 +77,11 @@ void ktimer_enable(bool on) {
   for (auto& kv : t.ev)
     for (auto& p : kv.second) {
       cudaEventSynchronize(p.second);
-      cudaEventDestroy(p.first);
-      cudaEventDestroy(p.second);
+      t.pool.push_back(p.first);
+      t.pool.push_back(p.second);
     }
   t.ev.clear();
-  for (auto& kv : t.open) cudaEventDestroy(kv.second);
+  for (auto& kv : t.open) t.pool.push_back(kv.second);
   t.open.clear();
   t.on = on;
 }
