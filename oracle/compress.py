@@ -36,12 +36,17 @@ def _freqs(tokens: np.ndarray) -> Dict[int, int]:
 
 
 def compress_layer(W: np.ndarray, density: float, r: int, k: int,
-                   bias: Optional[np.ndarray] = None) -> Compressed:
+                   bias: Optional[np.ndarray] = None, quantizer: str = "linear") -> Compressed:
     W = np.asarray(W, dtype=np.float32)
     rows, cols = W.shape
     mask = prune.prune_mask(W, density)                       # P:L55, C-10
     kept_vals = W[mask]                                       # row-major order
-    cb = quantize.linear_codebook(kept_vals, r)               # P:L244-246, C-04/05
+    if quantizer == "linear":
+        cb = quantize.linear_codebook(kept_vals, r)           # P:L244-246, C-04/05
+    elif quantizer == "kmeans":
+        cb = quantize.lloyd_codebook(kept_vals, r)            # P:L244, C-33
+    else:
+        raise ValueError(f"unknown quantizer {quantizer!r}")
     q = np.zeros(W.shape, dtype=np.int64)
     q[mask] = quantize.assign(kept_vals, cb)                  # nearest centre, C-07
     vt, gt, row_tokens = relindex.encode_matrix(mask, q, k)

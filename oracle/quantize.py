@@ -15,6 +15,16 @@ Readings:
   C-07: assignment = argmin_{j>=1} |w - C[j]| in binary64 over the fp32 centres,
        ties to the smaller j.  lo == hi gives duplicate centres; the smallest
        j wins.  No kept weights -> lo = hi = 0.
+
+Variant: 1-D Lloyd k-means refinement of the
+same 2^r - 1 centres ("similar valued non-zero entries of val are clustered",
+P:L244).  Reading C-33: start from the C-05 grid; per iteration assign every
+kept weight to its nearest centre in binary64 (ties to the smaller index),
+then move each non-empty centre to the binary64 mean of its weights, summed
+in row-major order; an empty centre stays where it is; stop after 50
+iterations or when no centre moved by more than 1e-7 * max(|lo|, |hi|).  The
+stored codebook is fp32(centre); the final assignment is C-07 over the stored
+fp32 centres.
 """
 from __future__ import annotations
 
@@ -32,6 +42,37 @@ def linear_codebook(kept: np.ndarray, r: int) -> np.ndarray:
     denom = float(n - 2) if n > 2 else 1.0
     for j in range(1, n):
         cb[j] = np.float32(lo + (hi - lo) * (j - 1) / denom)
+    return cb
+
+
+def lloyd_codebook(kept: np.ndarray, r: int, iters: int = 50, tol: float = 1e-7) -> np.ndarray:
+    """fp32 codebook of 2^r entries, entry 0 == 0.0, centres refined by 1-D
+    Lloyd iterations from the linear grid (C-33)."""
+    n = 1 << r
+    cb = np.zeros(n, dtype=np.float32)
+    if kept.size == 0:
+        return cb
+    v = kept.astype(np.float64)
+    lo, hi = float(np.min(v)), float(np.max(v))
+    denom = float(n - 2) if n > 2 else 1.0
+    c = np.array([lo + (hi - lo) * (j - 1) / denom for j in range(1, n)], dtype=np.float64)
+    eps = tol * max(abs(lo), abs(hi))
+    for _ in range(iters):
+        # nearest centre, binary64, ties -> smaller index (argmin returns the first)
+        idx = np.empty(v.size, dtype=np.int64)
+        for s in range(0, v.size, 1 << 20):
+            idx[s:s + (1 << 20)] = np.argmin(np.abs(v[s:s + (1 << 20), None] - c[None, :]), axis=1)
+        # bincount adds the weights one by one in array (row-major) order
+        sums = np.bincount(idx, weights=v, minlength=c.size)
+        cnt = np.bincount(idx, minlength=c.size)
+        new = c.copy()
+        nz = cnt > 0
+        new[nz] = sums[nz] / cnt[nz]
+        moved = float(np.max(np.abs(new - c)))
+        c = new
+        if moved <= eps:
+            break
+    cb[1:] = c.astype(np.float32)
     return cb
 
 

@@ -96,6 +96,8 @@ _SIGS = {
     "cdn_model_profile": (C.c_int32, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "cdn_compress_dense": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_int,
                                        C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "cdn_compress_dense_q": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_int,
+                                         C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     "cdn_free": (None, [C.c_void_p]),
     "cdn_plan_dp": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_uint64,
                                 C.c_double, C.c_uint64, C.c_void_p, C.POINTER(C.c_double)]),
@@ -147,15 +149,18 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def compress_dense(W: np.ndarray, density: float, r: int, k: int, bias: Optional[np.ndarray] = None) -> bytes:
-    """Product-side compressor: dense fp32 -> single-layer CDNI bytes."""
+def compress_dense(W: np.ndarray, density: float, r: int, k: int, bias: Optional[np.ndarray] = None,
+                   quantizer: str = "linear") -> bytes:
+    """Product-side compressor: dense fp32 -> single-layer CDNI bytes
+    (quantizer "linear" = C-05 grid, "kmeans" = Lloyd refinement, C-33)."""
     W = np.ascontiguousarray(W, dtype=np.float32)
     b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
     out = C.c_void_p()
     n = C.c_size_t()
     lib = load_library()
-    _check(lib.cdn_compress_dense(W.ctypes.data, None if b is None else b.ctypes.data, W.shape[0], W.shape[1],
-                                  float(density), int(r), int(k), C.byref(out), C.byref(n)))
+    qz = {"linear": 0, "kmeans": 1}[quantizer]
+    _check(lib.cdn_compress_dense_q(W.ctypes.data, None if b is None else b.ctypes.data, W.shape[0], W.shape[1],
+                                    float(density), int(r), int(k), qz, C.byref(out), C.byref(n)))
     try:
         return C.string_at(out, n.value)
     finally:

@@ -1205,9 +1205,14 @@ cdn_status cdn_model_memory_model(cdn_model* h, int Bmax, uint64_t* in_b, uint64
 
 cdn_status cdn_compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols, double density,
                               int r, int k, void** out, size_t* out_len) {
+  return cdn_compress_dense_q(W, bias, rows, cols, density, r, k, 0, out, out_len);
+}
+
+cdn_status cdn_compress_dense_q(const float* W, const float* bias, uint32_t rows, uint32_t cols, double density,
+                                int r, int k, int quantizer, void** out, size_t* out_len) {
   API_BEGIN
   if (!W || !out || !out_len) return fail(CDN_E_ARG, "NULL argument");
-  std::vector<uint8_t> v = compress_dense(W, bias, rows, cols, density, r, k);
+  std::vector<uint8_t> v = compress_dense(W, bias, rows, cols, density, r, k, quantizer);
   void* p = std::malloc(v.size());
   if (!p) return fail(CDN_E_OOM, "malloc");
   std::memcpy(p, v.data(), v.size());

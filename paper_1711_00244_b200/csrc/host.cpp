@@ -429,7 +429,8 @@ template <class T> void put(std::vector<uint8_t>& o, T v) {
 }  // namespace
 
 std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols,
-                                    double density, int r, int k) {
+                                    double density, int r, int k, int quantizer) {
+  if (quantizer != 0 && quantizer != 1) throw Error(CDN_E_ARG, "quantizer must be 0 (linear) or 1 (k-means)");
   if (!W || rows == 0 || cols == 0) throw Error(CDN_E_ARG, "empty matrix");
   if (r < 1 || r > 8 || k < 1 || k > 8) throw Error(CDN_E_UNSUPPORTED, "k and r must be in 1..8");
   if (!(density >= 0.0 && density <= 1.0)) throw Error(CDN_E_ARG, "density must be in [0,1]");
@@ -467,6 +468,42 @@ std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t 
   if (any) {
     const double denom = ncb > 2 ? (double)(ncb - 2) : 1.0;
     for (int j = 1; j < ncb; ++j) cb[j] = (float)(lo + (hi - lo) * (double)(j - 1) / denom);
+    if (quantizer == 1) {
+      // 1-D Lloyd k-means from the same grid (C-33): nearest centre in binary64
+      // (ties -> smaller index), move non-empty centres to the binary64 mean of
+      // their weights summed in row-major order, <= 50 iterations or until no
+      // centre moves by more than 1e-7 * max(|lo|, |hi|)
+      const int nc = ncb - 1;
+      std::vector<double> c(nc), sum(nc);
+      std::vector<uint64_t> cnt(nc);
+      for (int j = 0; j < nc; ++j) c[j] = lo + (hi - lo) * (double)j / denom;
+      const double eps = 1e-7 * std::max(std::fabs(lo), std::fabs(hi));
+      for (int it = 0; it < 50; ++it) {
+        std::fill(sum.begin(), sum.end(), 0.0);
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (uint64_t i = 0; i < n; ++i) {
+          if (!keep[i]) continue;
+          const double v = (double)W[i];
+          int best = 0;
+          double bd = std::fabs(v - c[0]);
+          for (int j = 1; j < nc; ++j) {
+            const double d = std::fabs(v - c[j]);
+            if (d < bd) { bd = d; best = j; }
+          }
+          sum[best] += v;
+          cnt[best]++;
+        }
+        double moved = 0.0;
+        for (int j = 0; j < nc; ++j) {
+          if (!cnt[j]) continue;
+          const double nv = sum[j] / (double)cnt[j];
+          moved = std::max(moved, std::fabs(nv - c[j]));
+          c[j] = nv;
+        }
+        if (moved <= eps) break;
+      }
+      for (int j = 0; j < nc; ++j) cb[j + 1] = (float)c[j];
+    }
   }
   // relative index (C-01..03) + token streams
   const uint32_t cap = (1u << k) - 1;

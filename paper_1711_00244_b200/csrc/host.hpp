@@ -108,7 +108,7 @@ int choose_lanes_per_row(const HostLayer& L, uint32_t r0, uint32_t r1, int targe
 
 // Product-side compressor (independent of oracle/, same readings).
 std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols,
-                                    double density, int r, int k);
+                                    double density, int r, int k, int quantizer = 0);
 
 // Variable-batch DP with memory axis granularity `step` bytes.
 struct PlanResult {

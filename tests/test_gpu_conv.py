@@ -60,13 +60,15 @@ def test_tcgen05_gemm_hook(torch_dev, M, N, K, relu):
 _CACHE = {}
 
 
-def conv_case(i):
+def conv_case(i, density=None, quantizer="linear"):
     spec = synth.ALEXNET_CONV[i]
-    if i not in _CACHE:
+    d = spec.density if density is None else density
+    key = (i, d, quantizer)
+    if key not in _CACHE:
         W, v = synth.fc_weights(spec, 0)
-        c = compress.compress_layer(W, spec.density, spec.r, spec.k, v)
-        _CACHE[i] = (spec, c, cdni.serialize([c.layer]), v)
-    return _CACHE[i]
+        c = compress.compress_layer(W, d, spec.r, spec.k, v, quantizer=quantizer)
+        _CACHE[key] = (spec, c, cdni.serialize([c.layer]), v)
+    return _CACHE[key]
 
 
 IN_HW = [227, 27, 13, 13, 13]
@@ -91,11 +93,15 @@ def oracle_conv(spec, c, v, x):
     return y
 
 
-@pytest.mark.parametrize("i,B", [(0, 2), (1, 2), (2, 3), (3, 2), (4, 2)])
-def test_alexnet_conv_layer_vs_oracle(torch_dev, i, B):
+@pytest.mark.parametrize("i,B,density,quantizer", [(0, 2, None, "linear"), (1, 2, None, "linear"),
+                                                   (2, 3, None, "linear"), (3, 2, None, "linear"),
+                                                   (4, 2, None, "linear"),
+                                                   # the paper's 63% conv5, k-means
+                                                   (4, 2, 0.63, "kmeans")])
+def test_alexnet_conv_layer_vs_oracle(torch_dev, i, B, density, quantizer):
     torch, dev = torch_dev
     import paper_1711_00244_b200 as cdn
-    spec, c, buf, v = conv_case(i)
+    spec, c, buf, v = conv_case(i, density, quantizer)
     x = conv_input(i, B)
     m = cdn.Model(0)
     m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, IN_HW[i], IN_HW[i], spec.kh, spec.kw, spec.stride, spec.pad,

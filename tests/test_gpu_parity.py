@@ -248,6 +248,31 @@ def test_row_shards_concatenate_to_full(torch_dev, world):
     assert np.array_equal(got, full)
 
 
+VARIANTS = [("kmeans", 4, 0.04), ("linear", 5, 0.04), ("kmeans", 5, 0.09), ("linear", 8, 0.2)]
+
+
+@pytest.mark.parametrize("quantizer,k,d", VARIANTS)
+@pytest.mark.parametrize("B,policy", [(1, (1000, 1 << 30)), (8, (1000, 1 << 30)), (64, (1, 1 << 30)),
+                                       (256, (1, 1))])
+def test_paper_variants_all_kernels(torch_dev, quantizer, k, d, B, policy):
+    """SURVEY §8(f) row 4 variants through every FC kernel: the Lloyd k-means
+    codebook (C-33) and 5-/8-bit relative indices (VGG's 5-bit gaps, P:L453;
+    k > 4 leaves the multi-symbol LUT kernels for the pad-folding ones)."""
+    torch, dev = torch_dev
+    key = f"variant-{quantizer}-{k}-{d}"
+    W = synth.random_matrix(700, 3000, seed=zlib.crc32(key.encode()) % 1000, scale=0.02)
+    v = synth.random_matrix(1, 700, seed=5).ravel()
+    if key not in _CACHE:
+        c = compress.compress_layer(W, d, 5, k, v, quantizer=quantizer)
+        _CACHE[key] = (c, cdni.serialize([c.layer]))
+    c, buf = _CACHE[key]
+    m = make_model(torch, buf, relu=True)
+    m.set_kernel_policy(*policy)
+    a = synth.fc_inputs(3000, B, 3)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=True, split_bf16=policy[1] == 1)
+    m.close()
+
+
 def test_tc_infer_stack_image_major_and_phases(torch_dev):
     """The tensor-core path inside infer: lists decoded ahead on the side stream
     and reused by later phases of the call, the first layer splitting the

@@ -51,6 +51,18 @@ def test_compressor_byte_identical_to_oracle(seed, rows, cols, d, r, k, bias):
     assert pb == ob
 
 
+@pytest.mark.parametrize("seed,rows,cols,d,r,k", [
+    (0, 23, 71, 0.2, 5, 4), (1, 40, 300, 0.03, 5, 4), (2, 17, 33, 0.7, 8, 8), (3, 9, 500, 0.01, 2, 1),
+    (6, 64, 64, 0.25, 1, 2), (7, 5, 1000, 0.5, 3, 2)])
+def test_kmeans_compressor_byte_identical_to_oracle(seed, rows, cols, d, r, k):
+    """The Lloyd quantizer (C-33) in the product compressor reproduces the
+    oracle's arithmetic exactly (binary64 means in row-major order)."""
+    W = synth.random_matrix(rows, cols, seed=seed, scale=0.05)
+    v = synth.random_matrix(1, rows, seed=seed + 99).ravel()
+    c = ocompress.compress_layer(W, d, r, k, v, quantizer="kmeans")
+    assert cdn.compress_dense(W, d, r, k, v, quantizer="kmeans") == ocdni.serialize([c.layer])
+
+
 def test_compressor_ties_and_duplicates():
     # many equal magnitudes: exact-count tie rule (C-10) and quantizer ties (C-07)
     rng = np.random.default_rng(3)

@@ -93,6 +93,54 @@ def test_degenerate_codebook():
 
 # ---------------------------------------------------- relative index
 
+# ------------------------------------------------ Lloyd k-means variant (C-33)
+
+def test_lloyd_spec_example():
+    """{0.9, 1.1, 2.9, 3.1}, r = 2 -> the used centres are 1.0 and
+    3.0 (the grid's middle centre gets no weight and stays unused)."""
+    v = np.array([0.9, 1.1, 2.9, 3.1], np.float32)
+    cb = quantize.lloyd_codebook(v, 2)
+    q = quantize.assign(v, cb)
+    assert cb[0] == 0.0
+    assert np.allclose(sorted(set(cb[q].tolist())), [1.0, 3.0], atol=1e-6)
+    assert q[0] == q[1] and q[2] == q[3] and q[0] != q[2]
+
+
+def _sse(v, cb):
+    return float(np.sum((v.astype(np.float64) - cb[quantize.assign(v, cb)].astype(np.float64)) ** 2))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_lloyd_fixed_point_and_no_worse_than_grid(seed):
+    """At convergence every used centre is the mean of the weights nearest to
+    it (1-D k-means stationarity, up to fp32 storage), and Lloyd steps never
+    increase the squared error of the linear grid they start from."""
+    rng = np.random.default_rng(seed)
+    v = np.concatenate([rng.normal(-0.05, 0.01, 300), rng.normal(0.04, 0.02, 500)]).astype(np.float32)
+    r = 3 + seed % 3
+    cb = quantize.lloyd_codebook(v, r)
+    q = quantize.assign(v, cb)
+    for j in np.unique(q):
+        m = float(np.mean(v[q == j].astype(np.float64)))
+        assert abs(m - float(cb[j])) <= 1e-5 * max(abs(float(v.min())), abs(float(v.max())))
+    assert _sse(v, cb) <= _sse(v, quantize.linear_codebook(v, r)) * (1 + 1e-9)
+    assert np.all(np.diff(cb[1:].astype(np.float64)) >= 0)          # 1-D clusters stay ordered
+
+
+def test_lloyd_degenerate_inputs():
+    assert np.all(quantize.lloyd_codebook(np.zeros(0, np.float32), 4) == 0)
+    cb = quantize.lloyd_codebook(np.full(50, 0.25, np.float32), 3)
+    q = quantize.assign(np.full(50, 0.25, np.float32), cb)
+    assert np.all(cb[q] == np.float32(0.25))
+
+
+@pytest.mark.parametrize("seed,d,r,k", [(0, 0.1, 5, 4), (1, 0.3, 3, 2), (2, 0.04, 5, 5)])
+def test_kmeans_decode_of_compress_is_prune_quantize(seed, d, r, k):
+    W = synth.random_matrix(40, 257, seed=seed, scale=0.05)
+    c = compress.compress_layer(W, d, r, k, quantizer="kmeans")
+    assert np.array_equal(decode.decode_dense(c.layer), c.dense_q())
+
+
 def test_relindex_spec_k2_example():
     # S:L96/L106: k=2, columns {0,5,11} -> gaps [0,3,0,3,1], vals [x,0,y,0,z]
     v, g = relindex.encode_row([0, 5, 11], [7, 8, 9], k=2)
