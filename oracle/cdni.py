@@ -6,11 +6,16 @@ Layout (all integers little-endian):
   "CDNI"  u16 version(=1)  u32 layer_count
   per layer:
     u32 rows, u32 cols, u32 bh, u32 bw          (unblocked: bh=1, bw=cols)
+      blocked (Alg. 2, reading C-34): rows % bh == 0, cols % bw
+      == 0; the streams hold the "modified matrix" M' whose stored row
+      i = bi * (cols/bw) + bj is block (bi, bj) flattened row-major (element
+      (r, c) of the block at position r*bw + c); row_ptr has one entry per
+      stored row (+1) and relative indexing runs along the stored rows
     u8 k, u8 r
     u16 n_codebook, n_codebook x f32           (codebook C, index 0 = 0.0)
     u16 n_val_syms, n x (u16 symbol, u8 length)  (val-stream Huffman lengths)
     u16 n_gap_syms, n x (u16 symbol, u8 length)  (gap-stream Huffman lengths)
-    (rows+1) x (u64 val_bit, u64 gap_bit)        (row_ptr 2-tuples)
+    (stored_rows+1) x (u64 val_bit, u64 gap_bit) (row_ptr 2-tuples)
     val stream: ceil(row_ptr[rows].val / 8) bytes
     gap stream: ceil(row_ptr[rows].gap / 8) bytes
     u8 has_bias, [rows x f32]
@@ -55,6 +60,29 @@ class Layer:
         if self.bw == 0:
             self.bw = self.cols
 
+    @property
+    def blocked(self) -> bool:
+        return not (self.bh == 1 and self.bw == self.cols)
+
+    @property
+    def stored_rows(self) -> int:
+        """Rows of the stored matrix: the weight rows, or the blocks of M' (C-34)."""
+        return (self.rows // self.bh) * (self.cols // self.bw) if self.blocked else self.rows
+
+    @property
+    def stored_cols(self) -> int:
+        return self.bh * self.bw if self.blocked else self.cols
+
+    def unflatten(self, i, p):
+        """(weight row, weight column) of position p of stored row i (Alg. 2
+        lines 11-13: col_id = (i % (cols/bw)) * bw, row_id = (i / (cols/bw)) * bh)."""
+        if not self.blocked:
+            return i, p
+        nbj = self.cols // self.bw
+        i = np.asarray(i)
+        p = np.asarray(p)
+        return (i // nbj) * self.bh + p // self.bw, (i % nbj) * self.bw + p % self.bw
+
 
 def _table(lengths: Dict[int, int]) -> bytes:
     out = [struct.pack("<H", len(lengths))]
@@ -73,7 +101,7 @@ def serialize(layers: List[Layer]) -> bytes:
         out.append(cb.tobytes())
         out.append(_table(L.val_lengths))
         out.append(_table(L.gap_lengths))
-        rp = np.asarray(L.row_ptr, dtype="<u8").reshape(L.rows + 1, 2)
+        rp = np.asarray(L.row_ptr, dtype="<u8").reshape(L.stored_rows + 1, 2)
         out.append(rp.tobytes())
         nv = (int(rp[-1, 0]) + 7) // 8
         ng = (int(rp[-1, 1]) + 7) // 8
@@ -128,7 +156,10 @@ def deserialize(buf: bytes) -> List[Layer]:
         cb = np.frombuffer(rd.take(4 * ncb), dtype="<f4").astype(np.float32)
         vl = _read_table(rd)
         gl = _read_table(rd)
-        rp = np.frombuffer(rd.take(16 * (rows + 1)), dtype="<u8").reshape(rows + 1, 2).astype(np.int64)
+        if bh == 0 or bw == 0 or rows % bh or cols % bw:
+            raise CDNIError("malformed", f"block {bh}x{bw} does not tile {rows}x{cols}")
+        nst = rows if (bh == 1 and bw == cols) else (rows // bh) * (cols // bw)
+        rp = np.frombuffer(rd.take(16 * (nst + 1)), dtype="<u8").reshape(nst + 1, 2).astype(np.int64)
         vb = rd.take((int(rp[-1, 0]) + 7) // 8)
         gb = rd.take((int(rp[-1, 1]) + 7) // 8)
         (hb,) = rd.unpack("<B")

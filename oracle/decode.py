@@ -30,19 +30,22 @@ def decode_row_tokens(layer: cdni.Layer, i: int, vdec=None, gdec=None) -> List[T
         raise cdni.CDNIError("malformed", f"row {i}: {len(dec_val)} val vs {len(dec_col)} col tokens")
     out = []
     for c, q in relindex.decode_row(dec_val, dec_col):
-        if c >= layer.cols:
-            raise cdni.CDNIError("malformed", f"row {i}: column {c} >= {layer.cols}")
+        if c >= layer.stored_cols:
+            raise cdni.CDNIError("malformed", f"row {i}: column {c} >= {layer.stored_cols}")
         out.append((c, q, float(layer.codebook[q])))
     return out
 
 
 def decode_layer(layer: cdni.Layer, rows: Optional[Iterable[int]] = None):
-    """Returns arrays (row, col, sym, val) of every token of the selected rows
-    in row-major token order, pads included."""
+    """Returns arrays (row, col, sym, val) of every token of the selected
+    stored rows in stored token order, pads included.  Row and column are the
+    stored matrix's: for a blocked layer (Alg. 2, C-34) the block index and
+    the position inside the flattened block (cdni.Layer.unflatten maps them
+    back to the weight matrix)."""
     vdec = huffman.CanonicalDecoder(layer.val_lengths)
     gdec = huffman.CanonicalDecoder(layer.gap_lengths)
     R, C, S, V = [], [], [], []
-    for i in (range(layer.rows) if rows is None else rows):
+    for i in (range(layer.stored_rows) if rows is None else rows):
         for c, q, v in decode_row_tokens(layer, i, vdec, gdec):
             R.append(i); C.append(c); S.append(q); V.append(v)
     return (np.array(R, dtype=np.int64), np.array(C, dtype=np.int64),
@@ -54,5 +57,6 @@ def decode_dense(layer: cdni.Layer) -> np.ndarray:
     r, c, s, v = decode_layer(layer)
     W = np.zeros((layer.rows, layer.cols), dtype=np.float32)
     real = s != 0
-    W[r[real], c[real]] = v[real]
+    wr, wc = layer.unflatten(r[real], c[real])   # Alg. 2 l.10-13 for a blocked layer
+    W[wr, wc] = v[real]
     return W

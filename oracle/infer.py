@@ -44,6 +44,29 @@ def fc_forward(Wq, a: np.ndarray, bias=None, apply_relu: bool = False) -> np.nda
     return relu(y) if apply_relu else y
 
 
+def fc_forward_blocked(layer, a: np.ndarray, bias=None, apply_relu: bool = False) -> np.ndarray:
+    """Algorithm 2 step by step, fp64: for every stored row i of a
+    block-contiguous layer (C-34) decode it (l.4-8), arrange the values as the
+    bh x bw block (l.9), and add block @ a[:, col_id:col_id+bw] into
+    y[:, row_id:row_id+bh] (l.10-12; MKL_CSRMM of the paper = a plain product)."""
+    from . import decode  # local: decode imports nothing from here
+    a64 = np.asarray(a, dtype=np.float64)
+    y = np.zeros((a64.shape[0], layer.rows), dtype=np.float64)
+    nbj = layer.cols // layer.bw
+    for i in range(layer.stored_rows):
+        blk = np.zeros(layer.bh * layer.bw, dtype=np.float64)
+        for c, q, v in decode.decode_row_tokens(layer, i):
+            if q != 0:
+                blk[c] = v
+        blk = blk.reshape(layer.bh, layer.bw)
+        col_id = (i % nbj) * layer.bw
+        row_id = (i // nbj) * layer.bh
+        y[:, row_id:row_id + layer.bh] += a64[:, col_id:col_id + layer.bw] @ blk.T
+    if bias is not None:
+        y = y + np.asarray(bias, dtype=np.float64)[None, :]
+    return relu(y) if apply_relu else y
+
+
 def fc_abs_scale(Wq, a: np.ndarray, bias=None) -> np.ndarray:
     """sum_j |W_ij a_j| + |v_i|: the natural scale of each output's rounding
     error (used to report the elementwise error metric)."""

@@ -141,6 +141,56 @@ def test_kmeans_decode_of_compress_is_prune_quantize(seed, d, r, k):
     assert np.array_equal(decode.decode_dense(c.layer), c.dense_q())
 
 
+# ------------------------------------ block-contiguous container (Alg. 2, C-34)
+
+def test_blocked_layout_paper_example():
+    """an 8x8 matrix in 4x4 blocks becomes 4x16, each row one block
+    stored contiguously; Alg. 2 l.11-12 map stored row i back to
+    (row_id, col_id) = ((i / (cols/bw)) * bh, (i % (cols/bw)) * bw)."""
+    A = np.arange(64).reshape(8, 8)
+    M = compress.to_blocked(A, 4, 4)
+    assert M.shape == (4, 16)
+    assert M[0].tolist() == [0, 1, 2, 3, 8, 9, 10, 11, 16, 17, 18, 19, 24, 25, 26, 27]
+    assert M[1].tolist() == [4, 5, 6, 7, 12, 13, 14, 15, 20, 21, 22, 23, 28, 29, 30, 31]
+    assert M[2, 0] == 32 and M[3, 15] == 63
+    L = cdni.Layer(8, 8, 4, 5, np.zeros(32, np.float32), {}, {}, np.zeros((5, 2), np.int64), b"", b"", None, 4, 4)
+    for i in range(4):
+        for p in range(16):
+            r, c = L.unflatten(i, p)
+            assert A[r, c] == M[i, p]
+
+
+@pytest.mark.parametrize("rows,cols,bh,bw,d,k", [(256, 512, 128, 128, 0.1, 4), (64, 256, 64, 256, 0.3, 2),
+                                                 (32, 128, 4, 64, 0.05, 4), (128, 192, 32, 64, 0.2, 8)])
+def test_blocked_decode_of_compress_is_prune_quantize(rows, cols, bh, bw, d, k):
+    W = synth.random_matrix(rows, cols, seed=rows + bh, scale=0.05)
+    c = compress.compress_layer(W, d, 5, k, bh=bh, bw=bw)
+    L = cdni.deserialize(cdni.serialize([c.layer]))[0]
+    assert (L.bh, L.bw, L.stored_rows) == (bh, bw, (rows // bh) * (cols // bw))
+    assert np.array_equal(decode.decode_dense(L), c.dense_q())
+    # the same prune/quantize as the unblocked container: only the storage order differs
+    u = compress.compress_layer(W, d, 5, k)
+    assert np.array_equal(u.dense_q(), c.dense_q())
+
+
+def test_blocked_unit_block_is_the_plain_container():
+    W = synth.random_matrix(20, 64, seed=3, scale=0.05)
+    a = compress.compress_layer(W, 0.3, 4, 3)
+    b = compress.compress_layer(W, 0.3, 4, 3, bh=1, bw=64)
+    assert cdni.serialize([a.layer]) == cdni.serialize([b.layer])
+
+
+def test_blocked_rejects_non_tiling_blocks():
+    W = synth.random_matrix(20, 64, seed=3, scale=0.05)
+    with pytest.raises(ValueError):
+        compress.compress_layer(W, 0.3, 4, 3, bh=3, bw=64)
+    c = compress.compress_layer(W, 0.3, 4, 3, bh=4, bw=32)
+    buf = bytearray(cdni.serialize([c.layer]))
+    buf[18:22] = (5).to_bytes(4, "little")           # bh = 5 does not divide 20 rows
+    with pytest.raises(cdni.CDNIError):
+        cdni.deserialize(bytes(buf))
+
+
 def test_relindex_spec_k2_example():
     # S:L96/L106: k=2, columns {0,5,11} -> gaps [0,3,0,3,1], vals [x,0,y,0,z]
     v, g = relindex.encode_row([0, 5, 11], [7, 8, 9], k=2)

@@ -179,3 +179,17 @@ def test_unconstrained_memory_gives_per_layer_optimum_shape():
     time = [{B: 10.0 + 0.01 * B for B in range(1, 9)} for _ in range(3)]
     p = planner.Problem(time, [1, 1, 1], [1, 1, 1], [0, 0, 0], tot=10 ** 9)
     assert planner.dp_plan(p, 8).batches == [8, 8, 8]
+
+
+@pytest.mark.parametrize("bh,bw", [(4, 64), (16, 32), (32, 128)])
+def test_algorithm2_blocked_inference_equals_dense_product(bh, bw):
+    """Alg. 2 step by step (decode a stored row, arrange bh x bw, multiply the
+    input slice, accumulate the output slice) = the plain product W_q a."""
+    from oracle import compress, infer
+    W = synth.random_matrix(64, 256, seed=bh + bw, scale=0.05)
+    v = synth.random_matrix(1, 64, seed=2).ravel()
+    c = compress.compress_layer(W, 0.15, 5, 4, v, bh=bh, bw=bw)
+    a = synth.random_activations(256, 5, seed=4)
+    y = infer.fc_forward_blocked(c.layer, a, v, apply_relu=True)
+    ref = infer.fc_forward(c.dense_q(), a, v, apply_relu=True)
+    assert np.allclose(y, ref, rtol=1e-12, atol=1e-12)
