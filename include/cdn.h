@@ -234,14 +234,18 @@ const char* cdn_layer_kernel_name(const cdn_model* m, int layer, int B);
  * Errors: CDN_E_ARG, CDN_E_UNSUPPORTED, CDN_E_OOM. */
 cdn_status cdn_compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols,
                               double density, int r, int k, void** out, size_t* out_len);
-/* As cdn_compress_dense with a choice of quantizer: 0 = the linear codebook
- * above (C-05), 1 = 1-D Lloyd k-means refined from that grid (C-33: binary64
- * nearest-centre assignment with ties to the smaller index, binary64 means in
- * row-major order, <= 50 iterations or until no centre moves by more than
- * 1e-7 max(|lo|,|hi|)).  Errors: as above, CDN_E_ARG for
- * another quantizer. */
+/* As cdn_compress_dense with a choice of quantizer and storage order.
+ * quantizer: 0 = the linear codebook above (C-05), 1 = 1-D Lloyd k-means
+ * refined from that grid (C-33: binary64 nearest-centre assignment with ties
+ * to the smaller index, binary64 means in row-major order, <= 50 iterations or
+ * until no centre moves by more than 1e-7 max(|lo|,|hi|)).
+ * bh x bw: 1 x 0 (0 = cols) is the plain row-major container; otherwise the
+ * block-contiguous container of Alg. 2 (C-34): rows % bh == 0,
+ * cols % bw == 0, relative indexing / Huffman / row_ptr over the stored rows
+ * of M' (block (bi, bj) flattened row-major = stored row bi*(cols/bw) + bj).
+ * Errors: as above, CDN_E_ARG for another quantizer or a non-tiling block. */
 cdn_status cdn_compress_dense_q(const float* W, const float* bias, uint32_t rows, uint32_t cols, double density,
-                                int r, int k, int quantizer, void** out, size_t* out_len);
+                                int r, int k, int quantizer, uint32_t bh, uint32_t bw, void** out, size_t* out_len);
 void cdn_free(void* p);
 
 /* Variable-batch DP of P:L694-720 on a given table (host).  time_ms[i*Bmax + B-1]

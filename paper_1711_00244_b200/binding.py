@@ -97,7 +97,8 @@ _SIGS = {
     "cdn_compress_dense": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_int,
                                        C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     "cdn_compress_dense_q": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_int,
-                                         C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+                                         C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p),
+                                         C.POINTER(C.c_size_t)]),
     "cdn_free": (None, [C.c_void_p]),
     "cdn_plan_dp": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_uint64,
                                 C.c_double, C.c_uint64, C.c_void_p, C.POINTER(C.c_double)]),
@@ -150,9 +151,10 @@ def nccl_unique_id() -> bytes:
 
 
 def compress_dense(W: np.ndarray, density: float, r: int, k: int, bias: Optional[np.ndarray] = None,
-                   quantizer: str = "linear") -> bytes:
+                   quantizer: str = "linear", bh: int = 1, bw: int = 0) -> bytes:
     """Product-side compressor: dense fp32 -> single-layer CDNI bytes
-    (quantizer "linear" = C-05 grid, "kmeans" = Lloyd refinement, C-33)."""
+    (quantizer "linear" = C-05 grid, "kmeans" = Lloyd refinement, C-33;
+    bh x bw != 1 x cols: the block-contiguous container of Alg. 2, C-34)."""
     W = np.ascontiguousarray(W, dtype=np.float32)
     b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
     out = C.c_void_p()
@@ -160,7 +162,8 @@ def compress_dense(W: np.ndarray, density: float, r: int, k: int, bias: Optional
     lib = load_library()
     qz = {"linear": 0, "kmeans": 1}[quantizer]
     _check(lib.cdn_compress_dense_q(W.ctypes.data, None if b is None else b.ctypes.data, W.shape[0], W.shape[1],
-                                    float(density), int(r), int(k), qz, C.byref(out), C.byref(n)))
+                                    float(density), int(r), int(k), qz, int(bh), int(bw), C.byref(out),
+                                    C.byref(n)))
     try:
         return C.string_at(out, n.value)
     finally:

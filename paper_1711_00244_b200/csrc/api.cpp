@@ -93,6 +93,7 @@ struct Layer {
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
+  bool blocked = false;  // block-contiguous container (Alg. 2, C-34): tensor-core path only
   cdn_layer_stats stats{};
   bool is_conv() const { return desc.kind == CDN_LAYER_CONV; }
   // features per image this layer produces (NHWC flatten for CONV, C-22)
@@ -223,6 +224,10 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   HostLayer H = parse_cdni_layer(buf, n, idx);
   if (d.kind != CDN_LAYER_FC && d.kind != CDN_LAYER_CONV) throw Error(CDN_E_ARG, "unknown layer kind");
   const bool conv = d.kind == CDN_LAYER_CONV;
+  const bool blocked = H.blocked();
+  if (blocked && (conv || m.world > 1 || H.bw % 64))
+    throw Error(CDN_E_UNSUPPORTED,
+                "block-contiguous layers (Alg. 2): FC on one GPU with bw a multiple of 64 (tensor-core path)");
   int conv_h = 0, conv_w = 0, out_h = 0, out_w = 0;
   if (conv) {
     if (d.in_c <= 0 || d.in_h <= 0 || d.in_w <= 0 || d.kh <= 0 || d.kw <= 0 || d.stride <= 0 || d.pad < 0 ||
@@ -243,7 +248,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   }
   if (!m.layers.empty()) {
     const Layer& prev = *m.layers.back();
-    const uint64_t need = conv ? (uint64_t)d.in_h * d.in_w * d.in_c : H.cols;
+    const uint64_t need = conv ? (uint64_t)d.in_h * d.in_w * d.in_c : H.wcols;
     if (prev.out_elems() != need || (conv && prev.is_conv() && (int)prev.rows != d.in_c))
       throw Error(CDN_E_SHAPE, "layer input features " + std::to_string(need) + " != previous output " +
                                    std::to_string(prev.out_elems()));
@@ -255,10 +260,11 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   L.conv_w = conv_w;
   L.out_h = out_h;
   L.out_w = out_w;
-  L.rows = H.rows;
-  L.cols = H.cols;
+  L.rows = H.wrows;
+  L.cols = H.wcols;
   L.k = H.k;
   L.r = H.r;
+  L.blocked = blocked;
   // FC: row-block shard per rank; CONV: replicas (every rank
   // holds all filters; the batch is what multi-GPU splits for conv layers).
   const ShardSlice sl = shard_slice(H, m.rank, m.world, conv);
@@ -295,6 +301,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     const double dens = nr ? (double)ix.nnz / ((double)nr * H.cols) : 1.0;
     uint32_t Wi = 16;
     while (Wi < 64 && (double)(2 * Wi) * dens <= 3.0) Wi <<= 1;
+    if (blocked) Wi = 64;  // the intervals then also index the tensor-core list (bw % 64 == 0)
     IntervalIndex iv;
     build_interval_index(H, L.row0, L.row1, Wi, iv);
     std::vector<uint32_t> ivg(2 * iv.v.size());
@@ -324,7 +331,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     IntervalIndex t64;
     const IntervalIndex* i64 = nullptr;
     if (Wi == 64) {
-      L.dev.tNI = (int)iv.NI;
+      L.dev.sNI = (int)iv.NI;
       i64 = &iv;
     } else if (!conv) {
       build_interval_index(H, L.row0, L.row1, 64, t64);
@@ -338,14 +345,28 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       }
       L.tivg.upload(tg);
       L.tivm.upload(tm);
-      L.dev.tNI = (int)t64.NI;
+      L.dev.sNI = (int)t64.NI;
     }
     if (i64 && !conv) {
       // decoded-list layout of the tensor-core path (tc.cu): one u16 per real
       // token, grouped in (128-row tile, 64-column K tile) blocks, block (rt, kt)
       // at tbase[rt * NI + kt], rows in order inside; troff[(rt * NI + kt) * 129 + r]
       // = offset of row r's entries in the block ([128] = the block's count)
-      const uint32_t NI = i64->NI, nrt = (nr + 127) / 128;
+      // Blocked (C-34): stored row i, interval j -> weight row and K tile
+      // (the host twin of tc.cu list_block).
+      const uint32_t SNI = i64->NI;
+      const uint32_t NI = blocked ? H.wcols / 64 : SNI;
+      const uint32_t nout = blocked ? H.wrows : nr;
+      const uint32_t nrt = (nout + 127) / 128;
+      std::vector<uint32_t> cnt((size_t)nout * NI, 0);
+      const uint32_t nbj = H.wcols / H.bw;
+      for (uint32_t i = 0; i < nr; ++i)
+        for (uint32_t j = 0; j < SNI; ++j) {
+          const uint32_t bi = i / nbj, bj = i % nbj, p0 = j * 64;
+          const uint32_t g = blocked ? bi * H.bh + p0 / H.bw : i;
+          const uint32_t kt = blocked ? (bj * H.bw + p0 % H.bw) / 64 : j;
+          cnt[(size_t)g * NI + kt] += i64->nnz[(size_t)i * SNI + j];
+        }
       std::vector<uint32_t> tb((size_t)nrt * NI);
       std::vector<uint16_t> to((size_t)nrt * NI * 129);
       uint64_t off = 0;
@@ -357,11 +378,12 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
           for (uint32_t r = 0; r < 128; ++r) {
             to[blk * 129 + r] = (uint16_t)o;
             const uint32_t row = rt * 128 + r;
-            if (row < nr) o += i64->nnz[(size_t)row * NI + kt];
+            if (row < nout) o += cnt[(size_t)row * NI + kt];
           }
           to[blk * 129 + 128] = (uint16_t)o;  // <= 128 * 64
           off += o;
         }
+      L.dev.tNI = (int)NI;
       if (off >= (1ull << 32)) throw Error(CDN_E_UNSUPPORTED, "shard with >= 2^32 nonzeros");
       L.tbase.upload(tb);
       L.troff.upload(to);
@@ -369,7 +391,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       // list-decoder tasks: chunks of up to kTcChunk K tiles, fewer when that
       // would leave the GPU short of threads (~64k wanted; measured on C5 fc7/fc8)
       int tch = kTcChunk;
-      while (tch > 1 && (uint64_t)nrt * 128 * ((NI + tch - 1) / tch) < 65536) tch >>= 1;
+      while (tch > 1 && (uint64_t)((nr + 127) / 128) * 128 * ((SNI + tch - 1) / tch) < 65536) tch >>= 1;
       if (const char* e = std::getenv("CDN_TC_CHUNK")) tch = std::max(1, std::min(kTcChunk, std::atoi(e)));
       L.dev.tch = tch;
     }
@@ -402,9 +424,10 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   L.vsorted.upload(vs);
   L.gsorted.upload(gs);
   L.cb.upload(H.codebook);
-  std::vector<float> bias(nr, 0.f);
+  const uint32_t nout = blocked ? H.wrows : nr;  // output rows of this rank
+  std::vector<float> bias(nout, 0.f);
   if (H.has_bias)
-    for (uint32_t i = 0; i < nr; ++i) bias[i] = H.bias[L.row0 + i];
+    for (uint32_t i = 0; i < nout; ++i) bias[i] = H.bias[(blocked ? 0 : L.row0) + i];
   L.bias.upload(bias);
 
   FcDev& f = L.dev;
@@ -423,6 +446,10 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.bias = L.bias.as<float>();
   f.nrows = (int)nr;
   f.cols = (int)H.cols;
+  f.wrows = (int)nout;
+  f.wcols = (int)H.wcols;
+  f.bh = (int)H.bh;
+  f.bw = (int)H.bw;
   f.G = ix.G;
   f.log2G = ix.log2G;
   f.W = (int)ix.W;
@@ -450,10 +477,10 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.ivm = L.ivm.as<uint16_t>();
 
   cdn_layer_stats& s = L.stats;
-  s.rows = H.rows;
-  s.cols = H.cols;
-  s.row_begin = L.row0;
-  s.row_end = L.row1;
+  s.rows = H.wrows;
+  s.cols = H.wcols;
+  s.row_begin = blocked ? 0 : L.row0;
+  s.row_end = blocked ? H.wrows : L.row1;
   s.k = H.k;
   s.r = H.r;
   s.lanes_per_row = (uint32_t)ix.G;
@@ -463,7 +490,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   s.nnz = ix.nnz;
   s.stream_bytes = (v1 - v0 + 7) / 8 + (g1 - g0 + 7) / 8;
   s.algo_bytes_fixed = s.stream_bytes + 8ull * (nr + 1) + 4ull * H.codebook.size() +
-                       3ull * (H.val.n + H.gap.n) + 4ull * nr;
+                       3ull * (H.val.n + H.gap.n) + 4ull * nout;
   s.index_bytes = ix.rec64 ? 8ull * ix.rec64v.size() : 4ull * ix.rec32.size();
   s.ws_bytes = 0;
   s.in_features = L.in_elems();
@@ -508,7 +535,12 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
   // Default policy for B >= 128: both large-batch kernels are timed once at the
   // first call with this B and the faster is kept for the layer (autotune).
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
-  if (m.tc_min == 0 && m.band_min == 0 && B >= 128 && tc_supported(L.dev) && ldx % 4 == 0) {
+  if (L.blocked) {
+    // the block-contiguous container (Alg. 2) is consumed by the list decoder
+    // of the tensor-core path only
+    if (!tc_supported(L.dev)) throw Error(CDN_E_UNSUPPORTED, "blocked layer outside the tensor-core path's limits");
+    tcmin = 1;
+  } else if (m.tc_min == 0 && m.band_min == 0 && B >= 128 && tc_supported(L.dev) && ldx % 4 == 0) {
     int choice = -1;
     for (auto& e : L.kchoice)
       if (e.first == B) choice = e.second;
@@ -585,6 +617,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
 // (a batch whose first-use autotune has not run yet counts as no).
 bool uses_tc(const Model& m, const Layer& L, int B) {
   if (L.is_conv() || !tc_supported(L.dev)) return false;
+  if (L.blocked) return true;
   if (m.tc_min == 0 && m.band_min == 0 && B >= 128) {
     for (auto& e : L.kchoice)
       if (e.first == B) return e.second == 1;
@@ -1178,6 +1211,7 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
   const Model& m = h->m;
   const Layer& L = *m.layers[layer];
   if (L.is_conv()) return "k_gemm_bf16 (conv)";
+  if (L.blocked) return "k_fc_tc";
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
   if (m.tc_min == 0 && m.band_min == 0 && B >= 128 && tc_supported(L.dev)) {
     for (auto& e : L.kchoice)
@@ -1205,14 +1239,14 @@ cdn_status cdn_model_memory_model(cdn_model* h, int Bmax, uint64_t* in_b, uint64
 
 cdn_status cdn_compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols, double density,
                               int r, int k, void** out, size_t* out_len) {
-  return cdn_compress_dense_q(W, bias, rows, cols, density, r, k, 0, out, out_len);
+  return cdn_compress_dense_q(W, bias, rows, cols, density, r, k, 0, 1, 0, out, out_len);
 }
 
 cdn_status cdn_compress_dense_q(const float* W, const float* bias, uint32_t rows, uint32_t cols, double density,
-                                int r, int k, int quantizer, void** out, size_t* out_len) {
+                                int r, int k, int quantizer, uint32_t bh, uint32_t bw, void** out, size_t* out_len) {
   API_BEGIN
   if (!W || !out || !out_len) return fail(CDN_E_ARG, "NULL argument");
-  std::vector<uint8_t> v = compress_dense(W, bias, rows, cols, density, r, k, quantizer);
+  std::vector<uint8_t> v = compress_dense(W, bias, rows, cols, density, r, k, quantizer, bh, bw);
   void* p = std::malloc(v.size());
   if (!p) return fail(CDN_E_OOM, "malloc");
   std::memcpy(p, v.data(), v.size());

@@ -117,6 +117,17 @@ HostLayer read_layer(Rd& rd, bool keep) {
   read_table(rd, L.val);
   read_table(rd, L.gap);
   if (L.rows == 0 || L.cols == 0) throw Error(CDN_E_MALFORMED, "empty layer geometry");
+  if (L.bh == 0 || L.bw == 0 || L.rows % L.bh || L.cols % L.bw)
+    throw Error(CDN_E_MALFORMED, "block " + std::to_string(L.bh) + "x" + std::to_string(L.bw) +
+                                     " does not tile the matrix (C-34)");
+  L.wrows = L.rows;
+  L.wcols = L.cols;
+  if (L.blocked()) {  // the streams index M' (Alg. 2)
+    const uint64_t nst = (uint64_t)(L.wrows / L.bh) * (L.wcols / L.bw), sc = (uint64_t)L.bh * L.bw;
+    if (nst >= (1ull << 31) || sc >= (1ull << 31)) throw Error(CDN_E_UNSUPPORTED, "blocked layer too large");
+    L.rows = (uint32_t)nst;
+    L.cols = (uint32_t)sc;
+  }
   const uint8_t* rp = rd.take(16ull * (L.rows + 1ull));
   L.rp.resize(2ull * (L.rows + 1));
   std::memcpy(L.rp.data(), rp, 16ull * (L.rows + 1ull));
@@ -125,10 +136,8 @@ HostLayer read_layer(Rd& rd, bool keep) {
   const uint8_t* vb = rd.take((L.vbits + 7) / 8);
   const uint8_t* gb = rd.take((L.gbits + 7) / 8);
   uint8_t hb = rd.get<uint8_t>();
-  const uint8_t* bias = hb ? rd.take(4ull * L.rows) : nullptr;
+  const uint8_t* bias = hb ? rd.take(4ull * L.wrows) : nullptr;
   if (!keep) return L;
-  if (L.bh != 1 || L.bw != L.cols)
-    throw Error(CDN_E_UNSUPPORTED, "blocked (bh x bw) layout not supported by this build");
   if (L.k < 1 || L.k > 8 || L.r < 1 || L.r > 8) throw Error(CDN_E_UNSUPPORTED, "k and r must be in 1..8");
   if (ncb != (1u << L.r)) throw Error(CDN_E_MALFORMED, "codebook size != 2^r");
   if (hb > 1) throw Error(CDN_E_MALFORMED, "bias flag");
@@ -146,8 +155,8 @@ HostLayer read_layer(Rd& rd, bool keep) {
   L.gbytes.resize(L.gbytes.size() + 8, 0);
   L.has_bias = hb != 0;
   if (bias) {
-    L.bias.resize(L.rows);
-    std::memcpy(L.bias.data(), bias, 4ull * L.rows);
+    L.bias.resize(L.wrows);
+    std::memcpy(L.bias.data(), bias, 4ull * L.wrows);
   }
   return L;
 }
@@ -333,9 +342,12 @@ ShardSlice shard_slice(const HostLayer& H, int rank, int world, bool replicate) 
 }
 
 HostLayer slice_rows(const HostLayer& H, const ShardSlice& sl) {
+  if (H.blocked()) throw Error(CDN_E_UNSUPPORTED, "row shards of a blocked layer");
   HostLayer S;
   S.rows = sl.row1 - sl.row0;
   S.cols = H.cols;
+  S.wrows = S.rows;
+  S.wcols = H.wcols;
   S.bh = H.bh;
   S.bw = H.bw;
   S.k = H.k;
@@ -429,8 +441,10 @@ template <class T> void put(std::vector<uint8_t>& o, T v) {
 }  // namespace
 
 std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols,
-                                    double density, int r, int k, int quantizer) {
+                                    double density, int r, int k, int quantizer, uint32_t bh, uint32_t bw) {
   if (quantizer != 0 && quantizer != 1) throw Error(CDN_E_ARG, "quantizer must be 0 (linear) or 1 (k-means)");
+  if (bw == 0) bw = cols;
+  if (bh == 0 || rows % bh || cols % bw) throw Error(CDN_E_ARG, "block does not tile the matrix (C-34)");
   if (!W || rows == 0 || cols == 0) throw Error(CDN_E_ARG, "empty matrix");
   if (r < 1 || r > 8 || k < 1 || k > 8) throw Error(CDN_E_UNSUPPORTED, "k and r must be in 1..8");
   if (!(density >= 0.0 && density <= 1.0)) throw Error(CDN_E_ARG, "density must be in [0,1]");
@@ -505,15 +519,22 @@ std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t 
       for (int j = 0; j < nc; ++j) cb[j + 1] = (float)c[j];
     }
   }
-  // relative index (C-01..03) + token streams
+  // relative index (C-01..03) + token streams, over the stored
+  // rows: the weight rows, or the blocks of M' (Alg. 2, C-34) flattened
+  // row-major (position p of block (bi, bj) = weight (bi*bh + p/bw, bj*bw + p%bw))
   const uint32_t cap = (1u << k) - 1;
+  const bool blocked = !(bh == 1 && bw == cols);
+  const uint32_t nbj = cols / bw;
+  const uint32_t srows = blocked ? (rows / bh) * nbj : rows, scols = blocked ? bh * bw : cols;
   std::vector<uint8_t> vt, gt;
-  std::vector<uint64_t> row_tok(rows + 1, 0);
-  for (uint32_t i = 0; i < rows; ++i) {
+  std::vector<uint64_t> row_tok(srows + 1, 0);
+  for (uint32_t i = 0; i < srows; ++i) {
     row_tok[i] = vt.size();
     int64_t prev = -1;
-    for (uint32_t c = 0; c < cols; ++c) {
-      uint64_t idx = (uint64_t)i * cols + c;
+    const uint32_t bi = i / nbj, bj = i % nbj;
+    for (uint32_t c = 0; c < scols; ++c) {
+      const uint64_t idx = blocked ? (uint64_t)(bi * bh + c / bw) * cols + bj * bw + c % bw
+                                   : (uint64_t)i * cols + c;
       if (!keep[idx]) continue;
       const double w = (double)W[idx];
       int best = 1;
@@ -534,7 +555,7 @@ std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t 
       prev = c;
     }
   }
-  row_tok[rows] = vt.size();
+  row_tok[srows] = vt.size();
   // Huffman per stream (C-14..17)
   std::vector<uint64_t> fv(ncb, 0), fg(1u << k, 0);
   for (uint8_t s : vt) fv[s]++;
@@ -548,8 +569,8 @@ std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t 
   hv.build(ncb, "val");
   hg.build(1 << k, "gap");
   BitWriter bv, bg;
-  std::vector<uint64_t> rp(2ull * (rows + 1));
-  for (uint32_t i = 0; i < rows; ++i) {
+  std::vector<uint64_t> rp(2ull * (srows + 1));
+  for (uint32_t i = 0; i < srows; ++i) {
     rp[2ull * i] = bv.nbits;
     rp[2ull * i + 1] = bg.nbits;
     for (uint64_t t = row_tok[i]; t < row_tok[i + 1]; ++t) {
@@ -557,14 +578,14 @@ std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t 
       bg.put(hg.code_of[gt[t]], hg.len_of[gt[t]]);
     }
   }
-  rp[2ull * rows] = bv.nbits;
-  rp[2ull * rows + 1] = bg.nbits;
+  rp[2ull * srows] = bv.nbits;
+  rp[2ull * srows + 1] = bg.nbits;
   // serialize
   std::vector<uint8_t> o;
   o.insert(o.end(), {'C', 'D', 'N', 'I'});
   put<uint16_t>(o, 1);
   put<uint32_t>(o, 1);
-  put<uint32_t>(o, rows); put<uint32_t>(o, cols); put<uint32_t>(o, 1); put<uint32_t>(o, cols);
+  put<uint32_t>(o, rows); put<uint32_t>(o, cols); put<uint32_t>(o, bh); put<uint32_t>(o, bw);
   put<uint8_t>(o, (uint8_t)k); put<uint8_t>(o, (uint8_t)r);
   put<uint16_t>(o, (uint16_t)ncb);
   for (float v : cb) put<float>(o, v);

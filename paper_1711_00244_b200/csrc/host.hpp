@@ -37,7 +37,12 @@ struct HuffCode {
 };
 
 struct HostLayer {
+  // rows x cols = the STORED matrix the streams and row_ptr index: the weight
+  // matrix, or for the block-contiguous container of Alg. 2 (C-34) its M'
+  // (one stored row per bh x bw block, flattened row-major)
   uint32_t rows = 0, cols = 0, bh = 1, bw = 0, k = 0, r = 0;
+  uint32_t wrows = 0, wcols = 0;  // the weight matrix (bias has wrows entries)
+  bool blocked() const { return !(bh == 1 && bw == wcols); }
   std::vector<float> codebook;
   HuffCode val, gap;
   std::vector<uint64_t> rp;       // 2*(rows+1): (val bit, gap bit) per row start
@@ -108,7 +113,8 @@ int choose_lanes_per_row(const HostLayer& L, uint32_t r0, uint32_t r1, int targe
 
 // Product-side compressor (independent of oracle/, same readings).
 std::vector<uint8_t> compress_dense(const float* W, const float* bias, uint32_t rows, uint32_t cols,
-                                    double density, int r, int k, int quantizer = 0);
+                                    double density, int r, int k, int quantizer = 0, uint32_t bh = 1,
+                                    uint32_t bw = 0);  // bw = 0: cols (unblocked)
 
 // Variable-batch DP with memory axis granularity `step` bytes.
 struct PlanResult {

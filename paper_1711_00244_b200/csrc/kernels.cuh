@@ -63,7 +63,13 @@ struct FcDev {
   // aliases ivg/ivm when the band index already uses Wi = 64
   const uint2* tivg = nullptr;
   const uint16_t* tivm = nullptr;
-  int tNI = 0;
+  int tNI = 0;                       // 64-column K tiles of the weight matrix (list blocks, contraction)
+  int sNI = 0;                       // 64-position intervals per stored row (tivg / tivm rows)
+  // Block-contiguous container (Alg. 2, C-34): nrows / cols above are the
+  // STORED matrix's (blocks of M' when blocked); the weight matrix is
+  // wrows x wcols in bh x bw blocks, stored row i = block (i / (wcols/bw),
+  // i % (wcols/bw)).  Unblocked: bh = 1, bw = wcols = cols, wrows = nrows.
+  int wrows = 0, wcols = 0, bh = 1, bw = 0;
   // decoded-entry list between the tensor-core path's two kernels: entry =
   // (column - 64 kt) | codebook index << 6, one per real token, in blocks of
   // (128-row tile rt, K tile kt) at tbase[rt * tNI + kt], rows in order inside,

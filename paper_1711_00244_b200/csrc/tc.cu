@@ -86,6 +86,21 @@ __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
   }
 }
 
+// List block of (stored row i, 64-position interval j) and the weight row's
+// slot in it: block (row tile, K tile) of the weight matrix.  Unblocked
+// (bw = wcols): row i, K tile j.  Blocked (Alg. 2 l.11-12, C-34; bw % 64 == 0):
+// block (bi, bj) = (i / nbj, i % nbj), position j*64 -> weight row
+// bi*bh + j*64/bw, column bj*bw + j*64 % bw.
+__device__ __forceinline__ size_t list_block(const FcDev& L, int i, int j, int& rr) {
+  const int nbj = L.wcols / L.bw;
+  const int bi = i / nbj, bj = i - bi * nbj;
+  const int p0 = j * 64;
+  const int g = bi * L.bh + p0 / L.bw;
+  const int kt = (bj * L.bw + p0 % L.bw) >> 6;
+  rr = g & 127;
+  return (size_t)(g >> 7) * L.tNI + kt;
+}
+
 // Stream-K work split: the tiles x nkt tile steps are cut into G equal
 // contiguous ranges, one per CTA; a CTA's range falls into one or more pieces
 // (tile, K range).  A tile covered by several CTAs is summed by k_tc_reduce
@@ -417,7 +432,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         ld = kTN;
       }
       (void)ld;
-      const float bias = (whole && row < L.nrows) ? L.bias[row] : 0.f;
+      const float bias = (whole && row < L.wrows) ? L.bias[row] : 0.f;
       // y rows are contiguous over the batch: whole float4s where the tile is inside B
       const bool vec_ok = (a.ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
       for (int c = 0; c < kTN; c += 16) {
@@ -428,7 +443,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
         if (whole) {
-          if (row < L.nrows) {
+          if (row < L.wrows) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               v[i] += bias;
@@ -602,28 +617,29 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
   // task = (row tile, chunk of L.tch <= kTcChunk K tiles, row in tile): consecutive
   // threads write adjacent slices of the same blocks
   const int tch = L.tch;
-  const int nch = (L.tNI + tch - 1) / tch;
+  const int nch = (L.sNI + tch - 1) / tch;
   const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
   const int r = (int)(task & 127);
   const size_t rc = task >> 7;
   const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
   const int row = rt * 128 + r;
   if (row >= L.nrows) return;
-  const int nk = L.tNI - kt0 < tch ? L.tNI - kt0 : tch;
+  const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
   // output slot of this row's first entry in each of the chunk's tiles
   uint32_t p[kTcChunk], n = 0;
 #pragma unroll
   for (int k = 0; k < kTcChunk; ++k) {
     p[k] = 0;
     if (k < nk) {
-      const size_t blk = (size_t)rt * L.tNI + kt0 + k;
-      const uint32_t o0 = L.troff[blk * 129 + r], o1 = L.troff[blk * 129 + r + 1];
+      int rr;
+      const size_t blk = list_block(L, row, kt0 + k, rr);
+      const uint32_t o0 = L.troff[blk * 129 + rr], o1 = L.troff[blk * 129 + rr + 1];
       p[k] = L.tbase[blk] + o0;
       n += o1 - o0;
     }
   }
   if (n == 0) return;
-  const size_t q = (size_t)row * L.tNI + kt0;
+  const size_t q = (size_t)row * L.sNI + kt0;
   const uint2 st = L.tivg[q];
   int col = kt0 * 64 - (int)(L.tivm[q] & 0xFFu) - 1;
   SReader vr, gr;
@@ -704,16 +720,16 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   __syncthreads();
   mbar_wait(&s_bar, 0);
   const int tch = L.tch;
-  const int nch = (L.tNI + tch - 1) / tch;
+  const int nch = (L.sNI + tch - 1) / tch;
   const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
   const int r = (int)(task & 127);
   const size_t rc = task >> 7;
   const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
   const int row = rt * 128 + r;
   if (row >= L.nrows) return;
-  const int nk = L.tNI - kt0 < tch ? L.tNI - kt0 : tch;
+  const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
   // the decoder state first (its loads gate everything), the output slots meanwhile
-  const size_t q = (size_t)row * L.tNI + kt0;
+  const size_t q = (size_t)row * L.sNI + kt0;
   const uint2 st = L.tivg[q];
   const uint32_t m0 = L.tivm[q];
   // this thread's first list slot in each tile of the chunk, in shared memory
@@ -723,8 +739,9 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   for (int k = 0; k < kTcChunk; ++k) {
     uint32_t pk = 0;
     if (k < nk) {
-      const size_t blk = (size_t)rt * L.tNI + kt0 + k;
-      const uint32_t o0 = L.troff[blk * 129 + r], o1 = L.troff[blk * 129 + r + 1];
+      int rr;
+      const size_t blk = list_block(L, row, kt0 + k, rr);
+      const uint32_t o0 = L.troff[blk * 129 + rr], o1 = L.troff[blk * 129 + rr + 1];
       pk = L.tbase[blk] + o0;
       left += o1 - o0;
     }
@@ -806,7 +823,7 @@ bool list_fold_forced() {
 }  // namespace
 
 bool tc_supported(const FcDev& L) {
-  return L.tivg && L.tivm && L.tNI > 0 && L.tbase && L.troff && L.tlist && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
+  return L.tivg && L.tivm && L.tNI > 0 && L.sNI > 0 && L.tbase && L.troff && L.tlist && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
          L.Lf == kFoldLutBits && L.Lg <= kLutMaxBits;
 }
 
@@ -814,9 +831,9 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   TcPlan p;
   if (!tc_supported(L) || B <= 0) return p;
   p.nbt = (B + kTN - 1) / kTN;
-  p.nrt = (L.nrows + kTM - 1) / kTM;
+  p.nrt = (L.wrows + kTM - 1) / kTM;
   p.nkt = L.tNI;
-  p.ldk = (L.cols + 7) & ~7;
+  p.ldk = (L.wcols + 7) & ~7;
   p.tiles = p.nrt * p.nbt;
   p.W = (long)p.tiles * p.nkt;
   long G;
@@ -852,7 +869,7 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
 
 cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
-  const size_t tasks = (size_t)((L.nrows + 127) / 128) * ((L.tNI + L.tch - 1) / L.tch) * 128;
+  const size_t tasks = (size_t)((L.nrows + 127) / 128) * ((L.sNI + L.tch - 1) / L.tch) * 128;
   const unsigned lgrid = (unsigned)((tasks + kListThreads - 1) / kListThreads);
   if (ms_supported(L) && !list_fold_forced()) {
     const size_t lsm = ms_smem_bytes(L);
@@ -879,10 +896,10 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   if (x_image_major) {
     const long n = (long)B * (p.ldk / 8);
     const int vec = (ldx % 4) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk, vec);
+    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk, vec);
   } else {
     dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
-    k_split_x<<<sg, 256, 0, s>>>(x, L.cols, ldx, B, xh, xl, p.ldk);
+    k_split_x<<<sg, 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk);
   }
   cudaError_t e = launched();
   ktimer_end("k_split_x", s);
@@ -915,7 +932,7 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   if (e == cudaSuccess && p.grid != p.tiles) {  // some tile is split over CTAs
     const long total = (long)p.tiles * kTM * (kTN / 4);
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
-    k_tc_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(ws, p.W, p.grid, p.nkt, p.mpt, p.nbt, L.nrows, B,
+    k_tc_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(ws, p.W, p.grid, p.nkt, p.mpt, p.nbt, L.wrows, B,
                                                                    L.bias, relu, y, ldy, vec_ok, total);
     e = launched();
   }

@@ -273,6 +273,83 @@ def test_paper_variants_all_kernels(torch_dev, quantizer, k, d, B, policy):
     m.close()
 
 
+# ------------------------------- block-contiguous container (Alg. 2)
+
+BLOCKED = [(512, 1024, 128, 128), (384, 768, 64, 256), (256, 640, 256, 64), (1024, 2048, 1024, 1024),
+           (300, 512, 100, 128)]
+
+
+def blocked_case(rows, cols, bh, bw, d=0.06):
+    key = ("blocked", rows, cols, bh, bw, d)
+    if key not in _CACHE:
+        W = synth.random_matrix(rows, cols, seed=(rows * 7 + bh) % 1000, scale=0.02)
+        v = synth.random_matrix(1, rows, seed=11).ravel()
+        c = compress.compress_layer(W, d, 5, 4, v, bh=bh, bw=bw)
+        _CACHE[key] = (c, cdni.serialize([c.layer]), v)
+    return _CACHE[key]
+
+
+@pytest.mark.parametrize("rows,cols,bh,bw", BLOCKED)
+@pytest.mark.parametrize("B", [1, 37, 300])
+def test_blocked_container_forward(torch_dev, rows, cols, bh, bw, B):
+    """Alg. 2's block-contiguous storage consumed natively: the list decoder
+    walks the stored rows of M' (blocks) and routes every entry to its weight
+    row / K tile; the tensor-core contraction is the same."""
+    torch, dev = torch_dev
+    c, buf, v = blocked_case(rows, cols, bh, bw)
+    m = make_model(torch, buf, relu=True)
+    assert m.kernel_name(0, B) == "k_fc_tc"
+    a = synth.fc_inputs(cols, B, 5)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=True, split_bf16=True)
+    if rows * cols <= 512 * 1024 and B == 37:   # and the paper's Alg. 2 itself, step by step
+        y = gpu_forward(torch, dev, m, a, rows)
+        ref = infer.fc_forward_blocked(c.layer, a, v, apply_relu=True)
+        assert rel_err(y, ref) <= TOL
+    m.close()
+
+
+def test_blocked_decode_hook_stored_coordinates(torch_dev):
+    """cdn_layer_decode on a blocked layer returns the stored matrix's tokens
+    (block index, position in the flattened block), bit-exact."""
+    torch, dev = torch_dev
+    c, buf, v = blocked_case(*BLOCKED[0])
+    m = make_model(torch, buf)
+    R, Cc, S, V = gpu_decode(torch, dev, m)
+    er, ec, es, ev = decode.decode_layer(c.layer)
+    assert np.array_equal(R, er) and np.array_equal(Cc, ec) and np.array_equal(S, es.astype(np.uint8))
+    assert np.array_equal(V.view(np.uint32), ev.astype(np.float32).view(np.uint32))
+    m.close()
+
+
+def test_blocked_layer_in_infer_stack(torch_dev):
+    """A blocked layer between plain ones inside infer (C3-sized)."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    W1 = synth.random_matrix(512, 1024, seed=21, scale=0.02)
+    v1 = synth.random_matrix(1, 512, seed=22).ravel()
+    c1 = compress.compress_layer(W1, 0.09, 5, 4, v1)
+    v2 = synth.random_matrix(1, 384, seed=26).ravel()
+    W3 = synth.random_matrix(100, 384, seed=23, scale=0.02)
+    v3 = synth.random_matrix(1, 100, seed=24).ravel()
+    c3 = compress.compress_layer(W3, 0.25, 5, 4, v3)
+    c2b = compress.compress_layer(synth.random_matrix(384, 512, seed=25, scale=0.02), 0.06, 5, 4, v2,
+                                  bh=128, bw=128)
+    m = cdn.Model(0)
+    m.load_layer(cdni.serialize([c1.layer]), cdn.LayerDesc.fc(True))
+    m.load_layer(cdni.serialize([c2b.layer]), cdn.LayerDesc.fc(True))
+    m.load_layer(cdni.serialize([c3.layer]), cdn.LayerDesc.fc(False))
+    K = 64
+    a = synth.fc_inputs(1024, K, 9)
+    scores = np.zeros((K, 100), np.float32)
+    m.set_plan([K, K, K])
+    m.infer(a, K, scores, on_device=False)
+    x = a
+    for c, v, relu in ((c1, v1, True), (c2b, v2, True), (c3, v3, False)):
+        x = infer.fc_forward(sparse_q(c), x, v, apply_relu=relu).astype(np.float32)
+    assert rel_err(scores, x) <= TOL
+    m.close()
+
+
 def test_tc_infer_stack_image_major_and_phases(torch_dev):
     """The tensor-core path inside infer: lists decoded ahead on the side stream
     and reused by later phases of the call, the first layer splitting the

@@ -63,6 +63,15 @@ def test_kmeans_compressor_byte_identical_to_oracle(seed, rows, cols, d, r, k):
     assert cdn.compress_dense(W, d, r, k, v, quantizer="kmeans") == ocdni.serialize([c.layer])
 
 
+@pytest.mark.parametrize("rows,cols,bh,bw,q", [(256, 512, 128, 128, "linear"), (64, 256, 4, 64, "kmeans"),
+                                               (30, 90, 10, 45, "linear"), (64, 64, 64, 64, "linear")])
+def test_blocked_compressor_byte_identical_to_oracle(rows, cols, bh, bw, q):
+    W = synth.random_matrix(rows, cols, seed=bh + bw, scale=0.05)
+    v = synth.random_matrix(1, rows, seed=3).ravel()
+    c = ocompress.compress_layer(W, 0.1, 5, 4, v, quantizer=q, bh=bh, bw=bw)
+    assert cdn.compress_dense(W, 0.1, 5, 4, v, quantizer=q, bh=bh, bw=bw) == ocdni.serialize([c.layer])
+
+
 def test_compressor_ties_and_duplicates():
     # many equal magnitudes: exact-count tie rule (C-10) and quantizer ties (C-07)
     rng = np.random.default_rng(3)
@@ -84,6 +93,19 @@ def test_host_walk_equals_oracle_decode():
     row, col, sym = cdn.debug_host_walk(buf)
     L = ocdni.deserialize(buf)[0]
     R, Cc, S, _ = odecode.decode_layer(L)
+    assert np.array_equal(row, R) and np.array_equal(col, Cc) and np.array_equal(sym, S)
+
+
+@pytest.mark.parametrize("bh,bw", [(128, 128), (4, 64), (64, 256)])
+def test_host_walk_blocked_equals_oracle_decode(bh, bw):
+    """A block-contiguous container (Alg. 2, C-34): the load-time walk runs over
+    the stored rows of M' (blocks) and reproduces the oracle's tokens."""
+    W = synth.random_matrix(256, 512, seed=bh, scale=0.05)
+    v = synth.random_matrix(1, 256, seed=1).ravel()
+    c = ocompress.compress_layer(W, 0.08, 5, 4, v, bh=bh, bw=bw)
+    buf = ocdni.serialize([c.layer])
+    row, col, sym = cdn.debug_host_walk(buf)
+    R, Cc, S, _ = odecode.decode_layer(c.layer)
     assert np.array_equal(row, R) and np.array_equal(col, Cc) and np.array_equal(sym, S)
 
 
@@ -116,10 +138,11 @@ def test_cdni_validation_errors():
     L3 = _layer_bytes()
     L3.val_lengths = {0: 1, 1: 33}
     _expect_error(ocdni.serialize([L3]), "CDN_E_UNSUPPORTED")
-    # blocked layout not supported
-    L4 = _layer_bytes()
-    L4.bh = 2
-    _expect_error(ocdni.serialize([L4]), "CDN_E_UNSUPPORTED")
+    # a block that does not tile the matrix (C-34)
+    bad = bytearray(good)
+    rows = struct.unpack_from("<I", bad, 10)[0]
+    bad[18:22] = struct.pack("<I", rows + 1)
+    _expect_error(bytes(bad), "CDN_E_MALFORMED")
     # row_ptr moved by one code: token counts of the two streams differ
     L5 = _layer_bytes()
     rp = L5.row_ptr.copy()
