@@ -391,7 +391,10 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       // list-decoder tasks: chunks of up to kTcChunk K tiles, fewer when that
       // would leave the GPU short of threads (~64k wanted; measured on C5 fc7/fc8)
       int tch = kTcChunk;
-      while (tch > 1 && (uint64_t)((nr + 127) / 128) * 128 * ((SNI + tch - 1) / tch) < 65536) tch >>= 1;
+      // task groups: a 128-row tile (adjacent list slots per warp), 32 rows for
+      // blocked layers, whose few long stored rows would leave most of a 128 idle
+      const uint64_t grp = blocked ? 32 : 128;
+      while (tch > 1 && (nr + grp - 1) / grp * grp * ((SNI + tch - 1) / tch) < 65536) tch >>= 1;
       if (const char* e = std::getenv("CDN_TC_CHUNK")) tch = std::max(1, std::min(kTcChunk, std::atoi(e)));
       L.dev.tch = tch;
     }

@@ -86,20 +86,46 @@ __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
   }
 }
 
-// List block of (stored row i, 64-position interval j) and the weight row's
-// slot in it: block (row tile, K tile) of the weight matrix.  Unblocked
-// (bw = wcols): row i, K tile j.  Blocked (Alg. 2 l.11-12, C-34; bw % 64 == 0):
-// block (bi, bj) = (i / nbj, i % nbj), position j*64 -> weight row
-// bi*bh + j*64/bw, column bj*bw + j*64 % bw.
-__device__ __forceinline__ size_t list_block(const FcDev& L, int i, int j, int& rr) {
-  const int nbj = L.wcols / L.bw;
-  const int bi = i / nbj, bj = i - bi * nbj;
-  const int p0 = j * 64;
-  const int g = bi * L.bh + p0 / L.bw;
-  const int kt = (bj * L.bw + p0 % L.bw) >> 6;
-  rr = g & 127;
-  return (size_t)(g >> 7) * L.tNI + kt;
-}
+// List blocks of the intervals j0, j0+1, ... of stored row i, and the weight
+// row's slot in each: block (row tile, K tile) of the weight matrix.
+// Unblocked (bw = wcols): row i, K tile j.  Blocked (Alg. 2 l.11-12, C-34;
+// bw % 64 == 0): block (bi, bj) = (i / nbj, i % nbj); position j*64 -> weight
+// row bi*bh + j*64/bw, column bj*bw + j*64 % bw.  One division per task, then
+// incremental steps (integer division is ~20 instructions).
+template <bool BLOCKED>
+struct ListMap {
+  int g, kt, c64, bw64, ktb;  // weight row, K tile, 64-block inside the block row, bw/64, first K tile of bj
+  __device__ __forceinline__ void init(const FcDev& L, int i, int j0) {
+    if (!BLOCKED) {
+      g = i;
+      kt = j0;
+      return;
+    }
+    const int nbj = L.wcols / L.bw;
+    const int bi = i / nbj, bj = i - bi * nbj;
+    bw64 = L.bw >> 6;
+    const int r = j0 / bw64;
+    c64 = j0 - r * bw64;
+    g = bi * L.bh + r;
+    ktb = bj * bw64;
+    kt = ktb + c64;
+  }
+  __device__ __forceinline__ size_t block(const FcDev& L, int& rr) const {
+    rr = g & 127;
+    return (size_t)(g >> 7) * L.tNI + kt;
+  }
+  __device__ __forceinline__ void next() {
+    if (!BLOCKED) {
+      ++kt;
+      return;
+    }
+    if (++c64 == bw64) {
+      c64 = 0;
+      ++g;
+    }
+    kt = ktb + c64;
+  }
+};
 
 // Stream-K work split: the tiles x nkt tile steps are cut into G equal
 // contiguous ranges, one per CTA; a CTA's range falls into one or more pieces
@@ -603,6 +629,7 @@ size_t tc_smem_bytes(const FcDev&) {
 // a row tile are consecutive threads, so their entry writes are adjacent.
 constexpr int kListThreads = 256;
 
+template <bool BLOCKED>
 __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
   __shared__ uint32_t s_flut[1 << kFoldLutBits];
   __shared__ uint32_t s_glut[1 << kLutMaxBits];
@@ -614,25 +641,34 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
   for (int i = threadIdx.x; i < L.nvs; i += blockDim.x) s_vsorted[i] = L.vsorted[i];
   for (int i = threadIdx.x; i < L.ngs; i += blockDim.x) s_gsorted[i] = L.gsorted[i];
   __syncthreads();
-  // task = (row tile, chunk of L.tch <= kTcChunk K tiles, row in tile): consecutive
+  // task = (row group, chunk of L.tch <= kTcChunk intervals, row in group): consecutive
   // threads write adjacent slices of the same blocks
   const int tch = L.tch;
   const int nch = (L.sNI + tch - 1) / tch;
   const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
-  const int r = (int)(task & 127);
-  const size_t rc = task >> 7;
+  // groups of 128 stored rows (a row tile: a warp's list slots are adjacent),
+  // 32 when blocked (few long stored rows)
+  constexpr int kGrp = BLOCKED ? 32 : 128, kGrpLog2 = BLOCKED ? 5 : 7;
+  const int r = (int)(task & (kGrp - 1));
+  const size_t rc = task >> kGrpLog2;
   const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
-  const int row = rt * 128 + r;
+  const int row = rt * kGrp + r;
   if (row >= L.nrows) return;
   const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
   // output slot of this row's first entry in each of the chunk's tiles
   uint32_t p[kTcChunk], n = 0;
 #pragma unroll
+  ListMap<BLOCKED> lm;
+  lm.init(L, row, kt0);
   for (int k = 0; k < kTcChunk; ++k) {
     p[k] = 0;
     if (k < nk) {
-      int rr;
-      const size_t blk = list_block(L, row, kt0 + k, rr);
+      int rr = r;
+      size_t blk = (size_t)rt * L.tNI + kt0 + k;  // unblocked: row tile rt, K tile kt0 + k
+      if constexpr (BLOCKED) {
+        blk = lm.block(L, rr);
+        lm.next();
+      }
       const uint32_t o0 = L.troff[blk * 129 + rr], o1 = L.troff[blk * 129 + rr + 1];
       p[k] = L.tbase[blk] + o0;
       n += o1 - o0;
@@ -696,6 +732,7 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
 // yields up to 4 codes, one on the gap stream up to 6; the two queues are
 // consumed up to 4 tokens per step, a pad being a token whose gap advances the
 // column by 2^k and whose symbol 0 emits nothing (C-01, C-04).
+template <bool BLOCKED>
 __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* s_vl = sm;
@@ -722,10 +759,13 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   const int tch = L.tch;
   const int nch = (L.sNI + tch - 1) / tch;
   const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
-  const int r = (int)(task & 127);
-  const size_t rc = task >> 7;
+  // groups of 128 stored rows (a row tile: a warp's list slots are adjacent),
+  // 32 when blocked (few long stored rows)
+  constexpr int kGrp = BLOCKED ? 32 : 128, kGrpLog2 = BLOCKED ? 5 : 7;
+  const int r = (int)(task & (kGrp - 1));
+  const size_t rc = task >> kGrpLog2;
   const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
-  const int row = rt * 128 + r;
+  const int row = rt * kGrp + r;
   if (row >= L.nrows) return;
   const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
   // the decoder state first (its loads gate everything), the output slots meanwhile
@@ -736,11 +776,17 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   // ([k][thread]: conflict-free) so the emission below picks it without branches
   uint32_t left = 0;
 #pragma unroll
+  ListMap<BLOCKED> lm;
+  lm.init(L, row, kt0);
   for (int k = 0; k < kTcChunk; ++k) {
     uint32_t pk = 0;
     if (k < nk) {
-      int rr;
-      const size_t blk = list_block(L, row, kt0 + k, rr);
+      int rr = r;
+      size_t blk = (size_t)rt * L.tNI + kt0 + k;  // unblocked: row tile rt, K tile kt0 + k
+      if constexpr (BLOCKED) {
+        blk = lm.block(L, rr);
+        lm.next();
+      }
       const uint32_t o0 = L.troff[blk * 129 + rr], o1 = L.troff[blk * 129 + rr + 1];
       pk = L.tbase[blk] + o0;
       left += o1 - o0;
@@ -869,21 +915,44 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
 
 cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
-  const size_t tasks = (size_t)((L.nrows + 127) / 128) * ((L.sNI + L.tch - 1) / L.tch) * 128;
+  const bool blocked = L.bw != L.wcols;
+  const size_t grp = blocked ? 32 : 128;
+  const size_t tasks = (size_t)((L.nrows + grp - 1) / grp) * ((L.sNI + L.tch - 1) / L.tch) * grp;
   const unsigned lgrid = (unsigned)((tasks + kListThreads - 1) / kListThreads);
   if (ms_supported(L) && !list_fold_forced()) {
-    const size_t lsm = ms_smem_bytes(L);
+    static const size_t pad = [] {
+      const char* e = std::getenv("CDN_LIST_SMEM_PAD");
+      return e ? (size_t)std::atoi(e) : (size_t)0;
+    }();
+    const size_t lsm = ms_smem_bytes(L) + pad;
     static size_t set_lsm = 0;
     if (lsm > set_lsm) {
-      e = cudaFuncSetAttribute(k_tc_list_ms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
-      if (e != cudaSuccess) return e;
+      for (auto kern : {k_tc_list_ms<false>, k_tc_list_ms<true>}) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
+        if (e != cudaSuccess) return e;
+      }
+      static const int carve = [] {
+        const char* c = std::getenv("CDN_LIST_CARVEOUT");
+        return c ? std::atoi(c) : -1;
+      }();
+      if (carve >= 0)
+        for (auto kern : {k_tc_list_ms<false>, k_tc_list_ms<true>}) {
+          e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+          if (e != cudaSuccess) return e;
+        }
       set_lsm = lsm;
     }
     ktimer_begin("k_tc_list", s);
-    k_tc_list_ms<<<lgrid, kListThreads, lsm, s>>>(L);
+    if (blocked)
+      k_tc_list_ms<true><<<lgrid, kListThreads, lsm, s>>>(L);
+    else
+      k_tc_list_ms<false><<<lgrid, kListThreads, lsm, s>>>(L);
   } else {
     ktimer_begin("k_tc_list", s);
-    k_tc_list<<<lgrid, kListThreads, 0, s>>>(L);
+    if (blocked)
+      k_tc_list<true><<<lgrid, kListThreads, 0, s>>>(L);
+    else
+      k_tc_list<false><<<lgrid, kListThreads, 0, s>>>(L);
   }
   e = launched();
   ktimer_end("k_tc_list", s);
