@@ -511,9 +511,9 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
 
 cudaStream_t pick(Model& m, void* s) { return s ? (cudaStream_t)s : m.stream; }
 
-// The tensor-core FC kernel is correct and parity-tested but, measured on B200,
-// still decode-bound and slower than the band kernel on C1-C5,
-// so it is opt-in: env CDN_TC_MIN_B or cdn_model_set_kernel_policy.
+// Explicit tensor-core threshold (env CDN_TC_MIN_B); without it and without a
+// kernel policy, B >= 128 is autotuned between the tensor-core and band kernels
+// at the first call with each B (fc_forward).
 int tc_min_batch() {
   static int v = [] {
     const char* e = std::getenv("CDN_TC_MIN_B");
