@@ -658,15 +658,9 @@ void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
   }
   CUDA_OK(cudaEventRecord(m.ev_call, s));
   CUDA_OK(cudaStreamWaitEvent(m.side, m.ev_call, 0));
-  static const int max_ahead = [] {
-    const char* e = std::getenv("CDN_LISTS_AHEAD");
-    return e ? std::atoi(e) : 1 << 20;
-  }();
-  int ahead = 0;
   for (size_t i = 0; i < m.layers.size(); ++i) {
     Layer& L = *m.layers[i];
     if (L.list_state != 0 || !uses_tc(m, L, bs[i])) continue;
-    if (ahead++ >= max_ahead) break;
     if (!L.list_ev) CUDA_OK(cudaEventCreateWithFlags(&L.list_ev, cudaEventDisableTiming));
     CUDA_OK(launch_tc_list(L.dev, m.side));
     CUDA_OK(cudaEventRecord(L.list_ev, m.side));

@@ -920,26 +920,13 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
   const size_t tasks = (size_t)((L.nrows + grp - 1) / grp) * ((L.sNI + L.tch - 1) / L.tch) * grp;
   const unsigned lgrid = (unsigned)((tasks + kListThreads - 1) / kListThreads);
   if (ms_supported(L) && !list_fold_forced()) {
-    static const size_t pad = [] {
-      const char* e = std::getenv("CDN_LIST_SMEM_PAD");
-      return e ? (size_t)std::atoi(e) : (size_t)0;
-    }();
-    const size_t lsm = ms_smem_bytes(L) + pad;
+    const size_t lsm = ms_smem_bytes(L);
     static size_t set_lsm = 0;
     if (lsm > set_lsm) {
       for (auto kern : {k_tc_list_ms<false>, k_tc_list_ms<true>}) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
         if (e != cudaSuccess) return e;
       }
-      static const int carve = [] {
-        const char* c = std::getenv("CDN_LIST_CARVEOUT");
-        return c ? std::atoi(c) : -1;
-      }();
-      if (carve >= 0)
-        for (auto kern : {k_tc_list_ms<false>, k_tc_list_ms<true>}) {
-          e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-          if (e != cudaSuccess) return e;
-        }
       set_lsm = lsm;
     }
     ktimer_begin("k_tc_list", s);
