@@ -41,6 +41,10 @@ cdn_status fail(cdn_status c, const std::string& m) {
   } while (0)
 
 // Owning device buffer.
+// bumped whenever a device buffer is (re)allocated or freed: captured graphs
+// hold raw pointers, so a changed counter retires them
+std::atomic<uint64_t> g_dbuf_gen{0};
+
 struct DBuf {
   void* p = nullptr;
   size_t n = 0;
@@ -54,7 +58,10 @@ struct DBuf {
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      g_dbuf_gen.fetch_add(1);
+    }
     p = nullptr;
     n = 0;
   }
@@ -62,6 +69,7 @@ struct DBuf {
     if (bytes <= n && p) return;
     release();
     CUDA_OK(cudaMalloc(&p, bytes ? bytes : 16));
+    g_dbuf_gen.fetch_add(1);
     n = bytes;
   }
   template <class T> void upload(const std::vector<T>& v) {
@@ -124,6 +132,17 @@ struct Model {
   int band_min = 0;             // cdn_model_set_kernel_policy (0: default)
   int tc_min = 0;               // cdn_model_set_kernel_policy tensor-core threshold (0: default)
   DBuf tc_xh, tc_xl;            // tensor-core FC: bf16 hi / lo split of the activations
+  // CUDA graphs of repeated infer calls (same buffers, K, plan and state):
+  // the second identical call is captured, later ones replay it
+  struct GraphEntry {
+    const float* in = nullptr;
+    float* out = nullptr;
+    int K = 0;
+    uint64_t sig = 0;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long launches = 0;  // kernels in the graph (the library's launch counter)
+  };
+  std::vector<GraphEntry> graphs;
 };
 
 uint32_t rows_per_rank(uint32_t rows, int world) { return (rows + world - 1) / world; }
@@ -974,6 +993,9 @@ void cdn_model_destroy(cdn_model* h) {
     h->m.lvl.clear();
     if (h->m.comm) ncclCommDestroy(h->m.comm);
     if (h->m.side) cudaStreamSynchronize(h->m.side);
+    for (auto& e : h->m.graphs)
+      if (e.exec) cudaGraphExecDestroy(e.exec);
+    h->m.graphs.clear();
     h->m.layers.clear();
     if (h->m.side) cudaStreamDestroy(h->m.side);
     if (h->m.ev_call) cudaEventDestroy(h->m.ev_call);
@@ -1035,17 +1057,10 @@ cdn_status cdn_model_plan(cdn_model* h, int K, int* batches, double* predicted_m
   API_END
 }
 
-cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* scores, int on_device, void* stream) {
-  API_BEGIN
-  if (!h || !input || K < 1 || (!scores && h->m.rank == 0)) return fail(CDN_E_ARG, "bad arguments");
-  Model& m = h->m;
-  if (m.layers.empty()) return fail(CDN_E_STATE, "no layers loaded");
-  if (m.busy) return fail(CDN_E_STATE, "concurrent call on one handle");
-  if (m.world > 1 && !m.comm) return fail(CDN_E_STATE, "shard-only handle (no NCCL id): use cdn_layer_forward");
-  m.busy = true;
-  struct Clear { bool& b; ~Clear() { b = false; } } clr{m.busy};
-  CUDA_OK(cudaSetDevice(m.device));
-  cudaStream_t s = pick(m, stream);
+namespace {
+
+// The work of one infer call on stream s (plans, list pre-decoding, rounds).
+void infer_body(Model& m, const float* input, int K, float* scores, int on_device, cudaStream_t s) {
   struct Lists { Model& m; cudaStream_t s; ~Lists() { reset_lists(m, s); } } lists{m, s};
   const int f = (int)m.layers.size();
   int o = 0;
@@ -1063,7 +1078,7 @@ cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* score
         bs = *hit;
       } else {
         PlanResult pr = plan_for(m, rem);
-        if (!pr.feasible) return fail(CDN_E_INFEASIBLE, "no batch plan fits TOT/latency");
+        if (!pr.feasible) throw Error(CDN_E_INFEASIBLE, "no batch plan fits TOT/latency");
         bs = pr.batches;
         m.plan_cache.emplace_back(rem, bs);
       }
@@ -1078,6 +1093,112 @@ cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* score
     const int rounds = rem / Bf;
     for (int r = 0; r < rounds; ++r) ex.round(o + r * Bf);
     o += rounds * Bf;
+  }
+  reset_lists(m, s);  // (inside a capture: joins the side stream back into s)
+}
+
+// Everything an infer call's work depends on besides its arguments: plans,
+// budget, kernel policy and choices, profile table, and every device buffer's
+// address (g_dbuf_gen).  Equal signatures => the same launches with the same
+// pointers.
+uint64_t state_sig(const Model& m) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+  mix(m.layers.size());
+  for (int b : m.fixed_plan) mix((uint64_t)b);
+  mix(m.tot);
+  uint64_t lat;
+  std::memcpy(&lat, &m.latency, sizeof(lat));
+  mix(lat);
+  mix((uint64_t)m.tc_min);
+  mix((uint64_t)m.band_min);
+  mix((uint64_t)m.prof_bmax);
+  mix(m.plan_cache.size());
+  for (auto& L : m.layers) mix(L->kchoice.size());
+  mix(g_dbuf_gen.load());
+  return h;
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CDN_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+}  // namespace
+
+cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* scores, int on_device, void* stream) {
+  API_BEGIN
+  if (!h || !input || K < 1 || (!scores && h->m.rank == 0)) return fail(CDN_E_ARG, "bad arguments");
+  Model& m = h->m;
+  if (m.layers.empty()) return fail(CDN_E_STATE, "no layers loaded");
+  if (m.busy) return fail(CDN_E_STATE, "concurrent call on one handle");
+  if (m.world > 1 && !m.comm) return fail(CDN_E_STATE, "shard-only handle (no NCCL id): use cdn_layer_forward");
+  m.busy = true;
+  struct Clear { bool& b; ~Clear() { b = false; } } clr{m.busy};
+  CUDA_OK(cudaSetDevice(m.device));
+  cudaStream_t s = pick(m, stream);
+  // Repeated identical calls (device buffers, K, unchanged state) replay a CUDA
+  // graph of the call: the first runs eagerly, the second is captured, the
+  // rest launch the graph -- one launch instead of a dozen kernels, events and
+  // stream joins.  Not with host buffers, several ranks or the kernel timer on.
+  const bool graphable = graphs_enabled() && on_device && m.world == 1 && !ktimer_active();
+  Model::GraphEntry* ge = nullptr;
+  if (graphable)
+    for (auto& e : m.graphs)
+      if (e.in == input && e.out == scores && e.K == K) ge = &e;
+  const uint64_t sig0 = graphable ? state_sig(m) : 0;
+  if (ge && ge->sig == sig0 && ge->exec) {
+    CUDA_OK(cudaGraphLaunch(ge->exec, s));
+    g_launches.fetch_add(ge->launches);
+  } else if (ge && ge->sig == sig0) {
+    const unsigned long long l0 = g_launches.load();
+    CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    try {
+      infer_body(m, input, K, scores, on_device, s);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g = nullptr;
+    CUDA_OK(cudaStreamEndCapture(s, &g));
+    const unsigned long long nl = g_launches.load() - l0;
+    g_launches.fetch_sub(nl);  // nothing ran yet
+    cudaGraphExec_t ex = nullptr;
+    const bool same = state_sig(m) == sig0;
+    if (same && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+      cudaGraphDestroy(g);
+      ge->exec = ex;
+      ge->launches = nl;
+      CUDA_OK(cudaGraphLaunch(ex, s));
+      g_launches.fetch_add(nl);
+    } else {  // the call changed state while captured: run it for real
+      cudaGraphDestroy(g);
+      infer_body(m, input, K, scores, on_device, s);
+      ge->sig = state_sig(m);
+    }
+  } else {
+    infer_body(m, input, K, scores, on_device, s);
+    if (graphable) {
+      if (!ge) {
+        if (m.graphs.size() >= 8) {
+          if (m.graphs.front().exec) cudaGraphExecDestroy(m.graphs.front().exec);
+          m.graphs.erase(m.graphs.begin());
+        }
+        m.graphs.push_back({});
+        ge = &m.graphs.back();
+        ge->in = input;
+        ge->out = scores;
+        ge->K = K;
+      }
+      if (ge->exec) cudaGraphExecDestroy(ge->exec);
+      ge->exec = nullptr;
+      ge->sig = state_sig(m);  // captured next time if nothing changes
+    }
   }
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
   CUDA_OK(cudaGetLastError());

@@ -86,6 +86,12 @@ void ktimer_enable(bool on) {
   t.on = on;
 }
 
+bool ktimer_active() {
+  KTimer& t = kt();
+  std::lock_guard<std::mutex> g(t.mu);
+  return t.on;
+}
+
 cudaError_t ktimer_read(const char* kernel, double* total_ms, int* launches) {
   KTimer& t = kt();
   std::lock_guard<std::mutex> g(t.mu);

@@ -22,6 +22,7 @@ inline cudaError_t launched(int n = 1) {
 void ktimer_begin(const char* kernel, cudaStream_t s);
 void ktimer_end(const char* kernel, cudaStream_t s);
 void ktimer_enable(bool on);  // (re)starts with no records
+bool ktimer_active();
 cudaError_t ktimer_read(const char* kernel, double* total_ms, int* launches);
 
 constexpr int kLutMaxBits = 10;   // plain LUT width cap (decode kernel); longer codes take the canonical slow path

@@ -382,6 +382,49 @@ def test_tc_infer_stack_image_major_and_phases(torch_dev):
     m.close()
 
 
+def test_repeated_infer_graph_replay(torch_dev):
+    """Identical infer calls on device buffers: the first runs eagerly, the
+    second is captured into a CUDA graph, later ones replay it; every call's
+    output is the same bits and counts the same kernel launches, and changing
+    the input buffer or the plan leaves the graph."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    cfg = synth.CONFIGS["C3"]
+    m = cdn.Model(0)
+    for i, spec in enumerate(cfg.fc):
+        _, c, buf = config_layer("C3", i)
+        m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+    m.set_kernel_policy(1, 128)
+    K = 256
+    a = synth.fc_inputs(cfg.fc[0].cols, K, 0)
+    xi = torch.from_numpy(a).to(dev)
+    so = torch.zeros((K, cfg.fc[-1].rows), dtype=torch.float32, device=dev)
+    outs, counts = [], []
+    for it in range(5):
+        if it == 3:
+            xi.mul_(1.0)                     # same buffer, same values: the graph reads the live input
+        n0 = cdn.kernel_launches()
+        m.infer(xi, K, so, on_device=True)
+        torch.cuda.synchronize()
+        counts.append(cdn.kernel_launches() - n0)
+        outs.append(so.cpu().numpy().copy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    assert len(set(counts)) == 1 and counts[0] > 0
+    # a new input buffer with other values: no stale graph
+    a2 = synth.fc_inputs(cfg.fc[0].cols, K, 1)
+    xi2 = torch.from_numpy(a2).to(dev)
+    for _ in range(3):
+        m.infer(xi2, K, so, on_device=True)
+    torch.cuda.synchronize()
+    x = a2
+    for i, spec in enumerate(cfg.fc):
+        _, c, _ = config_layer("C3", i)
+        x = infer.fc_forward(sparse_q(c), x, synth.fc_weights(spec, 0)[1], apply_relu=spec.relu).astype(np.float32)
+    assert rel_err(so.cpu().numpy(), x) <= TOL
+    m.close()
+
+
 def test_tc_fold_list_decoder_subprocess():
     """The pad-folding list decoder (layers outside the multi-symbol LUT
     limits; forced here with CDN_TC_LIST=fold) through the same parity check."""
