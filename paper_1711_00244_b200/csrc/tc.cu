@@ -549,26 +549,31 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
 // Split tiles (covered by several CTAs' ranges): y[row][b] = act(sum_i
 // ws[tile][i][row][b] + bias), i in CTA order (deterministic); one thread per 4
 // images of a row, coalesced, over every tile at once (whole tiles skip).
-__global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, long W, int G, int nkt, int mpt,
-                                                   int nbt, int nrows, int B, const float* __restrict__ bias, int relu,
-                                                   float* __restrict__ y, int ldy, int vec_ok, long total) {
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int c4 = (int)(i % (kTN / 4));
-  const long tr = i / (kTN / 4);  // tile * 128 + row in tile
-  const int r = (int)(tr % kTM);
-  const long tile = tr / kTM;
-  const long t0 = tile * nkt;
-  const int count = sk_cta(t0 + nkt - 1, W, G) - sk_cta(t0, W, G) + 1;
+__global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, uint32_t W, int G, int nkt,
+                                                   int mpt, int nbt, int nrows, int B, const float* __restrict__ bias,
+                                                   int relu, float* __restrict__ y, int ldy, int vec_ok) {
+  // block = 4 rows x 64 float4 columns of one tile (tile / row uniform per warp)
+  const uint32_t tile = blockIdx.x / (kTM / 4);
+  const int r = (int)(blockIdx.x % (kTM / 4)) * 4 + (threadIdx.x >> 6);
+  const int c4 = threadIdx.x & 63;
+  const uint32_t t0 = tile * (uint32_t)nkt;  // 32-bit: W = tiles * nkt < 2^32 / G (host-checked)
+  const int count = (int)(((t0 + nkt) * (uint32_t)G - 1) / W) - (int)(((t0 + 1) * (uint32_t)G - 1) / W) + 1;
   if (count == 1) return;
-  const int rt = (int)(tile / nbt), bt = (int)(tile % nbt);
+  const int rt = (int)(tile / (uint32_t)nbt), bt = (int)(tile % (uint32_t)nbt);
   const int row = rt * kTM + r, b = bt * kTN + 4 * c4;
   if (row >= nrows || b >= B) return;
   const float* p = ws + ((size_t)tile * mpt * kTM + r) * kTN + 4 * c4;
-  float4 acc = __ldcg(reinterpret_cast<const float4*>(p));
-  for (int j = 1; j < count; ++j) {
-    const float4 q = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * kTN));
-    acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+  float4 q[8];  // the partials' loads all in flight before the (ordered) sum
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < count) q[j] = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * kTN));
+  float4 acc = q[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j)
+    if (j < count) { acc.x += q[j].x; acc.y += q[j].y; acc.z += q[j].z; acc.w += q[j].w; }
+  for (int j = 8; j < count; ++j) {  // rare: more than 8 CTAs on one tile
+    const float4 e = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * kTN));
+    acc.x += e.x; acc.y += e.y; acc.z += e.z; acc.w += e.w;
   }
   const float bs = bias[row];
   float o[4] = {acc.x + bs, acc.y + bs, acc.z + bs, acc.w + bs};
@@ -909,7 +914,8 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   p.ws_floats = (size_t)p.tiles * p.mpt * kTM * kTN;
   p.xsplit_elems = (size_t)B * p.ldk;
   p.smem = tc_smem_bytes(L);
-  p.ok = p.smem <= 227 * 1024;
+  // 32-bit stream-K arithmetic in k_tc_reduce
+  p.ok = p.smem <= 227 * 1024 && (uint64_t)(p.W + p.nkt) * (uint64_t)p.grid < (1ull << 32);
   return p;
 }
 
@@ -986,10 +992,9 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   e = launched();
   ktimer_end("k_fc_tc", s);
   if (e == cudaSuccess && p.grid != p.tiles) {  // some tile is split over CTAs
-    const long total = (long)p.tiles * kTM * (kTN / 4);
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
-    k_tc_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(ws, p.W, p.grid, p.nkt, p.mpt, p.nbt, L.wrows, B,
-                                                                   L.bias, relu, y, ldy, vec_ok, total);
+    k_tc_reduce<<<(unsigned)(p.tiles * (kTM / 4)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt,
+                                                                 L.wrows, B, L.bias, relu, y, ldy, vec_ok);
     e = launched();
   }
   if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
