@@ -34,7 +34,7 @@ CFG = "C5"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--batch", type=int, default=512)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -531,7 +531,8 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
 cudaStream_t pick(Model& m, void* s) { return s ? (cudaStream_t)s : m.stream; }
 
 // Explicit tensor-core threshold (env CDN_TC_MIN_B); without it and without a
-// kernel policy, B >= 128 is autotuned between the tensor-core and band kernels
+// kernel policy, every B the band kernel would take (B >= band_min_batch(), 16)
+// is autotuned between the tensor-core and band kernels
 // at the first call with each B (fc_forward).
 int tc_min_batch() {
   static int v = [] {
@@ -554,7 +555,7 @@ int band_min_batch() {
 void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s,
                 bool x_im = false) {
   const int relu = L.desc.relu;
-  // Default policy for B >= 128: both large-batch kernels are timed once at the
+  // Default policy for B >= band_min_batch(): both large-batch kernels are timed once at the
   // first call with this B and the faster is kept for the layer (autotune).
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
   if (L.blocked) {
@@ -562,7 +563,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
     // of the tensor-core path only
     if (!tc_supported(L.dev)) throw Error(CDN_E_UNSUPPORTED, "blocked layer outside the tensor-core path's limits");
     tcmin = 1;
-  } else if (m.tc_min == 0 && m.band_min == 0 && B >= 128 && tc_supported(L.dev) && ldx % 4 == 0) {
+  } else if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev) && ldx % 4 == 0) {
     int choice = -1;
     for (auto& e : L.kchoice)
       if (e.first == B) choice = e.second;
@@ -640,7 +641,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
 bool uses_tc(const Model& m, const Layer& L, int B) {
   if (L.is_conv() || !tc_supported(L.dev)) return false;
   if (L.blocked) return true;
-  if (m.tc_min == 0 && m.band_min == 0 && B >= 128) {
+  if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch()) {
     for (auto& e : L.kchoice)
       if (e.first == B) return e.second == 1;
     return false;
@@ -1331,7 +1332,7 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
   if (L.is_conv()) return "k_gemm_bf16 (conv)";
   if (L.blocked) return "k_fc_tc";
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
-  if (m.tc_min == 0 && m.band_min == 0 && B >= 128 && tc_supported(L.dev)) {
+  if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev)) {
     for (auto& e : L.kchoice)
       if (e.first == B) tcmin = e.second ? B : (1 << 30);
   }

@@ -118,9 +118,9 @@ def check_forward(torch, dev, m, c, bias, a, relu):
     scale = infer.fc_abs_scale(c.dense_q(), a, bias)
     kmax = max(1, int(c.row_tokens.max()))
     elem = (np.abs(y - ref) / np.maximum(scale, 1e-30)).max()
-    # fp32 summation bound gamma_n; at B >= 128 the default policy may pick the
+    # fp32 summation bound gamma_n; at B >= 16 the default policy may pick the
     # split-bf16 tensor-core kernel (products within 2^-15)
-    split = 2.0 ** -15 if a.shape[0] >= 128 else 0.0
+    split = 2.0 ** -15 if a.shape[0] >= 16 else 0.0
     assert elem <= 2 * kmax * 2.0 ** -24 + split + 1e-12, elem
     return e
 
