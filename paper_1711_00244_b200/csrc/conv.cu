@@ -285,6 +285,56 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
   return launched();
 }
 
+// im2col for small channel groups (conv1: 3 channels, K = 11*11*3): a warp per
+// output position, lanes along K, so a warp reads the window's contiguous
+// (s, c) runs and writes 64 contiguous bytes per step; the (r, s, c) of every k
+// is tabled in shared memory once per block (no per-element division).
+constexpr int kIm2colMaxK = 4096;
+__global__ void __launch_bounds__(256) k_im2col_warp(const float* __restrict__ x, int B, int H, int W, int C, int kh,
+                                                     int kw, int stride, int pad, int c0, int cg, int Ho, int Wo,
+                                                     int Kreal, int Kpad, __nv_bfloat16* __restrict__ out) {
+  __shared__ int s_off[kIm2colMaxK];             // (r * W + s) * C + c, -1 past Kreal
+  __shared__ unsigned char s_r[kIm2colMaxK], s_s[kIm2colMaxK];
+  for (int k = threadIdx.x; k < Kpad; k += blockDim.x) {
+    if (k < Kreal) {
+      const int c = k % cg, rs = k / cg, sx = rs % kw, r = rs / kw;
+      s_off[k] = (r * W + sx) * C + c;
+      s_r[k] = (unsigned char)r;
+      s_s[k] = (unsigned char)sx;
+    } else {
+      s_off[k] = -1;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int npos = B * Ho * Wo;
+  for (int pos = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pos < npos; pos += warps) {
+    const int b = pos / (Ho * Wo), rem = pos - b * (Ho * Wo);
+    const int oh = rem / Wo, ow = rem - oh * Wo;
+    const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
+    const bool inside = ih0 >= 0 && iw0 >= 0 && ih0 + kh <= H && iw0 + kw <= W;  // no padding taps
+    const float* xw = x + (((size_t)b * H + ih0) * W + iw0) * C + c0;            // window origin (maybe outside)
+    // lane: 2 consecutive k per step (one 4-byte store; 128 contiguous bytes per warp)
+    uint32_t* o = reinterpret_cast<uint32_t*>(out + (size_t)pos * Kpad);
+    auto tap = [&](int k) -> float {
+      const int off = s_off[k];
+      if (off < 0) return 0.f;
+      if (!inside) {
+        const int ih = ih0 + s_r[k], iw = iw0 + s_s[k];
+        if (ih < 0 || ih >= H || iw < 0 || iw >= W) return 0.f;
+      }
+      return __ldg(xw + off);
+    };
+#pragma unroll 2
+    for (int k = 2 * lane; k < Kpad; k += 64) {
+      const float f0 = tap(k), f1 = tap(k + 1);
+      const __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
+      o[k >> 1] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+  }
+}
+
 cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, int kw, int stride, int pad, int c0,
                           int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
                           int num_sms) {
@@ -293,6 +343,9 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
   if (vec8)
     k_im2col<true><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
                                                                 Kreal, Kpad, out);
+  else if (Kpad <= kIm2colMaxK && (long)B * Ho * Wo < (1L << 31) && (long)B * H * W * C < (1L << 40))
+    k_im2col_warp<<<grid_for((long)B * Ho * Wo * 32, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad,
+                                                                                c0, cg, Ho, Wo, Kreal, Kpad, out);
   else
     k_im2col<false><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
                                                                  Kreal, Kpad, out);
