@@ -707,14 +707,17 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
     m.conv_o.alloc((size_t)npos * M * sizeof(float));
     cout = m.conv_o.as<float>();
   }
+  // LRN fused into the GEMM epilogue when one tile holds every channel (one
+  // group, <= 256 filters: conv1); otherwise a separate pass
+  const bool fuse_lrn = d.lrn && G == 1 && gemm_tile_n(M) >= M;
   for (int g = 0; g < G; ++g) {
     CUDA_OK(launch_im2col(x, B, d.in_h, d.in_w, d.in_c, d.kh, d.kw, d.stride, d.pad, g * cg, cg, Ho, Wo,
                           (int)L.cols, L.kpad, static_cast<__nv_bfloat16*>(m.conv_a.p), s, m.num_sms));
     CUDA_OK(launch_gemm_bf16(static_cast<__nv_bfloat16*>(m.conv_a.p), (int)npos, wd + (size_t)g * mg * L.kpad, mg,
-                             L.kpad, L.bias.as<float>() + g * mg, d.relu, cout, M, g * mg, s));
+                             L.kpad, L.bias.as<float>() + g * mg, d.relu, cout, M, g * mg, s, fuse_lrn ? 1 : 0));
   }
   const float* cur = cout;
-  if (d.lrn) {
+  if (d.lrn && !fuse_lrn) {
     float* dst = d.pool_k > 0 ? (m.conv_t.alloc((size_t)npos * M * sizeof(float)), m.conv_t.as<float>()) : y;
     CUDA_OK(launch_lrn(cur, npos, M, dst, s, m.num_sms));
     cur = dst;

@@ -39,7 +39,7 @@ constexpr int kGThreads = 128;
 __global__ void __launch_bounds__(kGThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int Mrows, int Nrows,
                 int nk, int BN, int tmem_cols, int kGStages, const float* __restrict__ bias,
-                float* __restrict__ out, int ldo, int col0, int relu) {
+                float* __restrict__ out, int ldo, int col0, int relu, int lrn) {
   extern __shared__ unsigned char smem_raw[];
   // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space,
   // so LUT/zero-fill accesses compile to LDS/STS instead of generic LD/ST)
@@ -105,6 +105,68 @@ __global__ void __launch_bounds__(kGThreads, 1)
   mbar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int row = m0 + warp * 32 + lane;
+  if (lrn) {
+    // LRN fused (the CTA holds all Nrows channels of its positions; one lane =
+    // one position): y_c = a_c * (2 + 1e-4/5 * sum_{q=c-2..c+2} a_q^2)^-0.75,
+    // a = act(conv + bias), summed in the order k_lrn uses (bit-identical).
+    // Chunks of 16 channels slide with the 2 before and the 16 after.
+    auto act = [&](float (&v)[16], int c) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = c + i;
+        float o = n < Nrows ? v[i] + __ldg(bias + n) : 0.f;  // (uniform over the warp: broadcast loads)
+        if (relu) o = fmaxf(o, 0.f);
+        v[i] = o;
+      }
+    };
+    float cur[16], nxt[16], p1 = 0.f, p2 = 0.f;  // p2 = a[c-2], p1 = a[c-1]
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), cur);
+    act(cur, 0);
+    for (int c = 0; c < Nrows; c += 16) {
+      if (c + 16 < Nrows) {
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c + 16), nxt);
+        act(nxt, c + 16);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) nxt[i] = 0.f;
+      }
+      float o[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int ch = c + i;
+        // window a[ch-2 .. ch+2] clipped to [0, Nrows)
+        float w[5];
+        w[0] = i >= 2 ? cur[i - 2] : (i == 1 ? p1 : p2);
+        w[1] = i >= 1 ? cur[i - 1] : p1;
+        w[2] = cur[i];
+        w[3] = i + 1 < 16 ? cur[i + 1] : nxt[i - 15];
+        w[4] = i + 2 < 16 ? cur[i + 2] : nxt[i - 14];
+        float sq = 0.f;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const int cq = ch - 2 + q;
+          if (cq >= 0 && cq < Nrows) sq = fmaf(w[q], w[q], sq);
+        }
+        o[i] = cur[i] * exp2f(-0.75f * __log2f(2.0f + (1e-4f / 5.0f) * sq));
+      }
+      if (row < Mrows) {
+        float* op = out + (size_t)row * ldo + col0 + c;
+        if (c + 16 <= Nrows && ((((uintptr_t)op) & 15) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            reinterpret_cast<float4*>(op)[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c + i < Nrows) op[i] = o[i];
+        }
+      }
+      p2 = cur[14];
+      p1 = cur[15];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+    }
+  } else
   for (int c = 0; c < BN; c += 16) {
     float v[16];
     tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
@@ -259,10 +321,11 @@ size_t gemm_smem_bytes(int BN) {
 }
 
 cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
-                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s) {
+                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s, int lrn) {
   if (Mrows <= 0 || Nrows <= 0) return cudaSuccess;
   if (Kpad % kBK) return cudaErrorInvalidValue;
   const int BN = gemm_tile_n(Nrows);
+  if (lrn && BN < Nrows) return cudaErrorInvalidValue;  // the fused LRN needs every channel in one tile
   int tcols = 32;
   while (tcols < BN) tcols <<= 1;
   CUtensorMap ta, tb;
@@ -281,7 +344,7 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
   }
   dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN);
   k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
-                                            ldo, col0, relu);
+                                            ldo, col0, relu, lrn);
   return launched();
 }
 

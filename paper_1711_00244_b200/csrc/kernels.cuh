@@ -145,8 +145,10 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
                           int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
                           int num_sms);
 // tcgen05 GEMM: out[pos*ldo + col0 + n] = act(sum_k A[pos][k] Wt[n][k] + bias[n]); Kpad % 64 == 0.
+int gemm_tile_n(int Nrows);  // N tile of the conv GEMM (<= 256)
 cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
-                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s);
+                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s,
+                             int lrn = 0);
 cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms);
 cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
                            int num_sms);

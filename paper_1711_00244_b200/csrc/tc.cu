@@ -447,17 +447,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const int row = t.rt * kTM + row_l;
       const int b0 = t.bt * kTN;
       const bool has = t.kt1 > t.kt0;
-      float* dst;
-      size_t ld;
       const bool whole = t.count == 1;  // this CTA owns the tile's whole K range
-      if (whole) {
-        dst = a.y + (size_t)row * a.ldy + b0;
-        ld = a.ldy;
-      } else {
-        dst = a.ws + (((size_t)t.tile * a.mpt + t.slot) * kTM + row_l) * kTN;
-        ld = kTN;
-      }
-      (void)ld;
+      float* const dst = whole ? a.y + (size_t)row * a.ldy + b0
+                               : a.ws + (((size_t)t.tile * a.mpt + t.slot) * kTM + row_l) * kTN;
       const float bias = (whole && row < L.wrows) ? L.bias[row] : 0.f;
       // y rows are contiguous over the batch: whole float4s where the tile is inside B
       const bool vec_ok = (a.ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
@@ -662,9 +654,9 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
   const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
   // output slot of this row's first entry in each of the chunk's tiles
   uint32_t p[kTcChunk], n = 0;
-#pragma unroll
   ListMap<BLOCKED> lm;
   lm.init(L, row, kt0);
+#pragma unroll
   for (int k = 0; k < kTcChunk; ++k) {
     p[k] = 0;
     if (k < nk) {
@@ -780,9 +772,9 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   // this thread's first list slot in each tile of the chunk, in shared memory
   // ([k][thread]: conflict-free) so the emission below picks it without branches
   uint32_t left = 0;
-#pragma unroll
   ListMap<BLOCKED> lm;
   lm.init(L, row, kt0);
+#pragma unroll
   for (int k = 0; k < kTcChunk; ++k) {
     uint32_t pk = 0;
     if (k < nk) {
