@@ -665,10 +665,23 @@ void reset_lists(Model& m, cudaStream_t s) {
 // the side stream right away, in layer order -- they depend on the compressed
 // weights only, so they overlap the earlier layers' work (and the activation
 // split) instead of sitting in front of each layer's contraction.
+// The per-call decode a layer can do before its input exists: the tensor-core
+// list of an FC layer, the dense bf16 filters of a CONV layer.
+bool predecodes(const Model& m, const Layer& L, int B) { return L.is_conv() || uses_tc(m, L, B); }
+
+void predecode_launch(Model& m, Layer& L, cudaStream_t s) {
+  if (L.is_conv()) {
+    CUDA_OK(cudaMemsetAsync(L.wd.p, 0, L.wd.n, s));
+    CUDA_OK(launch_decode_dense(L.dev, static_cast<__nv_bfloat16*>(L.wd.p), L.kpad, s, m.num_sms));
+  } else {
+    CUDA_OK(launch_tc_list(L.dev, s));
+  }
+}
+
 void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
   bool any = false;
   for (size_t i = 0; i < m.layers.size(); ++i)
-    any |= m.layers[i]->list_state == 0 && uses_tc(m, *m.layers[i], bs[i]);
+    any |= m.layers[i]->list_state == 0 && predecodes(m, *m.layers[i], bs[i]);
   if (!any) return;
   if (!m.side) {
     int least = 0, greatest = 0;
@@ -680,9 +693,9 @@ void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
   CUDA_OK(cudaStreamWaitEvent(m.side, m.ev_call, 0));
   for (size_t i = 0; i < m.layers.size(); ++i) {
     Layer& L = *m.layers[i];
-    if (L.list_state != 0 || !uses_tc(m, L, bs[i])) continue;
+    if (L.list_state != 0 || !predecodes(m, L, bs[i])) continue;
     if (!L.list_ev) CUDA_OK(cudaEventCreateWithFlags(&L.list_ev, cudaEventDisableTiming));
-    CUDA_OK(launch_tc_list(L.dev, m.side));
+    predecode_launch(m, L, m.side);
     CUDA_OK(cudaEventRecord(L.list_ev, m.side));
     L.list_state = 1;
   }
@@ -698,8 +711,12 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
   const int Ho = L.conv_h, Wo = L.conv_w;
   const long npos = (long)B * Ho * Wo;
   __nv_bfloat16* wd = static_cast<__nv_bfloat16*>(L.wd.p);
-  CUDA_OK(cudaMemsetAsync(L.wd.p, 0, L.wd.n, s));
-  CUDA_OK(launch_decode_dense(L.dev, wd, L.kpad, s, m.num_sms));
+  if (L.list_state == 1) {  // decoded ahead on the side stream (prelaunch_lists)
+    CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
+  } else if (L.list_state == 0) {
+    predecode_launch(m, L, s);
+  }
+  L.list_state = 2;  // later phases of the call reuse the decoded filters
   m.conv_a.alloc((size_t)npos * L.kpad * 2);
   const bool post = d.lrn || d.pool_k > 0;
   float* cout = y;
@@ -1234,6 +1251,8 @@ cdn_status cdn_conv_forward(cdn_model* h, int layer, const float* x, int B, floa
   if (!L.is_conv()) return fail(CDN_E_ARG, "layer is not a CONV layer");
   CUDA_OK(cudaSetDevice(m.device));
   cudaStream_t s = pick(m, stream);
+  struct Lists { Model& m; cudaStream_t s; ~Lists() { reset_lists(m, s); } } lists{m, s};
+  reset_lists(m, s);  // a single-layer call decodes its own filters
   conv_forward(m, L, x, B, y, s);
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
   API_END
