@@ -293,6 +293,56 @@ __global__ void k_maxpool(const float* __restrict__ x, int B, int H, int W, int 
   }
 }
 
+// 4 channels per thread (C % 4 == 0, 16-byte aligned), 32-bit indexing: the
+// common AlexNet case of the two kernels above.
+__global__ void k_maxpool4(const float4* __restrict__ x, int B, int H, int W, int C4, int k, int s, int Ho, int Wo,
+                           float4* __restrict__ y) {
+  const int total = B * Ho * Wo * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c = i % C4;
+    int p = i / C4;
+    const int ow = p % Wo;
+    p /= Wo;
+    const int oh = p % Ho, b = p / Ho;
+    float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    const float4* xb = x + ((size_t)(b * H + oh * s) * W + ow * s) * C4 + c;
+    for (int r = 0; r < k; ++r)
+      for (int q = 0; q < k; ++q) {
+        const float4 v = __ldg(xb + ((size_t)r * W + q) * C4);
+        m.x = fmaxf(m.x, v.x); m.y = fmaxf(m.y, v.y); m.z = fmaxf(m.z, v.z); m.w = fmaxf(m.w, v.w);
+      }
+    y[i] = m;
+  }
+}
+
+__global__ void k_lrn4(const float* __restrict__ x, int npos, int C, float* __restrict__ y) {
+  const int C4 = C >> 2, total = npos * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c0 = (i % C4) * 4;
+    const float* px = x + (size_t)(i / C4) * C;
+    float a[8];  // channels c0-2 .. c0+5 (0 outside, never summed)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 - 2 + j;
+      a[j] = (c >= 0 && c < C) ? __ldg(px + c) : 0.f;
+    }
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + j;
+      float sq = 0.f;
+      // the same order as k_lrn: q from max(0, c-2) to min(C-1, c+2)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int cq = c - 2 + q;
+        if (cq >= 0 && cq < C) sq = fmaf(a[j + q], a[j + q], sq);
+      }
+      o[j] = a[j + 2] * exp2f(-0.75f * __log2f(2.0f + (1e-4f / 5.0f) * sq));
+    }
+    *reinterpret_cast<float4*>(y + (size_t)(i / C4) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 int grid_for(long work, int threads, int num_sms) {
   const long g = (work + threads - 1) / threads;
   const long cap = (long)num_sms * 16;
@@ -416,14 +466,21 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
 }
 
 cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms) {
-  k_lrn<<<grid_for(npos * C, 256, num_sms), 256, 0, s>>>(x, npos, C, y);
+  if (C % 4 == 0 && npos * C < (1L << 31) && (((uintptr_t)x | (uintptr_t)y) & 15) == 0)
+    k_lrn4<<<grid_for(npos * C / 4, 256, num_sms), 256, 0, s>>>(x, (int)npos, C, y);
+  else
+    k_lrn<<<grid_for(npos * C, 256, num_sms), 256, 0, s>>>(x, npos, C, y);
   return launched();
 }
 
 cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
                            int num_sms) {
   const int Ho = (H - k) / st + 1, Wo = (W - k) / st + 1;
-  k_maxpool<<<grid_for((long)B * Ho * Wo * C, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y);
+  if (C % 4 == 0 && (long)B * H * W * C < (1L << 31) && (((uintptr_t)x | (uintptr_t)y) & 15) == 0)
+    k_maxpool4<<<grid_for((long)B * Ho * Wo * C / 4, 256, num_sms), 256, 0, s>>>(
+        reinterpret_cast<const float4*>(x), B, H, W, C / 4, k, st, Ho, Wo, reinterpret_cast<float4*>(y));
+  else
+    k_maxpool<<<grid_for((long)B * Ho * Wo * C, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y);
   return launched();
 }
 
