@@ -208,13 +208,15 @@ template <bool VEC8>
 __global__ void k_im2col(const float* __restrict__ x, int B, int H, int W, int C, int kh, int kw, int stride, int pad,
                          int c0, int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* __restrict__ out) {
   const int kq = Kpad / 8;
-  const long total = (long)B * Ho * Wo * kq;
-  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
-    const long pos = idx / kq;
-    const int k0 = (int)(idx % kq) * 8;
-    const int b = (int)(pos / (Ho * Wo));
-    const int rem = (int)(pos % (Ho * Wo));
-    const int oh = rem / Wo, ow = rem % Wo;
+  // 32-bit indexing (the launcher checks B * Ho * Wo * Kpad / 8 < 2^31): 64-bit
+  // division here cost more than the copy itself
+  const uint32_t total = (uint32_t)B * Ho * Wo * kq;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const uint32_t pos = idx / kq;
+    const int k0 = (int)(idx - pos * kq) * 8;
+    const int b = (int)(pos / (uint32_t)(Ho * Wo));
+    const int rem = (int)(pos - (uint32_t)b * (Ho * Wo));
+    const int oh = rem / Wo, ow = rem - oh * Wo;
     __align__(16) __nv_bfloat16 v[8];
     if (VEC8) {
       // cg % 8 == 0: the 8 k's are 8 consecutive channels of one (r, s) tap
@@ -255,7 +257,7 @@ __global__ void k_im2col(const float* __restrict__ x, int B, int H, int W, int C
         }
       }
     }
-    *reinterpret_cast<uint4*>(out + pos * Kpad + k0) = *reinterpret_cast<const uint4*>(v);
+    *reinterpret_cast<uint4*>(out + (size_t)pos * Kpad + k0) = *reinterpret_cast<const uint4*>(v);
   }
 }
 
@@ -452,6 +454,7 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
                           int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
                           int num_sms) {
   const long work = (long)B * Ho * Wo * (Kpad / 8);
+  if (work >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing in the kernels
   const bool vec8 = (cg % 8 == 0) && (C % 4 == 0) && (c0 % 4 == 0) && (((uintptr_t)x & 15) == 0);
   if (vec8)
     k_im2col<true><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
