@@ -100,6 +100,7 @@ cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, in
 struct TcPlan {
   bool ok = false;
   int nbt = 1, nrt = 1, nkt = 0, ldk = 0, tiles = 0, grid = 0, mpt = 1;  // mpt: max CTAs per tile
+  int tn = 256;  // images per tile (UMMA N): 128 when the batch fits one
   long W = 0;  // tile steps (stream-K split over `grid` CTAs)
   size_t ws_floats = 0, xsplit_elems = 0, smem = 0;
 };

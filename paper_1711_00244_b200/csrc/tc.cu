@@ -53,13 +53,11 @@ namespace {
 using namespace dev;
 
 constexpr int kTM = 128;            // rows per unit (UMMA M)
-constexpr int kTN = 256;            // images per unit (UMMA N)
+constexpr int kTN = 256;            // images per unit (UMMA N); 128 for B <= 128 (TN template)
 constexpr int kTK = 64;             // K tile (= interval width of the TC index)
 constexpr int kXStages = 3;         // X ring depth
 constexpr int kEnt = 16;            // list entries per row tile carried in registers (the rest: loads)
 constexpr int kRowBytes = 128;      // expand lane's private row: 64 bf16 (chunk-swizzled)
-constexpr int kXTile = kTN * kTK * 2;   // 32 KB bf16
-constexpr int kXStageBytes = 2 * kXTile;  // hi + lo
 constexpr int kDecW = 4;            // expand warps per K stream: 4 lane quarters (x {bf16 hi, lo} if 8)
 constexpr int kHalvesPerWarp = 8 / kDecW;  // bf16 halves (hi, lo) each expand warp builds
 constexpr int kStreams = 2;         // K halves of a unit expanded concurrently
@@ -191,8 +189,11 @@ __device__ __forceinline__ void stream_range(const TUnit& t, int q, int& k0, int
   k1 = q == 0 ? mid : t.kt1;
 }
 
+template <int TN>
 __global__ void __launch_bounds__(kTThreads, 1)
     k_fc_tc(FcDev L, TcArgs a, const __grid_constant__ CUtensorMap txh, const __grid_constant__ CUtensorMap txl) {
+  constexpr int kXTile = TN * kTK * 2;      // bf16 X tile [TN images][64 K]
+  constexpr int kXStageBytes = 2 * kXTile;  // hi + lo
   extern __shared__ unsigned char smem_raw[];
   // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space)
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   for (int i = threadIdx.x; i < kStreams * (kDecW / 4) * kTM * kRowBytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(rows)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  const uint32_t tmem_w = tmem + kTN;  // W buffers: column kTN + (q * kWBufs + b) * kWCols
+  const uint32_t tmem_w = tmem + TN;  // W buffers: column TN + (q * kWBufs + b) * kWCols
 
   // The MMA consumes the two streams' tiles alternately q = 0, 1, 0, 1, ...
   // (the longer first half finishes alone); the X producer loads in that order.
@@ -266,8 +267,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
             mbar_wait(&xempty[s], ((xc / kXStages) & 1) ^ 1);
             unsigned char* st = xst + s * kXStageBytes;
             mbar_arrive_expect_tx(&xfull[s], 2 * kXTile);
-            tma2d(st, &txh, kt * kTK, t.bt * kTN, &xfull[s]);
-            tma2d(st + kXTile, &txl, kt * kTK, t.bt * kTN, &xfull[s]);
+            tma2d(st, &txh, kt * kTK, t.bt * TN, &xfull[s]);
+            tma2d(st + kXTile, &txl, kt * kTK, t.bt * TN, &xfull[s]);
             ++xc;
           }
       }
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   } else if (warp == 1) {
     // --------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) |
                              ((uint32_t)(kTM >> 4) << 24);
       uint32_t xc = 0, gq[kStreams] = {0, 0}, uc = 0;
       TUnit t;
@@ -445,15 +446,15 @@ __global__ void __launch_bounds__(kTThreads, 1)
       if (ew == 0 && lane == 0) tc_trace(a, 13, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = t.rt * kTM + row_l;
-      const int b0 = t.bt * kTN;
+      const int b0 = t.bt * TN;
       const bool has = t.kt1 > t.kt0;
       const bool whole = t.count == 1;  // this CTA owns the tile's whole K range
       float* const dst = whole ? a.y + (size_t)row * a.ldy + b0
-                               : a.ws + (((size_t)t.tile * a.mpt + t.slot) * kTM + row_l) * kTN;
+                               : a.ws + (((size_t)t.tile * a.mpt + t.slot) * kTM + row_l) * TN;
       const float bias = (whole && row < L.wrows) ? L.bias[row] : 0.f;
       // y rows are contiguous over the batch: whole float4s where the tile is inside B
       const bool vec_ok = (a.ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
-      for (int c = 0; c < kTN; c += 16) {
+      for (int c = 0; c < TN; c += 16) {
         float v[16];
         tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c, v);
         if (!has) {
@@ -541,30 +542,32 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
 // Split tiles (covered by several CTAs' ranges): y[row][b] = act(sum_i
 // ws[tile][i][row][b] + bias), i in CTA order (deterministic); one thread per 4
 // images of a row, coalesced, over every tile at once (whole tiles skip).
+template <int TN>
 __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, uint32_t W, int G, int nkt,
                                                    int mpt, int nbt, int nrows, int B, const float* __restrict__ bias,
                                                    int relu, float* __restrict__ y, int ldy, int vec_ok) {
-  // block = 4 rows x 64 float4 columns of one tile (tile / row uniform per warp)
-  const uint32_t tile = blockIdx.x / (kTM / 4);
-  const int r = (int)(blockIdx.x % (kTM / 4)) * 4 + (threadIdx.x >> 6);
-  const int c4 = threadIdx.x & 63;
+  // block = (1024 / TN) rows x TN/4 float4 columns of one tile
+  constexpr int kR = 1024 / TN, kC4 = TN / 4;
+  const uint32_t tile = blockIdx.x / (kTM / kR);
+  const int r = (int)(blockIdx.x % (kTM / kR)) * kR + (int)(threadIdx.x / kC4);
+  const int c4 = threadIdx.x % kC4;
   const uint32_t t0 = tile * (uint32_t)nkt;  // 32-bit: W = tiles * nkt < 2^32 / G (host-checked)
   const int count = (int)(((t0 + nkt) * (uint32_t)G - 1) / W) - (int)(((t0 + 1) * (uint32_t)G - 1) / W) + 1;
   if (count == 1) return;
   const int rt = (int)(tile / (uint32_t)nbt), bt = (int)(tile % (uint32_t)nbt);
-  const int row = rt * kTM + r, b = bt * kTN + 4 * c4;
+  const int row = rt * kTM + r, b = bt * TN + 4 * c4;
   if (row >= nrows || b >= B) return;
-  const float* p = ws + ((size_t)tile * mpt * kTM + r) * kTN + 4 * c4;
+  const float* p = ws + ((size_t)tile * mpt * kTM + r) * TN + 4 * c4;
   float4 q[8];  // the partials' loads all in flight before the (ordered) sum
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    if (j < count) q[j] = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * kTN));
+    if (j < count) q[j] = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * TN));
   float4 acc = q[0];
 #pragma unroll
   for (int j = 1; j < 8; ++j)
     if (j < count) { acc.x += q[j].x; acc.y += q[j].y; acc.z += q[j].z; acc.w += q[j].w; }
   for (int j = 8; j < count; ++j) {  // rare: more than 8 CTAs on one tile
-    const float4 e = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * kTN));
+    const float4 e = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * TN));
     acc.x += e.x; acc.y += e.y; acc.z += e.z; acc.w += e.w;
   }
   const float bs = bias[row];
@@ -611,8 +614,8 @@ __global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x,
   *reinterpret_cast<uint4*>(xl + (size_t)b * ldk + k) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-size_t tc_smem_bytes(const FcDev&) {
-  size_t b = 1024 + (size_t)kXStages * kXStageBytes + (size_t)kStreams * (kDecW / 4) * kTM * kRowBytes + 8 * (2 * kXStages + 2 * kStreams * kWBufs + 2) + 16 + 4 * 256;
+size_t tc_smem_bytes(const FcDev&, int tn) {
+  size_t b = 1024 + (size_t)kXStages * (2 * tn * kTK * 2) + (size_t)kStreams * (kDecW / 4) * kTM * kRowBytes + 8 * (2 * kXStages + 2 * kStreams * kWBufs + 2) + 16 + 4 * 256;
   return (b + 127) & ~(size_t)127;
 }
 
@@ -873,7 +876,9 @@ bool tc_supported(const FcDev& L) {
 TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   TcPlan p;
   if (!tc_supported(L) || B <= 0) return p;
-  p.nbt = (B + kTN - 1) / kTN;
+  // a 128-image tile when the batch fits one (half the tensor work of 256)
+  p.tn = B <= 128 ? 128 : kTN;
+  p.nbt = (B + p.tn - 1) / p.tn;
   p.nrt = (L.wrows + kTM - 1) / kTM;
   p.nkt = L.tNI;
   p.ldk = (L.wcols + 7) & ~7;
@@ -903,9 +908,9 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   const long per = p.W / G;  // >= 1
   p.mpt = (int)((p.nkt + per - 1) / per) + 1;
   if (p.mpt > (int)G) p.mpt = (int)G;
-  p.ws_floats = (size_t)p.tiles * p.mpt * kTM * kTN;
+  p.ws_floats = (size_t)p.tiles * p.mpt * kTM * p.tn;
   p.xsplit_elems = (size_t)B * p.ldk;
-  p.smem = tc_smem_bytes(L);
+  p.smem = tc_smem_bytes(L, p.tn);
   // 32-bit stream-K arithmetic in k_tc_reduce
   p.ok = p.smem <= 227 * 1024 && (uint64_t)(p.W + p.nkt) * (uint64_t)p.grid < (1ull << 32);
   return p;
@@ -960,16 +965,18 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   if (e != cudaSuccess) return e;
   CUtensorMap th, tl;
   e = encode_tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xh, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
-                     kTK, kTN, CU_TENSOR_MAP_SWIZZLE_128B);
+                     kTK, (uint32_t)p.tn, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
   e = encode_tmap_2d(&tl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xl, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
-                     kTK, kTN, CU_TENSOR_MAP_SWIZZLE_128B);
+                     kTK, (uint32_t)p.tn, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
-  static size_t set_smem = 0;
-  if (p.smem > set_smem) {
-    e = cudaFuncSetAttribute(k_fc_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    if (e != cudaSuccess) return e;
-    set_smem = p.smem;
+  static bool attr_set = false;
+  if (!attr_set) {  // the largest footprint (256-image tiles) covers both
+    for (auto kern : {k_fc_tc<128>, k_fc_tc<256>}) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes(L, kTN));
+      if (e != cudaSuccess) return e;
+    }
+    attr_set = true;
   }
   static unsigned long long* trace = nullptr;
   const char* trace_path = getenv("CDN_TC_TRACE");
@@ -980,13 +987,20 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
   TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr};
   ktimer_begin("k_fc_tc", s);
-  k_fc_tc<<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
+  if (p.tn == 128)
+    k_fc_tc<128><<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
+  else
+    k_fc_tc<256><<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
   e = launched();
   ktimer_end("k_fc_tc", s);
   if (e == cudaSuccess && p.grid != p.tiles) {  // some tile is split over CTAs
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
-    k_tc_reduce<<<(unsigned)(p.tiles * (kTM / 4)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt,
-                                                                 L.wrows, B, L.bias, relu, y, ldy, vec_ok);
+    if (p.tn == 128)
+      k_tc_reduce<128><<<(unsigned)(p.tiles * (kTM / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
+                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok);
+    else
+      k_tc_reduce<256><<<(unsigned)(p.tiles * (kTM / 4)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
+                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok);
     e = launched();
   }
   if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
