@@ -109,12 +109,24 @@ struct Layer {
   uint64_t in_elems() const { return is_conv() ? (uint64_t)desc.in_h * desc.in_w * desc.in_c : cols; }
 };
 
+constexpr int kH2DChunks = 8;   // pieces per round
+constexpr int kH2DStreams = 4;  // concurrent copies (one copy stream alone reaches ~half the link here)
+
 struct Model {
   int device = 0, rank = 0, world = 1, num_sms = 148;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;    // list decoding ahead of the layers (tensor-core path)
   cudaEvent_t ev_call = nullptr;  // start of the current call on its stream
+  // host-buffer input: each round's images go up in kH2DChunks pieces spread
+  // over kH2DStreams copy streams, into one of two staging buffers; a
+  // first-layer phase waits only for the pieces it reads, so later pieces
+  // (and the next round) land while earlier phases compute
+  cudaStream_t cp[kH2DStreams] = {};
+  cudaEvent_t h2d_ev[2][kH2DChunks] = {};
+  cudaEvent_t stage_free[2] = {};
+  DBuf stage[2];
+  int stage_par = 0;
   std::vector<std::unique_ptr<Layer>> layers;
   uint64_t tot = 0;
   double latency = 0.0;
@@ -125,7 +137,7 @@ struct Model {
   std::vector<std::pair<int, std::vector<int>>> plan_cache;  // (K, batches) under the current budget
   // executor scratch
   std::vector<DBuf> lvl;        // per-level input buffers [K_i][B_i]
-  DBuf out, stage_in, loc, gath, host_stage;
+  DBuf out, loc, gath, host_stage;
   DBuf conv_a, conv_o, conv_t;  // CONV scratch: bf16 patches, conv output, LRN output
   DBuf ctmp;                    // conv -> FC boundary: image-major conv output of one phase
   bool busy = false;
@@ -687,8 +699,8 @@ void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
     int least = 0, greatest = 0;
     CUDA_OK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     CUDA_OK(cudaStreamCreateWithPriority(&m.side, cudaStreamNonBlocking, least));
-    CUDA_OK(cudaEventCreateWithFlags(&m.ev_call, cudaEventDisableTiming));
   }
+  if (!m.ev_call) CUDA_OK(cudaEventCreateWithFlags(&m.ev_call, cudaEventDisableTiming));
   CUDA_OK(cudaEventRecord(m.ev_call, s));
   CUDA_OK(cudaStreamWaitEvent(m.side, m.ev_call, 0));
   for (size_t i = 0; i < m.layers.size(); ++i) {
@@ -783,10 +795,10 @@ struct Exec {
     if (i == 0) {
       const size_t per = L.in_elems();
       const float* src = input + (size_t)o * per;
-      if (!on_device) {
-        m.stage_in.alloc((size_t)Bi * per * sizeof(float));
-        CUDA_OK(cudaMemcpyAsync(m.stage_in.p, src, (size_t)Bi * per * sizeof(float), cudaMemcpyHostToDevice, s));
-        src = m.stage_in.as<float>();
+      if (!on_device) {  // the phase's images, prefetched by round()
+        for (int c = (o - st_o) / st_chunk; c <= (o - st_o + Bi - 1) / st_chunk; ++c)
+          CUDA_OK(cudaStreamWaitEvent(s, m.h2d_ev[st_par][c], 0));
+        src = m.stage[st_par].as<float>() + (size_t)(o - st_o) * per;
       }
       if (L.is_conv()) {
         xin = const_cast<float*>(src);  // NHWC image-major is the conv layout
@@ -818,14 +830,39 @@ struct Exec {
     else
       layer_step(m, i, xin, li, Bi, dst, ld, s);
   }
+  int st_o = 0, st_chunk = 1, st_par = 0;  // the round's staged host input
+  // Host input: issue the round's H2D copies, kH2DChunks pieces round-robin
+  // over the copy streams, each with an event the phases reading it wait
+  // for; the staging buffer alternates between rounds.
+  void prefetch(int o) {
+    const int Bf = bs.back();
+    const size_t per = m.layers[0]->in_elems();
+    st_chunk = (Bf + kH2DChunks - 1) / kH2DChunks;
+    st_o = o;
+    st_par = m.stage_par;
+    m.stage_par ^= 1;
+    DBuf& st = m.stage[st_par];
+    st.alloc((size_t)Bf * per * sizeof(float));
+    // the buffer's previous round (two rounds back) has finished reading it
+    for (cudaStream_t c : m.cp) CUDA_OK(cudaStreamWaitEvent(c, m.stage_free[st_par], 0));
+    for (int c = 0; c * st_chunk < Bf; ++c) {
+      const int n = std::min(st_chunk, Bf - c * st_chunk);
+      cudaStream_t cs = m.cp[c % kH2DStreams];
+      CUDA_OK(cudaMemcpyAsync(st.as<float>() + (size_t)c * st_chunk * per, input + (size_t)(o + c * st_chunk) * per,
+                              (size_t)n * per * sizeof(float), cudaMemcpyHostToDevice, cs));
+      CUDA_OK(cudaEventRecord(m.h2d_ev[st_par][c], cs));
+    }
+  }
   void round(int o) {
     const int f = (int)m.layers.size();
     const int Bf = bs[f - 1];
     if (m.layers[f - 1]->is_conv()) throw Error(CDN_E_UNSUPPORTED, "the last layer must be FC (class scores)");
+    if (!on_device) prefetch(o);
     const uint32_t classes = m.layers[f - 1]->rows;
     const int lf = ld4(Bf);
     m.out.alloc((size_t)classes * lf * sizeof(float));
     run(f - 1, o, m.out.as<float>(), lf);
+    if (!on_device) CUDA_OK(cudaEventRecord(m.stage_free[st_par], s));
     if (m.rank != 0) return;
     // [classes][lf] -> scores[o..o+Bf)[classes]
     float* dst = scores + (size_t)o * classes;
@@ -1020,6 +1057,16 @@ void cdn_model_destroy(cdn_model* h) {
     h->m.layers.clear();
     if (h->m.side) cudaStreamDestroy(h->m.side);
     if (h->m.ev_call) cudaEventDestroy(h->m.ev_call);
+    for (cudaStream_t c : h->m.cp)
+      if (c) {
+        cudaStreamSynchronize(c);
+        cudaStreamDestroy(c);
+      }
+    for (int p = 0; p < 2; ++p) {
+      if (h->m.stage_free[p]) cudaEventDestroy(h->m.stage_free[p]);
+      for (int c = 0; c < kH2DChunks; ++c)
+        if (h->m.h2d_ev[p][c]) cudaEventDestroy(h->m.h2d_ev[p][c]);
+    }
     if (h->m.stream) cudaStreamDestroy(h->m.stream);
   } catch (...) {
   }
@@ -1084,6 +1131,18 @@ namespace {
 void infer_body(Model& m, const float* input, int K, float* scores, int on_device, cudaStream_t s) {
   struct Lists { Model& m; cudaStream_t s; ~Lists() { reset_lists(m, s); } } lists{m, s};
   const int f = (int)m.layers.size();
+  if (!on_device) {  // the copy streams start with the call (and never wait for its kernels)
+    for (cudaStream_t& c : m.cp)
+      if (!c) CUDA_OK(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+    if (!m.ev_call) CUDA_OK(cudaEventCreateWithFlags(&m.ev_call, cudaEventDisableTiming));
+    if (!m.stage_free[0])
+      for (int p = 0; p < 2; ++p) {
+        CUDA_OK(cudaEventCreateWithFlags(&m.stage_free[p], cudaEventDisableTiming));
+        for (int c = 0; c < kH2DChunks; ++c) CUDA_OK(cudaEventCreateWithFlags(&m.h2d_ev[p][c], cudaEventDisableTiming));
+      }
+    CUDA_OK(cudaEventRecord(m.ev_call, s));
+    for (cudaStream_t c : m.cp) CUDA_OK(cudaStreamWaitEvent(c, m.ev_call, 0));
+  }
   int o = 0;
   while (o < K) {
     const int rem = K - o;

@@ -382,6 +382,34 @@ def test_tc_infer_stack_image_major_and_phases(torch_dev):
     m.close()
 
 
+def test_host_input_prefetch_many_rounds(torch_dev):
+    """Host-buffer infer: each round's input goes up in pieces on the copy
+    streams into alternating staging buffers while earlier phases compute.
+    Many rounds (and a ragged remainder) must give the same bits as the
+    device-resident call, and a second call with other inputs must not see
+    the first call's staged data."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    cfg = synth.CONFIGS["C3"]
+    m = cdn.Model(0)
+    for i, spec in enumerate(cfg.fc):
+        _, _, buf = config_layer("C3", i)
+        m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+    n_out = cfg.fc[-1].rows
+    for K, plan in ((200, [8, 16, 32]), (300, [50, 100, 100]), (77, [1, 4, 12])):
+        m.set_plan(plan)
+        for seed in (1, 2):
+            a = synth.fc_inputs(cfg.fc[0].cols, K, seed)
+            host = np.zeros((K, n_out), np.float32)
+            m.infer(a, K, host, on_device=False)
+            xi = torch.from_numpy(a).to(dev)
+            so = torch.zeros((K, n_out), dtype=torch.float32, device=dev)
+            m.infer(xi, K, so, on_device=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(host, so.cpu().numpy()), (K, plan, seed)
+    m.close()
+
+
 def test_repeated_infer_graph_replay(torch_dev):
     """Identical infer calls on device buffers: the first runs eagerly, the
     second is captured into a CUDA graph, later ones replay it; every call's
