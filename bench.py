@@ -138,6 +138,11 @@ def run_ours(args):
     layers = compressed_layers(cdn)
     m = build_model(cdn, rank, world, nccl_id, layers)
     m.set_plan([B] * len(specs))
+    # The tensor-core path for every layer: what the library's first-use autotune
+    # picks for this workload on an idle B200 (scripts/grid_report.py), fixed here
+    # so the ncu launch list of this same command (where profiler gaps between
+    # launches skew the autotune's event timing) runs the same kernels.
+    m.set_kernel_policy(0, 16)
     stats = [m.stats(i) for i in range(len(specs))]
     K_in, N_out = specs[0].cols, specs[-1].rows
 
@@ -171,7 +176,9 @@ def run_ours(args):
             flush.zero_()                      # L2 flush between timed iterations
             barrier()
             ev[i][0].record(stream)
+            torch.cuda.nvtx.range_push("cdn_timed")  # the ncu launch list keeps only these
             step()
+            torch.cuda.nvtx.range_pop()
             ev[i][1].record(stream)
         barrier()
     launches = cdn.kernel_launches() - launches0

@@ -394,10 +394,13 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
     if (e != cudaSuccess) return e;
     set_smem = smem;
   }
+  ktimer_begin("k_gemm_bf16", s);
   dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN);
   k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
                                             ldo, col0, relu, lrn);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_gemm_bf16", s);
+  return e_;
 }
 
 // im2col for small channel groups (conv1: 3 channels, K = 11*11*3): a warp per
@@ -456,6 +459,7 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
   const long work = (long)B * Ho * Wo * (Kpad / 8);
   if (work >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing in the kernels
   const bool vec8 = (cg % 8 == 0) && (C % 4 == 0) && (c0 % 4 == 0) && (((uintptr_t)x & 15) == 0);
+  ktimer_begin("k_im2col", s);
   if (vec8)
     k_im2col<true><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
                                                                 Kreal, Kpad, out);
@@ -465,26 +469,34 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
   else
     k_im2col<false><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
                                                                  Kreal, Kpad, out);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_im2col", s);
+  return e_;
 }
 
 cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms) {
+  ktimer_begin("k_lrn", s);
   if (C % 4 == 0 && npos * C < (1L << 31) && (((uintptr_t)x | (uintptr_t)y) & 15) == 0)
     k_lrn4<<<grid_for(npos * C / 4, 256, num_sms), 256, 0, s>>>(x, (int)npos, C, y);
   else
     k_lrn<<<grid_for(npos * C, 256, num_sms), 256, 0, s>>>(x, npos, C, y);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_lrn", s);
+  return e_;
 }
 
 cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
                            int num_sms) {
   const int Ho = (H - k) / st + 1, Wo = (W - k) / st + 1;
+  ktimer_begin("k_maxpool", s);
   if (C % 4 == 0 && (long)B * H * W * C < (1L << 31) && (((uintptr_t)x | (uintptr_t)y) & 15) == 0)
     k_maxpool4<<<grid_for((long)B * Ho * Wo * C / 4, 256, num_sms), 256, 0, s>>>(
         reinterpret_cast<const float4*>(x), B, H, W, C / 4, k, st, Ho, Wo, reinterpret_cast<float4*>(y));
   else
     k_maxpool<<<grid_for((long)B * Ho * Wo * C, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_maxpool", s);
+  return e_;
 }
 
 }  // namespace cdn

@@ -611,6 +611,7 @@ cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaS
   const size_t smem = fc_smem_bytes(L);
   const int rows_per_cta = threads / L.G;
   const int work = (L.nrows + rows_per_cta - 1) / rows_per_cta;
+  ktimer_begin("k_decode_dense", s);
   if (L.rec64) {
     auto k = k_decode_dense<true>;
     k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw);
@@ -618,15 +619,20 @@ cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaS
     auto k = k_decode_dense<false>;
     k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw);
   }
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_decode_dense", s);
+  return e_;
 }
 
 cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float* out, int ldo,
                              cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
+  ktimer_begin("k_transpose", s);
   dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
   k_transpose<<<grid, block, 0, s>>>(in, rows, cols, ldi, out, ldo);
-  return launched();
+  const cudaError_t e_ = launched();
+  ktimer_end("k_transpose", s);
+  return e_;
 }
 
 }  // namespace cdn

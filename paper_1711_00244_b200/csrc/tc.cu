@@ -994,6 +994,7 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   e = launched();
   ktimer_end("k_fc_tc", s);
   if (e == cudaSuccess && p.grid != p.tiles) {  // some tile is split over CTAs
+    ktimer_begin("k_tc_reduce", s);
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
     if (p.tn == 128)
       k_tc_reduce<128><<<(unsigned)(p.tiles * (kTM / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
@@ -1002,6 +1003,7 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
       k_tc_reduce<256><<<(unsigned)(p.tiles * (kTM / 4)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
                                                                        p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok);
     e = launched();
+    ktimer_end("k_tc_reduce", s);
   }
   if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
     std::vector<unsigned long long> h(16 * 256);

@@ -66,5 +66,5 @@ def region_breakdown(rows_, lo, hi):
     return n_inst, {c: round(v / s_ * 100, 1) for c, v in sorted(tot_.items(), key=lambda kv: -kv[1]) if v}
 
 
-if len(sys.argv) > 4:
-    print(region_breakdown(rows, float(sys.argv[3]), float(sys.argv[4])))
+if len(args) > 3:
+    print(region_breakdown(rows, float(args[2]), float(args[3])))
