@@ -729,7 +729,7 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
     predecode_launch(m, L, s);
   }
   L.list_state = 2;  // later phases of the call reuse the decoded filters
-  m.conv_a.alloc((size_t)npos * L.kpad * 2);
+  m.conv_a.alloc((size_t)npos * L.kpad * 2 * G);  // the groups' patch matrices, stacked
   const bool post = d.lrn || d.pool_k > 0;
   float* cout = y;
   if (post) {
@@ -739,12 +739,14 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
   // LRN fused into the GEMM epilogue when one tile holds every channel (one
   // group, <= 256 filters: conv1); otherwise a separate pass
   const bool fuse_lrn = d.lrn && G == 1 && gemm_tile_n(M) >= M;
-  for (int g = 0; g < G; ++g) {
+  // every group's patches, then one GEMM launch over all groups (grid.z), so
+  // a grouped layer fills the GPU instead of running its groups back to back
+  __nv_bfloat16* pa = static_cast<__nv_bfloat16*>(m.conv_a.p);
+  for (int g = 0; g < G; ++g)
     CUDA_OK(launch_im2col(x, B, d.in_h, d.in_w, d.in_c, d.kh, d.kw, d.stride, d.pad, g * cg, cg, Ho, Wo,
-                          (int)L.cols, L.kpad, static_cast<__nv_bfloat16*>(m.conv_a.p), s, m.num_sms));
-    CUDA_OK(launch_gemm_bf16(static_cast<__nv_bfloat16*>(m.conv_a.p), (int)npos, wd + (size_t)g * mg * L.kpad, mg,
-                             L.kpad, L.bias.as<float>() + g * mg, d.relu, cout, M, g * mg, s, fuse_lrn ? 1 : 0));
-  }
+                          (int)L.cols, L.kpad, pa + (size_t)g * npos * L.kpad, s, m.num_sms));
+  CUDA_OK(launch_gemm_bf16(pa, (int)npos, wd, mg, L.kpad, L.bias.as<float>(), d.relu, cout, M, 0, s,
+                           fuse_lrn ? 1 : 0, G));
   const float* cur = cout;
   if (d.lrn && !fuse_lrn) {
     float* dst = d.pool_k > 0 ? (m.conv_t.alloc((size_t)npos * M * sizeof(float)), m.conv_t.as<float>()) : y;
@@ -960,7 +962,7 @@ std::vector<uint64_t> out_bytes(const Model& m) {
     // (reading C-24 for CONV layers); WS(i) keeps the decoded filters.
     if (L->is_conv())
       b += (uint64_t)L->conv_h * L->conv_w *
-           (2ull * L->kpad + (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows);
+           (2ull * L->kpad * (uint64_t)L->desc.groups + (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows);
     v.push_back(b);
   }
   return v;

@@ -53,6 +53,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
+  const int z = blockIdx.z;  // group of a grouped convolution: its own A / W planes, output columns, bias
+  col0 += z * Nrows;
+  bias += z * Nrows;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGStages; ++s) {
@@ -79,8 +82,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
       const int s = kt % kGStages;
       mbar_wait(&empty[s], ((kt / kGStages) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], (uint32_t)(a_bytes + b_bytes));
-      tma2d(sA + s * a_bytes, &ta, kt * kBK, m0, &full[s]);
-      tma2d(sB + s * b_bytes, &tb, kt * kBK, n0, &full[s]);
+      tma3d(sA + s * a_bytes, &ta, kt * kBK, m0, z, &full[s]);
+      tma3d(sB + s * b_bytes, &tb, kt * kBK, n0, z, &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer: 4 x (128 x BN x 16) per 64-wide K tile
@@ -373,19 +376,22 @@ size_t gemm_smem_bytes(int BN) {
 }
 
 cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
-                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s, int lrn) {
-  if (Mrows <= 0 || Nrows <= 0) return cudaSuccess;
+                             const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s, int lrn,
+                             int groups) {
+  if (Mrows <= 0 || Nrows <= 0 || groups <= 0) return cudaSuccess;
   if (Kpad % kBK) return cudaErrorInvalidValue;
   const int BN = gemm_tile_n(Nrows);
   if (lrn && BN < Nrows) return cudaErrorInvalidValue;  // the fused LRN needs every channel in one tile
   int tcols = 32;
   while (tcols < BN) tcols <<= 1;
+  // groups stacked as planes: A [groups][Mrows][Kpad], W [groups][Nrows][Kpad]
   CUtensorMap ta, tb;
-  cudaError_t e = encode_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, A, (uint64_t)Kpad, (uint64_t)Mrows,
-                                 (uint64_t)Kpad * 2, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  cudaError_t e = encode_tmap_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, A, (uint64_t)Kpad, (uint64_t)Mrows,
+                                 (uint64_t)groups, (uint64_t)Kpad * 2, (uint64_t)Kpad * 2 * Mrows, kBK, kBM,
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
-  e = encode_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Wt, (uint64_t)Kpad, (uint64_t)Nrows, (uint64_t)Kpad * 2,
-                     kBK, (uint32_t)BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  e = encode_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Wt, (uint64_t)Kpad, (uint64_t)Nrows, (uint64_t)groups,
+                     (uint64_t)Kpad * 2, (uint64_t)Kpad * 2 * Nrows, kBK, (uint32_t)BN, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
   const size_t smem = gemm_smem_bytes(BN);
   static thread_local size_t set_smem = 0;
@@ -395,7 +401,7 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
     set_smem = smem;
   }
   ktimer_begin("k_gemm_bf16", s);
-  dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN);
+  dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN, groups);
   k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
                                             ldo, col0, relu, lrn);
   const cudaError_t e_ = launched();
@@ -453,6 +459,142 @@ __global__ void __launch_bounds__(256) k_im2col_warp(const float* __restrict__ x
   }
 }
 
+// im2col for small channel groups (conv1: 3 channels, 11x11 taps, stride 4):
+// a block per output row (b, oh).  The kh input rows it reads are staged once
+// in shared memory as bf16 (padding columns and rows as zeros), so each input
+// element is fetched from L2 once per block instead of once per tap that
+// covers it (~(kh/stride)^2 = 7.6x for conv1); patches are then built from
+// shared memory, a lane per 8 consecutive k (one 16-byte store, 512 contiguous
+// bytes per warp instruction), through a per-k offset table.
+constexpr int kIm2colRowsMaxSmem = 40 * 1024;
+__global__ void __launch_bounds__(256) k_im2col_rows(const float* __restrict__ x, int B, int H, int W, int C, int kh,
+                                                     int kw, int stride, int pad, int c0, int cg, int Ho, int Wo,
+                                                     int Kreal, int Kpad, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char ir_smem[];
+  const int Wp = W + 2 * pad;
+  const int plane = kh * Wp * cg;                                       // staged rows, + one zero slot
+  int* s_off = reinterpret_cast<int*>(ir_smem);                         // [Kpad]
+  __nv_bfloat16* s_x = reinterpret_cast<__nv_bfloat16*>(ir_smem + 4 * Kpad);  // [kh][Wp][cg], [plane] = 0
+  const int b = blockIdx.x / Ho, oh = blockIdx.x - b * Ho;
+  const int ih0 = oh * stride - pad;
+  for (int k = threadIdx.x; k < Kpad; k += blockDim.x) {
+    int off = plane;  // the zero slot
+    if (k < Kreal) {
+      const int c = k % cg, rs = k / cg, sx = rs % kw, r = rs / kw;
+      off = (r * Wp + sx) * cg + c;
+    }
+    s_off[k] = off;
+  }
+  // stage the kh input rows (cg == C: a pixel row is one contiguous run of W * C
+  // floats), padding columns and out-of-image rows as zeros; no division
+  // (eight independent loads in flight per thread: the staging is latency-bound otherwise)
+  const int rowlen = Wp * cg, lo = pad * cg, hi = (pad + W) * cg;
+  const float* xb = x + (size_t)b * H * W * C - lo;
+  for (int i0 = threadIdx.x; i0 < plane; i0 += 8 * blockDim.x) {
+    int r = i0 / rowlen, j = i0 - r * rowlen;
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int ih = ih0 + r;
+      const bool ok = i0 + u * (int)blockDim.x < plane && ih >= 0 && ih < H && j >= lo && j < hi;
+      v[u] = ok ? __ldg(xb + (size_t)ih * W * C + j) : 0.f;
+      j += blockDim.x;  // rowlen >= blockDim.x (launcher): at most one wrap
+      if (j >= rowlen) {
+        j -= rowlen;
+        ++r;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u * (int)blockDim.x < plane) s_x[i0 + u * blockDim.x] = __float2bfloat16_rn(v[u]);
+  }
+  if (threadIdx.x == 0) s_x[plane] = __float2bfloat16_rn(0.f);
+  __syncthreads();
+  const int nq = Kpad >> 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned short* sx16 = reinterpret_cast<const unsigned short*>(s_x);
+  for (int ow = warp; ow < Wo; ow += nw) {
+    const int base = ow * stride * cg;
+    uint4* o = reinterpret_cast<uint4*>(out + ((size_t)blockIdx.x * Wo + ow) * Kpad);
+    for (int q = lane; q < nq; q += 32) {
+      const int4 oa = *reinterpret_cast<const int4*>(&s_off[8 * q]);
+      const int4 ob = *reinterpret_cast<const int4*>(&s_off[8 * q + 4]);
+      auto at = [&](int off) -> uint32_t { return sx16[off == plane ? plane : base + off]; };
+      uint4 v;
+      v.x = at(oa.x) | (at(oa.y) << 16);
+      v.y = at(oa.z) | (at(oa.w) << 16);
+      v.z = at(ob.x) | (at(ob.y) << 16);
+      v.w = at(ob.z) | (at(ob.w) << 16);
+      o[q] = v;
+    }
+  }
+}
+
+static size_t im2col_rows_smem(int kh, int W, int pad, int cg, int Kpad) {
+  return (size_t)4 * Kpad + 2 * ((size_t)kh * (W + 2 * pad) * cg + 1);
+}
+
+// im2col for channel groups of 8k (conv2-5): a warp per output position, a
+// lane per 8-channel chunk of K (two float4 loads, one 16-byte store, 512
+// contiguous bytes per warp step); the (r, s, c) of every chunk is tabled in
+// shared memory once per block, so the per-chunk work is a table read and the
+// bounds test -- no integer division (the per-thread decomposition of
+// k_im2col<true> made that kernel issue-bound at ~3x the HBM time).
+constexpr int kIm2colMaxChunks = 1024;
+__global__ void __launch_bounds__(256) k_im2col_warp8(const float* __restrict__ x, int B, int H, int W, int C, int kh,
+                                                      int kw, int stride, int pad, int c0, int cg, int Ho, int Wo,
+                                                      int Kreal, int Kpad, __nv_bfloat16* __restrict__ out) {
+  __shared__ int s_off[kIm2colMaxChunks];  // (r * W + s) * C + c of the chunk's first channel, -1 past Kreal
+  __shared__ unsigned char s_r[kIm2colMaxChunks], s_s[kIm2colMaxChunks];
+  const int nq = Kpad >> 3;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    const int k = q << 3;
+    if (k < Kreal) {
+      const int c = k % cg, rs = k / cg, sx = rs % kw, r = rs / kw;
+      s_off[q] = (r * W + sx) * C + c;
+      s_r[q] = (unsigned char)r;
+      s_s[q] = (unsigned char)sx;
+    } else {
+      s_off[q] = -1;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int npos = B * Ho * Wo;
+  for (int pos = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pos < npos; pos += warps) {
+    const int b = pos / (Ho * Wo), rem = pos - b * (Ho * Wo);
+    const int oh = rem / Wo, ow = rem - oh * Wo;
+    const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
+    const bool inside = ih0 >= 0 && iw0 >= 0 && ih0 + kh <= H && iw0 + kw <= W;
+    const float* xw = x + ((ptrdiff_t)((size_t)b * H + ih0) * W + iw0) * C + c0;  // window origin (maybe outside)
+    uint4* o = reinterpret_cast<uint4*>(out + (size_t)pos * Kpad);
+#pragma unroll 4
+    for (int q = lane; q < nq; q += 32) {
+      const int off = s_off[q];
+      bool ok = off >= 0;
+      if (ok && !inside) {
+        const int ih = ih0 + s_r[q], iw = iw0 + s_s[q];
+        ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
+      }
+      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+      if (ok) {
+        const float4* px = reinterpret_cast<const float4*>(xw + off);
+        a0 = __ldg(px);
+        a1 = __ldg(px + 1);
+      }
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(a0.x, a0.y), h1 = __floats2bfloat162_rn(a0.z, a0.w);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(a1.x, a1.y), h3 = __floats2bfloat162_rn(a1.z, a1.w);
+      uint4 v;
+      v.x = *reinterpret_cast<const uint32_t*>(&h0);
+      v.y = *reinterpret_cast<const uint32_t*>(&h1);
+      v.z = *reinterpret_cast<const uint32_t*>(&h2);
+      v.w = *reinterpret_cast<const uint32_t*>(&h3);
+      o[q] = v;
+    }
+  }
+}
+
 cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, int kw, int stride, int pad, int c0,
                           int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
                           int num_sms) {
@@ -460,9 +602,16 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
   if (work >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing in the kernels
   const bool vec8 = (cg % 8 == 0) && (C % 4 == 0) && (c0 % 4 == 0) && (((uintptr_t)x & 15) == 0);
   ktimer_begin("k_im2col", s);
-  if (vec8)
+  if (vec8 && Kpad / 8 <= kIm2colMaxChunks && (long)B * Ho * Wo < (1L << 31) && kh < 256 && kw < 256)
+    k_im2col_warp8<<<grid_for((long)B * Ho * Wo * 32, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad,
+                                                                                 c0, cg, Ho, Wo, Kreal, Kpad, out);
+  else if (vec8)
     k_im2col<true><<<grid_for(work, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo,
                                                                 Kreal, Kpad, out);
+  else if (cg == C && c0 == 0 && (W + 2 * pad) * cg >= 256 && im2col_rows_smem(kh, W, pad, cg, Kpad) <= kIm2colRowsMaxSmem && (long)B * Ho < (1L << 31) &&
+           (long)B * Ho * Wo * Kpad < (1L << 40))
+    k_im2col_rows<<<(unsigned)((long)B * Ho), 256, im2col_rows_smem(kh, W, pad, cg, Kpad), s>>>(
+        x, B, H, W, C, kh, kw, stride, pad, c0, cg, Ho, Wo, Kreal, Kpad, out);
   else if (Kpad <= kIm2colMaxK && (long)B * Ho * Wo < (1L << 31) && (long)B * H * W * C < (1L << 40))
     k_im2col_warp<<<grid_for((long)B * Ho * Wo * 32, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, kh, kw, stride, pad,
                                                                                 c0, cg, Ho, Wo, Kreal, Kpad, out);

@@ -149,7 +149,7 @@ cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, in
 int gemm_tile_n(int Nrows);  // N tile of the conv GEMM (<= 256)
 cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
                              const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s,
-                             int lrn = 0);
+                             int lrn = 0, int groups = 1);
 cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms);
 cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
                            int num_sms);
