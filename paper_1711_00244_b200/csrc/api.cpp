@@ -729,7 +729,6 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
     predecode_launch(m, L, s);
   }
   L.list_state = 2;  // later phases of the call reuse the decoded filters
-  m.conv_a.alloc((size_t)npos * L.kpad * 2 * G);  // the groups' patch matrices, stacked
   const bool post = d.lrn || d.pool_k > 0;
   float* cout = y;
   if (post) {
@@ -741,6 +740,9 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
   const bool fuse_lrn = d.lrn && G == 1 && gemm_tile_n(M) >= M;
   // every group's patches, then one GEMM launch over all groups (grid.z), so
   // a grouped layer fills the GPU instead of running its groups back to back
+  // (image chunks sized for L2 residency of the patches were slower: the
+  // small launches lose more than the HBM traffic they save)
+  m.conv_a.alloc((size_t)npos * L.kpad * 2 * G);  // the groups' patch matrices, stacked
   __nv_bfloat16* pa = static_cast<__nv_bfloat16*>(m.conv_a.p);
   for (int g = 0; g < G; ++g)
     CUDA_OK(launch_im2col(x, B, d.in_h, d.in_w, d.in_c, d.kh, d.kw, d.stride, d.pad, g * cg, cg, Ho, Wo,

@@ -5,14 +5,17 @@
 // unfolded to bf16 patches (K order (r, s, c), channel fastest, reading C-18),
 // and the contraction runs on the 5th-generation tensor cores:
 //
-//   k_gemm_bf16: D[pos][filter] = sum_k A[pos][k] * W[filter][k]
-//     * 128 positions x BN filters per CTA, K in 64-element (128-byte) tiles;
-//     * warp 0 / lane 0: TMA producer (cp.async.bulk.tensor, 128B swizzle)
-//       into a 4-stage smem ring on full/empty mbarriers;
+//   k_gemm_bf16: D[pos][filter] = sum_k A[pos][k] * W[filter][k], every group
+//   of the layer in one persistent launch (a CTA per SM walking the tiles)
+//     * 128 positions x BN filters per tile, K in 64-element (128-byte) tiles;
+//     * warp 0 / lane 0: TMA producer (cp.async.bulk.tensor 3D, 128B swizzle)
+//       into a smem ring (~200 KB) on full/empty mbarriers, across tiles;
 //     * warp 1 / lane 0: issues tcgen05.mma.cta_group::1.kind::f16 (bf16 x
-//       bf16 -> fp32 accumulator in TMEM), commits to the stage's empty
-//       barrier and, after the last tile, to the accumulator-ready barrier;
-//     * 4 warps: epilogue tcgen05.ld (32x32b) -> + bias -> ReLU -> fp32 NHWC.
+//       bf16 -> fp32 accumulator in TMEM, two accumulator buffers), commits
+//       to the stage's empty barrier and, after a tile's last K step, to that
+//       buffer's ready barrier;
+//     * warps 2-5: epilogue tcgen05.ld (32x32b) -> + bias -> ReLU (-> LRN) ->
+//       fp32 NHWC, then release the buffer -- overlapping the next tile.
 //   k_lrn, k_maxpool: the AlexNet norm / pool layers (C-19, C-20), NHWC fp32.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -30,44 +33,55 @@ using namespace dev;
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kGMaxStages = 4;
-constexpr int kGThreads = 128;
+constexpr int kGMaxStages = 8;
+constexpr int kGEpiWarps = 4;
+constexpr int kGMaxBias = 4096;  // groups * filters per group staged in shared memory
+constexpr int kGThreads = 64 + 32 * kGEpiWarps;  // TMA warp, MMA warp, epilogue warps
 
-// out[pos * ldo + col0 + n] = act( sum_k A[pos][k] W[n][k] + bias[n] ),
-// pos in [0, Mrows), n in [0, Nrows).  A: tensor map over [Mrows][Kpad] bf16,
-// W: over [Nrows][Kpad] bf16; nk = Kpad / 64.
+// out[pos * ldo + col0 + z * Nrows + n] = act( sum_k A_z[pos][k] W_z[n][k] + bias[z * Nrows + n] ),
+// pos in [0, Mrows), n in [0, Nrows), z the group.  A: tensor map over
+// [groups][Mrows][Kpad] bf16, W: over [groups][Nrows][Kpad] bf16; nk = Kpad / 64.
+// Persistent: a CTA per SM walks the (m, n, z) tiles; the TMEM accumulator is
+// double-buffered, so the epilogue of one tile overlaps the loads and MMAs of
+// the next (warp 0 TMA, warp 1 MMA, warps 2-5 epilogue, TMEM lane quadrant =
+// warp % 4).
 __global__ void __launch_bounds__(kGThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int Mrows, int Nrows,
                 int nk, int BN, int tmem_cols, int kGStages, const float* __restrict__ bias,
-                float* __restrict__ out, int ldo, int col0, int relu, int lrn) {
+                float* __restrict__ out, int ldo, int col0, int relu, int lrn, int groups) {
   extern __shared__ unsigned char smem_raw[];
-  // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space,
-  // so LUT/zero-fill accesses compile to LDS/STS instead of generic LD/ST)
+  // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space)
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const int a_bytes = kBM * kBK * 2, b_bytes = BN * kBK * 2;
   unsigned char* sA = smem;
   unsigned char* sB = smem + kGStages * a_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kGStages * b_bytes);
   uint64_t* empty = full + kGStages;
-  uint64_t* done = empty + kGStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + kGStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // [groups * Nrows], 16-byte aligned (float4 reads): off the epilogue's load latency
+  float* s_bias = reinterpret_cast<float*>(
+      smem + ((reinterpret_cast<unsigned char*>(tmem_slot + 4) - smem + 15) & ~(ptrdiff_t)15));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
-  const int z = blockIdx.z;  // group of a grouped convolution: its own A / W planes, output columns, bias
-  col0 += z * Nrows;
-  bias += z * Nrows;
+  const int mt = (Mrows + kBM - 1) / kBM, ntl = (Nrows + BN - 1) / BN;
+  const int tiles = mt * ntl * groups;
+  for (int i = threadIdx.x; i < groups * Nrows; i += blockDim.x) s_bias[i] = bias[i];
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kGEpiWarps);
+    }
     mbar_fence_init();
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
-                 "r"(tmem_cols)
+                 "r"(2 * tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -76,133 +90,158 @@ __global__ void __launch_bounds__(kGThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer
-    for (int kt = 0; kt < nk; ++kt) {
-      const int s = kt % kGStages;
-      mbar_wait(&empty[s], ((kt / kGStages) & 1) ^ 1);
-      mbar_arrive_expect_tx(&full[s], (uint32_t)(a_bytes + b_bytes));
-      tma3d(sA + s * a_bytes, &ta, kt * kBK, m0, z, &full[s]);
-      tma3d(sB + s * b_bytes, &tb, kt * kBK, n0, z, &full[s]);
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer, the stage ring running on across tiles
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m = t % mt, n = (t / mt) % ntl, z = t / (mt * ntl);
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int s = it % kGStages;
+          mbar_wait(&empty[s], ((it / kGStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(a_bytes + b_bytes));
+          tma3d(sA + s * a_bytes, &ta, kt * kBK, m * kBM, z, &full[s]);
+          tma3d(sB + s * b_bytes, &tb, kt * kBK, n * BN, z, &full[s]);
+        }
+      }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer: 4 x (128 x BN x 16) per 64-wide K tile
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(kBM >> 4) << 24);
-    for (int kt = 0; kt < nk; ++kt) {
-      const int s = kt % kGStages;
-      mbar_wait(&full[s], (kt / kGStages) & 1);
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: 4 x (128 x BN x 16) per 64-wide K tile, into accumulator (local tile & 1)
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(kBM >> 4) << 24);
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int buf = i & 1;
+        mbar_wait(&acc_empty[buf], ((i >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(buf * tmem_cols);
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int s = it % kGStages;
+          mbar_wait(&full[s], (it / kGStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ad = sw128_desc(smem_addr(sA + s * a_bytes));
+          const uint64_t bd = sw128_desc(smem_addr(sB + s * b_bytes));
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) umma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (kt | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[buf]);
+      }
+    }
+  } else {
+    // ---- epilogue warps: TMEM lane = position row (quadrant warp % 4), column = filter
+    const int q = warp & 3;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int m = t % mt, n = (t / mt) % ntl, z = t / (mt * ntl);
+      const int buf = i & 1;
+      const int n0 = n * BN, c0z = col0 + z * Nrows;
+      const float* bz = s_bias + z * Nrows;
+      mbar_wait(&acc_full[buf], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t ad = sw128_desc(smem_addr(sA + s * a_bytes));
-      const uint64_t bd = sw128_desc(smem_addr(sB + s * b_bytes));
+      const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * tmem_cols);
+      const int row = m * kBM + q * 32 + lane;
+      if (lrn) {
+        // LRN fused (the tile holds all Nrows channels of its positions; one lane =
+        // one position): y_c = a_c * (2 + 1e-4/5 * sum_{q=c-2..c+2} a_q^2)^-0.75,
+        // a = act(conv + bias), summed in the order k_lrn uses (bit-identical).
+        // Chunks of 16 channels slide with the 2 before and the 16 after.
+        auto act = [&](float (&v)[16], int c) {
 #pragma unroll
-      for (int k = 0; k < kBK / 16; ++k)
-        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kt | k) != 0);
-      umma_commit(&empty[s]);
-    }
-    umma_commit(done);
-  }
-  __syncwarp();
-
-  // ---- epilogue: TMEM lane = position row, column = filter
-  mbar_wait(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = m0 + warp * 32 + lane;
-  if (lrn) {
-    // LRN fused (the CTA holds all Nrows channels of its positions; one lane =
-    // one position): y_c = a_c * (2 + 1e-4/5 * sum_{q=c-2..c+2} a_q^2)^-0.75,
-    // a = act(conv + bias), summed in the order k_lrn uses (bit-identical).
-    // Chunks of 16 channels slide with the 2 before and the 16 after.
-    auto act = [&](float (&v)[16], int c) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int n = c + i;
-        float o = n < Nrows ? v[i] + __ldg(bias + n) : 0.f;  // (uniform over the warp: broadcast loads)
-        if (relu) o = fmaxf(o, 0.f);
-        v[i] = o;
-      }
-    };
-    float cur[16], nxt[16], p1 = 0.f, p2 = 0.f;  // p2 = a[c-2], p1 = a[c-1]
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), cur);
-    act(cur, 0);
-    for (int c = 0; c < Nrows; c += 16) {
-      if (c + 16 < Nrows) {
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c + 16), nxt);
-        act(nxt, c + 16);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) nxt[i] = 0.f;
-      }
-      float o[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int ch = c + i;
-        // window a[ch-2 .. ch+2] clipped to [0, Nrows)
-        float w[5];
-        w[0] = i >= 2 ? cur[i - 2] : (i == 1 ? p1 : p2);
-        w[1] = i >= 1 ? cur[i - 1] : p1;
-        w[2] = cur[i];
-        w[3] = i + 1 < 16 ? cur[i + 1] : nxt[i - 15];
-        w[4] = i + 2 < 16 ? cur[i + 2] : nxt[i - 14];
-        float sq = 0.f;
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-          const int cq = ch - 2 + q;
-          if (cq >= 0 && cq < Nrows) sq = fmaf(w[q], w[q], sq);
-        }
-        o[i] = cur[i] * exp2f(-0.75f * __log2f(2.0f + (1e-4f / 5.0f) * sq));
-      }
-      if (row < Mrows) {
-        float* op = out + (size_t)row * ldo + col0 + c;
-        if (c + 16 <= Nrows && ((((uintptr_t)op) & 15) == 0)) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            reinterpret_cast<float4*>(op)[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c + i < Nrows) op[i] = o[i];
-        }
-      }
-      p2 = cur[14];
-      p1 = cur[15];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
-    }
-  } else
-  for (int c = 0; c < BN; c += 16) {
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
-    if (row < Mrows) {
-      float* op = out + (size_t)row * ldo + col0 + n0 + c;
-      if (n0 + c + 16 <= Nrows && ((((uintptr_t)op) & 15) == 0)) {
-        const float4* bp = reinterpret_cast<const float4*>(bias + n0 + c);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 bq = __ldg(bp + q);
-          float4 o = make_float4(v[4 * q] + bq.x, v[4 * q + 1] + bq.y, v[4 * q + 2] + bq.z, v[4 * q + 3] + bq.w);
-          if (relu) {
-            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
-          }
-          reinterpret_cast<float4*>(op)[q] = o;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int n = n0 + c + i;
-          if (n < Nrows) {
-            float o = v[i] + bias[n];
+          for (int u = 0; u < 16; ++u) {
+            const int ch = c + u;
+            float o = ch < Nrows ? v[u] + bz[ch] : 0.f;  // (uniform over the warp: smem broadcast)
             if (relu) o = fmaxf(o, 0.f);
-            op[i] = o;
+            v[u] = o;
+          }
+        };
+        float cur[16], nxt[16], p1 = 0.f, p2 = 0.f;  // p2 = a[c-2], p1 = a[c-1]
+        tmem_ld16(tq, cur);
+        act(cur, 0);
+        for (int c = 0; c < Nrows; c += 16) {
+          if (c + 16 < Nrows) {
+            tmem_ld16(tq + (uint32_t)(c + 16), nxt);
+            act(nxt, c + 16);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) nxt[u] = 0.f;
+          }
+          float o[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int ch = c + u;
+            // window a[ch-2 .. ch+2] clipped to [0, Nrows)
+            float w[5];
+            w[0] = u >= 2 ? cur[u - 2] : (u == 1 ? p1 : p2);
+            w[1] = u >= 1 ? cur[u - 1] : p1;
+            w[2] = cur[u];
+            w[3] = u + 1 < 16 ? cur[u + 1] : nxt[u - 15];
+            w[4] = u + 2 < 16 ? cur[u + 2] : nxt[u - 14];
+            float sq = 0.f;
+#pragma unroll
+            for (int r = 0; r < 5; ++r) {
+              const int cq = ch - 2 + r;
+              if (cq >= 0 && cq < Nrows) sq = fmaf(w[r], w[r], sq);
+            }
+            o[u] = cur[u] * exp2f(-0.75f * __log2f(2.0f + (1e-4f / 5.0f) * sq));
+          }
+          if (row < Mrows) {
+            float* op = out + (size_t)row * ldo + c0z + c;
+            if (c + 16 <= Nrows && ((((uintptr_t)op) & 15) == 0)) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r)
+                reinterpret_cast<float4*>(op)[r] = make_float4(o[4 * r], o[4 * r + 1], o[4 * r + 2], o[4 * r + 3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 16; ++u)
+                if (c + u < Nrows) op[u] = o[u];
+            }
+          }
+          p2 = cur[14];
+          p1 = cur[15];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
+        }
+      } else {
+        for (int c = 0; c < BN; c += 16) {
+          float v[16];
+          tmem_ld16(tq + (uint32_t)c, v);
+          if (row < Mrows) {
+            float* op = out + (size_t)row * ldo + c0z + n0 + c;
+            if (n0 + c + 16 <= Nrows && ((((uintptr_t)op) & 15) == 0)) {
+              const float4* bp = reinterpret_cast<const float4*>(bz + n0 + c);
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                const float4 bq = bp[r];
+                float4 o = make_float4(v[4 * r] + bq.x, v[4 * r + 1] + bq.y, v[4 * r + 2] + bq.z, v[4 * r + 3] + bq.w);
+                if (relu) {
+                  o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                }
+                reinterpret_cast<float4*>(op)[r] = o;
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int ch = n0 + c + u;
+                if (ch < Nrows) {
+                  float o = v[u] + bz[ch];
+                  if (relu) o = fmaxf(o, 0.f);
+                  op[u] = o;
+                }
+              }
+            }
           }
         }
       }
+      // the accumulator buffer is free again once every epilogue warp has read it
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tmem_cols) : "memory");
 }
 
 // NHWC fp32 -> bf16 (RNE) patches [pos][Kpad] of channels [c0, c0+cg):
@@ -362,23 +401,24 @@ int gemm_tile_n(int Nrows) {
   return (bn + 15) & ~15;
 }
 
-// Pipeline depth: as many stages as fit ~100 KB, so two CTAs share an SM and
-// one CTA's epilogue overlaps the other's tensor-core main loop.
+// Pipeline depth: as many stages as fit ~200 KB (one persistent CTA per SM;
+// its double-buffered accumulator overlaps the epilogue with the next tile).
 int gemm_stages(int BN) {
   const int per = kBM * kBK * 2 + BN * kBK * 2;
-  int st = (100 * 1024) / per;
+  int st = (200 * 1024) / per;
   return st < 2 ? 2 : (st > kGMaxStages ? kGMaxStages : st);
 }
 
 size_t gemm_smem_bytes(int BN) {
   const int st = gemm_stages(BN);
-  return 1024 + (size_t)st * (kBM * kBK * 2 + BN * kBK * 2) + (2 * st + 1) * 8 + 16;
+  return 1024 + (size_t)st * (kBM * kBK * 2 + BN * kBK * 2) + (2 * st + 4) * 8 + 32 + 4 * kGMaxBias;
 }
 
 cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloat16* Wt, int Nrows, int Kpad,
                              const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s, int lrn,
                              int groups) {
   if (Mrows <= 0 || Nrows <= 0 || groups <= 0) return cudaSuccess;
+  if ((long)groups * Nrows > kGMaxBias) return cudaErrorInvalidValue;
   if (Kpad % kBK) return cudaErrorInvalidValue;
   const int BN = gemm_tile_n(Nrows);
   if (lrn && BN < Nrows) return cudaErrorInvalidValue;  // the fused LRN needs every channel in one tile
@@ -401,9 +441,15 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
     set_smem = smem;
   }
   ktimer_begin("k_gemm_bf16", s);
-  dim3 grid((Mrows + kBM - 1) / kBM, (Nrows + BN - 1) / BN, groups);
+  const long tiles = (long)((Mrows + kBM - 1) / kBM) * ((Nrows + BN - 1) / BN) * groups;
+  int num_sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
   k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
-                                            ldo, col0, relu, lrn);
+                                            ldo, col0, relu, lrn, groups);
   const cudaError_t e_ = launched();
   ktimer_end("k_gemm_bf16", s);
   return e_;
