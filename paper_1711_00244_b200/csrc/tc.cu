@@ -70,7 +70,7 @@ constexpr int kTmemCols = 512;      // accumulator 256 + W buffers 4 x 64
 struct TcArgs {
   float* y;
   int ldy, B, relu;
-  float* ws;   // [tiles][mpt][128][256] partials of split tiles, summed by k_tc_reduce
+  float* ws;   // [tiles][mpt][TN / 4][128] float4 partials of split tiles, summed by k_tc_reduce
   int nbt, nrt, nkt, G, mpt;  // batch tiles, row tiles, K tiles, CTAs, max pieces per tile
   long W;                     // total tile steps = tiles * nkt (stream-K)
   unsigned long long* trace;    // debug (env CDN_TC_TRACE): CTA 0 event clocks [event][256], else null
@@ -449,8 +449,11 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const int b0 = t.bt * TN;
       const bool has = t.kt1 > t.kt0;
       const bool whole = t.count == 1;  // this CTA owns the tile's whole K range
+      // partials: [tile][slot][TN / 4 column groups][128 rows] float4, so a warp's
+      // 32 rows of one column group are 512 contiguous bytes (row-major 1 KB
+      // rows made every store instruction 32 scattered half-sectors)
       float* const dst = whole ? a.y + (size_t)row * a.ldy + b0
-                               : a.ws + (((size_t)t.tile * a.mpt + t.slot) * kTM + row_l) * TN;
+                               : a.ws + ((size_t)t.tile * a.mpt + t.slot) * kTM * TN + (size_t)row_l * 4;
       const float bias = (whole && row < L.wrows) ? L.bias[row] : 0.f;
       // y rows are contiguous over the batch: whole float4s where the tile is inside B
       const bool vec_ok = (a.ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
@@ -481,7 +484,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
         } else {
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
-            __stcg(reinterpret_cast<float4*>(dst + c + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+            __stcg(reinterpret_cast<float4*>(dst + (size_t)((c + i) >> 2) * (kTM * 4)),
+                   make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -546,39 +550,56 @@ template <int TN>
 __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, uint32_t W, int G, int nkt,
                                                    int mpt, int nbt, int nrows, int B, const float* __restrict__ bias,
                                                    int relu, float* __restrict__ y, int ldy, int vec_ok) {
-  // block = (1024 / TN) rows x TN/4 float4 columns of one tile
-  constexpr int kR = 1024 / TN, kC4 = TN / 4;
-  const uint32_t tile = blockIdx.x / (kTM / kR);
-  const int r = (int)(blockIdx.x % (kTM / kR)) * kR + (int)(threadIdx.x / kC4);
-  const int c4 = threadIdx.x % kC4;
+  // block = 32 rows x 8 float4 column groups of one tile.  Reads go row-fastest
+  // (the partials are column-group major, [TN / 4][128] float4 per piece:
+  // coalesced), the sums are transposed through shared memory, and the y
+  // writes go column-fastest (128 contiguous bytes per row)
+  constexpr int kC4 = TN / 4, kCC = kC4 / 8;
+  __shared__ float4 s_t[32][9];
+  const uint32_t tile = blockIdx.x / (4 * kCC);
+  const int rg = (int)(blockIdx.x % (4 * kCC)) / kCC, cc = (int)(blockIdx.x % kCC);
   const uint32_t t0 = tile * (uint32_t)nkt;  // 32-bit: W = tiles * nkt < 2^32 / G (host-checked)
   const int count = (int)(((t0 + nkt) * (uint32_t)G - 1) / W) - (int)(((t0 + 1) * (uint32_t)G - 1) / W) + 1;
-  if (count == 1) return;
+  if (count == 1) return;  // (uniform over the block)
   const int rt = (int)(tile / (uint32_t)nbt), bt = (int)(tile % (uint32_t)nbt);
-  const int row = rt * kTM + r, b = bt * TN + 4 * c4;
-  if (row >= nrows || b >= B) return;
-  const float* p = ws + ((size_t)tile * mpt * kTM + r) * TN + 4 * c4;
-  float4 q[8];  // the partials' loads all in flight before the (ordered) sum
+  {
+    const int r = rg * 32 + (int)(threadIdx.x & 31), g = (int)(threadIdx.x >> 5);
+    const int c4 = cc * 8 + g;
+    const int row = rt * kTM + r, b = bt * TN + 4 * c4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < nrows && b < B) {
+      const float* p = ws + (size_t)tile * mpt * kTM * TN + ((size_t)c4 * kTM + r) * 4;
+      float4 q[8];  // the partials' loads all in flight before the (ordered) sum
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < count) q[j] = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * TN));
-  float4 acc = q[0];
+      for (int j = 0; j < 8; ++j)
+        if (j < count) q[j] = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * TN));
+      acc = q[0];
 #pragma unroll
-  for (int j = 1; j < 8; ++j)
-    if (j < count) { acc.x += q[j].x; acc.y += q[j].y; acc.z += q[j].z; acc.w += q[j].w; }
-  for (int j = 8; j < count; ++j) {  // rare: more than 8 CTAs on one tile
-    const float4 e = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * TN));
-    acc.x += e.x; acc.y += e.y; acc.z += e.z; acc.w += e.w;
+      for (int j = 1; j < 8; ++j)
+        if (j < count) { acc.x += q[j].x; acc.y += q[j].y; acc.z += q[j].z; acc.w += q[j].w; }
+      for (int j = 8; j < count; ++j) {  // rare: more than 8 CTAs on one tile
+        const float4 e = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * TN));
+        acc.x += e.x; acc.y += e.y; acc.z += e.z; acc.w += e.w;
+      }
+      const float bs = bias[row];
+      acc.x += bs; acc.y += bs; acc.z += bs; acc.w += bs;
+      if (relu) {
+        acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+      }
+    }
+    s_t[threadIdx.x & 31][g] = acc;
   }
-  const float bs = bias[row];
-  float o[4] = {acc.x + bs, acc.y + bs, acc.z + bs, acc.w + bs};
-  if (relu)
-    for (int k = 0; k < 4; ++k) o[k] = fmaxf(o[k], 0.f);
+  __syncthreads();
+  const int g = (int)(threadIdx.x & 7), r = rg * 32 + (int)(threadIdx.x >> 3);
+  const int row = rt * kTM + r, b = bt * TN + 4 * (cc * 8 + g);
+  if (row >= nrows || b >= B) return;
+  const float4 o = s_t[threadIdx.x >> 3][g];
   float* yp = y + (size_t)row * ldy + b;
   if (vec_ok && b + 4 <= B) {
-    *reinterpret_cast<float4*>(yp) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(yp) = o;
   } else {
-    for (int k = 0; k < 4 && b + k < B; ++k) yp[k] = o[k];
+    const float ov[4] = {o.x, o.y, o.z, o.w};
+    for (int k = 0; k < 4 && b + k < B; ++k) yp[k] = ov[k];
   }
 }
 
@@ -997,10 +1018,10 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     ktimer_begin("k_tc_reduce", s);
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
     if (p.tn == 128)
-      k_tc_reduce<128><<<(unsigned)(p.tiles * (kTM / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
+      k_tc_reduce<128><<<(unsigned)(p.tiles * (128 / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
                                                                        p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok);
     else
-      k_tc_reduce<256><<<(unsigned)(p.tiles * (kTM / 4)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
+      k_tc_reduce<256><<<(unsigned)(p.tiles * (256 / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
                                                                        p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok);
     e = launched();
     ktimer_end("k_tc_reduce", s);
