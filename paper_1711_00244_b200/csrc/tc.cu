@@ -404,9 +404,15 @@ __global__ void __launch_bounds__(kTThreads, 1)
             if ((uint32_t)i >= wmax) break;
             sts_u16_if(ad[i], (hl[i] >> hsh) & 0xFFFFu, (uint32_t)i < nnz);
           }
-          for (uint32_t i = kEnt; i < nnz; ++i) {  // a denser row tile
-            const uint32_t e = __ldg(cur + i);
-            sts_u16_if(prow + rsw_off(row_l, e & 63u), (s_cbs[e >> 6] >> hsh) & 0xFFFFu, true);
+          // a denser row tile: the rest in groups of 8 whose loads are all in
+          // flight together (one at a time, each entry waited its full latency)
+          for (uint32_t i0 = kEnt; i0 < wmax; i0 += 8) {
+            uint32_t e[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) e[j] = i0 + j < nnz ? __ldg(cur + i0 + j) : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              sts_u16_if(prow + rsw_off(row_l, e[j] & 63u), (s_cbs[e[j] >> 6] >> hsh) & 0xFFFFu, i0 + j < nnz);
           }
           {  // 8 conflict-free LDS.128 -> one tcgen05.st of 32 columns
             uint32_t r[32];
@@ -423,7 +429,13 @@ __global__ void __launch_bounds__(kTThreads, 1)
             if ((uint32_t)i >= wmax) break;
             sts_u16_if(ad[i], 0u, (uint32_t)i < nnz);
           }
-          for (uint32_t i = kEnt; i < nnz; ++i) sts_u16_if(prow + rsw_off(row_l, __ldg(cur + i) & 63u), 0u, true);
+          for (uint32_t i0 = kEnt; i0 < wmax; i0 += 8) {
+            uint32_t e[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) e[j] = i0 + j < nnz ? __ldg(cur + i0 + j) : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sts_u16_if(prow + rsw_off(row_l, e[j] & 63u), 0u, i0 + j < nnz);
+          }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
