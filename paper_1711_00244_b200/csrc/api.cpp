@@ -565,7 +565,7 @@ int band_min_batch() {
 // One fused FC layer launch: the warp-specialised band kernel for large
 // batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
 void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s,
-                bool x_im = false) {
+                bool x_im = false, bool y_im = false) {
   const int relu = L.desc.relu;
   // Default policy for B >= band_min_batch(): both large-batch kernels are timed once at the
   // first call with this B and the faster is kept for the layer (autotune).
@@ -619,11 +619,11 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       }
       L.list_state = 2;
       CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<__nv_bfloat16*>(m.tc_xh.p),
-                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), s, x_im));
+                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), s, x_im, y_im));
       return;
     }
   }
-  if (x_im) throw Error(CDN_E_ARG, "internal: an image-major input needs the tensor-core path");
+  if (x_im || y_im) throw Error(CDN_E_ARG, "internal: an image-major input / output needs the tensor-core path");
   if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
     BandPlan p = plan_fc_band(L.dev, x, ldx, B, m.num_sms);
     if (p.ok) {
@@ -761,12 +761,13 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
 // One layer step: local rows -> (all-gather if world > 1) -> dst [rows][ld_dst].
 // x: feature-major [K][ldx], or image-major [B][ldx] when x_im (tensor-core layers only)
 void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, int ld_dst, cudaStream_t s,
-                bool x_im = false) {
+                bool x_im = false, bool y_im = false) {
   Layer& L = *m.layers[li];
   if (m.world == 1) {
-    fc_forward(m, L, x, ldx, B, dst, ld_dst, s, x_im);
+    fc_forward(m, L, x, ldx, B, dst, ld_dst, s, x_im, y_im);
     return;
   }
+  if (y_im) throw Error(CDN_E_ARG, "internal: image-major output with several ranks");
   const uint32_t rb = rows_per_rank(L.rows, m.world);
   const size_t slab = (size_t)rb * B;
   m.loc.alloc(slab * sizeof(float));
@@ -809,7 +810,7 @@ struct Exec {
       } else if (uses_tc(m, L, Bi)) {
         // the tensor-core layer splits the image-major input into bf16 hi / lo
         // directly (no feature-major copy)
-        layer_step(m, i, src, (int)per, Bi, dst, ld, s, true);
+        layer_step(m, i, src, (int)per, Bi, dst, ld, s, true, yt_last && i + 1 == (int)m.layers.size());
         return;
       } else {
         CUDA_OK(launch_transpose(src, Bi, (int)per, (int)per, xin, li, s));
@@ -832,9 +833,10 @@ struct Exec {
     if (L.is_conv())
       conv_forward(m, L, xin, Bi, dst, s);
     else
-      layer_step(m, i, xin, li, Bi, dst, ld, s);
+      layer_step(m, i, xin, li, Bi, dst, ld, s, false, yt_last && i + 1 == (int)m.layers.size());
   }
   int st_o = 0, st_chunk = 1, st_par = 0;  // the round's staged host input
+  bool yt_last = false;  // the last layer writes the image-major scores itself (no transpose)
   // Host input: issue the round's H2D copies, kH2DChunks pieces round-robin
   // over the copy streams, each with an event the phases reading it wait
   // for; the staging buffer alternates between rounds.
@@ -864,12 +866,29 @@ struct Exec {
     if (!on_device) prefetch(o);
     const uint32_t classes = m.layers[f - 1]->rows;
     const int lf = ld4(Bf);
+    float* dst = scores + (size_t)o * classes;
+    // a tensor-core last layer stores [Bf][classes] straight from its epilogue
+    // / reduce (a warp's rows are contiguous floats there)
+    Layer& Lf = *m.layers[f - 1];
+    yt_last = m.world == 1 && uses_tc(m, Lf, Bf) && plan_fc_tc(Lf.dev, Bf, m.num_sms).ok;
+    if (yt_last) {
+      float* yd = dst;
+      if (!on_device) {
+        m.host_stage.alloc((size_t)classes * Bf * sizeof(float));
+        yd = m.host_stage.as<float>();
+      }
+      run(f - 1, o, yd, (int)classes);
+      if (!on_device) {
+        CUDA_OK(cudaEventRecord(m.stage_free[st_par], s));
+        CUDA_OK(cudaMemcpyAsync(dst, yd, (size_t)classes * Bf * sizeof(float), cudaMemcpyDeviceToHost, s));
+      }
+      return;
+    }
     m.out.alloc((size_t)classes * lf * sizeof(float));
     run(f - 1, o, m.out.as<float>(), lf);
     if (!on_device) CUDA_OK(cudaEventRecord(m.stage_free[st_par], s));
     if (m.rank != 0) return;
     // [classes][lf] -> scores[o..o+Bf)[classes]
-    float* dst = scores + (size_t)o * classes;
     if (on_device) {
       CUDA_OK(launch_transpose(m.out.as<float>(), (int)classes, Bf, lf, dst, (int)classes, s));
     } else {

@@ -111,7 +111,7 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms);
 cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s);
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s,
-                         bool x_image_major = false);  // x: [K][ldx] feature-major, or [B][ldx] image-major
+                         bool x_image_major = false, bool y_image_major = false);  // x: [K][ldx] feature-major, or [B][ldx] image-major
 
 // Small-batch multi-symbol kernel (B <= 8; r <= 5, k <= 4, 32-bit lane records).
 bool ms_supported(const FcDev& L);

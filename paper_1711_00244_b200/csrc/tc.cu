@@ -74,6 +74,7 @@ struct TcArgs {
   int nbt, nrt, nkt, G, mpt;  // batch tiles, row tiles, K tiles, CTAs, max pieces per tile
   long W;                     // total tile steps = tiles * nkt (stream-K)
   unsigned long long* trace;    // debug (env CDN_TC_TRACE): CTA 0 event clocks [event][256], else null
+  int yt;                       // 1: y image-major [B][ldy] (the class scores of the last layer), else [rows][ldy]
 };
 
 __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       // partials: [tile][slot][TN / 4 column groups][128 rows] float4, so a warp's
       // 32 rows of one column group are 512 contiguous bytes (row-major 1 KB
       // rows made every store instruction 32 scattered half-sectors)
-      float* const dst = whole ? a.y + (size_t)row * a.ldy + b0
+      float* const dst = whole ? (a.yt ? a.y : a.y + (size_t)row * a.ldy + b0)
                                : a.ws + ((size_t)t.tile * a.mpt + t.slot) * kTM * TN + (size_t)row_l * 4;
       const float bias = (whole && row < L.wrows) ? L.bias[row] : 0.f;
       // y rows are contiguous over the batch: whole float4s where the tile is inside B
@@ -483,7 +484,11 @@ __global__ void __launch_bounds__(kTThreads, 1)
               v[i] += bias;
               if (a.relu) v[i] = fmaxf(v[i], 0.f);
             }
-            if (vec_ok && b0 + c + 16 <= a.B) {
+            if (a.yt) {  // image-major: a warp's 32 rows are 128 contiguous bytes per image
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (b0 + c + i < a.B) a.y[(size_t)(b0 + c + i) * a.ldy + row] = v[i];
+            } else if (vec_ok && b0 + c + 16 <= a.B) {
 #pragma unroll
               for (int i = 0; i < 16; i += 4)
                 *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -561,7 +566,7 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
 template <int TN>
 __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, uint32_t W, int G, int nkt,
                                                    int mpt, int nbt, int nrows, int B, const float* __restrict__ bias,
-                                                   int relu, float* __restrict__ y, int ldy, int vec_ok) {
+                                                   int relu, float* __restrict__ y, int ldy, int vec_ok, int yt) {
   // block = 32 rows x 8 float4 column groups of one tile.  Reads go row-fastest
   // (the partials are column-group major, [TN / 4][128] float4 per piece:
   // coalesced), the sums are transposed through shared memory, and the y
@@ -598,6 +603,13 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
       if (relu) {
         acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
       }
+    }
+    if (yt) {  // image-major y (class scores): consecutive rows are consecutive floats
+      if (row < nrows && b < B) {
+        const float ov[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (int k = 0; k < 4 && b + k < B; ++k) y[(size_t)(b + k) * ldy + row] = ov[k];
+      }
+      return;  // (yt is uniform: no block skips the barrier another one waits at)
     }
     s_t[threadIdx.x & 31][g] = acc;
   }
@@ -983,7 +995,8 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
 }
 
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s, bool x_image_major) {
+                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s, bool x_image_major,
+                         bool y_image_major) {
   ktimer_begin("k_split_x", s);
   if (x_image_major) {
     const long n = (long)B * (p.ldk / 8);
@@ -1018,7 +1031,8 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     if (e != cudaSuccess) return e;
   }
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
-  TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr};
+  TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr,
+           y_image_major ? 1 : 0};
   ktimer_begin("k_fc_tc", s);
   if (p.tn == 128)
     k_fc_tc<128><<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
@@ -1031,10 +1045,12 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
     if (p.tn == 128)
       k_tc_reduce<128><<<(unsigned)(p.tiles * (128 / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
-                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok);
+                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok,
+                                                                       y_image_major ? 1 : 0);
     else
       k_tc_reduce<256><<<(unsigned)(p.tiles * (256 / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
-                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok);
+                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok,
+                                                                       y_image_major ? 1 : 0);
     e = launched();
     ktimer_end("k_tc_reduce", s);
   }
