@@ -262,15 +262,27 @@ def run_ours(args):
     if dom_k == "k_fc_tc":
         # a dense contraction after decode: the tensor cores execute 3 bf16 passes
         # (hi*hi + hi*lo + lo*hi) over the 128-row x 64-col tiles and 256-image tiles
+        tn = 128 if B <= 128 else 256  # image tile of the kernel (tc.cu plan_fc_tc)
+
         def dense(i):
             kpad = (specs[i].cols + 63) // 64 * 64
-            return 3 * 2.0 * (-(-nloc_of(i) // 128) * 128) * kpad * (-(-B // 256) * 256)
+            return 3 * 2.0 * (-(-nloc_of(i) // 128) * 128) * kpad * (-(-B // tn) * tn)
         work = sum(dense(i) for i in lay) * args.steps
-        peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1392.1)))
+        # The burst peak when the SM clock held its maximum through the timed
+        # region (short steps between L2 flushes: no power throttling), else the
+        # sustained one (cuBLAS back to back for 4 s ran at ~1335 MHz).
+        cs = clk.summary()
+        at_max = bool(cs.get("sm_mhz") and cs.get("sm_max_mhz") and cs["sm_mhz"] >= 0.95 * cs["sm_max_mhz"])
+        if at_max and "bf16_tflops" in pk:
+            peak = float(pk["bf16_tflops"])
+            src = ("MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 burst; the SM clock stayed at its maximum "
+                   "through the timed region)")
+        else:
+            peak = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1392.1)))
+            src = "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, back to back)"
         roof = {"bound": "tensor", "achieved": work / t_s / 1e12, "peak": peak, "unit": "TFLOP/s",
                 "useful_tflops": useful / t_s / 1e12,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, back to back); "
-                               "achieved = executed 3-pass bf16 tile flops (DESIGN.md)"}
+                "peak_source": src + "; achieved = executed 3-pass bf16 tile flops (DESIGN.md)"}
     elif dom_k == "k_fc_band":
         roof = {"bound": "alu", "achieved": useful / t_s / 1e12, "peak": alu_peak, "unit": "TFLOP/s",
                 "peak_source": "148 SMs x 128 FP32 lanes x 2 x sm_max_mhz; achieved = 2*nnz*B + N*B"}
