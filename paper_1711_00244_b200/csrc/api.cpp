@@ -818,6 +818,14 @@ struct Exec {
     } else {
       const Layer& P = *m.layers[i - 1];
       const int b = bs[i - 1];
+      if (P.is_conv() && b == Bi && m.world == 1 && uses_tc(m, L, Bi) && plan_fc_tc(L.dev, Bi, m.num_sms).ok) {
+        // one conv phase feeding a tensor-core FC layer: its image-major NHWC
+        // output (flattened (h, w, c), C-22) is split into bf16 hi / lo directly
+        float* t = m.ctmp.as<float>();
+        run(i - 1, o, t, 0);
+        layer_step(m, i, t, (int)L.cols, Bi, dst, ld, s, true, yt_last && i + 1 == (int)m.layers.size());
+        return;
+      }
       for (int p = 0; p < Bi / b; ++p) {
         if (L.is_conv()) {
           run(i - 1, o + p * b, xin + (size_t)p * b * L.in_elems(), 0);
