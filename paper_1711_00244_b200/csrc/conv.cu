@@ -624,29 +624,23 @@ __global__ void __launch_bounds__(256) k_im2col_warp8(const float* __restrict__ 
     const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
     const bool inside = ih0 >= 0 && iw0 >= 0 && ih0 + kh <= H && iw0 + kw <= W;
     const float* xw = x + ((ptrdiff_t)((size_t)b * H + ih0) * W + iw0) * C + c0;  // window origin (maybe outside)
-    uint4* o = reinterpret_cast<uint4*>(out + (size_t)pos * Kpad);
+    // a lane per half chunk (4 channels): the two lanes of a chunk read its 32
+    // contiguous bytes in ONE load instruction (whole sectors; a lane reading
+    // both halves took two instructions on half sectors each), 8-byte stores
+    uint2* o = reinterpret_cast<uint2*>(out + (size_t)pos * Kpad);
 #pragma unroll 4
-    for (int q = lane; q < nq; q += 32) {
+    for (int q2 = lane; q2 < 2 * nq; q2 += 32) {
+      const int q = q2 >> 1;
       const int off = s_off[q];
       bool ok = off >= 0;
       if (ok && !inside) {
         const int ih = ih0 + s_r[q], iw = iw0 + s_s[q];
         ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
       }
-      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-      if (ok) {
-        const float4* px = reinterpret_cast<const float4*>(xw + off);
-        a0 = __ldg(px);
-        a1 = __ldg(px + 1);
-      }
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(a0.x, a0.y), h1 = __floats2bfloat162_rn(a0.z, a0.w);
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(a1.x, a1.y), h3 = __floats2bfloat162_rn(a1.z, a1.w);
-      uint4 v;
-      v.x = *reinterpret_cast<const uint32_t*>(&h0);
-      v.y = *reinterpret_cast<const uint32_t*>(&h1);
-      v.z = *reinterpret_cast<const uint32_t*>(&h2);
-      v.w = *reinterpret_cast<const uint32_t*>(&h3);
-      o[q] = v;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) a = __ldg(reinterpret_cast<const float4*>(xw + off + 4 * (q2 & 1)));
+      const __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+      o[q2] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
     }
   }
 }
