@@ -246,6 +246,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
   for (int i = threadIdx.x; i < kStreams * (kDecW / 4) * kTM * kRowBytes / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(rows)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
+  // launched as a programmatic dependent of the split kernel: everything above
+  // (TMEM, barriers, codebook) overlapped its tail; its output is read below
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");  // the reduce's blocks may take their slots
   const uint32_t tmem_w = tmem + TN;  // W buffers: column TN + (q * kWBufs + b) * kWCols
 
   // The MMA consumes the two streams' tiles alternately q = 0, 1, 0, 1, ...
@@ -525,6 +529,7 @@ constexpr int kSplitK = 64, kSplitB = 32;
 __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, int K, int ldx, int B,
                                                  __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl,
                                                  int ldk) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
   __shared__ float tile[kSplitK][kSplitB + 1];
   const int k0 = blockIdx.x * kSplitK, b0 = blockIdx.y * kSplitB;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
@@ -573,6 +578,7 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
   // writes go column-fastest (128 contiguous bytes per row)
   constexpr int kC4 = TN / 4, kCC = kC4 / 8;
   __shared__ float4 s_t[32][9];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of the contraction
   const uint32_t tile = blockIdx.x / (4 * kCC);
   const int rg = (int)(blockIdx.x % (4 * kCC)) / kCC, cc = (int)(blockIdx.x % kCC);
   const uint32_t t0 = tile * (uint32_t)nkt;  // 32-bit: W = tiles * nkt < 2^32 / G (host-checked)
@@ -633,6 +639,7 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
 __global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x, int K, int ldx, int B,
                                                     __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl,
                                                     int ldk, int vec) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
   const int nk8 = ldk / 8;
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long)B * nk8) return;
@@ -1034,24 +1041,46 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr,
            y_image_major ? 1 : 0};
   ktimer_begin("k_fc_tc", s);
-  if (p.tn == 128)
-    k_fc_tc<128><<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
-  else
-    k_fc_tc<256><<<p.grid, kTThreads, p.smem, s>>>(L, a, th, tl);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p.grid);
+    cfg.blockDim = dim3(kTThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the split
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (p.tn == 128)
+      e = cudaLaunchKernelEx(&cfg, k_fc_tc<128>, L, a, th, tl);
+    else
+      e = cudaLaunchKernelEx(&cfg, k_fc_tc<256>, L, a, th, tl);
+    if (e != cudaSuccess) return e;
+  }
   e = launched();
   ktimer_end("k_fc_tc", s);
   if (e == cudaSuccess && p.grid != p.tiles) {  // some tile is split over CTAs
     ktimer_begin("k_tc_reduce", s);
     const int vec_ok = (ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.tiles * (p.tn / 8)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // launch latency hidden under the contraction
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const float* wsc = ws;
+    const int yt = y_image_major ? 1 : 0;
     if (p.tn == 128)
-      k_tc_reduce<128><<<(unsigned)(p.tiles * (128 / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
-                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok,
-                                                                       y_image_major ? 1 : 0);
+      e = cudaLaunchKernelEx(&cfg, k_tc_reduce<128>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
+                             L.bias, relu, y, ldy, vec_ok, yt);
     else
-      k_tc_reduce<256><<<(unsigned)(p.tiles * (256 / 8)), 256, 0, s>>>(ws, (uint32_t)p.W, p.grid, p.nkt, p.mpt,
-                                                                       p.nbt, L.wrows, B, L.bias, relu, y, ldy, vec_ok,
-                                                                       y_image_major ? 1 : 0);
-    e = launched();
+      e = cudaLaunchKernelEx(&cfg, k_tc_reduce<256>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
+                             L.bias, relu, y, ldy, vec_ok, yt);
+    if (e == cudaSuccess) e = launched();
     ktimer_end("k_tc_reduce", s);
   }
   if (e == cudaSuccess && trace_path) {  // debug only: dump CTA 0's event clocks
