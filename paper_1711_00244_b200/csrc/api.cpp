@@ -302,7 +302,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   L.row0 = sl.row0;
   L.row1 = sl.row1;
   const uint32_t nr = L.row1 - L.row0;
-  int target = 64;
+  int target = 32;  // tokens per decode lane: 32 gives the short layers (fc7 / fc8) enough lanes
   if (const char* e = std::getenv("CDN_LANE_TOKENS")) target = std::max(1, std::atoi(e));
   int G = choose_lanes_per_row(H, 0, H.rows, target);  // whole layer: shard-invariant lanes
   if (const char* e = std::getenv("CDN_LANES_PER_ROW")) G = std::max(1, std::min(32, std::atoi(e)));
