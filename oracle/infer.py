@@ -11,7 +11,7 @@ to rows".  K order is (r, s, c), channel fastest, per group (C-18).  The
 product runs CONV on bf16 tensor cores with fp32 accumulation (config C4), so
 the oracle rounds the input and the weights to bf16 (RNE) first and then does
 the product in fp64 (C-21).  LRN/max-pool are the paper's "fixed functions"
-(Table 4 rows norm*/pool*); LRN constants follow C-20 (parity unpinned).
+(Table 4 rows norm*/pool*); LRN constants follow reading C-20; both are pinned by the hand-computed cases in tests/golden/lrn_maxpool_hand.txt.
 
 Activation layout in the oracle: image-major [B][features] (FC) and NHWC (CONV).
 """
@@ -154,7 +154,7 @@ def conv_direct(x: np.ndarray, Wq: np.ndarray, kh: int, kw: int, stride: int, pa
     return out
 
 
-LRN_N, LRN_ALPHA, LRN_BETA, LRN_K = 5, 1e-4, 0.75, 2.0   # C-20 (parity unpinned)
+LRN_N, LRN_ALPHA, LRN_BETA, LRN_K = 5, 1e-4, 0.75, 2.0   # C-20 (constants are the reading; the implementation is pinned by tests/golden/lrn_maxpool_hand.txt)
 
 
 def lrn(x: np.ndarray) -> np.ndarray:

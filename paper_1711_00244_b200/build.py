@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcdn.so")
-SOURCES = ["host.cpp", "kernels.cu", "band.cu", "small.cu", "tc.cu", "conv.cu", "api.cpp"]
+SOURCES = ["host.cpp", "kernels.cu", "band.cu", "small.cu", "joint.cu", "tc.cu", "conv.cu", "api.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,18 +40,33 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     inc, lib = _nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", inc,
-           "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES],
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib,]
+    common = [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v" if verbose else "-O3",
+              "-I", os.path.join(ROOT, "include"), "-I", inc]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    # one object per translation unit, compiled concurrently, then one link
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        r = subprocess.run(common + ["-c", os.path.join(CSRC, src), "-o", obj], capture_output=True, text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for src, _, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed compiling {src}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    cmd = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *[o for _, o, _ in results],
+           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libcdn.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libcdn.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -100,6 +101,8 @@ struct Layer {
   std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band) measured at first use
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
+  DBuf jw, jrow, jlane, jlut, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
+  std::vector<uint32_t> jrow_h;               // host copy of jrow (per-CTA stream ranges)
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
   bool blocked = false;  // block-contiguous container (Alg. 2, C-34): tensor-core path only
   cdn_layer_stats stats{};
@@ -143,7 +146,8 @@ struct Model {
   bool busy = false;
   int band_min = 0;             // cdn_model_set_kernel_policy (0: default)
   int tc_min = 0;               // cdn_model_set_kernel_policy tensor-core threshold (0: default)
-  DBuf tc_xh, tc_xl;            // tensor-core FC: bf16 hi / lo split of the activations
+  DBuf tc_xh, tc_xl;            // tensor-core FC: fp16 hi / lo split of the activations
+  DBuf tc_sc, tc_ctr;           // tensor-core FC: per-image split scales; their arrival counters (zero between calls)
   // CUDA graphs of repeated infer calls (same buffers, K, plan and state):
   // the second identical call is captured, later ones replay it
   struct GraphEntry {
@@ -296,8 +300,9 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   L.k = H.k;
   L.r = H.r;
   L.blocked = blocked;
-  // FC: row-block shard per rank; CONV: replicas (every rank
-  // holds all filters; the batch is what multi-GPU splits for conv layers).
+  // FC: row-block shard per rank; CONV: replicated (every rank
+  // holds all filters and, in infer, runs the conv layers on the whole batch:
+  // the conv trunk is not split across ranks).
   const ShardSlice sl = shard_slice(H, m.rank, m.world, conv);
   L.row0 = sl.row0;
   L.row1 = sl.row1;
@@ -322,6 +327,102 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     rp[2ull * i + 1] = (uint32_t)(H.rp[2ull * (L.row0 + i) + 1] - gbase);
   }
   L.rp.upload(rp);
+  if (!conv && !blocked && H.codebook.size() <= 32) {
+    // merged token stream + joint LUT of the small-batch kernel (joint.cu, C-35).
+    // LUT width: wider windows fold more tokens per lookup, but every CTA
+    // stages the table (4 << jL bytes), so small layers take narrower ones.
+    // Column groups Q: the smallest Q whose CTA (tables + x slice + stream
+    // slots) fits half an SM's shared memory, so the next launch's CTA can
+    // stage its weights beside a running one (programmatic dependent launch).
+    uint64_t tb = 0, rmax = 0;
+    for (uint32_t i = L.row0; i < L.row1; ++i) {
+      const uint64_t rb = (H.rp[2ull * i + 2] - H.rp[2ull * i]) + (H.rp[2ull * i + 3] - H.rp[2ull * i + 1]);
+      tb += rb;
+      rmax = std::max(rmax, rb);
+    }
+    const double per_sm = (double)tb / 8.0 / std::max(1, m.num_sms);
+    int jl = per_sm >= 24576 ? 14 : per_sm >= 12288 ? 13 : per_sm >= 6144 ? 12 : 11;
+    int jq = 1;
+    {
+      const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits)), Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
+      auto est = [&](int Q, int L2) {
+        const double rows_cta = std::ceil((double)nr * Q / std::max(1, m.num_sms));
+        return (double)(4u << L2) + (4u << Lv) + (4u << Lg) + 2048.0 + 4.0 * std::ceil((double)H.cols / Q) +
+               rows_cta * ((double)rmax / 8.0 / Q + 48.0);
+      };
+      bool found = false;
+      for (int L2 = jl; L2 >= 12 && !found; --L2)
+        for (int Q = 1; Q <= 8 && Q <= G && !found; Q *= 2)
+          if (G % Q == 0 && est(Q, L2) <= 110.0 * 1024) {
+            jq = Q;
+            jl = L2;
+            found = true;
+          }
+    }
+    if (const char* e = std::getenv("CDN_JL")) jl = std::max(8, std::min(16, std::atoi(e)));
+    if (const char* e = std::getenv("CDN_JQ")) jq = std::max(1, std::min(G, std::atoi(e)));
+    while (G % jq) jq >>= 1;
+    JointIndex jx;
+    if (build_joint_index(H, L.row0, L.row1, G, jq, jx)) {
+      // per-row staging slot: the largest byte span of one (row, column group)
+      uint32_t sub = 0;
+      const int GQ = G / jq;
+      for (uint32_t i = 0; i < nr; ++i)
+        for (int q = 0; q < jq; ++q) {
+          const uint32_t base = jx.row_bit[i];
+          const uint32_t a = base + (jx.lane[(size_t)i * G + q * GQ] & 0xffffu);
+          const uint32_t b = q + 1 < jq ? base + (jx.lane[(size_t)i * G + (q + 1) * GQ] & 0xffffu) : jx.row_bit[i + 1];
+          sub = std::max<uint32_t>(sub, (((b + 127) >> 7) - (a >> 7)) * 16u + 16u);
+        }
+      L.jw.upload(jx.words);
+      L.jrow.upload(jx.row_bit);
+      L.jrow_h = jx.row_bit;
+      L.jlane.upload(jx.lane);
+      // one blob of every table the kernel stages, in its shared-memory layout
+      // (a single bulk copy per CTA): joint LUT, the slow path's plain LUTs and
+      // canonical tables, the codebook (entry 0 = padding = 0.0)
+      const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
+      const int Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
+      std::vector<uint8_t> blob;
+      auto put = [&](const void* p, size_t n) {
+        const size_t o = (blob.size() + 127) & ~(size_t)127;
+        blob.resize(o + n);
+        std::memcpy(blob.data() + o, p, n);
+        return (uint32_t)o;
+      };
+      const auto jlut = build_joint_lut(H.val, H.gap, jl);
+      const auto vl = build_lut(H.val, Lv), gl = build_lut(H.gap, Lg), vt = build_tab(H.val), gt = build_tab(H.gap);
+      std::vector<uint16_t> vs = H.val.sorted, gs = H.gap.sorted;
+      vs.push_back(0);
+      gs.push_back(0);
+      std::vector<float> cb(32, 0.f);
+      for (size_t i = 1; i < H.codebook.size() && i < 32; ++i) cb[i] = H.codebook[i];
+      put(jlut.data(), jlut.size() * 4);
+      L.dev.jo_vlut = put(vl.data(), vl.size() * 4);
+      L.dev.jo_glut = put(gl.data(), gl.size() * 4);
+      L.dev.jo_vtab = put(vt.data(), vt.size() * 4);
+      L.dev.jo_gtab = put(gt.data(), gt.size() * 4);
+      L.dev.jo_vs = put(vs.data(), vs.size() * 2);
+      L.dev.jo_gs = put(gs.data(), gs.size() * 2);
+      L.dev.jo_cb = put(cb.data(), cb.size() * 4);
+      blob.resize((blob.size() + 15) & ~(size_t)15);
+      L.dev.jblob = (uint32_t)blob.size();
+      L.jlut.upload(blob);
+      L.dev.jL = jl;
+      L.dev.jsub = sub;
+      L.dev.jQ = jq;
+      L.dev.jKq = (int)jx.Kq;
+      if (std::getenv("CDN_JDEBUG"))
+        fprintf(stderr, "[cdn] joint layer rows=%u cols=%u G=%d Q=%d jL=%d sub=%u blob=%u\n", nr, H.cols, G, jq, jl, sub,
+                L.dev.jblob);
+      if (jq > 1) {
+        const int units = (int)((nr + (uint32_t)(32 / GQ) - 1) / (uint32_t)(32 / GQ));
+        L.jpart.alloc(sizeof(float) * 4 * (size_t)jq * nr);
+        L.jctr.alloc(sizeof(int) * (size_t)units);
+        CUDA_OK(cudaMemset(L.jctr.p, 0, sizeof(int) * (size_t)units));
+      }
+    }
+  }
   if (ix.rec64) L.rec.upload(ix.rec64v); else L.rec.upload(ix.rec32);
   L.tok.upload(ix.tok_start);
   {
@@ -477,6 +578,15 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.vsorted = L.vsorted.as<uint16_t>();
   f.gsorted = L.gsorted.as<uint16_t>();
   f.codebook = L.cb.as<float>();
+  {
+    // power-of-two weight scale of the tensor-core path's fp16 split:
+    // max |C| s in [2^14, 2^15)
+    float mx = 0.f;
+    for (float c : H.codebook) mx = std::max(mx, std::fabs(c));
+    int E = 0;
+    if (mx > 0.f && std::isfinite(mx)) std::frexp(mx, &E);
+    f.tc_wsc = mx > 0.f && std::isfinite(mx) ? std::ldexp(1.0f, std::max(-120, std::min(120, 15 - E))) : 1.0f;
+  }
   f.bias = L.bias.as<float>();
   f.nrows = (int)nr;
   f.cols = (int)H.cols;
@@ -502,6 +612,12 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.Lpg = pad_glen;
   f.msv = L.msv.p ? L.msv.as<uint32_t>() : nullptr;
   f.msg = L.msg.p ? L.msg.as<uint32_t>() : nullptr;
+  f.jw = L.jw.p ? L.jw.as<uint32_t>() : nullptr;
+  f.jrow = L.jrow.p ? L.jrow.as<uint32_t>() : nullptr;
+  f.jlane = L.jlane.p ? L.jlane.as<uint32_t>() : nullptr;
+  f.jlut = L.jlut.p ? L.jlut.as<uint32_t>() : nullptr;
+  f.jpart = L.jpart.p ? L.jpart.as<float>() : nullptr;
+  f.jctr = L.jctr.p ? L.jctr.as<int>() : nullptr;
   f.tivg = L.tivg.p ? L.tivg.as<uint2>() : (L.dev.Wi == 64 ? L.ivg.as<uint2>() : nullptr);
   f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : (L.dev.Wi == 64 ? L.ivm.as<uint16_t>() : nullptr);
   f.tbase = L.tbase.as<uint32_t>();
@@ -584,6 +700,11 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       CUDA_OK(cudaEventCreate(&e0));
       CUDA_OK(cudaEventCreate(&e1));
       CUDA_OK(cudaEventCreate(&e2));
+      // the forced policies below are undone however this block exits
+      struct Restore {
+        int& v;
+        ~Restore() { v = 0; }
+      } restore{m.tc_min};
       m.tc_min = B;  // force the tensor-core kernel for one timed launch
       fc_forward(m, L, x, ldx, B, y, ldy, s);
       CUDA_OK(cudaEventRecord(e0, s));
@@ -611,6 +732,11 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
     if (p.ok) {
       m.tc_xh.alloc(p.xsplit_elems * 2);
       m.tc_xl.alloc(p.xsplit_elems * 2);
+      m.tc_sc.alloc(tc_scale_floats(B) * sizeof(float));
+      if (m.tc_ctr.n < sizeof(int) * (size_t)B || !m.tc_ctr.p) {
+        m.tc_ctr.alloc(sizeof(int) * (size_t)B);
+        CUDA_OK(cudaMemsetAsync(m.tc_ctr.p, 0, m.tc_ctr.n, s));
+      }
       if (p.ws_floats) L.bws.alloc(p.ws_floats * sizeof(float));
       if (L.list_state == 1) {
         CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
@@ -618,8 +744,9 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
         CUDA_OK(launch_tc_list(L.dev, s));
       }
       L.list_state = 2;
-      CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<__nv_bfloat16*>(m.tc_xh.p),
-                           static_cast<__nv_bfloat16*>(m.tc_xl.p), L.bws.as<float>(), s, x_im, y_im));
+      CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<uint16_t*>(m.tc_xh.p),
+                           static_cast<uint16_t*>(m.tc_xl.p), L.bws.as<float>(), m.tc_sc.as<float>(), m.tc_ctr.as<int>(), s,
+                           x_im, y_im));
       return;
     }
   }
@@ -637,10 +764,18 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       return;
     }
   }
-  static const bool force_fold = [] {
+  static const int small_kernel = [] {  // debug override: "fold" / "ms" (older small-batch kernels)
     const char* e = std::getenv("CDN_SMALL_KERNEL");
-    return e && std::strcmp(e, "fold") == 0;
+    return !e ? 0 : std::strcmp(e, "fold") == 0 ? 1 : std::strcmp(e, "ms") == 0 ? 2 : 0;
   }();
+  const bool force_fold = small_kernel == 1;
+  if (B <= 4 && small_kernel == 0 && j_supported(L.dev)) {
+    const JPlan p = plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data());
+    if (p.ok) {
+      CUDA_OK(launch_fc_j(L.dev, p, x, ldx, B, y, ldy, relu, s));
+      return;
+    }
+  }
   if (B <= 8 && !force_fold && ms_supported(L.dev)) {
     CUDA_OK(launch_fc_ms(L.dev, x, ldx, B, y, ldy, relu, s, m.num_sms));
     return;
@@ -974,6 +1109,16 @@ void profile(Model& m, int Bmax, int reps) {
   cudaEventDestroy(e1);
   CUDA_OK(cudaStreamSynchronize(s));
   for (auto& L : m.layers) L->list_state = 0;  // profiling's lists are not the caller's
+  if (m.world > 1 && m.comm) {
+    // every rank must run the same plan (the same phases issue the same
+    // all-gathers): the DP runs on one table, the slowest rank's time per
+    // (layer, batch) -- close plans would otherwise flip on timing noise
+    DBuf d;
+    d.upload(m.prof);
+    NCCL_OK(ncclAllReduce(d.p, d.p, m.prof.size(), ncclDouble, ncclMax, m.comm, s));
+    CUDA_OK(cudaMemcpyAsync(m.prof.data(), d.p, m.prof.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+  }
   m.prof_bmax = Bmax;
 }
 
@@ -1325,6 +1470,7 @@ cdn_status cdn_layer_forward(cdn_model* h, int layer, const float* x, int ldx, i
   Layer& L = *m.layers[layer];
   if (L.is_conv()) return fail(CDN_E_ARG, "CONV layer: use cdn_conv_forward");
   if (ldx < B || ldy < B) return fail(CDN_E_ARG, "leading dimension < B");
+  CUDA_OK(cudaSetDevice(m.device));
   cudaStream_t s = pick(m, stream);
   struct Lists { Model& m; cudaStream_t s; ~Lists() { reset_lists(m, s); } } lists{m, s};
   reset_lists(m, s);  // a single-layer call decodes its own list
@@ -1407,6 +1553,7 @@ cdn_status cdn_layer_decode(cdn_model* h, int layer, int32_t* row, int32_t* col,
   *n_tokens = L.stats.tokens;
   if (!row && !col && !sym && !val) return CDN_OK;
   if (!row || !col || !sym || !val) return fail(CDN_E_ARG, "all four outputs required");
+  CUDA_OK(cudaSetDevice(h->m.device));
   cudaStream_t s = pick(h->m, stream);
   CUDA_OK(launch_decode(L.dev, (int)L.row0, row, col, sym, val, s, h->m.num_sms));
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
@@ -1453,6 +1600,8 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
     const int vec = B > 64 ? 4 : (B > 32 ? 2 : 1);
     return vec == 4 ? "k_fc_band<4>" : (vec == 2 ? "k_fc_band<2>" : "k_fc_band<1>");
   }
+  if (B <= 4 && j_supported(L.dev) && plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data()).ok && !std::getenv("CDN_SMALL_KERNEL"))
+    return "k_fc_j";
   if (B <= 8 && ms_supported(L.dev)) return "k_fc_ms";
   return "k_fc_fold";
 }

@@ -331,6 +331,137 @@ void build_interval_index(const HostLayer& L, uint32_t r0, uint32_t r1, uint32_t
   }
 }
 
+// ------------------------------------------------- merged token stream
+
+bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, JointIndex& out) {
+  const uint32_t nr = r1 - r0;
+  if (L.cols > 65535 || G < 1 || Q < 1 || G % Q) return false;
+  uint64_t total = 0;
+  uint32_t mx = 0;
+  for (uint32_t i = r0; i < r1; ++i) {
+    const uint64_t rb = (L.rp[2ull * i + 2] - L.rp[2ull * i]) + (L.rp[2ull * i + 3] - L.rp[2ull * i + 1]);
+    if (rb >= 65536) return false;
+    mx = std::max<uint32_t>(mx, (uint32_t)rb);
+    total += rb;
+  }
+  if (total >= (1ull << 32) - 1024) return false;
+  const int GQ = G / Q;
+  const uint32_t Kq = (uint32_t)(((L.cols + Q - 1) / Q + 3) & ~3u);  // column group width (16-byte x slices)
+  out.G = G;
+  out.Q = Q;
+  out.Kq = Kq;
+  out.bits = total;
+  out.max_row_bits = mx;
+  out.words.assign((size_t)((total + 31) / 32) + 8, 0u);
+  out.row_bit.assign((size_t)nr + 1, 0u);
+  out.lane.assign((size_t)nr * G, 0u);
+  uint64_t pos = 0;
+  auto put = [&](uint32_t code, uint32_t len) {  // MSB-first, len <= 32
+    for (uint32_t b = 0; b < len; ++b) {
+      if ((code >> (len - 1 - b)) & 1u) out.words[pos >> 5] |= 0x80000000u >> (pos & 31);
+      ++pos;
+    }
+  };
+  std::vector<uint32_t> tbit;   // bit offset (from the row start) of each token
+  std::vector<int32_t> tprev;   // previous column before each token
+  std::vector<int32_t> tcol;    // column of each token
+  std::vector<uint8_t> tpad;    // token is padding
+  std::vector<size_t> real_at;  // token index of each real token
+  for (uint32_t i = r0; i < r1; ++i) {
+    const size_t li = i - r0;
+    out.row_bit[li] = (uint32_t)pos;
+    tbit.clear();
+    tprev.clear();
+    tcol.clear();
+    tpad.clear();
+    real_at.clear();
+    uint64_t vpos = L.rp[2ull * i], gpos = L.rp[2ull * i + 1];
+    const uint64_t vend = L.rp[2ull * i + 2];
+    int32_t prev = -1;
+    while (vpos < vend) {
+      uint32_t vs, vl, gs, gl;
+      if (!L.val.decode(window32(L.vbytes, vpos), vs, vl) || !L.gap.decode(window32(L.gbytes, gpos), gs, gl))
+        throw Error(CDN_E_MALFORMED, "row " + std::to_string(i) + ": bad code (merged stream)");
+      tbit.push_back((uint32_t)(pos - out.row_bit[li]));
+      tprev.push_back(prev);
+      tpad.push_back(vs == 0);
+      put(L.val.code_of[vs], vl);
+      put(L.gap.code_of[gs], gl);
+      prev += (int32_t)gs + 1;
+      tcol.push_back(prev);
+      if (vs != 0) real_at.push_back(tbit.size() - 1);
+      vpos += vl;
+      gpos += gl;
+    }
+    const size_t T = tbit.size();
+    // column group q = the tokens from the first with column >= q*Kq, moved
+    // back over the padding before it; inside a group, lane j starts at its
+    // real token of rank ~j*R_q/GQ (the kernel spends one step per real
+    // token: padding folds into the lookup of the token it precedes), again
+    // moved back over padding -- no lane ends with padding
+    size_t bprev = 0;
+    size_t rq = 0;  // first real-token rank of the group
+    for (int q = 0; q < Q; ++q) {
+      size_t gb = 0;  // group's first token
+      if (q > 0) {
+        while (gb < T && tcol[gb] < (int64_t)q * Kq) ++gb;
+        gb = std::max(gb, bprev);
+        while (gb > bprev && tpad[gb - 1]) --gb;
+      }
+      size_t ge = T;  // next group's first token (before moving back): the group's real tokens end there
+      if (q + 1 < Q) {
+        ge = 0;
+        while (ge < T && tcol[ge] < (int64_t)(q + 1) * Kq) ++ge;
+      }
+      size_t re = rq;
+      while (re < real_at.size() && real_at[re] < ge) ++re;
+      const size_t R = re - rq;
+      for (int jj = 0; jj < GQ; ++jj) {
+        size_t b = gb;
+        if (jj > 0) {
+          b = R ? real_at[rq + std::min<size_t>((uint64_t)jj * R / (uint64_t)GQ, R - 1)] : ge;
+          if (R == 0) b = std::max(gb, std::min(ge, T));
+        }
+        b = std::max(b, bprev);
+        while (b > bprev && tpad[b - 1]) --b;
+        b = std::max(b, bprev);
+        bprev = b;
+        const uint32_t off = b < T ? tbit[b] : (uint32_t)(pos - out.row_bit[li]);
+        const int32_t pc = b < T ? tprev[b] : prev;
+        out.lane[li * G + q * GQ + jj] = off | ((uint32_t)(pc + 1) << 16);
+      }
+      rq = re;
+    }
+  }
+  out.row_bit[nr] = (uint32_t)pos;
+  if (pos != total) throw Error(CDN_E_MALFORMED, "internal: merged stream length");
+  return true;
+}
+
+std::vector<uint32_t> build_joint_lut(const HuffCode& val, const HuffCode& gap, int Lb) {
+  std::vector<uint32_t> lut((size_t)1 << Lb, 0u);
+  for (uint32_t w = 0; w < (1u << Lb); ++w) {
+    const uint32_t win = w << (32 - Lb);
+    uint32_t pos = 0, adv = 0, sym = 0;
+    bool any = false;
+    for (;;) {
+      uint32_t vs, vl, gs, gl;
+      if (pos >= (uint32_t)Lb || !val.decode(win << pos, vs, vl) || pos + vl > (uint32_t)Lb) break;
+      if (pos + vl >= 32 || !gap.decode(win << (pos + vl), gs, gl) || pos + vl + gl > (uint32_t)Lb) break;
+      pos += vl + gl;
+      adv += gs + 1;
+      any = true;
+      if (vs != 0) {  // a real token ends the entry; padding tokens (symbol 0, C-04) fold into it
+        sym = vs;
+        break;
+      }
+    }
+    if (!any || pos > 31 || adv * 4 >= (1u << 17) || sym > 255) continue;  // slow path
+    lut[w] = (sym * 4) | ((adv * 4) << 10) | (pos << 27);
+  }
+  return lut;
+}
+
 ShardSlice shard_slice(const HostLayer& H, int rank, int world, bool replicate) {
   ShardSlice sl;
   const uint32_t rb = replicate ? H.rows : (H.rows + (uint32_t)world - 1) / (uint32_t)world;

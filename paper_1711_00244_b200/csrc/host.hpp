@@ -82,6 +82,35 @@ struct Token { int32_t row, col; uint8_t sym; };
 void build_lane_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, LaneIndex& out,
                       std::vector<Token>* tokens_out = nullptr);
 
+// Merged token stream of the small-batch kernel (k_fc_j, joint.cu; reading
+// C-35): the row's two Huffman code streams interleaved token by token --
+// val code, then its gap code -- so one MSB-first reader and one lookup serve
+// both (a bit permutation of the same codes: the same number of bits).
+// Decode lanes: G per row in Q column groups (group q = G/Q lanes holding the
+// columns [q Kq, (q+1) Kq), so a CTA of group q stages only that slice of x);
+// inside a group the lanes are split by REAL-token count (lane j starts near
+// the group's real token of rank j R_q Q/G), every boundary moved back over
+// padding tokens so that no lane ends with padding (a row never does: padding
+// precedes a real token, C-02).  A lane record = bit offset of its first
+// token from the row start (u16) | (previous column + 1) << 16 (u16).
+struct JointIndex {
+  int G = 1, Q = 1;                // lanes per row; column groups (lanes [q G/Q, (q+1) G/Q) hold columns [q Kq, (q+1) Kq))
+  uint32_t Kq = 0;
+  std::vector<uint32_t> words;     // big-endian u32 words (bit i = bit 31-(i%32) of word i/32), >= 8 words padding
+  std::vector<uint32_t> row_bit;   // nr+1: start bit of each local row (relative to the slice)
+  std::vector<uint32_t> lane;      // nr*G records
+  uint64_t bits = 0;
+  uint32_t max_row_bits = 0;
+};
+// false (nothing built) when a row has >= 2^16 bits or cols > 65535
+bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, JointIndex& out);
+// Joint LUT over the next Lb bits of the merged stream: the leading padding
+// tokens (val symbol 0 with its gap code) and then one real token, when they
+// lie inside the window.  Entry: 4 * val symbol (bits 0-9) | 4 * column
+// advance << 10 (17 bits) | total bits << 27 (5 bits); 0 = the first token is
+// longer than the window (the kernel's slow path decodes it code by code).
+std::vector<uint32_t> build_joint_lut(const HuffCode& val, const HuffCode& gap, int Lb);
+
 // Restart index of the large-batch band kernel: every row split into NI
 // intervals of W columns; per (row, interval) the decoder state before the
 // first token whose column is >= i*W (bit offsets in both streams, previous

@@ -1,0 +1,439 @@
+// Small-batch fused FC kernel on the merged token stream (sm_100a): the
+// decode-bound regime, nominally HBM-bound on the compressed bytes (SURVEY
+// §8(d)).  PAPER.md Alg. 1 lines 4-9, Eq. 1-2.
+//
+// One table lookup per real token:
+//   * the row's val (codebook index) and col_ind (gap) Huffman codes are
+//     resident interleaved token by token (host.hpp JointIndex, reading C-35),
+//     so a lane runs ONE MSB-first reader: a two-word register window refilled
+//     from the row's bits, which a bulk async copy (UBLKCP) staged in shared
+//     memory;
+//   * one lookup of the next jL bits in the joint LUT (shared memory) decodes
+//     the leading padding tokens (val symbol 0, C-04) together with the real
+//     token that follows: 4 x its codebook index, the bits consumed and the
+//     column advance sum(g + 1) (Alg. 1 l.7, reading C-01) as a byte offset
+//     into x; a window whose first token is longer than jL bits yields 0, a
+//     no-op step that leaves the inner loop for a code-by-code slow path
+//     (plain LUTs + canonical tables);
+//   * w = C[sym] from the 32-entry codebook in shared memory (conflict-free:
+//     equal indices broadcast, distinct ones sit in distinct banks; l.8) and
+//     acc += w * x[c] with x staged in shared memory (l.9).
+// Lanes: thread = (row, lane j) of the token-balanced lane split recorded at
+// load (start bit, previous column); no lane ends with padding, so the lookup
+// never decodes past a lane's end.  The G lanes of a row are reduced by a
+// fixed shuffle tree (deterministic).
+// A programmatic dependent launch: the LUT / stream staging runs before
+// griddepcontrol.wait, x (the previous layer's output) after it.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "dev_common.cuh"
+#include "kernels.cuh"
+
+namespace cdn {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kJMaxWarps = 32;
+constexpr int kJMaxCta = 160;  // CTA stream ranges passed in the launch parameters
+
+struct JArgs {
+  const float* x;
+  int ldx;
+  float* y;
+  int ldy;
+  int relu;
+  int B;
+  int Q, GQ, RPW, nw, units;
+  uint32_t sub;       // bytes of one row's staging sub-slot (16-aligned)
+  uint32_t off_x, off_slot;  // dynamic smem offsets (the table blob sits at 0)
+  int xbulk;          // 1: x contiguous (ldx == 1, B == 1) and 16-byte aligned
+  unsigned long long* trace;  // debug (env CDN_J_TRACE): per CTA 8 globaltimer stamps, else null
+  int ncta;           // Q == 1: CTAs whose stream range is in cta[] (the rest read row_bit)
+  uint2 cta[kJMaxCta];  // Q == 1: per CTA (16-byte index of its first row's bits, bytes to stage)
+};
+
+__device__ __forceinline__ void jtrace(const JArgs& A, int ev) {
+  if (A.trace != nullptr && (threadIdx.x & 31) == 0 && threadIdx.x < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + ev] = t;
+  }
+}
+
+// shared-window address of a shared-memory object, computed once (volatile:
+// the compiler would otherwise rematerialise it inside the hot loop)
+static __device__ __forceinline__ uint32_t saddr(const void* p) {
+  uint32_t a;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+  return a;
+}
+static __device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+static __device__ __forceinline__ float ldsf(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+// if (off >= 32) { off -= 32; w0 = w1; w1 = word at sp; sp += 4; } -- the load
+// lands straight in w1 (no temporary the compiler would wait on)
+static __device__ __forceinline__ void refill(uint32_t& w0, uint32_t& w1, uint32_t& off, uint32_t& sp) {
+  asm volatile(
+      "{ .reg .pred p; setp.ge.u32 p, %2, 32; @p mov.b32 %0, %1; @p ld.shared.u32 %1, [%3]; "
+      "@p add.u32 %3, %3, 4; @p sub.u32 %2, %2, 32; }"
+      : "+r"(w0), "+r"(w1), "+r"(off), "+r"(sp));
+}
+
+template <int BS>
+__device__ __forceinline__ void gather_fma(float (&acc)[BS], float w, uint32_t xa) {
+  if constexpr (BS == 1) {
+    acc[0] = fmaf(w, ldsf(xa), acc[0]);
+  } else if constexpr (BS == 2) {
+    float a, b;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(xa));
+    acc[0] = fmaf(w, a, acc[0]);
+    acc[1] = fmaf(w, b, acc[1]);
+  } else {
+    float a, b, c, d;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(xa));
+    acc[0] = fmaf(w, a, acc[0]);
+    acc[1] = fmaf(w, b, acc[1]);
+    acc[2] = fmaf(w, c, acc[2]);
+    acc[3] = fmaf(w, d, acc[3]);
+  }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __grid_constant__ JArgs A) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_w, bar_x;
+  __shared__ __align__(8) uint64_t bar_s[kJMaxWarps];
+  constexpr int LBS = BS == 1 ? 0 : (BS == 2 ? 1 : 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  jtrace(A, 0);
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  const int G = L.G, GQ = A.GQ, q = blockIdx.y;
+  const int rr = lane / GQ, jj = lane - rr * GQ, j = q * GQ + jj;  // row of the warp unit, lane of the row
+  const int xc0 = q * L.jKq, xcols = min(L.jKq, L.cols - xc0);      // this column group's slice of x
+  const int u = blockIdx.x * A.nw + warp;  // warp unit: rows u RPW .. u RPW + RPW - 1
+  const int row = u * A.RPW + rr;
+  const bool ok = u < A.units && row < L.nrows;
+  // lane records first: their loads fly while the bulk copies are set up
+  uint32_t r0 = 0, r1 = 0, rec = 0, nxt = 0;
+  if (ok) {
+    r0 = L.jrow[row];
+    r1 = L.jrow[row + 1];
+    rec = L.jlane[(size_t)row * G + j];
+    if (j + 1 < G) nxt = L.jlane[(size_t)row * G + j + 1];
+  }
+  const bool whole = A.Q == 1 && (int)blockIdx.x < A.ncta;  // one stream copy for the whole CTA
+  if (tid == 0) {
+    mbar_init(&bar_w, 1);
+    mbar_init(&bar_x, 1);
+    for (int w = 0; w < A.nw; ++w) mbar_init(&bar_s[w], 1);
+    mbar_fence_init();
+    if (whole) {  // the CTA's rows are contiguous: their bits in one bulk copy
+      const uint2 c = A.cta[blockIdx.x];
+      mbar_arrive_expect_tx(&bar_s[0], c.y);
+      if (c.y) bulk_g2s(smem + A.off_slot, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)c.x * 16u, c.y, &bar_s[0]);
+    }
+    // every table in one bulk copy (host-built blob in this layout)
+    mbar_arrive_expect_tx(&bar_w, L.jblob);
+    bulk_g2s(smem, L.jlut, L.jblob, &bar_w);
+  }
+  const uint32_t* s_vtab = reinterpret_cast<const uint32_t*>(smem + L.jo_vtab);
+  const uint32_t* s_gtab = reinterpret_cast<const uint32_t*>(smem + L.jo_gtab);
+  const uint16_t* s_vs = reinterpret_cast<const uint16_t*>(smem + L.jo_vs);
+  const uint16_t* s_gs = reinterpret_cast<const uint16_t*>(smem + L.jo_gs);
+
+  const uint32_t lb = ok ? r0 + (rec & 0xffffu) : 0u;                         // lane's bits [lb, le)
+  const uint32_t le = ok ? r0 + (j + 1 < G ? (nxt & 0xffffu) : r1 - r0) : 0u;
+  const int prev = (int)(rec >> 16) - 1;                                      // lane's previous column
+  uint32_t rs, slot_off;  // staged bits start (128-bit aligned) and its shared-memory offset
+  if (whole) {
+    rs = A.cta[blockIdx.x].x * 128u;
+    slot_off = A.off_slot;
+  } else {
+    // per warp: each row's range of this column group [first lane's start, last lane's end)
+    const uint32_t g0 = __shfl_sync(0xffffffffu, lb, rr * GQ);
+    const uint32_t g1 = __shfl_sync(0xffffffffu, le, rr * GQ + GQ - 1);
+    rs = (g0 >> 7) << 7;
+    slot_off = A.off_slot + ((uint32_t)warp * A.RPW + rr) * A.sub;
+    const uint32_t bytes = ok ? (((g1 + 127) >> 7) - (g0 >> 7)) * 16u + 16u : 0u;
+    uint32_t tot = jj == 0 ? bytes : 0u;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    __syncthreads();  // the barriers are initialised
+    if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], tot);
+    __syncwarp();
+    if (jj == 0 && bytes)
+      bulk_g2s(smem + slot_off, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)(g0 >> 7) * 16u, bytes,
+               &bar_s[warp]);
+  }
+  jtrace(A, 1);
+
+  // ---- activations (after the producer of x finished)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  jtrace(A, 2);
+  float* xs = reinterpret_cast<float*>(smem + A.off_x);
+  const int K = xcols;
+  if (A.xbulk) {
+    const int nb = (K * 4) & ~15;
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar_x, (uint32_t)nb);
+      if (nb) bulk_g2s(xs, A.x + xc0, (uint32_t)nb, &bar_x);
+    }
+    for (int i = nb / 4 + tid; i < K; i += blockDim.x) xs[i] = A.x[xc0 + i];
+  } else {
+    if (tid == 0) mbar_arrive(&bar_x);
+    // eight loads in flight per thread before their stores (small CTAs would
+    // otherwise pay one memory latency per element)
+    const int n = K * BS, step = blockDim.x;
+    for (int i0 = tid; i0 < n; i0 += 8 * step) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * step, c = i >> LBS, b = i & (BS - 1);
+        v[k] = (i < n && b < A.B) ? A.x[(size_t)(xc0 + c) * A.ldx + b] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i0 + k * step < n) xs[i0 + k * step] = v[k];
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar_w, 0);
+  mbar_wait(&bar_x, 0);
+  jtrace(A, 3);
+
+  const uint32_t sb = saddr(smem);
+  const uint32_t lut = sb;
+  const uint32_t cbase = sb + L.jo_cb;
+  const int jsh = 32 - L.jL;
+  const int vsh = 32 - L.Lv, gsh = 32 - L.Lg;
+  const uint32_t xbase = sb + A.off_x;
+  if (u < A.units) {
+    mbar_wait(&bar_s[whole ? 0 : warp], 0);
+    jtrace(A, 4);
+    int nrem = (int)lb - (int)le;  // -(bits left in the lane)
+    uint32_t sp = sb + slot_off + ((lb - rs) >> 5) * 4u;  // (ok lanes only: the others never load)
+    uint32_t off = lb & 31;
+    uint32_t w0 = 0, w1 = 0;
+    if (nrem < 0) {
+      w0 = lds32(sp);
+      w1 = lds32(sp + 4);
+    }
+    sp += 8;
+    uint32_t xa = xbase + (uint32_t)((prev - xc0) * 4 * BS);
+    float acc[BS];
+#pragma unroll
+    for (int b = 0; b < BS; ++b) acc[b] = 0.f;
+    while (nrem < 0) {  // one lookup per (padding run +) real token
+      const uint32_t win = __funnelshift_l(w1, w0, off);
+      uint32_t e = lds32(lut + ((win >> jsh) << 2));
+      if (e == 0) {
+        // slow path, taken by this lane alone (the others wait a few dozen
+        // instructions, not until their lanes end): one token whose codes did
+        // not fit the window, code by code through the plain LUTs (canonical
+        // tables for codes longer than those)
+        const uint32_t ev = lds32(sb + L.jo_vlut + ((win >> vsh) << 2));
+        uint32_t vl, vsym;
+        if (ev) { vl = ev >> 16; vsym = ev & 0xffffu; }
+        else { const uint32_t r = slow_sym(win, L.Lv + 1, s_vtab, s_vs, L.vmax); vl = r >> 16; vsym = r & 0xffffu; }
+        off += vl;
+        nrem += (int)vl;
+        refill(w0, w1, off, sp);
+        const uint32_t win2 = __funnelshift_l(w1, w0, off);
+        const uint32_t eg = lds32(sb + L.jo_glut + ((win2 >> gsh) << 2));
+        uint32_t gl, gsym;
+        if (eg) { gl = eg >> 16; gsym = eg & 0xffffu; }
+        else { const uint32_t r = slow_sym(win2, L.Lg + 1, s_gtab, s_gs, L.gmax); gl = r >> 16; gsym = r & 0xffffu; }
+        off += gl;
+        nrem += (int)gl;
+        refill(w0, w1, off, sp);
+        // an entry as the LUT would have built it, both codes already consumed
+        e = (vsym * 4u) | (((gsym + 1) * 4u) << 10);
+      }
+      off += e >> 27;
+      nrem += (int)(e >> 27);
+      refill(w0, w1, off, sp);
+      const uint32_t ca = e & 0x3fcu;
+      const float w = ldsf(cbase + ca);
+      xa += ((e & 0x07fffc00u) >> 10) << LBS;
+      if (ca) gather_fma<BS>(acc, w, xa);
+    }
+    // lanes of a row: fixed shuffle tree (deterministic)
+#pragma unroll
+    for (int b = 0; b < BS; ++b)
+      for (int o = GQ >> 1; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o, GQ);
+    if (A.Q == 1) {
+      if (jj == 0 && row < L.nrows) {
+        const float v = L.bias[row];
+#pragma unroll
+        for (int b = 0; b < BS; ++b) {
+          if (b < A.B) {
+            float o = acc[b] + v;
+            if (A.relu) o = fmaxf(o, 0.f);
+            A.y[(size_t)row * A.ldy + b] = o;
+          }
+        }
+      }
+    } else {
+      // column groups: the last of the unit's Q CTAs adds the Q partial sums in
+      // group order (deterministic) and applies bias / ReLU
+      if (jj == 0 && row < L.nrows) {
+#pragma unroll
+        for (int b = 0; b < BS; ++b) __stcg(&L.jpart[((size_t)q * L.nrows + row) * BS + b], acc[b]);
+      }
+      __threadfence();
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(&L.jctr[u], 1) == A.Q - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        if (jj == 0 && row < L.nrows) {
+          const float v = L.bias[row];
+#pragma unroll
+          for (int b = 0; b < BS; ++b) {
+            if (b < A.B) {
+              float sum = 0.f;
+              for (int qq = 0; qq < A.Q; ++qq) sum += __ldcg(&L.jpart[((size_t)qq * L.nrows + row) * BS + b]);
+              float o = sum + v;
+              if (A.relu) o = fmaxf(o, 0.f);
+              A.y[(size_t)row * A.ldy + b] = o;
+            }
+          }
+        }
+        if (lane == 0) L.jctr[u] = 0;
+      }
+    }
+    jtrace(A, 5);
+  }
+  __syncthreads();
+  jtrace(A, 6);
+}
+
+}  // namespace
+
+bool j_supported(const FcDev& L) { return L.jw && L.jlut && L.ncb <= 32 && L.G <= 32; }
+
+JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
+  JPlan p;
+  if (!j_supported(L) || B < 1 || B > 4 || L.nrows <= 0) return p;
+  p.BS = B <= 1 ? 1 : (B <= 2 ? 2 : 4);
+  p.Q = L.jQ;
+  p.GQ = L.G / p.Q;
+  p.RPW = 32 / p.GQ;
+  p.units = (L.nrows + p.RPW - 1) / p.RPW;
+  // one CTA per SM (Q column groups of a row block side by side), every
+  // warp one unit of RPW rows
+  const int rb = std::max(1, num_sms / p.Q);
+  auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
+  const size_t off_x = al(L.jblob);
+  const size_t off_slot = al(off_x + (size_t)4 * p.BS * L.jKq);
+  for (p.nw = std::min(kJMaxWarps, std::max(1, (p.units + rb - 1) / rb)); p.nw >= 1; --p.nw) {
+    p.nrb = (p.units + p.nw - 1) / p.nw;
+    p.cta.clear();
+    size_t slot = (size_t)p.nw * p.RPW * L.jsub;  // per-warp row slots
+    if (p.Q == 1 && row_bit && p.nrb <= kJMaxCta) {
+      // the CTA's rows are contiguous: one range of the merged stream
+      size_t mx = 0;
+      for (int c = 0; c < p.nrb; ++c) {
+        const int r0 = c * p.nw * p.RPW, r1 = std::min(L.nrows, (c + 1) * p.nw * p.RPW);
+        const uint32_t a = row_bit[r0] >> 7, b = (row_bit[r1] + 127) >> 7;
+        const uint32_t bytes = (b - a) * 16u + 16u;  // + one word of read-ahead
+        p.cta.push_back(make_uint2(a, bytes));
+        mx = std::max<size_t>(mx, bytes);
+      }
+      slot = mx;
+    }
+    p.off_x = (uint32_t)off_x;
+    p.off_slot = (uint32_t)off_slot;
+    p.sub = L.jsub;
+    p.smem = off_slot + slot;
+    if (p.smem <= 227 * 1024 - 1024) break;
+  }
+  p.ok = p.nw >= 1 && p.smem <= 227 * 1024 - 1024 && (p.Q == 1 || (L.jpart && L.jctr));
+  return p;
+}
+
+cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
+                        cudaStream_t s) {
+  if (!p.ok) return cudaErrorInvalidValue;
+  JArgs a{};
+  a.x = x;
+  a.ldx = ldx;
+  a.y = y;
+  a.ldy = ldy;
+  a.relu = relu;
+  a.B = B;
+  a.Q = p.Q;
+  a.GQ = p.GQ;
+  a.RPW = p.RPW;
+  a.nw = p.nw;
+  a.units = p.units;
+  a.sub = p.sub;
+  a.off_x = p.off_x;
+  a.off_slot = p.off_slot;
+  a.ncta = (int)p.cta.size();
+  for (size_t i = 0; i < p.cta.size() && i < (size_t)kJMaxCta; ++i) a.cta[i] = p.cta[i];
+  static unsigned long long* trace = nullptr;
+  static const char* trace_path = getenv("CDN_J_TRACE");
+  const size_t ntr = (size_t)p.nrb * p.Q * 8;
+  static size_t trace_n = 0;
+  if (trace_path && trace_n < ntr) {
+    if (trace) cudaFree(trace);
+    if (cudaMalloc(&trace, ntr * sizeof(unsigned long long)) != cudaSuccess) return cudaErrorMemoryAllocation;
+    trace_n = ntr;
+  }
+  if (trace_path) cudaMemsetAsync(trace, 0, ntr * sizeof(unsigned long long), s);
+  a.trace = trace_path ? trace : nullptr;
+  a.xbulk = (p.BS == 1 && ldx == 1 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && L.jKq % 4 == 0) ? 1 : 0;
+  cudaError_t e = cudaSuccess;
+  static thread_local size_t set_smem[3] = {0, 0, 0};
+  auto run = [&](auto kern, int bi) {
+    if (p.smem > 48 * 1024 && p.smem > set_smem[bi]) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      if (e != cudaSuccess) return;
+      set_smem[bi] = p.smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p.nrb, (unsigned)p.Q);
+    cfg.blockDim = dim3((unsigned)(p.nw * 32));
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // LUT / stream staging overlaps the producer of x
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, L, a);
+  };
+  ktimer_begin("k_fc_j", s);
+  if (p.BS == 1) run(k_fc_j<1>, 0);
+  else if (p.BS == 2) run(k_fc_j<2>, 1);
+  else run(k_fc_j<4>, 2);
+  if (e == cudaSuccess) e = launched();
+  ktimer_end("k_fc_j", s);
+  if (e == cudaSuccess && trace_path) {  // debug only: append this launch's stamps
+    std::vector<unsigned long long> h(ntr);
+    e = cudaMemcpyAsync(h.data(), trace, ntr * sizeof(h[0]), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (FILE* fp = fopen(trace_path, "ab")) {
+      const unsigned long long n = ntr;
+      fwrite(&n, sizeof(n), 1, fp);
+      fwrite(h.data(), sizeof(h[0]), h.size(), fp);
+      fclose(fp);
+    }
+  }
+  return e;
+}
+
+}  // namespace cdn

@@ -3,6 +3,7 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <vector>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -83,7 +84,34 @@ struct FcDev {
   const uint32_t* msv = nullptr;
   const uint32_t* msg = nullptr;
   int msLv = 12, msLg = 12;
+  float tc_wsc = 1.f;                // tensor-core path: power-of-two weight scale of the fp16 split
+  // merged-stream small-batch kernel (joint.cu; host.hpp JointIndex): words,
+  // row start bits (nrows + 1), token-balanced lane records (nrows * G), joint LUT
+  const uint32_t* jw = nullptr;
+  const uint32_t* jrow = nullptr;
+  const uint32_t* jlane = nullptr;
+  const uint32_t* jlut = nullptr;   // the kernel's tables as one blob, laid out as in shared memory:
+  int jL = 12;                       // [joint LUT 4<<jL | vlut | glut | vtab | gtab | vsorted | gsorted | codebook]
+  uint32_t jo_vlut = 0, jo_glut = 0, jo_vtab = 0, jo_gtab = 0, jo_vs = 0, jo_gs = 0, jo_cb = 0, jblob = 0;
+  uint32_t jsub = 0;                 // bytes of one row's staging sub-slot
+  int jQ = 1, jKq = 0;               // column groups of the lane split, group width (columns)
+  float* jpart = nullptr;            // column-group partial sums [Q][nrows][BS]
+  int* jctr = nullptr;               // per-warp-unit arrival counters (Q > 1), zero between calls
 };
+
+// Launch plan of the merged-stream kernel for one (layer, B <= 4).
+struct JPlan {
+  bool ok = false;
+  int BS = 1, Q = 1, GQ = 1, RPW = 1, units = 0, nw = 1, nrb = 0;
+  uint32_t sub = 0, off_x = 0, off_slot = 0;
+  size_t smem = 0;
+  std::vector<uint2> cta;  // Q == 1: per CTA (16-byte index of its rows' first bits, bytes to stage)
+};
+bool j_supported(const FcDev& L);
+// row_bit: the host copy of L.jrow (nrows + 1), for the per-CTA stream ranges
+JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit);
+cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
+                        cudaStream_t s);
 
 // Launch plan of the band kernel for one (layer, B, x) — ok == false means the
 // inputs do not meet its alignment rules (the small-batch kernel then runs).
@@ -95,8 +123,8 @@ struct BandPlan {
 BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms);
 cudaError_t launch_fc_band(const FcDev& L, const BandPlan& p, const float* x, int ldx, int B, float* y, int ldy,
                            int relu, float* ws, int* tctr, cudaStream_t s);
-// Tensor-core FC kernel (tc.cu, B >= ~128): decode W tiles into shared memory,
-// 3-pass bf16 split tcgen05 contraction.  xh/xl: bf16 scratch [B][ldk].
+// Tensor-core FC kernel (tc.cu, B >= ~16): decode W tiles into tensor memory,
+// 3-pass fp16 split (per-image / per-layer power-of-two scales) tcgen05 contraction.
 struct TcPlan {
   bool ok = false;
   int nbt = 1, nrt = 1, nkt = 0, ldk = 0, tiles = 0, grid = 0, mpt = 1;  // mpt: max CTAs per tile
@@ -109,8 +137,11 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms);
 // list decoder of the tensor-core path (k_tc_list[_ms]): fills L.tlist from the
 // compressed streams; launch_fc_tc reads it (the caller orders the two)
 cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s);
+// xh / xl: fp16 hi / lo scratch [B][ldk]; scw: tc_scale_floats(B) floats (per-image split
+// scales); xctr: >= B ints, zero at allocation (the kernels leave them zero)
+size_t tc_scale_floats(int B);
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s,
+                         uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
                          bool x_image_major = false, bool y_image_major = false);  // x: [K][ldx] feature-major, or [B][ldx] image-major
 
 // Small-batch multi-symbol kernel (B <= 8; r <= 5, k <= 4, 32-bit lane records).

@@ -16,12 +16,16 @@
 //
 // At B >= 128 the sparse CUDA-core kernel is bound by one shared-memory load
 // per FMA; the tensor cores run the DENSE tile product 25x faster per flop, so
-// even at 4% density they win.  fp32 fidelity with bf16 tensor cores: every
-// weight (codebook value) and activation is split into hi = bf16(v) and
-// lo = bf16(v - hi); D += Whi*Xhi + Whi*Xlo + Wlo*Xhi (three UMMAs per K step;
-// the dropped Wlo*Xlo term and the two splits are each <= 2^-16 relative per
-// product).
-//
+// even at 4% density they win.  fp32 fidelity with 16-bit tensor cores: every
+// weight (codebook value) and activation is split into two fp16 halves,
+// hi = fp16(v s) and lo = fp16(v s - hi), after scaling by a power of two s
+// (per layer for W, per image for X: max |v| s in [2^14, 2^15), so hi never
+// overflows and lo stays normal for every value within 2^-17 of the maximum);
+// D += Whi*Xhi + Whi*Xlo + Wlo*Xhi (three UMMAs per K step, kind::f16 with
+// fp16 operands), and the epilogue multiplies by 1 / (s_W s_b) (exact).  A
+// 2-way fp16 split keeps 22 significant bits; each product is within ~2^-21
+// relative of the fp32 product (the dropped lo*lo term and the two splits),
+// against 2^-15 for a bf16 split.
 //   unit = (128 output rows, 256 images, K range), split in two K halves
 //   ("streams") expanded concurrently; per 64-column K tile:
 //     * 4 EXPAND warps per stream, one lane per row (= TMEM lane): the lane
@@ -40,6 +44,7 @@
 #include <cstdlib>
 #include <vector>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "dev_common.cuh"
 #include "kernels.cuh"
@@ -75,6 +80,8 @@ struct TcArgs {
   long W;                     // total tile steps = tiles * nkt (stream-K)
   unsigned long long* trace;    // debug (env CDN_TC_TRACE): CTA 0 event clocks [event][256], else null
   int yt;                       // 1: y image-major [B][ldy] (the class scores of the last layer), else [rows][ldy]
+  const float* xsc;             // [B] per-image power-of-two scales of the fp16 split (k_xscale_*)
+  float winv;                   // 1 / the layer's weight scale
 };
 
 __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
@@ -213,10 +220,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
   {
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int i = tid; i < L.ncb; i += nt) {
-      const float w = L.codebook[i];
-      const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-      const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
-      s_cbs[i] = (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+      const float w = L.codebook[i] * L.tc_wsc;  // |w s_W| < 2^15 (power-of-two scale: exact)
+      const __half hi = __float2half_rn(w);
+      const __half lo = __float2half_rn(w - __half2float(hi));
+      s_cbs[i] = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
     }
     if (tid == 0) {
       for (int s = 0; s < kXStages; ++s) {
@@ -281,8 +288,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
   } else if (warp == 1) {
     // --------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) |
-                             ((uint32_t)(kTM >> 4) << 24);
+      // kind::f16: D fp32 (bits 4-5 = 1), A and B fp16 (bits 7-9, 10-12 = 0), K-major, N / 8, M / 16
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
       uint32_t xc = 0, gq[kStreams] = {0, 0}, uc = 0;
       TUnit t;
       for (int pc = 0; cta_piece(a, blockIdx.x, pc, t); ++pc, ++uc) {
@@ -480,6 +487,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
         if (!has) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        } else {
+          // undo the fp16 split's scales: D / (s_W s_b), exact (powers of two)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= a.winv / __ldg(a.xsc + min(b0 + c + i, a.B - 1));
         }
         if (whole) {
           if (row < L.wrows) {
@@ -521,14 +532,81 @@ __global__ void __launch_bounds__(kTThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
-// X fp32 feature-major [K][ldx] -> bf16 hi / lo image-major [B][ldk] (K contiguous).
+// Per-image power-of-two scale of the fp16 split: s = 2^e with m s in
+// [2^14, 2^15) for m = max_k |x[b][k]| (m == 0, inf or NaN: s = 1).
+__device__ __forceinline__ float pow2_scale(float m) {
+  if (!(m > 0.f) || isinf(m)) return 1.f;
+  int E;
+  frexpf(m, &E);  // m = f 2^E, f in [0.5, 1)
+  return ldexpf(1.f, max(-120, min(120, 15 - E)));
+}
+
+// max |x| per image over a K chunk (blockIdx.y of KS) -> part[ks][b]; the last
+// block of an image (arrival counter, reset by it) writes its scale sc[b].
+// Feature-major x [K][ldx]: block = 32 images x 8 row groups; image-major x
+// [B][ldx]: block = one image.
+constexpr int kScaleChunks = 8;
+__device__ __forceinline__ void scale_finish(float m, int b, int B, int nparts, float* part, int* ctr, float* sc) {
+  part[(size_t)blockIdx.y * B + b] = m;
+  __threadfence();
+  if (atomicAdd(&ctr[b], 1) == nparts - 1) {
+    __threadfence();
+    float mm = 0.f;
+    for (int i = 0; i < nparts; ++i) mm = fmaxf(mm, __ldcg(&part[(size_t)i * B + b]));
+    sc[b] = pow2_scale(mm);
+    ctr[b] = 0;
+  }
+}
+__global__ void __launch_bounds__(256) k_xscale_cols(const float* __restrict__ x, int K, int ldx, int B,
+                                                     float* part, int* ctr, float* sc) {
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, b = blockIdx.x * 32 + tx;
+  const int kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc, k1 = min(K, k0 + kc);
+  float m = 0.f;
+  if (b < B)
+    for (int k = k0 + ty; k < k1; k += 8) m = fmaxf(m, fabsf(__ldg(x + (size_t)k * ldx + b)));
+  red[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0 && b < B) {
+    for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i][tx]);
+    scale_finish(m, b, B, gridDim.y, part, ctr, sc);
+  }
+}
+__global__ void __launch_bounds__(256) k_xscale_rows(const float* __restrict__ x, int K, int ldx, int B,
+                                                     float* part, int* ctr, float* sc) {
+  __shared__ float red[8];
+  const int b = blockIdx.x;
+  const int kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc, k1 = min(K, k0 + kc);
+  const float* p = x + (size_t)b * ldx;
+  float m = 0.f;
+  for (int k = k0 + (int)threadIdx.x; k < k1; k += 256) m = fmaxf(m, fabsf(__ldg(p + k)));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i]);
+    scale_finish(m, b, B, gridDim.y, part, ctr, sc);
+  }
+}
+
+// fp16 hi / lo of v * s (s a power of two: |v s| < 2^15), packed in pairs
+__device__ __forceinline__ void split_pair(float v0, float v1, float s, uint32_t& h, uint32_t& l) {
+  v0 *= s;
+  v1 *= s;
+  const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+  const __half l0 = __float2half_rn(v0 - __half2float(h0)), l1 = __float2half_rn(v1 - __half2float(h1));
+  h = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+  l = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+}
+
+// X fp32 feature-major [K][ldx] -> fp16 hi / lo of x s_b, image-major [B][ldk] (K contiguous).
 // Tile = 64 k x 32 images: coalesced 128-byte row loads, then each thread
 // converts 8 consecutive k of one image and writes them as one 16-byte store
 // per half (8 lanes cover a 128-byte run of an image row).
 constexpr int kSplitK = 64, kSplitB = 32;
 __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, int K, int ldx, int B,
-                                                 __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl,
-                                                 int ldk) {
+                                                 uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int ldk,
+                                                 const float* __restrict__ xsc) {
   asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
   __shared__ float tile[kSplitK][kSplitB + 1];
   const int k0 = blockIdx.x * kSplitK, b0 = blockIdx.y * kSplitB;
@@ -542,25 +620,19 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
   const int c = threadIdx.x & 7, bl = threadIdx.x >> 3;  // k chunk (8 values), image
   const int b = b0 + bl, k = k0 + 8 * c;
   if (b >= B || k >= ldk) return;
+  const float sb = xsc[b];
   uint32_t h[4], l[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float v0 = tile[8 * c + 2 * i][bl], v1 = tile[8 * c + 2 * i + 1][bl];
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(v0), h1 = __float2bfloat16_rn(v1);
-    const __nv_bfloat16 l0 = __float2bfloat16_rn(v0 - __bfloat162float(h0));
-    const __nv_bfloat16 l1 = __float2bfloat16_rn(v1 - __bfloat162float(h1));
-    h[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-    l[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-  }
-  __nv_bfloat16* ph = xh + (size_t)b * ldk + k;
-  __nv_bfloat16* pl = xl + (size_t)b * ldk + k;
+  for (int i = 0; i < 4; ++i) split_pair(tile[8 * c + 2 * i][bl], tile[8 * c + 2 * i + 1][bl], sb, h[i], l[i]);
+  uint16_t* ph = xh + (size_t)b * ldk + k;
+  uint16_t* pl = xl + (size_t)b * ldk + k;
   if (k + 8 <= ldk) {  // ldk % 8 == 0 and k % 8 == 0: 16-byte aligned
     *reinterpret_cast<uint4*>(ph) = make_uint4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<uint4*>(pl) = make_uint4(l[0], l[1], l[2], l[3]);
   } else {
     for (int i = 0; i < 8 && k + i < ldk; ++i) {
-      ph[i] = __ushort_as_bfloat16((unsigned short)(h[i >> 1] >> (16 * (i & 1))));
-      pl[i] = __ushort_as_bfloat16((unsigned short)(l[i >> 1] >> (16 * (i & 1))));
+      ph[i] = (uint16_t)(h[i >> 1] >> (16 * (i & 1)));
+      pl[i] = (uint16_t)(l[i >> 1] >> (16 * (i & 1)));
     }
   }
 }
@@ -633,12 +705,12 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
   }
 }
 
-// X fp32 image-major [B][ldx] (the public infer input) -> bf16 hi / lo [B][ldk]:
-// a plain streaming conversion, 8 consecutive k per thread (two 16-byte loads
-// when aligned, one 16-byte store per half).
+// X fp32 image-major [B][ldx] (the public infer input) -> fp16 hi / lo of x s_b,
+// [B][ldk]: a plain streaming conversion, 8 consecutive k per thread (two
+// 16-byte loads when aligned, one 16-byte store per half).
 __global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x, int K, int ldx, int B,
-                                                    __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl,
-                                                    int ldk, int vec) {
+                                                    uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int ldk,
+                                                    int vec, const float* __restrict__ xsc) {
   asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
   const int nk8 = ldk / 8;
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -653,15 +725,10 @@ __global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x,
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = k + j < K ? p[j] : 0.f;
   }
+  const float sb = xsc[b];
   uint32_t h[4], l[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(v[2 * j]), h1 = __float2bfloat16_rn(v[2 * j + 1]);
-    const __nv_bfloat16 l0 = __float2bfloat16_rn(v[2 * j] - __bfloat162float(h0));
-    const __nv_bfloat16 l1 = __float2bfloat16_rn(v[2 * j + 1] - __bfloat162float(h1));
-    h[j] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-    l[j] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-  }
+  for (int j = 0; j < 4; ++j) split_pair(v[2 * j], v[2 * j + 1], sb, h[j], l[j]);
   *reinterpret_cast<uint4*>(xh + (size_t)b * ldk + k) = make_uint4(h[0], h[1], h[2], h[3]);
   *reinterpret_cast<uint4*>(xl + (size_t)b * ldk + k) = make_uint4(l[0], l[1], l[2], l[3]);
 }
@@ -920,6 +987,8 @@ bool list_fold_forced() {
 
 }  // namespace
 
+size_t tc_scale_floats(int B) { return (size_t)B * (kScaleChunks + 1); }
+
 bool tc_supported(const FcDev& L) {
   return L.tivg && L.tivm && L.tNI > 0 && L.sNI > 0 && L.tbase && L.troff && L.tlist && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
          L.Lf == kFoldLutBits && L.Lg <= kLutMaxBits;
@@ -1002,25 +1071,31 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
 }
 
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-                         __nv_bfloat16* xh, __nv_bfloat16* xl, float* ws, cudaStream_t s, bool x_image_major,
-                         bool y_image_major) {
+                         uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
+                         bool x_image_major, bool y_image_major) {
+  // per-image scales of the fp16 split: scw = [B scales | kScaleChunks x B
+  // partial maxima]; xctr: >= B arrival counters, zero between calls
+  float* xsc = scw;
+  float* xpart = scw + (size_t)B;
   ktimer_begin("k_split_x", s);
   if (x_image_major) {
+    k_xscale_rows<<<dim3((unsigned)B, 4), 256, 0, s>>>(x, L.wcols, ldx, B, xpart, xctr, xsc);
     const long n = (long)B * (p.ldk / 8);
     const int vec = (ldx % 4) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk, vec);
+    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk, vec, xsc);
   } else {
+    k_xscale_cols<<<dim3((unsigned)((B + 31) / 32), kScaleChunks), 256, 0, s>>>(x, L.wcols, ldx, B, xpart, xctr, xsc);
     dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
-    k_split_x<<<sg, 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk);
+    k_split_x<<<sg, 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk, xsc);
   }
-  cudaError_t e = launched();
+  cudaError_t e = launched(2);
   ktimer_end("k_split_x", s);
   if (e != cudaSuccess) return e;
   CUtensorMap th, tl;
-  e = encode_tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xh, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
+  e = encode_tmap_2d(&th, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, xh, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
                      kTK, (uint32_t)p.tn, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
-  e = encode_tmap_2d(&tl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xl, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
+  e = encode_tmap_2d(&tl, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, xl, (uint64_t)p.ldk, (uint64_t)B, (uint64_t)p.ldk * 2,
                      kTK, (uint32_t)p.tn, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
   static bool attr_set = false;
@@ -1039,7 +1114,7 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   }
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
   TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr,
-           y_image_major ? 1 : 0};
+           y_image_major ? 1 : 0, xsc, 1.0f / L.tc_wsc};
   ktimer_begin("k_fc_tc", s);
   {
     cudaLaunchConfig_t cfg = {};

@@ -119,8 +119,9 @@ def check_forward(torch, dev, m, c, bias, a, relu):
     kmax = max(1, int(c.row_tokens.max()))
     elem = (np.abs(y - ref) / np.maximum(scale, 1e-30)).max()
     # fp32 summation bound gamma_n; at B >= 16 the default policy may pick the
-    # split-bf16 tensor-core kernel (products within 2^-15)
-    split = 2.0 ** -15 if a.shape[0] >= 16 else 0.0
+    # fp16-split tensor-core kernel (each product within ~2^-21 relative,
+    # DESIGN.md §9)
+    split = 2.0 ** -20 if a.shape[0] >= 16 else 0.0
     assert elem <= 2 * kmax * 2.0 ** -24 + split + 1e-12, elem
     return e
 
@@ -269,7 +270,7 @@ def test_paper_variants_all_kernels(torch_dev, quantizer, k, d, B, policy):
     m = make_model(torch, buf, relu=True)
     m.set_kernel_policy(*policy)
     a = synth.fc_inputs(3000, B, 3)
-    check_forward_sparse(torch, dev, m, c, v, a, relu=True, split_bf16=policy[1] == 1)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=True, split_tc=policy[1] == 1)
     m.close()
 
 
@@ -300,7 +301,7 @@ def test_blocked_container_forward(torch_dev, rows, cols, bh, bw, B):
     m = make_model(torch, buf, relu=True)
     assert m.kernel_name(0, B) == "k_fc_tc"
     a = synth.fc_inputs(cols, B, 5)
-    check_forward_sparse(torch, dev, m, c, v, a, relu=True, split_bf16=True)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=True, split_tc=True)
     if rows * cols <= 512 * 1024 and B == 37:   # and the paper's Alg. 2 itself, step by step
         y = gpu_forward(torch, dev, m, a, rows)
         ref = infer.fc_forward_blocked(c.layer, a, v, apply_relu=True)
@@ -507,7 +508,7 @@ def sparse_q(c):
     return sp.csr_matrix((vals, (r, col)), shape=c.mask.shape)
 
 
-def check_forward_sparse(torch, dev, m, c, bias, a, relu, split_bf16=False):
+def check_forward_sparse(torch, dev, m, c, bias, a, relu, split_tc=False):
     y = gpu_forward(torch, dev, m, a, c.layer.rows)
     Wq = sparse_q(c)
     ref = infer.fc_forward(Wq, a, bias, apply_relu=relu)
@@ -517,9 +518,9 @@ def check_forward_sparse(torch, dev, m, c, bias, a, relu, split_bf16=False):
     scale = infer.fc_abs_scale(Wq, a, bias)
     kmax = max(1, int(c.row_tokens.max()))
     elem = (np.abs(y - ref) / np.maximum(scale, 1e-30)).max()
-    # fp32 accumulation bound; the tensor-core kernel adds the 3-pass bf16 split
-    # error (each product within 2^-15 relative)
-    bound = 2 * kmax * 2.0 ** -24 + (2.0 ** -15 if split_bf16 else 0.0) + 1e-12
+    # fp32 accumulation bound; the tensor-core kernel adds the fp16-split
+    # error (each product within ~2^-21 relative)
+    bound = 2 * kmax * 2.0 ** -24 + (2.0 ** -20 if split_tc else 0.0) + 1e-12
     assert elem <= bound, elem
     return e
 
@@ -665,7 +666,7 @@ def test_tc_forward_configs(torch_dev, cfg, i, B):
     m.set_kernel_policy(1, 1)
     _, v = synth.fc_weights(spec, synth.CONFIGS[cfg].seed)
     a = synth.fc_inputs(spec.cols, B, synth.CONFIGS[cfg].seed)
-    check_forward_sparse(torch, dev, m, c, v, a, relu=spec.relu, split_bf16=True)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=spec.relu, split_tc=True)
 
 
 @pytest.mark.parametrize("name,rows,cols,d,r,k,scale", EDGE)
@@ -677,4 +678,4 @@ def test_tc_edge_fixtures(torch_dev, name, rows, cols, d, r, k, scale):
     m = make_model(torch, buf)
     m.set_kernel_policy(1, 1)
     a = synth.random_activations(cols, 36, seed=99)
-    check_forward_sparse(torch, dev, m, c, v, a, relu=False, split_bf16=True)
+    check_forward_sparse(torch, dev, m, c, v, a, relu=False, split_tc=True)

@@ -3,6 +3,8 @@ import itertools
 import math
 import random
 
+import os
+
 import numpy as np
 import pytest
 
@@ -81,14 +83,65 @@ def test_pool_and_lrn_special_cases():
     assert (infer.lrn(np.zeros((1, 2, 2, 8))) == 0).all()
 
 
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _golden(name):
+    rows = {}
+    for line in open(os.path.join(GOLDEN, name)):
+        line = line.split("#")[0].strip()
+        if line:
+            k, *v = line.split()
+            rows[k] = [float(t) for t in v]
+    return rows
+
+
+def test_lrn_hand_computed_cases():
+    """tests/golden/lrn_maxpool_hand.txt: closed-form LRN values that pin the
+    window (+-2 channels, clipped at the channel edges, no wrap-around), the
+    alpha/n scaling, beta and k of reading C-20."""
+    g = _golden("lrn_maxpool_hand.txt")
+    for case in ("lrnA", "lrnB"):
+        a = np.array(g[case + "_in"]).reshape(1, 1, 1, -1)
+        got = infer.lrn(a).ravel()
+        assert np.allclose(got, g[case + "_out"], rtol=1e-12, atol=0), (case, got)
+    # the same pixel repeated over a 2x3 image and a batch of 2: LRN is per pixel
+    a = np.tile(np.array(g["lrnA_in"]), (2, 2, 3, 1))
+    assert np.allclose(infer.lrn(a), np.tile(np.array(g["lrnA_out"]), (2, 2, 3, 1)), rtol=1e-12)
+
+
+def test_maxpool_hand_computed_case():
+    """3x3 / stride 2 max-pool of a non-constant 5x5x2 image (golden file):
+    window size, stride and the no-padding output size 2x2."""
+    g = _golden("lrn_maxpool_hand.txt")
+    h, w = np.meshgrid(np.arange(5), np.arange(5), indexing="ij")
+    x = np.stack([5 * h + w, -(5 * h + w)], axis=-1).astype(np.float64)[None]
+    y = infer.maxpool(x, 3, 2)
+    assert y.shape == (1, 2, 2, 2)
+    assert np.array_equal(y[0, :, :, 0].ravel(), g["pool_c0"])
+    assert np.array_equal(y[0, :, :, 1].ravel(), g["pool_c1"])
+    # batch of two distinct images: each pooled on its own
+    x2 = np.concatenate([x, x + 100.0])
+    y2 = infer.maxpool(x2, 3, 2)
+    assert np.array_equal(y2[1], y[0] + 100.0)
+
+
+def test_fc_abs_scale_hand_computed():
+    """sum_j |W_ij a_j| + |v_i| on a 2x2 example worked by hand:
+    row 0: |1*1| + |-2*-1| + |0.5| = 3.5; row 1: |0| + |3*-1| + |-0.25| = 3.25."""
+    W = np.array([[1.0, -2.0], [0.0, 3.0]])
+    a = np.array([[1.0, -1.0]])
+    v = np.array([0.5, -0.25])
+    assert np.array_equal(infer.fc_abs_scale(W, a, v), [[3.5, 3.25]])
+    import scipy.sparse as sp
+    assert np.array_equal(infer.fc_abs_scale(sp.csr_matrix(W), a, v), [[3.5, 3.25]])
+
+
 def test_table4_memory_column():
     """P:L584-596 Table 4 'Memory (MB)' = OUT(i,B) = 4 B x elements x B, in MiB,
-    reproduced to the printed 2 decimals for all 13 layers at B=16 and B=256.
-    Pins the C-19 conv/pool geometry."""
-    table4 = {"conv1": (17.72, 283.59), "norm1": (17.72, 283.59), "pool1": (4.27, 68.34),
-              "conv2": (11.39, 182.25), "norm2": (11.39, 182.25), "pool2": (2.64, 42.25),
-              "conv3": (3.96, 63.38), "conv4": (3.96, 63.38), "conv5": (2.64, 42.25),
-              "pool5": (0.56, 9.00), "fc6": (0.25, 4.00), "fc7": (0.25, 4.00), "fc8": (0.06, 0.98)}
+    reproduced to the printed 2 decimals for all 13 layers at B=16 and B=256
+    (tests/golden/table4_memory_mib.txt).  Pins the C-19 conv/pool geometry."""
+    table4 = _golden("table4_memory_mib.txt")
     rows = infer.alexnet_layer_shapes()
     assert [n for n, _ in rows] == list(table4)
     for name, elems in rows:
