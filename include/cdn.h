@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define CDN_ABI_VERSION 1
+#define CDN_ABI_VERSION 2
 
 typedef int32_t cdn_status;
 enum {
@@ -218,10 +218,24 @@ cdn_status cdn_model_profile(cdn_model* m, int Bmax, int reps, double* time_ms);
 cdn_status cdn_model_memory_model(cdn_model* m, int Bmax, uint64_t* in_bytes, uint64_t* out_bytes,
                                   uint64_t* ws_bytes);
 
+/* ---- inference scratch (the memory TOT bounds: everything but the
+ * resident compressed model -- level activation buffers, workspaces, per-call
+ * decoded lists / filters, staging): bytes allocated now and the high-water
+ * mark since the model was created or the peak last reset (reset_peak != 0
+ * sets it to the current bytes after reading).  Under a memory budget the
+ * planner only runs plans whose executor scratch fits TOT (reading C-36).
+ * Either output may be NULL.  Errors: CDN_E_ARG. */
+cdn_status cdn_model_scratch_bytes(cdn_model* m, uint64_t* current, uint64_t* peak, int reset_peak);
+
+/* Free every inference-scratch buffer of the model (the next call allocates
+ * what its plan needs); waits for the model's streams.  Errors: CDN_E_ARG,
+ * CDN_E_STATE (a call in progress), CDN_E_CUDA. */
+cdn_status cdn_model_release_scratch(cdn_model* m);
+
 /* Name of the kernel a layer launches for batch B under the current policy
- * (after the first-use autotune at that B, if any): "k_fc_ms", "k_fc_fold",
- * "k_fc_band<V>", "k_fc_tc" or "k_gemm_bf16 (conv)"; "" for bad arguments.
- * The string is static. */
+ * (after the first-use autotune at that B, if any): "k_fc_j" (B <= 4),
+ * "k_fc_ms", "k_fc_fold", "k_fc_band<V>", "k_fc_tc" or "k_gemm_bf16 (conv)";
+ * "" for bad arguments.  The string is static. */
 const char* cdn_layer_kernel_name(const cdn_model* m, int layer, int B);
 
 /* ---- host-only utilities (no device needed) ----------------------------- */

@@ -76,6 +76,8 @@ _SIGS = {
     "cdn_model_plan": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "cdn_model_set_plan": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int), C.c_int]),
     "cdn_model_infer": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
+    "cdn_model_scratch_bytes": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int]),
+    "cdn_model_release_scratch": (C.c_int32, [C.c_void_p]),
     "cdn_layer_forward": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                       C.c_void_p]),
     "cdn_layer_decode": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -307,6 +309,15 @@ class Model:
     def set_kernel_policy(self, band_min_batch: int = 0, tc_min_batch: int = 0):
         """B >= tc_min_batch -> tensor-core kernel; B >= band_min_batch -> band kernel (0: defaults)."""
         _check(self._lib.cdn_model_set_kernel_policy(self._h, int(band_min_batch), int(tc_min_batch)))
+
+    def scratch_bytes(self, reset_peak: bool = False) -> Tuple[int, int]:
+        """(current, high-water) bytes of inference scratch (cdn_model_scratch_bytes)."""
+        cur, peak = C.c_uint64(), C.c_uint64()
+        _check(self._lib.cdn_model_scratch_bytes(self._h, C.byref(cur), C.byref(peak), int(bool(reset_peak))))
+        return cur.value, peak.value
+
+    def release_scratch(self):
+        _check(self._lib.cdn_model_release_scratch(self._h))
 
     def decode_count(self, layer: int) -> int:
         n = C.c_uint64()

@@ -46,15 +46,24 @@ cdn_status fail(cdn_status c, const std::string& m) {
 // hold raw pointers, so a changed counter retires them
 std::atomic<uint64_t> g_dbuf_gen{0};
 
+// Device bytes of a model's inference scratch (everything but the resident
+// compressed model: activations, workspaces, per-call decoded lists / filters),
+// current and high-water (cdn_model_scratch_bytes): the memory the budget TOT
+// of P:L651 bounds.
+struct Acct {
+  uint64_t cur = 0, peak = 0;
+};
+
 struct DBuf {
   void* p = nullptr;
   size_t n = 0;
+  Acct* acct = nullptr;  // scratch accounting of the owning model (null: resident data)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), acct(o.acct) { o.p = nullptr; o.n = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; acct = o.acct; o.p = nullptr; o.n = 0; }
     return *this;
   }
   ~DBuf() { release(); }
@@ -62,6 +71,7 @@ struct DBuf {
     if (p) {
       cudaFree(p);
       g_dbuf_gen.fetch_add(1);
+      if (acct) acct->cur -= n;
     }
     p = nullptr;
     n = 0;
@@ -72,6 +82,10 @@ struct DBuf {
     CUDA_OK(cudaMalloc(&p, bytes ? bytes : 16));
     g_dbuf_gen.fetch_add(1);
     n = bytes;
+    if (acct) {
+      acct->cur += n;
+      acct->peak = std::max(acct->peak, acct->cur);
+    }
   }
   template <class T> void upload(const std::vector<T>& v) {
     alloc(v.size() * sizeof(T));
@@ -100,6 +114,7 @@ struct Layer {
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
   std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band) measured at first use
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
+  size_t tlist_bytes = 0, wd_bytes = 0;  // sizes of the per-call scratch above (allocated at first use)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
   DBuf jw, jrow, jlane, jlut, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
   std::vector<uint32_t> jrow_h;               // host copy of jrow (per-CTA stream ranges)
@@ -148,6 +163,13 @@ struct Model {
   int tc_min = 0;               // cdn_model_set_kernel_policy tensor-core threshold (0: default)
   DBuf tc_xh, tc_xl;            // tensor-core FC: fp16 hi / lo split of the activations
   DBuf tc_sc, tc_ctr;           // tensor-core FC: per-image split scales; their arrival counters (zero between calls)
+  Acct scratch;                 // inference scratch of this model (every buffer above and the layers' workspaces)
+  std::vector<int> last_plan;   // plan of the last budgeted round (its scratch is what is allocated)
+  void tag_scratch() {
+    for (DBuf* b : {&stage[0], &stage[1], &out, &loc, &gath, &host_stage, &conv_a, &conv_o, &conv_t, &ctmp, &tc_xh,
+                    &tc_xl, &tc_sc, &tc_ctr})
+      b->acct = &scratch;
+  }
   // CUDA graphs of repeated infer calls (same buffers, K, plan and state):
   // the second identical call is captured, later ones replay it
   struct GraphEntry {
@@ -331,9 +353,15 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     // merged token stream + joint LUT of the small-batch kernel (joint.cu, C-35).
     // LUT width: wider windows fold more tokens per lookup, but every CTA
     // stages the table (4 << jL bytes), so small layers take narrower ones.
-    // Column groups Q: the smallest Q whose CTA (tables + x slice + stream
-    // slots) fits half an SM's shared memory, so the next launch's CTA can
-    // stage its weights beside a running one (programmatic dependent launch).
+    // Lanes per row of this kernel (its own split, independent of the lane
+    // index above): enough lanes for ~28 warps per SM, none shorter than ~8 tokens
+    int G = 1;
+    {
+      const double toks = (double)ix.tokens / std::max<uint32_t>(1, nr);
+      const double want = (double)m.num_sms * 28 * 32 / std::max<uint32_t>(1, nr);
+      while (G < 32 && G < want && toks / (2 * G) >= 8.0) G *= 2;
+      if (const char* e = std::getenv("CDN_JG")) G = std::max(1, std::min(32, std::atoi(e)));
+    }
     uint64_t tb = 0, rmax = 0;
     for (uint32_t i = L.row0; i < L.row1; ++i) {
       const uint64_t rb = (H.rp[2ull * i + 2] - H.rp[2ull * i]) + (H.rp[2ull * i + 3] - H.rp[2ull * i + 1]);
@@ -342,22 +370,17 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     }
     const double per_sm = (double)tb / 8.0 / std::max(1, m.num_sms);
     int jl = per_sm >= 24576 ? 14 : per_sm >= 12288 ? 13 : per_sm >= 6144 ? 12 : 11;
+    // Column groups only when the CTA's x slice would not fit beside the
+    // tables and streams (measured: Q > 1 costs more in partial sums and
+    // per-row staging than the smaller x slice saves)
     int jq = 1;
     {
-      const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits)), Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
-      auto est = [&](int Q, int L2) {
-        const double rows_cta = std::ceil((double)nr * Q / std::max(1, m.num_sms));
-        return (double)(4u << L2) + (4u << Lv) + (4u << Lg) + 2048.0 + 4.0 * std::ceil((double)H.cols / Q) +
-               rows_cta * ((double)rmax / 8.0 / Q + 48.0);
+      const double rows_cta = std::ceil((double)nr / std::max(1, m.num_sms));
+      auto est = [&](int Q) {
+        return (double)(4u << jl) + 16384.0 + 4.0 * std::ceil((double)H.cols / Q) +
+               rows_cta * Q * ((double)rmax / 8.0 / Q + 48.0);
       };
-      bool found = false;
-      for (int L2 = jl; L2 >= 12 && !found; --L2)
-        for (int Q = 1; Q <= 8 && Q <= G && !found; Q *= 2)
-          if (G % Q == 0 && est(Q, L2) <= 110.0 * 1024) {
-            jq = Q;
-            jl = L2;
-            found = true;
-          }
+      while (jq < G && jq < 8 && est(jq) > 220.0 * 1024) jq *= 2;
     }
     if (const char* e = std::getenv("CDN_JL")) jl = std::max(8, std::min(16, std::atoi(e)));
     if (const char* e = std::getenv("CDN_JQ")) jq = std::max(1, std::min(G, std::atoi(e)));
@@ -411,6 +434,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       L.dev.jL = jl;
       L.dev.jsub = sub;
       L.dev.jQ = jq;
+      L.dev.jG = G;
       L.dev.jKq = (int)jx.Kq;
       if (std::getenv("CDN_JDEBUG"))
         fprintf(stderr, "[cdn] joint layer rows=%u cols=%u G=%d Q=%d jL=%d sub=%u blob=%u\n", nr, H.cols, G, jq, jl, sub,
@@ -519,7 +543,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       if (off >= (1ull << 32)) throw Error(CDN_E_UNSUPPORTED, "shard with >= 2^32 nonzeros");
       L.tbase.upload(tb);
       L.troff.upload(to);
-      L.tlist.alloc((off + 64) * sizeof(uint16_t));
+      L.tlist_bytes = (off + 64) * sizeof(uint16_t);  // per-call scratch, allocated at first use (ensure_list)
       // list-decoder tasks: chunks of up to kTcChunk K tiles, fewer when that
       // would leave the GPU short of threads (~64k wanted; measured on C5 fc7/fc8)
       int tch = kTcChunk;
@@ -622,7 +646,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : (L.dev.Wi == 64 ? L.ivm.as<uint16_t>() : nullptr);
   f.tbase = L.tbase.as<uint32_t>();
   f.troff = L.troff.as<uint16_t>();
-  f.tlist = L.tlist.as<uint16_t>();
+  f.tlist = nullptr;  // ensure_list
   f.ivg = L.ivg.as<uint2>();
   f.ivm = L.ivm.as<uint16_t>();
 
@@ -647,9 +671,12 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   s.out_features = L.out_elems();
   if (conv) {
     L.kpad = (int)((H.cols + 63) / 64 * 64);
-    L.wd.alloc((size_t)H.rows * L.kpad * 2);
+    L.wd_bytes = (size_t)H.rows * L.kpad * 2;  // per-call scratch, allocated at first use (ensure_wd)
     s.ws_bytes = (uint64_t)H.rows * L.kpad * 2;  // decoded bf16 filters (per-call scratch, C-24)
   }
+  for (DBuf* b : {&L.bws, &L.bctr, &L.tlist, &L.wd, &L.jpart, &L.jctr, &L.ctr}) b->acct = &m.scratch;
+  m.scratch.cur += L.jpart.n + L.jctr.n + L.ctr.n;  // (allocated above, before the tags)
+  m.scratch.peak = std::max(m.scratch.peak, m.scratch.cur);
   m.layers.push_back(std::move(Lp));
   m.prof_bmax = 0;
   m.plan_cache.clear();
@@ -657,6 +684,18 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
 }
 
 cudaStream_t pick(Model& m, void* s) { return s ? (cudaStream_t)s : m.stream; }
+
+// Per-call scratch of a layer's decode, allocated at its first use
+void ensure_list(Layer& L) {
+  if (!L.tlist.p && L.tlist_bytes) {
+    L.tlist.alloc(L.tlist_bytes);
+    L.dev.tlist = L.tlist.as<uint16_t>();
+  }
+}
+void ensure_wd(Layer& L) {
+  if (!L.wd.p && L.wd_bytes) L.wd.alloc(L.wd_bytes);
+}
+
 
 // Explicit tensor-core threshold (env CDN_TC_MIN_B); without it and without a
 // kernel policy, every B the band kernel would take (B >= band_min_batch(), 16)
@@ -741,6 +780,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       if (L.list_state == 1) {
         CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
       } else if (L.list_state == 0) {
+        ensure_list(L);
         CUDA_OK(launch_tc_list(L.dev, s));
       }
       L.list_state = 2;
@@ -818,9 +858,11 @@ bool predecodes(const Model& m, const Layer& L, int B) { return L.is_conv() || u
 
 void predecode_launch(Model& m, Layer& L, cudaStream_t s) {
   if (L.is_conv()) {
+    ensure_wd(L);
     CUDA_OK(cudaMemsetAsync(L.wd.p, 0, L.wd.n, s));
     CUDA_OK(launch_decode_dense(L.dev, static_cast<__nv_bfloat16*>(L.wd.p), L.kpad, s, m.num_sms));
   } else {
+    ensure_list(L);
     CUDA_OK(launch_tc_list(L.dev, s));
   }
 }
@@ -857,12 +899,12 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
   const int M = (int)L.rows, G = d.groups, cg = d.in_c / G, mg = M / G;
   const int Ho = L.conv_h, Wo = L.conv_w;
   const long npos = (long)B * Ho * Wo;
-  __nv_bfloat16* wd = static_cast<__nv_bfloat16*>(L.wd.p);
   if (L.list_state == 1) {  // decoded ahead on the side stream (prelaunch_lists)
     CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
   } else if (L.list_state == 0) {
     predecode_launch(m, L, s);
   }
+  __nv_bfloat16* wd = static_cast<__nv_bfloat16*>(L.wd.p);
   L.list_state = 2;  // later phases of the call reuse the decoded filters
   const bool post = d.lrn || d.pool_k > 0;
   float* cout = y;
@@ -1044,6 +1086,7 @@ struct Exec {
 
 void alloc_levels(Model& m, const std::vector<int>& bs) {
   m.lvl.resize(m.layers.size());
+  for (auto& b : m.lvl) b.acct = &m.scratch;
   for (size_t i = 0; i < m.layers.size(); ++i) {
     const Layer& L = *m.layers[i];
     if (L.is_conv()) {
@@ -1062,6 +1105,79 @@ void check_chain(const Model& m, const std::vector<int>& bs) {
     if (i && (bs[i] < bs[i - 1] || bs[i] % bs[i - 1]))
       throw Error(CDN_E_ARG, "plan is not a divisor chain (P:L675-679)");
   }
+}
+
+// Free every inference-scratch buffer (activations, workspaces, per-call
+// decoded lists / filters): the next call allocates what its plan needs.
+void release_scratch(Model& m) {
+  for (DBuf* b : {&m.stage[0], &m.stage[1], &m.out, &m.loc, &m.gath, &m.host_stage, &m.conv_a, &m.conv_o, &m.conv_t,
+                  &m.ctmp, &m.tc_xh, &m.tc_xl, &m.tc_sc, &m.tc_ctr})
+    b->release();
+  for (auto& b : m.lvl) b.release();
+  for (auto& L : m.layers) {
+    L->bws.release();
+    L->bctr.release();
+    L->tlist.release();
+    L->dev.tlist = nullptr;
+    L->wd.release();
+    L->list_state = 0;
+  }
+  // (captured graphs hold the freed pointers: the g_dbuf_gen bump retires them)
+}
+
+// Device scratch the executor allocates for plan bs (an upper bound: for a
+// batch the first-use autotune may run, both large-batch kernels' workspaces):
+// level buffers, scores, host staging, the tensor-core split / scales /
+// partials / decoded lists, band partials, CONV patches / outputs / decoded
+// filters, all-gather slabs, and the per-layer constants (counters, column-group
+// partials).  plan_for keeps plans whose scratch exceeds TOT out.
+uint64_t exec_scratch_bytes(const Model& m, const std::vector<int>& bs, bool host_input) {
+  const int f = (int)m.layers.size();
+  uint64_t total = 0, ctmp = 0, xs = 0, sc = 0, tctr = 0, ca = 0, co = 0, ct = 0, slab = 0;
+  for (int i = 0; i < f; ++i) {
+    const Layer& L = *m.layers[i];
+    const int B = bs[i];
+    total += L.jpart.n + L.jctr.n + L.ctr.n;
+    if (L.is_conv()) {
+      if (i > 0) total += 4ull * L.in_elems() * B;
+      const cdn_layer_desc& d = L.desc;
+      const uint64_t npos = (uint64_t)B * L.conv_h * L.conv_w;
+      ca = std::max<uint64_t>(ca, npos * L.kpad * 2ull * d.groups);
+      if (d.lrn || d.pool_k > 0) co = std::max<uint64_t>(co, npos * L.rows * 4ull);
+      if (d.lrn && d.pool_k > 0) ct = std::max<uint64_t>(ct, npos * L.rows * 4ull);
+      total += L.wd_bytes;
+      continue;
+    }
+    total += 4ull * L.cols * ld4(B);
+    if (i > 0 && m.layers[i - 1]->is_conv()) ctmp = std::max<uint64_t>(ctmp, 4ull * L.cols * bs[i - 1]);
+    uint64_t bws = 0, bctr = 0;
+    const bool big = L.blocked || B >= band_min_batch() || (m.tc_min > 0 && B >= m.tc_min) ||
+                     (m.band_min > 0 && B >= m.band_min);
+    if (big && tc_supported(L.dev)) {
+      const TcPlan tp = plan_fc_tc(L.dev, B, m.num_sms);
+      if (tp.ok) {
+        xs = std::max<uint64_t>(xs, tp.xsplit_elems * 2);
+        sc = std::max<uint64_t>(sc, tc_scale_floats(B) * 4);
+        tctr = std::max<uint64_t>(tctr, 4ull * B);
+        bws = std::max<uint64_t>(bws, tp.ws_floats * 4);
+        total += L.tlist_bytes;
+      }
+    }
+    if (big && !L.blocked) {
+      const BandPlan bp = plan_fc_band(L.dev, reinterpret_cast<const float*>(256), ld4(B), B, m.num_sms);
+      if (bp.ok) {
+        bws = std::max<uint64_t>(bws, bp.ws_floats * 4);
+        bctr = 4ull * bp.tiles;
+      }
+    }
+    total += bws + bctr;
+    if (m.world > 1) slab = std::max<uint64_t>(slab, 4ull * rows_per_rank(L.rows, m.world) * B * (m.world + 1));
+  }
+  const Layer& Lf = *m.layers[f - 1];
+  const int Bf = bs[f - 1];
+  total += 4ull * Lf.rows * ld4(Bf);  // scores (feature-major; a tensor-core last layer writes them directly)
+  if (host_input) total += 2ull * 4 * Bf * m.layers[0]->in_elems() + 4ull * Lf.rows * Bf;  // staging, host scores
+  return total + ctmp + 2 * xs + sc + tctr + ca + co + ct + slab;
 }
 
 void profile(Model& m, int Bmax, int reps) {
@@ -1086,14 +1202,25 @@ void profile(Model& m, int Bmax, int reps) {
   for (int i = 0; i < f; ++i) {
     Layer& L = *m.layers[i];
     auto step = [&](int B) {
-      L.list_state = 0;  // every timed call decodes its list
       if (L.is_conv())
         conv_forward(m, L, xb.as<float>(), B, yb.as<float>(), s);
       else
         layer_step(m, i, xb.as<float>(), ld4(B), B, yb.as<float>(), ld4(B), s);
     };
     for (int B = 1; B <= Bmax; ++B) {
-      step(B);  // warm-up
+      L.list_state = 0;
+      step(B);  // warm-up (and the first-use autotune at this B)
+      // Time(i,B) as infer runs the layer: the per-call decode of its tensor-core
+      // list / CONV filters is launched at the start of the call on a side
+      // stream, ahead of (and overlapped with) the layers before it and decoded
+      // once per call, not per phase -- so it is done here before the timed
+      // runs, which reuse it (list_state 2)
+      if (predecodes(m, L, B)) {
+        predecode_launch(m, L, s);
+        L.list_state = 2;
+      } else {
+        L.list_state = 0;
+      }
       for (int r = 0; r < reps; ++r) {
         CUDA_OK(cudaEventRecord(e0, s));
         step(B);
@@ -1109,6 +1236,8 @@ void profile(Model& m, int Bmax, int reps) {
   cudaEventDestroy(e1);
   CUDA_OK(cudaStreamSynchronize(s));
   for (auto& L : m.layers) L->list_state = 0;  // profiling's lists are not the caller's
+  release_scratch(m);  // profiling grew the scratch to Bmax; the plan's run allocates its own
+  m.last_plan.clear();
   if (m.world > 1 && m.comm) {
     // every rank must run the same plan (the same phases issue the same
     // all-gathers): the DP runs on one table, the slowest rank's time per
@@ -1127,16 +1256,30 @@ std::vector<uint64_t> in_bytes(const Model& m) {
   for (auto& L : m.layers) v.push_back(4ull * L->in_elems());
   return v;
 }
-std::vector<uint64_t> out_bytes(const Model& m) {
+std::vector<uint64_t> out_bytes(const Model& m, int Bmax) {
   std::vector<uint64_t> v;
   for (auto& L : m.layers) {
     uint64_t b = 4ull * L->out_elems();
-    // CONV scratch grows with the batch (bf16 patches + conv / LRN outputs), so
-    // it is charged per image with OUT(i,B) rather than as a constant WS(i)
-    // (reading C-24 for CONV layers); WS(i) keeps the decoded filters.
-    if (L->is_conv())
+    // Scratch that grows with the batch is charged per image with OUT(i,B)
+    // (reading C-24): CONV -- bf16 patches + conv / LRN outputs; FC on the
+    // large-batch kernels -- the fp16 hi / lo split of the input (4 bytes per
+    // input feature), the per-image split scales, and the K-split partial sums
+    // (their largest per-image share over the profiled batches).  WS(i) keeps
+    // the batch-independent scratch (ws_bytes).
+    if (L->is_conv()) {
       b += (uint64_t)L->conv_h * L->conv_w *
            (2ull * L->kpad * (uint64_t)L->desc.groups + (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows);
+    } else if (tc_supported(L->dev) || L->dev.ivg) {
+      uint64_t part = 0;
+      for (int B : {16, 32, 64, 128, 256, 512, Bmax}) {
+        if (B > Bmax || B < 1) continue;
+        const TcPlan tp = plan_fc_tc(L->dev, B, m.num_sms);
+        if (tp.ok) part = std::max<uint64_t>(part, (tp.ws_floats * 4 + B - 1) / B);
+        const BandPlan bp = plan_fc_band(L->dev, reinterpret_cast<const float*>(256), ld4(B), B, m.num_sms);
+        if (bp.ok) part = std::max<uint64_t>(part, (bp.ws_floats * 4 + 4ull * bp.tiles + B - 1) / B);
+      }
+      b += 4ull * ((L->cols + 7) & ~7u) + 4ull * (tc_scale_floats(1) + 1) + part;
+    }
     v.push_back(b);
   }
   return v;
@@ -1144,18 +1287,18 @@ std::vector<uint64_t> out_bytes(const Model& m) {
 std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
   std::vector<uint64_t> v;
   for (auto& L : m.layers) {
-    uint64_t ws = L->stats.ws_bytes;
-    if (L->is_conv()) {
-      // decoded bf16 filters only (the per-image scratch is in out_bytes)
-    } else if (m.world > 1) {
-      ws += 4ull * rows_per_rank(L->rows, m.world) * (m.world + 1) * Bmax;  // C-24: max over grid
-    }
+    // decoded bf16 filters (CONV) / the tensor-core path's decoded list (FC),
+    // the per-layer counters and column-group partials
+    uint64_t ws = L->is_conv() ? L->wd_bytes : L->tlist_bytes;
+    ws += L->jpart.n + L->jctr.n + L->ctr.n;
+    if (!L->is_conv() && m.world > 1)
+      ws += 4ull * rows_per_rank(L->rows, m.world) * (m.world + 1) * Bmax;  // all-gather slabs, C-24: max over grid
     v.push_back(ws);
   }
   return v;
 }
 
-PlanResult plan_for(Model& m, int K) {
+PlanResult plan_for(Model& m, int K, bool host_input = false) {
   if (m.prof_bmax < K) m.plan_cache.clear();  // the table is about to change
   profile(m, K, 5);
   // Time(i, B) for B = 1..K out of the (possibly wider) cached table
@@ -1163,8 +1306,26 @@ PlanResult plan_for(Model& m, int K) {
   for (size_t i = 0; i < m.layers.size(); ++i)
     for (int B = 1; B <= K; ++B) t[i * K + (B - 1)] = m.prof[i * (size_t)m.prof_bmax + (B - 1)];
   const int f = (int)m.layers.size();
-  auto inb = in_bytes(m), outb = out_bytes(m), ws = ws_bytes(m, K);
-  return plan_dp(t.data(), inb.data(), outb.data(), ws.data(), f, K, m.tot, m.latency, 64 * 1024);
+  auto inb = in_bytes(m), outb = out_bytes(m, K), ws = ws_bytes(m, K);
+  // The DP is the paper's recurrence on these IN / OUT / WS.  The
+  // executor keeps every level's input buffer at full width and its workspaces
+  // allocated through the round, so its scratch can exceed the recurrence's
+  // per-layer bound by one phase slot per deeper level: a plan whose executor
+  // scratch (exec_scratch_bytes) exceeds TOT is re-planned under TOT less the
+  // excess until it fits (reading C-36).
+  uint64_t budget = m.tot;
+  PlanResult pr;
+  for (int it = 0; it < 16; ++it) {
+    pr = plan_dp(t.data(), inb.data(), outb.data(), ws.data(), f, K, budget, m.latency, 64 * 1024);
+    if (!pr.feasible) return pr;
+    const uint64_t need = exec_scratch_bytes(m, pr.batches, host_input);
+    if (need <= m.tot) return pr;
+    const uint64_t over = need - m.tot;
+    if (budget <= over) break;
+    budget -= std::max<uint64_t>(over, 64 * 1024);
+  }
+  pr.feasible = false;
+  return pr;
 }
 
 }  // namespace
@@ -1206,6 +1367,7 @@ cdn_status cdn_model_create(int device, int rank, int world, const uint8_t* nccl
   m.device = device;
   m.rank = rank;
   m.world = world;
+  m.tag_scratch();
   CUDA_OK(cudaSetDevice(device));
   CUDA_OK(cudaDeviceGetAttribute(&m.num_sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_OK(cudaStreamCreateWithFlags(&m.stream, cudaStreamNonBlocking));
@@ -1328,15 +1490,26 @@ void infer_body(Model& m, const float* input, int K, float* scores, int on_devic
     } else if (m.tot > 0) {
       // plans are cached per request size until the budget, layers or table change
       const std::vector<int>* hit = nullptr;
+      const int key = on_device ? rem : -rem;  // host input stages a round on the device too
       for (auto& e : m.plan_cache)
-        if (e.first == rem && m.prof_bmax >= rem) hit = &e.second;
+        if (e.first == key && m.prof_bmax >= rem) hit = &e.second;
       if (hit) {
         bs = *hit;
       } else {
-        PlanResult pr = plan_for(m, rem);
+        PlanResult pr = plan_for(m, rem, !on_device);
         if (!pr.feasible) throw Error(CDN_E_INFEASIBLE, "no batch plan fits TOT/latency");
         bs = pr.batches;
-        m.plan_cache.emplace_back(rem, bs);
+        m.plan_cache.emplace_back(key, bs);
+      }
+      // a new plan at the start of a call: the scratch of the previous one
+      // would count against TOT (a remainder plan later in the call reuses the
+      // call's buffers; a captured call repeats the eager one exactly)
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      CUDA_OK(cudaStreamIsCapturing(s, &cap));
+      if (o == 0 && bs != m.last_plan && cap == cudaStreamCaptureStatusNone) {
+        CUDA_OK(cudaStreamSynchronize(s));
+        release_scratch(m);
+        m.last_plan = bs;
       }
     } else {
       bs.assign(f, rem);  // no budget: the whole request as one batch
@@ -1529,6 +1702,28 @@ cdn_status cdn_debug_kernel_timer_read(const char* kernel, double* total_ms, int
   API_END
 }
 
+cdn_status cdn_model_scratch_bytes(cdn_model* h, uint64_t* current, uint64_t* peak, int reset_peak) {
+  API_BEGIN
+  if (!h) return fail(CDN_E_ARG, "NULL model");
+  if (current) *current = h->m.scratch.cur;
+  if (peak) *peak = h->m.scratch.peak;
+  if (reset_peak) h->m.scratch.peak = h->m.scratch.cur;
+  API_END
+}
+
+cdn_status cdn_model_release_scratch(cdn_model* h) {
+  API_BEGIN
+  if (!h) return fail(CDN_E_ARG, "NULL model");
+  if (h->m.busy) return fail(CDN_E_STATE, "concurrent call on one handle");
+  CUDA_OK(cudaSetDevice(h->m.device));
+  CUDA_OK(cudaStreamSynchronize(h->m.stream));
+  if (h->m.side) CUDA_OK(cudaStreamSynchronize(h->m.side));
+  CUDA_OK(cudaDeviceSynchronize());
+  release_scratch(h->m);
+  h->m.last_plan.clear();
+  API_END
+}
+
 cdn_status cdn_debug_kernel_launches(uint64_t* out) {
   API_BEGIN
   if (!out) return fail(CDN_E_ARG, "null out");
@@ -1610,7 +1805,7 @@ cdn_status cdn_model_memory_model(cdn_model* h, int Bmax, uint64_t* in_b, uint64
   API_BEGIN
   if (!h || Bmax < 1 || !in_b || !out_b || !ws) return fail(CDN_E_ARG, "bad arguments");
   Model& m = h->m;
-  auto a = in_bytes(m), b = out_bytes(m), c = ws_bytes(m, Bmax);
+  auto a = in_bytes(m), b = out_bytes(m, Bmax), c = ws_bytes(m, Bmax);
   std::copy(a.begin(), a.end(), in_b);
   std::copy(b.begin(), b.end(), out_b);
   std::copy(c.begin(), c.end(), ws);

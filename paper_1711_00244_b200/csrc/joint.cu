@@ -39,6 +39,7 @@ using namespace dev;
 
 constexpr int kJMaxWarps = 32;
 constexpr int kJMaxCta = 160;  // CTA stream ranges passed in the launch parameters
+constexpr int kJPieces = 4;    // a CTA's stream bits arrive in this many pieces (warps start on their own)
 
 struct JArgs {
   const float* x;
@@ -52,8 +53,9 @@ struct JArgs {
   uint32_t off_x, off_slot;  // dynamic smem offsets (the table blob sits at 0)
   int xbulk;          // 1: x contiguous (ldx == 1, B == 1) and 16-byte aligned
   unsigned long long* trace;  // debug (env CDN_J_TRACE): per CTA 8 globaltimer stamps, else null
-  int ncta;           // Q == 1: CTAs whose stream range is in cta[] (the rest read row_bit)
-  uint2 cta[kJMaxCta];  // Q == 1: per CTA (16-byte index of its first row's bits, bytes to stage)
+  int ncta;           // Q == 1: CTAs whose stream ranges are in cta[] (the rest stage per warp)
+  uint2 cta[kJMaxCta * kJPieces];  // Q == 1: per CTA and piece (16-byte index of the piece's first bits,
+                                   // bytes to stage); piece p = the CTA's warps [p nw / P, (p+1) nw / P)
 };
 
 __device__ __forceinline__ void jtrace(const JArgs& A, int ev) {
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
   jtrace(A, 0);
   asm volatile("griddepcontrol.launch_dependents;");
 
-  const int G = L.G, GQ = A.GQ, q = blockIdx.y;
+  const int G = L.jG, GQ = A.GQ, q = blockIdx.y;
   const int rr = lane / GQ, jj = lane - rr * GQ, j = q * GQ + jj;  // row of the warp unit, lane of the row
   const int xc0 = q * L.jKq, xcols = min(L.jKq, L.cols - xc0);      // this column group's slice of x
   const int u = blockIdx.x * A.nw + warp;  // warp unit: rows u RPW .. u RPW + RPW - 1
@@ -139,10 +141,15 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
     mbar_init(&bar_x, 1);
     for (int w = 0; w < A.nw; ++w) mbar_init(&bar_s[w], 1);
     mbar_fence_init();
-    if (whole) {  // the CTA's rows are contiguous: their bits in one bulk copy
-      const uint2 c = A.cta[blockIdx.x];
-      mbar_arrive_expect_tx(&bar_s[0], c.y);
-      if (c.y) bulk_g2s(smem + A.off_slot, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)c.x * 16u, c.y, &bar_s[0]);
+    if (whole) {  // the CTA's rows are contiguous: their bits in kJPieces bulk copies
+      const uint32_t base = A.cta[blockIdx.x * kJPieces].x;
+      for (int pc = 0; pc < kJPieces; ++pc) {
+        const uint2 c = A.cta[blockIdx.x * kJPieces + pc];
+        mbar_arrive_expect_tx(&bar_s[pc], c.y);
+        if (c.y)
+          bulk_g2s(smem + A.off_slot + (c.x - base) * 16u, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)c.x * 16u,
+                   c.y, &bar_s[pc]);
+      }
     }
     // every table in one bulk copy (host-built blob in this layout)
     mbar_arrive_expect_tx(&bar_w, L.jblob);
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
   const int prev = (int)(rec >> 16) - 1;                                      // lane's previous column
   uint32_t rs, slot_off;  // staged bits start (128-bit aligned) and its shared-memory offset
   if (whole) {
-    rs = A.cta[blockIdx.x].x * 128u;
+    rs = A.cta[blockIdx.x * kJPieces].x * 128u;
     slot_off = A.off_slot;
   } else {
     // per warp: each row's range of this column group [first lane's start, last lane's end)
@@ -219,7 +226,8 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
   const int vsh = 32 - L.Lv, gsh = 32 - L.Lg;
   const uint32_t xbase = sb + A.off_x;
   if (u < A.units) {
-    mbar_wait(&bar_s[whole ? 0 : warp], 0);
+    // piece pc holds warps [pc nw / P, (pc + 1) nw / P): warp w's is the last pc whose start is <= w
+    mbar_wait(&bar_s[whole ? ((warp + 1) * kJPieces - 1) / A.nw : warp], 0);
     jtrace(A, 4);
     int nrem = (int)lb - (int)le;  // -(bits left in the lane)
     uint32_t sp = sb + slot_off + ((lb - rs) >> 5) * 4u;  // (ok lanes only: the others never load)
@@ -322,14 +330,14 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
 
 }  // namespace
 
-bool j_supported(const FcDev& L) { return L.jw && L.jlut && L.ncb <= 32 && L.G <= 32; }
+bool j_supported(const FcDev& L) { return L.jw && L.jlut && L.ncb <= 32 && L.jG <= 32 && L.jG >= 1; }
 
 JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
   JPlan p;
   if (!j_supported(L) || B < 1 || B > 4 || L.nrows <= 0) return p;
   p.BS = B <= 1 ? 1 : (B <= 2 ? 2 : 4);
   p.Q = L.jQ;
-  p.GQ = L.G / p.Q;
+  p.GQ = L.jG / p.Q;
   p.RPW = 32 / p.GQ;
   p.units = (L.nrows + p.RPW - 1) / p.RPW;
   // one CTA per SM (Q column groups of a row block side by side), every
@@ -342,15 +350,23 @@ JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
     p.nrb = (p.units + p.nw - 1) / p.nw;
     p.cta.clear();
     size_t slot = (size_t)p.nw * p.RPW * L.jsub;  // per-warp row slots
-    if (p.Q == 1 && row_bit && p.nrb <= kJMaxCta) {
-      // the CTA's rows are contiguous: one range of the merged stream
+    if (p.Q == 1 && row_bit && p.nrb <= kJMaxCta && p.nw >= kJPieces) {
+      // the CTA's rows are contiguous: one range of the merged stream, staged
+      // in kJPieces copies of whole warp units (pieces overlap by at most the
+      // 16-byte block of a shared boundary, copied twice)
       size_t mx = 0;
       for (int c = 0; c < p.nrb; ++c) {
-        const int r0 = c * p.nw * p.RPW, r1 = std::min(L.nrows, (c + 1) * p.nw * p.RPW);
-        const uint32_t a = row_bit[r0] >> 7, b = (row_bit[r1] + 127) >> 7;
-        const uint32_t bytes = (b - a) * 16u + 16u;  // + one word of read-ahead
-        p.cta.push_back(make_uint2(a, bytes));
-        mx = std::max<size_t>(mx, bytes);
+        const int cr0 = c * p.nw * p.RPW;
+        uint32_t first = 0;
+        for (int pc = 0; pc < kJPieces; ++pc) {
+          const int w0 = pc * p.nw / kJPieces, w1 = (pc + 1) * p.nw / kJPieces;
+          const int r0 = std::min(L.nrows, cr0 + w0 * p.RPW), r1 = std::min(L.nrows, cr0 + w1 * p.RPW);
+          const uint32_t a = row_bit[r0] >> 7, b = (row_bit[r1] + 127) >> 7;
+          const uint32_t bytes = r1 > r0 ? (b - a) * 16u + 16u : 0u;  // + one word of read-ahead
+          if (pc == 0) first = a;
+          p.cta.push_back(make_uint2(a, bytes));
+          mx = std::max<size_t>(mx, (size_t)(a - first) * 16u + bytes);
+        }
       }
       slot = mx;
     }
@@ -382,8 +398,8 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   a.sub = p.sub;
   a.off_x = p.off_x;
   a.off_slot = p.off_slot;
-  a.ncta = (int)p.cta.size();
-  for (size_t i = 0; i < p.cta.size() && i < (size_t)kJMaxCta; ++i) a.cta[i] = p.cta[i];
+  a.ncta = (int)(p.cta.size() / kJPieces);
+  for (size_t i = 0; i < p.cta.size() && i < (size_t)kJMaxCta * kJPieces; ++i) a.cta[i] = p.cta[i];
   static unsigned long long* trace = nullptr;
   static const char* trace_path = getenv("CDN_J_TRACE");
   const size_t ntr = (size_t)p.nrb * p.Q * 8;

@@ -94,6 +94,7 @@ struct FcDev {
   int jL = 12;                       // [joint LUT 4<<jL | vlut | glut | vtab | gtab | vsorted | gsorted | codebook]
   uint32_t jo_vlut = 0, jo_glut = 0, jo_vtab = 0, jo_gtab = 0, jo_vs = 0, jo_gs = 0, jo_cb = 0, jblob = 0;
   uint32_t jsub = 0;                 // bytes of one row's staging sub-slot
+  int jG = 1;                        // lanes per row of the merged-stream split
   int jQ = 1, jKq = 0;               // column groups of the lane split, group width (columns)
   float* jpart = nullptr;            // column-group partial sums [Q][nrows][BS]
   int* jctr = nullptr;               // per-warp-unit arrival counters (Q > 1), zero between calls

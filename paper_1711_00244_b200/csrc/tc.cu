@@ -990,7 +990,7 @@ bool list_fold_forced() {
 size_t tc_scale_floats(int B) { return (size_t)B * (kScaleChunks + 1); }
 
 bool tc_supported(const FcDev& L) {
-  return L.tivg && L.tivm && L.tNI > 0 && L.sNI > 0 && L.tbase && L.troff && L.tlist && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
+  return L.tivg && L.tivm && L.tNI > 0 && L.sNI > 0 && L.tbase && L.troff && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
          L.Lf == kFoldLutBits && L.Lg <= kLutMaxBits;
 }
 

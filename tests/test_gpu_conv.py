@@ -213,12 +213,16 @@ def test_c4_variable_batch_plan_under_budget(torch_dev):
     """SURVEY NEXT #1 on the device: AlexNet conv1-5 + fc6-8 under TOT = 128 MiB
     for K = 32 images.  conv1's per-image footprint (input, patches, conv/LRN
     outputs) caps the conv batch well below what the FC layers afford, so the
-    DP picks a variable-batch divisor chain; infer with it
-    reproduces the fixed-batch GPU scores (same kernels, different grouping)."""
+    DP picks a variable-batch divisor chain.  Infer with it: the
+    library's inference scratch stays within TOT (reading C-36), the scores
+    match the oracle chain (bf16 CONV emulation, C-21) within the bound of the
+    fixed-batch end-to-end test, and equal the fixed-batch GPU scores up to
+    rounding."""
     torch, dev = torch_dev
     import paper_1711_00244_b200 as cdn
     cfg = synth.CONFIGS["C4"]
     m = cdn.Model(0)
+    comps = []
     hw = 227
     for i, spec in enumerate(cfg.conv):
         _, c, buf, v = conv_case(i)
@@ -226,21 +230,77 @@ def test_c4_variable_batch_plan_under_budget(torch_dev):
                                              spec.groups, relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
                                              pool_s=2 if spec.pool else 0))
         hw = m.out_shape(i)[0]
+        comps.append(("conv", spec, c, v))
     for spec in cfg.fc:
         W, v = synth.fc_weights(spec, cfg.seed)
         c = compress.compress_layer(W, spec.density, spec.r, spec.k, v)
         m.load_layer(cdni.serialize([c.layer]), cdn.LayerDesc.fc(spec.relu))
+        comps.append(("fc", spec, c, v))
     K = 32
-    m.set_memory_budget(128 << 20)
+    tot = 128 << 20
+    m.set_memory_budget(tot)
     batches, predicted = m.plan(K)
     print("C4 plan under 128 MiB:", batches, f"{predicted:.3f} ms for {K} images")
     assert all(batches[i + 1] % batches[i] == 0 for i in range(len(batches) - 1))
     assert batches[0] < batches[-1]            # conv batch capped below the FC batch
     x = synth.conv_inputs(K, 227, 3, seed=1)
     s_plan = np.zeros((K, 1000), np.float32)
+    m.release_scratch()
+    m.scratch_bytes(reset_peak=True)
     m.infer(x, K, s_plan, on_device=False)
+    _, peak = m.scratch_bytes()
+    print(f"C4 scratch peak {peak / 2**20:.2f} MiB of {tot / 2**20:.0f} MiB")
+    assert peak <= tot
+    # the oracle chain (fp64 layers; CONV on bf16-rounded inputs and weights, C-21)
+    chain = x
+    for kind, spec, c, v in comps:
+        if kind == "conv":
+            chain = oracle_conv(spec, c, v, chain).astype(np.float32)
+        else:
+            chain = infer.fc_forward(sparse_q(c), chain.reshape(K, -1), v, apply_relu=spec.relu).astype(np.float32)
+    e = rel_err(s_plan, chain)
+    print(f"C4 planned scores vs oracle chain: {e:.2e}")
+    assert e <= 2e-3
     m.set_plan([K] * len(batches))
     s_fix = np.zeros((K, 1000), np.float32)
     m.infer(x, K, s_fix, on_device=False)
     assert rel_err(s_plan, s_fix) <= 1e-4
+    m.close()
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 3, 4])
+def test_conv_layer_decode_bit_exact(torch_dev, i):
+    """SURVEY §4 T3 on the CONV layers of C4 (r = k = 8, 256-entry codebooks,
+    8-bit gaps, densities 84/38/35/37/37 %): cdn_layer_decode's tokens (row,
+    column, symbol, codebook value) equal the oracle's pre-encoding streams
+    bit for bit, and the real tokens are exactly the kept weights."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    spec, c, buf, v = conv_case(i)
+    m = cdn.Model(0)
+    m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, IN_HW[i], IN_HW[i], spec.kh, spec.kw, spec.stride, spec.pad,
+                                         spec.groups, relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
+                                         pool_s=2 if spec.pool else 0))
+    n = m.decode_count(0)
+    assert n == c.val_tokens.size
+    row = torch.empty(n, dtype=torch.int32, device=dev)
+    col = torch.empty(n, dtype=torch.int32, device=dev)
+    sym = torch.empty(n, dtype=torch.uint8, device=dev)
+    val = torch.empty(n, dtype=torch.float32, device=dev)
+    m.decode(0, row, col, sym, val)
+    torch.cuda.synchronize()
+    R, Cc, S, V = (t.cpu().numpy() for t in (row, col, sym, val))
+    er = np.repeat(np.arange(c.row_tokens.size), c.row_tokens)
+    # columns by the C-01 prefix sum within each row
+    ec = np.empty(n, np.int64)
+    o = 0
+    for t in c.row_tokens:
+        ec[o:o + t] = np.cumsum(c.gap_tokens[o:o + t] + 1) - 1
+        o += t
+    assert np.array_equal(R, er)
+    assert np.array_equal(Cc, ec)
+    assert np.array_equal(S, c.val_tokens.astype(np.uint8))
+    assert np.array_equal(V.view(np.uint32), c.layer.codebook[c.val_tokens].astype(np.float32).view(np.uint32))
+    real = S != 0
+    assert real.sum() == c.mask.sum() and c.mask[R[real], Cc[real]].all()
     m.close()

@@ -167,3 +167,34 @@ def test_small_batch_infer_stack_c3(torch_dev):
     y = so.cpu().numpy()
     assert np.abs(y - h).max() / np.abs(h).max() <= 1e-4
     m.close()
+
+
+@pytest.mark.parametrize("cfg,i", [("C5", 0), ("C5", 2), ("C2", 0), ("C1", 0)])
+def test_cold_back_to_back_replicas(torch_dev, cfg, i):
+    """The b1_cold protocol as a correctness check: R resident replicas of a
+    layer, L2 flushed, launches back to back on one stream (programmatic
+    dependent launches; every CTA's stream pieces still in flight when its
+    warps start) -- every replica's output equal to the first one's and within
+    the oracle bound.  Catches staging races that a single warm launch hides."""
+    torch, dev = torch_dev
+    spec, c, buf, v = config_layer(cfg, i)
+    R = 6
+    ms = [load(buf, False) for _ in range(R)]
+    a = synth.fc_inputs(spec.cols, 1, 9)
+    x = torch.from_numpy(np.ascontiguousarray(a.T)).to(dev)
+    ys = [torch.full((spec.rows, 1), float("nan"), dtype=torch.float32, device=dev) for _ in range(R)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(dev)
+    ref = infer.fc_forward(c.dense_q(), a, v, apply_relu=False)[0]
+    for rep in range(3):
+        flush.zero_()
+        torch.cuda.synchronize()
+        for m, y in zip(ms, ys):
+            m.layer_forward(0, x, 1, 1, y, 1, stream=s.cuda_stream)
+        torch.cuda.synchronize()
+        out = [y.cpu().numpy()[:, 0] for y in ys]
+        for o in out:
+            assert np.array_equal(o, out[0])
+            assert np.abs(o - ref).max() / np.abs(ref).max() <= 1e-4
+    for m in ms:
+        m.close()

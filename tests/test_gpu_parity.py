@@ -607,11 +607,15 @@ def test_band_repeated_launches_are_deterministic(torch_dev):
 
 def test_c3_planner_under_64mib_budget(torch_dev):
     """Config C3: AlexNet FC stack, TOT = 64 MiB, batch chosen by the planner
-    from 1..K.  On the device-profiled Time table, the library's
-    plan is a divisor chain, feasible under the EXACT memory model, never
-    better than the exact oracle DP (C-25), equal to the host C++ DP on the same
-    table; infer with it (remainder re-plan) matches the oracle chain."""
+    from 1..K.  On the device-profiled Time table and the
+    library's memory model (IN / OUT / WS with every workspace, reading C-24),
+    the library's plan is a divisor chain, feasible under the EXACT memory
+    model, never better than the exact oracle DP (C-25); infer with it
+    (remainder re-plan) matches the oracle chain, the library's
+    inference scratch never exceeds TOT (reading C-36), and the DP's predicted
+    time matches the measured one."""
     torch, dev = torch_dev
+    import time
     import paper_1711_00244_b200 as cdn
     from oracle import planner as oplanner
     cfg = synth.CONFIGS["C3"]
@@ -625,28 +629,52 @@ def test_c3_planner_under_64mib_budget(torch_dev):
     m.set_memory_budget(cfg.tot_bytes)
     T = m.profile(K, 5)
     batches, predicted = m.plan(K)
-    st = [m.stats(i) for i in range(3)]
-    inb = [4 * s["in_features"] for s in st]
-    outb = [4 * s["out_features"] for s in st]
-    ws = [s["ws_bytes"] for s in st]
-    p = oplanner.Problem([{B: float(T[i][B - 1]) for B in range(1, K + 1)} for i in range(3)], inb, outb, ws,
-                         cfg.tot_bytes)
+    inb, outb, ws = m.memory_model(K)
+    p = oplanner.Problem([{B: float(T[i][B - 1]) for B in range(1, K + 1)} for i in range(3)], list(inb), list(outb),
+                         list(ws), cfg.tot_bytes)
     assert all(batches[i + 1] % batches[i] == 0 for i in range(2))
     cost = oplanner.chain_cost(p, batches)
     assert np.isfinite(cost)
     exact = oplanner.dp_plan(p, K)
     assert cost / batches[-1] >= exact.per_image * (1 - 1e-9)
-    bs2, opt2 = cdn.plan_dp(T, inb, outb, ws, cfg.tot_bytes, 0.0, step=64 * 1024)
-    assert bs2 == batches
     assert predicted > 0
-    # the whole request through the planned executor
+    # the whole request through the planned executor, host buffers: scratch <= TOT
     a = synth.fc_inputs(cfg.fc[0].cols, K, 0)
     scores = np.zeros((K, cfg.fc[-1].rows), np.float32)
+    m.release_scratch()
+    m.scratch_bytes(reset_peak=True)
     m.infer(a, K, scores, on_device=False)
+    cur, peak = m.scratch_bytes()
+    print(f"C3 plan {batches}: scratch peak {peak / 2**20:.2f} MiB of {cfg.tot_bytes / 2**20:.0f} MiB")
+    assert peak <= cfg.tot_bytes
     x = a
     for c, v, relu in comps:
         x = infer.fc_forward(sparse_q(c), x, v, apply_relu=relu).astype(np.float32)
     assert rel_err(scores, x) <= TOL
+    # device buffers: the same bound, and the DP's predicted time against the
+    # measured one (graph replay of the planned call, median of 20)
+    _, predicted_dev = m.plan(K)
+    xi = torch.from_numpy(a).to(dev)
+    so = torch.zeros((K, cfg.fc[-1].rows), dtype=torch.float32, device=dev)
+    s = torch.cuda.Stream(dev)
+    m.scratch_bytes(reset_peak=True)
+    for _ in range(3):
+        m.infer(xi, K, so, on_device=True, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(20):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        m.infer(xi, K, so, on_device=True, stream=s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    meas = float(np.median(ms))
+    _, peak = m.scratch_bytes()
+    assert peak <= cfg.tot_bytes
+    print(f"C3 predicted {predicted_dev:.4f} ms, measured {meas:.4f} ms")
+    assert abs(predicted_dev - meas) <= 0.10 * meas
+    assert rel_err(so.cpu().numpy(), x) <= TOL
     m.close()
 
 

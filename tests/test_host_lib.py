@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     lib = cdn.load_library()
     for n in sorted(names):
         assert hasattr(lib, n), n
-    assert cdn.abi_version() == 1
+    assert cdn.abi_version() == 2
 
 
 def _oracle_bytes(W, d, r, k, bias):
