@@ -421,7 +421,9 @@ def bench_b1(cdn, torch, dev, R, flush, pk):
         warm = med(lambda: timed([models[0]] * R))
         one = med(single)
         algo = st["algo_bytes_fixed"] + 4 * spec.cols + 4 * spec.rows
-        row = {"kernel": models[0].kernel_name(0, 1), "algo_bytes": algo, "index_bytes": st["index_bytes"],
+        row = {"kernel": models[0].kernel_name(0, 1), "algo_bytes": algo,
+               "call_index_bytes": st["call_index_bytes"], "resident_bytes": st["resident_bytes"],
+               "resident_index_bytes": st["index_bytes"],
                "cold_us": cold * 1e3, "cold_gbs": algo / (cold / 1e3) / 1e9,
                "cold_frac": algo / (cold / 1e3) / 1e9 / pk["hbm_gbs"],
                "warm_us": warm * 1e3, "single_call_us": one * 1e3}

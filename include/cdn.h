@@ -78,9 +78,15 @@ typedef struct {
   uint64_t nnz;                  /* real (non-pad) tokens of this rank's rows         */
   uint64_t stream_bytes;         /* ceil(val bits/8) + ceil(gap bits/8) of the shard  */
   uint64_t algo_bytes_fixed;     /* stream + row_ptr + codebook + tables + bias bytes */
-  uint64_t index_bytes;          /* decode-lane index bytes (overhead)                */
+  uint64_t index_bytes;          /* every resident restart index (overhead): decode-  */
+                                 /* lane records and token starts, interval indices,  */
+                                 /* tensor-core list layout, merged-stream lanes      */
   uint64_t ws_bytes;             /* WS(i): device scratch the layer uses     */
   uint64_t in_features, out_features; /* per image                                     */
+  uint64_t resident_bytes;       /* every device byte the loaded layer keeps resident */
+                                 /* (streams, merged stream, indices, tables, bias)   */
+  uint64_t call_index_bytes;     /* index bytes the small-batch kernel (k_fc_j) reads */
+                                 /* per call (lane records + row starts)              */
 } cdn_layer_stats;
 
 /* ---- library / errors ------------------------------------------------- */

@@ -56,7 +56,8 @@ class LayerStats(C.Structure):
                 ("lanes_per_row", C.c_uint32), ("max_len_val", C.c_uint32), ("max_len_gap", C.c_uint32),
                 ("tokens", C.c_uint64), ("nnz", C.c_uint64), ("stream_bytes", C.c_uint64),
                 ("algo_bytes_fixed", C.c_uint64), ("index_bytes", C.c_uint64), ("ws_bytes", C.c_uint64),
-                ("in_features", C.c_uint64), ("out_features", C.c_uint64)]
+                ("in_features", C.c_uint64), ("out_features", C.c_uint64), ("resident_bytes", C.c_uint64),
+                ("call_index_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

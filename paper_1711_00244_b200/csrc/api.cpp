@@ -118,6 +118,7 @@ struct Layer {
   DBuf msv, msg;        // small-batch multi-symbol LUTs
   DBuf jw, jrow, jlane, jlut, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
   std::vector<uint32_t> jrow_h;               // host copy of jrow (per-CTA stream ranges)
+  JPlan jplan[3];                             // launch plans of k_fc_j for B = 1, 2, 3-4 (built at first use)
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
   bool blocked = false;  // block-contiguous container (Alg. 2, C-34): tensor-core path only
   cdn_layer_stats stats{};
@@ -386,7 +387,8 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     if (const char* e = std::getenv("CDN_JQ")) jq = std::max(1, std::min(G, std::atoi(e)));
     while (G % jq) jq >>= 1;
     JointIndex jx;
-    if (build_joint_index(H, L.row0, L.row1, G, jq, jx)) {
+    const auto jlut = build_joint_lut(H.val, H.gap, jl);
+    if (build_joint_index(H, L.row0, L.row1, G, jq, jlut, jl, jx)) {
       // per-row staging slot: the largest byte span of one (row, column group)
       uint32_t sub = 0;
       const int GQ = G / jq;
@@ -413,7 +415,6 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
         std::memcpy(blob.data() + o, p, n);
         return (uint32_t)o;
       };
-      const auto jlut = build_joint_lut(H.val, H.gap, jl);
       const auto vl = build_lut(H.val, Lv), gl = build_lut(H.gap, Lg), vt = build_tab(H.val), gt = build_tab(H.gap);
       std::vector<uint16_t> vs = H.val.sorted, gs = H.gap.sorted;
       vs.push_back(0);
@@ -665,7 +666,14 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   s.stream_bytes = (v1 - v0 + 7) / 8 + (g1 - g0 + 7) / 8;
   s.algo_bytes_fixed = s.stream_bytes + 8ull * (nr + 1) + 4ull * H.codebook.size() +
                        3ull * (H.val.n + H.gap.n) + 4ull * nout;
-  s.index_bytes = ix.rec64 ? 8ull * ix.rec64v.size() : 4ull * ix.rec32.size();
+  s.index_bytes = L.rec.n + L.tok.n + L.ivg.n + L.ivm.n + L.tivg.n + L.tivm.n + L.tbase.n + L.troff.n + L.jlane.n +
+                  L.jrow.n;
+  s.call_index_bytes = L.jlane.n + L.jrow.n;
+  s.resident_bytes = 0;
+  for (const DBuf* b : {&L.vw, &L.gw, &L.rp, &L.rec, &L.tok, &L.vlut, &L.glut, &L.vtab, &L.gtab, &L.vsorted,
+                        &L.gsorted, &L.cb, &L.bias, &L.flut, &L.ivg, &L.ivm, &L.tivg, &L.tivm, &L.tbase, &L.troff,
+                        &L.msv, &L.msg, &L.jw, &L.jrow, &L.jlane, &L.jlut})
+    s.resident_bytes += b->n;
   s.ws_bytes = 0;
   s.in_features = L.in_elems();
   s.out_features = L.out_elems();
@@ -810,7 +818,8 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
   }();
   const bool force_fold = small_kernel == 1;
   if (B <= 4 && small_kernel == 0 && j_supported(L.dev)) {
-    const JPlan p = plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data());
+    JPlan& p = L.jplan[B <= 1 ? 0 : (B <= 2 ? 1 : 2)];  // cached: the plan is host work on every call otherwise
+    if (p.nrb == 0) p = plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data());
     if (p.ok) {
       CUDA_OK(launch_fc_j(L.dev, p, x, ldx, B, y, ldy, relu, s));
       return;

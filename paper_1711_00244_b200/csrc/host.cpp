@@ -333,7 +333,8 @@ void build_interval_index(const HostLayer& L, uint32_t r0, uint32_t r1, uint32_t
 
 // ------------------------------------------------- merged token stream
 
-bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, JointIndex& out) {
+bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, const std::vector<uint32_t>& lut,
+                       int Lb, JointIndex& out) {
   const uint32_t nr = r1 - r0;
   if (L.cols > 65535 || G < 1 || Q < 1 || G % Q) return false;
   uint64_t total = 0;
@@ -366,7 +367,6 @@ bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int 
   std::vector<int32_t> tprev;   // previous column before each token
   std::vector<int32_t> tcol;    // column of each token
   std::vector<uint8_t> tpad;    // token is padding
-  std::vector<size_t> real_at;  // token index of each real token
   for (uint32_t i = r0; i < r1; ++i) {
     const size_t li = i - r0;
     out.row_bit[li] = (uint32_t)pos;
@@ -374,7 +374,6 @@ bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int 
     tprev.clear();
     tcol.clear();
     tpad.clear();
-    real_at.clear();
     uint64_t vpos = L.rp[2ull * i], gpos = L.rp[2ull * i + 1];
     const uint64_t vend = L.rp[2ull * i + 2];
     int32_t prev = -1;
@@ -389,18 +388,40 @@ bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int 
       put(L.gap.code_of[gs], gl);
       prev += (int32_t)gs + 1;
       tcol.push_back(prev);
-      if (vs != 0) real_at.push_back(tbit.size() - 1);
       vpos += vl;
       gpos += gl;
     }
     const size_t T = tbit.size();
+    // the kernel's steps over tokens [a, b): from a, one joint-LUT lookup per
+    // step consumes the padding run and the real token after it (or, for a
+    // window the LUT cannot resolve, one token through the slow path)
+    auto window_at = [&](uint64_t bit) {
+      const uint64_t w = bit >> 5, o = bit & 31;
+      const uint64_t v = ((uint64_t)out.words[w] << 32) | out.words[w + 1];
+      return (uint32_t)(v >> (32 - o));
+    };
+    std::vector<size_t> step_at;
+    auto steps = [&](size_t a, size_t b) {
+      step_at.clear();
+      size_t t = a;
+      while (t < b) {
+        step_at.push_back(t);
+        const uint32_t e = lut[window_at(out.row_bit[li] + tbit[t]) >> (32 - Lb)];
+        if (e == 0) {
+          ++t;
+        } else {
+          const uint32_t end = tbit[t] + (e >> 27);
+          while (t < b && tbit[t] < end) ++t;
+        }
+      }
+    };
     // column group q = the tokens from the first with column >= q*Kq, moved
-    // back over the padding before it; inside a group, lane j starts at its
-    // real token of rank ~j*R_q/GQ (the kernel spends one step per real
-    // token: padding folds into the lookup of the token it precedes), again
-    // moved back over padding -- no lane ends with padding
+    // back over the padding before it (a group never ends with padding, so no
+    // lookup folds padding into the next group's first real token); inside a
+    // group, lane j starts at the kernel's step ~j*S_q/GQ of the group (S_q
+    // steps), so every lane runs the same number of lookups (+-1) and ends
+    // exactly at a step boundary
     size_t bprev = 0;
-    size_t rq = 0;  // first real-token rank of the group
     for (int q = 0; q < Q; ++q) {
       size_t gb = 0;  // group's first token
       if (q > 0) {
@@ -408,29 +429,22 @@ bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int 
         gb = std::max(gb, bprev);
         while (gb > bprev && tpad[gb - 1]) --gb;
       }
-      size_t ge = T;  // next group's first token (before moving back): the group's real tokens end there
+      size_t ge = T;  // next group's first token
       if (q + 1 < Q) {
         ge = 0;
         while (ge < T && tcol[ge] < (int64_t)(q + 1) * Kq) ++ge;
+        ge = std::max(ge, gb);
+        while (ge > gb && tpad[ge - 1]) --ge;
       }
-      size_t re = rq;
-      while (re < real_at.size() && real_at[re] < ge) ++re;
-      const size_t R = re - rq;
+      steps(gb, ge);
+      const size_t S = step_at.size();
       for (int jj = 0; jj < GQ; ++jj) {
-        size_t b = gb;
-        if (jj > 0) {
-          b = R ? real_at[rq + std::min<size_t>((uint64_t)jj * R / (uint64_t)GQ, R - 1)] : ge;
-          if (R == 0) b = std::max(gb, std::min(ge, T));
-        }
-        b = std::max(b, bprev);
-        while (b > bprev && tpad[b - 1]) --b;
-        b = std::max(b, bprev);
-        bprev = b;
-        const uint32_t off = b < T ? tbit[b] : (uint32_t)(pos - out.row_bit[li]);
-        const int32_t pc = b < T ? tprev[b] : prev;
+        const size_t bb = jj == 0 ? gb : (S ? step_at[(uint64_t)jj * S / (uint64_t)GQ] : ge);
+        const uint32_t off = bb < T ? tbit[bb] : (uint32_t)(pos - out.row_bit[li]);
+        const int32_t pc = bb < T ? tprev[bb] : prev;
         out.lane[li * G + q * GQ + jj] = off | ((uint32_t)(pc + 1) << 16);
       }
-      rq = re;
+      bprev = ge;
     }
   }
   out.row_bit[nr] = (uint32_t)pos;

@@ -88,10 +88,11 @@ void build_lane_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, LaneI
 // both (a bit permutation of the same codes: the same number of bits).
 // Decode lanes: G per row in Q column groups (group q = G/Q lanes holding the
 // columns [q Kq, (q+1) Kq), so a CTA of group q stages only that slice of x);
-// inside a group the lanes are split by REAL-token count (lane j starts near
-// the group's real token of rank j R_q Q/G), every boundary moved back over
-// padding tokens so that no lane ends with padding (a row never does: padding
-// precedes a real token, C-02).  A lane record = bit offset of its first
+// inside a group the lanes are split at the kernel's joint-LUT steps (lane j
+// starts at the group's step ~j S_q Q/G: every lane runs the same number of
+// lookups, +-1); group boundaries are moved back over padding tokens so no
+// lookup folds a group's padding into the next group's first real token (a
+// row never ends with padding: padding precedes a real token, C-02).  A lane record = bit offset of its first
 // token from the row start (u16) | (previous column + 1) << 16 (u16).
 struct JointIndex {
   int G = 1, Q = 1;                // lanes per row; column groups (lanes [q G/Q, (q+1) G/Q) hold columns [q Kq, (q+1) Kq))
@@ -103,7 +104,10 @@ struct JointIndex {
   uint32_t max_row_bits = 0;
 };
 // false (nothing built) when a row has >= 2^16 bits or cols > 65535
-bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, JointIndex& out);
+// lut / Lb: the joint LUT the kernel will use (build_joint_lut): lanes start
+// at the kernel's lookup steps, so they are balanced in steps
+bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, const std::vector<uint32_t>& lut,
+                       int Lb, JointIndex& out);
 // Joint LUT over the next Lb bits of the merged stream: the leading padding
 // tokens (val symbol 0 with its gap code) and then one real token, when they
 // lie inside the window.  Entry: 4 * val symbol (bits 0-9) | 4 * column

@@ -80,7 +80,7 @@ struct TcArgs {
   long W;                     // total tile steps = tiles * nkt (stream-K)
   unsigned long long* trace;    // debug (env CDN_TC_TRACE): CTA 0 event clocks [event][256], else null
   int yt;                       // 1: y image-major [B][ldy] (the class scores of the last layer), else [rows][ldy]
-  const float* xsc;             // [B] per-image power-of-two scales of the fp16 split (k_xscale_*)
+  const float* xsc;             // [2B] per-image power-of-two scales of the fp16 split and their inverses (k_xscale_*)
   float winv;                   // 1 / the layer's weight scale
 };
 
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         } else {
           // undo the fp16 split's scales: D / (s_W s_b), exact (powers of two)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] *= a.winv / __ldg(a.xsc + min(b0 + c + i, a.B - 1));
+          for (int i = 0; i < 16; ++i) v[i] *= a.winv * __ldg(a.xsc + a.B + min(b0 + c + i, a.B - 1));
         }
         if (whole) {
           if (row < L.wrows) {
@@ -546,6 +546,7 @@ __device__ __forceinline__ float pow2_scale(float m) {
 // Feature-major x [K][ldx]: block = 32 images x 8 row groups; image-major x
 // [B][ldx]: block = one image.
 constexpr int kScaleChunks = 8;
+// sc[b] = s_b, sc[B + b] = 1 / s_b (exact: a power of two)
 __device__ __forceinline__ void scale_finish(float m, int b, int B, int nparts, float* part, int* ctr, float* sc) {
   part[(size_t)blockIdx.y * B + b] = m;
   __threadfence();
@@ -553,7 +554,9 @@ __device__ __forceinline__ void scale_finish(float m, int b, int B, int nparts, 
     __threadfence();
     float mm = 0.f;
     for (int i = 0; i < nparts; ++i) mm = fmaxf(mm, __ldcg(&part[(size_t)i * B + b]));
-    sc[b] = pow2_scale(mm);
+    const float s = pow2_scale(mm);
+    sc[b] = s;
+    sc[B + b] = 1.0f / s;
     ctr[b] = 0;
   }
 }
@@ -987,7 +990,7 @@ bool list_fold_forced() {
 
 }  // namespace
 
-size_t tc_scale_floats(int B) { return (size_t)B * (kScaleChunks + 1); }
+size_t tc_scale_floats(int B) { return (size_t)B * (kScaleChunks + 2); }
 
 bool tc_supported(const FcDev& L) {
   return L.tivg && L.tivm && L.tNI > 0 && L.sNI > 0 && L.tbase && L.troff && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
@@ -1073,10 +1076,10 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
                          bool x_image_major, bool y_image_major) {
-  // per-image scales of the fp16 split: scw = [B scales | kScaleChunks x B
-  // partial maxima]; xctr: >= B arrival counters, zero between calls
+  // per-image scales of the fp16 split: scw = [B scales | B inverse scales |
+  // kScaleChunks x B partial maxima]; xctr: >= B arrival counters, zero between calls
   float* xsc = scw;
-  float* xpart = scw + (size_t)B;
+  float* xpart = scw + 2 * (size_t)B;
   ktimer_begin("k_split_x", s);
   if (x_image_major) {
     k_xscale_rows<<<dim3((unsigned)B, 4), 256, 0, s>>>(x, L.wcols, ldx, B, xpart, xctr, xsc);
