@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--b1-replicas", type=int, default=8, help="cold-L2 B=1 replicas (0: skip)")
     p.add_argument("--no-c4", action="store_true", help="skip the AlexNet conv+fc (config C4) line")
+    p.add_argument("--shard", default="cols", choices=["rows", "cols"],
+                   help="N > 1: FC layers in row blocks (all-gather) or Megatron-style column blocks (reduce-scatter)")
     return p.parse_args()
 
 
@@ -96,8 +98,10 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_model(cdn, rank, world, nccl_id, cdni_bytes):
+def build_model(cdn, rank, world, nccl_id, cdni_bytes, shard="rows"):
     m = cdn.Model(int(os.environ.get("LOCAL_RANK", 0)), rank=rank, world=world, nccl_id=nccl_id)
+    if world > 1 and shard == "cols":
+        m.set_sharding(cdn.CDN_SHARD_COLS)
     for spec, buf in zip(synth.CONFIGS[CFG].fc, cdni_bytes):
         m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
     return m
@@ -136,7 +140,7 @@ def run_ours(args):
     B = args.batch
     specs = synth.CONFIGS[CFG].fc
     layers = compressed_layers(cdn)
-    m = build_model(cdn, rank, world, nccl_id, layers)
+    m = build_model(cdn, rank, world, nccl_id, layers, args.shard)
     m.set_plan([B] * len(specs))
     # The tensor-core path for every layer: what the library's first-use autotune
     # picks for this workload on an idle B200 (scripts/grid_report.py), fixed here
@@ -227,9 +231,9 @@ def run_ours(args):
         e_ms = float(t.item())
 
     # ---- per-layer kernel durations inside the same workload (roofline of the dominant kernel)
-    xs = []
-    feats = [specs[0].cols] + [s.rows for s in specs]
-    bufs = [torch.from_numpy(np.ascontiguousarray(a.T)).to(dev)]
+    # (per rank: its row block, or for column-sharded layers its column block of
+    # the input and the partial sums of every row)
+    bufs = [torch.from_numpy(np.ascontiguousarray(a[:, stats[0]["col_begin"]:stats[0]["col_end"]].T)).to(dev)]
     for i, s in enumerate(specs):
         bufs.append(torch.zeros((stats[i]["row_end"] - stats[i]["row_begin"], B), dtype=torch.float32, device=dev))
     lay_ms = np.zeros(len(specs))
@@ -238,7 +242,8 @@ def run_ours(args):
         flush.zero_()
         torch.cuda.synchronize(dev)
         for i in range(len(specs)):
-            xin = bufs[i] if i == 0 else torch.zeros((feats[i], B), dtype=torch.float32, device=dev)
+            kin = max(1, stats[i]["col_end"] - stats[i]["col_begin"])
+            xin = bufs[i] if i == 0 else torch.zeros((kin, B), dtype=torch.float32, device=dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             m.layer_forward(i, xin, B, B, bufs[i + 1], B, stream=sp)
@@ -257,7 +262,10 @@ def run_ours(args):
     lay = [i for i in range(len(specs)) if kern_of[i] == dom_k]
     def nloc_of(i):
         return stats[i]["row_end"] - stats[i]["row_begin"]
-    useful = sum(2.0 * stats[i]["nnz"] * B + nloc_of(i) * B for i in lay) * args.steps
+
+    def colfrac(i):  # share of the layer's columns this rank multiplies (1: not column-sharded)
+        return (stats[i]["col_end"] - stats[i]["col_begin"]) / max(1, stats[i]["cols"])
+    useful = sum(2.0 * stats[i]["nnz"] * colfrac(i) * B + nloc_of(i) * B for i in lay) * args.steps
     t_s = k_ms / 1e3
     if dom_k == "k_fc_tc":
         # The method's own work (2 nnz B + N B useful flops, pads excluded) per
@@ -268,7 +276,7 @@ def run_ours(args):
         tn = 128 if B <= 128 else 256  # image tile of the kernel (tc.cu plan_fc_tc)
 
         def dense(i):
-            kpad = (specs[i].cols + 63) // 64 * 64
+            kpad = (stats[i]["col_end"] - stats[i]["col_begin"] + 63) // 64 * 64
             return 3 * 2.0 * (-(-nloc_of(i) // 128) * 128) * kpad * (-(-B // tn) * tn)
         work = sum(dense(i) for i in lay) * args.steps
         cs = clk.summary()
@@ -319,7 +327,8 @@ def run_ours(args):
                                 "oracle (tests/test_gpu_parity.py)"},
         "data": "synthetic",
         "config": {"workload": "C5 VGG-16 FC stack fc6/fc7/fc8 (4%/4%/23%, r=5, k=4, Huffman)",
-                   "global_batch": B, "parallelism": f"row-shard{world}" if world > 1 else "single",
+                   "global_batch": B,
+                   "parallelism": (f"{'col' if args.shard == 'cols' else 'row'}-shard{world}" if world > 1 else "single"),
                    "l2": "flushed (256 MB write) between timed steps", "plan": [B] * len(specs)},
         "compressed_gbs": comp_bytes / (tot_ms / args.steps / 1e3) / 1e9,
         "compressed_bytes": comp_bytes,

@@ -87,6 +87,8 @@ typedef struct {
                                  /* (streams, merged stream, indices, tables, bias)   */
   uint64_t call_index_bytes;     /* index bytes the small-batch kernel (k_fc_j) reads */
                                  /* per call (lane records + row starts)              */
+  uint32_t col_begin, col_end;   /* input columns this rank multiplies (column-sharded */
+                                 /* FC layers: the rank's K block; else 0, cols)       */
 } cdn_layer_stats;
 
 /* ---- library / errors ------------------------------------------------- */
@@ -223,6 +225,25 @@ cdn_status cdn_model_profile(cdn_model* m, int Bmax, int reps, double* time_ms);
  * same numbers cdn_model_plan uses.  Arrays of n_layers.  Errors: CDN_E_ARG. */
 cdn_status cdn_model_memory_model(cdn_model* m, int Bmax, uint64_t* in_bytes, uint64_t* out_bytes,
                                   uint64_t* ws_bytes);
+
+/* ---- sharding of the FC layers across ranks (call before loading layers):
+ * CDN_SHARD_ROWS (default): rank r keeps a contiguous block of
+ * output rows; layer outputs are all-gathered.  CDN_SHARD_COLS (Megatron-style,
+ * SURVEY §8(f) row 4): rank r multiplies a contiguous block of input columns
+ * (K tiles of 64) for every output row; the partial sums are reduce-scattered
+ * into the next layer's column blocks (bias and ReLU applied after the sum)
+ * and reduced to rank 0 after the last layer -- the first layer reads only its
+ * column block of the input.  Column-sharded layers run the tensor-core path;
+ * cdn_layer_forward on such a layer returns the rank's partial sums (no bias,
+ * no ReLU) from its column block of x ([col_end - col_begin][ldx]).
+ * Errors: CDN_E_ARG, CDN_E_STATE (layers already loaded). */
+#define CDN_SHARD_ROWS 0
+#define CDN_SHARD_COLS 1
+cdn_status cdn_model_set_sharding(cdn_model* m, int mode);
+
+/* The column block [*k0, *k1) rank `rank` of `world` multiplies in a
+ * column-sharded layer with `cols` input columns (host only). */
+cdn_status cdn_col_block(uint32_t cols, int rank, int world, uint32_t* k0, uint32_t* k1);
 
 /* ---- inference scratch (the memory TOT bounds: everything but the
  * resident compressed model -- level activation buffers, workspaces, per-call

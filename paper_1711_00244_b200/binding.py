@@ -57,7 +57,7 @@ class LayerStats(C.Structure):
                 ("tokens", C.c_uint64), ("nnz", C.c_uint64), ("stream_bytes", C.c_uint64),
                 ("algo_bytes_fixed", C.c_uint64), ("index_bytes", C.c_uint64), ("ws_bytes", C.c_uint64),
                 ("in_features", C.c_uint64), ("out_features", C.c_uint64), ("resident_bytes", C.c_uint64),
-                ("call_index_bytes", C.c_uint64)]
+                ("call_index_bytes", C.c_uint64), ("col_begin", C.c_uint32), ("col_end", C.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -77,6 +77,8 @@ _SIGS = {
     "cdn_model_plan": (C.c_int32, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "cdn_model_set_plan": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int), C.c_int]),
     "cdn_model_infer": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
+    "cdn_model_set_sharding": (C.c_int32, [C.c_void_p, C.c_int]),
+    "cdn_col_block": (C.c_int32, [C.c_uint32, C.c_int, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "cdn_model_scratch_bytes": (C.c_int32, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int]),
     "cdn_model_release_scratch": (C.c_int32, [C.c_void_p]),
     "cdn_layer_forward": (C.c_int32, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
@@ -213,6 +215,17 @@ def debug_gemm_bf16(A, M: int, Wt, N: int, Kpad: int, bias, relu: bool, out, ldo
                                               int(bool(relu)), _ptr(out), int(ldo), stream or None))
 
 
+CDN_SHARD_ROWS, CDN_SHARD_COLS = 0, 1
+
+
+def col_block(cols: int, rank: int, world: int) -> Tuple[int, int]:
+    """Input columns [k0, k1) rank `rank` of `world` multiplies in a column-sharded layer."""
+    lib = load_library()
+    k0, k1 = C.c_uint32(), C.c_uint32()
+    _check(lib.cdn_col_block(int(cols), int(rank), int(world), C.byref(k0), C.byref(k1)))
+    return k0.value, k1.value
+
+
 def debug_host_walk_shard(cdni: bytes, rank: int, world: int, layer_in_file: int = 0):
     """Host walk of one rank's row-block shard (tokens with global row indices)."""
     lib = load_library()
@@ -310,6 +323,10 @@ class Model:
     def set_kernel_policy(self, band_min_batch: int = 0, tc_min_batch: int = 0):
         """B >= tc_min_batch -> tensor-core kernel; B >= band_min_batch -> band kernel (0: defaults)."""
         _check(self._lib.cdn_model_set_kernel_policy(self._h, int(band_min_batch), int(tc_min_batch)))
+
+    def set_sharding(self, mode: int):
+        """CDN_SHARD_ROWS (0) or CDN_SHARD_COLS (1); before loading layers."""
+        _check(self._lib.cdn_model_set_sharding(self._h, int(mode)))
 
     def scratch_bytes(self, reset_peak: bool = False) -> Tuple[int, int]:
         """(current, high-water) bytes of inference scratch (cdn_model_scratch_bytes)."""

@@ -121,6 +121,11 @@ struct Layer {
   JPlan jplan[3];                             // launch plans of k_fc_j for B = 1, 2, 3-4 (built at first use)
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
   bool blocked = false;  // block-contiguous container (Alg. 2, C-34): tensor-core path only
+  // column-sharded FC layer (CDN_SHARD_COLS, world > 1): this rank multiplies
+  // K tiles [kt0, kt1) = input columns [kc0, kc1) for every output row
+  bool col = false;
+  int kt0 = 0, kt1 = -1;
+  uint32_t kc0 = 0, kc1 = 0;
   cdn_layer_stats stats{};
   bool is_conv() const { return desc.kind == CDN_LAYER_CONV; }
   // features per image this layer produces (NHWC flatten for CONV, C-22)
@@ -165,10 +170,14 @@ struct Model {
   DBuf tc_xh, tc_xl;            // tensor-core FC: fp16 hi / lo split of the activations
   DBuf tc_sc, tc_ctr;           // tensor-core FC: per-image split scales; their arrival counters (zero between calls)
   Acct scratch;                 // inference scratch of this model (every buffer above and the layers' workspaces)
+  int sharding = CDN_SHARD_ROWS;  // FC layers across ranks (cdn_model_set_sharding)
+  cudaStream_t comm_s = nullptr;  // world > 1: the exchanges, overlapped with the next micro-batch's compute
+  std::vector<cudaEvent_t> mb_ev; // micro-batch handovers compute -> exchange, exchange -> compute
+  DBuf part, rsblk;             // column sharding: a layer's partial sums (all rows), the reduced block
   std::vector<int> last_plan;   // plan of the last budgeted round (its scratch is what is allocated)
   void tag_scratch() {
     for (DBuf* b : {&stage[0], &stage[1], &out, &loc, &gath, &host_stage, &conv_a, &conv_o, &conv_t, &ctmp, &tc_xh,
-                    &tc_xl, &tc_sc, &tc_ctr})
+                    &tc_xl, &tc_sc, &tc_ctr, &part, &rsblk})
       b->acct = &scratch;
   }
   // CUDA graphs of repeated infer calls (same buffers, K, plan and state):
@@ -185,6 +194,25 @@ struct Model {
 };
 
 uint32_t rows_per_rank(uint32_t rows, int world) { return (rows + world - 1) / world; }
+
+// Column block of rank r in a column-sharded layer with `cols` input columns:
+// contiguous K tiles of 64 (the tensor-core K tile), ceil(tiles / world) per
+// rank.  Also the row block of the reduce-scatter that produces that input.
+struct ColBlock {
+  int kt0, kt1;
+  uint32_t k0, k1, per;  // columns [k0, k1); per = 64 * tiles per rank (every rank's block height)
+};
+ColBlock col_block(uint32_t cols, int rank, int world) {
+  const int nkt = (int)((cols + 63) / 64);
+  const int per = (nkt + world - 1) / world;
+  ColBlock b;
+  b.kt0 = std::min(nkt, rank * per);
+  b.kt1 = std::min(nkt, (rank + 1) * per);
+  b.k0 = std::min<uint32_t>(cols, (uint32_t)b.kt0 * 64);
+  b.k1 = std::min<uint32_t>(cols, (uint32_t)b.kt1 * 64);
+  b.per = (uint32_t)per * 64;
+  return b;
+}
 
 // Upload one stream slice [b0, b1) bits as big-endian words starting at word b0/32.
 void upload_words(DBuf& d, const std::vector<uint8_t>& bytes, uint64_t b0, uint64_t b1, uint64_t* base_bit) {
@@ -326,7 +354,9 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   // FC: row-block shard per rank; CONV: replicated (every rank
   // holds all filters and, in infer, runs the conv layers on the whole batch:
   // the conv trunk is not split across ranks).
-  const ShardSlice sl = shard_slice(H, m.rank, m.world, conv);
+  const bool colsh = !conv && m.world > 1 && m.sharding == CDN_SHARD_COLS;
+  if (colsh && blocked) throw Error(CDN_E_UNSUPPORTED, "column sharding of a block-contiguous layer");
+  const ShardSlice sl = shard_slice(H, m.rank, m.world, conv || colsh);
   L.row0 = sl.row0;
   L.row1 = sl.row1;
   const uint32_t nr = L.row1 - L.row0;
@@ -355,12 +385,12 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     // LUT width: wider windows fold more tokens per lookup, but every CTA
     // stages the table (4 << jL bytes), so small layers take narrower ones.
     // Lanes per row of this kernel (its own split, independent of the lane
-    // index above): enough lanes for ~28 warps per SM, none shorter than ~8 tokens
+    // index above): enough lanes for ~28 warps per SM, none shorter than ~2 tokens (measured: C1 at 4 tokens per lane beats 16)
     int G = 1;
     {
       const double toks = (double)ix.tokens / std::max<uint32_t>(1, nr);
       const double want = (double)m.num_sms * 28 * 32 / std::max<uint32_t>(1, nr);
-      while (G < 32 && G < want && toks / (2 * G) >= 8.0) G *= 2;
+      while (G < 32 && G < want && toks / (2 * G) >= 2.0) G *= 2;
       if (const char* e = std::getenv("CDN_JG")) G = std::max(1, std::min(32, std::atoi(e)));
     }
     uint64_t tb = 0, rmax = 0;
@@ -651,6 +681,15 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.ivg = L.ivg.as<uint2>();
   f.ivm = L.ivm.as<uint16_t>();
 
+  if (colsh) {
+    const ColBlock cb = col_block(H.wcols, m.rank, m.world);
+    L.col = true;
+    L.kt0 = cb.kt0;
+    L.kt1 = cb.kt1;
+    L.kc0 = cb.k0;
+    L.kc1 = cb.k1;
+    if (!tc_supported(L.dev)) throw Error(CDN_E_UNSUPPORTED, "column sharding needs the tensor-core path's limits");
+  }
   cdn_layer_stats& s = L.stats;
   s.rows = H.wrows;
   s.cols = H.wcols;
@@ -676,6 +715,8 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     s.resident_bytes += b->n;
   s.ws_bytes = 0;
   s.in_features = L.in_elems();
+  s.col_begin = L.col ? L.kc0 : 0;
+  s.col_end = L.col ? L.kc1 : H.wcols;
   s.out_features = L.out_elems();
   if (conv) {
     L.kpad = (int)((H.cols + 63) / 64 * 64);
@@ -727,9 +768,47 @@ int band_min_batch() {
 
 // One fused FC layer launch: the warp-specialised band kernel for large
 // batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
+// The tensor-core path on plan p (list decode unless done ahead this call).
+// bias null: partial sums without bias / ReLU (column-sharded layers).
+void tc_call(Model& m, Layer& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
+             const float* bias, cudaStream_t s, bool x_im, bool y_im) {
+  m.tc_xh.alloc(p.xsplit_elems * 2);
+  m.tc_xl.alloc(p.xsplit_elems * 2);
+  m.tc_sc.alloc(tc_scale_floats(B) * sizeof(float));
+  if (m.tc_ctr.n < sizeof(int) * (size_t)B || !m.tc_ctr.p) {
+    m.tc_ctr.alloc(sizeof(int) * (size_t)B);
+    CUDA_OK(cudaMemsetAsync(m.tc_ctr.p, 0, m.tc_ctr.n, s));
+  }
+  if (p.ws_floats) L.bws.alloc(p.ws_floats * sizeof(float));
+  if (L.list_state == 1) {
+    CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
+  } else if (L.list_state == 0) {
+    ensure_list(L);
+    CUDA_OK(launch_tc_list(L.dev, s, L.col ? L.kt0 : 0, L.col ? L.kt1 : -1));
+  }
+  L.list_state = 2;
+  CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<uint16_t*>(m.tc_xh.p),
+                       static_cast<uint16_t*>(m.tc_xl.p), L.bws.as<float>(), m.tc_sc.as<float>(), m.tc_ctr.as<int>(), s,
+                       x_im, y_im, bias));
+}
+
 void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s,
                 bool x_im = false, bool y_im = false) {
   const int relu = L.desc.relu;
+  if (L.col) {
+    // column-sharded: this rank's K tiles for every output row, partial sums
+    // (no bias / ReLU: they follow the cross-rank sum); x = the rank's column
+    // block ([kc1 - kc0][ldx] feature-major, or image-major rows from column kc0)
+    if (y_im) throw Error(CDN_E_ARG, "internal: image-major output of a column-sharded layer");
+    if (L.kt1 <= L.kt0) {  // an empty block (more ranks than K tiles): zero partials
+      CUDA_OK(cudaMemset2DAsync(y, (size_t)ldy * 4, 0, (size_t)B * 4, L.dev.wrows, s));
+      return;
+    }
+    const TcPlan p = plan_fc_tc(L.dev, B, m.num_sms, L.kt0, L.kt1);
+    if (!p.ok) throw Error(CDN_E_UNSUPPORTED, "column-sharded layer outside the tensor-core path's limits");
+    tc_call(m, L, p, x, ldx, B, y, ldy, 0, nullptr, s, x_im, false);
+    return;
+  }
   // Default policy for B >= band_min_batch(): both large-batch kernels are timed once at the
   // first call with this B and the faster is kept for the layer (autotune).
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
@@ -775,26 +854,9 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
     tcmin = choice ? B : (1 << 30);
   }
   if (B >= tcmin && tc_supported(L.dev)) {
-    TcPlan p = plan_fc_tc(L.dev, B, m.num_sms);
+    const TcPlan p = plan_fc_tc(L.dev, B, m.num_sms);
     if (p.ok) {
-      m.tc_xh.alloc(p.xsplit_elems * 2);
-      m.tc_xl.alloc(p.xsplit_elems * 2);
-      m.tc_sc.alloc(tc_scale_floats(B) * sizeof(float));
-      if (m.tc_ctr.n < sizeof(int) * (size_t)B || !m.tc_ctr.p) {
-        m.tc_ctr.alloc(sizeof(int) * (size_t)B);
-        CUDA_OK(cudaMemsetAsync(m.tc_ctr.p, 0, m.tc_ctr.n, s));
-      }
-      if (p.ws_floats) L.bws.alloc(p.ws_floats * sizeof(float));
-      if (L.list_state == 1) {
-        CUDA_OK(cudaStreamWaitEvent(s, L.list_ev, 0));
-      } else if (L.list_state == 0) {
-        ensure_list(L);
-        CUDA_OK(launch_tc_list(L.dev, s));
-      }
-      L.list_state = 2;
-      CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<uint16_t*>(m.tc_xh.p),
-                           static_cast<uint16_t*>(m.tc_xl.p), L.bws.as<float>(), m.tc_sc.as<float>(), m.tc_ctr.as<int>(), s,
-                           x_im, y_im));
+      tc_call(m, L, p, x, ldx, B, y, ldy, relu, L.dev.bias, s, x_im, y_im);
       return;
     }
   }
@@ -836,7 +898,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
 // (a batch whose first-use autotune has not run yet counts as no).
 bool uses_tc(const Model& m, const Layer& L, int B) {
   if (L.is_conv() || !tc_supported(L.dev)) return false;
-  if (L.blocked) return true;
+  if (L.blocked || L.col) return true;
   if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch()) {
     for (auto& e : L.kchoice)
       if (e.first == B) return e.second == 1;
@@ -872,7 +934,7 @@ void predecode_launch(Model& m, Layer& L, cudaStream_t s) {
     CUDA_OK(launch_decode_dense(L.dev, static_cast<__nv_bfloat16*>(L.wd.p), L.kpad, s, m.num_sms));
   } else {
     ensure_list(L);
-    CUDA_OK(launch_tc_list(L.dev, s));
+    CUDA_OK(launch_tc_list(L.dev, s, L.col ? L.kt0 : 0, L.col ? L.kt1 : -1));
   }
 }
 
@@ -954,15 +1016,85 @@ void layer_step(Model& m, int li, const float* x, int ldx, int B, float* dst, in
     return;
   }
   if (y_im) throw Error(CDN_E_ARG, "internal: image-major output with several ranks");
-  const uint32_t rb = rows_per_rank(L.rows, m.world);
-  const size_t slab = (size_t)rb * B;
-  m.loc.alloc(slab * sizeof(float));
-  m.gath.alloc(slab * m.world * sizeof(float));
-  CUDA_OK(cudaMemsetAsync(m.loc.p, 0, slab * sizeof(float), s));
-  fc_forward(m, L, x, ldx, B, m.loc.as<float>(), B, s, x_im);
-  NCCL_OK(ncclAllGather(m.loc.p, m.gath.p, slab, ncclFloat, m.comm, s));
-  CUDA_OK(cudaMemcpy2DAsync(dst, (size_t)ld_dst * sizeof(float), m.gath.p, (size_t)B * sizeof(float),
-                            (size_t)B * sizeof(float), L.rows, cudaMemcpyDeviceToDevice, s));
+  if (!m.comm) throw Error(CDN_E_STATE, "shard-only handle (no NCCL id): use cdn_layer_forward");
+  // The exchange of a layer runs on the comm stream per micro-batch (M of
+  // them, B/M images each): micro-batch m's collective overlaps the compute
+  // of micro-batch m + 1 on s; s waits for the last one before the next layer.
+  int M = 1;
+  {
+    static const int env_m = [] {
+      const char* e = std::getenv("CDN_MICRO_BATCHES");
+      return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    const int want = env_m ? env_m : (B >= 256 ? 4 : (B >= 64 ? 2 : 1));
+    for (M = want; M > 1 && B % M; --M) {
+    }
+  }
+  const int mb = B / M;
+  if (!m.comm_s) CUDA_OK(cudaStreamCreateWithFlags(&m.comm_s, cudaStreamNonBlocking));
+  while ((int)m.mb_ev.size() < 2 * M + 1) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    m.mb_ev.push_back(e);
+  }
+  // the comm stream joins s first: it must not touch buffers s still uses
+  CUDA_OK(cudaEventRecord(m.mb_ev[2 * M], s));
+  CUDA_OK(cudaStreamWaitEvent(m.comm_s, m.mb_ev[2 * M], 0));
+  auto xm = [&](int k) {  // micro-batch k's input: feature-major columns / image-major rows
+    return x_im ? x + (size_t)k * mb * ldx : x + (size_t)k * mb;
+  };
+  if (L.col) {
+    // column-sharded (Megatron-style): partial sums of every row from this
+    // rank's column block, then the cross-rank sum -- reduce-scattered into
+    // the next layer's column blocks (rows [r per, (r+1) per) of this layer's
+    // output), or reduced to rank 0 after the last layer -- and bias / ReLU
+    // on the summed block
+    const uint32_t N = L.rows;
+    const bool last = li + 1 == (int)m.layers.size();
+    const ColBlock nb = col_block(N, m.rank, m.world);
+    const size_t npad = last ? N : (size_t)nb.per * m.world;
+    const size_t nblk = last ? N : nb.per;
+    m.part.alloc(npad * B * sizeof(float));
+    m.rsblk.alloc(nblk * B * sizeof(float));
+    for (int k = 0; k < M; ++k) {
+      float* part = m.part.as<float>() + npad * mb * k;
+      float* blk = m.rsblk.as<float>() + nblk * mb * k;
+      if (npad > N) CUDA_OK(cudaMemsetAsync(part + (size_t)N * mb, 0, (npad - N) * mb * sizeof(float), s));
+      fc_forward(m, L, xm(k), ldx, mb, part, mb, s, x_im);
+      CUDA_OK(cudaEventRecord(m.mb_ev[k], s));
+      CUDA_OK(cudaStreamWaitEvent(m.comm_s, m.mb_ev[k], 0));
+      if (last) {
+        NCCL_OK(ncclReduce(part, blk, (size_t)N * mb, ncclFloat, ncclSum, 0, m.comm, m.comm_s));
+        if (m.rank == 0)
+          CUDA_OK(launch_bias_act(blk, (int)N, mb, mb, L.dev.bias, 0, (int)N, L.desc.relu, dst + (size_t)k * mb,
+                                  ld_dst, m.comm_s));
+      } else {
+        NCCL_OK(ncclReduceScatter(part, blk, (size_t)nb.per * mb, ncclFloat, ncclSum, m.comm, m.comm_s));
+        CUDA_OK(launch_bias_act(blk, (int)(nb.k1 - nb.k0), mb, mb, L.dev.bias, (int)nb.k0, (int)N, L.desc.relu,
+                                dst + (size_t)k * mb, ld_dst, m.comm_s));
+      }
+    }
+  } else {
+    // row blocks: this rank's rows of every micro-batch, all-gathered into the
+    // next layer's feature-major input
+    const uint32_t rb = rows_per_rank(L.rows, m.world);
+    const size_t slab = (size_t)rb * mb;
+    m.loc.alloc(slab * M * sizeof(float));
+    m.gath.alloc(slab * m.world * M * sizeof(float));
+    for (int k = 0; k < M; ++k) {
+      float* loc = m.loc.as<float>() + slab * k;
+      float* gath = m.gath.as<float>() + slab * m.world * k;
+      CUDA_OK(cudaMemsetAsync(loc, 0, slab * sizeof(float), s));
+      fc_forward(m, L, xm(k), ldx, mb, loc, mb, s, x_im);
+      CUDA_OK(cudaEventRecord(m.mb_ev[k], s));
+      CUDA_OK(cudaStreamWaitEvent(m.comm_s, m.mb_ev[k], 0));
+      NCCL_OK(ncclAllGather(loc, gath, slab, ncclFloat, m.comm, m.comm_s));
+      CUDA_OK(cudaMemcpy2DAsync(dst + (size_t)k * mb, (size_t)ld_dst * sizeof(float), gath, (size_t)mb * sizeof(float),
+                                (size_t)mb * sizeof(float), L.rows, cudaMemcpyDeviceToDevice, m.comm_s));
+    }
+  }
+  CUDA_OK(cudaEventRecord(m.mb_ev[M], m.comm_s));
+  CUDA_OK(cudaStreamWaitEvent(s, m.mb_ev[M], 0));
 }
 
 int ld4(int b) { return (b + 3) & ~3; }  // feature-major leading dimension (16-byte rows for TMA)
@@ -994,9 +1126,11 @@ struct Exec {
       if (L.is_conv()) {
         xin = const_cast<float*>(src);  // NHWC image-major is the conv layout
       } else if (uses_tc(m, L, Bi)) {
-        // the tensor-core layer splits the image-major input into bf16 hi / lo
-        // directly (no feature-major copy)
-        layer_step(m, i, src, (int)per, Bi, dst, ld, s, true, yt_last && i + 1 == (int)m.layers.size());
+        // the tensor-core layer splits the image-major input into fp16 hi / lo
+        // directly (no feature-major copy); a column-sharded one reads its
+        // column block of each image
+        layer_step(m, i, src + (L.col ? L.kc0 : 0), (int)per, Bi, dst, ld, s, true,
+                   yt_last && i + 1 == (int)m.layers.size());
         return;
       } else {
         CUDA_OK(launch_transpose(src, Bi, (int)per, (int)per, xin, li, s));
@@ -1018,7 +1152,8 @@ struct Exec {
         } else if (P.is_conv()) {  // flatten (h, w, c) (C-22) and go feature-major
           float* t = m.ctmp.as<float>();
           run(i - 1, o + p * b, t, 0);
-          CUDA_OK(launch_transpose(t, b, (int)L.cols, (int)L.cols, xin + p * b, li, s));
+          const uint32_t c0 = L.col ? L.kc0 : 0, nc = L.col ? L.kc1 - L.kc0 : L.cols;  // (the rank's column block)
+          CUDA_OK(launch_transpose(t + c0, b, (int)nc, (int)L.cols, xin + p * b, li, s));
         } else {
           run(i - 1, o + p * b, xin + p * b, li);
         }
@@ -1101,7 +1236,7 @@ void alloc_levels(Model& m, const std::vector<int>& bs) {
     if (L.is_conv()) {
       if (i > 0) m.lvl[i].alloc((size_t)L.in_elems() * bs[i] * sizeof(float));
     } else {
-      m.lvl[i].alloc((size_t)L.cols * ld4(bs[i]) * sizeof(float));
+      m.lvl[i].alloc((size_t)(L.col ? L.kc1 - L.kc0 : L.cols) * ld4(bs[i]) * sizeof(float));
       if (i > 0 && m.layers[i - 1]->is_conv()) m.ctmp.alloc((size_t)L.cols * bs[i - 1] * sizeof(float));
     }
   }
@@ -1120,7 +1255,7 @@ void check_chain(const Model& m, const std::vector<int>& bs) {
 // decoded lists / filters): the next call allocates what its plan needs.
 void release_scratch(Model& m) {
   for (DBuf* b : {&m.stage[0], &m.stage[1], &m.out, &m.loc, &m.gath, &m.host_stage, &m.conv_a, &m.conv_o, &m.conv_t,
-                  &m.ctmp, &m.tc_xh, &m.tc_xl, &m.tc_sc, &m.tc_ctr})
+                  &m.ctmp, &m.tc_xh, &m.tc_xl, &m.tc_sc, &m.tc_ctr, &m.part, &m.rsblk})
     b->release();
   for (auto& b : m.lvl) b.release();
   for (auto& L : m.layers) {
@@ -1180,7 +1315,13 @@ uint64_t exec_scratch_bytes(const Model& m, const std::vector<int>& bs, bool hos
       }
     }
     total += bws + bctr;
-    if (m.world > 1) slab = std::max<uint64_t>(slab, 4ull * rows_per_rank(L.rows, m.world) * B * (m.world + 1));
+    if (m.world > 1 && L.col) {  // partial sums of every row + the reduced block
+      const ColBlock nb = col_block(L.rows, m.rank, m.world);
+      const bool last = i + 1 == f;
+      slab = std::max<uint64_t>(slab, 4ull * B * ((last ? L.rows : (uint64_t)nb.per * m.world) + (last ? L.rows : nb.per)));
+    } else if (m.world > 1) {
+      slab = std::max<uint64_t>(slab, 4ull * rows_per_rank(L.rows, m.world) * B * (m.world + 1));
+    }
   }
   const Layer& Lf = *m.layers[f - 1];
   const int Bf = bs[f - 1];
@@ -1300,7 +1441,9 @@ std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
     // the per-layer counters and column-group partials
     uint64_t ws = L->is_conv() ? L->wd_bytes : L->tlist_bytes;
     ws += L->jpart.n + L->jctr.n + L->ctr.n;
-    if (!L->is_conv() && m.world > 1)
+    if (!L->is_conv() && m.world > 1 && L->col)
+      ws += 4ull * (2ull * L->rows + 128ull * m.world) * Bmax;  // partial sums + reduced block, C-24: max over grid
+    else if (!L->is_conv() && m.world > 1)
       ws += 4ull * rows_per_rank(L->rows, m.world) * (m.world + 1) * Bmax;  // all-gather slabs, C-24: max over grid
     v.push_back(ws);
   }
@@ -1403,6 +1546,11 @@ void cdn_model_destroy(cdn_model* h) {
     h->m.graphs.clear();
     h->m.layers.clear();
     if (h->m.side) cudaStreamDestroy(h->m.side);
+    if (h->m.comm_s) {
+      cudaStreamSynchronize(h->m.comm_s);
+      cudaStreamDestroy(h->m.comm_s);
+    }
+    for (cudaEvent_t e : h->m.mb_ev) cudaEventDestroy(e);
     if (h->m.ev_call) cudaEventDestroy(h->m.ev_call);
     for (cudaStream_t c : h->m.cp)
       if (c) {
@@ -1581,8 +1729,9 @@ cdn_status cdn_model_infer(cdn_model* h, const float* input, int K, float* score
   // Repeated identical calls (device buffers, K, unchanged state) replay a CUDA
   // graph of the call: the first runs eagerly, the second is captured, the
   // rest launch the graph -- one launch instead of a dozen kernels, events and
-  // stream joins.  Not with host buffers, several ranks or the kernel timer on.
-  const bool graphable = graphs_enabled() && on_device && m.world == 1 && !ktimer_active();
+  // stream joins.  Not with host buffers or the kernel timer on.
+  // (several ranks: NCCL calls are captured too; every rank captures the same call)
+  const bool graphable = graphs_enabled() && on_device && !ktimer_active();
   Model::GraphEntry* ge = nullptr;
   if (graphable)
     for (auto& e : m.graphs)
@@ -1711,6 +1860,23 @@ cdn_status cdn_debug_kernel_timer_read(const char* kernel, double* total_ms, int
   API_END
 }
 
+cdn_status cdn_model_set_sharding(cdn_model* h, int mode) {
+  API_BEGIN
+  if (!h || (mode != CDN_SHARD_ROWS && mode != CDN_SHARD_COLS)) return fail(CDN_E_ARG, "bad arguments");
+  if (!h->m.layers.empty()) return fail(CDN_E_STATE, "set the sharding before loading layers");
+  h->m.sharding = mode;
+  API_END
+}
+
+cdn_status cdn_col_block(uint32_t cols, int rank, int world, uint32_t* k0, uint32_t* k1) {
+  API_BEGIN
+  if (!k0 || !k1 || world < 1 || rank < 0 || rank >= world) return fail(CDN_E_ARG, "bad arguments");
+  const ColBlock b = col_block(cols, rank, world);
+  *k0 = b.k0;
+  *k1 = b.k1;
+  API_END
+}
+
 cdn_status cdn_model_scratch_bytes(cdn_model* h, uint64_t* current, uint64_t* peak, int reset_peak) {
   API_BEGIN
   if (!h) return fail(CDN_E_ARG, "NULL model");
@@ -1793,7 +1959,7 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
   const Model& m = h->m;
   const Layer& L = *m.layers[layer];
   if (L.is_conv()) return "k_gemm_bf16 (conv)";
-  if (L.blocked) return "k_fc_tc";
+  if (L.blocked || L.col) return "k_fc_tc";
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
   if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev)) {
     for (auto& e : L.kchoice)

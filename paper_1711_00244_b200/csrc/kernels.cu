@@ -635,4 +635,26 @@ cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float
   return e_;
 }
 
+// dst[r][b] = act(src[r][b] + bias[r0 + r]) for r < rows, b < B (column-sharded
+// layers: the reduce-scattered block of partial sums becomes the next layer's
+// input block; bias rows past the layer's end read as 0)
+__global__ void k_bias_act(const float* __restrict__ src, int rows, int B, int lds, const float* __restrict__ bias,
+                           int r0, int nbias, int relu, float* __restrict__ dst, int ldd) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)rows * B) return;
+  const int r = (int)(i / B), b = (int)(i % B);
+  float v = src[(size_t)r * lds + b];
+  if (r0 + r < nbias) v += bias[r0 + r];
+  if (relu) v = fmaxf(v, 0.f);
+  dst[(size_t)r * ldd + b] = v;
+}
+
+cudaError_t launch_bias_act(const float* src, int rows, int B, int lds, const float* bias, int r0, int nbias, int relu,
+                            float* dst, int ldd, cudaStream_t s) {
+  if (rows <= 0 || B <= 0) return cudaSuccess;
+  const long n = (long)rows * B;
+  k_bias_act<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, rows, B, lds, bias, r0, nbias, relu, dst, ldd);
+  return launched();
+}
+
 }  // namespace cdn

@@ -130,20 +130,24 @@ struct TcPlan {
   bool ok = false;
   int nbt = 1, nrt = 1, nkt = 0, ldk = 0, tiles = 0, grid = 0, mpt = 1;  // mpt: max CTAs per tile
   int tn = 256;  // images per tile (UMMA N): 128 when the batch fits one
+  int kbase = 0, kcols = 0;  // first K tile and K columns of the call (column-sharded layers: the rank's block)
   long W = 0;  // tile steps (stream-K split over `grid` CTAs)
   size_t ws_floats = 0, xsplit_elems = 0, smem = 0;
 };
 bool tc_supported(const FcDev& L);
-TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms);
+// K tiles [kt0, kt1) only (kt1 < 0: all): a column-sharded layer's block
+TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms, int kt0 = 0, int kt1 = -1);
 // list decoder of the tensor-core path (k_tc_list[_ms]): fills L.tlist from the
 // compressed streams; launch_fc_tc reads it (the caller orders the two)
-cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s);
+cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s, int kt0 = 0, int kt1 = -1);
 // xh / xl: fp16 hi / lo scratch [B][ldk]; scw: tc_scale_floats(B) floats (per-image split
 // scales); xctr: >= B ints, zero at allocation (the kernels leave them zero)
 size_t tc_scale_floats(int B);
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
-                         bool x_image_major = false, bool y_image_major = false);  // x: [K][ldx] feature-major, or [B][ldx] image-major
+                         bool x_image_major, bool y_image_major,
+                         const float* bias);  // x: [kcols][ldx] feature-major, or [B][ldx] image-major (the plan's K
+                                              // columns); bias null: partial sums without bias / ReLU
 
 // Small-batch multi-symbol kernel (B <= 8; r <= 5, k <= 4, 32-bit lane records).
 bool ms_supported(const FcDev& L);
@@ -169,6 +173,11 @@ cudaError_t launch_transpose(const float* in, int rows, int cols, int ldi, float
                              cudaStream_t s);
 
 size_t fc_smem_bytes(const FcDev& L);
+
+// dst[r][b] = act(src[r][b] + bias[r0 + r]) (bias rows >= nbias add 0): the
+// reduce-scattered block of a column-sharded layer -> the next layer's input
+cudaError_t launch_bias_act(const float* src, int rows, int B, int lds, const float* bias, int r0, int nbias, int relu,
+                            float* dst, int ldd, cudaStream_t s);
 
 // ---- CONV path (conv.cu)
 // Decode the rank's rows into dense bf16 W[row][col] (zero-filled by caller).

@@ -82,6 +82,8 @@ struct TcArgs {
   int yt;                       // 1: y image-major [B][ldy] (the class scores of the last layer), else [rows][ldy]
   const float* xsc;             // [2B] per-image power-of-two scales of the fp16 split and their inverses (k_xscale_*)
   float winv;                   // 1 / the layer's weight scale
+  int kbase;                    // first K tile of this call (column-sharded layers: the rank's K block)
+  const float* bias;            // added in the epilogue; null: partial sums (column-sharded layers)
 };
 
 __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       int k0, k1;
       stream_range(t, q, k0, k1);
       // tile kt's entries: block (rt, kt) of the list, this row's slice of it
-      const size_t blk0 = (size_t)t.rt * L.tNI;
+      const size_t blk0 = (size_t)t.rt * L.tNI + a.kbase;
       // raw loads only: the base / count arithmetic happens a tile later, at use
       struct Off { uint32_t b, o0, o1; };
       auto offs = [&](int kt) -> Off {
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       // rows made every store instruction 32 scattered half-sectors)
       float* const dst = whole ? (a.yt ? a.y : a.y + (size_t)row * a.ldy + b0)
                                : a.ws + ((size_t)t.tile * a.mpt + t.slot) * kTM * TN + (size_t)row_l * 4;
-      const float bias = (whole && row < L.wrows) ? L.bias[row] : 0.f;
+      const float bias = (whole && row < L.wrows && a.bias) ? a.bias[row] : 0.f;
       // y rows are contiguous over the batch: whole float4s where the tile is inside B
       const bool vec_ok = (a.ldy % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
       for (int c = 0; c < TN; c += 16) {
@@ -679,7 +681,7 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
         const float4 e = __ldcg(reinterpret_cast<const float4*>(p + (size_t)j * kTM * TN));
         acc.x += e.x; acc.y += e.y; acc.z += e.z; acc.w += e.w;
       }
-      const float bs = bias[row];
+      const float bs = bias ? bias[row] : 0.f;
       acc.x += bs; acc.y += bs; acc.z += bs; acc.w += bs;
       if (relu) {
         acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
@@ -752,7 +754,7 @@ size_t tc_smem_bytes(const FcDev&, int tn) {
 constexpr int kListThreads = 256;
 
 template <bool BLOCKED>
-__global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
+__global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L, int c0, int nchr) {
   __shared__ uint32_t s_flut[1 << kFoldLutBits];
   __shared__ uint32_t s_glut[1 << kLutMaxBits];
   __shared__ uint32_t s_vtab[99], s_gtab[99];
@@ -766,14 +768,14 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
   // task = (row group, chunk of L.tch <= kTcChunk intervals, row in group): consecutive
   // threads write adjacent slices of the same blocks
   const int tch = L.tch;
-  const int nch = (L.sNI + tch - 1) / tch;
+  // chunks [c0, c0 + nchr) of the row's (column-sharded layers: the rank's K block)
   const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
   // groups of 128 stored rows (a row tile: a warp's list slots are adjacent),
   // 32 when blocked (few long stored rows)
   constexpr int kGrp = BLOCKED ? 32 : 128, kGrpLog2 = BLOCKED ? 5 : 7;
   const int r = (int)(task & (kGrp - 1));
   const size_t rc = task >> kGrpLog2;
-  const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
+  const int rt = (int)(rc / nchr), kt0 = (c0 + (int)(rc % nchr)) * tch;
   const int row = rt * kGrp + r;
   if (row >= L.nrows) return;
   const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
@@ -855,7 +857,7 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L) {
 // consumed up to 4 tokens per step, a pad being a token whose gap advances the
 // column by 2^k and whose symbol 0 emits nothing (C-01, C-04).
 template <bool BLOCKED>
-__global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
+__global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L, int c0, int nchr) {
   extern __shared__ __align__(16) uint32_t sm[];
   uint32_t* s_vl = sm;
   uint32_t* s_gl = s_vl + (1 << L.msLv);
@@ -879,14 +881,14 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L) {
   __syncthreads();
   mbar_wait(&s_bar, 0);
   const int tch = L.tch;
-  const int nch = (L.sNI + tch - 1) / tch;
+  // chunks [c0, c0 + nchr) of the row's (column-sharded layers: the rank's K block)
   const size_t task = (size_t)blockIdx.x * kListThreads + threadIdx.x;
   // groups of 128 stored rows (a row tile: a warp's list slots are adjacent),
   // 32 when blocked (few long stored rows)
   constexpr int kGrp = BLOCKED ? 32 : 128, kGrpLog2 = BLOCKED ? 5 : 7;
   const int r = (int)(task & (kGrp - 1));
   const size_t rc = task >> kGrpLog2;
-  const int rt = (int)(rc / nch), kt0 = (int)(rc % nch) * tch;
+  const int rt = (int)(rc / nchr), kt0 = (c0 + (int)(rc % nchr)) * tch;
   const int row = rt * kGrp + r;
   if (row >= L.nrows) return;
   const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
@@ -997,15 +999,19 @@ bool tc_supported(const FcDev& L) {
          L.Lf == kFoldLutBits && L.Lg <= kLutMaxBits;
 }
 
-TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
+TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms, int kt0, int kt1) {
   TcPlan p;
   if (!tc_supported(L) || B <= 0) return p;
+  if (kt1 < 0) kt1 = L.tNI;
+  if (kt0 < 0 || kt1 > L.tNI || kt1 <= kt0 || ((kt0 > 0 || kt1 < L.tNI) && L.bw != L.wcols)) return p;
   // a 128-image tile when the batch fits one (half the tensor work of 256)
   p.tn = B <= 128 ? 128 : kTN;
   p.nbt = (B + p.tn - 1) / p.tn;
   p.nrt = (L.wrows + kTM - 1) / kTM;
-  p.nkt = L.tNI;
-  p.ldk = (L.wcols + 7) & ~7;
+  p.kbase = kt0;
+  p.nkt = kt1 - kt0;
+  p.kcols = std::min(L.wcols, kt1 * kTK) - kt0 * kTK;
+  p.ldk = (p.kcols + 7) & ~7;
   p.tiles = p.nrt * p.nbt;
   p.W = (long)p.tiles * p.nkt;
   long G;
@@ -1040,11 +1046,16 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms) {
   return p;
 }
 
-cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
+cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s, int kt0, int kt1) {
   cudaError_t e = cudaSuccess;
   const bool blocked = L.bw != L.wcols;
   const size_t grp = blocked ? 32 : 128;
-  const size_t tasks = (size_t)((L.nrows + grp - 1) / grp) * ((L.sNI + L.tch - 1) / L.tch) * grp;
+  if (kt1 < 0 || kt1 > L.sNI) kt1 = L.sNI;
+  // the chunks of L.tch K tiles that cover [kt0, kt1) (edge chunks decode a
+  // few tiles outside the range into their own -- valid -- list blocks)
+  const int c0 = kt0 / L.tch, c1 = (kt1 + L.tch - 1) / L.tch;
+  const int nchr = std::max(1, c1 - c0);
+  const size_t tasks = (size_t)((L.nrows + grp - 1) / grp) * nchr * grp;
   const unsigned lgrid = (unsigned)((tasks + kListThreads - 1) / kListThreads);
   if (ms_supported(L) && !list_fold_forced()) {
     const size_t lsm = ms_smem_bytes(L);
@@ -1058,15 +1069,15 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
     }
     ktimer_begin("k_tc_list", s);
     if (blocked)
-      k_tc_list_ms<true><<<lgrid, kListThreads, lsm, s>>>(L);
+      k_tc_list_ms<true><<<lgrid, kListThreads, lsm, s>>>(L, c0, nchr);
     else
-      k_tc_list_ms<false><<<lgrid, kListThreads, lsm, s>>>(L);
+      k_tc_list_ms<false><<<lgrid, kListThreads, lsm, s>>>(L, c0, nchr);
   } else {
     ktimer_begin("k_tc_list", s);
     if (blocked)
-      k_tc_list<true><<<lgrid, kListThreads, 0, s>>>(L);
+      k_tc_list<true><<<lgrid, kListThreads, 0, s>>>(L, c0, nchr);
     else
-      k_tc_list<false><<<lgrid, kListThreads, 0, s>>>(L);
+      k_tc_list<false><<<lgrid, kListThreads, 0, s>>>(L, c0, nchr);
   }
   e = launched();
   ktimer_end("k_tc_list", s);
@@ -1075,21 +1086,21 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s) {
 
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
-                         bool x_image_major, bool y_image_major) {
+                         bool x_image_major, bool y_image_major, const float* bias) {
   // per-image scales of the fp16 split: scw = [B scales | B inverse scales |
   // kScaleChunks x B partial maxima]; xctr: >= B arrival counters, zero between calls
   float* xsc = scw;
   float* xpart = scw + 2 * (size_t)B;
   ktimer_begin("k_split_x", s);
   if (x_image_major) {
-    k_xscale_rows<<<dim3((unsigned)B, 4), 256, 0, s>>>(x, L.wcols, ldx, B, xpart, xctr, xsc);
+    k_xscale_rows<<<dim3((unsigned)B, 4), 256, 0, s>>>(x, p.kcols, ldx, B, xpart, xctr, xsc);
     const long n = (long)B * (p.ldk / 8);
     const int vec = (ldx % 4) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk, vec, xsc);
+    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, vec, xsc);
   } else {
-    k_xscale_cols<<<dim3((unsigned)((B + 31) / 32), kScaleChunks), 256, 0, s>>>(x, L.wcols, ldx, B, xpart, xctr, xsc);
+    k_xscale_cols<<<dim3((unsigned)((B + 31) / 32), kScaleChunks), 256, 0, s>>>(x, p.kcols, ldx, B, xpart, xctr, xsc);
     dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
-    k_split_x<<<sg, 256, 0, s>>>(x, L.wcols, ldx, B, xh, xl, p.ldk, xsc);
+    k_split_x<<<sg, 256, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, xsc);
   }
   cudaError_t e = launched(2);
   ktimer_end("k_split_x", s);
@@ -1117,7 +1128,7 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   }
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
   TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr,
-           y_image_major ? 1 : 0, xsc, 1.0f / L.tc_wsc};
+           y_image_major ? 1 : 0, xsc, 1.0f / L.tc_wsc, p.kbase, bias};
   ktimer_begin("k_fc_tc", s);
   {
     cudaLaunchConfig_t cfg = {};
@@ -1154,10 +1165,10 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     const int yt = y_image_major ? 1 : 0;
     if (p.tn == 128)
       e = cudaLaunchKernelEx(&cfg, k_tc_reduce<128>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
-                             L.bias, relu, y, ldy, vec_ok, yt);
+                             bias, relu, y, ldy, vec_ok, yt);
     else
       e = cudaLaunchKernelEx(&cfg, k_tc_reduce<256>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
-                             L.bias, relu, y, ldy, vec_ok, yt);
+                             bias, relu, y, ldy, vec_ok, yt);
     if (e == cudaSuccess) e = launched();
     ktimer_end("k_tc_reduce", s);
   }

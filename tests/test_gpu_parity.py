@@ -707,3 +707,49 @@ def test_tc_edge_fixtures(torch_dev, name, rows, cols, d, r, k, scale):
     m.set_kernel_policy(1, 1)
     a = synth.random_activations(cols, 36, seed=99)
     check_forward_sparse(torch, dev, m, c, v, a, relu=False, split_tc=True)
+
+
+# ------------------------------------- column-sharded layers
+
+@pytest.mark.parametrize("cfg,i", [("C5", 0), ("C5", 1), ("C5", 2), ("C3", 2)])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_column_sharded_layer_partials(torch_dev, cfg, i, world):
+    """Megatron-style column blocks through shard-only handles (rank r of
+    `world`, CDN_SHARD_COLS, no communicator): each rank's cdn_layer_forward on
+    its column block of x gives the partial sums of every row (no bias / ReLU);
+    their sum + bias (+ ReLU) matches the oracle within the north_star bound and
+    the fp16-split elementwise bound."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    spec, c, buf = config_layer(cfg, i)
+    _, v = synth.fc_weights(spec, synth.CONFIGS[cfg].seed)
+    B = 96
+    a = synth.fc_inputs(spec.cols, B, 2)
+    total = np.zeros((spec.rows, B), np.float64)
+    cover = 0
+    for r in range(world):
+        m = cdn.Model(0, rank=r, world=world)
+        m.set_sharding(cdn.CDN_SHARD_COLS)
+        m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+        st = m.stats(0)
+        k0, k1 = st["col_begin"], st["col_end"]
+        assert (k0, k1) == cdn.col_block(spec.cols, r, world) and st["row_begin"] == 0 and st["row_end"] == spec.rows
+        assert m.kernel_name(0, B) == "k_fc_tc"
+        cover += k1 - k0
+        x = torch.from_numpy(np.ascontiguousarray(a[:, k0:k1].T)).to(dev)
+        if k1 == k0:
+            x = torch.zeros((1, B), dtype=torch.float32, device=dev)
+        y = torch.full((spec.rows, B), float("nan"), dtype=torch.float32, device=dev)
+        m.layer_forward(0, x, B, B, y, B)
+        torch.cuda.synchronize()
+        total += y.cpu().numpy().astype(np.float64)
+        m.close()
+    assert cover == spec.cols
+    out = (total + v[:, None]).T
+    if spec.relu:
+        out = np.maximum(out, 0.0)
+    ref = infer.fc_forward(sparse_q(c), a, v, apply_relu=spec.relu)
+    assert rel_err(out, ref) <= TOL
+    scale = infer.fc_abs_scale(sparse_q(c), a, v)
+    kmax = int(c.row_tokens.max())
+    assert (np.abs(out - ref) / np.maximum(scale, 1e-30)).max() <= 2 * kmax * 2.0 ** -24 + world * 2.0 ** -20
