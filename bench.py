@@ -273,7 +273,7 @@ def run_ours(args):
         # P:L284, L314); what the tensor cores execute -- dense 128 x 64 tiles,
         # three fp16 products per element pair -- is a side field against the
         # measured 16-bit peak.
-        tn = 128 if B <= 128 else 256  # image tile of the kernel (tc.cu plan_fc_tc)
+        tn = 64 if B <= 64 else (128 if B <= 128 else 256)  # image tile of the kernel (tc.cu plan_fc_tc)
 
         def dense(i):
             kpad = (stats[i]["col_end"] - stats[i]["col_begin"] + 63) // 64 * 64

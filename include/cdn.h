@@ -261,7 +261,8 @@ cdn_status cdn_model_release_scratch(cdn_model* m);
 
 /* Name of the kernel a layer launches for batch B under the current policy
  * (after the first-use autotune at that B, if any): "k_fc_j" (B <= 4),
- * "k_fc_ms", "k_fc_fold", "k_fc_band<V>", "k_fc_tc" or "k_gemm_bf16 (conv)";
+ * "k_fc_ms", "k_fc_fold", "k_fc_band<V>", "k_fc_tc", "k_gemm_bf16 (conv)" or
+ * "k_gemm_bf16 (conv, implicit im2col)";
  * "" for bad arguments.  The string is static. */
 const char* cdn_layer_kernel_name(const cdn_model* m, int layer, int B);
 

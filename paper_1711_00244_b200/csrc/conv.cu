@@ -18,6 +18,7 @@
 //       fp32 NHWC, then release the buffer -- overlapping the next tile.
 //   k_lrn, k_maxpool: the AlexNet norm / pool layers (C-19, C-20), NHWC fp32.
 #include <cuda.h>
+#include <algorithm>
 #include <cuda_bf16.h>
 
 #include "dev_common.cuh"
@@ -48,7 +49,10 @@ constexpr int kGThreads = 64 + 32 * kGEpiWarps;  // TMA warp, MMA warp, epilogue
 __global__ void __launch_bounds__(kGThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int Mrows, int Nrows,
                 int nk, int BN, int tmem_cols, int kGStages, const float* __restrict__ bias,
-                float* __restrict__ out, int ldo, int col0, int relu, int lrn, int groups) {
+                float* __restrict__ out, int ldo, int col0, int relu, int lrn, int groups, int4 imc, int4 imc2) {
+  // imc = (im2col mode, Wo, Ho * Wo, pad), imc2 = (kw, channel chunks per tap, padded channels per group, -):
+  // in im2col mode `ta` is an im2col map over the bf16 NHWC input and K tile kt
+  // = (tap, chunk) = (r * kw + s, c / 64) of group z
   extern __shared__ unsigned char smem_raw[];
   // align within the shared window (pointer arithmetic on smem_raw keeps the .shared address space)
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
@@ -99,7 +103,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
           const int s = it % kGStages;
           mbar_wait(&empty[s], ((it / kGStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[s], (uint32_t)(a_bytes + b_bytes));
-          tma3d(sA + s * a_bytes, &ta, kt * kBK, m * kBM, z, &full[s]);
+          if (imc.x) {  // implicit GEMM: the 128 output pixels' tap (r, s) channels, straight from the input
+            const int p0 = m * kBM, img = p0 / imc.z, rem = p0 - img * imc.z, oh = rem / imc.y, ow = rem - oh * imc.y;
+            const int tap = kt / imc2.y, ch = kt - tap * imc2.y, r = tap / imc2.x, sx = tap - r * imc2.x;
+            tma_im2col4d(sA + s * a_bytes, &ta, z * imc2.z + ch * kBK, ow - imc.w, oh - imc.w, img, sx, r, &full[s]);
+          } else {
+            tma3d(sA + s * a_bytes, &ta, kt * kBK, m * kBM, z, &full[s]);
+          }
           tma3d(sB + s * b_bytes, &tb, kt * kBK, n * BN, z, &full[s]);
         }
       }
@@ -459,9 +469,80 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
   }
   const int grid = (int)(tiles < num_sms ? tiles : num_sms);
   k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
-                                            ldo, col0, relu, lrn, groups);
+                                            ldo, col0, relu, lrn, groups, make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0));
   const cudaError_t e_ = launched();
   ktimer_end("k_gemm_bf16", s);
+  return e_;
+}
+
+cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
+                                 int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
+                                 int relu, float* out, int ldo, cudaStream_t s, int lrn) {
+  const int Mrows = B * Ho * Wo;
+  if (Mrows <= 0 || Nrows <= 0 || G <= 0) return cudaSuccess;
+  if ((long)G * Nrows > kGMaxBias || cgp % kBK || kh != kw || Ho != H + 2 * pad - kh + 1 || Wo != W + 2 * pad - kw + 1)
+    return cudaErrorInvalidValue;
+  const int BN = gemm_tile_n(Nrows);
+  if (lrn && BN < Nrows) return cudaErrorInvalidValue;
+  int tcols = 32;
+  while (tcols < BN) tcols <<= 1;
+  const int nch = cgp / kBK, Kpad = kh * kw * cgp;
+  CUtensorMap ta, tb;
+  cudaError_t e = encode_tmap_im2col4d(&ta, act, (uint64_t)G * cgp, (uint64_t)W, (uint64_t)H, (uint64_t)B, -pad,
+                                       pad - (kh - 1), kBK, kBM);
+  if (e != cudaSuccess) return e;
+  e = encode_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Wt, (uint64_t)Kpad, (uint64_t)Nrows, (uint64_t)G,
+                     (uint64_t)Kpad * 2, (uint64_t)Kpad * 2 * Nrows, kBK, (uint32_t)BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  const size_t smem = gemm_smem_bytes(BN);
+  static thread_local size_t set_smem = 0;
+  if (smem > set_smem) {
+    e = cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set_smem = smem;
+  }
+  ktimer_begin("k_gemm_bf16", s);
+  const long tiles = (long)((Mrows + kBM - 1) / kBM) * ((Nrows + BN - 1) / BN) * G;
+  int num_sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
+  k_gemm_bf16<<<grid, kGThreads, smem, s>>>(ta, tb, Mrows, Nrows, Kpad / kBK, BN, tcols, gemm_stages(BN), bias, out,
+                                            ldo, 0, relu, lrn, G, make_int4(1, Wo, Ho * Wo, pad),
+                                            make_int4(kw, nch, cgp, 0));
+  const cudaError_t e_ = launched();
+  ktimer_end("k_gemm_bf16", s);
+  return e_;
+}
+
+// x fp32 NHWC [npix][C] (G groups of cg channels) -> bf16 (RNE, reading C-21)
+// [npix][G * cgp], each group's channels padded with zeros to cgp: the
+// implicit GEMM's TMA im2col reads 64-channel (128-byte) runs per tap.
+__global__ void k_to_bf16_pad(const float* __restrict__ x, long npix, int C, int G, int cg, int cgp,
+                              __nv_bfloat16* __restrict__ out) {
+  const int cp = G * cgp, q = cp / 2;  // channel pairs per pixel
+  const long n = npix * q;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const long p = i / q;
+    const int c2 = (int)(i - p * q) * 2, z = c2 / cgp, c = c2 - z * cgp;
+    const float* xp = x + p * C + z * cg;
+    const float a = c < cg ? xp[c] : 0.f, b = c + 1 < cg ? xp[c + 1] : 0.f;
+    reinterpret_cast<__nv_bfloat162*>(out)[i] = __floats2bfloat162_rn(a, b);
+  }
+}
+
+cudaError_t launch_to_bf16_pad(const float* x, long npix, int C, int G, int cg, int cgp, __nv_bfloat16* out,
+                               cudaStream_t s) {
+  if (npix <= 0) return cudaSuccess;
+  if (cgp % 2) return cudaErrorInvalidValue;
+  const long n = npix * G * cgp / 2;
+  const int grid = (int)std::min<long>((n + 255) / 256, 148L * 16);
+  ktimer_begin("k_to_bf16_pad", s);
+  k_to_bf16_pad<<<grid, 256, 0, s>>>(x, npix, C, G, cg, cgp, out);
+  const cudaError_t e_ = launched();
+  ktimer_end("k_to_bf16_pad", s);
   return e_;
 }
 

@@ -464,7 +464,8 @@ __global__ void __launch_bounds__(256, 4) k_decode(FcDev L, int row_offset, int3
 // value, reading C-21) for the CONV tensor-core path; pads and pruned entries
 // stay 0 (the caller zero-fills W).
 template <bool REC64>
-__global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16* __restrict__ W, int ldw) {
+__global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16* __restrict__ W, int ldw, int cg,
+                                                          int cgp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemTables t = carve(L, smem);
   stage_tables(L, t);
@@ -489,7 +490,9 @@ __global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16*
       const uint32_t gs = decode_sym(gr.peek(), t.glut, L.Lg, t.gtab, t.gsorted, L.gmax, lg);
       gr.skip(lg);
       col += (int)gs + 1;
-      if (vs) W[(size_t)row * ldw + col] = __float2bfloat16_rn(t.cb[vs]);
+      // K order (r, s, c) (C-18); channels padded from cg to cgp per tap for
+      // the implicit-GEMM layers (cg == cgp: identity)
+      if (vs) W[(size_t)row * ldw + (col / cg) * cgp + col % cg] = __float2bfloat16_rn(t.cb[vs]);
     }
   }
 }
@@ -605,7 +608,9 @@ cudaError_t launch_decode(const FcDev& L, int row_offset, int32_t* row, int32_t*
   return launched();
 }
 
-cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms) {
+cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms, int cg,
+                                int cgp) {
+  if (cg <= 0) cg = cgp = 1;
   if (L.nrows <= 0) return cudaSuccess;
   const int threads = 256;
   const size_t smem = fc_smem_bytes(L);
@@ -614,10 +619,10 @@ cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaS
   ktimer_begin("k_decode_dense", s);
   if (L.rec64) {
     auto k = k_decode_dense<true>;
-    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw);
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw, cg, cgp);
   } else {
     auto k = k_decode_dense<false>;
-    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw);
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw, cg, cgp);
   }
   const cudaError_t e_ = launched();
   ktimer_end("k_decode_dense", s);

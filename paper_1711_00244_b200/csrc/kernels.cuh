@@ -181,7 +181,10 @@ cudaError_t launch_bias_act(const float* src, int rows, int B, int lds, const fl
 
 // ---- CONV path (conv.cu)
 // Decode the rank's rows into dense bf16 W[row][col] (zero-filled by caller).
-cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms);
+// cg / cgp: channels per group and their padding per tap (implicit-GEMM layers;
+// column (r*kw + s)*cg + c lands at (r*kw + s)*cgp + c); 0: no remap
+cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms, int cg = 0,
+                                int cgp = 0);
 // NHWC fp32 -> bf16 patches [B*Ho*Wo][Kpad] of channels [c0, c0+cg), k = (r*kw+s)*cg + c.
 cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, int kw, int stride, int pad, int c0,
                           int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
@@ -192,6 +195,15 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
                              const float* bias, int relu, float* out, int ldo, int col0, cudaStream_t s,
                              int lrn = 0, int groups = 1);
 cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t s, int num_sms);
+// Implicit-GEMM CONV (stride 1, channel groups of cg padded to cgp = 64k):
+// x fp32 NHWC [npix][C] -> bf16 [npix][G * cgp] (channels of a group padded with
+// zeros), then the tcgen05 GEMM with its activation tiles loaded by TMA in
+// im2col mode from that tensor (no patch matrix).
+cudaError_t launch_to_bf16_pad(const float* x, long npix, int C, int G, int cg, int cgp, __nv_bfloat16* out,
+                               cudaStream_t s);
+cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
+                                 int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
+                                 int relu, float* out, int ldo, cudaStream_t s, int lrn);
 cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
                            int num_sms);
 

@@ -58,7 +58,7 @@ namespace {
 using namespace dev;
 
 constexpr int kTM = 128;            // rows per unit (UMMA M)
-constexpr int kTN = 256;            // images per unit (UMMA N); 128 for B <= 128 (TN template)
+constexpr int kTN = 256;            // images per unit (UMMA N); 128 for B <= 128, 64 for B <= 64 (TN template)
 constexpr int kTK = 64;             // K tile (= interval width of the TC index)
 constexpr int kXStages = 3;         // X ring depth
 constexpr int kEnt = 16;            // list entries per row tile carried in registers (the rest: loads)
@@ -547,7 +547,7 @@ __device__ __forceinline__ float pow2_scale(float m) {
 // block of an image (arrival counter, reset by it) writes its scale sc[b].
 // Feature-major x [K][ldx]: block = 32 images x 8 row groups; image-major x
 // [B][ldx]: block = one image.
-constexpr int kScaleChunks = 8;
+constexpr int kScaleChunks = 16;
 // sc[b] = s_b, sc[B + b] = 1 / s_b (exact: a power of two)
 __device__ __forceinline__ void scale_finish(float m, int b, int B, int nparts, float* part, int* ctr, float* sc) {
   part[(size_t)blockIdx.y * B + b] = m;
@@ -568,8 +568,17 @@ __global__ void __launch_bounds__(256) k_xscale_cols(const float* __restrict__ x
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, b = blockIdx.x * 32 + tx;
   const int kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc, k1 = min(K, k0 + kc);
   float m = 0.f;
-  if (b < B)
-    for (int k = k0 + ty; k < k1; k += 8) m = fmaxf(m, fabsf(__ldg(x + (size_t)k * ldx + b)));
+  if (b < B) {
+    int k = k0 + ty;
+    for (; k + 56 < k1; k += 64) {  // eight rows in flight per thread
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(x + (size_t)(k + 8 * j) * ldx + b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m = fmaxf(m, fabsf(v[j]));
+    }
+    for (; k < k1; k += 8) m = fmaxf(m, fabsf(__ldg(x + (size_t)k * ldx + b)));
+  }
   red[ty][tx] = m;
   __syncthreads();
   if (ty == 0 && b < B) {
@@ -584,7 +593,15 @@ __global__ void __launch_bounds__(256) k_xscale_rows(const float* __restrict__ x
   const int kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc, k1 = min(K, k0 + kc);
   const float* p = x + (size_t)b * ldx;
   float m = 0.f;
-  for (int k = k0 + (int)threadIdx.x; k < k1; k += 256) m = fmaxf(m, fabsf(__ldg(p + k)));
+  int k = k0 + (int)threadIdx.x;
+  for (; k + 7 * 256 < k1; k += 8 * 256) {  // eight loads in flight per thread
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldg(p + k + 256 * j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m = fmaxf(m, fabsf(v[j]));
+  }
+  for (; k < k1; k += 256) m = fmaxf(m, fabsf(__ldg(p + k)));
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -1005,7 +1022,7 @@ TcPlan plan_fc_tc(const FcDev& L, int B, int num_sms, int kt0, int kt1) {
   if (kt1 < 0) kt1 = L.tNI;
   if (kt0 < 0 || kt1 > L.tNI || kt1 <= kt0 || ((kt0 > 0 || kt1 < L.tNI) && L.bw != L.wcols)) return p;
   // a 128-image tile when the batch fits one (half the tensor work of 256)
-  p.tn = B <= 128 ? 128 : kTN;
+  p.tn = B <= 64 ? 64 : (B <= 128 ? 128 : kTN);
   p.nbt = (B + p.tn - 1) / p.tn;
   p.nrt = (L.wrows + kTM - 1) / kTM;
   p.kbase = kt0;
@@ -1114,7 +1131,7 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   if (e != cudaSuccess) return e;
   static bool attr_set = false;
   if (!attr_set) {  // the largest footprint (256-image tiles) covers both
-    for (auto kern : {k_fc_tc<128>, k_fc_tc<256>}) {
+    for (auto kern : {k_fc_tc<64>, k_fc_tc<128>, k_fc_tc<256>}) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes(L, kTN));
       if (e != cudaSuccess) return e;
     }
@@ -1143,6 +1160,8 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     cfg.numAttrs = 1;
     if (p.tn == 128)
       e = cudaLaunchKernelEx(&cfg, k_fc_tc<128>, L, a, th, tl);
+    else if (p.tn == 64)
+      e = cudaLaunchKernelEx(&cfg, k_fc_tc<64>, L, a, th, tl);
     else
       e = cudaLaunchKernelEx(&cfg, k_fc_tc<256>, L, a, th, tl);
     if (e != cudaSuccess) return e;
@@ -1165,6 +1184,9 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     const int yt = y_image_major ? 1 : 0;
     if (p.tn == 128)
       e = cudaLaunchKernelEx(&cfg, k_tc_reduce<128>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
+                             bias, relu, y, ldy, vec_ok, yt);
+    else if (p.tn == 64)
+      e = cudaLaunchKernelEx(&cfg, k_tc_reduce<64>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
                              bias, relu, y, ldy, vec_ok, yt);
     else
       e = cudaLaunchKernelEx(&cfg, k_tc_reduce<256>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,

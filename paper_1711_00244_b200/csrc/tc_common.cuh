@@ -32,6 +32,20 @@ static __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, 
       : "memory");
 }
 
+// im2col-mode TMA: the box of the map's pixelsPerColumn output pixels starting at
+// base pixel (w, h, n) (input coordinates, may be negative: padding) x its
+// channelsPerPixel channels from c, each pixel shifted by the filter tap
+// (offW, offH); out-of-bounds elements read as zeros.
+static __device__ __forceinline__ void tma_im2col4d(void* dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                                    int offW, int offH, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6], {%7, %8};" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_addr(bar)), "h"((unsigned short)offW),
+      "h"((unsigned short)offH)
+      : "memory");
+}
+
 static __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(

@@ -57,4 +57,34 @@ inline cudaError_t encode_tmap_3d(CUtensorMap* m, CUtensorMapDataType dt, const 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 4D im2col map over an NHWC tensor {C, W, H, N} (bf16): boxes of
+// pixels_per_column output pixels x channels_per_pixel channels; the
+// traversal bounding box is [lower, dim - 1 + upper] per spatial dimension
+// (lower = -pad, upper = pad - (k - 1) for a stride-1 convolution).
+inline cudaError_t encode_tmap_im2col4d(CUtensorMap* m, const void* base, uint64_t C, uint64_t W, uint64_t H,
+                                        uint64_t N, int lower, int upper, uint32_t channels_per_pixel,
+                                        uint32_t pixels_per_column) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return cudaErrorNotSupported;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * 2 * W, (cuuint64_t)C * 2 * W * H};
+  const int lo[2] = {lower, lower}, up[2] = {upper, upper};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lo, up,
+                      channels_per_pixel, pixels_per_column, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 }  // namespace cdn

@@ -108,6 +108,10 @@ def test_alexnet_conv_layer_vs_oracle(torch_dev, i, B, density, quantizer):
                                          spec.groups, relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
                                          pool_s=2 if spec.pool else 0))
     oh, ow, oc = m.out_shape(0)
+    # stride-1 layers with channel groups of >= 8 channels (conv2-5) run the
+    # implicit GEMM (TMA im2col, no patch matrix); conv1 (3 channels, stride 4)
+    # the explicit im2col
+    assert m.kernel_name(0, B) == ("k_gemm_bf16 (conv)" if i == 0 else "k_gemm_bf16 (conv, implicit im2col)")
     xd = torch.from_numpy(x).to(dev)
     yd = torch.full((B, oh, ow, oc), float("nan"), dtype=torch.float32, device=dev)
     m.conv_forward(0, xd, B, yd)
