@@ -545,8 +545,8 @@ __device__ __forceinline__ float pow2_scale(float m) {
 
 // max |x| per image over a K chunk (blockIdx.y of KS) -> part[ks][b]; the last
 // block of an image (arrival counter, reset by it) writes its scale sc[b].
-// Feature-major x [K][ldx]: block = 32 images x 8 row groups; image-major x
-// [B][ldx]: block = one image.
+// Feature-major x [K][ldx]: block = 32 images x 8 row groups (image-major
+// input: k_scale_split_rows).
 constexpr int kScaleChunks = 16;
 // sc[b] = s_b, sc[B + b] = 1 / s_b (exact: a power of two)
 __device__ __forceinline__ void scale_finish(float m, int b, int B, int nparts, float* part, int* ctr, float* sc) {
@@ -586,31 +586,6 @@ __global__ void __launch_bounds__(256) k_xscale_cols(const float* __restrict__ x
     scale_finish(m, b, B, gridDim.y, part, ctr, sc);
   }
 }
-__global__ void __launch_bounds__(256) k_xscale_rows(const float* __restrict__ x, int K, int ldx, int B,
-                                                     float* part, int* ctr, float* sc) {
-  __shared__ float red[8];
-  const int b = blockIdx.x;
-  const int kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc, k1 = min(K, k0 + kc);
-  const float* p = x + (size_t)b * ldx;
-  float m = 0.f;
-  int k = k0 + (int)threadIdx.x;
-  for (; k + 7 * 256 < k1; k += 8 * 256) {  // eight loads in flight per thread
-    float v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = __ldg(p + k + 256 * j);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) m = fmaxf(m, fabsf(v[j]));
-  }
-  for (; k < k1; k += 256) m = fmaxf(m, fabsf(__ldg(p + k)));
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i]);
-    scale_finish(m, b, B, gridDim.y, part, ctr, sc);
-  }
-}
-
 // fp16 hi / lo of v * s (s a power of two: |v s| < 2^15), packed in pairs
 __device__ __forceinline__ void split_pair(float v0, float v1, float s, uint32_t& h, uint32_t& l) {
   v0 *= s;
@@ -725,34 +700,6 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
     const float ov[4] = {o.x, o.y, o.z, o.w};
     for (int k = 0; k < 4 && b + k < B; ++k) yp[k] = ov[k];
   }
-}
-
-// X fp32 image-major [B][ldx] (the public infer input) -> fp16 hi / lo of x s_b,
-// [B][ldk]: a plain streaming conversion, 8 consecutive k per thread (two
-// 16-byte loads when aligned, one 16-byte store per half).
-__global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x, int K, int ldx, int B,
-                                                    uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int ldk,
-                                                    int vec, const float* __restrict__ xsc) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
-  const int nk8 = ldk / 8;
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (long)B * nk8) return;
-  const int b = (int)(i / nk8), k = (int)(i % nk8) * 8;
-  const float* p = x + (size_t)b * ldx + k;
-  float v[8];
-  if (vec && k + 8 <= K) {
-    const float4 a0 = __ldcs(reinterpret_cast<const float4*>(p)), a1 = __ldcs(reinterpret_cast<const float4*>(p + 4));
-    v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = k + j < K ? p[j] : 0.f;
-  }
-  const float sb = xsc[b];
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) split_pair(v[2 * j], v[2 * j + 1], sb, h[j], l[j]);
-  *reinterpret_cast<uint4*>(xh + (size_t)b * ldk + k) = make_uint4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<uint4*>(xl + (size_t)b * ldk + k) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 size_t tc_smem_bytes(const FcDev&, int tn) {
@@ -1009,6 +956,68 @@ bool list_fold_forced() {
 
 }  // namespace
 
+// Image-major input (the public infer input / a conv trunk's output): one
+// block per image finds max |x| over its K features, writes the power-of-two
+// scale and its inverse, then splits the row (second read: L2-resident) into
+// fp16 hi / lo of x s_b -- k_xscale_rows + k_split_rows in one launch.
+__global__ void __launch_bounds__(512) k_scale_split_rows(const float* __restrict__ x, int K, int ldx, int B,
+                                                          uint16_t* __restrict__ xh, uint16_t* __restrict__ xl,
+                                                          int ldk, int vec, float* __restrict__ sc) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
+  __shared__ float red[16];
+  __shared__ float s_scale;
+  const int b = blockIdx.x;
+  const float* p = x + (size_t)b * ldx;
+  float m = 0.f;
+  if (vec) {
+    const int k4 = K / 4;
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    int k = threadIdx.x;
+    for (; k + 3 * 512 < k4; k += 4 * 512) {  // four 16-byte loads in flight per thread
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = __ldg(p4 + k + 512 * j);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
+    }
+    for (; k < k4; k += 512) {
+      const float4 v = __ldg(p4 + k);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (int kk = k4 * 4 + threadIdx.x; kk < K; kk += 512) m = fmaxf(m, fabsf(__ldg(p + kk)));
+  } else {
+    for (int kk = threadIdx.x; kk < K; kk += 512) m = fmaxf(m, fabsf(__ldg(p + kk)));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 16; ++i) m = fmaxf(m, red[i]);
+    const float s = pow2_scale(m);
+    s_scale = s;
+    sc[b] = s;
+    sc[B + b] = 1.0f / s;
+  }
+  __syncthreads();
+  const float sb = s_scale;
+  for (int k8 = threadIdx.x; k8 * 8 < ldk; k8 += 512) {
+    const int k = k8 * 8;
+    float v[8];
+    if (vec && k + 8 <= K) {
+      const float4 a0 = __ldg(reinterpret_cast<const float4*>(p + k)), a1 = __ldg(reinterpret_cast<const float4*>(p + k + 4));
+      v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = k + j < K ? p[k + j] : 0.f;
+    }
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) split_pair(v[2 * j], v[2 * j + 1], sb, h[j], l[j]);
+    *reinterpret_cast<uint4*>(xh + (size_t)b * ldk + k) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(xl + (size_t)b * ldk + k) = make_uint4(l[0], l[1], l[2], l[3]);
+  }
+}
+
 size_t tc_scale_floats(int B) { return (size_t)B * (kScaleChunks + 2); }
 
 bool tc_supported(const FcDev& L) {
@@ -1110,16 +1119,14 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   float* xpart = scw + 2 * (size_t)B;
   ktimer_begin("k_split_x", s);
   if (x_image_major) {
-    k_xscale_rows<<<dim3((unsigned)B, 4), 256, 0, s>>>(x, p.kcols, ldx, B, xpart, xctr, xsc);
-    const long n = (long)B * (p.ldk / 8);
     const int vec = (ldx % 4) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    k_split_rows<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, vec, xsc);
+    k_scale_split_rows<<<(unsigned)B, 512, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, vec, xsc);
   } else {
     k_xscale_cols<<<dim3((unsigned)((B + 31) / 32), kScaleChunks), 256, 0, s>>>(x, p.kcols, ldx, B, xpart, xctr, xsc);
     dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
     k_split_x<<<sg, 256, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, xsc);
   }
-  cudaError_t e = launched(2);
+  cudaError_t e = launched(x_image_major ? 1 : 2);
   ktimer_end("k_split_x", s);
   if (e != cudaSuccess) return e;
   CUtensorMap th, tl;
