@@ -112,13 +112,15 @@ struct Layer {
     if (list_ev) cudaEventDestroy(list_ev);
   }
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
-  std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band) measured at first use
+  std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band / 2: k_fc_j medium) measured at first use
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   size_t tlist_bytes = 0, wd_bytes = 0;  // sizes of the per-call scratch above (allocated at first use)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
   DBuf jw, jrow, jlane, jlut, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
   std::vector<uint32_t> jrow_h;               // host copy of jrow (per-CTA stream ranges)
   JPlan jplan[3];                             // launch plans of k_fc_j for B = 1, 2, 3-4 (built at first use)
+  DBuf jmlane;                                // medium-batch split: lane records
+  std::vector<std::pair<int, JPlan>> jmplan;  // its launch plans per B (built at first use)
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
   // implicit-GEMM CONV (stride 1, channel groups of >= 8 channels): activations
   // converted to bf16 NHWC with each group's cg channels padded to cgp (a
@@ -172,6 +174,7 @@ struct Model {
   bool busy = false;
   int band_min = 0;             // cdn_model_set_kernel_policy (0: default)
   int tc_min = 0;               // cdn_model_set_kernel_policy tensor-core threshold (0: default)
+  bool force_jm = false;        // autotune: the medium-batch merged-stream kernel for one timed launch
   DBuf tc_xh, tc_xl;            // tensor-core FC: fp16 hi / lo split of the activations
   DBuf tc_sc, tc_ctr;           // tensor-core FC: per-image split scales; their arrival counters (zero between calls)
   Acct scratch;                 // inference scratch of this model (every buffer above and the layers' workspaces)
@@ -179,10 +182,11 @@ struct Model {
   cudaStream_t comm_s = nullptr;  // world > 1: the exchanges, overlapped with the next micro-batch's compute
   std::vector<cudaEvent_t> mb_ev; // micro-batch handovers compute -> exchange, exchange -> compute
   DBuf part, rsblk;             // column sharding: a layer's partial sums (all rows), the reduced block
+  DBuf jmpart;                  // medium-batch kernel: column-group partial sums of the running layer (<= 32 images)
   std::vector<int> last_plan;   // plan of the last budgeted round (its scratch is what is allocated)
   void tag_scratch() {
     for (DBuf* b : {&stage[0], &stage[1], &out, &loc, &gath, &host_stage, &conv_a, &conv_o, &conv_t, &ctmp, &tc_xh,
-                    &tc_xl, &tc_sc, &tc_ctr, &part, &rsblk})
+                    &tc_xl, &tc_sc, &tc_ctr, &part, &rsblk, &jmpart})
       b->acct = &scratch;
   }
   // CUDA graphs of repeated infer calls (same buffers, K, plan and state):
@@ -475,6 +479,36 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       if (std::getenv("CDN_JDEBUG"))
         fprintf(stderr, "[cdn] joint layer rows=%u cols=%u G=%d Q=%d jL=%d sub=%u blob=%u\n", nr, H.cols, G, jq, jl, sub,
                 L.dev.jblob);
+      // Medium-batch split (plan_fc_jm): one lane per (row, column group) of the
+      // same stream; groups narrow enough that a CTA's x slice holds 32 images
+      // (<= 96 KB), and more of them while the lanes fill ~16 warps per SM
+      // and keep >= 16 tokens each
+      {
+        const double toks = (double)ix.tokens / std::max<uint32_t>(1, nr);
+        int q2 = (int)std::ceil((double)H.cols * 32 * 4 / (96.0 * 1024));
+        const int want = (int)std::ceil((double)m.num_sms * 16 * 32 / std::max<uint32_t>(1, nr));
+        const int cap = std::max(1, (int)(toks / 16));
+        q2 = std::max(q2, std::min(want, cap));
+        q2 = std::max(1, std::min(q2, std::max(64, (int)std::ceil((double)H.cols * 32 * 4 / (96.0 * 1024)))));
+        if (const char* e = std::getenv("CDN_JMQ")) q2 = std::max(1, std::atoi(e));
+        JointIndex jm;
+        if (build_joint_index(H, L.row0, L.row1, q2, q2, jlut, jl, jm)) {
+          uint32_t sub2 = 0;
+          for (uint32_t i = 0; i < nr; ++i)
+            for (int q = 0; q < q2; ++q) {
+              const uint32_t base = jm.row_bit[i];
+              const uint32_t a = base + (jm.lane[(size_t)i * q2 + q] & 0xffffu);
+              const uint32_t b = q + 1 < q2 ? base + (jm.lane[(size_t)i * q2 + q + 1] & 0xffffu) : jm.row_bit[i + 1];
+              sub2 = std::max<uint32_t>(sub2, (((b + 127) >> 7) - (a >> 7)) * 16u + 16u);
+            }
+          L.jmlane.upload(jm.lane);
+          L.dev.jmQ = q2;
+          L.dev.jmKq = (int)jm.Kq;
+          L.dev.jmsub = sub2;
+          if (std::getenv("CDN_JDEBUG"))
+            fprintf(stderr, "[cdn] joint medium split Q=%d Kq=%u sub=%u\n", q2, jm.Kq, sub2);
+        }
+      }
       if (jq > 1) {
         const int units = (int)((nr + (uint32_t)(32 / GQ) - 1) / (uint32_t)(32 / GQ));
         L.jpart.alloc(sizeof(float) * 4 * (size_t)jq * nr);
@@ -678,6 +712,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.jlut = L.jlut.p ? L.jlut.as<uint32_t>() : nullptr;
   f.jpart = L.jpart.p ? L.jpart.as<float>() : nullptr;
   f.jctr = L.jctr.p ? L.jctr.as<int>() : nullptr;
+  f.jmlane = L.jmlane.p ? L.jmlane.as<uint32_t>() : nullptr;
   f.tivg = L.tivg.p ? L.tivg.as<uint2>() : (L.dev.Wi == 64 ? L.ivg.as<uint2>() : nullptr);
   f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : (L.dev.Wi == 64 ? L.ivm.as<uint16_t>() : nullptr);
   f.tbase = L.tbase.as<uint32_t>();
@@ -711,12 +746,12 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   s.algo_bytes_fixed = s.stream_bytes + 8ull * (nr + 1) + 4ull * H.codebook.size() +
                        3ull * (H.val.n + H.gap.n) + 4ull * nout;
   s.index_bytes = L.rec.n + L.tok.n + L.ivg.n + L.ivm.n + L.tivg.n + L.tivm.n + L.tbase.n + L.troff.n + L.jlane.n +
-                  L.jrow.n;
+                  L.jrow.n + L.jmlane.n;
   s.call_index_bytes = L.jlane.n + L.jrow.n;
   s.resident_bytes = 0;
   for (const DBuf* b : {&L.vw, &L.gw, &L.rp, &L.rec, &L.tok, &L.vlut, &L.glut, &L.vtab, &L.gtab, &L.vsorted,
                         &L.gsorted, &L.cb, &L.bias, &L.flut, &L.ivg, &L.ivm, &L.tivg, &L.tivm, &L.tbase, &L.troff,
-                        &L.msv, &L.msg, &L.jw, &L.jrow, &L.jlane, &L.jlut})
+                        &L.msv, &L.msg, &L.jw, &L.jrow, &L.jlane, &L.jlut, &L.jmlane})
     s.resident_bytes += b->n;
   s.ws_bytes = 0;
   s.in_features = L.in_elems();
@@ -786,6 +821,38 @@ int band_min_batch() {
 // batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
 // The tensor-core path on plan p (list decode unless done ahead this call).
 // bias null: partial sums without bias / ReLU (column-sharded layers).
+// The medium-batch split of the merged-stream kernel (joint.cu plan_fc_jm):
+// image groups of up to kJmGroup images, one launch (+ k_j_reduce) each, so
+// the column-group partial sums (one model-wide buffer: the layers run in
+// stream order) stay <= Q * rows * kJmGroup floats whatever B.
+// nullptr / false: the layer or batch is outside its limits (the caller takes
+// another kernel).
+constexpr int kJmMaxB = 128, kJmGroup = 32;
+const JPlan* jm_plan(const Model& m, const Layer& L, int B) {
+  if (B < 1 || B > kJmMaxB || !jm_supported(L.dev) || L.col || L.blocked) return nullptr;
+  const int Bg = std::min(B, kJmGroup);
+  for (auto& e : L.jmplan)
+    if (e.first == Bg) return e.second.ok ? &e.second : nullptr;
+  auto& v = const_cast<Layer&>(L).jmplan;  // (a cache of a pure function of the layer and B)
+  v.emplace_back(Bg, plan_fc_jm(L.dev, Bg, m.num_sms));
+  return v.back().second.ok ? &v.back().second : nullptr;
+}
+uint64_t jm_scratch(const Model& m, const Layer& L, int B) {
+  const JPlan* p = jm_plan(m, L, B);
+  return p ? jm_part_bytes(L.dev, *p) : 0;
+}
+
+bool jm_call(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, int relu, cudaStream_t s) {
+  const JPlan* p = jm_plan(m, L, B);
+  if (!p) return false;
+  const size_t pb = jm_part_bytes(L.dev, *p);
+  if (pb) m.jmpart.alloc(pb);
+  for (int b0 = 0; b0 < B; b0 += kJmGroup)
+    CUDA_OK(launch_fc_j(L.dev, *p, x + b0, ldx, std::min(kJmGroup, B - b0), y + b0, ldy, relu, s,
+                        m.jmpart.as<float>()));
+  return true;
+}
+
 void tc_call(Model& m, Layer& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
              const float* bias, cudaStream_t s, bool x_im, bool y_im) {
   m.tc_xh.alloc(p.xsplit_elems * 2);
@@ -833,6 +900,9 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
     // of the tensor-core path only
     if (!tc_supported(L.dev)) throw Error(CDN_E_UNSUPPORTED, "blocked layer outside the tensor-core path's limits");
     tcmin = 1;
+  } else if (m.force_jm) {
+    if (!jm_call(m, L, x, ldx, B, y, ldy, relu, s)) throw Error(CDN_E_ARG, "internal: medium-batch kernel forced outside its limits");
+    return;
   } else if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev) && ldx % 4 == 0) {
     int choice = -1;
     for (auto& e : L.kchoice)
@@ -857,6 +927,26 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       fc_forward(m, L, x, ldx, B, y, ldy, s);
       CUDA_OK(cudaEventRecord(e2, s));
       m.tc_min = 0;
+      float tjm = 1e30f;
+      if (jm_plan(m, L, B)) {  // then the medium-batch merged-stream kernel
+        cudaEvent_t e3, e4;
+        CUDA_OK(cudaEventCreate(&e3));
+        CUDA_OK(cudaEventCreate(&e4));
+        struct Unforce {
+          bool& v;
+          ~Unforce() { v = false; }
+        } unforce{m.force_jm};
+        m.force_jm = true;
+        fc_forward(m, L, x, ldx, B, y, ldy, s);  // (untimed: partial-sum buffer, smem attribute)
+        CUDA_OK(cudaEventRecord(e3, s));
+        fc_forward(m, L, x, ldx, B, y, ldy, s);
+        CUDA_OK(cudaEventRecord(e4, s));
+        m.force_jm = false;
+        CUDA_OK(cudaEventSynchronize(e4));
+        CUDA_OK(cudaEventElapsedTime(&tjm, e3, e4));
+        cudaEventDestroy(e3);
+        cudaEventDestroy(e4);
+      }
       CUDA_OK(cudaEventSynchronize(e2));
       float ttc = 0.f, tband = 0.f;
       CUDA_OK(cudaEventElapsedTime(&ttc, e0, e1));
@@ -865,9 +955,11 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       cudaEventDestroy(e1);
       cudaEventDestroy(e2);
       choice = ttc < tband ? 1 : 0;
+      if (tjm < std::min(ttc, tband)) choice = 2;
       L.kchoice.emplace_back(B, choice);
     }
-    tcmin = choice ? B : (1 << 30);
+    if (choice == 2 && jm_call(m, L, x, ldx, B, y, ldy, relu, s)) return;
+    tcmin = choice == 1 ? B : (1 << 30);
   }
   if (B >= tcmin && tc_supported(L.dev)) {
     const TcPlan p = plan_fc_tc(L.dev, B, m.num_sms);
@@ -903,6 +995,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       return;
     }
   }
+  if (B > 4 && small_kernel == 0 && jm_call(m, L, x, ldx, B, y, ldy, relu, s)) return;
   if (B <= 8 && !force_fold && ms_supported(L.dev)) {
     CUDA_OK(launch_fc_ms(L.dev, x, ldx, B, y, ldy, relu, s, m.num_sms));
     return;
@@ -1303,7 +1396,7 @@ void check_chain(const Model& m, const std::vector<int>& bs) {
 // decoded lists / filters): the next call allocates what its plan needs.
 void release_scratch(Model& m) {
   for (DBuf* b : {&m.stage[0], &m.stage[1], &m.out, &m.loc, &m.gath, &m.host_stage, &m.conv_a, &m.conv_o, &m.conv_t,
-                  &m.ctmp, &m.tc_xh, &m.tc_xl, &m.tc_sc, &m.tc_ctr, &m.part, &m.rsblk})
+                  &m.ctmp, &m.tc_xh, &m.tc_xl, &m.tc_sc, &m.tc_ctr, &m.part, &m.rsblk, &m.jmpart})
     b->release();
   for (auto& b : m.lvl) b.release();
   for (auto& L : m.layers) {
@@ -1325,7 +1418,7 @@ void release_scratch(Model& m) {
 // partials).  plan_for keeps plans whose scratch exceeds TOT out.
 uint64_t exec_scratch_bytes(const Model& m, const std::vector<int>& bs, bool host_input) {
   const int f = (int)m.layers.size();
-  uint64_t total = 0, ctmp = 0, xs = 0, sc = 0, tctr = 0, ca = 0, co = 0, ct = 0, slab = 0;
+  uint64_t total = 0, ctmp = 0, xs = 0, sc = 0, tctr = 0, ca = 0, co = 0, ct = 0, slab = 0, jmp = 0;
   for (int i = 0; i < f; ++i) {
     const Layer& L = *m.layers[i];
     const int B = bs[i];
@@ -1364,6 +1457,7 @@ uint64_t exec_scratch_bytes(const Model& m, const std::vector<int>& bs, bool hos
       }
     }
     total += bws + bctr;
+    if (B > 4) jmp = std::max(jmp, jm_scratch(m, L, B));  // medium-batch kernel (small path or autotune candidate)
     if (m.world > 1 && L.col) {  // partial sums of every row + the reduced block
       const ColBlock nb = col_block(L.rows, m.rank, m.world);
       const bool last = i + 1 == f;
@@ -1376,7 +1470,7 @@ uint64_t exec_scratch_bytes(const Model& m, const std::vector<int>& bs, bool hos
   const int Bf = bs[f - 1];
   total += 4ull * Lf.rows * ld4(Bf);  // scores (feature-major; a tensor-core last layer writes them directly)
   if (host_input) total += 2ull * 4 * Bf * m.layers[0]->in_elems() + 4ull * Lf.rows * Bf;  // staging, host scores
-  return total + ctmp + 2 * xs + sc + tctr + ca + co + ct + slab;
+  return total + ctmp + 2 * xs + sc + tctr + ca + co + ct + slab + jmp;
 }
 
 void profile(Model& m, int Bmax, int reps) {
@@ -1507,6 +1601,9 @@ std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
     // the per-layer counters and column-group partials
     uint64_t ws = L->is_conv() ? L->wd_bytes : L->tlist_bytes;
     ws += L->jpart.n + L->jctr.n + L->ctr.n;
+    // the medium-batch kernel's partial sums: bounded by its image group
+    // (kJmGroup), so batch-independent -- the largest over the batches it may take
+    if (!L->is_conv() && Bmax > 4) ws += jm_scratch(m, *L, std::min(Bmax, kJmGroup));
     if (!L->is_conv() && m.world > 1 && L->col)
       ws += 4ull * (2ull * L->rows + 128ull * m.world) * Bmax;  // partial sums + reduced block, C-24: max over grid
     else if (!L->is_conv() && m.world > 1)
@@ -2029,15 +2126,20 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
   if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev)) {
     for (auto& e : L.kchoice)
-      if (e.first == B) tcmin = e.second ? B : (1 << 30);
+      if (e.first == B) tcmin = e.second == 1 ? B : (1 << 30);
   }
   if (B >= tcmin && tc_supported(L.dev)) return "k_fc_tc";
+  if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev)) {
+    for (auto& e : L.kchoice)
+      if (e.first == B && e.second == 2) return "k_fc_j";
+  }
   if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
     const int vec = B > 64 ? 4 : (B > 32 ? 2 : 1);
     return vec == 4 ? "k_fc_band<4>" : (vec == 2 ? "k_fc_band<2>" : "k_fc_band<1>");
   }
   if (B <= 4 && j_supported(L.dev) && plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data()).ok && !std::getenv("CDN_SMALL_KERNEL"))
     return "k_fc_j";
+  if (B > 4 && !std::getenv("CDN_SMALL_KERNEL") && jm_plan(m, L, B)) return "k_fc_j";
   if (B <= 8 && ms_supported(L.dev)) return "k_fc_ms";
   return "k_fc_fold";
 }

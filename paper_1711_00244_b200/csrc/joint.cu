@@ -49,6 +49,11 @@ struct JArgs {
   int relu;
   int B;
   int Q, GQ, RPW, nw, units;
+  const uint32_t* lanes;  // lane records (nrows * G) of the split this launch runs
+  int G, Kq;              // lanes per row, column-group width
+  float* part;            // Q > 1: partial sums [Q][nrows][Bp]
+  int* ctr;               // Q > 1 and !sep: per-warp-unit arrival counters
+  int Bp, sep;            // padded batch (image groups x BS); sep: partials only (k_j_reduce adds them)
   uint32_t sub;       // bytes of one row's staging sub-slot (16-aligned)
   uint32_t off_x, off_slot;  // dynamic smem offsets (the table blob sits at 0)
   int xbulk;          // 1: x contiguous (ldx == 1, B == 1) and 16-byte aligned
@@ -93,8 +98,27 @@ static __device__ __forceinline__ void refill(uint32_t& w0, uint32_t& w1, uint32
 }
 
 template <int BS>
-__device__ __forceinline__ void gather_fma(float (&acc)[BS], float w, uint32_t xa) {
-  if constexpr (BS == 1) {
+__host__ __device__ constexpr int log2_bs() { return BS == 1 ? 0 : BS == 2 ? 1 : BS == 4 ? 2 : BS == 8 ? 3 : BS == 16 ? 4 : 5; }
+// BS >= 8: a column's BS values are BS / 4 16-byte chunks, row c at c * 4 BS
+// bytes.  Lane l reads its column's chunks in the rotated order (j + l) mod
+// (BS / 4), so the eight lanes of a quarter warp hit distinct 16-byte bank
+// groups whatever their columns (BS = 32: conflict-free, 4 wavefronts per
+// 128-bit load); its accumulators hold the images in the same rotated order.
+template <int BS>
+__device__ __forceinline__ void gather_fma(float (&acc)[BS], float w, uint32_t xa, uint32_t rot16) {
+  if constexpr (BS >= 8) {
+#pragma unroll
+    for (int j = 0; j < BS / 4; ++j) {
+      float a, b, cc, d;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(a), "=f"(b), "=f"(cc), "=f"(d)
+                   : "r"(xa + ((((uint32_t)j << 4) + rot16) & (uint32_t)(BS * 4 - 1))));
+      acc[4 * j] = fmaf(w, a, acc[4 * j]);
+      acc[4 * j + 1] = fmaf(w, b, acc[4 * j + 1]);
+      acc[4 * j + 2] = fmaf(w, cc, acc[4 * j + 2]);
+      acc[4 * j + 3] = fmaf(w, d, acc[4 * j + 3]);
+    }
+  } else if constexpr (BS == 1) {
     acc[0] = fmaf(w, ldsf(xa), acc[0]);
   } else if constexpr (BS == 2) {
     float a, b;
@@ -111,19 +135,24 @@ __device__ __forceinline__ void gather_fma(float (&acc)[BS], float w, uint32_t x
   }
 }
 
+// threads per CTA: BS accumulators per thread beside the decoder state
 template <int BS>
-__global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __grid_constant__ JArgs A) {
+__host__ __device__ constexpr int j_max_warps() { return BS >= 32 ? 16 : BS >= 16 ? 24 : kJMaxWarps; }
+
+template <int BS>
+__global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, const __grid_constant__ JArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_w, bar_x;
   __shared__ __align__(8) uint64_t bar_s[kJMaxWarps];
-  constexpr int LBS = BS == 1 ? 0 : (BS == 2 ? 1 : 2);
+  constexpr int LBS = log2_bs<BS>();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   jtrace(A, 0);
   asm volatile("griddepcontrol.launch_dependents;");
 
-  const int G = L.jG, GQ = A.GQ, q = blockIdx.y;
+  const int G = A.G, GQ = A.GQ, q = blockIdx.y;
+  const int b0 = blockIdx.z * BS;                                  // image group
   const int rr = lane / GQ, jj = lane - rr * GQ, j = q * GQ + jj;  // row of the warp unit, lane of the row
-  const int xc0 = q * L.jKq, xcols = min(L.jKq, L.cols - xc0);      // this column group's slice of x
+  const int xc0 = q * A.Kq, xcols = max(0, min(A.Kq, L.cols - xc0));  // this column group's slice of x
   const int u = blockIdx.x * A.nw + warp;  // warp unit: rows u RPW .. u RPW + RPW - 1
   const int row = u * A.RPW + rr;
   const bool ok = u < A.units && row < L.nrows;
@@ -132,8 +161,8 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
   if (ok) {
     r0 = L.jrow[row];
     r1 = L.jrow[row + 1];
-    rec = L.jlane[(size_t)row * G + j];
-    if (j + 1 < G) nxt = L.jlane[(size_t)row * G + j + 1];
+    rec = A.lanes[(size_t)row * G + j];
+    if (j + 1 < G) nxt = A.lanes[(size_t)row * G + j + 1];
   }
   const bool whole = A.Q == 1 && (int)blockIdx.x < A.ncta;  // one stream copy for the whole CTA
   if (tid == 0) {
@@ -197,6 +226,36 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
       if (nb) bulk_g2s(xs, A.x + xc0, (uint32_t)nb, &bar_x);
     }
     for (int i = nb / 4 + tid; i < K; i += blockDim.x) xs[i] = A.x[xc0 + i];
+  } else if constexpr (BS >= 8) {
+    if (tid == 0) mbar_arrive(&bar_x);
+    // 16-byte chunks (4 images of a column), eight loads in flight per thread
+    constexpr int NCH = BS / 4;
+    const int n = K * NCH, step = blockDim.x;
+    const bool v4 = (A.ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(A.x) & 15) == 0;
+    for (int i0 = tid; i0 < n; i0 += 8 * step) {
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * step, c = i / NCH, b = b0 + 4 * (i - c * NCH);
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < n) {
+          const float* src = A.x + (size_t)(xc0 + c) * A.ldx + b;
+          if (v4 && b + 3 < A.B) {
+            v[k] = *reinterpret_cast<const float4*>(src);
+          } else {
+            if (b < A.B) v[k].x = src[0];
+            if (b + 1 < A.B) v[k].y = src[1];
+            if (b + 2 < A.B) v[k].z = src[2];
+            if (b + 3 < A.B) v[k].w = src[3];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * step;
+        if (i < n) reinterpret_cast<float4*>(xs)[i] = v[k];
+      }
+    }
   } else {
     if (tid == 0) mbar_arrive(&bar_x);
     // eight loads in flight per thread before their stores (small CTAs would
@@ -239,6 +298,8 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
     }
     sp += 8;
     uint32_t xa = xbase + (uint32_t)((prev - xc0) * 4 * BS);
+    const uint32_t rot = BS >= 8 ? (uint32_t)lane & (uint32_t)(BS / 4 - 1) : 0u;  // chunk rotation (gather_fma)
+    const uint32_t rot16 = rot << 4;
     float acc[BS];
 #pragma unroll
     for (int b = 0; b < BS; ++b) acc[b] = 0.f;
@@ -274,22 +335,38 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
       const uint32_t ca = e & 0x3fcu;
       const float w = ldsf(cbase + ca);
       xa += ((e & 0x07fffc00u) >> 10) << LBS;
-      if (ca) gather_fma<BS>(acc, w, xa);
+      if (ca) gather_fma<BS>(acc, w, xa, rot16);
     }
     // lanes of a row: fixed shuffle tree (deterministic)
 #pragma unroll
     for (int b = 0; b < BS; ++b)
       for (int o = GQ >> 1; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o, GQ);
+    // accumulator b holds image b0 + img(b) (BS >= 8: chunks rotated by the lane)
+    auto img = [&](int b) { return BS >= 8 ? (int)((((uint32_t)(b >> 2) + rot) & (uint32_t)(BS / 4 - 1)) << 2) + (b & 3) : b; };
     if (A.Q == 1) {
       if (jj == 0 && row < L.nrows) {
         const float v = L.bias[row];
 #pragma unroll
         for (int b = 0; b < BS; ++b) {
-          if (b < A.B) {
+          const int bi = b0 + img(b);
+          if (bi < A.B) {
             float o = acc[b] + v;
             if (A.relu) o = fmaxf(o, 0.f);
-            A.y[(size_t)row * A.ldy + b] = o;
+            A.y[(size_t)row * A.ldy + bi] = o;
           }
+        }
+      }
+    } else if (A.sep) {
+      // column groups, partial sums only: k_j_reduce adds them in group order
+      if (jj == 0 && row < L.nrows) {
+        float* dst = A.part + ((size_t)q * L.nrows + row) * A.Bp + b0;
+        if constexpr (BS >= 4) {
+#pragma unroll
+          for (int b = 0; b < BS; b += 4)
+            __stcg(reinterpret_cast<float4*>(dst + img(b)), make_float4(acc[b], acc[b + 1], acc[b + 2], acc[b + 3]));
+        } else {
+#pragma unroll
+          for (int b = 0; b < BS; ++b) __stcg(dst + b, acc[b]);
         }
       }
     } else {
@@ -297,12 +374,12 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
       // group order (deterministic) and applies bias / ReLU
       if (jj == 0 && row < L.nrows) {
 #pragma unroll
-        for (int b = 0; b < BS; ++b) __stcg(&L.jpart[((size_t)q * L.nrows + row) * BS + b], acc[b]);
+        for (int b = 0; b < BS; ++b) __stcg(&A.part[((size_t)q * L.nrows + row) * A.Bp + b], acc[b]);
       }
       __threadfence();
       __syncwarp();
       int last = 0;
-      if (lane == 0) last = atomicAdd(&L.jctr[u], 1) == A.Q - 1;
+      if (lane == 0) last = atomicAdd(&A.ctr[u], 1) == A.Q - 1;
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
         __threadfence();
@@ -312,20 +389,48 @@ __global__ void __launch_bounds__(kJMaxWarps * 32, 1) k_fc_j(FcDev L, const __gr
           for (int b = 0; b < BS; ++b) {
             if (b < A.B) {
               float sum = 0.f;
-              for (int qq = 0; qq < A.Q; ++qq) sum += __ldcg(&L.jpart[((size_t)qq * L.nrows + row) * BS + b]);
+              for (int qq = 0; qq < A.Q; ++qq) sum += __ldcg(&A.part[((size_t)qq * L.nrows + row) * A.Bp + b]);
               float o = sum + v;
               if (A.relu) o = fmaxf(o, 0.f);
               A.y[(size_t)row * A.ldy + b] = o;
             }
           }
         }
-        if (lane == 0) L.jctr[u] = 0;
+        if (lane == 0) A.ctr[u] = 0;
       }
     }
     jtrace(A, 5);
   }
   __syncthreads();
   jtrace(A, 6);
+}
+
+// Column-group partial sums of the medium-batch split (A.sep): y = act(sum over
+// the Q groups, in group order, + bias) -- Alg. 1 l.9 completed across groups.
+// Thread per output (row, image), consecutive images on consecutive threads.
+__global__ void __launch_bounds__(256) k_j_reduce(const float* __restrict__ part, int Q, int N, int Bp, int B,
+                                                  const float* __restrict__ bias, int relu, float* __restrict__ y,
+                                                  int ldy) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const size_t n = (size_t)N * B, plane = (size_t)N * Bp;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i / B), b = (int)(i - (size_t)row * B);
+    const float* p = part + (size_t)row * Bp + b;
+    float v[8];
+    float sum = 0.f;
+    int q = 0;
+    for (; q + 8 <= Q; q += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcg(p + (size_t)(q + k) * plane);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += v[k];
+    }
+    for (; q < Q; ++q) sum += __ldcg(p + (size_t)q * plane);
+    float o = sum + bias[row];
+    if (relu) o = fmaxf(o, 0.f);
+    y[(size_t)row * ldy + b] = o;
+  }
 }
 
 }  // namespace
@@ -380,9 +485,56 @@ JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
   return p;
 }
 
+bool jm_supported(const FcDev& L) { return L.jw && L.jlut && L.jmlane && L.ncb <= 32 && L.jmQ >= 1; }
+
+JPlan plan_fc_jm(const FcDev& L, int B, int num_sms) {
+  JPlan p;
+  if (!jm_supported(L) || B < 1 || L.nrows <= 0) return p;
+  p.medium = true;
+  if (B > 32) return p;  // (image groups of 32: the caller's launches)
+  p.BS = B <= 8 ? 8 : (B <= 16 ? 16 : 32);
+  p.nbg = 1;
+  p.Bp = p.nbg * p.BS;
+  p.Q = L.jmQ;
+  p.GQ = 1;
+  p.RPW = 32;
+  p.units = (L.nrows + 31) / 32;
+  const int maxw = p.BS >= 32 ? 16 : (p.BS >= 16 ? 24 : kJMaxWarps);
+  auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
+  const size_t off_x = al(L.jblob);
+  const size_t off_slot = al(off_x + (size_t)4 * p.BS * L.jmKq);
+  // every (row block, column group, image group) one CTA of nw warps (one
+  // warp unit of 32 rows each); nw minimises the work of the busiest SM,
+  // ceil(CTAs / SMs) * (nw + kStage) (the CTAs are alike; kStage = a CTA's
+  // table and x staging in warp units), ties to fewer CTAs
+  const long long per = (long long)p.Q * p.nbg;
+  int nw = 0;
+  long long best = 0;
+  for (int w = maxw; w >= 1; --w) {
+    if (off_slot + (size_t)w * 32 * L.jmsub > 227 * 1024 - 1024) continue;
+    const long long ctas = (long long)((p.units + w - 1) / w) * per;
+    constexpr int kStage = 8;
+    const long long cost = (ctas + num_sms - 1) / num_sms * (w + kStage);
+    if (nw == 0 || cost < best) { nw = w; best = cost; }
+  }
+  if (nw >= 1) p.smem = off_slot + (size_t)nw * 32 * L.jmsub;
+  p.nw = nw;
+  p.nrb = nw >= 1 ? (p.units + nw - 1) / nw : 0;
+  p.off_x = (uint32_t)off_x;
+  p.off_slot = (uint32_t)off_slot;
+  p.sub = L.jmsub;
+  p.ok = nw >= 1 && p.nrb * per < 65535LL * 65535LL && p.nbg < 65536;
+  return p;
+}
+
+size_t jm_part_bytes(const FcDev& L, const JPlan& p) {
+  return p.medium && p.Q > 1 ? sizeof(float) * (size_t)p.Q * L.nrows * p.Bp : 0;
+}
+
 cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-                        cudaStream_t s) {
+                        cudaStream_t s, float* part) {
   if (!p.ok) return cudaErrorInvalidValue;
+  if (p.medium && p.Q > 1 && !part) return cudaErrorInvalidValue;
   JArgs a{};
   a.x = x;
   a.ldx = ldx;
@@ -395,6 +547,23 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   a.RPW = p.RPW;
   a.nw = p.nw;
   a.units = p.units;
+  if (p.medium) {
+    a.lanes = L.jmlane;
+    a.G = L.jmQ;
+    a.Kq = L.jmKq;
+    a.part = part;
+    a.ctr = nullptr;
+    a.Bp = p.Bp;
+    a.sep = 1;
+  } else {
+    a.lanes = L.jlane;
+    a.G = L.jG;
+    a.Kq = L.jKq;
+    a.part = L.jpart;
+    a.ctr = L.jctr;
+    a.Bp = p.BS;
+    a.sep = 0;
+  }
   a.sub = p.sub;
   a.off_x = p.off_x;
   a.off_slot = p.off_slot;
@@ -402,7 +571,7 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   for (size_t i = 0; i < p.cta.size() && i < (size_t)kJMaxCta * kJPieces; ++i) a.cta[i] = p.cta[i];
   static unsigned long long* trace = nullptr;
   static const char* trace_path = getenv("CDN_J_TRACE");
-  const size_t ntr = (size_t)p.nrb * p.Q * 8;
+  const size_t ntr = (size_t)p.nrb * p.Q * p.nbg * 8;
   static size_t trace_n = 0;
   if (trace_path && trace_n < ntr) {
     if (trace) cudaFree(trace);
@@ -411,9 +580,9 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   }
   if (trace_path) cudaMemsetAsync(trace, 0, ntr * sizeof(unsigned long long), s);
   a.trace = trace_path ? trace : nullptr;
-  a.xbulk = (p.BS == 1 && ldx == 1 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && L.jKq % 4 == 0) ? 1 : 0;
+  a.xbulk = (p.BS == 1 && ldx == 1 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && a.Kq % 4 == 0) ? 1 : 0;
   cudaError_t e = cudaSuccess;
-  static thread_local size_t set_smem[3] = {0, 0, 0};
+  static thread_local size_t set_smem[6] = {0, 0, 0, 0, 0, 0};
   auto run = [&](auto kern, int bi) {
     if (p.smem > 48 * 1024 && p.smem > set_smem[bi]) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
@@ -421,7 +590,7 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
       set_smem[bi] = p.smem;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)p.nrb, (unsigned)p.Q);
+    cfg.gridDim = dim3((unsigned)p.nrb, (unsigned)p.Q, (unsigned)p.nbg);
     cfg.blockDim = dim3((unsigned)(p.nw * 32));
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = s;
@@ -435,9 +604,28 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   ktimer_begin("k_fc_j", s);
   if (p.BS == 1) run(k_fc_j<1>, 0);
   else if (p.BS == 2) run(k_fc_j<2>, 1);
-  else run(k_fc_j<4>, 2);
+  else if (p.BS == 4) run(k_fc_j<4>, 2);
+  else if (p.BS == 8) run(k_fc_j<8>, 3);
+  else if (p.BS == 16) run(k_fc_j<16>, 4);
+  else run(k_fc_j<32>, 5);
   if (e == cudaSuccess) e = launched();
   ktimer_end("k_fc_j", s);
+  if (e == cudaSuccess && p.medium && p.Q > 1) {
+    cudaLaunchConfig_t cfg = {};
+    const size_t n = (size_t)L.nrows * B;
+    cfg.gridDim = dim3((unsigned)std::min<size_t>((n + 255) / 256, 8 * 148));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ktimer_begin("k_j_reduce", s);
+    e = cudaLaunchKernelEx(&cfg, k_j_reduce, (const float*)part, p.Q, L.nrows, p.Bp, B, L.bias, relu, y, ldy);
+    if (e == cudaSuccess) e = launched();
+    ktimer_end("k_j_reduce", s);
+  }
   if (e == cudaSuccess && trace_path) {  // debug only: append this launch's stamps
     std::vector<unsigned long long> h(ntr);
     e = cudaMemcpyAsync(h.data(), trace, ntr * sizeof(h[0]), cudaMemcpyDeviceToHost, s);

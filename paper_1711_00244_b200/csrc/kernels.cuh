@@ -98,12 +98,19 @@ struct FcDev {
   int jQ = 1, jKq = 0;               // column groups of the lane split, group width (columns)
   float* jpart = nullptr;            // column-group partial sums [Q][nrows][BS]
   int* jctr = nullptr;               // per-warp-unit arrival counters (Q > 1), zero between calls
+  // medium-batch split of the same stream (5 <= B <~ 128, joint.cu plan_fc_jm):
+  // one lane per (row, column group), jmQ groups of jmKq columns, so a CTA's
+  // x slice holds 32 images
+  const uint32_t* jmlane = nullptr;  // nrows * jmQ lane records
+  int jmQ = 0, jmKq = 0;
+  uint32_t jmsub = 0;                // bytes of one (row, group) staging sub-slot
 };
 
 // Launch plan of the merged-stream kernel for one (layer, B <= 4).
 struct JPlan {
   bool ok = false;
-  int BS = 1, Q = 1, GQ = 1, RPW = 1, units = 0, nw = 1, nrb = 0;
+  bool medium = false;  // the medium-batch split (jm*): image groups of BS on grid z, partials + k_j_reduce
+  int BS = 1, Q = 1, GQ = 1, RPW = 1, units = 0, nw = 1, nrb = 0, nbg = 1, Bp = 1;
   uint32_t sub = 0, off_x = 0, off_slot = 0;
   size_t smem = 0;
   std::vector<uint2> cta;  // Q == 1: per CTA (16-byte index of its rows' first bits, bytes to stage)
@@ -111,8 +118,12 @@ struct JPlan {
 bool j_supported(const FcDev& L);
 // row_bit: the host copy of L.jrow (nrows + 1), for the per-CTA stream ranges
 JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit);
+// part: medium plans with Q > 1, jm_part_bytes(L, p) of scratch (else unused)
 cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-                        cudaStream_t s);
+                        cudaStream_t s, float* part = nullptr);
+bool jm_supported(const FcDev& L);
+JPlan plan_fc_jm(const FcDev& L, int B, int num_sms);
+size_t jm_part_bytes(const FcDev& L, const JPlan& p);
 
 // Launch plan of the band kernel for one (layer, B, x) — ok == false means the
 // inputs do not meet its alignment rules (the small-batch kernel then runs).

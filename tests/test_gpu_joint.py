@@ -198,3 +198,70 @@ def test_cold_back_to_back_replicas(torch_dev, cfg, i):
             assert np.abs(o - ref).max() / np.abs(ref).max() <= 1e-4
     for m in ms:
         m.close()
+
+
+# ---- the medium-batch split (plan_fc_jm): one lane per (row, column group),
+# image groups of 8 / 16 / 32 on grid z, partial sums added by k_j_reduce
+
+
+def load_medium(buf, relu, monkeypatch=None, jmq=None):
+    import paper_1711_00244_b200 as cdn
+    if monkeypatch is not None and jmq is not None:
+        monkeypatch.setenv("CDN_JMQ", str(jmq))
+    m = cdn.Model(0)
+    m.load_layer(buf, cdn.LayerDesc.fc(relu))
+    if monkeypatch is not None:
+        monkeypatch.delenv("CDN_JMQ", raising=False)
+    m.set_kernel_policy(1 << 20, 1 << 20)  # no large-batch kernels: B > 4 takes the medium split
+    return m
+
+
+@pytest.mark.parametrize("cfg,i", CONFIG_LAYERS)
+def test_medium_config_layers(torch_dev, cfg, i):
+    torch, dev = torch_dev
+    spec, c, buf, v = config_layer(cfg, i)
+    m = load_medium(buf, spec.relu)
+    for B in (5, 8, 13, 32, 45, 128):
+        a = synth.fc_inputs(spec.cols, B, B)
+        y0 = check(torch, dev, m, c, v, a, spec.relu)
+        assert np.array_equal(forward(torch, dev, m, a, spec.rows), y0)  # fixed reduction order
+    m.close()
+
+
+@pytest.mark.parametrize("name,rows,cols,d,r,k,scale", EDGE)
+@pytest.mark.parametrize("jmq", [None, 1, 3])
+def test_medium_edge_fixtures(torch_dev, monkeypatch, name, rows, cols, d, r, k, scale, jmq):
+    """Q = 1 (direct outputs), 3 (ragged groups, rows with empty groups) and
+    the load-time choice; batches that leave image groups partly empty."""
+    torch, dev = torch_dev
+    W = synth.random_matrix(rows, cols, seed=zlib.crc32(name.encode()) % 1000, scale=scale)
+    v = synth.random_matrix(1, rows, seed=7).ravel()
+    c, buf = layer(name, W, d, r, k, v)
+    m = load_medium(buf, False, monkeypatch, jmq)
+    for B in (5, 16, 33):
+        if m.kernel_name(0, B) != "k_fc_j":  # x slice of a single group larger than shared memory
+            assert cols > 4000
+            continue
+        a = synth.random_activations(cols, B, seed=B)
+        check(torch, dev, m, c, v, a, False)
+    m.close()
+
+
+def test_medium_strided_input(torch_dev):
+    """ldx > B (a slice of a wider activation buffer) and an unaligned ldx:
+    the staging loads fall back from 16-byte vectors to scalars."""
+    torch, dev = torch_dev
+    spec, c, buf, v = config_layer("C2", 0)
+    m = load_medium(buf, spec.relu)
+    for B, ldx in ((7, 9), (20, 24), (32, 35)):
+        a = synth.fc_inputs(spec.cols, B, 11)
+        xb = np.full((spec.cols, ldx), np.nan, dtype=np.float32)
+        xb[:, :B] = a.T
+        x = torch.from_numpy(xb).to(dev)
+        y = torch.full((spec.rows, B), float("nan"), dtype=torch.float32, device=dev)
+        m.layer_forward(0, x, ldx, B, y, B)
+        torch.cuda.synchronize()
+        yy = y.cpu().numpy().T
+        ref = infer.fc_forward(c.dense_q(), a, v, apply_relu=spec.relu)
+        assert np.abs(yy - ref).max() / np.abs(ref).max() <= 1e-4
+    m.close()
