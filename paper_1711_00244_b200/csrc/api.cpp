@@ -112,14 +112,14 @@ struct Layer {
     if (list_ev) cudaEventDestroy(list_ev);
   }
   DBuf bws, bctr;       // band-kernel split partials / arrival counters (grown on demand)
-  std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band / 2: k_fc_j medium) measured at first use
+  std::vector<std::pair<int, int>> kchoice;  // (B, 1: tensor-core / 0: band / 2: k_fc_jm) measured at first use
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   size_t tlist_bytes = 0, wd_bytes = 0;  // sizes of the per-call scratch above (allocated at first use)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
   DBuf jw, jrow, jlane, jlut, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
   std::vector<uint32_t> jrow_h;               // host copy of jrow (per-CTA stream ranges)
   JPlan jplan[3];                             // launch plans of k_fc_j for B = 1, 2, 3-4 (built at first use)
-  DBuf jmlane;                                // medium-batch split: lane records
+  DBuf jmlane, jmperm, jmlut;                 // medium-batch split: lane records, per-group row order, tables
   std::vector<std::pair<int, JPlan>> jmplan;  // its launch plans per B (built at first use)
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
   // implicit-GEMM CONV (stride 1, channel groups of >= 8 channels): activations
@@ -447,30 +447,40 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       // canonical tables, the codebook (entry 0 = padding = 0.0)
       const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
       const int Lg = std::max(1, std::min(H.gap.max_len, kLutMaxBits));
-      std::vector<uint8_t> blob;
-      auto put = [&](const void* p, size_t n) {
-        const size_t o = (blob.size() + 127) & ~(size_t)127;
-        blob.resize(o + n);
-        std::memcpy(blob.data() + o, p, n);
-        return (uint32_t)o;
-      };
       const auto vl = build_lut(H.val, Lv), gl = build_lut(H.gap, Lg), vt = build_tab(H.val), gt = build_tab(H.gap);
       std::vector<uint16_t> vs = H.val.sorted, gs = H.gap.sorted;
       vs.push_back(0);
       gs.push_back(0);
       std::vector<float> cb(32, 0.f);
       for (size_t i = 1; i < H.codebook.size() && i < 32; ++i) cb[i] = H.codebook[i];
-      put(jlut.data(), jlut.size() * 4);
-      L.dev.jo_vlut = put(vl.data(), vl.size() * 4);
-      L.dev.jo_glut = put(gl.data(), gl.size() * 4);
-      L.dev.jo_vtab = put(vt.data(), vt.size() * 4);
-      L.dev.jo_gtab = put(gt.data(), gt.size() * 4);
-      L.dev.jo_vs = put(vs.data(), vs.size() * 2);
-      L.dev.jo_gs = put(gs.data(), gs.size() * 2);
-      L.dev.jo_cb = put(cb.data(), cb.size() * 4);
-      blob.resize((blob.size() + 15) & ~(size_t)15);
-      L.dev.jblob = (uint32_t)blob.size();
-      L.jlut.upload(blob);
+      // o: offsets of vlut, glut, vtab, gtab, vsorted, gsorted, codebook
+      auto make_blob = [&](const std::vector<uint32_t>& joint, uint32_t (&o)[7]) {
+        std::vector<uint8_t> blob;
+        auto put = [&](const void* p, size_t n) {
+          const size_t at = (blob.size() + 127) & ~(size_t)127;
+          blob.resize(at + n);
+          std::memcpy(blob.data() + at, p, n);
+          return (uint32_t)at;
+        };
+        put(joint.data(), joint.size() * 4);
+        o[0] = put(vl.data(), vl.size() * 4);
+        o[1] = put(gl.data(), gl.size() * 4);
+        o[2] = put(vt.data(), vt.size() * 4);
+        o[3] = put(gt.data(), gt.size() * 4);
+        o[4] = put(vs.data(), vs.size() * 2);
+        o[5] = put(gs.data(), gs.size() * 2);
+        o[6] = put(cb.data(), cb.size() * 4);
+        blob.resize((blob.size() + 15) & ~(size_t)15);
+        return blob;
+      };
+      {
+        uint32_t o[7];
+        const auto blob = make_blob(jlut, o);
+        L.dev.jo_vlut = o[0]; L.dev.jo_glut = o[1]; L.dev.jo_vtab = o[2]; L.dev.jo_gtab = o[3];
+        L.dev.jo_vs = o[4]; L.dev.jo_gs = o[5]; L.dev.jo_cb = o[6];
+        L.dev.jblob = (uint32_t)blob.size();
+        L.jlut.upload(blob);
+      }
       L.dev.jL = jl;
       L.dev.jsub = sub;
       L.dev.jQ = jq;
@@ -479,18 +489,34 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       if (std::getenv("CDN_JDEBUG"))
         fprintf(stderr, "[cdn] joint layer rows=%u cols=%u G=%d Q=%d jL=%d sub=%u blob=%u\n", nr, H.cols, G, jq, jl, sub,
                 L.dev.jblob);
-      // Medium-batch split (plan_fc_jm): one lane per (row, column group) of the
-      // same stream; groups narrow enough that a CTA's x slice holds 32 images
-      // (<= 96 KB), and more of them while the lanes fill ~16 warps per SM
-      // and keep >= 16 tokens each
+      // Medium-batch split (plan_fc_jm / k_fc_jm): one lane per (row, column
+      // group) of the same stream.  Q: groups narrow enough that a CTA's x
+      // slice holds 32 images in <= 96 KB, and enough of them for ~16 warp
+      // units per SM (while each lane keeps >= 16 tokens); then the Q whose
+      // CTAs (Q x row ranges of upc warp units) fill the SMs best (one CTA per
+      // SM, a single wave)
+      const uint32_t U = (nr + 31) / 32;
+      int q2 = 1, nrb2 = 1;
       {
         const double toks = (double)ix.tokens / std::max<uint32_t>(1, nr);
-        int q2 = (int)std::ceil((double)H.cols * 32 * 4 / (96.0 * 1024));
-        const int want = (int)std::ceil((double)m.num_sms * 16 * 32 / std::max<uint32_t>(1, nr));
+        const int qx = (int)std::ceil((double)H.cols * 32 * 4 / (96.0 * 1024));
+        const int qw = (int)std::ceil((double)m.num_sms * 16 / std::max<uint32_t>(1, U));
         const int cap = std::max(1, (int)(toks / 16));
-        q2 = std::max(q2, std::min(want, cap));
-        q2 = std::max(1, std::min(q2, std::max(64, (int)std::ceil((double)H.cols * 32 * 4 / (96.0 * 1024)))));
-        if (const char* e = std::getenv("CDN_JMQ")) q2 = std::max(1, std::atoi(e));
+        const int lo = std::max({1, qx, std::min(qw, cap)});
+        double best = -1;
+        for (int q = lo; q <= std::max(lo, std::min(96, cap)); ++q) {
+          const int nrb = std::max(1, std::min<int>((int)U, m.num_sms / q));
+          const double eff = (double)q * nrb / m.num_sms;
+          if (eff > best + 1e-9) { best = eff; q2 = q; nrb2 = nrb; }
+          if (eff >= 0.95) break;
+        }
+        if (const char* e = std::getenv("CDN_JMQ")) {
+          q2 = std::max(1, std::atoi(e));
+          nrb2 = std::max(1, std::min<int>((int)U, m.num_sms / q2));
+        }
+      }
+      {
+        const int upc = (int)((U + nrb2 - 1) / nrb2);
         JointIndex jm;
         if (build_joint_index(H, L.row0, L.row1, q2, q2, jlut, jl, jm)) {
           uint32_t sub2 = 0;
@@ -502,11 +528,45 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
               sub2 = std::max<uint32_t>(sub2, (((b + 127) >> 7) - (a >> 7)) * 16u + 16u);
             }
           L.jmlane.upload(jm.lane);
+          // per group, the rows of each CTA's range (upc warp units) by
+          // decreasing bits: the warp units then hold lanes alike in length
+          // (a warp runs as long as its longest lane) and come longest first
+          // (the CTA's warps take them dynamically)
+          if (nr <= 65536) {
+            const uint32_t kJmSortRows = (uint32_t)upc * 32u;
+            std::vector<uint16_t> perm((size_t)q2 * nr);
+            std::vector<std::pair<uint32_t, uint32_t>> key;
+            for (int q = 0; q < q2; ++q)
+              for (uint32_t b0 = 0; b0 < nr; b0 += kJmSortRows) {
+                const uint32_t b1 = std::min(nr, b0 + kJmSortRows);
+                key.clear();
+                for (uint32_t i = b0; i < b1; ++i) {
+                  const uint32_t a = jm.lane[(size_t)i * q2 + q] & 0xffffu;
+                  const uint32_t b = q + 1 < q2 ? jm.lane[(size_t)i * q2 + q + 1] & 0xffffu : jm.row_bit[i + 1] - jm.row_bit[i];
+                  key.emplace_back(b - a, i);
+                }
+                std::stable_sort(key.begin(), key.end(), [](auto& x, auto& y) { return x.first > y.first; });
+                for (uint32_t k = 0; k < b1 - b0; ++k) perm[(size_t)q * nr + b0 + k] = (uint16_t)key[k].second;
+              }
+            L.jmperm.upload(perm);
+          }
           L.dev.jmQ = q2;
+          L.dev.jmupc = upc;
           L.dev.jmKq = (int)jm.Kq;
           L.dev.jmsub = sub2;
+          // its table blob: a 12-bit joint LUT (16 KB; the x slice and lanes
+          // take the rest of the CTA's share of shared memory)
+          uint32_t o[7];
+          const int jml = std::min(jl, 12);
+          const auto blob = make_blob(jml == jl ? jlut : build_joint_lut(H.val, H.gap, jml), o);
+          L.dev.jmo_vlut = o[0]; L.dev.jmo_glut = o[1]; L.dev.jmo_vtab = o[2]; L.dev.jmo_gtab = o[3];
+          L.dev.jmo_vs = o[4]; L.dev.jmo_gs = o[5]; L.dev.jmo_cb = o[6];
+          L.dev.jmblob = (uint32_t)blob.size();
+          L.dev.jmL = jml;
+          L.jmlut.upload(blob);
           if (std::getenv("CDN_JDEBUG"))
-            fprintf(stderr, "[cdn] joint medium split Q=%d Kq=%u sub=%u\n", q2, jm.Kq, sub2);
+            fprintf(stderr, "[cdn] joint medium split Q=%d Kq=%u sub=%u units/CTA=%d CTAs=%d\n", q2, jm.Kq, sub2, upc,
+                    q2 * (int)((U + upc - 1) / upc));
         }
       }
       if (jq > 1) {
@@ -713,6 +773,8 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.jpart = L.jpart.p ? L.jpart.as<float>() : nullptr;
   f.jctr = L.jctr.p ? L.jctr.as<int>() : nullptr;
   f.jmlane = L.jmlane.p ? L.jmlane.as<uint32_t>() : nullptr;
+  f.jmperm = L.jmperm.p ? L.jmperm.as<uint16_t>() : nullptr;
+  f.jmlut = L.jmlut.p ? L.jmlut.as<uint32_t>() : nullptr;
   f.tivg = L.tivg.p ? L.tivg.as<uint2>() : (L.dev.Wi == 64 ? L.ivg.as<uint2>() : nullptr);
   f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : (L.dev.Wi == 64 ? L.ivm.as<uint16_t>() : nullptr);
   f.tbase = L.tbase.as<uint32_t>();
@@ -746,12 +808,12 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   s.algo_bytes_fixed = s.stream_bytes + 8ull * (nr + 1) + 4ull * H.codebook.size() +
                        3ull * (H.val.n + H.gap.n) + 4ull * nout;
   s.index_bytes = L.rec.n + L.tok.n + L.ivg.n + L.ivm.n + L.tivg.n + L.tivm.n + L.tbase.n + L.troff.n + L.jlane.n +
-                  L.jrow.n + L.jmlane.n;
+                  L.jrow.n + L.jmlane.n + L.jmperm.n;
   s.call_index_bytes = L.jlane.n + L.jrow.n;
   s.resident_bytes = 0;
   for (const DBuf* b : {&L.vw, &L.gw, &L.rp, &L.rec, &L.tok, &L.vlut, &L.glut, &L.vtab, &L.gtab, &L.vsorted,
                         &L.gsorted, &L.cb, &L.bias, &L.flut, &L.ivg, &L.ivm, &L.tivg, &L.tivm, &L.tbase, &L.troff,
-                        &L.msv, &L.msg, &L.jw, &L.jrow, &L.jlane, &L.jlut, &L.jmlane})
+                        &L.msv, &L.msg, &L.jw, &L.jrow, &L.jlane, &L.jlut, &L.jmlane, &L.jmperm, &L.jmlut})
     s.resident_bytes += b->n;
   s.ws_bytes = 0;
   s.in_features = L.in_elems();
@@ -821,20 +883,20 @@ int band_min_batch() {
 // batches (FMA/smem-bound regime), the lane-parallel kernel for small ones.
 // The tensor-core path on plan p (list decode unless done ahead this call).
 // bias null: partial sums without bias / ReLU (column-sharded layers).
-// The medium-batch split of the merged-stream kernel (joint.cu plan_fc_jm):
-// image groups of up to kJmGroup images, one launch (+ k_j_reduce) each, so
-// the column-group partial sums (one model-wide buffer: the layers run in
-// stream order) stay <= Q * rows * kJmGroup floats whatever B.
+// The medium-batch kernel k_fc_jm (joint.cu plan_fc_jm): image groups of up
+// to 32 on grid z, as many per launch as keep the column-group partial sums
+// (one model-wide buffer: the layers run in stream order) within
+// kJmPartCap, further launches for the rest.
 // nullptr / false: the layer or batch is outside its limits (the caller takes
 // another kernel).
-constexpr int kJmMaxB = 128, kJmGroup = 32;
+constexpr int kJmMaxB = 128;
+constexpr size_t kJmPartCap = 16ull << 20;
 const JPlan* jm_plan(const Model& m, const Layer& L, int B) {
   if (B < 1 || B > kJmMaxB || !jm_supported(L.dev) || L.col || L.blocked) return nullptr;
-  const int Bg = std::min(B, kJmGroup);
   for (auto& e : L.jmplan)
-    if (e.first == Bg) return e.second.ok ? &e.second : nullptr;
+    if (e.first == B) return e.second.ok ? &e.second : nullptr;
   auto& v = const_cast<Layer&>(L).jmplan;  // (a cache of a pure function of the layer and B)
-  v.emplace_back(Bg, plan_fc_jm(L.dev, Bg, m.num_sms));
+  v.emplace_back(B, plan_fc_jm(L.dev, B, m.num_sms, kJmPartCap));
   return v.back().second.ok ? &v.back().second : nullptr;
 }
 uint64_t jm_scratch(const Model& m, const Layer& L, int B) {
@@ -847,9 +909,8 @@ bool jm_call(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int l
   if (!p) return false;
   const size_t pb = jm_part_bytes(L.dev, *p);
   if (pb) m.jmpart.alloc(pb);
-  for (int b0 = 0; b0 < B; b0 += kJmGroup)
-    CUDA_OK(launch_fc_j(L.dev, *p, x + b0, ldx, std::min(kJmGroup, B - b0), y + b0, ldy, relu, s,
-                        m.jmpart.as<float>()));
+  for (int b0 = 0; b0 < B; b0 += p->Bp)
+    CUDA_OK(launch_fc_j(L.dev, *p, x + b0, ldx, std::min(p->Bp, B - b0), y + b0, ldy, relu, s, m.jmpart.as<float>()));
   return true;
 }
 
@@ -1515,6 +1576,19 @@ void profile(Model& m, int Bmax, int reps) {
       } else {
         L.list_state = 0;
       }
+      if (!pre && !L.is_conv()) {
+        // a layer without per-call decode: as infer runs it, right behind the
+        // work before it (its staging overlaps that work's tail through the
+        // programmatic dependent launch) -- reps back-to-back runs, the mean
+        CUDA_OK(cudaEventRecord(e0, s));
+        for (int r = 0; r < reps; ++r) step(B);
+        CUDA_OK(cudaEventRecord(e1, s));
+        CUDA_OK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        m.prof[(size_t)i * Bmax + (B - 1)] = ms / reps;
+        continue;
+      }
       for (int r = 0; r < reps; ++r) {
         CUDA_OK(cudaEventRecord(e0, s));
         if (pre && i == 0) {
@@ -1601,9 +1675,14 @@ std::vector<uint64_t> ws_bytes(const Model& m, int Bmax) {
     // the per-layer counters and column-group partials
     uint64_t ws = L->is_conv() ? L->wd_bytes : L->tlist_bytes;
     ws += L->jpart.n + L->jctr.n + L->ctr.n;
-    // the medium-batch kernel's partial sums: bounded by its image group
-    // (kJmGroup), so batch-independent -- the largest over the batches it may take
-    if (!L->is_conv() && Bmax > 4) ws += jm_scratch(m, *L, std::min(Bmax, kJmGroup));
+    // the medium-batch kernel's partial sums: bounded by kJmPartCap (further
+    // launches past it), so batch-independent -- the largest over the batches it may take
+    if (!L->is_conv() && Bmax > 4) {
+      uint64_t jp = 0;
+      for (int B : {5, 9, 17, 33, 65, 97, kJmMaxB})
+        if (B <= Bmax) jp = std::max(jp, jm_scratch(m, *L, B));
+      ws += jp;
+    }
     if (!L->is_conv() && m.world > 1 && L->col)
       ws += 4ull * (2ull * L->rows + 128ull * m.world) * Bmax;  // partial sums + reduced block, C-24: max over grid
     else if (!L->is_conv() && m.world > 1)
@@ -2131,7 +2210,7 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
   if (B >= tcmin && tc_supported(L.dev)) return "k_fc_tc";
   if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev)) {
     for (auto& e : L.kchoice)
-      if (e.first == B && e.second == 2) return "k_fc_j";
+      if (e.first == B && e.second == 2) return "k_fc_jm";
   }
   if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
     const int vec = B > 64 ? 4 : (B > 32 ? 2 : 1);
@@ -2139,7 +2218,7 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
   }
   if (B <= 4 && j_supported(L.dev) && plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data()).ok && !std::getenv("CDN_SMALL_KERNEL"))
     return "k_fc_j";
-  if (B > 4 && !std::getenv("CDN_SMALL_KERNEL") && jm_plan(m, L, B)) return "k_fc_j";
+  if (B > 4 && !std::getenv("CDN_SMALL_KERNEL") && jm_plan(m, L, B)) return "k_fc_jm";
   if (B <= 8 && ms_supported(L.dev)) return "k_fc_ms";
   return "k_fc_fold";
 }

@@ -24,6 +24,7 @@
 // fixed shuffle tree (deterministic).
 // A programmatic dependent launch: the LUT / stream staging runs before
 // griddepcontrol.wait, x (the previous layer's output) after it.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -54,6 +55,13 @@ struct JArgs {
   float* part;            // Q > 1: partial sums [Q][nrows][Bp]
   int* ctr;               // Q > 1 and !sep: per-warp-unit arrival counters
   int Bp, sep;            // padded batch (image groups x BS); sep: partials only (k_j_reduce adds them)
+  const uint16_t* perm;   // GQ == 1: per column group, the row of each warp-unit slot (null: identity)
+  const uint32_t* blob;   // the tables, one bulk copy (FcDev jlut / jmlut) and their offsets
+  uint32_t blob_bytes;
+  int jL;                 // joint LUT width of this blob
+  uint32_t o_vlut, o_glut, o_vtab, o_gtab, o_vs, o_gs, o_cb;
+  int lanecopy;           // GQ == 1: each lane stages its own stream piece (no bulk copies)
+  int upc;                // k_fc_jm: warp units per CTA (taken dynamically by its warps)
   uint32_t sub;       // bytes of one row's staging sub-slot (16-aligned)
   uint32_t off_x, off_slot;  // dynamic smem offsets (the table blob sits at 0)
   int xbulk;          // 1: x contiguous (ldx == 1, B == 1) and 16-byte aligned
@@ -135,6 +143,70 @@ __device__ __forceinline__ void gather_fma(float (&acc)[BS], float w, uint32_t x
   }
 }
 
+// One lane's decode (Alg. 1 l.4-9 over the lane's tokens): the merged-stream
+// reader over bits [lb, le) staged at shared address sp (the 32-bit word
+// holding bit lb), x gathered at xa (shared address of the lane's previous
+// column), acc = sum of w * x over the lane's real tokens.  sb: the tables'
+// shared base (A's blob layout).
+template <int BS>
+__device__ __forceinline__ void j_lane(const FcDev& L, const JArgs& A, uint32_t sb, uint32_t sp, uint32_t lb,
+                                       uint32_t le, uint32_t xa, uint32_t rot16, float (&acc)[BS]) {
+  constexpr int LBS = log2_bs<BS>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t* s_vtab = reinterpret_cast<const uint32_t*>(smem + A.o_vtab);
+  const uint32_t* s_gtab = reinterpret_cast<const uint32_t*>(smem + A.o_gtab);
+  const uint16_t* s_vs = reinterpret_cast<const uint16_t*>(smem + A.o_vs);
+  const uint16_t* s_gs = reinterpret_cast<const uint16_t*>(smem + A.o_gs);
+  const uint32_t lut = sb;
+  const uint32_t cbase = sb + A.o_cb;
+  const int jsh = 32 - A.jL;
+  const int vsh = 32 - L.Lv, gsh = 32 - L.Lg;
+#pragma unroll
+  for (int b = 0; b < BS; ++b) acc[b] = 0.f;
+  int nrem = (int)lb - (int)le;  // -(bits left in the lane)
+  uint32_t off = lb & 31;
+  uint32_t w0 = 0, w1 = 0;
+  if (nrem < 0) {  // (lanes with bits only: the others never load)
+    w0 = lds32(sp);
+    w1 = lds32(sp + 4);
+  }
+  sp += 8;
+  while (nrem < 0) {  // one lookup per (padding run +) real token
+    const uint32_t win = __funnelshift_l(w1, w0, off);
+    uint32_t e = lds32(lut + ((win >> jsh) << 2));
+    if (e == 0) {
+      // slow path, taken by this lane alone (the others wait a few dozen
+      // instructions, not until their lanes end): one token whose codes did
+      // not fit the window, code by code through the plain LUTs (canonical
+      // tables for codes longer than those)
+      const uint32_t ev = lds32(sb + A.o_vlut + ((win >> vsh) << 2));
+      uint32_t vl, vsym;
+      if (ev) { vl = ev >> 16; vsym = ev & 0xffffu; }
+      else { const uint32_t r = slow_sym(win, L.Lv + 1, s_vtab, s_vs, L.vmax); vl = r >> 16; vsym = r & 0xffffu; }
+      off += vl;
+      nrem += (int)vl;
+      refill(w0, w1, off, sp);
+      const uint32_t win2 = __funnelshift_l(w1, w0, off);
+      const uint32_t eg = lds32(sb + A.o_glut + ((win2 >> gsh) << 2));
+      uint32_t gl, gsym;
+      if (eg) { gl = eg >> 16; gsym = eg & 0xffffu; }
+      else { const uint32_t r = slow_sym(win2, L.Lg + 1, s_gtab, s_gs, L.gmax); gl = r >> 16; gsym = r & 0xffffu; }
+      off += gl;
+      nrem += (int)gl;
+      refill(w0, w1, off, sp);
+      // an entry as the LUT would have built it, both codes already consumed
+      e = (vsym * 4u) | (((gsym + 1) * 4u) << 10);
+    }
+    off += e >> 27;
+    nrem += (int)(e >> 27);
+    refill(w0, w1, off, sp);
+    const uint32_t ca = e & 0x3fcu;
+    const float w = ldsf(cbase + ca);
+    xa += ((e & 0x07fffc00u) >> 10) << LBS;
+    if (ca) gather_fma<BS>(acc, w, xa, rot16);
+  }
+}
+
 // threads per CTA: BS accumulators per thread beside the decoder state
 template <int BS>
 __host__ __device__ constexpr int j_max_warps() { return BS >= 32 ? 16 : BS >= 16 ? 24 : kJMaxWarps; }
@@ -150,7 +222,6 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
   asm volatile("griddepcontrol.launch_dependents;");
 
   const int G = A.G, GQ = A.GQ, q = blockIdx.y;
-  const int b0 = blockIdx.z * BS;                                  // image group
   const int rr = lane / GQ, jj = lane - rr * GQ, j = q * GQ + jj;  // row of the warp unit, lane of the row
   const int xc0 = q * A.Kq, xcols = max(0, min(A.Kq, L.cols - xc0));  // this column group's slice of x
   const int u = blockIdx.x * A.nw + warp;  // warp unit: rows u RPW .. u RPW + RPW - 1
@@ -181,13 +252,9 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
       }
     }
     // every table in one bulk copy (host-built blob in this layout)
-    mbar_arrive_expect_tx(&bar_w, L.jblob);
-    bulk_g2s(smem, L.jlut, L.jblob, &bar_w);
+    mbar_arrive_expect_tx(&bar_w, A.blob_bytes);
+    bulk_g2s(smem, A.blob, A.blob_bytes, &bar_w);
   }
-  const uint32_t* s_vtab = reinterpret_cast<const uint32_t*>(smem + L.jo_vtab);
-  const uint32_t* s_gtab = reinterpret_cast<const uint32_t*>(smem + L.jo_gtab);
-  const uint16_t* s_vs = reinterpret_cast<const uint16_t*>(smem + L.jo_vs);
-  const uint16_t* s_gs = reinterpret_cast<const uint16_t*>(smem + L.jo_gs);
 
   const uint32_t lb = ok ? r0 + (rec & 0xffffu) : 0u;                         // lane's bits [lb, le)
   const uint32_t le = ok ? r0 + (j + 1 < G ? (nxt & 0xffffu) : r1 - r0) : 0u;
@@ -219,43 +286,13 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
   jtrace(A, 2);
   float* xs = reinterpret_cast<float*>(smem + A.off_x);
   const int K = xcols;
-  if (A.xbulk) {
-    const int nb = (K * 4) & ~15;
+  if (A.xbulk) {  // x contiguous: ldx == BS == B (the slice is one range)
+    const int nb = (K * 4 * BS) & ~15;
     if (tid == 0) {
       mbar_arrive_expect_tx(&bar_x, (uint32_t)nb);
-      if (nb) bulk_g2s(xs, A.x + xc0, (uint32_t)nb, &bar_x);
+      if (nb) bulk_g2s(xs, A.x + (size_t)xc0 * BS, (uint32_t)nb, &bar_x);
     }
-    for (int i = nb / 4 + tid; i < K; i += blockDim.x) xs[i] = A.x[xc0 + i];
-  } else if constexpr (BS >= 8) {
-    if (tid == 0) mbar_arrive(&bar_x);
-    // 16-byte chunks (4 images of a column), eight loads in flight per thread
-    constexpr int NCH = BS / 4;
-    const int n = K * NCH, step = blockDim.x;
-    const bool v4 = (A.ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(A.x) & 15) == 0;
-    for (int i0 = tid; i0 < n; i0 += 8 * step) {
-      float4 v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = i0 + k * step, c = i / NCH, b = b0 + 4 * (i - c * NCH);
-        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < n) {
-          const float* src = A.x + (size_t)(xc0 + c) * A.ldx + b;
-          if (v4 && b + 3 < A.B) {
-            v[k] = *reinterpret_cast<const float4*>(src);
-          } else {
-            if (b < A.B) v[k].x = src[0];
-            if (b + 1 < A.B) v[k].y = src[1];
-            if (b + 2 < A.B) v[k].z = src[2];
-            if (b + 3 < A.B) v[k].w = src[3];
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = i0 + k * step;
-        if (i < n) reinterpret_cast<float4*>(xs)[i] = v[k];
-      }
-    }
+    for (int i = nb / 4 + tid; i < K * BS; i += blockDim.x) xs[i] = A.x[(size_t)xc0 * BS + i];
   } else {
     if (tid == 0) mbar_arrive(&bar_x);
     // eight loads in flight per thread before their stores (small CTAs would
@@ -279,94 +316,28 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
   jtrace(A, 3);
 
   const uint32_t sb = saddr(smem);
-  const uint32_t lut = sb;
-  const uint32_t cbase = sb + L.jo_cb;
-  const int jsh = 32 - L.jL;
-  const int vsh = 32 - L.Lv, gsh = 32 - L.Lg;
   const uint32_t xbase = sb + A.off_x;
   if (u < A.units) {
     // piece pc holds warps [pc nw / P, (pc + 1) nw / P): warp w's is the last pc whose start is <= w
     mbar_wait(&bar_s[whole ? ((warp + 1) * kJPieces - 1) / A.nw : warp], 0);
     jtrace(A, 4);
-    int nrem = (int)lb - (int)le;  // -(bits left in the lane)
-    uint32_t sp = sb + slot_off + ((lb - rs) >> 5) * 4u;  // (ok lanes only: the others never load)
-    uint32_t off = lb & 31;
-    uint32_t w0 = 0, w1 = 0;
-    if (nrem < 0) {
-      w0 = lds32(sp);
-      w1 = lds32(sp + 4);
-    }
-    sp += 8;
-    uint32_t xa = xbase + (uint32_t)((prev - xc0) * 4 * BS);
-    const uint32_t rot = BS >= 8 ? (uint32_t)lane & (uint32_t)(BS / 4 - 1) : 0u;  // chunk rotation (gather_fma)
-    const uint32_t rot16 = rot << 4;
     float acc[BS];
-#pragma unroll
-    for (int b = 0; b < BS; ++b) acc[b] = 0.f;
-    while (nrem < 0) {  // one lookup per (padding run +) real token
-      const uint32_t win = __funnelshift_l(w1, w0, off);
-      uint32_t e = lds32(lut + ((win >> jsh) << 2));
-      if (e == 0) {
-        // slow path, taken by this lane alone (the others wait a few dozen
-        // instructions, not until their lanes end): one token whose codes did
-        // not fit the window, code by code through the plain LUTs (canonical
-        // tables for codes longer than those)
-        const uint32_t ev = lds32(sb + L.jo_vlut + ((win >> vsh) << 2));
-        uint32_t vl, vsym;
-        if (ev) { vl = ev >> 16; vsym = ev & 0xffffu; }
-        else { const uint32_t r = slow_sym(win, L.Lv + 1, s_vtab, s_vs, L.vmax); vl = r >> 16; vsym = r & 0xffffu; }
-        off += vl;
-        nrem += (int)vl;
-        refill(w0, w1, off, sp);
-        const uint32_t win2 = __funnelshift_l(w1, w0, off);
-        const uint32_t eg = lds32(sb + L.jo_glut + ((win2 >> gsh) << 2));
-        uint32_t gl, gsym;
-        if (eg) { gl = eg >> 16; gsym = eg & 0xffffu; }
-        else { const uint32_t r = slow_sym(win2, L.Lg + 1, s_gtab, s_gs, L.gmax); gl = r >> 16; gsym = r & 0xffffu; }
-        off += gl;
-        nrem += (int)gl;
-        refill(w0, w1, off, sp);
-        // an entry as the LUT would have built it, both codes already consumed
-        e = (vsym * 4u) | (((gsym + 1) * 4u) << 10);
-      }
-      off += e >> 27;
-      nrem += (int)(e >> 27);
-      refill(w0, w1, off, sp);
-      const uint32_t ca = e & 0x3fcu;
-      const float w = ldsf(cbase + ca);
-      xa += ((e & 0x07fffc00u) >> 10) << LBS;
-      if (ca) gather_fma<BS>(acc, w, xa, rot16);
-    }
+    j_lane<BS>(L, A, sb, sb + slot_off + ((lb - rs) >> 5) * 4u, lb, le, xbase + (uint32_t)((prev - xc0) * 4 * BS), 0u,
+               acc);
     // lanes of a row: fixed shuffle tree (deterministic)
 #pragma unroll
     for (int b = 0; b < BS; ++b)
       for (int o = GQ >> 1; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o, GQ);
-    // accumulator b holds image b0 + img(b) (BS >= 8: chunks rotated by the lane)
-    auto img = [&](int b) { return BS >= 8 ? (int)((((uint32_t)(b >> 2) + rot) & (uint32_t)(BS / 4 - 1)) << 2) + (b & 3) : b; };
     if (A.Q == 1) {
       if (jj == 0 && row < L.nrows) {
         const float v = L.bias[row];
 #pragma unroll
         for (int b = 0; b < BS; ++b) {
-          const int bi = b0 + img(b);
-          if (bi < A.B) {
+          if (b < A.B) {
             float o = acc[b] + v;
             if (A.relu) o = fmaxf(o, 0.f);
-            A.y[(size_t)row * A.ldy + bi] = o;
+            A.y[(size_t)row * A.ldy + b] = o;
           }
-        }
-      }
-    } else if (A.sep) {
-      // column groups, partial sums only: k_j_reduce adds them in group order
-      if (jj == 0 && row < L.nrows) {
-        float* dst = A.part + ((size_t)q * L.nrows + row) * A.Bp + b0;
-        if constexpr (BS >= 4) {
-#pragma unroll
-          for (int b = 0; b < BS; b += 4)
-            __stcg(reinterpret_cast<float4*>(dst + img(b)), make_float4(acc[b], acc[b + 1], acc[b + 2], acc[b + 3]));
-        } else {
-#pragma unroll
-          for (int b = 0; b < BS; ++b) __stcg(dst + b, acc[b]);
         }
       }
     } else {
@@ -403,6 +374,152 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
   }
   __syncthreads();
   jtrace(A, 6);
+}
+
+// Medium-batch kernel (FC, one launch per group of <= 32 images): the same
+// lane decode over the medium split -- one lane per (row, column group), the
+// CTA = one column group (its x slice, BS images per column) x a range of
+// upc warp units (32 rows each, taken in the group's row order, longest
+// first).  Its warps take the units dynamically (the first nw in order, staged
+// before griddepcontrol.wait; the rest from a shared counter), so the CTA's
+// warps finish together however the lanes' lengths vary; each lane stages its
+// own piece of the stream in its sub-slot before decoding a unit.  Output:
+// the column group's partial sums (Q > 1; k_j_reduce adds them in group
+// order) or y itself (Q == 1).
+template <int BS>
+__global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_jm(FcDev L, const __grid_constant__ JArgs A) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_w, bar_x;
+  __shared__ int s_next;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  jtrace(A, 0);
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int q = blockIdx.y;
+  const int b0 = blockIdx.z * BS;  // image group of this CTA
+  const int xc0 = q * A.Kq, K = max(0, min(A.Kq, L.cols - xc0));
+  const int u0 = blockIdx.x * A.upc, u1 = min(A.units, u0 + A.upc);
+  if (tid == 0) {
+    mbar_init(&bar_w, 1);
+    mbar_init(&bar_x, 1);
+    mbar_fence_init();
+    s_next = A.nw;
+    mbar_arrive_expect_tx(&bar_w, A.blob_bytes);
+    bulk_g2s(smem, A.blob, A.blob_bytes, &bar_w);
+  }
+  const uint32_t sb = saddr(smem);
+  const uint32_t sub_off = A.off_slot + ((uint32_t)warp * 32u + (uint32_t)lane) * A.sub;
+  const uint32_t rot = (uint32_t)lane & (uint32_t)(BS / 4 - 1);
+  uint32_t lb = 0, le = 0;
+  int prev = 0, row = L.nrows;
+  // lane of unit u: its row (the group's order), bits [lb, le), previous
+  // column; its piece (16-byte blocks + one of read-ahead) into the sub-slot
+  auto setup = [&](int u) {
+    const int slot = u * 32 + lane;
+    lb = le = 0;
+    prev = 0;
+    row = L.nrows;
+    if (slot < L.nrows) {
+      row = A.perm ? (int)A.perm[(size_t)q * L.nrows + slot] : slot;
+      const uint32_t r0 = L.jrow[row], r1 = L.jrow[row + 1];
+      const uint32_t rec = A.lanes[(size_t)row * A.G + q];
+      const uint32_t nxt = q + 1 < A.G ? A.lanes[(size_t)row * A.G + q + 1] : 0u;
+      lb = r0 + (rec & 0xffffu);
+      le = r0 + (q + 1 < A.G ? (nxt & 0xffffu) : r1 - r0);
+      prev = (int)(rec >> 16) - 1;
+      if (le > lb) {
+        const uint32_t n16 = ((le + 127) >> 7) - (lb >> 7) + 1;
+        const uint4* src = reinterpret_cast<const uint4*>(L.jw) + (lb >> 7);
+        uint4* dst = reinterpret_cast<uint4*>(smem + sub_off);
+        for (uint32_t i0 = 0; i0 < n16; i0 += 8) {
+          uint4 v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (i0 + k < n16) v[k] = __ldg(src + i0 + k);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (i0 + k < n16) dst[i0 + k] = v[k];
+        }
+      }
+    }
+  };
+  int u = u0 + warp;
+  if (u < u1) setup(u);
+  jtrace(A, 1);
+
+  // ---- activations (after the producer of x finished)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  jtrace(A, 2);
+  float* xs = reinterpret_cast<float*>(smem + A.off_x);
+  if (A.xbulk) {  // x contiguous: ldx == BS == B (the slice is one range)
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar_x, (uint32_t)(K * 4 * BS));
+      if (K) bulk_g2s(xs, A.x + (size_t)xc0 * BS, (uint32_t)(K * 4 * BS), &bar_x);
+    }
+  } else {
+    // (image group b0: columns' images b0 .. b0 + BS - 1)
+    if (tid == 0) mbar_arrive(&bar_x);
+    // 16-byte chunks (4 images of a column), eight loads in flight per thread
+    constexpr int NCH = BS / 4;
+    const int n = K * NCH, step = blockDim.x;
+    const bool v4 = (A.ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(A.x) & 15) == 0;
+    for (int i0 = tid; i0 < n; i0 += 8 * step) {
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * step, c = i / NCH, b = b0 + 4 * (i - c * NCH);
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < n) {
+          const float* src = A.x + (size_t)(xc0 + c) * A.ldx + b;
+          if (v4 && b + 3 < A.B) {
+            v[k] = *reinterpret_cast<const float4*>(src);
+          } else {
+            if (b < A.B) v[k].x = src[0];
+            if (b + 1 < A.B) v[k].y = src[1];
+            if (b + 2 < A.B) v[k].z = src[2];
+            if (b + 3 < A.B) v[k].w = src[3];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i0 + k * step < n) reinterpret_cast<float4*>(xs)[i0 + k * step] = v[k];
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar_w, 0);
+  mbar_wait(&bar_x, 0);
+  jtrace(A, 3);
+  const uint32_t xbase = sb + A.off_x;
+  auto img = [&](int b) { return (int)((((uint32_t)(b >> 2) + rot) & (uint32_t)(BS / 4 - 1)) << 2) + (b & 3); };
+  while (u < u1) {
+    float acc[BS];
+    j_lane<BS>(L, A, sb, sb + sub_off + ((lb & 127u) >> 5) * 4u, lb, le, xbase + (uint32_t)((prev - xc0) * 4 * BS),
+               rot << 4, acc);
+    if (row < L.nrows) {
+      if (A.Q == 1) {
+        const float v = L.bias[row];
+#pragma unroll
+        for (int b = 0; b < BS; ++b) {
+          const int bi = b0 + img(b);
+          if (bi < A.B) {
+            float o = acc[b] + v;
+            if (A.relu) o = fmaxf(o, 0.f);
+            A.y[(size_t)row * A.ldy + bi] = o;
+          }
+        }
+      } else {
+        float* dst = A.part + ((size_t)q * L.nrows + row) * A.Bp + b0;
+#pragma unroll
+        for (int b = 0; b < BS; b += 4)
+          __stcg(reinterpret_cast<float4*>(dst + img(b)), make_float4(acc[b], acc[b + 1], acc[b + 2], acc[b + 3]));
+      }
+    }
+    int nu = 0;
+    if (lane == 0) nu = atomicAdd(&s_next, 1);
+    u = u0 + __shfl_sync(0xffffffffu, nu, 0);
+    if (u < u1) setup(u);
+  }
+  jtrace(A, 5);
 }
 
 // Column-group partial sums of the medium-batch split (A.sep): y = act(sum over
@@ -485,45 +602,47 @@ JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
   return p;
 }
 
-bool jm_supported(const FcDev& L) { return L.jw && L.jlut && L.jmlane && L.ncb <= 32 && L.jmQ >= 1; }
+int j_max_warps_host(int BS) { return BS >= 32 ? j_max_warps<32>() : BS >= 16 ? j_max_warps<16>() : j_max_warps<8>(); }
 
-JPlan plan_fc_jm(const FcDev& L, int B, int num_sms) {
+bool jm_supported(const FcDev& L) { return L.jw && L.jmlut && L.jmlane && L.ncb <= 32 && L.jmQ >= 1; }
+
+JPlan plan_fc_jm(const FcDev& L, int B, int num_sms, size_t part_cap) {
+  (void)num_sms;  // (the CTA geometry is the load-time split's: L.jmupc)
   JPlan p;
   if (!jm_supported(L) || B < 1 || L.nrows <= 0) return p;
   p.medium = true;
-  if (B > 32) return p;  // (image groups of 32: the caller's launches)
   p.BS = B <= 8 ? 8 : (B <= 16 ? 16 : 32);
-  p.nbg = 1;
+  // image groups of BS on grid z, as many per launch as the partial sums
+  // (Q x rows x groups x BS floats) fit in part_cap (at least one)
+  const int groups = (B + p.BS - 1) / p.BS;
+  const size_t per_group = sizeof(float) * (size_t)std::max(1, L.jmQ) * L.nrows * p.BS;
+  p.nbg = L.jmQ > 1 ? (int)std::max<size_t>(1, std::min<size_t>(groups, part_cap / per_group)) : groups;
   p.Bp = p.nbg * p.BS;
   p.Q = L.jmQ;
   p.GQ = 1;
   p.RPW = 32;
   p.units = (L.nrows + 31) / 32;
-  const int maxw = p.BS >= 32 ? 16 : (p.BS >= 16 ? 24 : kJMaxWarps);
+  p.upc = std::max(1, L.jmupc);
+  p.nrb = (p.units + p.upc - 1) / p.upc;
   auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
-  const size_t off_x = al(L.jblob);
-  const size_t off_slot = al(off_x + (size_t)4 * p.BS * L.jmKq);
-  // every (row block, column group, image group) one CTA of nw warps (one
-  // warp unit of 32 rows each); nw minimises the work of the busiest SM,
-  // ceil(CTAs / SMs) * (nw + kStage) (the CTAs are alike; kStage = a CTA's
-  // table and x staging in warp units), ties to fewer CTAs
-  const long long per = (long long)p.Q * p.nbg;
-  int nw = 0;
-  long long best = 0;
-  for (int w = maxw; w >= 1; --w) {
-    if (off_slot + (size_t)w * 32 * L.jmsub > 227 * 1024 - 1024) continue;
-    const long long ctas = (long long)((p.units + w - 1) / w) * per;
-    constexpr int kStage = 8;
-    const long long cost = (ctas + num_sms - 1) / num_sms * (w + kStage);
-    if (nw == 0 || cost < best) { nw = w; best = cost; }
-  }
-  if (nw >= 1) p.smem = off_slot + (size_t)nw * 32 * L.jmsub;
+  // warps per CTA: up to the register budget of BS accumulators, no more than
+  // the CTA's units; the small-batch kernel's tables (the wider joint LUT:
+  // fewer lookups) when they fit beside the x slice and the staging
+  // sub-slots, else the narrow-LUT blob, and fewer warps while even that
+  // does not fit
+  const int nw0 = std::min(j_max_warps_host(p.BS), p.upc);
+  const size_t xb = (size_t)4 * p.BS * L.jmKq, sl = (size_t)nw0 * 32 * L.jmsub;
+  p.jbig = L.jlut && al(al(L.jblob) + xb) + sl <= 227 * 1024 - 1024;
+  const size_t off_x = al(p.jbig ? L.jblob : L.jmblob);
+  const size_t off_slot = al(off_x + xb);
+  int nw = nw0;
+  while (nw >= 1 && off_slot + (size_t)nw * 32 * L.jmsub > 227 * 1024 - 1024) --nw;
   p.nw = nw;
-  p.nrb = nw >= 1 ? (p.units + nw - 1) / nw : 0;
+  p.smem = nw >= 1 ? off_slot + (size_t)nw * 32 * L.jmsub : 0;
   p.off_x = (uint32_t)off_x;
   p.off_slot = (uint32_t)off_slot;
   p.sub = L.jmsub;
-  p.ok = nw >= 1 && p.nrb * per < 65535LL * 65535LL && p.nbg < 65536;
+  p.ok = nw >= 1 && p.nrb < 65535 && p.Q < 65535 && p.nbg < 65535;
   return p;
 }
 
@@ -555,6 +674,22 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
     a.ctr = nullptr;
     a.Bp = p.Bp;
     a.sep = 1;
+    a.perm = L.jmperm;
+    a.lanecopy = 1;
+    a.upc = p.upc;
+    if (p.jbig) {
+      a.blob = L.jlut;
+      a.blob_bytes = L.jblob;
+      a.jL = L.jL;
+      a.o_vlut = L.jo_vlut; a.o_glut = L.jo_glut; a.o_vtab = L.jo_vtab; a.o_gtab = L.jo_gtab;
+      a.o_vs = L.jo_vs; a.o_gs = L.jo_gs; a.o_cb = L.jo_cb;
+    } else {
+      a.blob = L.jmlut;
+      a.blob_bytes = L.jmblob;
+      a.jL = L.jmL;
+      a.o_vlut = L.jmo_vlut; a.o_glut = L.jmo_glut; a.o_vtab = L.jmo_vtab; a.o_gtab = L.jmo_gtab;
+      a.o_vs = L.jmo_vs; a.o_gs = L.jmo_gs; a.o_cb = L.jmo_cb;
+    }
   } else {
     a.lanes = L.jlane;
     a.G = L.jG;
@@ -563,6 +698,13 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
     a.ctr = L.jctr;
     a.Bp = p.BS;
     a.sep = 0;
+    a.perm = nullptr;
+    a.lanecopy = 0;
+    a.blob = L.jlut;
+    a.blob_bytes = L.jblob;
+    a.jL = L.jL;
+    a.o_vlut = L.jo_vlut; a.o_glut = L.jo_glut; a.o_vtab = L.jo_vtab; a.o_gtab = L.jo_gtab;
+    a.o_vs = L.jo_vs; a.o_gs = L.jo_gs; a.o_cb = L.jo_cb;
   }
   a.sub = p.sub;
   a.off_x = p.off_x;
@@ -580,7 +722,7 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   }
   if (trace_path) cudaMemsetAsync(trace, 0, ntr * sizeof(unsigned long long), s);
   a.trace = trace_path ? trace : nullptr;
-  a.xbulk = (p.BS == 1 && ldx == 1 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && a.Kq % 4 == 0) ? 1 : 0;
+  a.xbulk = (ldx == p.BS && B == p.BS && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && a.Kq % 4 == 0) ? 1 : 0;
   cudaError_t e = cudaSuccess;
   static thread_local size_t set_smem[6] = {0, 0, 0, 0, 0, 0};
   auto run = [&](auto kern, int bi) {
@@ -601,15 +743,21 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, kern, L, a);
   };
-  ktimer_begin("k_fc_j", s);
-  if (p.BS == 1) run(k_fc_j<1>, 0);
-  else if (p.BS == 2) run(k_fc_j<2>, 1);
-  else if (p.BS == 4) run(k_fc_j<4>, 2);
-  else if (p.BS == 8) run(k_fc_j<8>, 3);
-  else if (p.BS == 16) run(k_fc_j<16>, 4);
-  else run(k_fc_j<32>, 5);
-  if (e == cudaSuccess) e = launched();
-  ktimer_end("k_fc_j", s);
+  if (!p.medium) {
+    ktimer_begin("k_fc_j", s);
+    if (p.BS == 1) run(k_fc_j<1>, 0);
+    else if (p.BS == 2) run(k_fc_j<2>, 1);
+    else run(k_fc_j<4>, 2);
+    if (e == cudaSuccess) e = launched();
+    ktimer_end("k_fc_j", s);
+  } else {
+    ktimer_begin("k_fc_jm", s);
+    if (p.BS == 8) run(k_fc_jm<8>, 3);
+    else if (p.BS == 16) run(k_fc_jm<16>, 4);
+    else run(k_fc_jm<32>, 5);
+    if (e == cudaSuccess) e = launched();
+    ktimer_end("k_fc_jm", s);
+  }
   if (e == cudaSuccess && p.medium && p.Q > 1) {
     cudaLaunchConfig_t cfg = {};
     const size_t n = (size_t)L.nrows * B;

@@ -102,8 +102,15 @@ struct FcDev {
   // one lane per (row, column group), jmQ groups of jmKq columns, so a CTA's
   // x slice holds 32 images
   const uint32_t* jmlane = nullptr;  // nrows * jmQ lane records
+  const uint16_t* jmperm = nullptr;  // [jmQ][nrows]: rows of each group by decreasing bits within blocks of
+                                     // kJmSortRows (a warp's lanes then run about equally many steps)
   int jmQ = 0, jmKq = 0;
+  int jmupc = 1;                     // warp units (32 rows) per CTA: rows sorted within these ranges
   uint32_t jmsub = 0;                // bytes of one (row, group) staging sub-slot
+  const uint32_t* jmlut = nullptr;   // its table blob (the jlut layout with a narrower joint LUT, jmL bits:
+  uint32_t jmblob = 0;               // small enough for two CTAs per SM)
+  int jmL = 12;
+  uint32_t jmo_vlut = 0, jmo_glut = 0, jmo_vtab = 0, jmo_gtab = 0, jmo_vs = 0, jmo_gs = 0, jmo_cb = 0;
 };
 
 // Launch plan of the merged-stream kernel for one (layer, B <= 4).
@@ -111,6 +118,8 @@ struct JPlan {
   bool ok = false;
   bool medium = false;  // the medium-batch split (jm*): image groups of BS on grid z, partials + k_j_reduce
   int BS = 1, Q = 1, GQ = 1, RPW = 1, units = 0, nw = 1, nrb = 0, nbg = 1, Bp = 1;
+  int upc = 0;          // medium: warp units per CTA (its warps take them dynamically)
+  bool jbig = false;    // medium: stages the small-batch kernel's table blob (wider joint LUT), else jmlut
   uint32_t sub = 0, off_x = 0, off_slot = 0;
   size_t smem = 0;
   std::vector<uint2> cta;  // Q == 1: per CTA (16-byte index of its rows' first bits, bytes to stage)
@@ -122,7 +131,9 @@ JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit);
 cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                         cudaStream_t s, float* part = nullptr);
 bool jm_supported(const FcDev& L);
-JPlan plan_fc_jm(const FcDev& L, int B, int num_sms);
+// part_cap: largest partial-sum buffer a launch may use (image groups beyond
+// it run in further launches); the caller launches ceil(B / Bp) times
+JPlan plan_fc_jm(const FcDev& L, int B, int num_sms, size_t part_cap);
 size_t jm_part_bytes(const FcDev& L, const JPlan& p);
 
 // Launch plan of the band kernel for one (layer, B, x) — ok == false means the

@@ -23,3 +23,14 @@ while o < len(data):
         c = rel[:, ev]
         print(f"  ev{ev}: min {np.nanmin(c):7.2f} med {np.nanmedian(c):7.2f} max {np.nanmax(c):7.2f} us")
     k += 1
+
+# per-CTA phase durations of the last launch (us): staging (entry -> tables
+# and x resident), warp 0's decode (ev4 -> ev5), and its wait for the CTA's
+# other warps (ev5 -> ev6); CTA entry times show the waves
+if k:
+    d = lambda a, b: rel[:, b] - rel[:, a]
+    for name, a, b in (("staging", 0, 3), ("warp0 decode", 4, 5), ("tail", 5, 6), ("cta", 0, 6)):
+        c = d(a, b)
+        print(f"  {name:13s}: min {np.nanmin(c):7.2f} med {np.nanmedian(c):7.2f} max {np.nanmax(c):7.2f} us")
+    st = np.sort(rel[:, 0])
+    print("  entry times (every 16th CTA):", " ".join(f"{v:.1f}" for v in st[::16]))

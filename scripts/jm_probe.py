@@ -56,7 +56,7 @@ def main():
             r["jm_us"] = timed(torch, m, x, B, y, sp)
             cdn.kernel_timer(True)
             timed(torch, m, x, B, y, sp)
-            for k in ("k_fc_j", "k_j_reduce"):
+            for k in ("k_fc_jm", "k_j_reduce"):
                 t, n = cdn.kernel_time(k)
                 r[k + "_us"] = t / max(n, 1) * 1e3
             cdn.kernel_timer(False)

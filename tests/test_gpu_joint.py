@@ -1,8 +1,9 @@
-"""GPU parity of the merged-stream small-batch kernel k_fc_j (joint.cu, B <= 4)
-against the fp64 oracle: every FC config layer at B = 1..4, the edge fixtures
-with narrow joint LUTs (many slow-path tokens) and column groups Q = 1, 2, 4
-(the lane split and the cross-CTA partial sums), and bit-identical repeated
-launches (fixed reduction orders).  Tolerance: ||dy||_inf / ||y||_inf <= 1e-4
+"""GPU parity of the merged-stream kernels (joint.cu) against the fp64 oracle:
+the small-batch k_fc_j (B <= 4) on every FC config layer at B = 1..4, the edge
+fixtures with narrow joint LUTs (many slow-path tokens) and column groups
+Q = 1, 2, 4 (the lane split and the cross-CTA partial sums); the medium-batch
+k_fc_jm (B = 5..128, groups of <= 32 images) on the same layers and fixtures;
+bit-identical repeated launches (fixed reduction orders).  Tolerance: ||dy||_inf / ||y||_inf <= 1e-4
 (north_star) and the elementwise fp32 accumulation bound."""
 import zlib
 
@@ -63,8 +64,8 @@ def forward(torch, dev, m, a, N, stream=0):
     return y.cpu().numpy().T
 
 
-def check(torch, dev, m, c, v, a, relu):
-    assert m.kernel_name(0, a.shape[0]) == "k_fc_j"
+def check(torch, dev, m, c, v, a, relu, kernel="k_fc_j"):
+    assert m.kernel_name(0, a.shape[0]) == kernel
     y = forward(torch, dev, m, a, c.layer.rows)
     ref = infer.fc_forward(c.dense_q(), a, v, apply_relu=relu)
     assert np.isfinite(y).all()
@@ -200,8 +201,8 @@ def test_cold_back_to_back_replicas(torch_dev, cfg, i):
         m.close()
 
 
-# ---- the medium-batch split (plan_fc_jm): one lane per (row, column group),
-# image groups of 8 / 16 / 32 on grid z, partial sums added by k_j_reduce
+# ---- the medium-batch kernel k_fc_jm (plan_fc_jm): one lane per (row, column
+# group), launches of <= 32 images, partial sums added by k_j_reduce
 
 
 def load_medium(buf, relu, monkeypatch=None, jmq=None):
@@ -223,7 +224,7 @@ def test_medium_config_layers(torch_dev, cfg, i):
     m = load_medium(buf, spec.relu)
     for B in (5, 8, 13, 32, 45, 128):
         a = synth.fc_inputs(spec.cols, B, B)
-        y0 = check(torch, dev, m, c, v, a, spec.relu)
+        y0 = check(torch, dev, m, c, v, a, spec.relu, "k_fc_jm")
         assert np.array_equal(forward(torch, dev, m, a, spec.rows), y0)  # fixed reduction order
     m.close()
 
@@ -239,11 +240,11 @@ def test_medium_edge_fixtures(torch_dev, monkeypatch, name, rows, cols, d, r, k,
     c, buf = layer(name, W, d, r, k, v)
     m = load_medium(buf, False, monkeypatch, jmq)
     for B in (5, 16, 33):
-        if m.kernel_name(0, B) != "k_fc_j":  # x slice of a single group larger than shared memory
+        if m.kernel_name(0, B) != "k_fc_jm":  # x slice of a single group larger than shared memory
             assert cols > 4000
             continue
         a = synth.random_activations(cols, B, seed=B)
-        check(torch, dev, m, c, v, a, False)
+        check(torch, dev, m, c, v, a, False, "k_fc_jm")
     m.close()
 
 
