@@ -119,6 +119,7 @@ struct Layer {
   DBuf jw, jrow, jlane, jlut, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
   std::vector<uint32_t> jrow_h;               // host copy of jrow (per-CTA stream ranges)
   JPlan jplan[3];                             // launch plans of k_fc_j for B = 1, 2, 3-4 (built at first use)
+  DBuf jcta[3];                               // their per-CTA stream ranges (device copies of JPlan::cta)
   DBuf jmlane, jmperm, jmlut;                 // medium-batch split: lane records, per-group row order, tables
   std::vector<std::pair<int, JPlan>> jmplan;  // its launch plans per B (built at first use)
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
@@ -1049,8 +1050,15 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
   }();
   const bool force_fold = small_kernel == 1;
   if (B <= 4 && small_kernel == 0 && j_supported(L.dev)) {
-    JPlan& p = L.jplan[B <= 1 ? 0 : (B <= 2 ? 1 : 2)];  // cached: the plan is host work on every call otherwise
-    if (p.nrb == 0) p = plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data());
+    const int pi = B <= 1 ? 0 : (B <= 2 ? 1 : 2);
+    JPlan& p = L.jplan[pi];  // cached: the plan is host work on every call otherwise
+    if (p.nrb == 0) {
+      p = plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data());
+      if (p.ok && !p.cta.empty()) {
+        L.jcta[pi].upload(p.cta);
+        p.cta_dev = L.jcta[pi].as<uint2>();
+      }
+    }
     if (p.ok) {
       CUDA_OK(launch_fc_j(L.dev, p, x, ldx, B, y, ldy, relu, s));
       return;

@@ -39,7 +39,7 @@ namespace {
 using namespace dev;
 
 constexpr int kJMaxWarps = 32;
-constexpr int kJMaxCta = 160;  // CTA stream ranges passed in the launch parameters
+constexpr int kJMaxCta = 1024;  // CTAs whose rows are staged as one stream range
 constexpr int kJPieces = 4;    // a CTA's stream bits arrive in this many pieces (warps start on their own)
 
 struct JArgs {
@@ -67,8 +67,9 @@ struct JArgs {
   int xbulk;          // 1: x contiguous (ldx == 1, B == 1) and 16-byte aligned
   unsigned long long* trace;  // debug (env CDN_J_TRACE): per CTA 8 globaltimer stamps, else null
   int ncta;           // Q == 1: CTAs whose stream ranges are in cta[] (the rest stage per warp)
-  uint2 cta[kJMaxCta * kJPieces];  // Q == 1: per CTA and piece (16-byte index of the piece's first bits,
-                                   // bytes to stage); piece p = the CTA's warps [p nw / P, (p+1) nw / P)
+  const uint2* cta;   // Q == 1: per CTA and piece (16-byte index of the piece's first bits, bytes to
+                      // stage); piece p = the CTA's warps [p nw / P, (p+1) nw / P) (device memory: kernel
+                      // parameters stay under 4 KB)
 };
 
 __device__ __forceinline__ void jtrace(const JArgs& A, int ev) {
@@ -709,8 +710,8 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   a.sub = p.sub;
   a.off_x = p.off_x;
   a.off_slot = p.off_slot;
-  a.ncta = (int)(p.cta.size() / kJPieces);
-  for (size_t i = 0; i < p.cta.size() && i < (size_t)kJMaxCta * kJPieces; ++i) a.cta[i] = p.cta[i];
+  a.ncta = p.cta_dev ? (int)(p.cta.size() / kJPieces) : 0;
+  a.cta = p.cta_dev;
   static unsigned long long* trace = nullptr;
   static const char* trace_path = getenv("CDN_J_TRACE");
   const size_t ntr = (size_t)p.nrb * p.Q * p.nbg * 8;

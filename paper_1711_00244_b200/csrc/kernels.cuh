@@ -123,6 +123,7 @@ struct JPlan {
   uint32_t sub = 0, off_x = 0, off_slot = 0;
   size_t smem = 0;
   std::vector<uint2> cta;  // Q == 1: per CTA (16-byte index of its rows' first bits, bytes to stage)
+  const uint2* cta_dev = nullptr;  // the same in device memory (the caller uploads it; null: per-warp staging)
 };
 bool j_supported(const FcDev& L);
 // row_bit: the host copy of L.jrow (nrows + 1), for the per-CTA stream ranges
