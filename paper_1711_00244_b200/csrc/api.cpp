@@ -116,10 +116,9 @@ struct Layer {
   DBuf wd;              // CONV: decoded dense bf16 filters [rows][kpad] (per-call scratch)
   size_t tlist_bytes = 0, wd_bytes = 0;  // sizes of the per-call scratch above (allocated at first use)
   DBuf msv, msg;        // small-batch multi-symbol LUTs
-  DBuf jw, jrow, jlane, jlut, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
+  DBuf jw, jrow, jlane, jlut, jlutr, jpart, jctr;  // merged-stream small-batch kernel (joint.cu)
   std::vector<uint32_t> jrow_h;               // host copy of jrow (per-CTA stream ranges)
   JPlan jplan[3];                             // launch plans of k_fc_j for B = 1, 2, 3-4 (built at first use)
-  DBuf jcta[3];                               // their per-CTA stream ranges (device copies of JPlan::cta)
   DBuf jmlane, jmperm, jmlut;                 // medium-batch split: lane records, per-group row order, tables
   std::vector<std::pair<int, JPlan>> jmplan;  // its launch plans per B (built at first use)
   int kpad = 0, out_h = 0, out_w = 0, conv_h = 0, conv_w = 0;  // CONV geometry (after conv / after pool)
@@ -401,6 +400,9 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       const double toks = (double)ix.tokens / std::max<uint32_t>(1, nr);
       const double want = (double)m.num_sms * 28 * 32 / std::max<uint32_t>(1, nr);
       while (G < 32 && G < want && toks / (2 * G) >= 2.0) G *= 2;
+      // short layers (few rows, e.g. VGG fc8): rows over several warps so the
+      // SMs still hold ~28 warps, while a lane keeps >= 6 tokens
+      while (G >= 32 && G < 128 && 2 * G <= want && toks / (2 * G) >= 6.0) G *= 2;
       if (const char* e = std::getenv("CDN_JG")) G = std::max(1, std::min(32, std::atoi(e)));
     }
     uint64_t tb = 0, rmax = 0;
@@ -426,17 +428,18 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     if (const char* e = std::getenv("CDN_JL")) jl = std::max(8, std::min(16, std::atoi(e)));
     if (const char* e = std::getenv("CDN_JQ")) jq = std::max(1, std::min(G, std::atoi(e)));
     while (G % jq) jq >>= 1;
+    if (jq > 1) G = std::min(G, 32 * jq);  // (column groups: a row's group lanes in one warp)
     JointIndex jx;
     const auto jlut = build_joint_lut(H.val, H.gap, jl);
-    if (build_joint_index(H, L.row0, L.row1, G, jq, jlut, jl, jx)) {
+    if (build_joint_index(H, L.row0, L.row1, G, jq, jlut, jl, jx, /*tail=*/true)) {
       // per-row staging slot: the largest byte span of one (row, column group)
       uint32_t sub = 0;
       const int GQ = G / jq;
       for (uint32_t i = 0; i < nr; ++i)
         for (int q = 0; q < jq; ++q) {
           const uint32_t base = jx.row_bit[i];
-          const uint32_t a = base + (jx.lane[(size_t)i * G + q * GQ] & 0xffffu);
-          const uint32_t b = q + 1 < jq ? base + (jx.lane[(size_t)i * G + (q + 1) * GQ] & 0xffffu) : jx.row_bit[i + 1];
+          const uint32_t a = base + (jx.lane[(size_t)i * (G + 1) + q * GQ] & 0xffffu);
+          const uint32_t b = base + (jx.lane[(size_t)i * (G + 1) + (q + 1) * GQ] & 0xffffu);
           sub = std::max<uint32_t>(sub, (((b + 127) >> 7) - (a >> 7)) * 16u + 16u);
         }
       L.jw.upload(jx.words);
@@ -481,6 +484,19 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
         L.dev.jo_vs = o[4]; L.dev.jo_gs = o[5]; L.dev.jo_cb = o[6];
         L.dev.jblob = (uint32_t)blob.size();
         L.jlut.upload(blob);
+        // the small-batch kernel's copy: the same blob with the joint LUT in
+        // its entry layout (build_joint_lut_r; same offsets)
+        // its entries permuted: index i at i ^ ((i >> 5) & 31), so the bank
+        // bits (the window's last five) mix with the five before them (the
+        // next code's first bits are skewed towards the padding code)
+        const auto lr = build_joint_lut_r(H.val, H.gap, jl);
+        const uint32_t hsh = jl >= 10 ? 31u : 0u;
+        std::vector<uint32_t> lp(lr.size());
+        for (uint32_t i = 0; i < (uint32_t)lr.size(); ++i) lp[i ^ ((i >> 5) & hsh)] = lr[i];
+        uint32_t o2[7];
+        const auto blob2 = make_blob(lp, o2);
+        L.jlutr.upload(blob2);
+        L.dev.jlhash = hsh;
       }
       L.dev.jL = jl;
       L.dev.jsub = sub;
@@ -770,6 +786,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.jw = L.jw.p ? L.jw.as<uint32_t>() : nullptr;
   f.jrow = L.jrow.p ? L.jrow.as<uint32_t>() : nullptr;
   f.jlane = L.jlane.p ? L.jlane.as<uint32_t>() : nullptr;
+  f.jlutr = L.jlutr.p ? L.jlutr.as<uint32_t>() : nullptr;
   f.jlut = L.jlut.p ? L.jlut.as<uint32_t>() : nullptr;
   f.jpart = L.jpart.p ? L.jpart.as<float>() : nullptr;
   f.jctr = L.jctr.p ? L.jctr.as<int>() : nullptr;
@@ -814,7 +831,7 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   s.resident_bytes = 0;
   for (const DBuf* b : {&L.vw, &L.gw, &L.rp, &L.rec, &L.tok, &L.vlut, &L.glut, &L.vtab, &L.gtab, &L.vsorted,
                         &L.gsorted, &L.cb, &L.bias, &L.flut, &L.ivg, &L.ivm, &L.tivg, &L.tivm, &L.tbase, &L.troff,
-                        &L.msv, &L.msg, &L.jw, &L.jrow, &L.jlane, &L.jlut, &L.jmlane, &L.jmperm, &L.jmlut})
+                        &L.msv, &L.msg, &L.jw, &L.jrow, &L.jlane, &L.jlut, &L.jlutr, &L.jmlane, &L.jmperm, &L.jmlut})
     s.resident_bytes += b->n;
   s.ws_bytes = 0;
   s.in_features = L.in_elems();
@@ -1052,13 +1069,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
   if (B <= 4 && small_kernel == 0 && j_supported(L.dev)) {
     const int pi = B <= 1 ? 0 : (B <= 2 ? 1 : 2);
     JPlan& p = L.jplan[pi];  // cached: the plan is host work on every call otherwise
-    if (p.nrb == 0) {
-      p = plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data());
-      if (p.ok && !p.cta.empty()) {
-        L.jcta[pi].upload(p.cta);
-        p.cta_dev = L.jcta[pi].as<uint2>();
-      }
-    }
+    if (p.nrb == 0) p = plan_fc_j(L.dev, B, m.num_sms, L.jrow_h.empty() ? nullptr : L.jrow_h.data());
     if (p.ok) {
       CUDA_OK(launch_fc_j(L.dev, p, x, ldx, B, y, ldy, relu, s));
       return;

@@ -334,8 +334,9 @@ void build_interval_index(const HostLayer& L, uint32_t r0, uint32_t r1, uint32_t
 // ------------------------------------------------- merged token stream
 
 bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, const std::vector<uint32_t>& lut,
-                       int Lb, JointIndex& out) {
+                       int Lb, JointIndex& out, bool tail) {
   const uint32_t nr = r1 - r0;
+  const int GS = G + (tail ? 1 : 0);  // records per row
   if (L.cols > 65535 || G < 1 || Q < 1 || G % Q) return false;
   uint64_t total = 0;
   uint32_t mx = 0;
@@ -355,7 +356,7 @@ bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int 
   out.max_row_bits = mx;
   out.words.assign((size_t)((total + 31) / 32) + 8, 0u);
   out.row_bit.assign((size_t)nr + 1, 0u);
-  out.lane.assign((size_t)nr * G, 0u);
+  out.lane.assign((size_t)nr * GS, 0u);
   uint64_t pos = 0;
   auto put = [&](uint32_t code, uint32_t len) {  // MSB-first, len <= 32
     for (uint32_t b = 0; b < len; ++b) {
@@ -442,10 +443,11 @@ bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int 
         const size_t bb = jj == 0 ? gb : (S ? step_at[(uint64_t)jj * S / (uint64_t)GQ] : ge);
         const uint32_t off = bb < T ? tbit[bb] : (uint32_t)(pos - out.row_bit[li]);
         const int32_t pc = bb < T ? tprev[bb] : prev;
-        out.lane[li * G + q * GQ + jj] = off | ((uint32_t)(pc + 1) << 16);
+        out.lane[li * GS + q * GQ + jj] = off | ((uint32_t)(pc + 1) << 16);
       }
       bprev = ge;
     }
+    if (tail) out.lane[li * GS + G] = (uint32_t)(pos - out.row_bit[li]) | ((uint32_t)(prev + 1) << 16);
   }
   out.row_bit[nr] = (uint32_t)pos;
   if (pos != total) throw Error(CDN_E_MALFORMED, "internal: merged stream length");
@@ -472,6 +474,19 @@ std::vector<uint32_t> build_joint_lut(const HuffCode& val, const HuffCode& gap, 
     }
     if (!any || pos > 31 || adv * 4 >= (1u << 17) || sym > 255) continue;  // slow path
     lut[w] = (sym * 4) | ((adv * 4) << 10) | (pos << 27);
+  }
+  return lut;
+}
+
+std::vector<uint32_t> build_joint_lut_r(const HuffCode& val, const HuffCode& gap, int Lb) {
+  const std::vector<uint32_t> a = build_joint_lut(val, gap, Lb);
+  std::vector<uint32_t> lut(a.size(), 0u);
+  for (size_t w = 0; w < a.size(); ++w) {
+    const uint32_t e = a[w];
+    if (e == 0) continue;
+    const uint32_t sym4 = e & 0x3ffu, adv4 = (e >> 10) & 0x1ffffu, len = e >> 27;
+    if (adv4 >= (1u << 16)) continue;  // (slow path)
+    lut[w] = sym4 | (len << 10) | (adv4 << 16);
   }
   return lut;
 }

@@ -106,14 +106,21 @@ struct JointIndex {
 // false (nothing built) when a row has >= 2^16 bits or cols > 65535
 // lut / Lb: the joint LUT the kernel will use (build_joint_lut): lanes start
 // at the kernel's lookup steps, so they are balanced in steps
+// tail: one more record per row (index G: the row's bit length | (last column + 1) << 16), so
+// lane j's end (bits and last column) is always record j + 1 (the small-batch kernel's layout)
 bool build_joint_index(const HostLayer& L, uint32_t r0, uint32_t r1, int G, int Q, const std::vector<uint32_t>& lut,
-                       int Lb, JointIndex& out);
+                       int Lb, JointIndex& out, bool tail = false);
 // Joint LUT over the next Lb bits of the merged stream: the leading padding
 // tokens (val symbol 0 with its gap code) and then one real token, when they
 // lie inside the window.  Entry: 4 * val symbol (bits 0-9) | 4 * column
 // advance << 10 (17 bits) | total bits << 27 (5 bits); 0 = the first token is
 // longer than the window (the kernel's slow path decodes it code by code).
 std::vector<uint32_t> build_joint_lut(const HuffCode& val, const HuffCode& gap, int Lb);
+// The same lookups in the small-batch kernel's entry layout: 4 * val symbol
+// (bits 0-9) | total bits << 10 (5 bits) | 0 (bit 15) | 4 * column advance << 16
+// (16 bits) -- (entry >> 10) adds the bits to a lane's bit offset and the
+// advance to the x offset above it in one add (joint.cu); 0 = slow path.
+std::vector<uint32_t> build_joint_lut_r(const HuffCode& val, const HuffCode& gap, int Lb);
 
 // Restart index of the large-batch band kernel: every row split into NI
 // intervals of W columns; per (row, interval) the decoder state before the

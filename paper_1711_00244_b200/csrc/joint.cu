@@ -18,12 +18,21 @@
 //   * w = C[sym] from the 32-entry codebook in shared memory (conflict-free:
 //     equal indices broadcast, distinct ones sit in distinct banks; l.8) and
 //     acc += w * x[c] with x staged in shared memory (l.9).
-// Lanes: thread = (row, lane j) of the token-balanced lane split recorded at
-// load (start bit, previous column); no lane ends with padding, so the lookup
-// never decodes past a lane's end.  The G lanes of a row are reduced by a
-// fixed shuffle tree (deterministic).
-// A programmatic dependent launch: the LUT / stream staging runs before
-// griddepcontrol.wait, x (the previous layer's output) after it.
+// Lanes: thread = (row, lane j) of the lane split recorded at load (start bit,
+// previous column; lanes split at the kernel's lookup steps, so every lane runs
+// the same number of lookups +-1).  A lane ends at its last column (record
+// j + 1).  The G lanes of a row are reduced by a fixed shuffle tree, and rows
+// of G > 32 lanes (short layers: VGG fc8) over several warps in warp order
+// (deterministic).
+// A programmatic dependent launch: the table / stream copies are issued at
+// entry, x (the previous layer's output) right after griddepcontrol.wait,
+// before the lane records are consumed.
+// Measured bound (ncu, C5 fc6 at B = 1, profiles/r02_k_fc_j_*): during the
+// decode the shared-memory data path runs at ~90% of its one wavefront per
+// clock -- per lookup ~3.5 wavefronts of joint-LUT gather, ~3.3 of x gather
+// (random columns), ~2 of stream refills, 1 of codebook -- with instruction
+// issue at ~70%; the staging of tables + x (~165 KB per SM from L2) takes
+// ~2.3 us of the ~11.5 us launch.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -39,7 +48,7 @@ namespace {
 using namespace dev;
 
 constexpr int kJMaxWarps = 32;
-constexpr int kJMaxCta = 1024;  // CTAs whose rows are staged as one stream range
+constexpr int kJMaxCta = 148;  // CTAs whose rows are staged as one stream range (one per SM)
 constexpr int kJPieces = 4;    // a CTA's stream bits arrive in this many pieces (warps start on their own)
 
 struct JArgs {
@@ -66,11 +75,17 @@ struct JArgs {
   uint32_t off_x, off_slot;  // dynamic smem offsets (the table blob sits at 0)
   int xbulk;          // 1: x contiguous (ldx == 1, B == 1) and 16-byte aligned
   unsigned long long* trace;  // debug (env CDN_J_TRACE): per CTA 8 globaltimer stamps, else null
-  int ncta;           // Q == 1: CTAs whose stream ranges are in cta[] (the rest stage per warp)
-  const uint2* cta;   // Q == 1: per CTA and piece (16-byte index of the piece's first bits, bytes to
-                      // stage); piece p = the CTA's warps [p nw / P, (p+1) nw / P) (device memory: kernel
-                      // parameters stay under 4 KB)
+  int ncta;           // Q == 1: CTAs whose stream ranges are in cta_a / cta_n (the rest stage per warp)
+  int wpr;            // warps per row (k_fc_j, G > 32: a row's lanes span wpr warps of one CTA; else 1)
+  uint32_t lhash;     // k_fc_j: joint LUT entry of index i at i ^ ((i >> 5) & lhash) (spreads the banks)
+  // Q == 1, per CTA and piece: 16-byte index of the piece's first bits and bytes to stage; piece p =
+  // the CTA's warps [pw(p), pw(p + 1)), pw(p) = (p nw / P) rounded down to whole rows (j_piece_warp)
+  uint32_t cta_a[kJMaxCta * kJPieces];
+  uint16_t cta_n[kJMaxCta * kJPieces];
 };
+static_assert(sizeof(JArgs) <= 4000, "k_fc_j parameters must stay under 4 KB");
+
+__host__ __device__ __forceinline__ int j_piece_warp(int p, int nw, int wpr) { return (p * nw / kJPieces) / wpr * wpr; }
 
 __device__ __forceinline__ void jtrace(const JArgs& A, int ev) {
   if (A.trace != nullptr && (threadIdx.x & 31) == 0 && threadIdx.x < 32) {
@@ -212,81 +227,144 @@ __device__ __forceinline__ void j_lane(const FcDev& L, const JArgs& A, uint32_t 
 template <int BS>
 __host__ __device__ constexpr int j_max_warps() { return BS >= 32 ? 16 : BS >= 16 ? 24 : kJMaxWarps; }
 
+// if (R & 32) { w0 = w1; w1 = word at sp; sp += 4; R -= 32; } -- the refill
+// of the small-batch kernel's lane, whose bit offset is R's low 5 bits
+static __device__ __forceinline__ void refill_r(uint32_t& w0, uint32_t& w1, uint32_t& R, uint32_t& sp) {
+  asm volatile(
+      "{ .reg .pred p; .reg .b32 t; and.b32 t, %2, 32; setp.ne.u32 p, t, 0; @p mov.b32 %0, %1; "
+      "@p ld.shared.u32 %1, [%3]; @p add.u32 %3, %3, 4; @p sub.u32 %2, %2, 32; }"
+      : "+r"(w0), "+r"(w1), "+r"(R), "+r"(sp));
+}
+
+// One lane of the small-batch kernel (Alg. 1 l.4-9 over the lane's tokens) on
+// the entry layout of build_joint_lut_r: one register R = (x offset << 6) |
+// refill flag (bit 5) | bit offset (bits 0-4) -- an entry's (e >> 10) adds the
+// bits consumed to the offset and the column advance (x 4 bytes) to the x
+// offset in a single add, the funnel shift reads the offset from R's low bits,
+// and the lane ends when the x offset reaches its last column (lanes cover
+// whole steps; the column only grows).  BS == 1: R's x offset is the x
+// address itself.  sp: shared address of the word holding bit lb; xa0: shared
+// address of x at the lane's previous column; span = last - previous column.
+template <int BS>
+__device__ __forceinline__ void j_lane_r(const FcDev& L, const JArgs& A, uint32_t sb, uint32_t sp, uint32_t lb,
+                                         uint32_t xa0, uint32_t span, float (&acc)[BS]) {
+  constexpr int LBS = log2_bs<BS>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t* s_vtab = reinterpret_cast<const uint32_t*>(smem + A.o_vtab);
+  const uint32_t* s_gtab = reinterpret_cast<const uint32_t*>(smem + A.o_gtab);
+  const uint16_t* s_vs = reinterpret_cast<const uint16_t*>(smem + A.o_vs);
+  const uint16_t* s_gs = reinterpret_cast<const uint16_t*>(smem + A.o_gs);
+  const uint32_t lut = sb;
+  const uint32_t cbase = sb + A.o_cb;
+  const int jsh = 32 - A.jL;
+  const int vsh = 32 - L.Lv, gsh = 32 - L.Lg;
+#pragma unroll
+  for (int b = 0; b < BS; ++b) acc[b] = 0.f;
+  const uint32_t x0 = BS == 1 ? xa0 : 0u;
+  uint32_t R = (x0 << 6) | (lb & 31);
+  const uint32_t Rend = (x0 + span * 4u) << 6;
+  uint32_t w0 = 0, w1 = 0;
+  if (R < Rend) {  // (lanes with tokens only: the others never load)
+    w0 = lds32(sp);
+    w1 = lds32(sp + 4);
+  }
+  sp += 8;
+  while (R < Rend) {  // one lookup per (padding run +) real token
+    const uint32_t win = __funnelshift_l(w1, w0, R);
+    const uint32_t li = win >> jsh;
+    uint32_t e = lds32(lut + ((li ^ ((li >> 5) & A.lhash)) << 2));  // (bank bits hashed, j_lut_pos)
+    if (e == 0) {
+      // slow path, this lane alone: one token whose codes did not fit the
+      // window, code by code (plain LUTs, canonical tables for longer codes)
+      const uint32_t ev = lds32(sb + A.o_vlut + ((win >> vsh) << 2));
+      uint32_t vl, vsym;
+      if (ev) { vl = ev >> 16; vsym = ev & 0xffffu; }
+      else { const uint32_t r = slow_sym(win, L.Lv + 1, s_vtab, s_vs, L.vmax); vl = r >> 16; vsym = r & 0xffffu; }
+      R += vl;
+      refill_r(w0, w1, R, sp);
+      const uint32_t win2 = __funnelshift_l(w1, w0, R);
+      const uint32_t eg = lds32(sb + A.o_glut + ((win2 >> gsh) << 2));
+      uint32_t gl, gsym;
+      if (eg) { gl = eg >> 16; gsym = eg & 0xffffu; }
+      else { const uint32_t r = slow_sym(win2, L.Lg + 1, s_gtab, s_gs, L.gmax); gl = r >> 16; gsym = r & 0xffffu; }
+      R += gl;
+      refill_r(w0, w1, R, sp);
+      // an entry as the LUT would have built it, both codes already consumed
+      e = (vsym * 4u) | (((gsym + 1) * 4u) << 16);
+    }
+    R += e >> 10;  // bits consumed (offset) and column advance (x offset), one add
+    const uint32_t ca = e & 0x3fcu;
+    const float w = ldsf(cbase + ca);
+    const uint32_t xa = BS == 1 ? (R >> 6) : xa0 + ((R >> 6) << LBS);
+    if (ca) gather_fma<BS>(acc, w, xa, 0u);
+    refill_r(w0, w1, R, sp);
+  }
+}
+
 template <int BS>
 __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, const __grid_constant__ JArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_w, bar_x;
   __shared__ __align__(8) uint64_t bar_s[kJMaxWarps];
-  constexpr int LBS = log2_bs<BS>();
+  __shared__ float s_red[kJMaxWarps][BS];  // rows spanning several warps: each warp's sum
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   jtrace(A, 0);
   asm volatile("griddepcontrol.launch_dependents;");
 
-  const int G = A.G, GQ = A.GQ, q = blockIdx.y;
-  const int rr = lane / GQ, jj = lane - rr * GQ, j = q * GQ + jj;  // row of the warp unit, lane of the row
+  const int G = A.G, GQ = A.GQ, q = blockIdx.y, WPR = A.wpr;
   const int xc0 = q * A.Kq, xcols = max(0, min(A.Kq, L.cols - xc0));  // this column group's slice of x
-  const int u = blockIdx.x * A.nw + warp;  // warp unit: rows u RPW .. u RPW + RPW - 1
-  const int row = u * A.RPW + rr;
+  const int u = blockIdx.x * A.nw + warp;  // warp unit: RPW rows, or 1 / WPR of a row
+  int row, j, jj;                          // row, lane of the row (of G), lane of the row in this group (of GQ)
+  if (WPR > 1) {
+    row = u / WPR;
+    jj = (u - row * WPR) * 32 + lane;
+    j = jj;
+  } else {
+    const int rr = lane / GQ;
+    jj = lane - rr * GQ;
+    row = u * A.RPW + rr;
+    j = q * GQ + jj;
+  }
   const bool ok = u < A.units && row < L.nrows;
-  // lane records first: their loads fly while the bulk copies are set up
-  uint32_t r0 = 0, r1 = 0, rec = 0, nxt = 0;
+  // lane records (G + 1 per row: lane j's end is record j + 1) and the row's
+  // first bit: the loads fly while the copies are issued and x is requested
+  uint32_t r0 = 0, rec = 0, nxt = 0;
   if (ok) {
     r0 = L.jrow[row];
-    r1 = L.jrow[row + 1];
-    rec = A.lanes[(size_t)row * G + j];
-    if (j + 1 < G) nxt = A.lanes[(size_t)row * G + j + 1];
+    rec = A.lanes[(size_t)row * (G + 1) + j];
+    nxt = A.lanes[(size_t)row * (G + 1) + j + 1];
   }
-  const bool whole = A.Q == 1 && (int)blockIdx.x < A.ncta;  // one stream copy for the whole CTA
+  const bool whole = A.Q == 1 && (int)blockIdx.x < A.ncta;  // the CTA's rows in kJPieces copies
   if (tid == 0) {
     mbar_init(&bar_w, 1);
     mbar_init(&bar_x, 1);
     for (int w = 0; w < A.nw; ++w) mbar_init(&bar_s[w], 1);
     mbar_fence_init();
-    if (whole) {  // the CTA's rows are contiguous: their bits in kJPieces bulk copies
-      const uint32_t base = A.cta[blockIdx.x * kJPieces].x;
+    if (whole) {
+      const uint32_t base = A.cta_a[blockIdx.x * kJPieces];
       for (int pc = 0; pc < kJPieces; ++pc) {
-        const uint2 c = A.cta[blockIdx.x * kJPieces + pc];
-        mbar_arrive_expect_tx(&bar_s[pc], c.y);
-        if (c.y)
-          bulk_g2s(smem + A.off_slot + (c.x - base) * 16u, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)c.x * 16u,
-                   c.y, &bar_s[pc]);
+        const uint32_t a = A.cta_a[blockIdx.x * kJPieces + pc], n = A.cta_n[blockIdx.x * kJPieces + pc];
+        mbar_arrive_expect_tx(&bar_s[pc], n);
+        if (n)
+          bulk_g2s(smem + A.off_slot + (a - base) * 16u, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)a * 16u, n,
+                   &bar_s[pc]);
       }
     }
+  }
+  if (tid == 0) {
     // every table in one bulk copy (host-built blob in this layout)
     mbar_arrive_expect_tx(&bar_w, A.blob_bytes);
     bulk_g2s(smem, A.blob, A.blob_bytes, &bar_w);
   }
-
-  const uint32_t lb = ok ? r0 + (rec & 0xffffu) : 0u;                         // lane's bits [lb, le)
-  const uint32_t le = ok ? r0 + (j + 1 < G ? (nxt & 0xffffu) : r1 - r0) : 0u;
-  const int prev = (int)(rec >> 16) - 1;                                      // lane's previous column
-  uint32_t rs, slot_off;  // staged bits start (128-bit aligned) and its shared-memory offset
-  if (whole) {
-    rs = A.cta[blockIdx.x * kJPieces].x * 128u;
-    slot_off = A.off_slot;
-  } else {
-    // per warp: each row's range of this column group [first lane's start, last lane's end)
-    const uint32_t g0 = __shfl_sync(0xffffffffu, lb, rr * GQ);
-    const uint32_t g1 = __shfl_sync(0xffffffffu, le, rr * GQ + GQ - 1);
-    rs = (g0 >> 7) << 7;
-    slot_off = A.off_slot + ((uint32_t)warp * A.RPW + rr) * A.sub;
-    const uint32_t bytes = ok ? (((g1 + 127) >> 7) - (g0 >> 7)) * 16u + 16u : 0u;
-    uint32_t tot = jj == 0 ? bytes : 0u;
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    __syncthreads();  // the barriers are initialised
-    if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], tot);
-    __syncwarp();
-    if (jj == 0 && bytes)
-      bulk_g2s(smem + slot_off, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)(g0 >> 7) * 16u, bytes,
-               &bar_s[warp]);
-  }
   jtrace(A, 1);
 
-  // ---- activations (after the producer of x finished)
+  // ---- activations (after the producer of x finished), requested before the
+  // lane records are needed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   jtrace(A, 2);
   float* xs = reinterpret_cast<float*>(smem + A.off_x);
   const int K = xcols;
+  constexpr int LBS = log2_bs<BS>();
   if (A.xbulk) {  // x contiguous: ldx == BS == B (the slice is one range)
     const int nb = (K * 4 * BS) & ~15;
     if (tid == 0) {
@@ -311,6 +389,31 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
         if (i0 + k * step < n) xs[i0 + k * step] = v[k];
     }
   }
+
+  const uint32_t lb = ok ? r0 + (rec & 0xffffu) : 0u;  // lane's bits from lb
+  const int prev = (int)(rec >> 16) - 1;                // lane's previous column
+  const int last = ok ? (int)(nxt >> 16) - 1 : prev;    // its last token's column
+  uint32_t rs, slot_off;  // staged bits start (128-bit aligned) and its shared-memory offset
+  if (whole) {
+    rs = A.cta_a[blockIdx.x * kJPieces] * 128u;
+    slot_off = A.off_slot;
+  } else {
+    // per warp (WPR == 1): each row's range of this column group [first lane's start, last lane's end)
+    const uint32_t le = ok ? r0 + (nxt & 0xffffu) : 0u;
+    const uint32_t g0 = __shfl_sync(0xffffffffu, lb, (lane / GQ) * GQ);
+    const uint32_t g1 = __shfl_sync(0xffffffffu, le, (lane / GQ) * GQ + GQ - 1);
+    rs = (g0 >> 7) << 7;
+    slot_off = A.off_slot + ((uint32_t)warp * A.RPW + (uint32_t)(lane / GQ)) * A.sub;
+    const uint32_t bytes = ok ? (((g1 + 127) >> 7) - (g0 >> 7)) * 16u + 16u : 0u;
+    uint32_t tot = jj == 0 ? bytes : 0u;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    __syncthreads();  // the barriers are initialised
+    if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], tot);
+    __syncwarp();
+    if (jj == 0 && bytes)
+      bulk_g2s(smem + slot_off, reinterpret_cast<const uint8_t*>(L.jw) + (size_t)(g0 >> 7) * 16u, bytes,
+               &bar_s[warp]);
+  }
   __syncthreads();
   mbar_wait(&bar_w, 0);
   mbar_wait(&bar_x, 0);
@@ -318,17 +421,48 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
 
   const uint32_t sb = saddr(smem);
   const uint32_t xbase = sb + A.off_x;
+  float acc[BS];
+#pragma unroll
+  for (int b = 0; b < BS; ++b) acc[b] = 0.f;
   if (u < A.units) {
-    // piece pc holds warps [pc nw / P, (pc + 1) nw / P): warp w's is the last pc whose start is <= w
-    mbar_wait(&bar_s[whole ? ((warp + 1) * kJPieces - 1) / A.nw : warp], 0);
+    // the piece holding this warp's rows: the last whose first warp is <= warp
+    int pc = 0;
+    if (whole) {
+      for (int k = 1; k < kJPieces; ++k)
+        if (j_piece_warp(k, A.nw, WPR) <= warp) pc = k;
+    }
+    mbar_wait(&bar_s[whole ? pc : warp], 0);
     jtrace(A, 4);
-    float acc[BS];
-    j_lane<BS>(L, A, sb, sb + slot_off + ((lb - rs) >> 5) * 4u, lb, le, xbase + (uint32_t)((prev - xc0) * 4 * BS), 0u,
-               acc);
+    if (ok)
+      j_lane_r<BS>(L, A, sb, sb + slot_off + ((lb - rs) >> 5) * 4u, lb,
+                   xbase + (uint32_t)((prev - xc0) * 4 * BS), (uint32_t)(last - prev), acc);
     // lanes of a row: fixed shuffle tree (deterministic)
+    const int width = WPR > 1 ? 32 : GQ;
 #pragma unroll
     for (int b = 0; b < BS; ++b)
-      for (int o = GQ >> 1; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o, GQ);
+      for (int o = width >> 1; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o, width);
+  }
+  if (WPR > 1) {
+    // a row's warps: their sums in warp order (deterministic)
+    if (lane == 0) {
+#pragma unroll
+      for (int b = 0; b < BS; ++b) s_red[warp][b] = acc[b];
+    }
+    __syncthreads();
+    if (lane == 0 && ok && (u % WPR) == 0) {
+      const float v = L.bias[row];
+#pragma unroll
+      for (int b = 0; b < BS; ++b) {
+        float t = 0.f;
+        for (int k = 0; k < WPR; ++k) t += s_red[warp + k][b];
+        if (b < A.B) {
+          float o = t + v;
+          if (A.relu) o = fmaxf(o, 0.f);
+          A.y[(size_t)row * A.ldy + b] = o;
+        }
+      }
+    }
+  } else if (u < A.units) {
     if (A.Q == 1) {
       if (jj == 0 && row < L.nrows) {
         const float v = L.bias[row];
@@ -350,10 +484,10 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
       }
       __threadfence();
       __syncwarp();
-      int last = 0;
-      if (lane == 0) last = atomicAdd(&A.ctr[u], 1) == A.Q - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
+      int lst = 0;
+      if (lane == 0) lst = atomicAdd(&A.ctr[u], 1) == A.Q - 1;
+      lst = __shfl_sync(0xffffffffu, lst, 0);
+      if (lst) {
         __threadfence();
         if (jj == 0 && row < L.nrows) {
           const float v = L.bias[row];
@@ -371,8 +505,8 @@ __global__ void __launch_bounds__(j_max_warps<BS>() * 32, 1) k_fc_j(FcDev L, con
         if (lane == 0) A.ctr[u] = 0;
       }
     }
-    jtrace(A, 5);
   }
+  jtrace(A, 5);
   __syncthreads();
   jtrace(A, 6);
 }
@@ -553,7 +687,7 @@ __global__ void __launch_bounds__(256) k_j_reduce(const float* __restrict__ part
 
 }  // namespace
 
-bool j_supported(const FcDev& L) { return L.jw && L.jlut && L.ncb <= 32 && L.jG <= 32 && L.jG >= 1; }
+bool j_supported(const FcDev& L) { return L.jw && L.jlutr && L.ncb <= 32 && L.jG <= 128 && L.jG >= 1; }
 
 JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
   JPlan p;
@@ -561,45 +695,62 @@ JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
   p.BS = B <= 1 ? 1 : (B <= 2 ? 2 : 4);
   p.Q = L.jQ;
   p.GQ = L.jG / p.Q;
-  p.RPW = 32 / p.GQ;
-  p.units = (L.nrows + p.RPW - 1) / p.RPW;
+  if (p.GQ > 32) {  // a row's lanes span wpr warps (one column group only)
+    if (p.Q != 1 || p.GQ % 32) return p;
+    p.wpr = p.GQ / 32;
+    p.RPW = 1;
+    p.units = L.nrows * p.wpr;
+  } else {
+    p.wpr = 1;
+    p.RPW = 32 / p.GQ;
+    p.units = (L.nrows + p.RPW - 1) / p.RPW;
+  }
   // one CTA per SM (Q column groups of a row block side by side), every
-  // warp one unit of RPW rows
+  // warp one unit of RPW rows (or 1 / wpr of a row); a CTA holds whole rows
   const int rb = std::max(1, num_sms / p.Q);
   auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
   const size_t off_x = al(L.jblob);
   const size_t off_slot = al(off_x + (size_t)4 * p.BS * L.jKq);
-  for (p.nw = std::min(kJMaxWarps, std::max(1, (p.units + rb - 1) / rb)); p.nw >= 1; --p.nw) {
+  int nw0 = std::min(kJMaxWarps, std::max(1, (p.units + rb - 1) / rb));
+  nw0 = std::max(p.wpr, nw0 / p.wpr * p.wpr);
+  for (p.nw = nw0; p.nw >= p.wpr; p.nw -= p.wpr) {
     p.nrb = (p.units + p.nw - 1) / p.nw;
     p.cta.clear();
     size_t slot = (size_t)p.nw * p.RPW * L.jsub;  // per-warp row slots
-    if (p.Q == 1 && row_bit && p.nrb <= kJMaxCta && p.nw >= kJPieces) {
+    const bool whole = p.Q == 1 && row_bit && p.nrb <= kJMaxCta && p.nw >= kJPieces;
+    if (whole) {
       // the CTA's rows are contiguous: one range of the merged stream, staged
-      // in kJPieces copies of whole warp units (pieces overlap by at most the
-      // 16-byte block of a shared boundary, copied twice)
+      // in kJPieces copies of whole rows (pieces overlap by at most the
+      // 16-byte blocks of a shared boundary, copied twice)
       size_t mx = 0;
+      const int rows_cta = p.nw * p.RPW / p.wpr;
       for (int c = 0; c < p.nrb; ++c) {
-        const int cr0 = c * p.nw * p.RPW;
+        const int cr0 = c * rows_cta;
         uint32_t first = 0;
         for (int pc = 0; pc < kJPieces; ++pc) {
-          const int w0 = pc * p.nw / kJPieces, w1 = (pc + 1) * p.nw / kJPieces;
-          const int r0 = std::min(L.nrows, cr0 + w0 * p.RPW), r1 = std::min(L.nrows, cr0 + w1 * p.RPW);
-          const uint32_t a = row_bit[r0] >> 7, b = (row_bit[r1] + 127) >> 7;
-          const uint32_t bytes = r1 > r0 ? (b - a) * 16u + 16u : 0u;  // + one word of read-ahead
+          const int w0 = j_piece_warp(pc, p.nw, p.wpr), w1 = pc + 1 < kJPieces ? j_piece_warp(pc + 1, p.nw, p.wpr) : p.nw;
+          const int r0 = std::min(L.nrows, cr0 + w0 * p.RPW / p.wpr), r1 = std::min(L.nrows, cr0 + w1 * p.RPW / p.wpr);
+          const uint32_t a = row_bit[r0] >> 7, e = (row_bit[r1] + 127) >> 7;
+          const uint32_t bytes = r1 > r0 ? (e - a) * 16u + 16u : 0u;  // + 16 bytes of read-ahead
           if (pc == 0) first = a;
           p.cta.push_back(make_uint2(a, bytes));
           mx = std::max<size_t>(mx, (size_t)(a - first) * 16u + bytes);
         }
       }
       slot = mx;
+    } else if (p.wpr > 1) {
+      continue;  // (per-warp staging serves whole-row warp units only)
     }
     p.off_x = (uint32_t)off_x;
     p.off_slot = (uint32_t)off_slot;
     p.sub = L.jsub;
     p.smem = off_slot + slot;
-    if (p.smem <= 227 * 1024 - 1024) break;
+    if (p.smem <= 227 * 1024 - 1024 && (!whole || std::all_of(p.cta.begin(), p.cta.end(), [](const uint2& c) {
+          return c.y < 65536u;
+        })))
+      break;
   }
-  p.ok = p.nw >= 1 && p.smem <= 227 * 1024 - 1024 && (p.Q == 1 || (L.jpart && L.jctr));
+  p.ok = p.nw >= p.wpr && p.smem <= 227 * 1024 - 1024 && (p.Q == 1 || (L.jpart && L.jctr));
   return p;
 }
 
@@ -701,7 +852,7 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
     a.sep = 0;
     a.perm = nullptr;
     a.lanecopy = 0;
-    a.blob = L.jlut;
+    a.blob = L.jlutr;
     a.blob_bytes = L.jblob;
     a.jL = L.jL;
     a.o_vlut = L.jo_vlut; a.o_glut = L.jo_glut; a.o_vtab = L.jo_vtab; a.o_gtab = L.jo_gtab;
@@ -710,8 +861,13 @@ cudaError_t launch_fc_j(const FcDev& L, const JPlan& p, const float* x, int ldx,
   a.sub = p.sub;
   a.off_x = p.off_x;
   a.off_slot = p.off_slot;
-  a.ncta = p.cta_dev ? (int)(p.cta.size() / kJPieces) : 0;
-  a.cta = p.cta_dev;
+  a.ncta = (int)std::min<size_t>(p.cta.size() / kJPieces, kJMaxCta);
+  for (int i = 0; i < a.ncta * kJPieces; ++i) {
+    a.cta_a[i] = p.cta[i].x;
+    a.cta_n[i] = (uint16_t)p.cta[i].y;
+  }
+  a.wpr = p.wpr;
+  a.lhash = p.medium ? 0u : L.jlhash;
   static unsigned long long* trace = nullptr;
   static const char* trace_path = getenv("CDN_J_TRACE");
   const size_t ntr = (size_t)p.nrb * p.Q * p.nbg * 8;

@@ -90,6 +90,8 @@ struct FcDev {
   const uint32_t* jw = nullptr;
   const uint32_t* jrow = nullptr;
   const uint32_t* jlane = nullptr;
+  const uint32_t* jlutr = nullptr;  // the same blob with the joint LUT in k_fc_j's entry layout (build_joint_lut_r),
+  uint32_t jlhash = 0;               // entry of index i at i ^ ((i >> 5) & jlhash)
   const uint32_t* jlut = nullptr;   // the kernel's tables as one blob, laid out as in shared memory:
   int jL = 12;                       // [joint LUT 4<<jL | vlut | glut | vtab | gtab | vsorted | gsorted | codebook]
   uint32_t jo_vlut = 0, jo_glut = 0, jo_vtab = 0, jo_gtab = 0, jo_vs = 0, jo_gs = 0, jo_cb = 0, jblob = 0;
@@ -123,7 +125,7 @@ struct JPlan {
   uint32_t sub = 0, off_x = 0, off_slot = 0;
   size_t smem = 0;
   std::vector<uint2> cta;  // Q == 1: per CTA (16-byte index of its rows' first bits, bytes to stage)
-  const uint2* cta_dev = nullptr;  // the same in device memory (the caller uploads it; null: per-warp staging)
+  int wpr = 1;             // k_fc_j: warps per row (G > 32)
 };
 bool j_supported(const FcDev& L);
 // row_bit: the host copy of L.jrow (nrows + 1), for the per-CTA stream ranges

@@ -26,7 +26,10 @@ def main():
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6542.4
     out = {}
-    for cfg, li in [("C5", 0), ("C5", 1), ("C5", 2), ("C2", 0), ("C1", 0)]:
+    todo = [("C5", 0), ("C5", 1), ("C5", 2), ("C2", 0), ("C1", 0)]
+    if os.environ.get("B1_LAYERS"):  # e.g. "C5:0,C2:0"
+        todo = [(c.split(":")[0], int(c.split(":")[1])) for c in os.environ["B1_LAYERS"].split(",")]
+    for cfg, li in todo:
         spec = synth.CONFIGS[cfg].fc[li]
         W, v = synth.fc_weights(spec, synth.CONFIGS[cfg].seed)
         buf = cdn.compress_dense(W, spec.density, spec.r, spec.k, v)
