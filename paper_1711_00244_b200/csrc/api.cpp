@@ -127,6 +127,16 @@ struct Layer {
   // multiple of 64), the GEMM's A tiles loaded by TMA in im2col mode
   bool implicit = false;
   int cg = 0, cgp = 0;
+  // space-to-depth (a strided CONV with no padding, s * s * C <= 64 channels:
+  // AlexNet conv1): the input regrouped into s x s super-pixels of s*s*C
+  // channels, the kernel into a ceil(kh / s)-square one over them (filter taps
+  // past kh are zero), run on the implicit-GEMM path; s2d_kmap sends each
+  // decoded K index (r, s, c) to its place in that layout
+  int s2d = 0, s2d_h = 0, s2d_w = 0, s2d_k = 0;  // stride (0: off), super-pixel grid, super-kernel size
+  DBuf s2d_kmap;
+  uint64_t act_bytes(int B) const {  // the implicit GEMM's bf16 input copy
+    return s2d ? 2ull * B * s2d_h * s2d_w * cgp : 2ull * B * desc.in_h * desc.in_w * (uint64_t)desc.groups * cgp;
+  }
   bool blocked = false;  // block-contiguous container (Alg. 2, C-34): tensor-core path only
   // column-sharded FC layer (CDN_SHARD_COLS, world > 1): this rank multiplies
   // K tiles [kt0, kt1) = input columns [kc0, kc1) for every output row
@@ -845,11 +855,32 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       return !(e && e[0] == '0');
     }();
     const int cg = d.in_c / d.groups;
+    const char* s2d_env = std::getenv("CDN_CONV_S2D");  // (read per load: tests run both conv1 paths)
+    const bool s2d_on = !(s2d_env && s2d_env[0] == '0');
+    const int st = d.stride;
     if (implicit_on && d.stride == 1 && d.kh == d.kw && cg % 8 == 0 && d.pad <= 64 && d.kh - 1 - d.pad >= -64) {
       L.implicit = true;
       L.cg = cg;
       L.cgp = (cg + 63) / 64 * 64;
       L.kpad = d.kh * d.kw * L.cgp;  // K order (r, s, c padded): K tile = (tap, 64-channel chunk)
+    } else if (implicit_on && s2d_on && st > 1 && d.groups == 1 && d.pad == 0 && d.kh == d.kw &&
+               st * st * d.in_c <= 64 && (st == 2 || st == 4) && (d.in_c == 3 || d.in_c == 4) &&
+               (d.in_h + st - 1) / st - (d.kh + st - 1) / st + 1 == L.conv_h &&
+               (d.in_w + st - 1) / st - (d.kw + st - 1) / st + 1 == L.conv_w) {
+      L.implicit = true;
+      L.s2d = st;
+      L.s2d_h = (d.in_h + st - 1) / st;
+      L.s2d_w = (d.in_w + st - 1) / st;
+      L.s2d_k = (d.kh + st - 1) / st;
+      L.cg = st * st * d.in_c;
+      L.cgp = 64;
+      L.kpad = L.s2d_k * L.s2d_k * L.cgp;  // K order (R, S, (dy, dx, c) padded)
+      std::vector<int> km(H.cols);
+      for (uint32_t k = 0; k < H.cols; ++k) {  // decoded K index (r, s, c) (C-18)
+        const int c = (int)(k % d.in_c), rs = (int)(k / d.in_c), sx = rs % d.kw, r = rs / d.kw;
+        km[k] = ((r / st) * L.s2d_k + sx / st) * L.cgp + ((r % st) * st + sx % st) * d.in_c + c;
+      }
+      L.s2d_kmap.upload(km);
     }
     L.wd_bytes = (size_t)H.rows * L.kpad * 2;  // per-call scratch, allocated at first use (ensure_wd)
     s.ws_bytes = (uint64_t)H.rows * L.kpad * 2;  // decoded bf16 filters (per-call scratch, C-24)
@@ -1121,7 +1152,8 @@ void predecode_launch(Model& m, Layer& L, cudaStream_t s) {
     ensure_wd(L);
     CUDA_OK(cudaMemsetAsync(L.wd.p, 0, L.wd.n, s));
     CUDA_OK(launch_decode_dense(L.dev, static_cast<__nv_bfloat16*>(L.wd.p), L.kpad, s, m.num_sms,
-                                L.implicit ? L.cg : 0, L.implicit ? L.cgp : 0));
+                                L.implicit ? L.cg : 0, L.implicit ? L.cgp : 0,
+                                L.s2d ? L.s2d_kmap.as<int>() : nullptr));
   } else {
     ensure_list(L);
     CUDA_OK(launch_tc_list(L.dev, s, L.col ? L.kt0 : 0, L.col ? L.kt1 : -1));
@@ -1139,14 +1171,15 @@ void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
     CUDA_OK(cudaStreamCreateWithPriority(&m.side, cudaStreamNonBlocking, least));
   }
   if (!m.ev_call) CUDA_OK(cudaEventCreateWithFlags(&m.ev_call, cudaEventDisableTiming));
+  cudaStream_t ds = m.side;
   CUDA_OK(cudaEventRecord(m.ev_call, s));
-  CUDA_OK(cudaStreamWaitEvent(m.side, m.ev_call, 0));
+  CUDA_OK(cudaStreamWaitEvent(ds, m.ev_call, 0));
   for (size_t i = 0; i < m.layers.size(); ++i) {
     Layer& L = *m.layers[i];
     if (L.list_state != 0 || !predecodes(m, L, bs[i])) continue;
     if (!L.list_ev) CUDA_OK(cudaEventCreateWithFlags(&L.list_ev, cudaEventDisableTiming));
-    predecode_launch(m, L, m.side);
-    CUDA_OK(cudaEventRecord(L.list_ev, m.side));
+    predecode_launch(m, L, ds);
+    CUDA_OK(cudaEventRecord(L.list_ev, ds));
     L.list_state = 1;
   }
 }
@@ -1180,12 +1213,18 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
     // implicit GEMM: the input once as bf16 NHWC (groups padded to cgp
     // channels); the GEMM's TMA gathers every (pixel, tap) tile in im2col mode
     // -- no patch matrix (conv2's would be 227 MB at B = 64)
-    const long npix = (long)B * d.in_h * d.in_w;
-    m.conv_a.alloc((size_t)npix * G * L.cgp * 2);
+    m.conv_a.alloc(L.act_bytes(B));
     __nv_bfloat16* act = static_cast<__nv_bfloat16*>(m.conv_a.p);
-    CUDA_OK(launch_to_bf16_pad(x, npix, d.in_c, G, cg, L.cgp, act, s));
-    CUDA_OK(launch_gemm_implicit(act, B, d.in_h, d.in_w, G, L.cgp, d.kh, d.kw, d.pad, Ho, Wo, wd, mg,
-                                 L.bias.as<float>(), d.relu, cout, M, s, fuse_lrn ? 1 : 0));
+    if (L.s2d) {
+      CUDA_OK(launch_s2d_bf16(x, B, d.in_h, d.in_w, d.in_c, L.s2d, L.s2d_h, L.s2d_w, L.cgp, act, s));
+      CUDA_OK(launch_gemm_implicit(act, B, L.s2d_h, L.s2d_w, 1, L.cgp, L.s2d_k, L.s2d_k, 0, Ho, Wo, wd, mg,
+                                   L.bias.as<float>(), d.relu, cout, M, s, fuse_lrn ? 1 : 0));
+    } else {
+      const long npix = (long)B * d.in_h * d.in_w;
+      CUDA_OK(launch_to_bf16_pad(x, npix, d.in_c, G, cg, L.cgp, act, s));
+      CUDA_OK(launch_gemm_implicit(act, B, d.in_h, d.in_w, G, L.cgp, d.kh, d.kw, d.pad, Ho, Wo, wd, mg,
+                                   L.bias.as<float>(), d.relu, cout, M, s, fuse_lrn ? 1 : 0));
+    }
   } else {
     // every group's patches, then one GEMM launch over all groups (grid.z), so
     // a grouped layer fills the GPU instead of running its groups back to back
@@ -1507,8 +1546,7 @@ uint64_t exec_scratch_bytes(const Model& m, const std::vector<int>& bs, bool hos
       if (i > 0) total += 4ull * L.in_elems() * B;
       const cdn_layer_desc& d = L.desc;
       const uint64_t npos = (uint64_t)B * L.conv_h * L.conv_w;
-      ca = std::max<uint64_t>(ca, L.implicit ? 2ull * B * d.in_h * d.in_w * (uint64_t)d.groups * L.cgp
-                                             : npos * L.kpad * 2ull * d.groups);
+      ca = std::max<uint64_t>(ca, L.implicit ? L.act_bytes(B) : npos * L.kpad * 2ull * d.groups);
       if (d.lrn || d.pool_k > 0) co = std::max<uint64_t>(co, npos * L.rows * 4ull);
       if (d.lrn && d.pool_k > 0) ct = std::max<uint64_t>(ct, npos * L.rows * 4ull);
       total += L.wd_bytes;
@@ -1669,8 +1707,7 @@ std::vector<uint64_t> out_bytes(const Model& m, int Bmax) {
     // the batch-independent scratch (ws_bytes).
     if (L->is_conv()) {
       // implicit GEMM: the bf16 copy of the input (padded channels), not patches
-      const uint64_t a = L->implicit ? 2ull * L->desc.in_h * L->desc.in_w * (uint64_t)L->desc.groups * L->cgp
-                                     : 2ull * L->conv_h * L->conv_w * L->kpad * (uint64_t)L->desc.groups;
+      const uint64_t a = L->implicit ? L->act_bytes(1) : 2ull * L->conv_h * L->conv_w * L->kpad * (uint64_t)L->desc.groups;
       b += a + (uint64_t)L->conv_h * L->conv_w * (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows;
     } else if (tc_supported(L->dev) || L->dev.ivg) {
       uint64_t part = 0;
@@ -1726,16 +1763,27 @@ PlanResult plan_for(Model& m, int K, bool host_input = false) {
   // per-layer bound by one phase slot per deeper level: a plan whose executor
   // scratch (exec_scratch_bytes) exceeds TOT is re-planned under TOT less the
   // excess until it fits (reading C-36).
-  uint64_t budget = m.tot;
+  uint64_t budget = m.tot, step = 0;
   PlanResult pr;
-  for (int it = 0; it < 16; ++it) {
+  std::vector<int> prev;
+  for (int it = 0; it < 32; ++it) {
     pr = plan_dp(t.data(), inb.data(), outb.data(), ws.data(), f, K, budget, m.latency, 64 * 1024);
     if (!pr.feasible) return pr;
     const uint64_t need = exec_scratch_bytes(m, pr.batches, host_input);
+    if (std::getenv("CDN_PLAN_DEBUG")) {
+      fprintf(stderr, "[cdn] plan it %d budget %llu need %llu:", it, (unsigned long long)budget, (unsigned long long)need);
+      for (int b : pr.batches) fprintf(stderr, " %d", b);
+      fprintf(stderr, "\n");
+    }
     if (need <= m.tot) return pr;
+    // the excess comes back while the DP keeps the same plan (its model and
+    // the executor differ by a plan-dependent amount): cut the budget by the
+    // excess, doubling the cut each time the same plan returns
     const uint64_t over = need - m.tot;
-    if (budget <= over) break;
-    budget -= std::max<uint64_t>(over, 64 * 1024);
+    step = pr.batches == prev ? 2 * step : std::max<uint64_t>(over, 64 * 1024);
+    prev = pr.batches;
+    if (budget <= step) break;
+    budget -= step;
   }
   pr.feasible = false;
   return pr;
@@ -2219,7 +2267,9 @@ const char* cdn_layer_kernel_name(const cdn_model* h, int layer, int B) {
   if (!h || layer < 0 || layer >= (int)h->m.layers.size() || B < 1) return "";
   const Model& m = h->m;
   const Layer& L = *m.layers[layer];
-  if (L.is_conv()) return L.implicit ? "k_gemm_bf16 (conv, implicit im2col)" : "k_gemm_bf16 (conv)";
+  if (L.is_conv())
+    return L.s2d ? "k_gemm_bf16 (conv, space-to-depth, implicit im2col)"
+                 : L.implicit ? "k_gemm_bf16 (conv, implicit im2col)" : "k_gemm_bf16 (conv)";
   if (L.blocked || L.col) return "k_fc_tc";
   int tcmin = m.tc_min > 0 ? m.tc_min : tc_min_batch();
   if (m.tc_min == 0 && m.band_min == 0 && B >= band_min_batch() && tc_supported(L.dev)) {

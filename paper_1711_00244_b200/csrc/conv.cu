@@ -546,6 +546,65 @@ cudaError_t launch_to_bf16_pad(const float* x, long npix, int C, int G, int cg, 
   return e_;
 }
 
+// Space-to-depth of a strided CONV's input (conv1: 227 x 227 x 3, stride 4 ->
+// 57 x 57 x 48 padded to 64 channels): the layer becomes a stride-1 CONV with
+// a ceil(kh / s)-square kernel, whose filters are decoded into the matching K
+// order (api.cpp s2d_kmap) -- the same products, so the implicit GEMM's TMA
+// im2col path (>= 64-channel runs) serves it with no patch matrix.  A thread
+// per super-pixel: its s input row runs of s*C floats (adjacent threads read
+// adjacent runs) and one 2*cgp-byte row of 16-byte stores.
+template <int ST, int C>
+__global__ void __launch_bounds__(256) k_s2d_bf16(const float* __restrict__ x, int B, int H, int W, int Hs, int Ws,
+                                                  int cgp, __nv_bfloat16* __restrict__ out) {
+  constexpr int RUN = ST * C, NV = ST * RUN;  // floats per input row run, values per super-pixel
+  const long n = (long)B * Hs * Ws;
+  for (long p = (long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
+    const int X = (int)(p % Ws);
+    const long t = p / Ws;
+    const int Y = (int)(t % Hs), b = (int)(t / Hs);
+    float v[NV];
+#pragma unroll
+    for (int dy = 0; dy < ST; ++dy) {
+      const int yy = Y * ST + dy;
+      const float* row = x + (((size_t)b * H + yy) * W + (size_t)X * ST) * C;
+#pragma unroll
+      for (int i = 0; i < RUN; ++i) {
+        const int xx = X * ST + i / C;
+        v[dy * RUN + i] = (yy < H && xx < W) ? __ldg(row + i) : 0.f;
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)p * cgp);
+#pragma unroll
+    for (int c8 = 0; c8 < (NV + 7) / 8; ++c8) {
+      __nv_bfloat162 h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = c8 * 8 + 2 * k;
+        h[k] = __floats2bfloat162_rn(c < NV ? v[c] : 0.f, c + 1 < NV ? v[c + 1] : 0.f);
+      }
+      dst[c8] = *reinterpret_cast<const uint4*>(h);
+    }
+    for (int c8 = (NV + 7) / 8; c8 < cgp / 8; ++c8) dst[c8] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+cudaError_t launch_s2d_bf16(const float* x, int B, int H, int W, int C, int st, int Hs, int Ws, int cgp,
+                            __nv_bfloat16* out, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  if (cgp % 8 || st * st * C > cgp) return cudaErrorInvalidValue;
+  const long n = (long)B * Hs * Ws;
+  const int grid = (int)std::min<long>((n + 255) / 256, 148L * 16);
+  ktimer_begin("k_s2d_bf16", s);
+  if (st == 4 && C == 3) k_s2d_bf16<4, 3><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
+  else if (st == 2 && C == 3) k_s2d_bf16<2, 3><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
+  else if (st == 2 && C == 4) k_s2d_bf16<2, 4><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
+  else if (st == 4 && C == 4) k_s2d_bf16<4, 4><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
+  else return cudaErrorInvalidValue;
+  const cudaError_t e_ = launched();
+  ktimer_end("k_s2d_bf16", s);
+  return e_;
+}
+
 // im2col for small channel groups (conv1: 3 channels, K = 11*11*3): a warp per
 // output position, lanes along K, so a warp reads the window's contiguous
 // (s, c) runs and writes 64 contiguous bytes per step; the (r, s, c) of every k

@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(256, 4) k_decode(FcDev L, int row_offset, int3
     const LaneStart st = lane_start<REC64>(L, row, active, lj);
     if (!st.vlen) continue;
     uint64_t pos = L.tok_start[(size_t)row * L.G + lj];
-    BitReader vr, gr;
+    dev::SReader vr, gr;  // (four words in flight: the cold stream's latency off each refill)
     vr.init(L.vw, st.vbit);
     gr.init(L.gw, st.gbit);
     int rem = (int)st.vlen;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(256, 4) k_decode(FcDev L, int row_offset, int3
 // stay 0 (the caller zero-fills W).
 template <bool REC64>
 __global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16* __restrict__ W, int ldw, int cg,
-                                                          int cgp) {
+                                                          int cgp, const int* __restrict__ kmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemTables t = carve(L, smem);
   stage_tables(L, t);
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16*
     const bool active = row < L.nrows;
     const LaneStart st = lane_start<REC64>(L, row, active, lj);
     if (!st.vlen) continue;
-    BitReader vr, gr;
+    dev::SReader vr, gr;  // (four words in flight: the cold stream's latency off each refill)
     vr.init(L.vw, st.vbit);
     gr.init(L.gw, st.gbit);
     int rem = (int)st.vlen;
@@ -492,7 +492,8 @@ __global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16*
       col += (int)gs + 1;
       // K order (r, s, c) (C-18); channels padded from cg to cgp per tap for
       // the implicit-GEMM layers (cg == cgp: identity)
-      if (vs) W[(size_t)row * ldw + (col / cg) * cgp + col % cg] = __float2bfloat16_rn(t.cb[vs]);
+      // (kmap: a space-to-depth layer's K order, api.cpp s2d_kmap)
+      if (vs) W[(size_t)row * ldw + (kmap ? kmap[col] : (col / cg) * cgp + col % cg)] = __float2bfloat16_rn(t.cb[vs]);
     }
   }
 }
@@ -609,7 +610,7 @@ cudaError_t launch_decode(const FcDev& L, int row_offset, int32_t* row, int32_t*
 }
 
 cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms, int cg,
-                                int cgp) {
+                                int cgp, const int* kmap) {
   if (cg <= 0) cg = cgp = 1;
   if (L.nrows <= 0) return cudaSuccess;
   const int threads = 256;
@@ -619,10 +620,10 @@ cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaS
   ktimer_begin("k_decode_dense", s);
   if (L.rec64) {
     auto k = k_decode_dense<true>;
-    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw, cg, cgp);
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw, cg, cgp, kmap);
   } else {
     auto k = k_decode_dense<false>;
-    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw, cg, cgp);
+    k<<<occupancy_grid(k, threads, smem, num_sms, work), threads, smem, s>>>(L, W, ldw, cg, cgp, kmap);
   }
   const cudaError_t e_ = launched();
   ktimer_end("k_decode_dense", s);

@@ -209,7 +209,7 @@ cudaError_t launch_bias_act(const float* src, int rows, int B, int lds, const fl
 // cg / cgp: channels per group and their padding per tap (implicit-GEMM layers;
 // column (r*kw + s)*cg + c lands at (r*kw + s)*cgp + c); 0: no remap
 cudaError_t launch_decode_dense(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s, int num_sms, int cg = 0,
-                                int cgp = 0);
+                                int cgp = 0, const int* kmap = nullptr);
 // NHWC fp32 -> bf16 patches [B*Ho*Wo][Kpad] of channels [c0, c0+cg), k = (r*kw+s)*cg + c.
 cudaError_t launch_im2col(const float* x, int B, int H, int W, int C, int kh, int kw, int stride, int pad, int c0,
                           int cg, int Ho, int Wo, int Kreal, int Kpad, __nv_bfloat16* out, cudaStream_t s,
@@ -226,6 +226,11 @@ cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t 
 // im2col mode from that tensor (no patch matrix).
 cudaError_t launch_to_bf16_pad(const float* x, long npix, int C, int G, int cg, int cgp, __nv_bfloat16* out,
                                cudaStream_t s);
+// space-to-depth (strided CONV as a stride-1 one): x fp32 NHWC [B][H][W][C] ->
+// bf16 [B][Hs][Ws][cgp], channel (dy * s + dx) * C + c of super-pixel (Y, X) =
+// x[4Y+dy][4X+dx][c] for s = 4 (zero outside the image / past s*s*C)
+cudaError_t launch_s2d_bf16(const float* x, int B, int H, int W, int C, int st, int Hs, int Ws, int cgp,
+                            __nv_bfloat16* out, cudaStream_t s);
 cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
                                  int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
                                  int relu, float* out, int ldo, cudaStream_t s, int lrn);

@@ -98,20 +98,28 @@ def oracle_conv(spec, c, v, x):
                                                    (4, 2, None, "linear"),
                                                    # the paper's 63% conv5, k-means
                                                    (4, 2, 0.63, "kmeans")])
-def test_alexnet_conv_layer_vs_oracle(torch_dev, i, B, density, quantizer):
+@pytest.mark.parametrize("s2d", ["1", "0"])
+def test_alexnet_conv_layer_vs_oracle(torch_dev, monkeypatch, i, B, density, quantizer, s2d):
     torch, dev = torch_dev
     import paper_1711_00244_b200 as cdn
+    if s2d == "0" and i != 0:
+        pytest.skip("the space-to-depth switch concerns conv1 only")
     spec, c, buf, v = conv_case(i, density, quantizer)
     x = conv_input(i, B)
+    monkeypatch.setenv("CDN_CONV_S2D", s2d)
     m = cdn.Model(0)
     m.load_layer(buf, cdn.LayerDesc.conv(spec.in_ch, IN_HW[i], IN_HW[i], spec.kh, spec.kw, spec.stride, spec.pad,
                                          spec.groups, relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
                                          pool_s=2 if spec.pool else 0))
+    monkeypatch.delenv("CDN_CONV_S2D")
     oh, ow, oc = m.out_shape(0)
     # stride-1 layers with channel groups of >= 8 channels (conv2-5) run the
     # implicit GEMM (TMA im2col, no patch matrix); conv1 (3 channels, stride 4)
-    # the explicit im2col
-    assert m.kernel_name(0, B) == ("k_gemm_bf16 (conv)" if i == 0 else "k_gemm_bf16 (conv, implicit im2col)")
+    # the same after a space-to-depth regrouping (4 x 4 x 3 = 48 channels, a 3 x 3
+    # kernel), or the explicit im2col when that is switched off
+    want = ("k_gemm_bf16 (conv, space-to-depth, implicit im2col)" if s2d == "1" else "k_gemm_bf16 (conv)") \
+        if i == 0 else "k_gemm_bf16 (conv, implicit im2col)"
+    assert m.kernel_name(0, B) == want
     xd = torch.from_numpy(x).to(dev)
     yd = torch.full((B, oh, ow, oc), float("nan"), dtype=torch.float32, device=dev)
     m.conv_forward(0, xd, B, yd)
