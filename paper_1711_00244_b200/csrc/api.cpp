@@ -134,6 +134,7 @@ struct Layer {
   // decoded K index (r, s, c) to its place in that layout
   int s2d = 0, s2d_h = 0, s2d_w = 0, s2d_k = 0;  // stride (0: off), super-pixel grid, super-kernel size
   DBuf s2d_kmap;
+  DBuf clane;  // CONV: per-lane restart states of the filter decode (k_decode_conv)
   uint64_t act_bytes(int B) const {  // the implicit GEMM's bf16 input copy
     return s2d ? 2ull * B * s2d_h * s2d_w * cgp : 2ull * B * desc.in_h * desc.in_w * (uint64_t)desc.groups * cgp;
   }
@@ -882,6 +883,35 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       }
       L.s2d_kmap.upload(km);
     }
+    // the dense-W position of every decoded K index (k_decode_conv): padded
+    // channel groups (implicit GEMM), the space-to-depth order, or k itself
+    if (!L.s2d) {
+      std::vector<int> km(H.cols);
+      for (uint32_t k = 0; k < H.cols; ++k)
+        km[k] = L.implicit ? (int)((k / L.cg) * L.cgp + k % L.cg) : (int)k;
+      L.s2d_kmap.upload(km);
+    }
+    L.dev.kmap = L.s2d_kmap.as<int>();
+    // filter-decode lanes: ~8 tokens each (a CONV layer has few rows), absolute
+    // restart states from the load-time walk
+    {
+      const double toks = (double)ix.tokens / std::max<uint32_t>(1, nr);
+      int cG = 1;
+      while (cG < 256 && toks / (2 * cG) >= 8.0 && (uint32_t)(2 * cG) <= H.cols) cG *= 2;
+      LaneIndex cx;
+      build_lane_index(H, L.row0, L.row1, cG, cx);
+      std::vector<uint4> cl((size_t)nr * cG);
+      for (size_t q = 0; q < cl.size(); ++q) {
+        const uint64_t n = cx.tok_start[q + 1] - cx.tok_start[q];
+        cl[q] = make_uint4((uint32_t)(cx.start_v[q] - vbase), (uint32_t)(cx.start_g[q] - gbase),
+                           (uint32_t)(cx.start_prev[q] + 1), (uint32_t)n);
+      }
+      L.clane.upload(cl);
+      L.dev.clane = L.clane.as<uint4>();
+      L.dev.cG = cG;
+      s.index_bytes += L.clane.n;
+      s.resident_bytes += L.clane.n + L.s2d_kmap.n;
+    }
     L.wd_bytes = (size_t)H.rows * L.kpad * 2;  // per-call scratch, allocated at first use (ensure_wd)
     s.ws_bytes = (uint64_t)H.rows * L.kpad * 2;  // decoded bf16 filters (per-call scratch, C-24)
   }
@@ -1151,9 +1181,7 @@ void predecode_launch(Model& m, Layer& L, cudaStream_t s) {
   if (L.is_conv()) {
     ensure_wd(L);
     CUDA_OK(cudaMemsetAsync(L.wd.p, 0, L.wd.n, s));
-    CUDA_OK(launch_decode_dense(L.dev, static_cast<__nv_bfloat16*>(L.wd.p), L.kpad, s, m.num_sms,
-                                L.implicit ? L.cg : 0, L.implicit ? L.cgp : 0,
-                                L.s2d ? L.s2d_kmap.as<int>() : nullptr));
+    CUDA_OK(launch_decode_conv(L.dev, static_cast<__nv_bfloat16*>(L.wd.p), L.kpad, s));
   } else {
     ensure_list(L);
     CUDA_OK(launch_tc_list(L.dev, s, L.col ? L.kt0 : 0, L.col ? L.kt1 : -1));

@@ -498,6 +498,40 @@ __global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16*
   }
 }
 
+// CONV filter decode (Alg. 1 l.4-8 for a filter row): a thread per
+// lane of L.cG lanes per row, started from its absolute restart state (no scan
+// over the row's lanes), so the grid holds rows x cG threads -- a CONV layer
+// has only 96-384 rows, and a few long lanes per row left most SMs idle (and
+// the persistent GEMMs beside them waiting for their SMs).  Each real token's
+// bf16 codebook value (RNE, C-21) goes to W[row][kmap[col]].
+__global__ void __launch_bounds__(256) k_decode_conv(FcDev L, __nv_bfloat16* __restrict__ W, int ldw) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemTables t = carve(L, smem);
+  // this CTA's lane states first: their loads overlap the table staging
+  const long lane = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nl = (long)L.nrows * L.cG;
+  uint4 st = make_uint4(0u, 0u, 0u, 0u);
+  if (lane < nl) st = L.clane[lane];
+  stage_tables(L, t);
+  __syncthreads();
+  if (st.w == 0) return;
+  const int row = (int)(lane / L.cG);
+  dev::SReader vr, gr;
+  vr.init(L.vw, st.x);
+  gr.init(L.gw, st.y);
+  int col = (int)st.z - 1;
+  __nv_bfloat16* wr = W + (size_t)row * ldw;
+  for (uint32_t n = st.w; n > 0; --n) {
+    uint32_t lv, lg;
+    const uint32_t vs = decode_sym(vr.peek(), t.vlut, L.Lv, t.vtab, t.vsorted, L.vmax, lv);
+    vr.skip(lv);
+    const uint32_t gs = decode_sym(gr.peek(), t.glut, L.Lg, t.gtab, t.gsorted, L.gmax, lg);
+    gr.skip(lg);
+    col += (int)gs + 1;  // c = prev + g + 1 (Alg. 1 l.7, C-01); a pad (symbol 0) writes nothing
+    if (vs) wr[__ldg(L.kmap + col)] = __float2bfloat16_rn(t.cb[vs]);
+  }
+}
+
 __global__ void k_transpose(const float* __restrict__ in, int rows, int cols, int ldi,
                             float* __restrict__ out, int ldo) {
   __shared__ float tile[32][33];
@@ -584,6 +618,19 @@ size_t fc_smem_bytes(const FcDev& L) {
              2 * 99 * sizeof(uint32_t) + sizeof(uint16_t) * (L.nvs + 1) + sizeof(uint16_t) * (L.ngs + 1);
   return (b + 15) & ~(size_t)15;
 }
+
+cudaError_t launch_decode_conv(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s) {
+  if (L.nrows <= 0) return cudaSuccess;
+  if (!L.clane || !L.kmap || L.cG <= 0) return cudaErrorInvalidValue;
+  const long nl = (long)L.nrows * L.cG;
+  const size_t smem = fc_smem_bytes(L);
+  ktimer_begin("k_decode_dense", s);
+  k_decode_conv<<<(unsigned)((nl + 255) / 256), 256, smem, s>>>(L, W, ldw);
+  const cudaError_t e_ = launched();
+  ktimer_end("k_decode_dense", s);
+  return e_;
+}
+
 
 cudaError_t launch_fc_forward(const FcDev& L, const float* x, int ldx, int B, float* y, int ldy,
                               int relu, cudaStream_t s, int num_sms) {

@@ -90,6 +90,13 @@ struct FcDev {
   const uint32_t* jw = nullptr;
   const uint32_t* jrow = nullptr;
   const uint32_t* jlane = nullptr;
+  // CONV filter decode (k_decode_conv): cG lanes per row of cols / cG columns,
+  // per lane {val bit, gap bit, previous column + 1, tokens} (absolute restart
+  // states: no prefix scan, so a row spreads over any number of threads), and
+  // the dense-W position of each decoded K index (padded / space-to-depth order)
+  const uint4* clane = nullptr;
+  int cG = 0;
+  const int* kmap = nullptr;
   const uint32_t* jlutr = nullptr;  // the same blob with the joint LUT in k_fc_j's entry layout (build_joint_lut_r),
   uint32_t jlhash = 0;               // entry of index i at i ^ ((i >> 5) & jlhash)
   const uint32_t* jlut = nullptr;   // the kernel's tables as one blob, laid out as in shared memory:
@@ -226,6 +233,9 @@ cudaError_t launch_lrn(const float* x, long npos, int C, float* y, cudaStream_t 
 // im2col mode from that tensor (no patch matrix).
 cudaError_t launch_to_bf16_pad(const float* x, long npix, int C, int G, int cg, int cgp, __nv_bfloat16* out,
                                cudaStream_t s);
+// CONV filters decoded into dense bf16 W[row][kmap[col]] (the caller zero-fills
+// W) over the per-lane restart states L.clane (a thread per lane)
+cudaError_t launch_decode_conv(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s);
 // space-to-depth (strided CONV as a stride-1 one): x fp32 NHWC [B][H][W][C] ->
 // bf16 [B][Hs][Ws][cgp], channel (dy * s + dx) * C + c of super-pixel (Y, X) =
 // x[4Y+dy][4X+dx][c] for s = 4 (zero outside the image / past s*s*C)
