@@ -188,6 +188,14 @@ struct Model {
   bool force_jm = false;        // autotune: the medium-batch merged-stream kernel for one timed launch
   DBuf tc_xh, tc_xl;            // tensor-core FC: fp16 hi / lo split of the activations
   DBuf tc_sc, tc_ctr;           // tensor-core FC: per-image split scales; their arrival counters (zero between calls)
+  // fused split scales: a tensor-core layer's reduce / epilogue leaves max |y|
+  // per image (tc_xmax, two alternating halves of B u32) for the next
+  // tensor-core layer's split, which then skips its own pass over x.  Valid only
+  // inside one infer call, for the exact buffer the producer wrote (xmax_src)
+  DBuf tc_xmax;
+  const float* xmax_src = nullptr;
+  int xmax_B = 0, xmax_ld = 0, xmax_par = 0, xmax_nrg = 0;
+  bool fuse_scales = true;      // (CDN_TC_FUSE_SCALES=0: every split measures its own input)
   Acct scratch;                 // inference scratch of this model (every buffer above and the layers' workspaces)
   int sharding = CDN_SHARD_ROWS;  // FC layers across ranks (cdn_model_set_sharding)
   cudaStream_t comm_s = nullptr;  // world > 1: the exchanges, overlapped with the next micro-batch's compute
@@ -197,7 +205,7 @@ struct Model {
   std::vector<int> last_plan;   // plan of the last budgeted round (its scratch is what is allocated)
   void tag_scratch() {
     for (DBuf* b : {&stage[0], &stage[1], &out, &loc, &gath, &host_stage, &conv_a, &conv_o, &conv_t, &ctmp, &tc_xh,
-                    &tc_xl, &tc_sc, &tc_ctr, &part, &rsblk, &jmpart})
+                    &tc_xl, &tc_sc, &tc_ctr, &tc_xmax, &part, &rsblk, &jmpart})
       b->acct = &scratch;
   }
   // CUDA graphs of repeated infer calls (same buffers, K, plan and state):
@@ -408,13 +416,19 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     // index above): enough lanes for ~28 warps per SM, none shorter than ~2 tokens (measured: C1 at 4 tokens per lane beats 16)
     int G = 1;
     {
-      const double toks = (double)ix.tokens / std::max<uint32_t>(1, nr);
-      const double want = (double)m.num_sms * 28 * 32 / std::max<uint32_t>(1, nr);
+      // (both from the whole layer, like the lane index: every row shard splits
+      // its rows exactly as one GPU does, so shard outputs are bit-identical
+      // to the 1-GPU rows; tokens per row estimated from the val stream's bits
+      // and its codes' expected length, sum len 2^-len)
+      double el = 0;
+      for (int i = 0; i < H.val.n; ++i) el += H.val.lens[i] * std::ldexp(1.0, -H.val.lens[i]);
+      const double toks = (double)(H.rp[2ull * H.rows] - H.rp[0]) / std::max(1.0, el) / std::max<uint32_t>(1, H.rows);
+      const double want = (double)m.num_sms * 28 * 32 / std::max<uint32_t>(1, H.rows);
       while (G < 32 && G < want && toks / (2 * G) >= 2.0) G *= 2;
       // short layers (few rows, e.g. VGG fc8): rows over several warps so the
       // SMs still hold ~28 warps, while a lane keeps >= 6 tokens
       while (G >= 32 && G < 128 && 2 * G <= want && toks / (2 * G) >= 6.0) G *= 2;
-      if (const char* e = std::getenv("CDN_JG")) G = std::max(1, std::min(32, std::atoi(e)));
+      if (const char* e = std::getenv("CDN_JG")) G = std::max(1, std::min(128, std::atoi(e)));
     }
     uint64_t tb = 0, rmax = 0;
     for (uint32_t i = L.row0; i < L.row1; ++i) {
@@ -994,7 +1008,7 @@ bool jm_call(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int l
 }
 
 void tc_call(Model& m, Layer& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
-             const float* bias, cudaStream_t s, bool x_im, bool y_im) {
+             const float* bias, cudaStream_t s, bool x_im, bool y_im, const float* xmax_prev = nullptr) {
   m.tc_xh.alloc(p.xsplit_elems * 2);
   m.tc_xl.alloc(p.xsplit_elems * 2);
   m.tc_sc.alloc(tc_scale_floats(B) * sizeof(float));
@@ -1010,14 +1024,41 @@ void tc_call(Model& m, Layer& L, const TcPlan& p, const float* x, int ldx, int B
     CUDA_OK(launch_tc_list(L.dev, s, L.col ? L.kt0 : 0, L.col ? L.kt1 : -1));
   }
   L.list_state = 2;
+  // the previous tensor-core layer's max |y| per image, when it wrote exactly x
+  bool fuse = m.fuse_scales && !L.col && !x_im && xmax_prev == x && m.xmax_B == B && m.xmax_ld == ldx;
+  const bool produce = m.fuse_scales && !L.col && !y_im;
+  // two halves of [row group][B] maxima: the producer's for this split, this
+  // layer's for the next (a half holds the largest layer's groups x B)
+  const int nrg = (L.dev.wrows + 31) / 32;
+  int nrg_max = 1;
+  for (auto& l : m.layers) nrg_max = std::max(nrg_max, (l->dev.wrows + 31) / 32);
+  const size_t half = (size_t)nrg_max * B;
+  if ((produce || fuse) && m.tc_xmax.n < 2 * half * sizeof(float)) {
+    fuse = false;  // (a regrown buffer holds no producer maxima)
+    m.tc_xmax.alloc(2 * half * sizeof(float));
+  }
+  float* xm = m.tc_xmax.as<float>();
+  const size_t hsz = m.tc_xmax.n / (2 * sizeof(float));
+  const float* xin = fuse ? xm + (size_t)m.xmax_par * hsz : nullptr;
+  float* xout = produce ? xm + (size_t)(m.xmax_par ^ 1) * hsz : nullptr;
   CUDA_OK(launch_fc_tc(L.dev, p, x, ldx, B, y, ldy, relu, static_cast<uint16_t*>(m.tc_xh.p),
                        static_cast<uint16_t*>(m.tc_xl.p), L.bws.as<float>(), m.tc_sc.as<float>(), m.tc_ctr.as<int>(), s,
-                       x_im, y_im, bias));
+                       x_im, y_im, bias, xin, fuse ? m.xmax_nrg : 0, xout));
+  m.xmax_src = produce ? y : nullptr;
+  m.xmax_B = B;
+  m.xmax_ld = ldy;
+  m.xmax_nrg = nrg;
+  if (produce) m.xmax_par ^= 1;
 }
 
 void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int ldy, cudaStream_t s,
                 bool x_im = false, bool y_im = false) {
   const int relu = L.desc.relu;
+  // the previous tensor-core layer's output with its per-image max: a
+  // tensor-core call below may consume it (and set its own); any other kernel
+  // leaves none
+  const float* xmax_prev = m.xmax_src;
+  m.xmax_src = nullptr;
   if (L.col) {
     // column-sharded: this rank's K tiles for every output row, partial sums
     // (no bias / ReLU: they follow the cross-rank sum); x = the rank's column
@@ -1052,11 +1093,16 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       CUDA_OK(cudaEventCreate(&e0));
       CUDA_OK(cudaEventCreate(&e1));
       CUDA_OK(cudaEventCreate(&e2));
-      // the forced policies below are undone however this block exits
+      // the forced policies below are undone however this block exits; the
+      // timed runs neither consume nor produce fused split maxima (they would
+      // overwrite the previous layer's, which the real call below reads)
       struct Restore {
         int& v;
-        ~Restore() { v = 0; }
-      } restore{m.tc_min};
+        bool& f;
+        bool f0;
+        ~Restore() { v = 0; f = f0; }
+      } restore{m.tc_min, m.fuse_scales, m.fuse_scales};
+      m.fuse_scales = false;
       m.tc_min = B;  // force the tensor-core kernel for one timed launch
       fc_forward(m, L, x, ldx, B, y, ldy, s);
       CUDA_OK(cudaEventRecord(e0, s));
@@ -1097,6 +1143,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
       choice = ttc < tband ? 1 : 0;
       if (tjm < std::min(ttc, tband)) choice = 2;
       L.kchoice.emplace_back(B, choice);
+      m.fuse_scales = restore.f0;
     }
     if (choice == 2 && jm_call(m, L, x, ldx, B, y, ldy, relu, s)) return;
     tcmin = choice == 1 ? B : (1 << 30);
@@ -1104,7 +1151,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
   if (B >= tcmin && tc_supported(L.dev)) {
     const TcPlan p = plan_fc_tc(L.dev, B, m.num_sms);
     if (p.ok) {
-      tc_call(m, L, p, x, ldx, B, y, ldy, relu, L.dev.bias, s, x_im, y_im);
+      tc_call(m, L, p, x, ldx, B, y, ldy, relu, L.dev.bias, s, x_im, y_im, xmax_prev);
       return;
     }
   }
@@ -1216,6 +1263,7 @@ void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
 // dense bf16, im2col per group, tcgen05 GEMM (+bias, ReLU), then LRN and
 // max-pool as the descriptor asks.  y: [B][out_h][out_w][rows] NHWC fp32.
 void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStream_t s) {
+  m.xmax_src = nullptr;  // (no per-image max of a CONV output)
   if (B <= 0) return;
   const cdn_layer_desc& d = L.desc;
   const int M = (int)L.rows, G = d.groups, cg = d.in_c / G, mg = M / G;
@@ -1589,7 +1637,7 @@ uint64_t exec_scratch_bytes(const Model& m, const std::vector<int>& bs, bool hos
       const TcPlan tp = plan_fc_tc(L.dev, B, m.num_sms);
       if (tp.ok) {
         xs = std::max<uint64_t>(xs, tp.xsplit_elems * 2);
-        sc = std::max<uint64_t>(sc, tc_scale_floats(B) * 4);
+        sc = std::max<uint64_t>(sc, tc_scale_floats(B) * 4 + 8ull * B * ((L.dev.wrows + 31) / 32));  // + tc_xmax
         tctr = std::max<uint64_t>(tctr, 4ull * B);
         bws = std::max<uint64_t>(bws, tp.ws_floats * 4);
         total += L.tlist_bytes;
@@ -1746,7 +1794,7 @@ std::vector<uint64_t> out_bytes(const Model& m, int Bmax) {
         const BandPlan bp = plan_fc_band(L->dev, reinterpret_cast<const float*>(256), ld4(B), B, m.num_sms);
         if (bp.ok) part = std::max<uint64_t>(part, (bp.ws_floats * 4 + 4ull * bp.tiles + B - 1) / B);
       }
-      b += 4ull * ((L->cols + 7) & ~7u) + 4ull * (tc_scale_floats(1) + 1) + part;
+      b += 4ull * ((L->cols + 7) & ~7u) + 4ull * (tc_scale_floats(1) + 1) + 8ull * ((L->dev.wrows + 31) / 32) + part;
     }
     v.push_back(b);
   }
@@ -1856,6 +1904,7 @@ cdn_status cdn_model_create(int device, int rank, int world, const uint8_t* nccl
   m.device = device;
   m.rank = rank;
   m.world = world;
+  if (const char* e = std::getenv("CDN_TC_FUSE_SCALES")) m.fuse_scales = e[0] != '0';
   m.tag_scratch();
   CUDA_OK(cudaSetDevice(device));
   CUDA_OK(cudaDeviceGetAttribute(&m.num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -1962,6 +2011,7 @@ namespace {
 // The work of one infer call on stream s (plans, list pre-decoding, rounds).
 void infer_body(Model& m, const float* input, int K, float* scores, int on_device, cudaStream_t s) {
   struct Lists { Model& m; cudaStream_t s; ~Lists() { reset_lists(m, s); } } lists{m, s};
+  m.xmax_src = nullptr;  // fused split scales hold within one call only (the call's own buffers)
   const int f = (int)m.layers.size();
   if (!on_device) {  // the copy streams start with the call (and never wait for its kernels)
     for (cudaStream_t& c : m.cp)
@@ -2137,6 +2187,7 @@ cdn_status cdn_layer_forward(cdn_model* h, int layer, const float* x, int ldx, i
   Model& m = h->m;
   Layer& L = *m.layers[layer];
   if (L.is_conv()) return fail(CDN_E_ARG, "CONV layer: use cdn_conv_forward");
+  m.xmax_src = nullptr;  // the caller's x: its max is measured, never carried over from an earlier call
   if (ldx < B || ldy < B) return fail(CDN_E_ARG, "leading dimension < B");
   CUDA_OK(cudaSetDevice(m.device));
   cudaStream_t s = pick(m, stream);

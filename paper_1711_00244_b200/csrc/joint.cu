@@ -712,7 +712,7 @@ JPlan plan_fc_j(const FcDev& L, int B, int num_sms, const uint32_t* row_bit) {
   const size_t off_x = al(L.jblob);
   const size_t off_slot = al(off_x + (size_t)4 * p.BS * L.jKq);
   int nw0 = std::min(kJMaxWarps, std::max(1, (p.units + rb - 1) / rb));
-  nw0 = std::max(p.wpr, nw0 / p.wpr * p.wpr);
+  nw0 = std::min(kJMaxWarps, (nw0 + p.wpr - 1) / p.wpr * p.wpr);  // whole rows per CTA (rounded up: <= one wave)
   for (p.nw = nw0; p.nw >= p.wpr; p.nw -= p.wpr) {
     p.nrb = (p.units + p.nw - 1) / p.nw;
     p.cta.clear();

@@ -178,7 +178,8 @@ size_t tc_scale_floats(int B);
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
                          bool x_image_major, bool y_image_major,
-                         const float* bias);  // x: [kcols][ldx] feature-major, or [B][ldx] image-major (the plan's K
+                         const float* bias,
+                         const float* xrg_in = nullptr, int nrg_in = 0, float* xrg_out = nullptr);  // x: [kcols][ldx] feature-major, or [B][ldx] image-major (the plan's K
                                               // columns); bias null: partial sums without bias / ReLU
 
 // Small-batch multi-symbol kernel (B <= 8; r <= 5, k <= 4, 32-bit lane records).

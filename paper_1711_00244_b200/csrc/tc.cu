@@ -84,6 +84,7 @@ struct TcArgs {
   float winv;                   // 1 / the layer's weight scale
   int kbase;                    // first K tile of this call (column-sharded layers: the rank's K block)
   const float* bias;            // added in the epilogue; null: partial sums (column-sharded layers)
+  float* xrg;                   // non-null: max |y| per (32-row group, image), [row group][B], for the next split
 };
 
 __device__ __forceinline__ void tc_trace(const TcArgs& a, int ev, int i) {
@@ -501,6 +502,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
               v[i] += bias;
               if (a.relu) v[i] = fmaxf(v[i], 0.f);
             }
+          }
+          if (a.xrg) {  // the images' max |y| over the warp's 32 rows (the next layer's split scale)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t mx =
+                  __reduce_max_sync(0xffffffffu, row < L.wrows ? __float_as_uint(fabsf(v[i])) : 0u);
+              if (lane == 0 && b0 + c + i < a.B) a.xrg[(size_t)(t.rt * 4 + q4) * a.B + b0 + c + i] = __uint_as_float(mx);
+            }
+          }
+          if (row < L.wrows) {
             if (a.yt) {  // image-major: a warp's 32 rows are 128 contiguous bytes per image
 #pragma unroll
               for (int i = 0; i < 16; ++i)
@@ -603,8 +614,30 @@ __device__ __forceinline__ void split_pair(float v0, float v1, float s, uint32_t
 constexpr int kSplitK = 64, kSplitB = 32;
 __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, int K, int ldx, int B,
                                                  uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int ldk,
-                                                 const float* __restrict__ xsc) {
+                                                 float* __restrict__ xsc, const float* __restrict__ xrg, int nrg) {
   asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
+  // xrg: the producer's max |x| per (32-row group, image) -- the fused scale (no
+  // k_xscale_cols pass over x): every block reduces its 32 images' groups; the
+  // first K block of an image group writes the scales for the contraction
+  __shared__ float s_m[8][kSplitB + 1];
+  __shared__ float s_sc[kSplitB];
+  if (xrg) {
+    const int bl = (int)(threadIdx.x & 31), b = blockIdx.y * kSplitB + bl;
+    float mx = 0.f;
+    if (b < B)
+      for (int g = (int)(threadIdx.x >> 5); g < nrg; g += 8) mx = fmaxf(mx, __ldg(xrg + (size_t)g * B + b));
+    s_m[threadIdx.x >> 5][bl] = mx;
+    __syncthreads();
+    if (threadIdx.x < kSplitB) {
+      for (int i = 1; i < 8; ++i) mx = fmaxf(mx, s_m[i][bl]);
+      const float sc = pow2_scale(mx);
+      s_sc[bl] = sc;
+      if (blockIdx.x == 0 && b < B) {
+        xsc[b] = sc;
+        xsc[B + b] = 1.0f / sc;
+      }
+    }
+  }
   __shared__ float tile[kSplitK][kSplitB + 1];
   const int k0 = blockIdx.x * kSplitK, b0 = blockIdx.y * kSplitB;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
@@ -617,7 +650,7 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
   const int c = threadIdx.x & 7, bl = threadIdx.x >> 3;  // k chunk (8 values), image
   const int b = b0 + bl, k = k0 + 8 * c;
   if (b >= B || k >= ldk) return;
-  const float sb = xsc[b];
+  const float sb = xrg ? s_sc[bl] : xsc[b];
   uint32_t h[4], l[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) split_pair(tile[8 * c + 2 * i][bl], tile[8 * c + 2 * i + 1][bl], sb, h[i], l[i]);
@@ -640,7 +673,8 @@ __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, in
 template <int TN>
 __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws, uint32_t W, int G, int nkt,
                                                    int mpt, int nbt, int nrows, int B, const float* __restrict__ bias,
-                                                   int relu, float* __restrict__ y, int ldy, int vec_ok, int yt) {
+                                                   int relu, float* __restrict__ y, int ldy, int vec_ok, int yt,
+                                                   float* __restrict__ xrg) {
   // block = 32 rows x 8 float4 column groups of one tile.  Reads go row-fastest
   // (the partials are column-group major, [TN / 4][128] float4 per piece:
   // coalesced), the sums are transposed through shared memory, and the y
@@ -677,6 +711,15 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
       acc.x += bs; acc.y += bs; acc.z += bs; acc.w += bs;
       if (relu) {
         acc.x = fmaxf(acc.x, 0.f); acc.y = fmaxf(acc.y, 0.f); acc.z = fmaxf(acc.z, 0.f); acc.w = fmaxf(acc.w, 0.f);
+      }
+    }
+    if (xrg) {  // the images' max |y| over the warp's 32 rows (the next layer's split scale)
+      const bool in = row < nrows && b < B;
+      const float ov[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t mx = __reduce_max_sync(0xffffffffu, in ? __float_as_uint(fabsf(ov[k])) : 0u);
+        if ((threadIdx.x & 31) == 0 && b + k < B) xrg[(size_t)(rt * 4 + rg) * B + b + k] = __uint_as_float(mx);
       }
     }
     if (yt) {  // image-major y (class scores): consecutive rows are consecutive floats
@@ -1112,7 +1155,8 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s, int kt0, int kt1) {
 
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
-                         bool x_image_major, bool y_image_major, const float* bias) {
+                         bool x_image_major, bool y_image_major, const float* bias, const float* xrg_in,
+                         int nrg_in, float* xrg_out) {
   // per-image scales of the fp16 split: scw = [B scales | B inverse scales |
   // kScaleChunks x B partial maxima]; xctr: >= B arrival counters, zero between calls
   float* xsc = scw;
@@ -1122,11 +1166,12 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     const int vec = (ldx % 4) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     k_scale_split_rows<<<(unsigned)B, 512, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, vec, xsc);
   } else {
-    k_xscale_cols<<<dim3((unsigned)((B + 31) / 32), kScaleChunks), 256, 0, s>>>(x, p.kcols, ldx, B, xpart, xctr, xsc);
+    if (!xrg_in)  // (no producer maxima: a separate pass over x)
+      k_xscale_cols<<<dim3((unsigned)((B + 31) / 32), kScaleChunks), 256, 0, s>>>(x, p.kcols, ldx, B, xpart, xctr, xsc);
     dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
-    k_split_x<<<sg, 256, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, xsc);
+    k_split_x<<<sg, 256, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, xsc, xrg_in, nrg_in);
   }
-  cudaError_t e = launched(x_image_major ? 1 : 2);
+  cudaError_t e = launched(x_image_major || xrg_in ? 1 : 2);
   ktimer_end("k_split_x", s);
   if (e != cudaSuccess) return e;
   CUtensorMap th, tl;
@@ -1152,7 +1197,7 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   }
   if (trace) cudaMemsetAsync(trace, 0, 16 * 256 * sizeof(unsigned long long), s);
   TcArgs a{y, ldy, B, relu, ws, p.nbt, p.nrt, p.nkt, p.grid, p.mpt, p.W, trace_path ? trace : nullptr,
-           y_image_major ? 1 : 0, xsc, 1.0f / L.tc_wsc, p.kbase, bias};
+           y_image_major ? 1 : 0, xsc, 1.0f / L.tc_wsc, p.kbase, bias, y_image_major ? nullptr : xrg_out};
   ktimer_begin("k_fc_tc", s);
   {
     cudaLaunchConfig_t cfg = {};
@@ -1191,13 +1236,13 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
     const int yt = y_image_major ? 1 : 0;
     if (p.tn == 128)
       e = cudaLaunchKernelEx(&cfg, k_tc_reduce<128>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
-                             bias, relu, y, ldy, vec_ok, yt);
+                             bias, relu, y, ldy, vec_ok, yt, yt ? nullptr : xrg_out);
     else if (p.tn == 64)
       e = cudaLaunchKernelEx(&cfg, k_tc_reduce<64>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
-                             bias, relu, y, ldy, vec_ok, yt);
+                             bias, relu, y, ldy, vec_ok, yt, yt ? nullptr : xrg_out);
     else
       e = cudaLaunchKernelEx(&cfg, k_tc_reduce<256>, wsc, (uint32_t)p.W, p.grid, p.nkt, p.mpt, p.nbt, (int)L.wrows, B,
-                             bias, relu, y, ldy, vec_ok, yt);
+                             bias, relu, y, ldy, vec_ok, yt, yt ? nullptr : xrg_out);
     if (e == cudaSuccess) e = launched();
     ktimer_end("k_tc_reduce", s);
   }

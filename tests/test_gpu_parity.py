@@ -753,3 +753,40 @@ def test_column_sharded_layer_partials(torch_dev, cfg, i, world):
     scale = infer.fc_abs_scale(sparse_q(c), a, v)
     kmax = int(c.row_tokens.max())
     assert (np.abs(out - ref) / np.maximum(scale, 1e-30)).max() <= 2 * kmax * 2.0 ** -24 + world * 2.0 ** -20
+
+
+@pytest.mark.gpu
+def test_fused_split_scales_bit_identical(torch_dev, monkeypatch):
+    """A tensor-core layer's reduce / epilogue leaves the max |y| of every
+    (32-row group, image) for the next tensor-core layer's fp16 split, which
+    then skips its own pass over x.  The scale is the same
+    power of two either way, so the scores must be bit-identical to the
+    separate max pass -- for device and host input, the first call (whose
+    autotune runs must not clobber the producer's maxima) and graph replays,
+    whole-batch and variable-batch plans."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    cfg = synth.CONFIGS["C3"]
+    outs = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("CDN_TC_FUSE_SCALES", fuse)
+        m = cdn.Model(0)
+        monkeypatch.delenv("CDN_TC_FUSE_SCALES")
+        for i, spec in enumerate(cfg.fc):
+            _, _, buf = config_layer("C3", i)
+            m.load_layer(buf, cdn.LayerDesc.fc(spec.relu))
+        for K, plan in ((256, [256, 256, 256]), (300, [50, 100, 100])):
+            m.set_plan(plan)
+            a = synth.fc_inputs(cfg.fc[0].cols, K, 1)
+            host = np.zeros((K, 1000), np.float32)
+            m.infer(a, K, host, on_device=False)
+            xi = torch.from_numpy(a).to(dev)
+            for rep in range(3):  # eager, captured, replayed
+                so = torch.zeros((K, 1000), dtype=torch.float32, device=dev)
+                m.infer(xi, K, so, on_device=True)
+                torch.cuda.synchronize()
+                assert np.array_equal(so.cpu().numpy(), host), (fuse, K, rep)
+            outs[(fuse, K)] = host
+        m.close()
+    for K in (256, 300):
+        assert np.array_equal(outs[("1", K)], outs[("0", K)]), K
