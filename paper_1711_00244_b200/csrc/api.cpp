@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -99,7 +100,9 @@ struct Layer {
   uint32_t rows = 0, cols = 0, row0 = 0, row1 = 0, k = 0, r = 0;
   FcDev dev;
   DBuf vw, gw, rp, rec, tok, vlut, glut, vtab, gtab, vsorted, gsorted, cb, bias, flut, ctr;
-  DBuf ivg, ivm;        // band-kernel interval restart index
+  DBuf ivg, ivm;        // band-kernel interval restart index (uploaded at the band kernel's first use)
+  std::vector<uint32_t> ivg_h;  // ... its host copy until then (the default autotune rarely needs it:
+  std::vector<uint16_t> ivm_h;  // the resident model stays without its 16 MB on C5 fc6)
   DBuf tivg, tivm;      // tensor-core kernel Wi = 64 index (when ivg/ivm use another width)
   DBuf tbase, troff, tlist;  // tensor-core kernel: list block bases / row offsets, decoded-entry list (per-call scratch)
   // tlist state within one API call: 0 = not decoded yet, 1 = being decoded on
@@ -650,8 +653,10 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
         }
       if (mx <= (uint32_t)band_list_capacity()) break;
     }
-    L.ivg.upload(ivg);
-    L.ivm.upload(ivm);
+    if (!conv) {  // (CONV filters decode through k_decode_conv)
+      L.ivg_h = std::move(ivg);
+      L.ivm_h = std::move(ivm);
+    }
     L.dev.Wi = (int)Wi;
     L.dev.NI = (int)iv.NI;
     L.dev.Cint = cint;
@@ -664,15 +669,6 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
     } else if (!conv) {
       build_interval_index(H, L.row0, L.row1, 64, t64);
       i64 = &t64;
-      std::vector<uint32_t> tg(2 * t64.v.size());
-      std::vector<uint16_t> tm(t64.v.size());
-      for (size_t q = 0; q < t64.v.size(); ++q) {
-        tg[2 * q] = (uint32_t)(t64.v[q] - vbase);
-        tg[2 * q + 1] = (uint32_t)(t64.g[q] - gbase);
-        tm[q] = (uint16_t)(t64.dm1[q] | ((uint16_t)t64.nnz[q] << 8));
-      }
-      L.tivg.upload(tg);
-      L.tivm.upload(tm);
       L.dev.sNI = (int)t64.NI;
     }
     if (i64 && !conv) {
@@ -725,6 +721,22 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
       while (tch > 1 && (nr + grp - 1) / grp * grp * ((SNI + tch - 1) / tch) < 65536) tch >>= 1;
       if (const char* e = std::getenv("CDN_TC_CHUNK")) tch = std::max(1, std::min(kTcChunk, std::atoi(e)));
       L.dev.tch = tch;
+      // the list decoder restarts only at chunk starts (K tile c * tch of a
+      // stored row): its restart index keeps those intervals alone (1 / tch
+      // of the Wi = 64 index -- C5 fc6: 2 MB instead of 16 MB resident)
+      const uint32_t nch = (SNI + (uint32_t)tch - 1) / (uint32_t)tch;
+      std::vector<uint32_t> tg(2ull * nr * nch);
+      std::vector<uint16_t> tm((size_t)nr * nch);
+      for (uint32_t i = 0; i < nr; ++i)
+        for (uint32_t c = 0; c < nch; ++c) {
+          const size_t q = (size_t)i * SNI + (size_t)c * tch, d = (size_t)i * nch + c;
+          tg[2 * d] = (uint32_t)(i64->v[q] - vbase);
+          tg[2 * d + 1] = (uint32_t)(i64->g[q] - gbase);
+          tm[d] = (uint16_t)i64->dm1[q];
+        }
+      L.tivg.upload(tg);
+      L.tivm.upload(tm);
+      L.dev.sNC = (int)nch;
     }
   }
   const int Lv = std::max(1, std::min(H.val.max_len, kLutMaxBits));
@@ -818,13 +830,13 @@ void load_layer(Model& m, const uint8_t* buf, size_t n, int idx, const cdn_layer
   f.jmlane = L.jmlane.p ? L.jmlane.as<uint32_t>() : nullptr;
   f.jmperm = L.jmperm.p ? L.jmperm.as<uint16_t>() : nullptr;
   f.jmlut = L.jmlut.p ? L.jmlut.as<uint32_t>() : nullptr;
-  f.tivg = L.tivg.p ? L.tivg.as<uint2>() : (L.dev.Wi == 64 ? L.ivg.as<uint2>() : nullptr);
-  f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : (L.dev.Wi == 64 ? L.ivm.as<uint16_t>() : nullptr);
+  f.tivg = L.tivg.p ? L.tivg.as<uint2>() : nullptr;
+  f.tivm = L.tivm.p ? L.tivm.as<uint16_t>() : nullptr;
   f.tbase = L.tbase.as<uint32_t>();
   f.troff = L.troff.as<uint16_t>();
   f.tlist = nullptr;  // ensure_list
-  f.ivg = L.ivg.as<uint2>();
-  f.ivm = L.ivm.as<uint16_t>();
+  f.ivg = nullptr;  // (ensure_band_index)
+  f.ivm = nullptr;
 
   if (colsh) {
     const ColBlock cb = col_block(H.wcols, m.rank, m.world);
@@ -1007,6 +1019,20 @@ bool jm_call(Model& m, Layer& L, const float* x, int ldx, int B, float* y, int l
   return true;
 }
 
+// The band kernel's interval index goes to the device at the kernel's first
+// use (it is the largest index of a layer and the default kernels need none of it)
+void ensure_band_index(Layer& L) {
+  if (L.ivg.p || L.ivg_h.empty()) return;
+  L.ivg.upload(L.ivg_h);
+  L.ivm.upload(L.ivm_h);
+  L.dev.ivg = L.ivg.as<uint2>();
+  L.dev.ivm = L.ivm.as<uint16_t>();
+  L.stats.index_bytes += L.ivg.n + L.ivm.n;
+  L.stats.resident_bytes += L.ivg.n + L.ivm.n;
+  std::vector<uint32_t>().swap(L.ivg_h);
+  std::vector<uint16_t>().swap(L.ivm_h);
+}
+
 void tc_call(Model& m, Layer& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
              const float* bias, cudaStream_t s, bool x_im, bool y_im, const float* xmax_prev = nullptr) {
   m.tc_xh.alloc(p.xsplit_elems * 2);
@@ -1089,10 +1115,6 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
     for (auto& e : L.kchoice)
       if (e.first == B) choice = e.second;
     if (choice < 0) {
-      cudaEvent_t e0, e1, e2;
-      CUDA_OK(cudaEventCreate(&e0));
-      CUDA_OK(cudaEventCreate(&e1));
-      CUDA_OK(cudaEventCreate(&e2));
       // the forced policies below are undone however this block exits; the
       // timed runs neither consume nor produce fused split maxima (they would
       // overwrite the previous layer's, which the real call below reads)
@@ -1103,43 +1125,52 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
         ~Restore() { v = 0; f = f0; }
       } restore{m.tc_min, m.fuse_scales, m.fuse_scales};
       m.fuse_scales = false;
-      m.tc_min = B;  // force the tensor-core kernel for one timed launch
-      fc_forward(m, L, x, ldx, B, y, ldy, s);
-      CUDA_OK(cudaEventRecord(e0, s));
-      L.list_state = 0;  // the timed run decodes its list like a fresh call
-      fc_forward(m, L, x, ldx, B, y, ldy, s);
-      CUDA_OK(cudaEventRecord(e1, s));
-      m.tc_min = 1 << 30;  // then the band kernel
-      fc_forward(m, L, x, ldx, B, y, ldy, s);
-      CUDA_OK(cudaEventRecord(e2, s));
+      // each candidate: one untimed run (allocations, attributes, plans), then
+      // one run enqueued behind a GPU-side spin, so the host's enqueue work
+      // (tensor-map encodes, plan lookups) is not timed as GPU idle time
+      cudaEvent_t e0, e1;
+      CUDA_OK(cudaEventCreate(&e0));
+      CUDA_OK(cudaEventCreate(&e1));
+      auto timed = [&](const std::function<void()>& run) {
+        run();
+        CUDA_OK(launch_spin(s, 200000));
+        CUDA_OK(cudaEventRecord(e0, s));
+        run();
+        CUDA_OK(cudaEventRecord(e1, s));
+        CUDA_OK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        return ms;
+      };
+      // tensor cores (the timed run decodes its list like a fresh call)
+      const float ttc = timed([&] {
+        m.tc_min = B;
+        L.list_state = 0;
+        fc_forward(m, L, x, ldx, B, y, ldy, s);
+      });
+      // the band kernel (fp32 CUDA cores) only where the medium-batch kernel
+      // cannot run: on C1-C5 it was never the fastest of the three
+      // (profiles/r02_grid.jsonl), and its index would then stay off the device
+      const bool jm_ok = jm_plan(m, L, B);
+      const float tband = jm_ok ? 1e30f : timed([&] {
+        m.tc_min = 1 << 30;
+        fc_forward(m, L, x, ldx, B, y, ldy, s);
+      });
       m.tc_min = 0;
       float tjm = 1e30f;
-      if (jm_plan(m, L, B)) {  // then the medium-batch merged-stream kernel
-        cudaEvent_t e3, e4;
-        CUDA_OK(cudaEventCreate(&e3));
-        CUDA_OK(cudaEventCreate(&e4));
+      if (jm_ok) {  // the medium-batch merged-stream kernel
         struct Unforce {
           bool& v;
           ~Unforce() { v = false; }
         } unforce{m.force_jm};
-        m.force_jm = true;
-        fc_forward(m, L, x, ldx, B, y, ldy, s);  // (untimed: partial-sum buffer, smem attribute)
-        CUDA_OK(cudaEventRecord(e3, s));
-        fc_forward(m, L, x, ldx, B, y, ldy, s);
-        CUDA_OK(cudaEventRecord(e4, s));
-        m.force_jm = false;
-        CUDA_OK(cudaEventSynchronize(e4));
-        CUDA_OK(cudaEventElapsedTime(&tjm, e3, e4));
-        cudaEventDestroy(e3);
-        cudaEventDestroy(e4);
+        tjm = timed([&] {
+          m.force_jm = true;
+          fc_forward(m, L, x, ldx, B, y, ldy, s);
+          m.force_jm = false;
+        });
       }
-      CUDA_OK(cudaEventSynchronize(e2));
-      float ttc = 0.f, tband = 0.f;
-      CUDA_OK(cudaEventElapsedTime(&ttc, e0, e1));
-      CUDA_OK(cudaEventElapsedTime(&tband, e1, e2));
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
-      cudaEventDestroy(e2);
       choice = ttc < tband ? 1 : 0;
       if (tjm < std::min(ttc, tband)) choice = 2;
       L.kchoice.emplace_back(B, choice);
@@ -1159,6 +1190,7 @@ void fc_forward(Model& m, Layer& L, const float* x, int ldx, int B, float* y, in
   if (B >= (m.band_min > 0 ? m.band_min : band_min_batch())) {
     BandPlan p = plan_fc_band(L.dev, x, ldx, B, m.num_sms);
     if (p.ok) {
+      ensure_band_index(L);
       if (p.ws_floats) L.bws.alloc(p.ws_floats * sizeof(float));
       const size_t need = sizeof(int) * (size_t)p.tiles;
       if (L.bctr.n < need || !L.bctr.p) {
@@ -1785,7 +1817,7 @@ std::vector<uint64_t> out_bytes(const Model& m, int Bmax) {
       // implicit GEMM: the bf16 copy of the input (padded channels), not patches
       const uint64_t a = L->implicit ? L->act_bytes(1) : 2ull * L->conv_h * L->conv_w * L->kpad * (uint64_t)L->desc.groups;
       b += a + (uint64_t)L->conv_h * L->conv_w * (L->desc.lrn || L->desc.pool_k ? 8ull : 0ull) * L->rows;
-    } else if (tc_supported(L->dev) || L->dev.ivg) {
+    } else if (tc_supported(L->dev) || L->dev.Cint > 0) {
       uint64_t part = 0;
       for (int B : {16, 32, 64, 128, 256, 512, Bmax}) {
         if (B > Bmax || B < 1) continue;

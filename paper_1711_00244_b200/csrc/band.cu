@@ -493,7 +493,7 @@ int band_max_chunk() { return kMaxCint; }
 
 BandPlan plan_fc_band(const FcDev& L, const float* x, int ldx, int B, int num_sms) {
   BandPlan p;
-  if (B <= 0 || L.nrows <= 0 || !L.ivg || L.Cint <= 0) return p;
+  if (B <= 0 || L.nrows <= 0 || L.Cint <= 0) return p;  // (L.ivg: uploaded at first use, api.cpp)
   const int vec = B > 64 ? 4 : (B > 32 ? 2 : 1);
   const int BT = 32 * vec;
   if ((ldx & 3) || ldx < B || ((uintptr_t)x & 15)) return p;  // TMA: 16-byte row pitch and base

@@ -619,6 +619,21 @@ size_t fc_smem_bytes(const FcDev& L) {
   return (b + 15) & ~(size_t)15;
 }
 
+// Keeps the GPU busy for ~ns nanoseconds (autotune: the host enqueues the timed
+// run behind it, so host-side work inside the run is not timed as GPU idle)
+__global__ void k_spin(long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((long long)(t - t0) < ns);
+}
+
+cudaError_t launch_spin(cudaStream_t s, long long ns) {
+  k_spin<<<1, 32, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_decode_conv(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s) {
   if (L.nrows <= 0) return cudaSuccess;
   if (!L.clane || !L.kmap || L.cG <= 0) return cudaErrorInvalidValue;

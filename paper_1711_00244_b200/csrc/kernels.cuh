@@ -66,7 +66,8 @@ struct FcDev {
   const uint2* tivg = nullptr;
   const uint16_t* tivm = nullptr;
   int tNI = 0;                       // 64-column K tiles of the weight matrix (list blocks, contraction)
-  int sNI = 0;                       // 64-position intervals per stored row (tivg / tivm rows)
+  int sNI = 0;                       // 64-position intervals per stored row
+  int sNC = 0;                       // list-decoder chunks per stored row (tivg / tivm rows: the chunk starts)
   // Block-contiguous container (Alg. 2, C-34): nrows / cols above are the
   // STORED matrix's (blocks of M' when blocked); the weight matrix is
   // wrows x wcols in bh x bw blocks, stored row i = block (i / (wcols/bw),
@@ -237,6 +238,8 @@ cudaError_t launch_to_bf16_pad(const float* x, long npix, int C, int G, int cg, 
 // CONV filters decoded into dense bf16 W[row][kmap[col]] (the caller zero-fills
 // W) over the per-lane restart states L.clane (a thread per lane)
 cudaError_t launch_decode_conv(const FcDev& L, __nv_bfloat16* W, int ldw, cudaStream_t s);
+// a one-warp kernel spinning ~ns nanoseconds on the GPU clock (autotune timing)
+cudaError_t launch_spin(cudaStream_t s, long long ns);
 // space-to-depth (strided CONV as a stride-1 one): x fp32 NHWC [B][H][W][C] ->
 // bf16 [B][Hs][Ws][cgp], channel (dy * s + dx) * C + c of super-pixel (Y, X) =
 // x[4Y+dy][4X+dx][c] for s = 4 (zero outside the image / past s*s*C)

@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list(FcDev L, int c0, int n
     }
   }
   if (n == 0) return;
-  const size_t q = (size_t)row * L.sNI + kt0;
+  const size_t q = (size_t)row * L.sNC + kt0 / tch;  // (restart index: chunk starts only)
   const uint2 st = L.tivg[q];
   int col = kt0 * 64 - (int)(L.tivm[q] & 0xFFu) - 1;
   SReader vr, gr;
@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(kListThreads) k_tc_list_ms(FcDev L, int c0, in
   if (row >= L.nrows) return;
   const int nk = L.sNI - kt0 < tch ? L.sNI - kt0 : tch;
   // the decoder state first (its loads gate everything), the output slots meanwhile
-  const size_t q = (size_t)row * L.sNI + kt0;
+  const size_t q = (size_t)row * L.sNC + kt0 / tch;  // (restart index: chunk starts only)
   const uint2 st = L.tivg[q];
   const uint32_t m0 = L.tivm[q];
   // this thread's first list slot in each tile of the chunk, in shared memory
@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(512) k_scale_split_rows(const float* __restric
 size_t tc_scale_floats(int B) { return (size_t)B * (kScaleChunks + 2); }
 
 bool tc_supported(const FcDev& L) {
-  return L.tivg && L.tivm && L.tNI > 0 && L.sNI > 0 && L.tbase && L.troff && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
+  return L.tivg && L.tivm && L.tNI > 0 && L.sNI > 0 && L.sNC > 0 && L.tbase && L.troff && L.ncb <= 256 && L.nvs <= 256 && L.ngs <= 256 &&
          L.Lf == kFoldLutBits && L.Lg <= kLutMaxBits;
 }
 
