@@ -171,14 +171,31 @@ __device__ __forceinline__ SmemTables carve(const FcDev& L, unsigned char* base)
   return t;
 }
 
-__device__ void stage_tables(const FcDev& L, const SmemTables& t) {
+// A table copied global -> shared with every load of a batch in flight before
+// its stores (a plain loop waits one global latency per element: the compiler
+// cannot move a load above a store through a possibly aliasing pointer)
+template <typename T>
+__device__ __forceinline__ void stage_copy(T* __restrict__ dst, const T* __restrict__ src, int n) {
+  constexpr int NB = 8;
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < (1 << L.Lv); i += nt) t.vlut[i] = L.vlut[i];
-  for (int i = tid; i < (1 << L.Lg); i += nt) t.glut[i] = L.glut[i];
-  for (int i = tid; i < L.ncb; i += nt) t.cb[i] = L.codebook[i];
-  for (int i = tid; i < 99; i += nt) { t.vtab[i] = L.vtab[i]; t.gtab[i] = L.gtab[i]; }
-  for (int i = tid; i < L.nvs; i += nt) t.vsorted[i] = L.vsorted[i];
-  for (int i = tid; i < L.ngs; i += nt) t.gsorted[i] = L.gsorted[i];
+  for (int b = tid; b < n; b += NB * nt) {
+    T v[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) v[k] = b + k * nt < n ? __ldg(src + b + k * nt) : T(0);
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      if (b + k * nt < n) dst[b + k * nt] = v[k];
+  }
+}
+
+__device__ void stage_tables(const FcDev& L, const SmemTables& t) {
+  stage_copy(t.vlut, L.vlut, 1 << L.Lv);
+  stage_copy(t.glut, L.glut, 1 << L.Lg);
+  stage_copy(t.cb, L.codebook, L.ncb);
+  stage_copy(t.vtab, L.vtab, 99);
+  stage_copy(t.gtab, L.gtab, 99);
+  stage_copy(t.vsorted, L.vsorted, L.nvs);
+  stage_copy(t.gsorted, L.gsorted, L.ngs);
 }
 
 // Canonical decode of the code starting at the top of w: primary LUT on the
@@ -498,6 +515,12 @@ __global__ void __launch_bounds__(256, 4) k_decode_dense(FcDev L, __nv_bfloat16*
   }
 }
 
+__device__ __forceinline__ size_t fc_smem_bytes_dev(const FcDev& L) {  // (= fc_smem_bytes, host)
+  const size_t b = (sizeof(uint32_t) << L.Lv) + (sizeof(uint32_t) << L.Lg) + sizeof(float) * L.ncb +
+                   2 * 99 * sizeof(uint32_t) + sizeof(uint16_t) * (L.nvs + 1) + sizeof(uint16_t) * (L.ngs + 1);
+  return (b + 15) & ~(size_t)15;
+}
+
 // CONV filter decode (Alg. 1 l.4-8 for a filter row): a thread per
 // lane of L.cG lanes per row, started from its absolute restart state (no scan
 // over the row's lanes), so the grid holds rows x cG threads -- a CONV layer
@@ -513,6 +536,10 @@ __global__ void __launch_bounds__(256) k_decode_conv(FcDev L, __nv_bfloat16* __r
   uint4 st = make_uint4(0u, 0u, 0u, 0u);
   if (lane < nl) st = L.clane[lane];
   stage_tables(L, t);
+  // the K map beside the tables: one shared load per token instead of a
+  // dependent global one
+  int* s_kmap = reinterpret_cast<int*>(smem + fc_smem_bytes_dev(L));
+  stage_copy(s_kmap, L.kmap, L.cols);
   __syncthreads();
   if (st.w == 0) return;
   const int row = (int)(lane / L.cG);
@@ -528,7 +555,7 @@ __global__ void __launch_bounds__(256) k_decode_conv(FcDev L, __nv_bfloat16* __r
     const uint32_t gs = decode_sym(gr.peek(), t.glut, L.Lg, t.gtab, t.gsorted, L.gmax, lg);
     gr.skip(lg);
     col += (int)gs + 1;  // c = prev + g + 1 (Alg. 1 l.7, C-01); a pad (symbol 0) writes nothing
-    if (vs) wr[__ldg(L.kmap + col)] = __float2bfloat16_rn(t.cb[vs]);
+    if (vs) wr[s_kmap[col]] = __float2bfloat16_rn(t.cb[vs]);
   }
 }
 
@@ -638,7 +665,11 @@ cudaError_t launch_decode_conv(const FcDev& L, __nv_bfloat16* W, int ldw, cudaSt
   if (L.nrows <= 0) return cudaSuccess;
   if (!L.clane || !L.kmap || L.cG <= 0) return cudaErrorInvalidValue;
   const long nl = (long)L.nrows * L.cG;
-  const size_t smem = fc_smem_bytes(L);
+  const size_t smem = fc_smem_bytes(L) + sizeof(int) * (size_t)L.cols;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_decode_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   ktimer_begin("k_decode_dense", s);
   k_decode_conv<<<(unsigned)((nl + 255) / 256), 256, smem, s>>>(L, W, ldw);
   const cudaError_t e_ = launched();
