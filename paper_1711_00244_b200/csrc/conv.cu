@@ -19,6 +19,7 @@
 //   k_lrn, k_maxpool: the AlexNet norm / pool layers (C-19, C-20), NHWC fp32.
 #include <cuda.h>
 #include <algorithm>
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "dev_common.cuh"
@@ -416,7 +417,11 @@ int grid_for(long work, int threads, int num_sms) {
 }  // namespace
 
 int gemm_tile_n(int Nrows) {
-  int tiles = (Nrows + 255) / 256;
+  static const int cap = [] {  // (experiment knob: widest filter tile)
+    const char* e = std::getenv("CDN_GEMM_BN");
+    return e ? std::max(16, std::min(256, std::atoi(e))) : 256;
+  }();
+  int tiles = (Nrows + cap - 1) / cap;
   int bn = (Nrows + tiles - 1) / tiles;
   return (bn + 15) & ~15;
 }

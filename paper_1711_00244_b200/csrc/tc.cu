@@ -575,6 +575,7 @@ __device__ __forceinline__ void scale_finish(float m, int b, int B, int nparts, 
 }
 __global__ void __launch_bounds__(256) k_xscale_cols(const float* __restrict__ x, int K, int ldx, int B,
                                                      float* part, int* ctr, float* sc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (a programmatic dependent of the producer of x)
   __shared__ float red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, b = blockIdx.x * 32 + tx;
   const int kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc, k1 = min(K, k0 + kc);
@@ -615,6 +616,9 @@ constexpr int kSplitK = 64, kSplitB = 32;
 __global__ void __launch_bounds__(256) k_split_x(const float* __restrict__ x, int K, int ldx, int B,
                                                  uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int ldk,
                                                  float* __restrict__ xsc, const float* __restrict__ xrg, int nrg) {
+  // a programmatic dependent of the producer of x (its launch and prologue
+  // overlap that kernel's tail); nothing of x, xrg, xh / xl is touched before
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
   // xrg: the producer's max |x| per (32-row group, image) -- the fused scale (no
   // k_xscale_cols pass over x): every block reduces its 32 images' groups; the
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(256) k_tc_reduce(const float* __restrict__ ws,
   constexpr int kC4 = TN / 4, kCC = kC4 / 8;
   __shared__ float4 s_t[32][9];
   asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of the contraction
+  asm volatile("griddepcontrol.launch_dependents;");  // the next layer's split may launch (it waits for us)
   const uint32_t tile = blockIdx.x / (4 * kCC);
   const int rg = (int)(blockIdx.x % (4 * kCC)) / kCC, cc = (int)(blockIdx.x % kCC);
   const uint32_t t0 = tile * (uint32_t)nkt;  // 32-bit: W = tiles * nkt < 2^32 / G (host-checked)
@@ -1006,6 +1011,7 @@ bool list_fold_forced() {
 __global__ void __launch_bounds__(512) k_scale_split_rows(const float* __restrict__ x, int K, int ldx, int B,
                                                           uint16_t* __restrict__ xh, uint16_t* __restrict__ xl,
                                                           int ldk, int vec, float* __restrict__ sc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (a programmatic dependent of the work before it)
   asm volatile("griddepcontrol.launch_dependents;");  // the contraction's prologue may start
   __shared__ float red[16];
   __shared__ float s_scale;
@@ -1153,6 +1159,22 @@ cudaError_t launch_tc_list(const FcDev& L, cudaStream_t s, int kt0, int kt1) {
   return e;
 }
 
+// a launch as a programmatic dependent of the stream's previous kernel (the
+// kernel waits on griddepcontrol before touching anything that kernel wrote)
+template <typename... KArgs, typename... Args>
+static cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ldx, int B, float* y, int ldy, int relu,
                          uint16_t* xh, uint16_t* xl, float* ws, float* scw, int* xctr, cudaStream_t s,
                          bool x_image_major, bool y_image_major, const float* bias, const float* xrg_in,
@@ -1164,12 +1186,18 @@ cudaError_t launch_fc_tc(const FcDev& L, const TcPlan& p, const float* x, int ld
   ktimer_begin("k_split_x", s);
   if (x_image_major) {
     const int vec = (ldx % 4) == 0 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    k_scale_split_rows<<<(unsigned)B, 512, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, vec, xsc);
+    cudaError_t e0 = pdl_launch(k_scale_split_rows, dim3((unsigned)B), dim3(512), s, x, p.kcols, ldx, B, xh, xl, p.ldk,
+                                vec, xsc);
+    if (e0 != cudaSuccess) return e0;
   } else {
+    cudaError_t e0 = cudaSuccess;
     if (!xrg_in)  // (no producer maxima: a separate pass over x)
-      k_xscale_cols<<<dim3((unsigned)((B + 31) / 32), kScaleChunks), 256, 0, s>>>(x, p.kcols, ldx, B, xpart, xctr, xsc);
+      e0 = pdl_launch(k_xscale_cols, dim3((unsigned)((B + 31) / 32), kScaleChunks), dim3(256), s, x, p.kcols, ldx, B,
+                      xpart, xctr, xsc);
+    if (e0 != cudaSuccess) return e0;
     dim3 sg((p.ldk + kSplitK - 1) / kSplitK, (B + kSplitB - 1) / kSplitB);
-    k_split_x<<<sg, 256, 0, s>>>(x, p.kcols, ldx, B, xh, xl, p.ldk, xsc, xrg_in, nrg_in);
+    e0 = pdl_launch(k_split_x, sg, dim3(256), s, x, p.kcols, ldx, B, xh, xl, p.ldk, xsc, xrg_in, nrg_in);
+    if (e0 != cudaSuccess) return e0;
   }
   cudaError_t e = launched(x_image_major || xrg_in ? 1 : 2);
   ktimer_end("k_split_x", s);
