@@ -32,3 +32,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_g
 timeout 300 python scripts/step_breakdown.py --cfg C5 > $P/c5_breakdown.json 2>&1
 timeout 300 python scripts/step_breakdown.py --cfg C4 > $P/c4_breakdown.json 2>&1
 timeout 900 python scripts/grid_report.py > $P/grid.jsonl 2> $P/grid.err
+# in-pipeline DRAM traffic of the tensor-core path (caches not flushed between kernels)
+C="python scripts/layer_bench.py --policy tc --layers 0 --batches 512 --replicas 1 --single"
+timeout 900 ncu --set full --clock-control none --cache-control none \
+  -k regex:"k_fc_tc|k_tc_list|k_split|k_tc_reduce" -c 6 -f -o $P/tc_l0_warm $C > $P/ncu_l0_warm.log 2>&1
+timeout 1200 python scripts/variable_batch_gain.py > $P/variable_batch_c4.jsonl 2> $P/variable_batch.err
+timeout 900 python scripts/shard_timing.py rows > $P/shard_timing_rows.json 2> $P/shard_rows.err; timeout 900 python scripts/shard_timing.py cols > $P/shard_timing_cols.json 2> $P/shard_cols.err
