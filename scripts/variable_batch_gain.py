@@ -37,17 +37,18 @@ def build(cdn):
     return m
 
 
-def fixed_best(T, inb, outb, ws, tot, K):
-    """Best single batch B (all layers), feasible iff IN + WS + OUT <= TOT per
-    layer (no ancestor reserve when every phase count is 1); remainder rounds
-    at the same B are charged pro rata."""
-    best = None
+def fixed_candidates(T, inb, outb, ws, tot, K):
+    """Single batches B (all layers) by predicted time per image, those the
+    recurrence's model admits (IN + WS + OUT <= TOT per layer, no ancestor
+    reserve when every phase count is 1); remainder rounds at the same B are
+    charged pro rata.  The caller runs them best first and keeps the first
+    whose metered executor scratch stays within TOT -- the bar the planned
+    run meets too (reading C-36)."""
+    c = []
     for B in range(1, K + 1):
         if all(inb[i] * B + ws[i] + outb[i] * B <= tot for i in range(len(T))):
-            per = sum(T[i][B - 1] for i in range(len(T))) / B
-            if best is None or per < best[1]:
-                best = (B, per)
-    return best
+            c.append((sum(T[i][B - 1] for i in range(len(T))) / B, B))
+    return [(B, per) for per, B in sorted(c)]
 
 
 def main():
@@ -97,13 +98,21 @@ def main():
                 ts.append(e0.elapsed_time(e1))
             return float(np.median(ts))
 
+        m.release_scratch()
+        m.scratch_bytes(reset_peak=True)
         res["dp_ms"] = run([])  # [] = no fixed plan: the executor plans with the DP
-        # fixed-batch baseline: every layer at one B that fits TOT
-        # with no ancestor reserve; the best predicted B is run and timed
-        fb = fixed_best(T, inb, outb, ws, tot, K)
+        res["dp_scratch_peak_mib"] = m.scratch_bytes()[1] / 2**20
+        # fixed-batch baseline: every layer at one B, the best
+        # predicted B whose run keeps the executor's scratch within TOT
         best = None
-        if fb is not None:
-            best = {"B": fb[0], "pred_ms_per_image": fb[1], "ms": run([fb[0]] * f)}
+        for B, per in fixed_candidates(T, inb, outb, ws, tot, K):
+            m.release_scratch()
+            m.scratch_bytes(reset_peak=True)
+            ms = run([B] * f)
+            peak = m.scratch_bytes()[1]
+            if peak <= tot:
+                best = {"B": B, "pred_ms_per_image": per, "ms": ms, "scratch_peak_mib": peak / 2**20}
+                break
         res["fixed_best"] = best
         if best:
             res["dp_gain"] = best["ms"] / res["dp_ms"] - 1.0
