@@ -255,6 +255,192 @@ __global__ void __launch_bounds__(kGThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tmem_cols) : "memory");
 }
 
+// Halo-tile implicit GEMM for stride-1 CONV layers (k_conv_halo), computed
+// transposed: D[filter][position] = sum_k W[filter][k] * patch[position][k],
+// filters on the M side (128 per tile, TMEM lanes) and up to 256 positions on
+// the N side (TMEM columns) -- at N = 128 the 16-bit MMA reads its two smem
+// operands about as fast as it computes (measured: 128-filter tiles ran the
+// position-major form below the im2col GEMM), N up to 256 halves that.
+// The K loop runs (64-channel chunk, tap (r, s)); per chunk the CTA stages
+// ONCE the input rows its positions and their kh x kw windows need -- a
+// "halo", one 4D tiled TMA box, padding and edges from the TMA's
+// out-of-bounds zeros -- and every tap's B operand is that halo seen from a
+// shifted start.  Positions are flattened at the pitch P = Wo + kw - 1
+// (f = y P + x; positions with x >= Wo are computed and dropped), so the input
+// of position f for tap (r, s) sits at halo row (f - y_s P) + r P + s:
+// consecutive positions stay 128 bytes apart, i.e. the K-major 128B-swizzle
+// layout (8-row groups 1024 B apart) from an unaligned start, the swizzle
+// following the shared-memory address as the TMA wrote it (measured: the
+// descriptor's base-offset field must stay 0).  The im2col TMA it replaces
+// re-read each input pixel from L2 once per tap (kh kw = 9-25 times).
+// Tile = (image, position block of NT, 128-filter block, group); persistent,
+// double-buffered TMEM accumulator; warp 0 TMA, warp 1 MMA, warps 2-9 the
+// epilogue (two per TMEM lane quadrant, each half of the columns; lane =
+// filter: + bias, ReLU, each store a warp's 32 consecutive channels of one
+// position; the position walks (y, x) incrementally -- a division per column
+// had made the epilogue, not the MMA, the bound).
+struct HaloArgs {
+  int B, Ho, Wo, P, HR, kh, kw, pad, nch, cgp, Nrows, NT, spi, mtl, G, tiles;
+  int halo_bytes, SA, SB, talloc, relu, ldo;
+  const float* bias;
+  float* out;
+};
+
+constexpr int kHEpiWarps = 8;
+constexpr int kHThreads = 64 + 32 * kHEpiWarps;
+
+__global__ void __launch_bounds__(kHThreads, 1)
+    k_conv_halo(const __grid_constant__ CUtensorMap th, const __grid_constant__ CUtensorMap tb, const HaloArgs h) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  constexpr int f_bytes = kBM * kBK * 2;  // one filter tile (128 filters x 64 K)
+  unsigned char* sH = smem;                   // halo stages
+  unsigned char* sF = smem + h.SA * h.halo_bytes;  // filter stages
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sF + h.SB * f_bytes);
+  uint64_t* hempty = hfull + h.SA;
+  uint64_t* ffull = hempty + h.SA;
+  uint64_t* fempty = ffull + h.SB;
+  uint64_t* acc_full = fempty + h.SB;  // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < h.SA; ++s) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&hempty[s], 1);
+    }
+    for (int s = 0; s < h.SB; ++s) {
+      mbar_init(&ffull[s], 1);
+      mbar_init(&fempty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kHEpiWarps);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                 "r"(h.talloc)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int nsub = h.B * h.spi, taps = h.kh * h.kw;
+  // tile t: position block u (image u / spi), filter block m, group z
+  auto decode = [&](int t, int& img, int& f0, int& ys, int& m, int& z) {
+    const int u = t % nsub, rest = t / nsub;
+    m = rest % h.mtl;
+    z = rest / h.mtl;
+    img = u / h.spi;
+    f0 = (u - img * h.spi) * h.NT;
+    ys = f0 / h.P;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: per chunk the halo, then one filter tile per tap
+      int ai = 0, bi = 0;
+      for (int t = blockIdx.x; t < h.tiles; t += gridDim.x) {
+        int img, f0, ys, m, z;
+        decode(t, img, f0, ys, m, z);
+        for (int ch = 0; ch < h.nch; ++ch, ++ai) {
+          const int sa = ai % h.SA;
+          mbar_wait(&hempty[sa], ((ai / h.SA) & 1) ^ 1);
+          mbar_arrive_expect_tx(&hfull[sa], (uint32_t)(h.HR * h.P * 128));
+          tma4d(sH + sa * h.halo_bytes, &th, z * h.cgp + ch * kBK, -h.pad, ys - h.pad, img, &hfull[sa]);
+          for (int tap = 0; tap < taps; ++tap, ++bi) {
+            const int sb = bi % h.SB;
+            mbar_wait(&fempty[sb], ((bi / h.SB) & 1) ^ 1);
+            mbar_arrive_expect_tx(&ffull[sb], (uint32_t)f_bytes);
+            tma3d(sF + sb * f_bytes, &tb, (tap * h.nch + ch) * kBK, m * kBM, z, &ffull[sb]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: per tap 4 x (128 filters x NT positions x 16)
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(h.NT >> 3) << 17) |
+                             ((uint32_t)(kBM >> 4) << 24);
+      int ai = 0, bi = 0, i = 0;
+      for (int t = blockIdx.x; t < h.tiles; t += gridDim.x, ++i) {
+        int img, f0, ys, m, z;
+        decode(t, img, f0, ys, m, z);
+        const int off0 = f0 - ys * h.P;
+        const int buf = i & 1;
+        mbar_wait(&acc_empty[buf], ((i >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(buf * h.NT);
+        for (int ch = 0; ch < h.nch; ++ch, ++ai) {
+          const int sa = ai % h.SA;
+          mbar_wait(&hfull[sa], (ai / h.SA) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t hbase = smem_addr(sH + sa * h.halo_bytes);
+          for (int tap = 0; tap < taps; ++tap, ++bi) {
+            const int r = tap / h.kw, sx = tap - r * h.kw;
+            const int sb = bi % h.SB;
+            mbar_wait(&ffull[sb], (bi / h.SB) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad = sw128_desc(smem_addr(sF + sb * f_bytes));
+            const uint64_t bd = sw128_desc(hbase + (uint32_t)(off0 + r * h.P + sx) * 128u);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) umma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (ch | tap | k) != 0);
+            umma_commit(&fempty[sb]);
+          }
+          umma_commit(&hempty[sa]);
+        }
+        umma_commit(&acc_full[buf]);
+      }
+    }
+  } else {
+    // ---- epilogue warps: TMEM lane = filter (quadrant warp % 4), column = flattened
+    // position; the quadrant's two warps take the two halves of the columns
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int c_lo = half ? ((h.NT / 2 + 15) & ~15) : 0, c_hi = half ? h.NT : ((h.NT / 2 + 15) & ~15);
+    int i = 0;
+    for (int t = blockIdx.x; t < h.tiles; t += gridDim.x, ++i) {
+      int img, f0, ys, m, z;
+      decode(t, img, f0, ys, m, z);
+      const int buf = i & 1;
+      const int fl = m * kBM + q * 32 + lane;  // this lane's filter in the group
+      const bool fok = fl < h.Nrows;
+      const float bv = fok ? h.bias[z * h.Nrows + fl] : 0.f;
+      float* obase = h.out + (size_t)img * h.Ho * h.Wo * h.ldo + z * h.Nrows + fl;
+      // the first column's position, then stepped (uniform over the warp)
+      int y = (f0 + c_lo) / h.P, x = f0 + c_lo - y * h.P;
+      mbar_wait(&acc_full[buf], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * h.NT);
+      for (int c = c_lo; c < c_hi; c += 16) {
+        float v[16];
+        tmem_ld16(tq + (uint32_t)c, v);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if (fok && y < h.Ho && x < h.Wo) {
+            float o = v[u] + bv;
+            if (h.relu) o = fmaxf(o, 0.f);
+            obase[(size_t)(y * h.Wo + x) * h.ldo] = o;
+          }
+          if (++x == h.P) {
+            x = 0;
+            ++y;
+          }
+        }
+      }
+      // the accumulator buffer is free again once every epilogue warp has read it
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(h.talloc) : "memory");
+}
+
 // NHWC fp32 -> bf16 (RNE) patches [pos][Kpad] of channels [c0, c0+cg):
 // k = (r*kw + s)*cg + c, zero for padding taps and k >= kh*kw*cg.
 template <bool VEC8>
@@ -480,6 +666,41 @@ cudaError_t launch_gemm_bf16(const __nv_bfloat16* A, int Mrows, const __nv_bfloa
   return e_;
 }
 
+// Launch geometry of k_conv_halo for one stride-1 layer; false: it does not
+// apply (the im2col-TMA GEMM runs: fused LRN, halos over the smem budget).
+// Position blocks: an image's Ho P flattened positions in spi equal blocks of
+// NT <= 256 (multiple of 16); two halo stages, as many filter stages as fit.
+static bool halo_plan(int B, int G, int cgp, int kh, int kw, int pad, int Ho, int Wo, int Nrows, int lrn, HaloArgs& h,
+                      size_t& smem) {
+  static const int mode = [] {  // CDN_CONV_HALO=0: off (A/B knob)
+    const char* e = std::getenv("CDN_CONV_HALO");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!mode || lrn || cgp % kBK) return false;
+  h = HaloArgs{};
+  h.B = B; h.Ho = Ho; h.Wo = Wo; h.kh = kh; h.kw = kw; h.pad = pad; h.G = G; h.cgp = cgp; h.Nrows = Nrows;
+  h.P = Wo + kw - 1;
+  const int flat = Ho * h.P;
+  h.spi = (flat + 255) / 256;
+  h.NT = ((flat + h.spi - 1) / h.spi + 15) & ~15;
+  h.HR = (h.NT - 1) / h.P + 2 + kh - 1;  // a block's output rows (<= (NT-1)/P + 2) + kh - 1
+  if (h.P > 256 || h.HR > 256) return false;
+  const int rows_alloc = std::max(h.HR * h.P, (kh - 1) * h.P + kw + h.P + h.NT);  // + the dropped positions' overreach
+  h.halo_bytes = (rows_alloc * 128 + 1023) & ~1023;
+  h.nch = cgp / kBK;
+  h.mtl = (Nrows + kBM - 1) / kBM;
+  h.talloc = 32;
+  while (h.talloc < 2 * h.NT) h.talloc <<= 1;
+  h.SA = 2;
+  const size_t fixed = 1024 + 256;
+  const long left = 225L * 1024 - (long)fixed - (long)h.SA * h.halo_bytes;
+  h.SB = (int)std::min<long>(8, left / (kBM * kBK * 2));
+  if (h.SB < 3 || h.talloc > 512) return false;
+  h.tiles = B * h.spi * h.mtl * G;
+  smem = fixed + (size_t)h.SA * h.halo_bytes + (size_t)h.SB * kBM * kBK * 2;
+  return smem <= 227 * 1024;
+}
+
 cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
                                  int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
                                  int relu, float* out, int ldo, cudaStream_t s, int lrn) {
@@ -487,6 +708,40 @@ cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, 
   if (Mrows <= 0 || Nrows <= 0 || G <= 0) return cudaSuccess;
   if ((long)G * Nrows > kGMaxBias || cgp % kBK || kh != kw || Ho != H + 2 * pad - kh + 1 || Wo != W + 2 * pad - kw + 1)
     return cudaErrorInvalidValue;
+  {
+    HaloArgs h;
+    size_t smem = 0;
+    if (halo_plan(B, G, cgp, kh, kw, pad, Ho, Wo, Nrows, lrn, h, smem)) {
+      h.relu = relu;
+      h.ldo = ldo;
+      h.bias = bias;
+      h.out = out;
+      CUtensorMap th, tb;
+      cudaError_t e = encode_tmap_nhwc4d(&th, act, (uint64_t)G * cgp, (uint64_t)W, (uint64_t)H, (uint64_t)B, kBK,
+                                         (uint32_t)h.P, (uint32_t)h.HR);
+      if (e != cudaSuccess) return e;
+      const int Kpad = kh * kw * cgp;
+      e = encode_tmap_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Wt, (uint64_t)Kpad, (uint64_t)Nrows, (uint64_t)G,
+                         (uint64_t)Kpad * 2, (uint64_t)Kpad * 2 * Nrows, kBK, (uint32_t)kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (e != cudaSuccess) return e;
+      static thread_local size_t set_smem = 0;
+      if (smem > set_smem) {
+        e = cudaFuncSetAttribute(k_conv_halo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        set_smem = smem;
+      }
+      int num_sms = 148;
+      {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+      }
+      ktimer_begin("k_conv_halo", s);
+      k_conv_halo<<<std::min(h.tiles, num_sms), kHThreads, smem, s>>>(th, tb, h);
+      const cudaError_t e_ = launched();
+      ktimer_end("k_conv_halo", s);
+      return e_;
+    }
+  }
   const int BN = gemm_tile_n(Nrows);
   if (lrn && BN < Nrows) return cudaErrorInvalidValue;
   int tcols = 32;

@@ -23,6 +23,15 @@ static __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, 
       : "memory");
 }
 
+static __device__ __forceinline__ void tma4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
+      : "memory");
+}
+
 static __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                              uint64_t* bar) {
   asm volatile(

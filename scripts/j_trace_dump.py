@@ -2,7 +2,7 @@
 the stamps of every CTA relative to the earliest CTA entry (us).
 Events: 0 entry, 1 index loaded + stream copy issued, 2 griddepcontrol.wait
 returned, 3 tables + x in shared memory, 4 first unit's bits staged,
-5 last unit decoded, 6 CTA done."""
+5 last unit decoded, 6 CTA done, 7 (thread 0) table copy issued."""
 import struct
 import sys
 
@@ -19,7 +19,7 @@ while o < len(data):
     rel = (t - t0) / 1e3
     rel[t == 0] = np.nan
     print(f"launch {k}: {t.shape[0]} CTAs")
-    for ev in range(7):
+    for ev in range(8):
         c = rel[:, ev]
         print(f"  ev{ev}: min {np.nanmin(c):7.2f} med {np.nanmedian(c):7.2f} max {np.nanmax(c):7.2f} us")
     k += 1
