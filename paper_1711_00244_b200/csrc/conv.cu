@@ -255,6 +255,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tmem_cols) : "memory");
 }
 
+__device__ __forceinline__ void store_out(float* p, float o) { *p = o; }
+__device__ __forceinline__ void store_out(__nv_bfloat16* p, float o) { *p = __float2bfloat16_rn(o); }
+
 // Halo-tile implicit GEMM for stride-1 CONV layers (k_conv_halo), computed
 // transposed: D[filter][position] = sum_k W[filter][k] * patch[position][k],
 // filters on the M side (128 per tile, TMEM lanes) and up to 256 positions on
@@ -284,9 +287,10 @@ struct HaloArgs {
   int halo_bytes, SA, SB, talloc, relu, ldo;
   const float* bias;
   float* out;
+  __nv_bfloat16* out_bf;  // non-null: the output as bf16 (RNE), the next CONV layer's input (ldo = its channels)
 };
 
-constexpr int kHEpiWarps = 8;
+constexpr int kHEpiWarps = 16;
 constexpr int kHThreads = 64 + 32 * kHEpiWarps;
 
 __global__ void __launch_bounds__(kHThreads, 1)
@@ -397,8 +401,11 @@ __global__ void __launch_bounds__(kHThreads, 1)
   } else {
     // ---- epilogue warps: TMEM lane = filter (quadrant warp % 4), column = flattened
     // position; the quadrant's two warps take the two halves of the columns
-    const int q = warp & 3, half = (warp - 2) >> 2;
-    const int c_lo = half ? ((h.NT / 2 + 15) & ~15) : 0, c_hi = half ? h.NT : ((h.NT / 2 + 15) & ~15);
+    // (kHEpiWarps / 4 warps per quadrant, each a share of the columns in whole 16-column chunks)
+    constexpr int kParts = kHEpiWarps / 4;
+    const int q = warp & 3, part = (warp - 2) >> 2;
+    const int chunks = h.NT / 16;
+    const int c_lo = (chunks * part / kParts) * 16, c_hi = (chunks * (part + 1) / kParts) * 16;
     int i = 0;
     for (int t = blockIdx.x; t < h.tiles; t += gridDim.x, ++i) {
       int img, f0, ys, m, z;
@@ -407,28 +414,53 @@ __global__ void __launch_bounds__(kHThreads, 1)
       const int fl = m * kBM + q * 32 + lane;  // this lane's filter in the group
       const bool fok = fl < h.Nrows;
       const float bv = fok ? h.bias[z * h.Nrows + fl] : 0.f;
-      float* obase = h.out + (size_t)img * h.Ho * h.Wo * h.ldo + z * h.Nrows + fl;
-      // the first column's position, then stepped (uniform over the warp)
-      int y = (f0 + c_lo) / h.P, x = f0 + c_lo - y * h.P;
+      const size_t o0 = (size_t)img * h.Ho * h.Wo * h.ldo + z * h.Nrows + fl;
+      // (y0, x0) = the position of a 16-column chunk's first column (uniform over
+      // the warp).  Within the chunk every column derives its own position from
+      // that alone -- at most two row wraps in 16 columns (P >= 8) -- so the 16
+      // stores carry no serial chain: stepping (x, y) column by column had the
+      // epilogue warps latency-bound at ~150 clocks per column (conv1: 20 k clocks
+      // per tile against ~5 k of MMAs).
+      int y0 = (f0 + c_lo) / h.P, x0 = f0 + c_lo - y0 * h.P;
+      const int drop = h.P - h.Wo;
       mbar_wait(&acc_full[buf], (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * h.NT);
-      for (int c = c_lo; c < c_hi; c += 16) {
-        float v[16];
-        tmem_ld16(tq + (uint32_t)c, v);
+      auto cols = [&](auto* out) {
+        // (a quadrant past the layer's filters -- conv1: 96 of 128 -- only releases the buffer)
+        for (int c = c_lo; c < c_hi && __any_sync(0xffffffffu, fok); c += 16) {
+          float v[16];
+          tmem_ld16(tq + (uint32_t)c, v);
+          auto* pc = out + o0 + (size_t)(y0 * h.Wo + x0) * h.ldo;
+          if (x0 + 16 <= h.Wo && y0 < h.Ho) {  // the chunk inside one output row: no per-column tests
+            if (fok) {
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          if (fok && y < h.Ho && x < h.Wo) {
+              for (int u = 0; u < 16; ++u) {
+                float o = v[u] + bv;
+                if (h.relu) o = fmaxf(o, 0.f);
+                store_out(pc + (ptrdiff_t)u * h.ldo, o);
+              }
+            }
+            x0 += 16;
+            continue;
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int wraps = (x0 + u >= h.P) + (x0 + u >= 2 * h.P);
+            const int xu = x0 + u - wraps * h.P, yu = y0 + wraps;
             float o = v[u] + bv;
             if (h.relu) o = fmaxf(o, 0.f);
-            obase[(size_t)(y * h.Wo + x) * h.ldo] = o;
+            if (fok && xu < h.Wo && yu < h.Ho) store_out(pc + (ptrdiff_t)(u - wraps * drop) * h.ldo, o);
           }
-          if (++x == h.P) {
-            x = 0;
-            ++y;
+          x0 += 16;
+          while (x0 >= h.P) {
+            x0 -= h.P;
+            ++y0;
           }
         }
-      }
+      };
+      if (h.out_bf) cols(h.out_bf);
+      else cols(h.out);
       // the accumulator buffer is free again once every epilogue warp has read it
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -594,6 +626,221 @@ __global__ void k_lrn4(const float* __restrict__ x, int npos, int C, float* __re
   }
 }
 
+// Max-pool, optionally with the cross-channel LRN ahead of it in the same pass
+// (AlexNet conv2: the LRN output is never written), 8 channels per thread; the
+// result as fp32 NHWC, or (BF) as the next CONV layer's bf16 input -- G groups
+// of cg channels padded with zeros to cgp (rounding is monotonic, so the max
+// of the rounded values is the rounded max; reading C-21).  LRN is evaluated
+// per window position (2.25 x per input value for 3 x 3 / 2): the same
+// expression and summation order as k_lrn4.
+template <bool LRN, bool BF>
+__global__ void __launch_bounds__(256) k_pool8(const float* __restrict__ x, int B, int H, int W, int C, int k, int st,
+                                               int Ho, int Wo, float* __restrict__ yf, __nv_bfloat16* __restrict__ yb,
+                                               int G, int cg, int cgp) {
+  const int Q = (BF ? G * cgp : C) / 8;
+  const long total = (long)B * Ho * Wo * Q;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % Q) * 8;
+    long p = i / Q;
+    const int ow = (int)(p % Wo);
+    const long t = p / Wo;
+    const int oh = (int)(t % Ho), b = (int)(t / Ho);
+    int cin = c8;
+    if (BF) {
+      const int z = c8 / cgp, c = c8 - z * cgp;
+      if (c >= cg) {  // (cg % 8 == 0: a chunk is all real or all padding)
+        reinterpret_cast<uint4*>(yb)[i] = make_uint4(0u, 0u, 0u, 0u);
+        continue;
+      }
+      cin = z * cg + c;
+    }
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+    const float* xb = x + (((size_t)b * H + (size_t)oh * st) * W + (size_t)ow * st) * C + cin;
+    for (int r = 0; r < k; ++r) {
+#pragma unroll 3
+      for (int q = 0; q < k; ++q) {
+        const float4* px = reinterpret_cast<const float4*>(xb + ((size_t)r * W + q) * C);
+        if (LRN) {
+          float a[16];  // channels cin - 4 .. cin + 11 (0 outside: adds nothing to a window sum)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int c = cin - 4 + 4 * v;
+            const float4 f = (c >= 0 && c < C) ? __ldg(px - 1 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            a[4 * v] = f.x; a[4 * v + 1] = f.y; a[4 * v + 2] = f.z; a[4 * v + 3] = f.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float sq = 0.f;
+#pragma unroll
+            for (int w = 0; w < 5; ++w) {
+              const int cq = cin + j - 2 + w;
+              if (cq >= 0 && cq < C) sq = fmaf(a[j + 2 + w], a[j + 2 + w], sq);
+            }
+            m[j] = fmaxf(m[j], a[j + 4] * exp2f(-0.75f * __log2f(2.0f + (1e-4f / 5.0f) * sq)));
+          }
+        } else {
+          const float4 f0 = __ldg(px), f1 = __ldg(px + 1);
+          m[0] = fmaxf(m[0], f0.x); m[1] = fmaxf(m[1], f0.y); m[2] = fmaxf(m[2], f0.z); m[3] = fmaxf(m[3], f0.w);
+          m[4] = fmaxf(m[4], f1.x); m[5] = fmaxf(m[5], f1.y); m[6] = fmaxf(m[6], f1.z); m[7] = fmaxf(m[7], f1.w);
+        }
+      }
+    }
+    if (BF) {
+      __nv_bfloat162 h[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(m[2 * j], m[2 * j + 1]);
+      reinterpret_cast<uint4*>(yb)[i] = *reinterpret_cast<const uint4*>(h);
+    } else {
+      float4* dst = reinterpret_cast<float4*>(yf + p * C + c8);
+      dst[0] = make_float4(m[0], m[1], m[2], m[3]);
+      dst[1] = make_float4(m[4], m[5], m[6], m[7]);
+    }
+  }
+}
+
+// (2 + 1e-4/5 * sq)^-0.75 (reading C-20) through lg2 / ex2 without the library
+// wrappers' denormal branches: the argument is >= 2 and the exponent within
+// [-96, -0.75], where exp2f(-0.75f * __log2f(t)) returns the same bits.
+__device__ __forceinline__ float lrn_scale(float sq) {
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(fmaf(1e-4f / 5.0f, sq, 2.0f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-0.75f * l));
+  return r;
+}
+
+// LRN + max-pool with every LRN value computed once per pooled row: a CTA takes
+// one (image, pooled row) at a time, evaluates LRN over the k input rows under it
+// (contiguous in NHWC: k * W * C floats) into shared memory -- fp32, or already
+// rounded to bf16 when the output is the next CONV layer's input (rounding is
+// monotonic: the max of the rounded values is the rounded max) -- then pools
+// from there.  k_pool8<true> re-evaluated LRN per window position (k * k / st^2
+// = 2.25 x) and was bound by it (conv2: 39 us); here rows overlap only
+// vertically (k / st = 1.5 x).  The same expression and summation order as
+// k_lrn4.  Output layouts as k_pool8.
+template <bool BF>
+__global__ void __launch_bounds__(256) k_lrn_pool_rows(const float* __restrict__ x, int B, int H, int W, int C, int k,
+                                                       int st, int Ho, int Wo, float* __restrict__ yf,
+                                                       __nv_bfloat16* __restrict__ yb, int G, int cg, int cgp, int R) {
+  // R pooled rows per item: (R - 1) st + k input rows, each evaluated once per item
+  extern __shared__ __align__(16) unsigned char sm_lp[];
+  float* sf = reinterpret_cast<float*>(sm_lp);
+  __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(sm_lp);
+  const int Q8 = C / 8, HoR = (Ho + R - 1) / R;
+  const int Co = BF ? G * cgp : C, Qo = Co / 8;
+  for (int it = blockIdx.x; it < B * HoR; it += gridDim.x) {
+    const int b = it / HoR, oh = (it - b * HoR) * R;
+    const int Rc = min(R, Ho - oh);
+    const int n1 = ((Rc - 1) * st + k) * W * Q8, n2 = Rc * Wo * Qo;
+    const float* xr = x + ((size_t)b * H + (size_t)oh * st) * W * C;
+    // two items per thread per round (the eight 16-byte loads issued before either
+    // is used); (pixel, chunk) of item j stepped, not divided, from round to round
+    int pixs[2], c8s[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = threadIdx.x + e * blockDim.x;
+      pixs[e] = j / Q8;
+      c8s[e] = j - pixs[e] * Q8;  // (chunk index; * 8 = first channel)
+    }
+    const int dpix = 2 * blockDim.x / Q8, dq = 2 * blockDim.x - dpix * Q8;
+    float4 f[2][4];
+    // slot e's next item: channels c8 - 4 .. c8 + 11 (0 outside: adds nothing to a window sum)
+    auto load = [&](int e, bool in) {
+      const int c8 = c8s[e] * 8;
+      const float4* px = reinterpret_cast<const float4*>(xr + (size_t)pixs[e] * C + c8);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int c = c8 - 4 + 4 * v;
+        f[e][v] = (in && c >= 0 && c < C) ? __ldg(px - 1 + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    auto comp = [&](int e, bool in) {
+      if (in) {
+        const float a[16] = {f[e][0].x, f[e][0].y, f[e][0].z, f[e][0].w, f[e][1].x, f[e][1].y, f[e][1].z, f[e][1].w,
+                             f[e][2].x, f[e][2].y, f[e][2].z, f[e][2].w, f[e][3].x, f[e][3].y, f[e][3].z, f[e][3].w};
+        float o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          // q from c - 2 to c + 2 in k_lrn4's order; channels outside [0, C) hold 0 and fma(0, 0, sq) = sq
+          float sq = 0.f;
+#pragma unroll
+          for (int w = 0; w < 5; ++w) sq = fmaf(a[u + 2 + w], a[u + 2 + w], sq);
+          o[u] = a[u + 4] * lrn_scale(sq);
+        }
+        const size_t so = (size_t)pixs[e] * C + c8s[e] * 8;
+        if (BF) {
+          __nv_bfloat162 h[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(o[2 * u], o[2 * u + 1]);
+          *reinterpret_cast<uint4*>(sb + so) = *reinterpret_cast<const uint4*>(h);
+        } else {
+          float4* d = reinterpret_cast<float4*>(sf + so);
+          d[0] = make_float4(o[0], o[1], o[2], o[3]);
+          d[1] = make_float4(o[4], o[5], o[6], o[7]);
+        }
+      }
+      pixs[e] += dpix;
+      c8s[e] += dq;
+      if (c8s[e] >= Q8) {
+        c8s[e] -= Q8;
+        ++pixs[e];
+      }
+    };
+    // the loads of one slot stay in flight while the other slot is evaluated
+    const int bd = blockDim.x;
+    load(0, (int)threadIdx.x < n1);
+    for (int j0 = threadIdx.x; j0 < n1; j0 += 2 * bd) {
+      load(1, j0 + bd < n1);
+      comp(0, true);
+      load(0, j0 + 2 * bd < n1);
+      comp(1, j0 + bd < n1);
+    }
+    __syncthreads();
+    const size_t orow = ((size_t)b * Ho + oh) * Wo;  // (the item's pooled rows are consecutive: orow + rr * Wo + ow)
+    for (int j = threadIdx.x; j < n2; j += blockDim.x) {
+      const int pw = j / Qo, c8 = (j - pw * Qo) * 8;  // pw = rr * Wo + ow
+      const int rr = pw / Wo, ow = pw - rr * Wo;
+      const size_t s0 = ((size_t)rr * st * W + (size_t)ow * st) * C;
+      if (BF) {
+        uint4* dst = reinterpret_cast<uint4*>(yb + (orow + pw) * Co + c8);
+        const int z = c8 / cgp, c = c8 - z * cgp;
+        if (c >= cg) {  // (cg % 8 == 0: a chunk is all real or all padding)
+          *dst = make_uint4(0u, 0u, 0u, 0u);
+          continue;
+        }
+        const __nv_bfloat16* p0 = sb + s0 + z * cg + c;
+        uint4 m4 = *reinterpret_cast<const uint4*>(p0);
+        __nv_bfloat162* m = reinterpret_cast<__nv_bfloat162*>(&m4);
+        for (int r = 0; r < k; ++r)
+          for (int q = 0; q < k; ++q) {
+            const uint4 v4 = *reinterpret_cast<const uint4*>(p0 + ((size_t)r * W + q) * C);
+            const __nv_bfloat162* v = reinterpret_cast<const __nv_bfloat162*>(&v4);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) m[u] = __hmax2(m[u], v[u]);
+          }
+        *dst = m4;
+      } else {
+        const float* p0 = sf + s0 + c8;
+        float m[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m[u] = -INFINITY;
+        for (int r = 0; r < k; ++r)
+          for (int q = 0; q < k; ++q) {
+            const float4* v = reinterpret_cast<const float4*>(p0 + ((size_t)r * W + q) * C);
+            const float4 f0 = v[0], f1 = v[1];
+            m[0] = fmaxf(m[0], f0.x); m[1] = fmaxf(m[1], f0.y); m[2] = fmaxf(m[2], f0.z); m[3] = fmaxf(m[3], f0.w);
+            m[4] = fmaxf(m[4], f1.x); m[5] = fmaxf(m[5], f1.y); m[6] = fmaxf(m[6], f1.z); m[7] = fmaxf(m[7], f1.w);
+          }
+        float4* dst = reinterpret_cast<float4*>(yf + (orow + pw) * C + c8);
+        dst[0] = make_float4(m[0], m[1], m[2], m[3]);
+        dst[1] = make_float4(m[4], m[5], m[6], m[7]);
+      }
+    }
+    __syncthreads();  // the next item overwrites the rows
+  }
+}
+
 int grid_for(long work, int threads, int num_sms) {
   const long g = (work + threads - 1) / threads;
   const long cap = (long)num_sms * 16;
@@ -684,7 +931,7 @@ static bool halo_plan(int B, int G, int cgp, int kh, int kw, int pad, int Ho, in
   h.spi = (flat + 255) / 256;
   h.NT = ((flat + h.spi - 1) / h.spi + 15) & ~15;
   h.HR = (h.NT - 1) / h.P + 2 + kh - 1;  // a block's output rows (<= (NT-1)/P + 2) + kh - 1
-  if (h.P > 256 || h.HR > 256) return false;
+  if (h.P > 256 || h.HR > 256 || h.P < 8) return false;  // (P >= 8: the epilogue allows two row wraps per 16 columns)
   const int rows_alloc = std::max(h.HR * h.P, (kh - 1) * h.P + kw + h.P + h.NT);  // + the dropped positions' overreach
   h.halo_bytes = (rows_alloc * 128 + 1023) & ~1023;
   h.nch = cgp / kBK;
@@ -701,9 +948,15 @@ static bool halo_plan(int B, int G, int cgp, int kh, int kw, int pad, int Ho, in
   return smem <= 227 * 1024;
 }
 
+bool conv_halo_applies(int G, int cgp, int kh, int kw, int pad, int Ho, int Wo, int Nrows, int lrn) {
+  HaloArgs h;
+  size_t smem = 0;
+  return kh == kw && halo_plan(1, G, cgp, kh, kw, pad, Ho, Wo, Nrows, lrn, h, smem);
+}
+
 cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
                                  int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
-                                 int relu, float* out, int ldo, cudaStream_t s, int lrn) {
+                                 int relu, float* out, int ldo, cudaStream_t s, int lrn, __nv_bfloat16* out_bf) {
   const int Mrows = B * Ho * Wo;
   if (Mrows <= 0 || Nrows <= 0 || G <= 0) return cudaSuccess;
   if ((long)G * Nrows > kGMaxBias || cgp % kBK || kh != kw || Ho != H + 2 * pad - kh + 1 || Wo != W + 2 * pad - kw + 1)
@@ -716,6 +969,7 @@ cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, 
       h.ldo = ldo;
       h.bias = bias;
       h.out = out;
+      h.out_bf = out_bf;
       CUtensorMap th, tb;
       cudaError_t e = encode_tmap_nhwc4d(&th, act, (uint64_t)G * cgp, (uint64_t)W, (uint64_t)H, (uint64_t)B, kBK,
                                          (uint32_t)h.P, (uint32_t)h.HR);
@@ -742,6 +996,7 @@ cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, 
       return e_;
     }
   }
+  if (out_bf) return cudaErrorInvalidValue;  // (bf16 output: the halo kernel only, conv_halo_applies)
   const int BN = gemm_tile_n(Nrows);
   if (lrn && BN < Nrows) return cudaErrorInvalidValue;
   int tcols = 32;
@@ -1127,6 +1382,60 @@ cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, in
     k_maxpool<<<grid_for((long)B * Ho * Wo * C, 256, num_sms), 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y);
   const cudaError_t e_ = launched();
   ktimer_end("k_maxpool", s);
+  return e_;
+}
+
+bool pool8_ok(int C, int k, int cg, int cgp) { return C % 8 == 0 && k >= 1 && (cg == 0 || (cg % 8 == 0 && cgp % 8 == 0)); }
+
+cudaError_t launch_pool8(const float* x, int B, int H, int W, int C, int k, int st, int lrn, float* y,
+                         __nv_bfloat16* yb, int G, int cg, int cgp, cudaStream_t s, int num_sms) {
+  const int Ho = (H - k) / st + 1, Wo = (W - k) / st + 1;
+  if (B <= 0 || Ho <= 0 || Wo <= 0) return cudaSuccess;
+  if (!pool8_ok(C, k, yb ? cg : 0, cgp) || (yb && G * cg != C) ||
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(yb)) & 15))
+    return cudaErrorInvalidValue;
+  const long work = (long)B * Ho * Wo * ((yb ? G * cgp : C) / 8);
+  const int grid = grid_for(work, 256, num_sms);
+  ktimer_begin(lrn ? "k_lrn_pool" : "k_maxpool", s);
+  static const int rows_mode = [] {  // CDN_LRN_POOL_ROWS=0: the per-window kernel (A/B knob)
+    const char* e = std::getenv("CDN_LRN_POOL_ROWS");
+    return e ? std::atoi(e) : 1;
+  }();
+  // pooled rows per item: one.  Two (1.25 x LRN evaluations per input value instead
+  // of 1.5 x for 3 x 3 / 2) measured slower -- conv1 34 -> 38 us, conv2 23 -> 29 us:
+  // half as many, larger CTAs (CDN_LRN_POOL_R, A/B knob)
+  const size_t row_bytes = (size_t)W * C * (yb ? 2 : 4);
+  static const int r_env = [] {
+    const char* e = std::getenv("CDN_LRN_POOL_R");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  const int R = (size_t)((r_env - 1) * st + k) * row_bytes <= 160 * 1024 ? r_env : 1;
+  const size_t smem = (size_t)((R - 1) * st + k) * row_bytes;
+  if (lrn && rows_mode && smem <= 160 * 1024 && (long)B * Ho < (1L << 30)) {
+    static thread_local size_t set_bf = 0, set_f = 0;
+    size_t& set = yb ? set_bf : set_f;
+    if (smem > 48 * 1024 && smem > set) {
+      const cudaError_t e = yb ? cudaFuncSetAttribute(k_lrn_pool_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                               : cudaFuncSetAttribute(k_lrn_pool_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      set = smem;
+    }
+    // resident CTAs, then a grid every CTA of which takes the same number of (image, row) items
+    int per_sm = 0;
+    if (yb) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lrn_pool_rows<true>, 256, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lrn_pool_rows<false>, 256, smem);
+    per_sm = std::max(per_sm, 1);
+    const long items = (long)B * ((Ho + R - 1) / R), resident = (long)num_sms * per_sm;
+    const long rounds = (items + resident - 1) / resident;
+    const int g = (int)((items + rounds - 1) / rounds);
+    if (yb) k_lrn_pool_rows<true><<<g, 256, smem, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp, R);
+    else k_lrn_pool_rows<false><<<g, 256, smem, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp, R);
+  } else if (lrn && yb) k_pool8<true, true><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
+  else if (lrn) k_pool8<true, false><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
+  else if (yb) k_pool8<false, true><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
+  else k_pool8<false, false><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
+  const cudaError_t e_ = launched();
+  ktimer_end(lrn ? "k_lrn_pool" : "k_maxpool", s);
   return e_;
 }
 

@@ -247,7 +247,16 @@ cudaError_t launch_s2d_bf16(const float* x, int B, int H, int W, int C, int st, 
                             __nv_bfloat16* out, cudaStream_t s);
 cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
                                  int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
-                                 int relu, float* out, int ldo, cudaStream_t s, int lrn);
+                                 int relu, float* out, int ldo, cudaStream_t s, int lrn,
+                                 __nv_bfloat16* out_bf = nullptr);
+// whether the halo-tile kernel (the only one with a bf16 output: out_bf) takes the layer
+bool conv_halo_applies(int G, int cgp, int kh, int kw, int pad, int Ho, int Wo, int Nrows, int lrn);
+// max-pool (+ LRN ahead of it when lrn), 8 channels per thread; output fp32 NHWC
+// (y) or, when yb, bf16 with G groups of cg channels padded to cgp (the next
+// CONV layer's input).  pool8_ok: the shapes it takes (cg = 0: fp32 output)
+bool pool8_ok(int C, int k, int cg, int cgp);
+cudaError_t launch_pool8(const float* x, int B, int H, int W, int C, int k, int st, int lrn, float* y,
+                         __nv_bfloat16* yb, int G, int cg, int cgp, cudaStream_t s, int num_sms);
 cudaError_t launch_maxpool(const float* x, int B, int H, int W, int C, int k, int st, float* y, cudaStream_t s,
                            int num_sms);
 

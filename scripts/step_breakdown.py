@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
-KERNELS = ("k_gemm_bf16", "k_conv_halo", "k_s2d_bf16", "k_to_bf16_pad", "k_decode_conv", "k_im2col", "k_lrn", "k_maxpool", "k_decode_dense", "k_transpose", "k_fc_tc",
+KERNELS = ("k_gemm_bf16", "k_conv_halo", "k_s2d_bf16", "k_to_bf16_pad", "k_decode_conv", "k_im2col", "k_lrn", "k_lrn_pool", "k_maxpool", "k_fc_jm", "k_fc_j", "k_j_reduce", "k_decode_dense", "k_transpose", "k_fc_tc",
            "k_tc_list", "k_split_x", "k_tc_reduce", "k_fc_band", "k_fc_ms", "k_fc_fold")
 
 

@@ -318,8 +318,8 @@ def test_conv_layer_decode_bit_exact(torch_dev, i):
 
 
 def test_c4_planner_goes_variable_with_room(torch_dev):
-    """With room for the FC layers' batch (K = 64, TOT = 192 MiB) the DP's
-    variable-batch chain -- CONV layers at a smaller batch than the FC layers,
+    """With room for the FC layers' batch but not for the CONV trunk at it (K = 64,
+    some TOT between 64 and 192 MiB) the DP's variable-batch chain -- CONV layers at a smaller batch than the FC layers,
     the shape of the paper's Table 5 -- beats every fixed batch the executor
     can run within TOT (profiles/r02_variable_batch_c4.jsonl: 0.56 vs 0.67 ms)."""
     torch, dev = torch_dev
@@ -337,9 +337,16 @@ def test_c4_planner_goes_variable_with_room(torch_dev):
         W, v = synth.fc_weights(spec, cfg.seed)
         c = compress.compress_layer(W, spec.density, spec.r, spec.k, v)
         m.load_layer(cdni.serialize([c.layer]), cdn.LayerDesc.fc(spec.relu))
-    m.set_memory_budget(192 << 20)
-    batches, predicted = m.plan(64)
-    print("C4 plan under 192 MiB:", batches, f"{predicted:.3f} ms for 64 images")
-    assert all(batches[i + 1] % batches[i] == 0 for i in range(len(batches) - 1))
-    assert batches[0] < batches[-1]
+    # the budget where that happens moves with the executor's footprint (bf16
+    # levels between CONV layers shrank it: at 192 MiB a fixed 64 now fits), so
+    # the budgets between "nothing but small batches" and "64 everywhere" are scanned
+    variable = []
+    for mib in (64, 80, 96, 112, 128, 144, 160, 176, 192):
+        m.set_memory_budget(mib << 20)
+        batches, predicted = m.plan(64)
+        print(f"C4 plan under {mib} MiB:", batches, f"{predicted:.3f} ms for 64 images")
+        assert all(batches[i + 1] % batches[i] == 0 for i in range(len(batches) - 1))
+        if batches[0] < batches[-1]:
+            variable.append(mib)
+    assert variable, "no budget at which the planner runs the CONV layers at a smaller batch than the FC layers"
     m.close()
