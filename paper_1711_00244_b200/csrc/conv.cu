@@ -33,6 +33,36 @@ namespace {
 
 using namespace dev;
 
+// A launch as a programmatic dependent of the stream's previous kernel: the
+// kernel's CTAs may be scheduled while that kernel drains (launch latency and
+// prologue hidden); it touches nothing the stream's earlier work wrote before
+// pdl_wait().  Off by default (CDN_CONV_PDL=1 turns it on): measured slower on
+// AlexNet at B = 64 (C4 0.456 -> 0.476 ms) -- the dependents' CTAs (the halo
+// GEMM's hold ~200 KB of shared memory each) take SM slots from the kernel
+// still running and then sit in griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+cudaError_t conv_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  static const int mode = [] {
+    const char* e = std::getenv("CDN_CONV_PDL");
+    return e ? std::atoi(e) : 0;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = mode ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kGMaxStages = 8;
@@ -333,6 +363,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // (barriers and tensor memory were set up under the previous kernel's tail)
   const int nsub = h.B * h.spi, taps = h.kh * h.kw;
   // tile t: position block u (image u / spi), filter block m, group z
   auto decode = [&](int t, int& img, int& f0, int& ys, int& m, int& z) {
@@ -637,6 +668,7 @@ template <bool LRN, bool BF>
 __global__ void __launch_bounds__(256) k_pool8(const float* __restrict__ x, int B, int H, int W, int C, int k, int st,
                                                int Ho, int Wo, float* __restrict__ yf, __nv_bfloat16* __restrict__ yb,
                                                int G, int cg, int cgp) {
+  pdl_wait();
   const int Q = (BF ? G * cgp : C) / 8;
   const long total = (long)B * Ho * Wo * Q;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -727,6 +759,7 @@ __global__ void __launch_bounds__(256) k_lrn_pool_rows(const float* __restrict__
   extern __shared__ __align__(16) unsigned char sm_lp[];
   float* sf = reinterpret_cast<float*>(sm_lp);
   __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(sm_lp);
+  pdl_wait();
   const int Q8 = C / 8, HoR = (Ho + R - 1) / R;
   const int Co = BF ? G * cgp : C, Qo = Co / 8;
   for (int it = blockIdx.x; it < B * HoR; it += gridDim.x) {
@@ -990,7 +1023,8 @@ cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, 
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
       }
       ktimer_begin("k_conv_halo", s);
-      k_conv_halo<<<std::min(h.tiles, num_sms), kHThreads, smem, s>>>(th, tb, h);
+      e = conv_launch(k_conv_halo, dim3(std::min(h.tiles, num_sms)), dim3(kHThreads), smem, s, th, tb, h);
+      if (e != cudaSuccess) return e;
       const cudaError_t e_ = launched();
       ktimer_end("k_conv_halo", s);
       return e_;
@@ -1104,6 +1138,7 @@ template <int ST, int C>
 __global__ void __launch_bounds__(256) k_s2d_bf16(const float* __restrict__ x, int B, int H, int W, int Hs, int Ws,
                                                   int cgp, __nv_bfloat16* __restrict__ out) {
   constexpr int RUN = ST * C, NV = ST * RUN;  // floats per input row run, values per super-pixel
+  pdl_wait();
   const long n = (long)B * Hs * Ws;
   for (long p = (long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
     const int X = (int)(p % Ws);
@@ -1142,7 +1177,10 @@ cudaError_t launch_s2d_bf16(const float* x, int B, int H, int W, int C, int st, 
   const long n = (long)B * Hs * Ws;
   const int grid = (int)std::min<long>((n + 255) / 256, 148L * 16);
   ktimer_begin("k_s2d_bf16", s);
-  if (st == 4 && C == 3) k_s2d_bf16<4, 3><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
+  if (st == 4 && C == 3) {
+    const cudaError_t e = conv_launch(k_s2d_bf16<4, 3>, dim3(grid), dim3(256), 0, s, x, B, H, W, Hs, Ws, cgp, out);
+    if (e != cudaSuccess) return e;
+  }
   else if (st == 2 && C == 3) k_s2d_bf16<2, 3><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
   else if (st == 2 && C == 4) k_s2d_bf16<2, 4><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
   else if (st == 4 && C == 4) k_s2d_bf16<4, 4><<<grid, 256, 0, s>>>(x, B, H, W, Hs, Ws, cgp, out);
@@ -1428,12 +1466,17 @@ cudaError_t launch_pool8(const float* x, int B, int H, int W, int C, int k, int 
     const long items = (long)B * ((Ho + R - 1) / R), resident = (long)num_sms * per_sm;
     const long rounds = (items + resident - 1) / resident;
     const int g = (int)((items + rounds - 1) / rounds);
-    if (yb) k_lrn_pool_rows<true><<<g, 256, smem, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp, R);
-    else k_lrn_pool_rows<false><<<g, 256, smem, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp, R);
-  } else if (lrn && yb) k_pool8<true, true><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
-  else if (lrn) k_pool8<true, false><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
-  else if (yb) k_pool8<false, true><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
-  else k_pool8<false, false><<<grid, 256, 0, s>>>(x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
+    const cudaError_t e = yb ? conv_launch(k_lrn_pool_rows<true>, dim3(g), dim3(256), smem, s, x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp, R)
+                             : conv_launch(k_lrn_pool_rows<false>, dim3(g), dim3(256), smem, s, x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp, R);
+    if (e != cudaSuccess) return e;
+  } else {
+    const cudaError_t e =
+        lrn && yb ? conv_launch(k_pool8<true, true>, dim3(grid), dim3(256), 0, s, x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp)
+        : lrn     ? conv_launch(k_pool8<true, false>, dim3(grid), dim3(256), 0, s, x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp)
+        : yb      ? conv_launch(k_pool8<false, true>, dim3(grid), dim3(256), 0, s, x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp)
+                  : conv_launch(k_pool8<false, false>, dim3(grid), dim3(256), 0, s, x, B, H, W, C, k, st, Ho, Wo, y, yb, G, cg, cgp);
+    if (e != cudaSuccess) return e;
+  }
   const cudaError_t e_ = launched();
   ktimer_end(lrn ? "k_lrn_pool" : "k_maxpool", s);
   return e_;
