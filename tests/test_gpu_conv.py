@@ -350,3 +350,73 @@ def test_c4_planner_goes_variable_with_room(torch_dev):
             variable.append(mib)
     assert variable, "no budget at which the planner runs the CONV layers at a smaller batch than the FC layers"
     m.close()
+
+
+def test_small_conv_net_bf16_chain_vs_layers(torch_dev):
+    """A CONV trunk off AlexNet's shapes, through cdn_model_infer and layer by
+    layer: (a) 8 -> 16 channels, LRN + pool, feeding a layer whose 16-channel
+    groups are padded to 64 (k_lrn_pool_rows writes the padding zeros of the
+    bf16 level); (b) 16 -> 64, no LRN / pool, feeding a 64-channel layer (the
+    halo GEMM's epilogue writes the bf16 level); (c) 64 -> 24 in two groups,
+    pool only, feeding (d) 24 -> 40 (12-channel groups: not a multiple of 8, so
+    the level stays fp32 and the layer converts its own input); then an FC
+    layer.  Each layer is gated against the oracle on the GPU's own input, and
+    infer's scores equal the layer-by-layer chain bit for bit (rounding to bf16
+    in the producer is the consumer's own first step, C-21)."""
+    torch, dev = torch_dev
+    import paper_1711_00244_b200 as cdn
+    specs = [synth.ConvSpec("a", 16, 8, 3, 3, 1, 1, 1, 0.6, lrn=True, pool=True, seed_offset=301),
+             synth.ConvSpec("b", 64, 16, 3, 3, 1, 1, 1, 0.5, seed_offset=302),
+             synth.ConvSpec("c", 24, 64, 5, 5, 1, 2, 2, 0.5, pool=True, seed_offset=303),
+             synth.ConvSpec("d", 40, 24, 3, 3, 1, 1, 2, 0.7, seed_offset=304)]
+    B, hw0 = 5, 21
+    m = cdn.Model(0)
+    comps = []
+    hw = hw0
+    for i, spec in enumerate(specs):
+        W, v = synth.fc_weights(spec, 0)
+        c = compress.compress_layer(W, spec.density, spec.r, spec.k, v)
+        m.load_layer(cdni.serialize([c.layer]),
+                     cdn.LayerDesc.conv(spec.in_ch, hw, hw, spec.kh, spec.kw, spec.stride, spec.pad, spec.groups,
+                                        relu=True, lrn=spec.lrn, pool_k=3 if spec.pool else 0,
+                                        pool_s=2 if spec.pool else 0))
+        hw = m.out_shape(i)[0]
+        comps.append((spec, c, v))
+    feat = int(np.prod(m.out_shape(len(specs) - 1)))
+    fspec = synth.FCSpec("fc", 37, feat, 0.2, 0.05, relu=False, seed_offset=305)
+    Wf, vf = synth.fc_weights(fspec, 0)
+    cf = compress.compress_layer(Wf, fspec.density, fspec.r, fspec.k, vf)
+    m.load_layer(cdni.serialize([cf.layer]), cdn.LayerDesc.fc(False))
+    rng = np.random.default_rng(77)
+    x = rng.random((B, hw0, hw0, 8), dtype=np.float32)
+    m.set_plan([B] * (len(specs) + 1))
+    scores = np.zeros((B, 37), np.float32)
+    for _ in range(3):  # eager, captured, replayed
+        m.infer(x, B, scores, on_device=False)
+    cur = torch.from_numpy(x).to(dev)
+    for li, (spec, c, v) in enumerate(comps):
+        oh, ow, oc = m.out_shape(li)
+        y = torch.empty((B, oh, ow, oc), dtype=torch.float32, device=dev)
+        m.conv_forward(li, cur, B, y)
+        torch.cuda.synchronize()
+        ref = oracle_conv(spec, c, v, cur.cpu().numpy())
+        e = rel_err(y.cpu().numpy(), ref)
+        assert e <= TOL, (li, e)
+        cur = y
+    a = cur.reshape(B, -1)
+    ld = (B + 3) // 4 * 4
+    xp = torch.zeros((feat, ld), dtype=torch.float32, device=dev)
+    xp[:, :B] = a.T
+    yf = torch.zeros((37, ld), dtype=torch.float32, device=dev)
+    m.layer_forward(len(specs), xp, ld, B, yf, ld)
+    torch.cuda.synchronize()
+    ref = infer.fc_forward(sparse_q(cf), a.cpu().numpy(), vf, apply_relu=False)
+    yn = yf[:, :B].T.contiguous().cpu().numpy()
+    assert rel_err(yn, ref) <= TOL
+    assert np.array_equal(scores, yn)
+    # the same request in two phases of the trunk (variable batch: 2 + 2 + 1 is not a chain; 1 then 5)
+    m.set_plan([1] * len(specs) + [B])
+    s2 = np.zeros_like(scores)
+    m.infer(x, B, s2, on_device=False)
+    assert rel_err(s2, scores) <= 1e-5
+    m.close()
