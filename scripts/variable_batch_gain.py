@@ -54,7 +54,7 @@ def fixed_candidates(T, inb, outb, ws, tot, K):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--K", type=int, default=64)
-    ap.add_argument("--budgets", default="48,64,96,128,192")
+    ap.add_argument("--budgets", default="48,64,96,128,144,160,192")
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
     import torch
