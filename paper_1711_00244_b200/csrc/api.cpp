@@ -1319,9 +1319,6 @@ void prelaunch_lists(Model& m, const std::vector<int>& bs, cudaStream_t s) {
   }
 }
 
-// CONV layer on an NHWC fp32 batch: decode the filters into
-// dense bf16, im2col per group, tcgen05 GEMM (+bias, ReLU), then LRN and
-// max-pool as the descriptor asks.  y: [B][out_h][out_w][rows] NHWC fp32.
 // A CONV layer's input held as bf16 (G groups of cg channels padded to cgp):
 // what its implicit GEMM reads.  Between two CONV layers the producer writes
 // that layout itself (its pool, or the halo GEMM's epilogue: rounding to bf16
@@ -1351,6 +1348,13 @@ bool conv_chained(const Model& m, int i) {
                            P.conv_h, P.conv_w, (int)P.rows / pd.groups, 0);
 }
 
+// CONV layer on an NHWC fp32 batch: the filters decoded into
+// dense bf16 (per call, normally ahead on the side stream), the input as bf16
+// with padded channel groups (space-to-depth for a strided first layer), the
+// implicit tcgen05 GEMM (+ bias, ReLU) -- the halo-tile kernel where it applies,
+// else the TMA-im2col one; explicit patches for layers outside both -- then LRN
+// and max-pool as the descriptor asks (one pass when a pool follows the LRN).
+// y: [B][out_h][out_w][rows] NHWC fp32.
 // act_in: the layer's input already in its bf16 layout (conv_chained); sink: the
 // output goes to the next CONV layer's bf16 input instead of y.
 void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStream_t s,
