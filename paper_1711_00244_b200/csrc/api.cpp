@@ -1398,13 +1398,14 @@ void conv_forward(Model& m, Layer& L, const float* x, int B, float* y, cudaStrea
       CUDA_OK(launch_s2d_bf16(x, B, d.in_h, d.in_w, d.in_c, L.s2d, L.s2d_h, L.s2d_w, L.cgp,
                               static_cast<__nv_bfloat16*>(m.conv_a.p), s));
       CUDA_OK(launch_gemm_implicit(act, B, L.s2d_h, L.s2d_w, 1, L.cgp, L.s2d_k, L.s2d_k, 0, Ho, Wo, wd, mg,
-                                   L.bias.as<float>(), d.relu, cout, M, s, fuse_lrn ? 1 : 0, gemm_bf));
+                                   L.bias.as<float>(), d.relu, cout, M, s, fuse_lrn ? 1 : 0, gemm_bf,
+                                   L.s2d * L.s2d * d.in_c));
     } else {
       const long npix = (long)B * d.in_h * d.in_w;
       if (!act_in)
         CUDA_OK(launch_to_bf16_pad(x, npix, d.in_c, G, cg, L.cgp, static_cast<__nv_bfloat16*>(m.conv_a.p), s));
       CUDA_OK(launch_gemm_implicit(act, B, d.in_h, d.in_w, G, L.cgp, d.kh, d.kw, d.pad, Ho, Wo, wd, mg,
-                                   L.bias.as<float>(), d.relu, cout, M, s, fuse_lrn ? 1 : 0, gemm_bf));
+                                   L.bias.as<float>(), d.relu, cout, M, s, fuse_lrn ? 1 : 0, gemm_bf, cg));
     }
   } else {
     // every group's patches, then one GEMM launch over all groups (grid.z), so

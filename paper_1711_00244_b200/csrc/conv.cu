@@ -315,6 +315,7 @@ __device__ __forceinline__ void store_out(__nv_bfloat16* p, float o) { *p = __fl
 struct HaloArgs {
   int B, Ho, Wo, P, HR, kh, kw, pad, nch, cgp, Nrows, NT, spi, mtl, G, tiles;
   int halo_bytes, SA, SB, talloc, relu, ldo;
+  int klast;  // K16 slices of a group's last 64-channel chunk that hold real channels (the rest multiply zeros)
   const float* bias;
   float* out;
   __nv_bfloat16* out_bf;  // non-null: the output as bf16 (RNE), the next CONV layer's input (ldo = its channels)
@@ -420,8 +421,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint64_t ad = sw128_desc(smem_addr(sF + sb * f_bytes));
             const uint64_t bd = sw128_desc(hbase + (uint32_t)(off0 + r * h.P + sx) * 128u);
+            // (a last chunk padded from 48 to 64 channels -- conv1's super-pixels,
+            // conv2's groups -- issues 3 of the 4 K16 slices: the 4th is zeros x zeros)
+            const int nk = ch + 1 == h.nch ? h.klast : kBK / 16;
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) umma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (ch | tap | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k)
+              if (k < nk) umma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (ch | tap | k) != 0);
             umma_commit(&fempty[sb]);
           }
           umma_commit(&hempty[sa]);
@@ -989,7 +994,8 @@ bool conv_halo_applies(int G, int cgp, int kh, int kw, int pad, int Ho, int Wo, 
 
 cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
                                  int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
-                                 int relu, float* out, int ldo, cudaStream_t s, int lrn, __nv_bfloat16* out_bf) {
+                                 int relu, float* out, int ldo, cudaStream_t s, int lrn, __nv_bfloat16* out_bf,
+                                 int cg_real) {
   const int Mrows = B * Ho * Wo;
   if (Mrows <= 0 || Nrows <= 0 || G <= 0) return cudaSuccess;
   if ((long)G * Nrows > kGMaxBias || cgp % kBK || kh != kw || Ho != H + 2 * pad - kh + 1 || Wo != W + 2 * pad - kw + 1)
@@ -1003,6 +1009,8 @@ cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, 
       h.bias = bias;
       h.out = out;
       h.out_bf = out_bf;
+      h.klast = kBK / 16;
+      if (cg_real > 0 && cg_real <= cgp && cg_real > cgp - kBK) h.klast = (cg_real - (cgp - kBK) + 15) / 16;
       CUtensorMap th, tb;
       cudaError_t e = encode_tmap_nhwc4d(&th, act, (uint64_t)G * cgp, (uint64_t)W, (uint64_t)H, (uint64_t)B, kBK,
                                          (uint32_t)h.P, (uint32_t)h.HR);

@@ -248,7 +248,8 @@ cudaError_t launch_s2d_bf16(const float* x, int B, int H, int W, int C, int st, 
 cudaError_t launch_gemm_implicit(const __nv_bfloat16* act, int B, int H, int W, int G, int cgp, int kh, int kw,
                                  int pad, int Ho, int Wo, const __nv_bfloat16* Wt, int Nrows, const float* bias,
                                  int relu, float* out, int ldo, cudaStream_t s, int lrn,
-                                 __nv_bfloat16* out_bf = nullptr);
+                                 __nv_bfloat16* out_bf = nullptr, int cg_real = 0);
+// (cg_real: real channels per group, <= cgp; the filters' and the input's channels past it are zeros)
 // whether the halo-tile kernel (the only one with a bf16 output: out_bf) takes the layer
 bool conv_halo_applies(int G, int cgp, int kh, int kw, int pad, int Ho, int Wo, int Nrows, int lrn);
 // max-pool (+ LRN ahead of it when lrn), 8 channels per thread; output fp32 NHWC
