@@ -378,20 +378,34 @@ __global__ void __launch_bounds__(kHThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer: per chunk the halo, then one filter tile per tap
-      int ai = 0, bi = 0;
+      // (Both single-thread roles step their ring slot, phase, tap coordinates and
+      // descriptors instead of dividing per tap: one thread's dependent
+      // instructions issue ~4 clocks apart, and ~100 of them per tap -- three
+      // divisions by run-time values among them -- had set the kernel's pace at
+      // ~1000 clocks per tap whatever the tile size, ring depth or MMA count.)
+      const int SA = h.SA, SB = h.SB, nch = h.nch;
+      int sa = 0, pa = 1, sb = 0, pb = 1;  // ring slots and the parity their empty barriers are waited on
       for (int t = blockIdx.x; t < h.tiles; t += gridDim.x) {
         int img, f0, ys, m, z;
         decode(t, img, f0, ys, m, z);
-        for (int ch = 0; ch < h.nch; ++ch, ++ai) {
-          const int sa = ai % h.SA;
-          mbar_wait(&hempty[sa], ((ai / h.SA) & 1) ^ 1);
+        const int c_ch = z * h.cgp, m0 = m * kBM;
+        for (int ch = 0; ch < nch; ++ch) {
+          mbar_wait(&hempty[sa], (uint32_t)pa);
           mbar_arrive_expect_tx(&hfull[sa], (uint32_t)(h.HR * h.P * 128));
-          tma4d(sH + sa * h.halo_bytes, &th, z * h.cgp + ch * kBK, -h.pad, ys - h.pad, img, &hfull[sa]);
-          for (int tap = 0; tap < taps; ++tap, ++bi) {
-            const int sb = bi % h.SB;
-            mbar_wait(&fempty[sb], ((bi / h.SB) & 1) ^ 1);
+          tma4d(sH + sa * h.halo_bytes, &th, c_ch + ch * kBK, -h.pad, ys - h.pad, img, &hfull[sa]);
+          if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+          int kc = ch * kBK;  // K coordinate of (tap, ch): (tap * nch + ch) * 64
+          for (int tap = 0; tap < taps; ++tap, kc += nch * kBK) {
+            mbar_wait(&fempty[sb], (uint32_t)pb);
             mbar_arrive_expect_tx(&ffull[sb], (uint32_t)f_bytes);
-            tma3d(sF + sb * f_bytes, &tb, (tap * h.nch + ch) * kBK, m * kBM, z, &ffull[sb]);
+            tma3d(sF + sb * f_bytes, &tb, kc, m0, z, &ffull[sb]);
+            if (++sb == SB) {
+              sb = 0;
+              pb ^= 1;
+            }
           }
         }
       }
@@ -400,7 +414,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
     if (lane == 0) {  // ---- MMA issuer: per tap 4 x (128 filters x NT positions x 16)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(h.NT >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
-      int ai = 0, bi = 0, i = 0;
+      const int SA = h.SA, SB = h.SB, nch = h.nch, kw = h.kw, klast = h.klast;
+      const uint64_t fdesc0 = sw128_desc(smem_addr(sF));
+      const uint32_t fstep = (uint32_t)(f_bytes >> 4);               // descriptor units (16 B) per filter stage
+      const uint32_t rstep = (uint32_t)((h.P - kw) * 8);             // B start: next kernel row (after kw taps of +8)
+      int sa = 0, pa = 0, sb = 0, pb = 0, i = 0;
+      uint64_t ad = fdesc0;
       for (int t = blockIdx.x; t < h.tiles; t += gridDim.x, ++i) {
         int img, f0, ys, m, z;
         decode(t, img, f0, ys, m, z);
@@ -409,27 +428,43 @@ __global__ void __launch_bounds__(kHThreads, 1)
         mbar_wait(&acc_empty[buf], ((i >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + (uint32_t)(buf * h.NT);
-        for (int ch = 0; ch < h.nch; ++ch, ++ai) {
-          const int sa = ai % h.SA;
-          mbar_wait(&hfull[sa], (ai / h.SA) & 1);
+        uint32_t first = 0;  // 0 for the tile's first MMA (overwrites the accumulator)
+        for (int ch = 0; ch < nch; ++ch) {
+          mbar_wait(&hfull[sa], (uint32_t)pa);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t hbase = smem_addr(sH + sa * h.halo_bytes);
-          for (int tap = 0; tap < taps; ++tap, ++bi) {
-            const int r = tap / h.kw, sx = tap - r * h.kw;
-            const int sb = bi % h.SB;
-            mbar_wait(&ffull[sb], (bi / h.SB) & 1);
+          // tap (r, s) reads the halo from row off0 + r P + s: +8 units per s, + rstep more per r
+          uint64_t bd = sw128_desc(smem_addr(sH + sa * h.halo_bytes) + (uint32_t)off0 * 128u);
+          // (a last chunk padded from 48 to 64 channels -- conv1's super-pixels,
+          // conv2's groups -- issues 3 of the 4 K16 slices: the 4th is zeros x zeros)
+          const int nk = ch + 1 == nch ? klast : kBK / 16;
+          int sx = 0;
+          for (int tap = 0; tap < taps; ++tap) {
+            mbar_wait(&ffull[sb], (uint32_t)pb);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t ad = sw128_desc(smem_addr(sF + sb * f_bytes));
-            const uint64_t bd = sw128_desc(hbase + (uint32_t)(off0 + r * h.P + sx) * 128u);
-            // (a last chunk padded from 48 to 64 channels -- conv1's super-pixels,
-            // conv2's groups -- issues 3 of the 4 K16 slices: the 4th is zeros x zeros)
-            const int nk = ch + 1 == h.nch ? h.klast : kBK / 16;
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
-              if (k < nk) umma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (ch | tap | k) != 0);
+              if (k < nk) {
+                umma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, first);
+                first = 1;
+              }
             umma_commit(&fempty[sb]);
+            ad += fstep;
+            if (++sb == SB) {
+              sb = 0;
+              pb ^= 1;
+              ad = fdesc0;
+            }
+            bd += 8;
+            if (++sx == kw) {
+              sx = 0;
+              bd += rstep;
+            }
           }
           umma_commit(&hempty[sa]);
+          if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+          }
         }
         umma_commit(&acc_full[buf]);
       }
@@ -966,7 +1001,11 @@ static bool halo_plan(int B, int G, int cgp, int kh, int kw, int pad, int Ho, in
   h.B = B; h.Ho = Ho; h.Wo = Wo; h.kh = kh; h.kw = kw; h.pad = pad; h.G = G; h.cgp = cgp; h.Nrows = Nrows;
   h.P = Wo + kw - 1;
   const int flat = Ho * h.P;
-  h.spi = (flat + 255) / 256;
+  static const int nt_cap = [] {  // CDN_HALO_NT: widest position block (experiment knob, <= 256)
+    const char* e = std::getenv("CDN_HALO_NT");
+    return e ? std::max(16, std::min(256, std::atoi(e))) : 256;
+  }();
+  h.spi = (flat + nt_cap - 1) / nt_cap;
   h.NT = ((flat + h.spi - 1) / h.spi + 15) & ~15;
   h.HR = (h.NT - 1) / h.P + 2 + kh - 1;  // a block's output rows (<= (NT-1)/P + 2) + kh - 1
   if (h.P > 256 || h.HR > 256 || h.P < 8) return false;  // (P >= 8: the epilogue allows two row wraps per 16 columns)
@@ -979,7 +1018,11 @@ static bool halo_plan(int B, int G, int cgp, int kh, int kw, int pad, int Ho, in
   h.SA = 2;
   const size_t fixed = 1024 + 256;
   const long left = 225L * 1024 - (long)fixed - (long)h.SA * h.halo_bytes;
-  h.SB = (int)std::min<long>(8, left / (kBM * kBK * 2));
+  static const int sb_cap = [] {  // CDN_HALO_SB: filter stages cap (experiment knob)
+    const char* e = std::getenv("CDN_HALO_SB");
+    return e ? std::max(3, std::atoi(e)) : 8;
+  }();
+  h.SB = (int)std::min<long>(sb_cap, left / (kBM * kBK * 2));
   if (h.SB < 3 || h.talloc > 512) return false;
   h.tiles = B * h.spi * h.mtl * G;
   smem = fixed + (size_t)h.SA * h.halo_bytes + (size_t)h.SB * kBM * kBK * 2;
