@@ -322,6 +322,7 @@ struct HaloArgs {
 };
 
 constexpr int kHEpiWarps = 16;
+constexpr int kHTP = 2;  // filter taps per pipeline stage
 constexpr int kHThreads = 64 + 32 * kHEpiWarps;
 
 __global__ void __launch_bounds__(kHThreads, 1)
@@ -329,9 +330,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   constexpr int f_bytes = kBM * kBK * 2;  // one filter tile (128 filters x 64 K)
+  // kHTP taps per filter stage: one barrier round (wait, fence, commit -- ~300
+  // clocks of the MMA thread's serial time) per kHTP taps instead of per tap
+  constexpr int s_bytes = kHTP * f_bytes;
   unsigned char* sH = smem;                   // halo stages
   unsigned char* sF = smem + h.SA * h.halo_bytes;  // filter stages
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(sF + h.SB * f_bytes);
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sF + h.SB * s_bytes);
   uint64_t* hempty = hfull + h.SA;
   uint64_t* ffull = hempty + h.SA;
   uint64_t* fempty = ffull + h.SB;
@@ -398,10 +402,11 @@ __global__ void __launch_bounds__(kHThreads, 1)
             pa ^= 1;
           }
           int kc = ch * kBK;  // K coordinate of (tap, ch): (tap * nch + ch) * 64
-          for (int tap = 0; tap < taps; ++tap, kc += nch * kBK) {
+          for (int tap = 0; tap < taps; tap += kHTP) {
+            const int n = taps - tap < kHTP ? taps - tap : kHTP;  // taps of this stage
             mbar_wait(&fempty[sb], (uint32_t)pb);
-            mbar_arrive_expect_tx(&ffull[sb], (uint32_t)f_bytes);
-            tma3d(sF + sb * f_bytes, &tb, kc, m0, z, &ffull[sb]);
+            mbar_arrive_expect_tx(&ffull[sb], (uint32_t)(n * f_bytes));
+            for (int j = 0; j < n; ++j, kc += nch * kBK) tma3d(sF + sb * s_bytes + j * f_bytes, &tb, kc, m0, z, &ffull[sb]);
             if (++sb == SB) {
               sb = 0;
               pb ^= 1;
@@ -416,7 +421,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                              ((uint32_t)(kBM >> 4) << 24);
       const int SA = h.SA, SB = h.SB, nch = h.nch, kw = h.kw, klast = h.klast;
       const uint64_t fdesc0 = sw128_desc(smem_addr(sF));
-      const uint32_t fstep = (uint32_t)(f_bytes >> 4);               // descriptor units (16 B) per filter stage
+      const uint32_t fstep = (uint32_t)(f_bytes >> 4);               // descriptor units (16 B) per filter tile
       const uint32_t rstep = (uint32_t)((h.P - kw) * 8);             // B start: next kernel row (after kw taps of +8)
       int sa = 0, pa = 0, sb = 0, pb = 0, i = 0;
       uint64_t ad = fdesc0;
@@ -438,26 +443,29 @@ __global__ void __launch_bounds__(kHThreads, 1)
           // conv2's groups -- issues 3 of the 4 K16 slices: the 4th is zeros x zeros)
           const int nk = ch + 1 == nch ? klast : kBK / 16;
           int sx = 0;
-          for (int tap = 0; tap < taps; ++tap) {
+          for (int tap = 0; tap < taps; tap += kHTP) {
+            const int n = taps - tap < kHTP ? taps - tap : kHTP;
             mbar_wait(&ffull[sb], (uint32_t)pb);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int j = 0; j < n; ++j) {
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              if (k < nk) {
-                umma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, first);
-                first = 1;
+              for (int k = 0; k < kBK / 16; ++k)
+                if (k < nk) {
+                  umma_bf16(acc, ad + j * fstep + 2 * k, bd + 2 * k, idesc, first);
+                  first = 1;
+                }
+              bd += 8;
+              if (++sx == kw) {
+                sx = 0;
+                bd += rstep;
               }
+            }
             umma_commit(&fempty[sb]);
-            ad += fstep;
+            ad += kHTP * fstep;
             if (++sb == SB) {
               sb = 0;
               pb ^= 1;
               ad = fdesc0;
-            }
-            bd += 8;
-            if (++sx == kw) {
-              sx = 0;
-              bd += rstep;
             }
           }
           umma_commit(&hempty[sa]);
@@ -1022,10 +1030,10 @@ static bool halo_plan(int B, int G, int cgp, int kh, int kw, int pad, int Ho, in
     const char* e = std::getenv("CDN_HALO_SB");
     return e ? std::max(3, std::atoi(e)) : 8;
   }();
-  h.SB = (int)std::min<long>(sb_cap, left / (kBM * kBK * 2));
-  if (h.SB < 3 || h.talloc > 512) return false;
+  h.SB = (int)std::min<long>(sb_cap, left / (kHTP * kBM * kBK * 2));
+  if (h.SB < 2 || h.talloc > 512) return false;
   h.tiles = B * h.spi * h.mtl * G;
-  smem = fixed + (size_t)h.SA * h.halo_bytes + (size_t)h.SB * kBM * kBK * 2;
+  smem = fixed + (size_t)h.SA * h.halo_bytes + (size_t)h.SB * kHTP * kBM * kBK * 2;
   return smem <= 227 * 1024;
 }
 
