@@ -315,6 +315,7 @@ __device__ __forceinline__ void store_out(__nv_bfloat16* p, float o) { *p = __fl
 struct HaloArgs {
   int B, Ho, Wo, P, HR, kh, kw, pad, nch, cgp, Nrows, NT, spi, mtl, G, tiles;
   int halo_bytes, SA, SB, talloc, relu, ldo;
+  int TP;     // filter taps per pipeline stage (the most, <= kHTPMax, that leaves two stages)
   int klast;  // K16 slices of a group's last 64-channel chunk that hold real channels (the rest multiply zeros)
   const float* bias;
   float* out;
@@ -322,7 +323,7 @@ struct HaloArgs {
 };
 
 constexpr int kHEpiWarps = 16;
-constexpr int kHTP = 2;  // filter taps per pipeline stage
+constexpr int kHTPMax = 4;  // most filter taps per pipeline stage (HaloArgs::TP)
 constexpr int kHThreads = 64 + 32 * kHEpiWarps;
 
 __global__ void __launch_bounds__(kHThreads, 1)
@@ -330,9 +331,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   constexpr int f_bytes = kBM * kBK * 2;  // one filter tile (128 filters x 64 K)
-  // kHTP taps per filter stage: one barrier round (wait, fence, commit -- ~300
-  // clocks of the MMA thread's serial time) per kHTP taps instead of per tap
-  constexpr int s_bytes = kHTP * f_bytes;
+  // TP taps per filter stage: one barrier round (wait, fence, commit -- ~300
+  // clocks of the MMA thread's serial time) per TP taps instead of per tap
+  const int kHTP = h.TP, s_bytes = kHTP * f_bytes;
   unsigned char* sH = smem;                   // halo stages
   unsigned char* sF = smem + h.SA * h.halo_bytes;  // filter stages
   uint64_t* hfull = reinterpret_cast<uint64_t*>(sF + h.SB * s_bytes);
@@ -1030,10 +1031,16 @@ static bool halo_plan(int B, int G, int cgp, int kh, int kw, int pad, int Ho, in
     const char* e = std::getenv("CDN_HALO_SB");
     return e ? std::max(3, std::atoi(e)) : 8;
   }();
-  h.SB = (int)std::min<long>(sb_cap, left / (kHTP * kBM * kBK * 2));
+  static const int tp_cap = [] {  // CDN_HALO_TP: taps per stage cap (experiment knob)
+    const char* e = std::getenv("CDN_HALO_TP");
+    return e ? std::max(1, std::min(kHTPMax, std::atoi(e))) : 3;  // (4 on conv3-5, two stages: 35.1 / 30.0 / 19.5 vs 34.2 / 29.5 / 18.8 us)
+  }();
+  h.TP = std::min(tp_cap, kh * kw);
+  while (h.TP > 1 && left / (h.TP * kBM * kBK * 2) < 2) --h.TP;
+  h.SB = (int)std::min<long>(sb_cap, left / (h.TP * kBM * kBK * 2));
   if (h.SB < 2 || h.talloc > 512) return false;
   h.tiles = B * h.spi * h.mtl * G;
-  smem = fixed + (size_t)h.SA * h.halo_bytes + (size_t)h.SB * kHTP * kBM * kBK * 2;
+  smem = fixed + (size_t)h.SA * h.halo_bytes + (size_t)h.SB * h.TP * kBM * kBK * 2;
   return smem <= 227 * 1024;
 }
 
